@@ -1,0 +1,164 @@
+/* sagecut_cuda.h — C ABI of libsagecut_cuda.so, the B200-native drop-in for the
+ * CoFree-GNN per-partition training step of the reference `sagecut`
+ * (/root/reference/proj, arXiv 2308.03209).
+ *
+ * The reference has no FFI: its boundary is the C++ API in namespace sagecut
+ * (partition.hpp, reweight.hpp, dropedge.hpp, nn.hpp, trainer.hpp), called by
+ * proj/tools/main.cpp and the tests. Each entry point below replaces one of
+ * those functions (cited per declaration); a C++ facade that re-exports the
+ * reference signatures on top of this ABI is include/sagecut_b200.hpp, and the
+ * ctypes mirror used by tests/ and bench.py is paper_2308_03209_b200/sagecut.py.
+ *
+ * Conventions
+ *   - plain pointers + sizes; host buffers unless a name says _dev;
+ *   - device state lives in opaque handles with explicit *_destroy;
+ *   - edges are int32 [m][2] pairs; matrices are row-major;
+ *   - parameters are ONE flat fp32 vector in SageModel::for_each_matrix order
+ *     (layer0.message, layer0.update, ..., head), each matrix row-major;
+ *   - every function returns an sc_status; on failure sc_last_error() holds the
+ *     reference's message text where the reference throws
+ *     (std::invalid_argument -> SC_EINVAL, std::runtime_error -> SC_ERUNTIME,
+ *     std::logic_error -> SC_EINTERNAL), mirroring the CLI's exit-code map
+ *     (proj/tools/main.cpp:822-834).
+ */
+#ifndef SAGECUT_CUDA_H
+#define SAGECUT_CUDA_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SC_OK = 0,
+    SC_EINVAL = 1,     /* std::invalid_argument */
+    SC_ERUNTIME = 2,   /* std::runtime_error */
+    SC_EINTERNAL = 3,  /* std::logic_error / bug */
+    SC_ECUDA = 4,      /* CUDA runtime / launch failure */
+    SC_ENCCL = 5       /* NCCL failure */
+} sc_status;
+
+typedef struct sc_ctx sc_ctx;         /* one device + streams + scratch      */
+typedef struct sc_graph sc_graph;     /* sagecut::Graph on the device        */
+typedef struct sc_vcut sc_vcut;       /* sagecut::VertexCutPartition         */
+typedef struct sc_trainer sc_trainer; /* train_cofree_impl state             */
+
+const char* sc_last_error(void);
+const char* sc_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+sc_status sc_ctx_create(int device, sc_ctx** out);
+sc_status sc_ctx_destroy(sc_ctx* ctx);
+sc_status sc_ctx_sync(sc_ctx* ctx);
+/* Kernel launches issued by this library on ctx since creation (counter). */
+int64_t sc_ctx_launch_count(sc_ctx* ctx);
+
+/* ---- graph (proj/include/sagecut/graph.hpp:53-96, proj/src/graph.cpp) ---- */
+/* build_graph (graph.cpp:8-64): drop self-loops, canonicalise u<v, sort,
+ * dedup, CSR with ascending neighbour rows. raw_uv is a host buffer. */
+sc_status sc_build_graph(sc_ctx* ctx, int32_t num_nodes, const int32_t* raw_uv, int64_t m_raw, sc_graph** out,
+                         int64_t* dropped_self_loops, int64_t* merged_duplicates);
+/* Same, from a raw edge list already resident on the device. */
+sc_status sc_build_graph_dev(sc_ctx* ctx, int32_t num_nodes, const int32_t* raw_uv_dev, int64_t m_raw,
+                             sc_graph** out, int64_t* dropped_self_loops, int64_t* merged_duplicates);
+/* Attach features (fp32 n x d), class ids, and the train/val/test masks
+ * (Graph::features/labels/num_classes/*_mask). Host buffers. */
+sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, const int32_t* labels,
+                            int32_t num_classes, const uint8_t* train, const uint8_t* val, const uint8_t* test);
+/* Replace only the features (e.g. a new batch of the same graph). Host or device source. */
+sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_device);
+sc_status sc_graph_info(sc_graph* g, int32_t* num_nodes, int64_t* num_edges, int32_t* dim, int32_t* num_classes);
+sc_status sc_graph_copy_edges(sc_graph* g, int32_t* uv);
+sc_status sc_graph_copy_csr(sc_graph* g, int64_t* offsets, int32_t* neighbors, int32_t* edge_ids, int32_t* degrees);
+sc_status sc_graph_destroy(sc_graph* g);
+
+/* ---- vertex cut (proj/include/sagecut/partition.hpp, proj/src/partition.cpp) */
+/* partition_random (partition.cpp:92-100): edge e takes the e-th next_below(p)
+ * draw of Rng(substream(seed,"partition.random")). */
+sc_status sc_partition_random(sc_graph* g, int32_t num_parts, uint64_t seed, sc_vcut** out);
+/* partition_dbh (partition.cpp:102-114). */
+sc_status sc_partition_dbh(sc_graph* g, int32_t num_parts, uint64_t seed, sc_vcut** out);
+/* build_vertex_cut (partition.cpp:22-90) from a caller-supplied assignment. */
+sc_status sc_build_vertex_cut(sc_graph* g, int32_t num_parts, const int32_t* edge_assignment, sc_vcut** out);
+sc_status sc_vcut_num_parts(sc_vcut* vc, int32_t* num_parts);
+sc_status sc_vcut_assignment(sc_vcut* vc, int32_t* out);
+sc_status sc_vcut_part_sizes(sc_vcut* vc, int32_t part, int64_t* n_local, int64_t* n_edges);
+/* PartSubgraph fields (partition.hpp:14-31); any pointer may be NULL. */
+sc_status sc_vcut_part_copy(sc_vcut* vc, int32_t part, int32_t* nodes, int32_t* edges_uv, int32_t* edge_global_ids,
+                            int32_t* local_degrees, int64_t* offsets, int32_t* neighbors, int32_t* edge_ids,
+                            int32_t* global_to_local);
+/* replication_stats (partition.cpp:310-342). */
+sc_status sc_replication_stats(sc_vcut* vc, int32_t* per_node_rf, double* rf, double* edge_balance,
+                               double* node_balance, int64_t* duplicated_nodes);
+sc_status sc_vcut_destroy(sc_vcut* vc);
+
+/* ---- reweighting (proj/src/reweight.cpp:23-81) ---------------------------- */
+/* scheme: 0 dar, 1 vanilla_inv, 2 none. out: concatenated per part (sum n_i). */
+sc_status sc_compute_weights(sc_vcut* vc, int32_t scheme, double* out);
+
+/* ---- DropEdge-K (proj/src/dropedge.cpp:9-37) ------------------------------- */
+/* precompute_masks: K masks over num_edges local edges, each keeping exactly
+ * ceil((1-ratio)*num_edges); bit-exact with the reference's Fisher-Yates
+ * stream (computed on the device). out: K x num_edges bytes (host). */
+sc_status sc_precompute_masks(sc_ctx* ctx, int64_t num_edges, int32_t k, double ratio, uint64_t seed, uint8_t* out);
+/* select_mask with Rng(substream(seed,"dropedge.select",part,epoch))
+ * (trainer.hpp:261-266). */
+int32_t sc_select_mask(uint64_t seed, uint64_t part, uint64_t epoch, int32_t k);
+uint64_t sc_substream(uint64_t seed, const char* tag, int32_t nidx, uint64_t a, uint64_t b);
+
+/* ---- model (proj/include/sagecut/nn.hpp:73-102) ---------------------------- */
+int64_t sc_param_count(int32_t in_dim, const int32_t* hidden, int32_t layers, int32_t num_classes);
+/* make_sage_model<float>: Glorot draws from Rng(substream(seed,"init")). */
+sc_status sc_init_params(sc_ctx* ctx, int32_t in_dim, const int32_t* hidden, int32_t layers, int32_t num_classes,
+                         uint64_t seed, float* out);
+
+/* ---- trainer (proj/include/sagecut/trainer.hpp:20-33, 202-313) ------------- */
+typedef struct {
+    int32_t layers;          /* TrainConfig::layers */
+    const int32_t* hidden;   /* resolved per-layer hidden dims (length layers) */
+    double learning_rate;    /* TrainConfig::learning_rate */
+    int32_t loss;            /* 0 softmax_ce, 1 bce */
+    int32_t reweight;        /* 0 dar, 1 vanilla_inv, 2 none */
+    int32_t use_dropedge;
+    int32_t dropedge_k;
+    double drop_ratio;
+    uint64_t seed;
+    int32_t deterministic;   /* 1: ascending-partition gradient sum (bitwise
+                                invariant to GPU count); 0: local sum + allreduce */
+    int32_t gemm;            /* 0: auto (tcgen05 where shapes allow), 1: SIMT fp32 only */
+} sc_train_config;
+
+/* Partitions i with i % world == rank are trained on this rank's device. */
+sc_status sc_trainer_create(sc_ctx* ctx, sc_graph* g, sc_vcut* vc, const sc_train_config* cfg, int32_t rank,
+                            int32_t world, sc_trainer** out);
+/* NCCL: rank 0 calls sc_nccl_unique_id and ships the 128 bytes to the others. */
+sc_status sc_nccl_unique_id(uint8_t out[128]);
+sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
+/* One epoch of train_cofree_impl (trainer.hpp:255-302): every local
+ * partition's forward / loss / backward, the gradient exchange, grad_norm and
+ * one Adam step. Outputs are host scalars (the only D2H of the step). */
+sc_status sc_trainer_step(sc_trainer* t, int32_t epoch, double* loss, double* grad_norm);
+/* Same, but enqueue only (no host sync); results via sc_trainer_last(). */
+sc_status sc_trainer_step_async(sc_trainer* t, int32_t epoch);
+sc_status sc_trainer_last(sc_trainer* t, double* loss, double* grad_norm);
+sc_status sc_trainer_param_count(sc_trainer* t, int64_t* n);
+sc_status sc_trainer_get_params(sc_trainer* t, float* out);
+sc_status sc_trainer_set_params(sc_trainer* t, const float* in);
+sc_status sc_trainer_get_grads(sc_trainer* t, float* out);              /* gathered */
+sc_status sc_trainer_get_part_grads(sc_trainer* t, int32_t part, float* out);
+sc_status sc_trainer_get_part_logits(sc_trainer* t, int32_t part, float* out);
+sc_status sc_trainer_get_part_loss(sc_trainer* t, int32_t part, double* loss);
+sc_status sc_trainer_get_part_mask(sc_trainer* t, int32_t part, int32_t* mask_index);
+/* evaluate_splits (trainer.hpp:132-140): full-graph forward + accuracy. */
+sc_status sc_trainer_evaluate(sc_trainer* t, double* train, double* val, double* test);
+/* Per-kernel timing of the last step (CUDA events), for bench.py's roofline. */
+sc_status sc_trainer_profile(sc_trainer* t, int32_t enable);
+sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms, double* bytes, int32_t cap,
+                                  int32_t* count);
+sc_status sc_trainer_destroy(sc_trainer* t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,505 @@
+// capi.cu — the extern "C" boundary of libsagecut_cuda.so (include/sagecut_cuda.h).
+//
+// Every entry point converts C++ exceptions into sc_status codes with the
+// reference's message text in sc_last_error(), the same taxonomy the
+// reference's CLI maps to exit codes (proj/tools/main.cpp:822-834).
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sagecut_cuda.h"
+#include "internal.hpp"
+#include "trainer.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+sc_status guard(F&& f) {
+    try {
+        f();
+        return SC_OK;
+    } catch (const sc::CudaError& e) {
+        g_err = e.what();
+        return SC_ECUDA;
+    } catch (const sc::NcclError& e) {
+        g_err = e.what();
+        return SC_ENCCL;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SC_EINVAL;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return SC_EINTERNAL;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return SC_ERUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SC_EINTERNAL;
+    }
+}
+
+#define REQUIRE_ARG(cond, msg) \
+    if (!(cond)) throw std::invalid_argument(msg)
+
+void set_device(sc_ctx* ctx) { SC_CUDA(cudaSetDevice(ctx->device)); }
+
+}  // namespace
+
+using namespace sc;
+
+extern "C" {
+
+const char* sc_last_error(void) { return g_err.c_str(); }
+const char* sc_version(void) { return "sagecut_cuda 0.1 (sm_100a)"; }
+
+// ---- context ----
+sc_status sc_ctx_create(int device, sc_ctx** out) {
+    return guard([&] {
+        REQUIRE_ARG(out, "sc_ctx_create: null out");
+        int count = 0;
+        SC_CUDA(cudaGetDeviceCount(&count));
+        REQUIRE_ARG(device >= 0 && device < count, "sc_ctx_create: no such CUDA device");
+        SC_CUDA(cudaSetDevice(device));
+        auto ctx = std::make_unique<sc_ctx>();
+        ctx->device = device;
+        SC_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        *out = ctx.release();
+    });
+}
+sc_status sc_ctx_destroy(sc_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        set_device(ctx);
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+sc_status sc_ctx_sync(sc_ctx* ctx) {
+    return guard([&] { SC_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+int64_t sc_ctx_launch_count(sc_ctx*) { return sc::g_launches; }
+
+// ---- graph ----
+sc_status sc_build_graph_dev(sc_ctx* ctx, int32_t n, const int32_t* raw_dev, int64_t m_raw, sc_graph** out,
+                             int64_t* self_loops, int64_t* dups) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && out, "sc_build_graph: null argument");
+        REQUIRE_ARG(m_raw >= 0, "build_graph: negative edge count");
+        REQUIRE_ARG(m_raw < (int64_t(1) << 31), "build_graph: more than 2^31 edges");
+        set_device(ctx);
+        *out = build_graph_device(ctx, n, raw_dev, m_raw, self_loops, dups).release();
+    });
+}
+sc_status sc_build_graph(sc_ctx* ctx, int32_t n, const int32_t* raw_uv, int64_t m_raw, sc_graph** out,
+                         int64_t* self_loops, int64_t* dups) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && out && (raw_uv || m_raw == 0), "sc_build_graph: null argument");
+        REQUIRE_ARG(m_raw >= 0, "build_graph: negative edge count");
+        set_device(ctx);
+        DevBuf<int32_t> raw(std::max<int64_t>(2 * m_raw, 2));
+        h2d(raw.get(), raw_uv, 2 * m_raw, ctx->stream);
+        *out = build_graph_device(ctx, n, raw.get(), m_raw, self_loops, dups).release();
+    });
+}
+sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, const int32_t* labels, int32_t classes,
+                            const uint8_t* train, const uint8_t* val, const uint8_t* test) {
+    return guard([&] {
+        REQUIRE_ARG(g && features && labels && train && val && test, "sc_graph_set_data: null argument");
+        REQUIRE_ARG(dim >= 1, "sc_graph_set_data: feature dim must be positive");
+        REQUIRE_ARG(classes >= 1, "sc_graph_set_data: num_classes must be positive");
+        set_device(g->ctx);
+        cudaStream_t s = g->ctx->stream;
+        const int64_t n = g->n;
+        int64_t train_count = 0;
+        for (int64_t v = 0; v < n; ++v) {
+            // softmax_ce_loss validates every row's class id (nn.hpp:328-329)
+            if (labels[v] < 0 || labels[v] >= classes) throw std::invalid_argument("loss: class id out of range");
+            train_count += train[v] ? 1 : 0;
+        }
+        g->dim = dim;
+        g->num_classes = classes;
+        g->features.alloc(std::max<int64_t>(n * dim, 1));
+        g->labels.alloc(std::max<int64_t>(n, 1));
+        g->train.alloc(std::max<int64_t>(n, 1));
+        g->val.alloc(std::max<int64_t>(n, 1));
+        g->test.alloc(std::max<int64_t>(n, 1));
+        h2d(g->features.get(), features, n * dim, s);
+        h2d(g->labels.get(), labels, n, s);
+        h2d(g->train.get(), train, n, s);
+        h2d(g->val.get(), val, n, s);
+        h2d(g->test.get(), test, n, s);
+        g->train_count = train_count;
+        SC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_device) {
+    return guard([&] {
+        REQUIRE_ARG(g && features && g->dim > 0, "sc_graph_set_features: graph has no feature buffer");
+        set_device(g->ctx);
+        SC_CUDA(cudaMemcpyAsync(g->features.get(), features, sizeof(float) * size_t(g->n) * g->dim,
+                                is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->ctx->stream));
+    });
+}
+sc_status sc_graph_info(sc_graph* g, int32_t* n, int64_t* m, int32_t* dim, int32_t* classes) {
+    return guard([&] {
+        REQUIRE_ARG(g, "sc_graph_info: null graph");
+        if (n) *n = g->n;
+        if (m) *m = g->m;
+        if (dim) *dim = g->dim;
+        if (classes) *classes = g->num_classes;
+    });
+}
+sc_status sc_graph_copy_edges(sc_graph* g, int32_t* uv) {
+    return guard([&] {
+        set_device(g->ctx);
+        std::vector<int32_t> u(g->m), v(g->m);
+        d2h(u.data(), g->eu.get(), g->m, g->ctx->stream);
+        d2h(v.data(), g->ev.get(), g->m, g->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(g->ctx->stream));
+        for (int64_t e = 0; e < g->m; ++e) {
+            uv[2 * e] = u[e];
+            uv[2 * e + 1] = v[e];
+        }
+    });
+}
+sc_status sc_graph_copy_csr(sc_graph* g, int64_t* offsets, int32_t* nbrs, int32_t* eids, int32_t* degrees) {
+    return guard([&] {
+        set_device(g->ctx);
+        cudaStream_t s = g->ctx->stream;
+        if (offsets) d2h(offsets, g->offsets.get(), size_t(g->n) + 1, s);
+        if (nbrs) d2h(nbrs, g->nbrs.get(), 2 * g->m, s);
+        if (eids) d2h(eids, g->eids.get(), 2 * g->m, s);
+        if (degrees) d2h(degrees, g->degrees.get(), g->n, s);
+        SC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+sc_status sc_graph_destroy(sc_graph* g) {
+    return guard([&] {
+        if (!g) return;
+        set_device(g->ctx);
+        delete g;
+    });
+}
+
+// ---- vertex cut ----
+sc_status sc_partition_random(sc_graph* g, int32_t p, uint64_t seed, sc_vcut** out) {
+    return guard([&] {
+        REQUIRE_ARG(g && out, "sc_partition_random: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        REQUIRE_ARG(g->m > 0, "partition_random: graph has no edges");
+        set_device(g->ctx);
+        DevBuf<int32_t> a(g->m);
+        assign_random(g, p, seed, a.get());
+        *out = build_vertex_cut_device(g, p, std::move(a)).release();
+    });
+}
+sc_status sc_partition_dbh(sc_graph* g, int32_t p, uint64_t seed, sc_vcut** out) {
+    return guard([&] {
+        REQUIRE_ARG(g && out, "sc_partition_dbh: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        set_device(g->ctx);
+        DevBuf<int32_t> a(std::max<int64_t>(g->m, 1));
+        assign_dbh(g, p, seed, a.get());
+        *out = build_vertex_cut_device(g, p, std::move(a)).release();
+    });
+}
+sc_status sc_build_vertex_cut(sc_graph* g, int32_t p, const int32_t* assign, sc_vcut** out) {
+    return guard([&] {
+        REQUIRE_ARG(g && out && (assign || g->m == 0), "sc_build_vertex_cut: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        set_device(g->ctx);
+        DevBuf<int32_t> a(std::max<int64_t>(g->m, 1));
+        h2d(a.get(), assign, g->m, g->ctx->stream);
+        *out = build_vertex_cut_device(g, p, std::move(a)).release();
+    });
+}
+sc_status sc_vcut_num_parts(sc_vcut* vc, int32_t* p) {
+    return guard([&] { *p = vc->p; });
+}
+sc_status sc_vcut_assignment(sc_vcut* vc, int32_t* out) {
+    return guard([&] {
+        set_device(vc->g->ctx);
+        d2h(out, vc->assign.get(), vc->g->m, vc->g->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(vc->g->ctx->stream));
+    });
+}
+sc_status sc_vcut_part_sizes(sc_vcut* vc, int32_t part, int64_t* n_local, int64_t* n_edges) {
+    return guard([&] {
+        REQUIRE_ARG(vc && part >= 0 && part < vc->p, "sc_vcut_part_sizes: bad part index");
+        if (n_local) *n_local = vc->parts[part].n_local;
+        if (n_edges) *n_edges = vc->parts[part].m_local;
+    });
+}
+sc_status sc_vcut_part_copy(sc_vcut* vc, int32_t part, int32_t* nodes, int32_t* edges_uv, int32_t* gids,
+                            int32_t* local_deg, int64_t* offsets, int32_t* nbrs, int32_t* eids, int32_t* g2l) {
+    return guard([&] {
+        REQUIRE_ARG(vc && part >= 0 && part < vc->p, "sc_vcut_part_copy: bad part index");
+        set_device(vc->g->ctx);
+        cudaStream_t s = vc->g->ctx->stream;
+        const PartDev& pd = vc->parts[part];
+        if (nodes) d2h(nodes, pd.nodes.get(), pd.n_local, s);
+        if (gids) d2h(gids, pd.edge_gids.get(), pd.m_local, s);
+        if (local_deg) d2h(local_deg, pd.local_deg.get(), pd.n_local, s);
+        if (offsets) d2h(offsets, pd.offsets.get(), pd.n_local + 1, s);
+        if (nbrs) d2h(nbrs, pd.nbrs.get(), 2 * pd.m_local, s);
+        if (eids) d2h(eids, pd.eids.get(), 2 * pd.m_local, s);
+        if (g2l) d2h(g2l, vc->g2l.get() + int64_t(part) * vc->g->n, vc->g->n, s);
+        std::vector<int32_t> u, v;
+        if (edges_uv) {
+            u.resize(pd.m_local);
+            v.resize(pd.m_local);
+            d2h(u.data(), pd.lu.get(), pd.m_local, s);
+            d2h(v.data(), pd.lv.get(), pd.m_local, s);
+        }
+        SC_CUDA(cudaStreamSynchronize(s));
+        for (int64_t e = 0; edges_uv && e < pd.m_local; ++e) {
+            edges_uv[2 * e] = u[e];
+            edges_uv[2 * e + 1] = v[e];
+        }
+    });
+}
+sc_status sc_replication_stats(sc_vcut* vc, int32_t* per_node_rf, double* rf, double* edge_balance,
+                               double* node_balance, int64_t* duplicated) {
+    // partition.cpp:310-342
+    return guard([&] {
+        REQUIRE_ARG(vc, "replication_stats: null partition");
+        set_device(vc->g->ctx);
+        const sc_graph* g = vc->g;
+        if (per_node_rf) {
+            d2h(per_node_rf, vc->per_node_rf.get(), g->n, g->ctx->stream);
+            SC_CUDA(cudaStreamSynchronize(g->ctx->stream));
+        }
+        int64_t total = 0, maxn = 0, maxe = 0;
+        for (const auto& pd : vc->parts) {
+            total += pd.n_local;
+            maxn = std::max(maxn, pd.n_local);
+            maxe = std::max(maxe, pd.m_local);
+        }
+        const double n = static_cast<double>(g->n), p = static_cast<double>(vc->p);
+        if (rf) *rf = static_cast<double>(total) / n;
+        if (duplicated) *duplicated = total - g->n;
+        if (edge_balance) *edge_balance = g->m == 0 ? 0.0 : static_cast<double>(maxe) / (static_cast<double>(g->m) / p);
+        if (node_balance) *node_balance = total == 0 ? 0.0 : static_cast<double>(maxn) / (static_cast<double>(total) / p);
+    });
+}
+sc_status sc_vcut_destroy(sc_vcut* vc) {
+    return guard([&] {
+        if (!vc) return;
+        set_device(vc->g->ctx);
+        delete vc;
+    });
+}
+
+// ---- reweighting ----
+sc_status sc_compute_weights(sc_vcut* vc, int32_t scheme, double* out) {
+    return guard([&] {
+        REQUIRE_ARG(vc && out, "compute_weights: null argument");
+        REQUIRE_ARG(scheme >= 0 && scheme <= 2, "compute_weights: bad scheme");
+        set_device(vc->g->ctx);
+        int64_t off = 0;
+        for (int32_t i = 0; i < vc->p; ++i) {
+            const int64_t nl = vc->parts[i].n_local;
+            DevBuf<double> w(std::max<int64_t>(nl, 1));
+            compute_weights_device(vc, scheme, i, w.get());
+            d2h(out + off, w.get(), nl, vc->g->ctx->stream);
+            SC_CUDA(cudaStreamSynchronize(vc->g->ctx->stream));
+            off += nl;
+        }
+    });
+}
+
+// ---- DropEdge ----
+sc_status sc_precompute_masks(sc_ctx* ctx, int64_t m, int32_t k, double ratio, uint64_t seed, uint8_t* out) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && (out || m == 0), "precompute_masks: null argument");
+        set_device(ctx);
+        DevBuf<uint8_t> d(std::max<int64_t>(m * std::max(k, 1), 1));
+        precompute_masks_device(ctx, m, k, ratio, seed, d.get());
+        d2h(out, d.get(), m * k, ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int32_t sc_select_mask(uint64_t seed, uint64_t part, uint64_t epoch, int32_t k) {
+    if (k < 1) return -1;
+    HostRng rng(substream(seed, "dropedge.select", part, epoch));
+    return static_cast<int32_t>(rng.next_below(static_cast<uint64_t>(k)));
+}
+uint64_t sc_substream(uint64_t seed, const char* tag, int32_t nidx, uint64_t a, uint64_t b) {
+    return nidx == 0 ? substream(seed, tag) : (nidx == 1 ? substream(seed, tag, a) : substream(seed, tag, a, b));
+}
+
+// ---- model ----
+int64_t sc_param_count(int32_t in_dim, const int32_t* hidden, int32_t layers, int32_t classes) {
+    int64_t total = 0, in = in_dim;
+    for (int32_t l = 0; l < layers; ++l) {
+        total += int64_t(hidden[l]) * in + int64_t(hidden[l]) * (hidden[l] + in);
+        in = hidden[l];
+    }
+    return total + int64_t(classes) * in;
+}
+sc_status sc_init_params(sc_ctx* ctx, int32_t in_dim, const int32_t* hidden, int32_t layers, int32_t classes,
+                         uint64_t seed, float* out) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && out && (hidden || layers == 0), "make_sage_model: null argument");
+        set_device(ctx);
+        const int64_t P = sc_param_count(in_dim, hidden, layers, classes);
+        DevBuf<float> d(std::max<int64_t>(P, 1));
+        init_params_device(ctx, in_dim, hidden, layers, classes, seed, d.get());
+        d2h(out, d.get(), P, ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---- trainer ----
+sc_status sc_trainer_create(sc_ctx* ctx, sc_graph* g, sc_vcut* vc, const sc_train_config* cfg, int32_t rank,
+                            int32_t world, sc_trainer** out) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && g && vc && cfg && out, "sc_trainer_create: null argument");
+        REQUIRE_ARG(cfg->layers >= 0 && (cfg->hidden || cfg->layers == 0), "layers must be >= 0");
+        set_device(ctx);
+        auto t = std::make_unique<sc_trainer>();
+        t->ctx = ctx;
+        t->g = g;
+        t->vc = vc;
+        t->rank = rank;
+        t->world = world;
+        t->L = cfg->layers;
+        t->hidden.assign(cfg->hidden, cfg->hidden + cfg->layers);
+        t->lr = cfg->learning_rate;
+        t->loss = cfg->loss;
+        t->reweight = cfg->reweight;
+        t->use_dropedge = cfg->use_dropedge;
+        t->K = cfg->dropedge_k;
+        t->ratio = cfg->drop_ratio;
+        t->seed = cfg->seed;
+        t->deterministic = cfg->deterministic;
+        t->gemm_mode = cfg->gemm;
+        REQUIRE_ARG(t->loss == 0 || t->loss == 1, "unknown loss");
+        REQUIRE_ARG(t->reweight >= 0 && t->reweight <= 2, "unknown reweight scheme");
+        trainer_init(t.get());
+        *out = t.release();
+    });
+}
+sc_status sc_nccl_unique_id(uint8_t out[128]) {
+    return guard([&] { nccl_unique_id(out); });
+}
+sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
+    return guard([&] {
+        REQUIRE_ARG(t && id, "sc_trainer_init_comm: null argument");
+        if (t->world > 1) trainer_init_comm(t, id);
+    });
+}
+sc_status sc_trainer_step(sc_trainer* t, int32_t epoch, double* loss, double* gnorm) {
+    return guard([&] {
+        set_device(t->ctx);
+        trainer_step_async(t, epoch);
+        trainer_finish(t, loss, gnorm);
+    });
+}
+sc_status sc_trainer_step_async(sc_trainer* t, int32_t epoch) {
+    return guard([&] {
+        set_device(t->ctx);
+        trainer_finish(t, nullptr, nullptr);  // settle the previous step's host bookkeeping
+        trainer_step_async(t, epoch);
+    });
+}
+sc_status sc_trainer_last(sc_trainer* t, double* loss, double* gnorm) {
+    return guard([&] {
+        set_device(t->ctx);
+        trainer_finish(t, loss, gnorm);
+    });
+}
+sc_status sc_trainer_param_count(sc_trainer* t, int64_t* n) {
+    return guard([&] { *n = t->P; });
+}
+sc_status sc_trainer_get_params(sc_trainer* t, float* out) {
+    return guard([&] {
+        set_device(t->ctx);
+        d2h(out, t->theta.get(), t->P, t->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+sc_status sc_trainer_set_params(sc_trainer* t, const float* in) {
+    return guard([&] {
+        set_device(t->ctx);
+        h2d(t->theta.get(), in, t->P, t->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+sc_status sc_trainer_get_grads(sc_trainer* t, float* out) {
+    return guard([&] {
+        set_device(t->ctx);
+        d2h(out, t->gathered.get(), t->P, t->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+sc_status sc_trainer_get_part_grads(sc_trainer* t, int32_t part, float* out) {
+    return guard([&] {
+        REQUIRE_ARG(part >= 0 && part < t->p, "bad part index");
+        set_device(t->ctx);
+        d2h(out, t->slots.get() + int64_t(part) * t->P, t->P, t->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+sc_status sc_trainer_get_part_logits(sc_trainer* t, int32_t part, float* out) {
+    return guard([&] {
+        REQUIRE_ARG(part >= 0 && part < t->p, "bad part index");
+        REQUIRE_ARG(part % t->world == t->rank, "partition is not trained on this rank");
+        set_device(t->ctx);
+        d2h(out, t->ps[part].logits.get(), t->ps[part].n * t->C, t->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+sc_status sc_trainer_get_part_loss(sc_trainer* t, int32_t part, double* loss) {
+    return guard([&] {
+        REQUIRE_ARG(part >= 0 && part < t->p, "bad part index");
+        set_device(t->ctx);
+        d2h(loss, t->part_loss.get() + part, 1, t->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+sc_status sc_trainer_get_part_mask(sc_trainer* t, int32_t part, int32_t* idx) {
+    return guard([&] {
+        REQUIRE_ARG(part >= 0 && part < t->p, "bad part index");
+        *idx = t->ps[part].chosen;
+    });
+}
+sc_status sc_trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
+    return guard([&] {
+        set_device(t->ctx);
+        trainer_evaluate(t, tr, va, te);
+    });
+}
+sc_status sc_trainer_profile(sc_trainer* t, int32_t enable) {
+    return guard([&] { t->prof.enabled = enable != 0; });
+}
+sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms, double* bytes, int32_t cap,
+                                  int32_t* count) {
+    return guard([&] {
+        int32_t k = 0;
+        for (const auto& kv : t->prof.totals) {
+            if (k < cap) {
+                if (names) names[k] = kv.first.c_str();
+                if (ms) ms[k] = kv.second.ms;
+                if (bytes) bytes[k] = kv.second.bytes;
+            }
+            ++k;
+        }
+        *count = k;
+    });
+}
+sc_status sc_trainer_destroy(sc_trainer* t) {
+    return guard([&] {
+        if (!t) return;
+        set_device(t->ctx);
+        cudaStreamSynchronize(t->ctx->stream);
+        delete t;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,22 @@
+// gemm_tc.cuh — GEMM dispatcher for the M-huge products of the step.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "nn.cuh"
+
+struct sc_trainer;
+
+namespace sc {
+
+// C[M x N] = A1 op(B1) (+ A2 op(B2)) with an epilogue. Uses the tcgen05
+// tensor-core kernel (gemm_tc.cu) when the trainer allows it and the shape is
+// supported; otherwise the fp32 SIMT kernel (nn.cu).
+struct TcGemm {
+    bool enabled = false;
+    void init(sc_trainer* t);
+    void nt(sc_trainer* t, const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc,
+            int64_t M, int32_t N, int epi, const float* row_scale);
+};
+
+}  // namespace sc

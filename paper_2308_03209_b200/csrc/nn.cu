@@ -1,0 +1,654 @@
+// nn.cu — SIMT kernels of the per-partition training step (sm_100a).
+//
+// fp32 everywhere the reference's f32 mode is fp32, f64 where it accumulates
+// in f64 (loss total, grad norm). The aggregation kernels keep the reference's
+// summation order exactly (CSR order of kept neighbours, then * inv), so their
+// outputs are bitwise equal to nn.hpp:222-230 / 277-288 for equal inputs.
+//
+// The GEMMs here are the fp32 CUDA-core path (exact fp32 products, fp32
+// accumulate); gemm_tc.cu holds the tcgen05 tensor-core path that the trainer
+// uses for the large M x {H, in} products.
+#include <cub/cub.cuh>
+
+#include <cmath>
+
+#include "internal.hpp"
+#include "nn.cuh"
+
+namespace sc {
+namespace {
+
+// ---------------------------------------------------------------------------
+// SIMT GEMM: 128 x 128 x 16 tiles, 256 threads, 8 x 8 outputs per thread.
+// ---------------------------------------------------------------------------
+constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8, NT = 256;
+
+struct GemmArgs {
+    MatA a[2];
+    MatB b[2];
+    int nsrc;
+    float* C;
+    int64_t ldc;
+    int64_t M;
+    int32_t N;
+    int epi;
+    const float* row_scale;
+};
+
+__device__ __forceinline__ float load_a(const MatA& a, int64_t r, int32_t k, int64_t M) {
+    if (r >= M || k >= a.K) return 0.f;
+    const int64_t row = a.rows ? a.rows[r] : r;
+    return __ldg(a.ptr + row * a.ld + k);
+}
+__device__ __forceinline__ float load_b(const MatB& b, int32_t n, int32_t k, int32_t N, int32_t K) {
+    if (n >= N || k >= K) return 0.f;
+    return b.nn ? __ldg(b.ptr + int64_t(k) * b.ld + n) : __ldg(b.ptr + int64_t(n) * b.ld + k);
+}
+
+__global__ void __launch_bounds__(NT) gemm_nt_kernel(GemmArgs args) {
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int tid = threadIdx.x;
+    const int64_t m0 = int64_t(blockIdx.x) * BM;
+    const int32_t n0 = blockIdx.y * BN;
+    const int ty = tid / 16, tx = tid % 16;
+    float acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+
+    for (int src = 0; src < args.nsrc; ++src) {
+        const MatA& A = args.a[src];
+        const MatB& B = args.b[src];
+        const int32_t K = A.K;
+        for (int32_t k0 = 0; k0 < K; k0 += BK) {
+            // A tile: 128 rows x 16 k; thread loads 8 (row = tid/2, k = (tid%2)*8 ..)
+            {
+                const int r = tid >> 1, kc = (tid & 1) * 8;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) As[kc + j][r] = load_a(A, m0 + r, k0 + kc + j, args.M);
+            }
+            if (B.nn) {  // B[k][n]: coalesced along n
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int idx = tid + j * NT;  // 0..2047
+                    const int kk = idx / BN, nn = idx % BN;
+                    Bs[kk][nn] = load_b(B, n0 + nn, k0 + kk, args.N, K);
+                }
+            } else {
+                const int nn = tid >> 1, kc = (tid & 1) * 8;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) Bs[kc + j][nn] = load_b(B, n0 + nn, k0 + kc + j, args.N, K);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                float av[TM], bv[TN];
+#pragma unroll
+                for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
+#pragma unroll
+                for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+            }
+            __syncthreads();
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int64_t r = m0 + ty * TM + i;
+        if (r >= args.M) continue;
+        const float sc = args.epi == kEpiRowScale ? args.row_scale[r] : 1.f;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int32_t c = n0 + tx * TN + j;
+            if (c >= args.N) continue;
+            float v = acc[i][j];
+            if (args.epi == kEpiRelu) v = fmaxf(v, 0.f);
+            else if (args.epi == kEpiRowScale) v = sc * v;
+            args.C[r * args.ldc + c] = v;
+        }
+    }
+}
+
+// Weight-gradient GEMM, split-K: block (tile, split) accumulates a 128 x 128
+// tile of A^T B over its row range and writes it to workspace[split].
+struct TnArgs {
+    MatT a;
+    MatT b[2];
+    int32_t n2a;  // columns from b[0]; the rest from b[1]
+    int32_t N1, N2;
+    int64_t M;
+    int64_t rows_per_split;
+    float* ws;
+};
+__device__ __forceinline__ float load_t(const MatT& x, int64_t r, int32_t c) {
+    const int64_t row = x.rows ? x.rows[r] : r;
+    return __ldg(x.ptr + row * x.ld + c);
+}
+
+__global__ void __launch_bounds__(NT) gemm_tn_kernel(TnArgs args) {
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int tid = threadIdx.x;
+    const int32_t tiles_n2 = (args.N2 + BN - 1) / BN;
+    const int32_t t1 = blockIdx.x / tiles_n2, t2 = blockIdx.x % tiles_n2;
+    const int32_t n10 = t1 * BM, n20 = t2 * BN;
+    const int64_t r_begin = int64_t(blockIdx.y) * args.rows_per_split;
+    const int64_t r_end = min(args.M, r_begin + args.rows_per_split);
+    const int ty = tid / 16, tx = tid % 16;
+    float acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    for (int64_t k0 = r_begin; k0 < r_end; k0 += BK) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int idx = tid + j * NT;
+            const int kk = idx / BM, cc = idx % BM;
+            const int64_t r = k0 + kk;
+            const int32_t c1 = n10 + cc, c2 = n20 + cc;
+            float av = 0.f, bv = 0.f;
+            if (r < r_end) {
+                if (c1 < args.N1) av = load_t(args.a, r, c1);
+                if (c2 < args.N2) bv = c2 < args.n2a ? load_t(args.b[0], r, c2) : load_t(args.b[1], r, c2 - args.n2a);
+            }
+            As[kk][cc] = av;
+            Bs[kk][cc] = bv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            float av[TM], bv[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    float* out = args.ws + int64_t(blockIdx.y) * args.N1 * args.N2;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int32_t r = n10 + ty * TM + i;
+        if (r >= args.N1) continue;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int32_t c = n20 + tx * TN + j;
+            if (c < args.N2) out[int64_t(r) * args.N2 + c] = acc[i][j];
+        }
+    }
+}
+
+__global__ void splitk_reduce_kernel(int32_t S, int32_t N1, int32_t N2, const float* ws, float* C, int64_t ldc) {
+    const int64_t total = int64_t(N1) * N2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int32_t s = 0; s < S; ++s) acc += ws[int64_t(s) * total + i];
+        C[(i / N2) * ldc + (i % N2)] = acc;
+    }
+}
+
+constexpr int kMaxSplits = 256;
+
+int32_t tn_splits(int32_t N1, int32_t N2, int64_t M) {
+    const int32_t tiles = ((N1 + BM - 1) / BM) * ((N2 + BN - 1) / BN);
+    int64_t s = (int64_t(num_sms()) * 3 + tiles - 1) / tiles;  // ~3 waves
+    s = std::min<int64_t>(s, (M + 2047) / 2048);                  // >= 2048 rows per split
+    s = std::max<int64_t>(s, 1);
+    return static_cast<int32_t>(std::min<int64_t>(s, kMaxSplits));
+}
+
+// ---------------------------------------------------------------------------
+// Aggregation (warp per row; lanes own float4 column chunks).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool slot_kept(const uint32_t* bits, int64_t k) {
+    return bits == nullptr || ((__ldg(bits + (k >> 5)) >> (k & 31)) & 1u);
+}
+
+__global__ void inv_degree_kernel(int64_t n, const int64_t* __restrict__ off, const uint32_t* __restrict__ bits,
+                                  float* inv) {
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n; v += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t a = off[v], b = off[v + 1];
+        int32_t d = 0;
+        if (!bits) {
+            d = static_cast<int32_t>(b - a);
+        } else {
+            for (int64_t k = a; k < b; ++k) d += slot_kept(bits, k) ? 1 : 0;
+        }
+        inv[v] = d > 0 ? 1.f / static_cast<float>(d) : 0.f;
+    }
+}
+
+template <int NCH, bool kBwd>
+__global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
+                                                   const int32_t* __restrict__ nbrs,
+                                                   const uint32_t* __restrict__ bits, const float* __restrict__ inv,
+                                                   const float* __restrict__ src, const float* __restrict__ msg,
+                                                   float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    const int32_t H4 = H >> 2;
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += warps) {
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t a = off[v], b = off[v + 1];
+        for (int64_t base = a; base < b; base += 32) {
+            const int64_t k = base + lane;
+            const bool valid = k < b;
+            const int32_t nb = valid ? __ldg(nbrs + k) : 0;
+            const bool kept = valid && slot_kept(bits, k);
+            unsigned ballot = __ballot_sync(0xffffffffu, kept);
+            // Add kept neighbours in CSR order; up to 4 row loads in flight.
+            while (ballot) {
+                int32_t u[4];
+                int cnt = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (ballot) {
+                        const int sl = __ffs(ballot) - 1;
+                        ballot &= ballot - 1;
+                        u[q] = __shfl_sync(0xffffffffu, nb, sl);
+                        ++cnt;
+                    } else {
+                        u[q] = -1;
+                    }
+                }
+                float4 vals[4][NCH];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        const int32_t ch = lane + 32 * c;
+                        if (q < cnt && ch < H4)
+                            vals[q][c] = __ldg(reinterpret_cast<const float4*>(src + int64_t(u[q]) * H) + ch);
+                        else
+                            vals[q][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q < cnt)
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) {
+                            acc[c].x += vals[q][c].x;
+                            acc[c].y += vals[q][c].y;
+                            acc[c].z += vals[q][c].z;
+                            acc[c].w += vals[q][c].w;
+                        }
+            }
+        }
+        const float s = kBwd ? 1.f : inv[v];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int32_t ch = lane + 32 * c;
+            if (ch >= H4) continue;
+            float4 r = acc[c];
+            if (!kBwd) {
+                r.x *= s;
+                r.y *= s;
+                r.z *= s;
+                r.w *= s;
+            } else {
+                const float4 mv = __ldg(reinterpret_cast<const float4*>(msg + v * H) + ch);
+                r.x = mv.x > 0.f ? r.x : 0.f;
+                r.y = mv.y > 0.f ? r.y : 0.f;
+                r.z = mv.z > 0.f ? r.z : 0.f;
+                r.w = mv.w > 0.f ? r.w : 0.f;
+            }
+            reinterpret_cast<float4*>(out + v * H)[ch] = r;
+        }
+    }
+}
+
+// Scalar fallback for H % 4 != 0 (tests with odd widths): thread per (row, col).
+template <bool kBwd>
+__global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
+                                   const int32_t* __restrict__ nbrs, const uint32_t* __restrict__ bits,
+                                   const float* __restrict__ inv, const float* __restrict__ src,
+                                   const float* __restrict__ msg, float* __restrict__ out) {
+    const int64_t total = n * H;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t v = i / H;
+        const int32_t c = static_cast<int32_t>(i % H);
+        float acc = 0.f;
+        for (int64_t k = off[v]; k < off[v + 1]; ++k)
+            if (slot_kept(bits, k)) acc += src[int64_t(nbrs[k]) * H + c];
+        out[i] = kBwd ? (msg[i] > 0.f ? acc : 0.f) : acc * inv[v];
+    }
+}
+
+template <bool kBwd>
+void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
+                 const float* src, const float* msg, float* out, cudaStream_t s) {
+    if (n <= 0) return;
+    if (H % 4 != 0) {
+        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+    } else {
+        const int64_t warps_needed = n;
+        const unsigned grid = grid_for(warps_needed * 32, 256, int64_t(num_sms()) * 16);
+        const int nch = (H / 4 + 31) / 32;
+        if (nch <= 1)
+            spmm_kernel<1, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+        else if (nch == 2)
+            spmm_kernel<2, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+        else if (nch <= 4)
+            spmm_kernel<4, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+        else
+            spmm_kernel<8, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+    }
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+
+__global__ void mask_bits_kernel(int64_t nnz, const int32_t* __restrict__ eids, const uint8_t* __restrict__ mask,
+                                 uint32_t* bits) {
+    const int64_t words = (nnz + 31) / 32;
+    for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < words; w += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t x = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int64_t k = w * 32 + b;
+            if (k < nnz && mask[eids[k]]) x |= 1u << b;
+        }
+        bits[w] = x;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Loss (warp per row).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+__global__ void softmax_ce_kernel(int64_t n, int32_t C, const float* __restrict__ logits,
+                                  const int32_t* __restrict__ labels, const int32_t* __restrict__ rows,
+                                  const double* __restrict__ w, const float* __restrict__ scale, float* G,
+                                  double* row_loss) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+        const float* z = logits + r * C;
+        float* g = G + r * C;
+        const double wr = w[r];
+        if (wr == 0.0) {  // nn.hpp:330 rows with zero weight contribute nothing
+            for (int32_t c = lane; c < C; c += 32) g[c] = 0.f;
+            if (lane == 0) row_loss[r] = 0.0;
+            continue;
+        }
+        const int32_t y = labels[rows ? rows[r] : r];
+        float mx = -INFINITY;
+        for (int32_t c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
+        mx = warp_max(mx);
+        float se = 0.f;
+        for (int32_t c = lane; c < C; c += 32) se += expf(z[c] - mx);
+        se = warp_sum(se);
+        const float lse = mx + logf(se);
+        const float sc = scale[r];
+        for (int32_t c = lane; c < C; c += 32) g[c] = sc * (expf(z[c] - lse) - (c == y ? 1.f : 0.f));
+        if (lane == 0) row_loss[r] = wr * static_cast<double>(lse - z[y]);
+    }
+}
+
+__global__ void bce_kernel(int64_t n, int32_t C, const float* __restrict__ logits, const int32_t* __restrict__ labels,
+                           const int32_t* __restrict__ rows, const double* __restrict__ w,
+                           const float* __restrict__ scale, float* G, double* row_loss) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+        const float* z = logits + r * C;
+        float* g = G + r * C;
+        const double wr = w[r];
+        if (wr == 0.0) {
+            for (int32_t c = lane; c < C; c += 32) g[c] = 0.f;
+            if (lane == 0) row_loss[r] = 0.0;
+            continue;
+        }
+        const int32_t yl = labels[rows ? rows[r] : r];
+        const float sc = scale[r];
+        double acc = 0.0;
+        for (int32_t c = lane; c < C; c += 32) {
+            const float zc = z[c];
+            const float y = c == yl ? 1.f : 0.f;  // label_targets: one-hot (graph.cpp:91-98)
+            const float sp = fmaxf(zc, 0.f) + log1pf(expf(-fabsf(zc)));
+            acc += wr * static_cast<double>(sp - zc * y);
+            const float sg = zc >= 0.f ? 1.f / (1.f + expf(-zc)) : expf(zc) / (1.f + expf(zc));
+            g[c] = sc * (sg - y);
+        }
+        acc = warp_sum_d(acc);
+        if (lane == 0) row_loss[r] = acc;
+    }
+}
+
+constexpr int kRedBlocks = 512;
+constexpr int kRedThreads = 256;
+
+__global__ void sum_f64_partial_kernel(int64_t n, const double* __restrict__ x, double* partial) {
+    __shared__ double sh[kRedThreads];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        acc += x[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+__global__ void sum_f64_final_kernel(const double* partial, int nb, double* out, double divisor) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < nb; ++i) acc += partial[i];
+        *out = acc / divisor;
+    }
+}
+
+__global__ void gather_kernel(int64_t P, int32_t p, const float* __restrict__ slots, float* gathered, double* partial,
+                              int* nonfinite) {
+    __shared__ double sh[kRedThreads];
+    double acc = 0.0;
+    bool bad = false;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < P; k += int64_t(gridDim.x) * blockDim.x) {
+        float g = slots[k];
+        for (int32_t i = 1; i < p; ++i) g += slots[int64_t(i) * P + k];
+        gathered[k] = g;
+        bad |= !isfinite(g);
+        acc += static_cast<double>(g) * static_cast<double>(g);
+    }
+    if (bad) *nonfinite = 1;
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void finalize_kernel(const double* partial, int nb, const double* part_loss, int32_t p, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double sq = 0.0;
+        for (int i = 0; i < nb; ++i) sq += partial[i];
+        double l = 0.0;
+        for (int32_t i = 0; i < p; ++i) l += part_loss[i];
+        out[0] = sqrt(sq);
+        out[1] = l;
+    }
+}
+
+__global__ void adam_kernel(int64_t P, float* theta, float* m1, float* m2, const float* __restrict__ g, float b1,
+                            float b2, float c1, float c2, float lr, float eps, const int* nonfinite) {
+    if (*nonfinite) return;  // adam_step throws before touching anything (nn.hpp:404)
+    const float ob1 = 1.f - b1, ob2 = 1.f - b2;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < P; k += int64_t(gridDim.x) * blockDim.x) {
+        const float gi = g[k];
+        // Separate multiply/add roundings as in the reference (no FMA contraction).
+        const float m = __fadd_rn(__fmul_rn(b1, m1[k]), __fmul_rn(ob1, gi));
+        const float v = __fadd_rn(__fmul_rn(b2, m2[k]), __fmul_rn(ob2, __fmul_rn(gi, gi)));
+        m1[k] = m;
+        m2[k] = v;
+        const float mh = __fdiv_rn(m, c1), vh = __fdiv_rn(v, c2);
+        theta[k] = __fsub_rn(theta[k], __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps)));
+    }
+}
+
+__global__ void correct_kernel(int64_t n, int32_t C, const float* __restrict__ logits, const int32_t* __restrict__ labels,
+                               const uint8_t* __restrict__ mask, unsigned long long* out) {
+    unsigned long long corr = 0, tot = 0;
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
+        if (!mask[r]) continue;
+        ++tot;
+        const float* z = logits + r * C;
+        int32_t best = 0;
+        for (int32_t c = 1; c < C; ++c)
+            if (z[c] > z[best]) best = c;
+        corr += best == labels[r];
+    }
+    atomicAdd(&out[0], corr);
+    atomicAdd(&out[1], tot);
+}
+
+}  // namespace
+
+void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
+             int32_t N, int epi, const float* row_scale, cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    GemmArgs args{};
+    args.a[0] = a1;
+    args.b[0] = b1;
+    args.nsrc = 1;
+    if (a2) {
+        args.a[1] = *a2;
+        args.b[1] = *b2;
+        args.nsrc = 2;
+    }
+    args.C = C;
+    args.ldc = ldc;
+    args.M = M;
+    args.N = N;
+    args.epi = epi;
+    args.row_scale = row_scale;
+    dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
+    gemm_nt_kernel<<<grid, NT, 0, s>>>(args);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+
+int64_t gemm_tn_workspace_floats(int32_t N1, int32_t N2) { return int64_t(kMaxSplits) * N1 * N2; }
+
+void gemm_tn(const MatT& a, const MatT& b1, const MatT* b2, int64_t M, float* C, int64_t ldc, float* ws,
+             int64_t ws_floats, cudaStream_t s) {
+    const int32_t N1 = a.cols, N2 = b1.cols + (b2 ? b2->cols : 0);
+    if (N1 <= 0 || N2 <= 0) return;
+    if (M <= 0) {  // no rows: zero gradient
+        for (int32_t r = 0; r < N1; ++r) SC_CUDA(cudaMemsetAsync(C + int64_t(r) * ldc, 0, sizeof(float) * N2, s));
+        return;
+    }
+    const int32_t S = tn_splits(N1, N2, M);
+    if (int64_t(S) * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn: workspace too small");
+    TnArgs args{};
+    args.a = a;
+    args.b[0] = b1;
+    if (b2) args.b[1] = *b2;
+    args.n2a = b1.cols;
+    args.N1 = N1;
+    args.N2 = N2;
+    args.M = M;
+    args.rows_per_split = ((M + S - 1) / S + BK - 1) / BK * BK;
+    args.ws = ws;
+    const int32_t tiles = ((N1 + BM - 1) / BM) * ((N2 + BN - 1) / BN);
+    gemm_tn_kernel<<<dim3(tiles, S), NT, 0, s>>>(args);
+    SC_LAUNCH_CHECK();
+    splitk_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
+    SC_LAUNCH_CHECK();
+    count_launch(2);
+}
+
+void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* bits, float* inv, cudaStream_t s) {
+    if (n <= 0) return;
+    inv_degree_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, offsets, bits, inv);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits, const float* inv,
+              const float* msg, float* mean, cudaStream_t s) {
+    spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, mean, s);
+}
+void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
+              const float* dmean_s, const float* msg, float* dz, cudaStream_t s) {
+    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s);
+}
+void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_t* bits, cudaStream_t s) {
+    if (nnz <= 0) return;
+    mask_bits_kernel<<<grid_for((nnz + 31) / 32, 256), 256, 0, s>>>(nnz, eids, mask, bits);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+void softmax_ce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
+                const float* scale, float* G, double* row_loss, cudaStream_t s) {
+    if (n <= 0) return;
+    softmax_ce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, logits, labels, rows, w, scale, G, row_loss);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+void bce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
+         const float* scale, float* G, double* row_loss, cudaStream_t s) {
+    if (n <= 0) return;
+    bce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, logits, labels, rows, w, scale, G, row_loss);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+void sum_f64(int64_t n, const double* x, double* partial, double* out, double divisor, cudaStream_t s) {
+    sum_f64_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(n, x, partial);
+    SC_LAUNCH_CHECK();
+    sum_f64_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, out, divisor);
+    SC_LAUNCH_CHECK();
+    count_launch(2);
+}
+void gather_grads(int64_t P, int32_t p, const float* slots, float* gathered, double* partial, int* nonfinite,
+                  cudaStream_t s) {
+    gather_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(P, p, slots, gathered, partial, nonfinite);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+void finalize_step(const double* partial, const double* part_loss, int32_t p, double* out, cudaStream_t s) {
+    finalize_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, part_loss, p, out);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+void adam(int64_t P, float* theta, float* m1, float* m2, const float* g, float b1, float b2, float c1, float c2,
+          float lr, float eps, const int* nonfinite, cudaStream_t s) {
+    adam_kernel<<<grid_for(P, 256), 256, 0, s>>>(P, theta, m1, m2, g, b1, b2, c1, c2, lr, eps, nonfinite);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+void count_correct(int64_t n, int32_t C, const float* logits, const int32_t* labels, const uint8_t* mask,
+                   unsigned long long* out, cudaStream_t s) {
+    if (n <= 0) return;
+    correct_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, C, logits, labels, mask, out);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace sc

@@ -1,0 +1,77 @@
+// nn.cuh — kernels of the per-partition training step (declarations).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sc {
+
+// A operand of a row-major GEMM: A[r][k] = ptr[(rows ? rows[r] : r) * ld + k].
+struct MatA {
+    const float* ptr = nullptr;
+    int64_t ld = 0;
+    const int32_t* rows = nullptr;  // optional row gather (partition -> global features)
+    int32_t K = 0;
+};
+// B operand: NT: B is [N x K] (ld between rows of N); NN: B is [K x N] (ld between rows of K).
+struct MatB {
+    const float* ptr = nullptr;
+    int64_t ld = 0;
+    bool nn = false;
+};
+
+enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2 };
+
+// C[M x N] = A1 * op(B1) (+ A2 * op(B2)), fp32 in/out, fp32 accumulate, then epilogue.
+void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
+             int32_t N, int epi, const float* row_scale, cudaStream_t s);
+
+// Weight gradient: C[N1 x N2] = A^T [N1 x M] * Bcat [M x N2], where Bcat's
+// columns [0, n2a) come from b1 and [n2a, N2) from b2 (b2 may gather rows).
+// Split-K over M with a fixed-order reduction (deterministic). C has row stride ldc.
+struct MatT {
+    const float* ptr = nullptr;
+    int64_t ld = 0;
+    const int32_t* rows = nullptr;
+    int32_t cols = 0;
+};
+void gemm_tn(const MatT& a, const MatT& b1, const MatT* b2, int64_t M, float* C, int64_t ldc, float* workspace,
+             int64_t workspace_floats, cudaStream_t s);
+int64_t gemm_tn_workspace_floats(int32_t N1, int32_t N2);
+
+// Per-node inverse masked degree (nn.hpp:174-188, 209-215): inv = d > 0 ? 1/d : 0.
+void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* mask_bits, float* inv, cudaStream_t s);
+// mean[v] = inv[v] * sum_{k in CSR(v), kept} msg[nbr_k]   (nn.hpp:222-230)
+void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
+              const float* inv, const float* msg, float* mean, cudaStream_t s);
+// dz[u] = 1[msg[u] > 0] * sum_{v in CSR(u), kept} dmean_s[v]   (nn.hpp:277-288, pull form)
+void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
+              const float* dmean_s, const float* msg, float* dz, cudaStream_t s);
+// CSR-slot bitmap of a local-edge-indexed byte mask: bit k = mask[eids[k]].
+void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_t* bits, cudaStream_t s);
+
+// Loss + dloss/dlogits (nn.hpp:317-378). Rows with w == 0 get zero gradient.
+// row_loss[r] = w * (lse - z_y) (CE) in f64; scale[r] = (float)(w / normalizer).
+void softmax_ce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows,
+                const double* w, const float* scale, float* G, double* row_loss, cudaStream_t s);
+void bce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
+         const float* scale, float* G, double* row_loss, cudaStream_t s);
+// Deterministic f64 sum of x[0..n), divided by `divisor`, into *out (fixed-shape two-pass reduction).
+void sum_f64(int64_t n, const double* x, double* partial, double* out, double divisor, cudaStream_t s);
+
+// gathered[k] = sum_{i < p} slots[i][k] in ascending i (trainer.hpp:79-94);
+// f64 sum of squares + non-finite flag for grad_norm / adam_step's check.
+void gather_grads(int64_t P, int32_t p, const float* slots, float* gathered, double* partial, int* nonfinite,
+                  cudaStream_t s);
+// out[0] = sqrt(sum partial) (grad_norm), out[1] = sum part_loss[0..p) in order.
+void finalize_step(const double* partial, const double* part_loss, int32_t p, double* out, cudaStream_t s);
+// Adam (nn.hpp:400-432); skipped entirely when *nonfinite is set.
+void adam(int64_t P, float* theta, float* m1, float* m2, const float* g, float b1, float b2, float c1, float c2,
+          float lr, float eps, const int* nonfinite, cudaStream_t s);
+
+// Accuracy of argmax(logits) over masked rows (trainer.cpp:66-97, multi-class).
+void count_correct(int64_t n, int32_t C, const float* logits, const int32_t* labels, const uint8_t* mask,
+                   unsigned long long* correct_and_total, cudaStream_t s);
+
+}  // namespace sc

@@ -1,0 +1,441 @@
+// trainer.cu — train_cofree_impl (proj/include/sagecut/trainer.hpp:202-313) on
+// the device: one rank per GPU owns partitions i with i % world == rank, runs
+// their forward / loss / backward back to back on one stream, exchanges the
+// per-partition gradient slots with one NCCL all-reduce, then every rank sums
+// the slots in ascending partition order (the reference's gather_gradients,
+// trainer.hpp:79-94) and applies the same Adam step.
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "gemm_tc.cuh"
+#include "internal.hpp"
+#include "nn.cuh"
+#include "trainer.hpp"
+
+namespace sc {
+
+#define SC_NCCL(expr)                                                                                        \
+    do {                                                                                                     \
+        ncclResult_t sc_r_ = (expr);                                                                         \
+        if (sc_r_ != ncclSuccess) throw ::sc::NcclError(std::string(#expr) + ": " + ncclGetErrorString(sc_r_)); \
+    } while (0)
+
+// ---- per-kernel event profiler (bench.py roofline) ---------------------------
+void Profiler::begin(const char* name, double bytes, cudaStream_t s) {
+    if (!enabled) return;
+    if (used == events.size()) {
+        cudaEvent_t a, b;
+        SC_CUDA(cudaEventCreate(&a));
+        SC_CUDA(cudaEventCreate(&b));
+        events.push_back({a, b});
+    }
+    cur_name = name;
+    cur_bytes = bytes;
+    SC_CUDA(cudaEventRecord(events[used].first, s));
+}
+void Profiler::end(cudaStream_t s) {
+    if (!enabled) return;
+    SC_CUDA(cudaEventRecord(events[used].second, s));
+    records.push_back({cur_name, cur_bytes, used});
+    ++used;
+}
+void Profiler::collect() {
+    if (!enabled) return;
+    totals.clear();
+    for (const auto& r : records) {
+        float ms = 0.f;
+        SC_CUDA(cudaEventElapsedTime(&ms, events[r.slot].first, events[r.slot].second));
+        auto& t = totals[r.name];
+        t.ms += ms;
+        t.bytes += r.bytes;
+        t.calls += 1;
+    }
+    records.clear();
+    used = 0;
+}
+Profiler::~Profiler() {
+    for (auto& e : events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+sc_trainer::~sc_trainer() {
+    if (comm) ncclCommDestroy(comm);
+}
+
+namespace sc {
+
+void trainer_init(sc_trainer* t) {
+    sc_graph* g = t->g;
+    sc_vcut* vc = t->vc;
+    if (!(t->lr > 0.0)) throw std::invalid_argument("learning rate must be > 0");
+    if (t->L < 0) throw std::invalid_argument("layers must be >= 0");
+    for (int h : t->hidden)
+        if (h < 1) throw std::invalid_argument("hidden dims must be positive");
+    if (t->use_dropedge) {
+        if (t->K < 1) throw std::invalid_argument("dropedge_k must be >= 1");
+        if (t->ratio < 0.0 || t->ratio >= 1.0) throw std::invalid_argument("drop_ratio must lie in [0, 1)");
+    }
+    if (g->dim == 0) throw std::invalid_argument("training requires node features");
+    if (g->num_classes == 0) throw std::invalid_argument("training requires labels");
+    if (g->train_count == 0) throw std::invalid_argument("training requires a non-empty train mask");
+    if (vc->g != g || vc->parts.empty()) throw std::invalid_argument("train_cofree: partition does not match graph");
+    if (t->world < 1 || t->rank < 0 || t->rank >= t->world) throw std::invalid_argument("bad rank/world");
+    cudaStream_t s = t->ctx->stream;
+    t->normalizer = static_cast<double>(g->train_count);
+    t->d = g->dim;
+    t->C = g->num_classes;
+    t->p = vc->p;
+    // flat parameter layout (for_each_matrix order)
+    int64_t off = 0;
+    int in = t->d;
+    for (int l = 0; l < t->L; ++l) {
+        LayerOff lo;
+        lo.in = in;
+        lo.H = t->hidden[l];
+        lo.W = off;
+        off += int64_t(lo.H) * in;
+        lo.U = off;
+        off += int64_t(lo.H) * (lo.H + in);
+        t->lay.push_back(lo);
+        in = lo.H;
+    }
+    t->E = in;
+    t->head_off = off;
+    off += int64_t(t->C) * t->E;
+    t->P = off;
+    t->theta.alloc(t->P);
+    t->m1.alloc(t->P);
+    t->m2.alloc(t->P);
+    t->gathered.alloc(t->P);
+    t->slots.alloc(int64_t(t->p) * t->P);
+    SC_CUDA(cudaMemsetAsync(t->m1.get(), 0, t->m1.bytes(), s));
+    SC_CUDA(cudaMemsetAsync(t->m2.get(), 0, t->m2.bytes(), s));
+    SC_CUDA(cudaMemsetAsync(t->slots.get(), 0, t->slots.bytes(), s));
+    init_params_device(t->ctx, t->d, t->hidden.data(), t->L, t->C, t->seed, t->theta.get());
+
+    // per-partition inputs (trainer.hpp:218-243)
+    int64_t n_max = 1, nnz_max = 1;
+    t->local.clear();
+    for (int i = t->rank; i < t->p; i += t->world) t->local.push_back(i);
+    t->ps.resize(t->p);
+    DevBuf<double> wtmp;
+    for (int i = 0; i < t->p; ++i) {
+        PartState& st = t->ps[i];
+        const PartDev& pd = vc->parts[i];
+        st.n = pd.n_local;
+        st.nnz = 2 * pd.m_local;
+        const bool mine = (i % t->world) == t->rank;
+        if (!mine) continue;
+        n_max = std::max(n_max, st.n);
+        nnz_max = std::max(nnz_max, st.nnz);
+        st.w.alloc(std::max<int64_t>(st.n, 1));
+        st.scale.alloc(std::max<int64_t>(st.n, 1));
+        compute_weights_device(vc, t->reweight, i, st.w.get());
+        loss_weights(t, i);
+        st.logits.alloc(std::max<int64_t>(st.n * t->C, 1));
+        if (t->use_dropedge) {
+            st.words = (st.nnz + 31) / 32;
+            st.bits.alloc(std::max<int64_t>(st.words * t->K, 1));
+            DevBuf<uint8_t> masks(std::max<int64_t>(pd.m_local * t->K, 1));
+            // partition_mask_set (trainer.hpp:117-121)
+            precompute_masks_device(t->ctx, pd.m_local, t->K, t->ratio, substream(t->seed, "dropedge", uint64_t(i)),
+                                    masks.get());
+            for (int k = 0; k < t->K; ++k)
+                mask_to_bits(st.nnz, pd.eids.get(), masks.get() + int64_t(k) * pd.m_local, st.bits.get() + k * st.words,
+                             s);
+            SC_CUDA(cudaStreamSynchronize(s));
+        }
+    }
+    t->part_loss.alloc(t->p);
+    t->out2.alloc(2);
+    t->nonfinite.alloc(1);
+    t->red_partial.alloc(1024);
+    ensure_rows(t, n_max);
+    int32_t maxN1 = t->C, maxN2 = t->E;
+    for (auto& lo : t->lay) {
+        maxN1 = std::max(maxN1, lo.H);
+        maxN2 = std::max(maxN2, lo.H + lo.in);
+    }
+    t->ws_floats = gemm_tn_workspace_floats(maxN1, maxN2);
+    t->ws.alloc(t->ws_floats);
+    t->tc.init(t);
+    SC_CUDA(cudaStreamSynchronize(s));
+}
+
+// loss weight = train_mask ? scheme weight : 0; scale = (float)(w / normalizer)
+__global__ void loss_weight_kernel(int64_t n, const int32_t* nodes, const uint8_t* train, double* w, float* scale,
+                                   double normalizer) {
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
+        const double x = train[nodes[j]] ? w[j] : 0.0;
+        w[j] = x;
+        scale[j] = static_cast<float>(x / normalizer);
+    }
+}
+
+void loss_weights(sc_trainer* t, int i) {
+    PartState& st = t->ps[i];
+    if (st.n == 0) return;
+    loss_weight_kernel<<<grid_for(st.n, 256), 256, 0, t->ctx->stream>>>(
+        st.n, t->vc->parts[i].nodes.get(), t->g->train.get(), st.w.get(), st.scale.get(), t->normalizer);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+
+void ensure_rows(sc_trainer* t, int64_t n) {
+    if (n <= t->rows_cap) return;
+    t->rows_cap = n;
+    int32_t maxH = std::max<int32_t>(t->E, 1), maxW = std::max<int32_t>(t->E, t->d);
+    for (auto& lo : t->lay) {
+        maxH = std::max(maxH, lo.H);
+        maxW = std::max(maxW, std::max(lo.H, lo.in));
+    }
+    t->X.clear();
+    t->MSG.clear();
+    t->MEAN.clear();
+    t->X.resize(t->L + 1);
+    t->MSG.resize(t->L);
+    t->MEAN.resize(t->L);
+    for (int l = 0; l < t->L; ++l) {
+        t->X[l + 1].alloc(n * t->lay[l].H);
+        t->MSG[l].alloc(n * t->lay[l].H);
+        t->MEAN[l].alloc(n * t->lay[l].H);
+    }
+    t->inv.alloc(n);
+    t->G.alloc(n * t->C);
+    t->dh.alloc(n * maxW);
+    t->dh2.alloc(n * maxW);
+    t->dmean.alloc(n * maxH);
+    t->dz.alloc(n * maxH);
+    t->row_loss.alloc(n);
+    t->eval_logits.release();
+}
+
+namespace {
+
+struct Rows {
+    int64_t n;
+    const int64_t* offsets;
+    const int32_t* nbrs;
+    const uint32_t* bits;
+    const int32_t* nodes;  // local -> global row (features / labels); null = identity
+};
+
+// sage_forward (nn.hpp:192-242). Writes logits; keeps the cache in t's buffers.
+void forward(sc_trainer* t, const Rows& R, float* logits) {
+    cudaStream_t s = t->ctx->stream;
+    Profiler& P = t->prof;
+    const int64_t n = R.n;
+    P.begin("inv_degree", double(n) * 12 + double(R.offsets ? 8 : 0) * n, s);
+    inv_degree(n, R.offsets, R.bits, t->inv.get(), s);
+    P.end(s);
+    const MatA x0{t->g->features.get(), t->d, R.nodes, t->d};
+    for (int l = 0; l < t->L; ++l) {
+        const LayerOff& lo = t->lay[l];
+        const MatA xin = l == 0 ? x0 : MatA{t->X[l].get(), lo.in, nullptr, lo.in};
+        // msg = relu(h W^T)   (nn.hpp:220-221)
+        P.begin("gemm_msg", 4.0 * n * (lo.in + lo.H), s);
+        t->tc.nt(t, xin, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, t->MSG[l].get(), lo.H, n, lo.H,
+                 kEpiRelu, nullptr);
+        P.end(s);
+        // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
+        P.begin("spmm_fwd", 0.0, s);
+        spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->inv.get(), t->MSG[l].get(), t->MEAN[l].get(), s);
+        P.end(s);
+        // h' = mean U_L^T + h U_R^T   (nn.hpp:233-234)
+        const MatB uL{t->theta.get() + lo.U, lo.H + lo.in, false};
+        const MatB uR{t->theta.get() + lo.U + lo.H, lo.H + lo.in, false};
+        const MatA mean{t->MEAN[l].get(), lo.H, nullptr, lo.H};
+        P.begin("gemm_update", 4.0 * n * (2 * lo.H + lo.in), s);
+        t->tc.nt(t, mean, uL, &xin, &uR, t->X[l + 1].get(), lo.H, n, lo.H, kEpiNone, nullptr);
+        P.end(s);
+    }
+    const MatA emb = t->L == 0 ? x0 : MatA{t->X[t->L].get(), t->E, nullptr, t->E};
+    P.begin("gemm_head", 4.0 * n * (t->E + t->C), s);
+    gemm_nt(emb, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, logits, t->C, n, t->C, kEpiNone,
+            nullptr, s);
+    P.end(s);
+}
+
+// sage_backward (nn.hpp:246-293) into one gradient slot.
+void backward(sc_trainer* t, const Rows& R, float* slot) {
+    cudaStream_t s = t->ctx->stream;
+    Profiler& P = t->prof;
+    const int64_t n = R.n;
+    const MatA x0{t->g->features.get(), t->d, R.nodes, t->d};
+    const MatT x0t{t->g->features.get(), t->d, R.nodes, t->d};
+    const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L].get(), t->E, nullptr, t->E};
+    // head grad = G^T emb ; dh = G head   (:259-260)
+    P.begin("wgrad", 4.0 * n * (t->C + t->E), s);
+    gemm_tn(MatT{t->G.get(), t->C, nullptr, t->C}, embt, nullptr, n, slot + t->head_off, t->E, t->ws.get(), t->ws_floats,
+            s);
+    P.end(s);
+    float* dh = t->dh.get();
+    float* dh2 = t->dh2.get();
+    if (t->L == 0) return;
+    P.begin("gemm_dgrad", 4.0 * n * (t->C + t->E), s);
+    gemm_nt(MatA{t->G.get(), t->C, nullptr, t->C}, MatB{t->theta.get() + t->head_off, t->E, true}, nullptr, nullptr, dh,
+            t->E, n, t->E, kEpiNone, nullptr, s);
+    P.end(s);
+    for (int l = t->L - 1; l >= 0; --l) {
+        const LayerOff& lo = t->lay[l];
+        const MatT xint = l == 0 ? x0t : MatT{t->X[l].get(), lo.in, nullptr, lo.in};
+        const MatT dht{dh, lo.H, nullptr, lo.H};
+        // dU = dh^T [mean | h_in]   (:271-272)
+        const MatT meant{t->MEAN[l].get(), lo.H, nullptr, lo.H};
+        P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), s);
+        gemm_tn(dht, meant, &xint, n, slot + lo.U, lo.H + lo.in, t->ws.get(), t->ws_floats, s);
+        P.end(s);
+        // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
+        P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s);
+        t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr, nullptr,
+                 t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get());
+        P.end(s);
+        // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
+        P.begin("spmm_bwd", 0.0, s);
+        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s);
+        P.end(s);
+        // dW = dz^T h_in   (:289)
+        P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s);
+        gemm_tn(MatT{t->dz.get(), lo.H, nullptr, lo.H}, xint, nullptr, n, slot + lo.W, lo.in, t->ws.get(), t->ws_floats,
+                s);
+        P.end(s);
+        if (l > 0) {  // dh = dh U_R + dz W   (:275, :290); layer 0's is unused
+            const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz.get(), lo.H, nullptr, lo.H};
+            P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s);
+            const MatB wB{t->theta.get() + lo.W, lo.in, true};
+            t->tc.nt(t, dhA, MatB{t->theta.get() + lo.U + lo.H, lo.H + lo.in, true}, &dzA, &wB, dh2, lo.in, n, lo.in,
+                     kEpiNone, nullptr);
+            P.end(s);
+            std::swap(dh, dh2);
+        }
+    }
+}
+
+}  // namespace
+
+void run_partition(sc_trainer* t, int i, int epoch) {
+    cudaStream_t s = t->ctx->stream;
+    PartState& st = t->ps[i];
+    const PartDev& pd = t->vc->parts[i];
+    const uint32_t* bits = nullptr;
+    st.chosen = -1;
+    if (t->use_dropedge) {  // trainer.hpp:261-266
+        HostRng rng(substream(t->seed, "dropedge.select", uint64_t(i), uint64_t(epoch)));
+        st.chosen = static_cast<int>(rng.next_below(uint64_t(t->K)));
+        bits = st.bits.get() + int64_t(st.chosen) * st.words;
+    }
+    const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get()};
+    forward(t, R, st.logits.get());
+    t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
+    if (t->loss == 0)
+        softmax_ce(st.n, t->C, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
+                   t->G.get(), t->row_loss.get(), s);
+    else
+        bce(st.n, t->C, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(), t->G.get(),
+            t->row_loss.get(), s);
+    sum_f64(st.n, t->row_loss.get(), t->red_partial.get(), t->part_loss.get() + i, t->normalizer, s);
+    t->prof.end(s);
+    backward(t, R, t->slots.get() + int64_t(i) * t->P);
+}
+
+void trainer_step_async(sc_trainer* t, int epoch) {
+    cudaStream_t s = t->ctx->stream;
+    t->prof.records.clear();
+    t->prof.used = 0;
+    // Slots and losses of partitions owned by other ranks arrive via the all-reduce.
+    if (t->world > 1) {
+        SC_CUDA(cudaMemsetAsync(t->slots.get(), 0, t->slots.bytes(), s));
+        SC_CUDA(cudaMemsetAsync(t->part_loss.get(), 0, t->part_loss.bytes(), s));
+    }
+    for (int i : t->local) run_partition(t, i, epoch);
+    if (t->world > 1) {
+        if (!t->comm) throw std::invalid_argument("sc_trainer_init_comm must be called before stepping with world > 1");
+        t->prof.begin("allreduce", 4.0 * t->p * t->P, s);
+        SC_NCCL(ncclGroupStart());
+        SC_NCCL(ncclAllReduce(t->slots.get(), t->slots.get(), size_t(t->p) * t->P, ncclFloat32, ncclSum, t->comm, s));
+        SC_NCCL(ncclAllReduce(t->part_loss.get(), t->part_loss.get(), size_t(t->p), ncclFloat64, ncclSum, t->comm, s));
+        SC_NCCL(ncclGroupEnd());
+        t->prof.end(s);
+    }
+    SC_CUDA(cudaMemsetAsync(t->nonfinite.get(), 0, 4, s));
+    t->prof.begin("gather_adam", 4.0 * t->P * (t->p + 6), s);
+    gather_grads(t->P, t->p, t->slots.get(), t->gathered.get(), t->red_partial.get(), t->nonfinite.get(), s);
+    finalize_step(t->red_partial.get(), t->part_loss.get(), t->p, t->out2.get(), s);
+    // adam_step (nn.hpp:400-432): corrections in f64, cast to float
+    const int64_t step = t->adam_step + 1;
+    const float c1 = static_cast<float>(1.0 - std::pow(0.9, static_cast<double>(step)));
+    const float c2 = static_cast<float>(1.0 - std::pow(0.999, static_cast<double>(step)));
+    adam(t->P, t->theta.get(), t->m1.get(), t->m2.get(), t->gathered.get(), 0.9f, 0.999f, c1, c2,
+         static_cast<float>(t->lr), static_cast<float>(1e-8), t->nonfinite.get(), s);
+    t->prof.end(s);
+    d2h(t->host_out, t->out2.get(), 2, s);
+    d2h(&t->host_nonfinite, t->nonfinite.get(), 1, s);
+    t->pending = true;
+}
+
+void trainer_finish(sc_trainer* t, double* loss, double* gnorm) {
+    if (t->pending) {
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+        t->pending = false;
+        t->prof.collect();
+        if (t->host_nonfinite) throw std::invalid_argument("adam_step: non-finite gradient");
+        ++t->adam_step;
+        t->last_loss = t->host_out[1];
+        t->last_gnorm = t->host_out[0];
+    }
+    if (loss) *loss = t->last_loss;
+    if (gnorm) *gnorm = t->last_gnorm;
+}
+
+void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
+    cudaStream_t s = t->ctx->stream;
+    sc_graph* g = t->g;
+    ensure_rows(t, g->n);
+    if (t->eval_logits.size() < size_t(g->n) * t->C) t->eval_logits.alloc(size_t(g->n) * t->C);
+    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr};
+    const bool was = t->prof.enabled;
+    t->prof.enabled = false;
+    forward(t, R, t->eval_logits.get());
+    t->prof.enabled = was;
+    DevBuf<unsigned long long> cnt(6);
+    SC_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+    count_correct(g->n, t->C, t->eval_logits.get(), g->labels.get(), g->train.get(), cnt.get(), s);
+    count_correct(g->n, t->C, t->eval_logits.get(), g->labels.get(), g->val.get(), cnt.get() + 2, s);
+    count_correct(g->n, t->C, t->eval_logits.get(), g->labels.get(), g->test.get(), cnt.get() + 4, s);
+    unsigned long long h[6];
+    d2h(h, cnt.get(), 6, s);
+    SC_CUDA(cudaStreamSynchronize(s));
+    auto frac = [](unsigned long long c, unsigned long long n) { return n ? double(c) / double(n) : 0.0; };
+    *tr = frac(h[0], h[1]);
+    *va = frac(h[2], h[3]);
+    *te = frac(h[4], h[5]);
+}
+
+void trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
+    ncclUniqueId uid;
+    static_assert(sizeof(uid.internal) == 128, "ncclUniqueId size");
+    std::memcpy(uid.internal, id, 128);
+    SC_CUDA(cudaSetDevice(t->ctx->device));
+    SC_NCCL(ncclCommInitRank(&t->comm, t->world, uid, t->rank));
+}
+
+void nccl_unique_id(uint8_t out[128]) {
+    ncclUniqueId uid;
+    SC_NCCL(ncclGetUniqueId(&uid));
+    std::memcpy(out, uid.internal, 128);
+}
+
+}  // namespace sc

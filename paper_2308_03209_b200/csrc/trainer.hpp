@@ -1,0 +1,108 @@
+// trainer.hpp — sc_trainer state (train_cofree_impl, proj/include/sagecut/trainer.hpp:202-313).
+#pragma once
+
+#include <nccl.h>
+
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gemm_tc.cuh"
+#include "internal.hpp"
+#include "nn.cuh"
+
+namespace sc {
+
+struct LayerOff {
+    int in = 0, H = 0;
+    int64_t W = 0, U = 0;  // offsets of message / update in the flat parameter vector
+};
+
+struct PartState {
+    int64_t n = 0, nnz = 0;
+    DevBuf<double> w;      // loss weight (train ? scheme weight : 0)
+    DevBuf<float> scale;   // (float)(w / normalizer)
+    DevBuf<uint32_t> bits; // K CSR-slot bitmaps
+    int64_t words = 0;
+    DevBuf<float> logits;  // n x C, last step
+    int chosen = -1;
+};
+
+struct Profiler {
+    struct Rec {
+        const char* name;
+        double bytes;
+        size_t slot;
+    };
+    struct Total {
+        double ms = 0, bytes = 0;
+        int calls = 0;
+    };
+    bool enabled = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+    std::vector<Rec> records;
+    size_t used = 0;
+    const char* cur_name = nullptr;
+    double cur_bytes = 0;
+    std::map<std::string, Total> totals;
+    void begin(const char* name, double bytes, cudaStream_t s);
+    void end(cudaStream_t s);
+    void collect();
+    ~Profiler();
+};
+
+}  // namespace sc
+
+struct sc_trainer {
+    sc_ctx* ctx = nullptr;
+    sc_graph* g = nullptr;
+    sc_vcut* vc = nullptr;
+    int rank = 0, world = 1;
+    // config
+    int L = 0;
+    std::vector<int> hidden;
+    double lr = 0.01;
+    int loss = 0, reweight = 0, use_dropedge = 0, K = 10;
+    double ratio = 0.5;
+    uint64_t seed = 0;
+    int deterministic = 1, gemm_mode = 0;
+    // dims
+    int d = 0, C = 0, E = 0, p = 0;
+    std::vector<sc::LayerOff> lay;
+    int64_t head_off = 0, P = 0;
+    double normalizer = 1.0;
+    // parameters / optimizer / gradients
+    sc::DevBuf<float> theta, m1, m2, gathered, slots;
+    int64_t adam_step = 0;
+    // partitions
+    std::vector<int> local;
+    std::vector<sc::PartState> ps;
+    // activations (rows_cap rows)
+    int64_t rows_cap = 0;
+    std::vector<sc::DevBuf<float>> X, MSG, MEAN;
+    sc::DevBuf<float> inv, G, dh, dh2, dmean, dz, eval_logits, ws;
+    int64_t ws_floats = 0;
+    sc::DevBuf<double> row_loss, part_loss, out2, red_partial;
+    sc::DevBuf<int> nonfinite;
+    double host_out[2] = {0, 0};
+    int host_nonfinite = 0;
+    bool pending = false;
+    double last_loss = 0, last_gnorm = 0;
+    sc::TcGemm tc;
+    sc::Profiler prof;
+    ncclComm_t comm = nullptr;
+    ~sc_trainer();
+};
+
+namespace sc {
+void trainer_init(sc_trainer* t);
+void loss_weights(sc_trainer* t, int i);
+void ensure_rows(sc_trainer* t, int64_t n);
+void run_partition(sc_trainer* t, int i, int epoch);
+void trainer_step_async(sc_trainer* t, int epoch);
+void trainer_finish(sc_trainer* t, double* loss, double* gnorm);
+void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te);
+void trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
+void nccl_unique_id(uint8_t out[128]);
+}  // namespace sc

@@ -1,0 +1,583 @@
+"""Python mirror of the reference's `sagecut` API over libsagecut_cuda.so.
+
+Every public name follows the reference C++ API it replaces (cited per item);
+all compute runs in the sm_100a kernels of libsagecut_cuda.so behind the C ABI
+declared in include/sagecut_cuda.h. There is no CPU fallback: importing this
+module without the built library, or calling it without a CUDA device, raises.
+
+Used by tests/ (parity against the oracle) and bench.py. The C++ facade for
+C++ callers of the reference is include/sagecut_b200.hpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsagecut_cuda.so")
+
+SC_OK, SC_EINVAL, SC_ERUNTIME, SC_EINTERNAL, SC_ECUDA, SC_ENCCL = range(6)
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class NcclError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    return C.CDLL(LIB_PATH)
+
+
+_lib = _load()
+_vp = C.c_void_p
+_pp = C.POINTER(C.c_void_p)
+_i32, _i64, _u64, _f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+
+
+def _sig(name, args, res=C.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_sig("sc_last_error", [], C.c_char_p)
+_sig("sc_version", [], C.c_char_p)
+_sig("sc_ctx_create", [C.c_int, _pp])
+_sig("sc_ctx_destroy", [_vp])
+_sig("sc_ctx_sync", [_vp])
+_sig("sc_ctx_launch_count", [_vp], _i64)
+_sig("sc_build_graph", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i64)])
+_sig("sc_build_graph_dev", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i64)])
+_sig("sc_graph_set_data", [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp])
+_sig("sc_graph_set_features", [_vp, _vp, C.c_int])
+_sig("sc_graph_info", [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i32)])
+_sig("sc_graph_copy_edges", [_vp, _vp])
+_sig("sc_graph_copy_csr", [_vp, _vp, _vp, _vp, _vp])
+_sig("sc_graph_destroy", [_vp])
+_sig("sc_partition_random", [_vp, _i32, _u64, _pp])
+_sig("sc_partition_dbh", [_vp, _i32, _u64, _pp])
+_sig("sc_build_vertex_cut", [_vp, _i32, _vp, _pp])
+_sig("sc_vcut_num_parts", [_vp, C.POINTER(_i32)])
+_sig("sc_vcut_assignment", [_vp, _vp])
+_sig("sc_vcut_part_sizes", [_vp, _i32, C.POINTER(_i64), C.POINTER(_i64)])
+_sig("sc_vcut_part_copy", [_vp, _i32] + [_vp] * 8)
+_sig("sc_replication_stats", [_vp, _vp, C.POINTER(_f64), C.POINTER(_f64), C.POINTER(_f64), C.POINTER(_i64)])
+_sig("sc_vcut_destroy", [_vp])
+_sig("sc_compute_weights", [_vp, _i32, _vp])
+_sig("sc_precompute_masks", [_vp, _i64, _i32, _f64, _u64, _vp])
+_sig("sc_select_mask", [_u64, _u64, _u64, _i32], _i32)
+_sig("sc_substream", [_u64, C.c_char_p, _i32, _u64, _u64], _u64)
+_sig("sc_param_count", [_i32, _vp, _i32, _i32], _i64)
+_sig("sc_init_params", [_vp, _i32, _vp, _i32, _i32, _u64, _vp])
+
+
+class _TrainConfigC(C.Structure):
+    _fields_ = [("layers", _i32), ("hidden", _vp), ("learning_rate", _f64), ("loss", _i32), ("reweight", _i32),
+                ("use_dropedge", _i32), ("dropedge_k", _i32), ("drop_ratio", _f64), ("seed", _u64),
+                ("deterministic", _i32), ("gemm", _i32)]
+
+
+_sig("sc_trainer_create", [_vp, _vp, _vp, C.POINTER(_TrainConfigC), _i32, _i32, _pp])
+_sig("sc_nccl_unique_id", [_vp])
+_sig("sc_trainer_init_comm", [_vp, _vp])
+_sig("sc_trainer_step", [_vp, _i32, C.POINTER(_f64), C.POINTER(_f64)])
+_sig("sc_trainer_step_async", [_vp, _i32])
+_sig("sc_trainer_last", [_vp, C.POINTER(_f64), C.POINTER(_f64)])
+_sig("sc_trainer_param_count", [_vp, C.POINTER(_i64)])
+for _n in ("sc_trainer_get_params", "sc_trainer_set_params", "sc_trainer_get_grads"):
+    _sig(_n, [_vp, _vp])
+_sig("sc_trainer_get_part_grads", [_vp, _i32, _vp])
+_sig("sc_trainer_get_part_logits", [_vp, _i32, _vp])
+_sig("sc_trainer_get_part_loss", [_vp, _i32, C.POINTER(_f64)])
+_sig("sc_trainer_get_part_mask", [_vp, _i32, C.POINTER(_i32)])
+_sig("sc_trainer_evaluate", [_vp, C.POINTER(_f64), C.POINTER(_f64), C.POINTER(_f64)])
+_sig("sc_trainer_profile", [_vp, _i32])
+_sig("sc_trainer_kernel_times", [_vp, C.POINTER(C.c_char_p), C.POINTER(_f64), C.POINTER(_f64), _i32,
+                                 C.POINTER(_i32)])
+_sig("sc_trainer_destroy", [_vp])
+
+
+def _check(status: int, what: str = ""):
+    if status == SC_OK:
+        return
+    msg = _lib.sc_last_error().decode()
+    exc = {SC_EINVAL: ValueError, SC_ERUNTIME: RuntimeError, SC_EINTERNAL: AssertionError, SC_ECUDA: CudaError,
+           SC_ENCCL: NcclError}.get(status, RuntimeError)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(_vp)
+
+
+def version() -> str:
+    return _lib.sc_version().decode()
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """One CUDA device + stream + scratch (sc_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(_lib.sc_ctx_create(device, C.byref(h)), "sc_ctx_create")
+        self.h = h
+        self.device = device
+
+    def sync(self):
+        _check(_lib.sc_ctx_sync(self.h))
+
+    def launch_count(self) -> int:
+        return int(_lib.sc_ctx_launch_count(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.sc_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("SC_DEVICE") is None
+                               else int(os.environ["SC_DEVICE"]))
+    return _default_ctx
+
+
+@dataclass
+class ValidationReport:  # graph.hpp:43-48
+    dropped_self_loops: int = 0
+    merged_duplicate_edges: int = 0
+
+
+class Graph:
+    """sagecut::Graph (graph.hpp:53-80), device resident."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h, self.ctx = handle, ctx
+        n, m, d, c = _i32(), _i64(), _i32(), _i32()
+        _check(_lib.sc_graph_info(self.h, C.byref(n), C.byref(m), C.byref(d), C.byref(c)))
+        self.num_nodes, self._m, self.dim, self.num_classes = n.value, m.value, d.value, c.value
+
+    def num_edges(self) -> int:
+        return self._m
+
+    def edges(self) -> np.ndarray:
+        out = np.zeros((self._m, 2), np.int32)
+        _check(_lib.sc_graph_copy_edges(self.h, _ptr(out)))
+        return out
+
+    def csr(self):
+        off = np.zeros(self.num_nodes + 1, np.int64)
+        nb = np.zeros(2 * self._m, np.int32)
+        ei = np.zeros(2 * self._m, np.int32)
+        dg = np.zeros(self.num_nodes, np.int32)
+        _check(_lib.sc_graph_copy_csr(self.h, _ptr(off), _ptr(nb), _ptr(ei), _ptr(dg)))
+        return off, nb, ei, dg
+
+    def set_data(self, features, labels, num_classes, train_mask, val_mask, test_mask):
+        f = np.ascontiguousarray(features, np.float32)
+        if f.ndim != 2 or f.shape[0] != self.num_nodes:
+            raise ValueError("set_data: features must be num_nodes x d")
+        lab = np.ascontiguousarray(labels, np.int32)
+        tr, va, te = (np.ascontiguousarray(x, np.uint8) for x in (train_mask, val_mask, test_mask))
+        _check(_lib.sc_graph_set_data(self.h, _ptr(f), f.shape[1], _ptr(lab), int(num_classes), _ptr(tr), _ptr(va),
+                                      _ptr(te)), "set_data")
+        self.dim, self.num_classes = f.shape[1], int(num_classes)
+
+    def set_features(self, features, device_ptr: Optional[int] = None):
+        if device_ptr is not None:
+            _check(_lib.sc_graph_set_features(self.h, _vp(device_ptr), 1))
+        else:
+            f = np.ascontiguousarray(features, np.float32)
+            _check(_lib.sc_graph_set_features(self.h, _ptr(f), 0))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.sc_graph_destroy(self.h)
+            self.h = None
+
+
+def build_graph(num_nodes: int, raw_edges, ctx: Optional[Context] = None):
+    """build_graph (graph.cpp:8-64) on the device -> (Graph, ValidationReport)."""
+    ctx = ctx or default_context()
+    raw = np.ascontiguousarray(raw_edges, np.int32).reshape(-1, 2)
+    h = _vp()
+    sl, du = _i64(), _i64()
+    _check(_lib.sc_build_graph(ctx.h, int(num_nodes), _ptr(raw), len(raw), C.byref(h), C.byref(sl), C.byref(du)),
+           "build_graph")
+    return Graph(h, ctx), ValidationReport(sl.value, du.value)
+
+
+def build_graph_device(num_nodes: int, raw_dev_ptr: int, m_raw: int, ctx: Optional[Context] = None):
+    """build_graph from a raw int32 [m][2] edge list already in device memory."""
+    ctx = ctx or default_context()
+    h = _vp()
+    sl, du = _i64(), _i64()
+    _check(_lib.sc_build_graph_dev(ctx.h, int(num_nodes), _vp(raw_dev_ptr), int(m_raw), C.byref(h), C.byref(sl),
+                                   C.byref(du)), "build_graph")
+    return Graph(h, ctx), ValidationReport(sl.value, du.value)
+
+
+@dataclass
+class PartSubgraph:  # partition.hpp:14-31
+    nodes: np.ndarray
+    edges: np.ndarray
+    edge_global_ids: np.ndarray
+    local_degrees: np.ndarray
+    adj_offsets: np.ndarray
+    adj_neighbors: np.ndarray
+    adj_edge_ids: np.ndarray
+    global_to_local: np.ndarray
+
+    def num_local_nodes(self) -> int:
+        return len(self.nodes)
+
+
+@dataclass
+class ReplicationStats:  # partition.hpp:50-56
+    rf: float
+    per_node_rf: np.ndarray
+    edge_balance: float
+    node_balance: float
+    duplicated_nodes: int
+
+
+class VertexCutPartition:
+    """sagecut::VertexCutPartition (partition.hpp:35-40); parts stay on the device,
+    `part(i)` copies one PartSubgraph to the host for inspection."""
+
+    def __init__(self, handle, g: Graph):
+        self.h, self.g = handle, g
+        p = _i32()
+        _check(_lib.sc_vcut_num_parts(self.h, C.byref(p)))
+        self.num_parts = p.value
+
+    @property
+    def edge_assignment(self) -> np.ndarray:
+        out = np.zeros(self.g.num_edges(), np.int32)
+        _check(_lib.sc_vcut_assignment(self.h, _ptr(out)))
+        return out
+
+    def part_sizes(self, i: int):
+        nl, ne = _i64(), _i64()
+        _check(_lib.sc_vcut_part_sizes(self.h, i, C.byref(nl), C.byref(ne)))
+        return nl.value, ne.value
+
+    def part(self, i: int) -> PartSubgraph:
+        nl, ne = self.part_sizes(i)
+        s = PartSubgraph(np.zeros(nl, np.int32), np.zeros((ne, 2), np.int32), np.zeros(ne, np.int32),
+                         np.zeros(nl, np.int32), np.zeros(nl + 1, np.int64), np.zeros(2 * ne, np.int32),
+                         np.zeros(2 * ne, np.int32), np.zeros(self.g.num_nodes, np.int32))
+        _check(_lib.sc_vcut_part_copy(self.h, i, _ptr(s.nodes), _ptr(s.edges), _ptr(s.edge_global_ids),
+                                      _ptr(s.local_degrees), _ptr(s.adj_offsets), _ptr(s.adj_neighbors),
+                                      _ptr(s.adj_edge_ids), _ptr(s.global_to_local)))
+        return s
+
+    @property
+    def parts(self) -> List[PartSubgraph]:
+        return [self.part(i) for i in range(self.num_parts)]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.sc_vcut_destroy(self.h)
+            self.h = None
+
+
+def partition_random(g: Graph, num_parts: int, seed: int) -> VertexCutPartition:  # partition.cpp:92
+    h = _vp()
+    _check(_lib.sc_partition_random(g.h, num_parts, seed, C.byref(h)), "partition_random")
+    return VertexCutPartition(h, g)
+
+
+def partition_dbh(g: Graph, num_parts: int, seed: int) -> VertexCutPartition:  # partition.cpp:102
+    h = _vp()
+    _check(_lib.sc_partition_dbh(g.h, num_parts, seed, C.byref(h)), "partition_dbh")
+    return VertexCutPartition(h, g)
+
+
+def build_vertex_cut(g: Graph, num_parts: int, edge_assignment) -> VertexCutPartition:  # partition.cpp:22
+    a = np.ascontiguousarray(edge_assignment, np.int32)
+    if len(a) != g.num_edges():
+        raise ValueError("edge assignment length does not match edge count")
+    h = _vp()
+    _check(_lib.sc_build_vertex_cut(g.h, num_parts, _ptr(a), C.byref(h)), "build_vertex_cut")
+    return VertexCutPartition(h, g)
+
+
+def replication_stats(part: VertexCutPartition, g: Graph) -> ReplicationStats:  # partition.cpp:310
+    rfv = np.zeros(g.num_nodes, np.int32)
+    rf, eb, nb = _f64(), _f64(), _f64()
+    dup = _i64()
+    _check(_lib.sc_replication_stats(part.h, _ptr(rfv), C.byref(rf), C.byref(eb), C.byref(nb), C.byref(dup)))
+    return ReplicationStats(rf.value, rfv, eb.value, nb.value, dup.value)
+
+
+_SCHEMES = {"dar": 0, "vanilla_inv": 1, "none": 2}
+_LOSSES = {"softmax_ce": 0, "bce": 1}
+
+
+@dataclass
+class NodeWeights:  # reweight.hpp:15-19
+    scheme: str
+    per_part: List[np.ndarray]
+
+
+def compute_weights(scheme: str, g: Graph, part: VertexCutPartition) -> NodeWeights:  # reweight.cpp:73
+    if scheme not in _SCHEMES:
+        raise ValueError(f"unknown reweight scheme: {scheme}")
+    sizes = [part.part_sizes(i)[0] for i in range(part.num_parts)]
+    out = np.zeros(sum(sizes), np.float64)
+    _check(_lib.sc_compute_weights(part.h, _SCHEMES[scheme], _ptr(out)), "compute_weights")
+    res, k = [], 0
+    for s in sizes:
+        res.append(out[k:k + s].copy())
+        k += s
+    return NodeWeights(scheme, res)
+
+
+@dataclass
+class DropEdgeMaskSet:  # dropedge.hpp:13-18
+    num_masks: int
+    ratio: float
+    seed: int
+    masks: np.ndarray  # [K, num_edges] uint8
+
+
+def precompute_masks(num_edges: int, num_masks: int, ratio: float, seed: int,
+                     ctx: Optional[Context] = None) -> DropEdgeMaskSet:  # dropedge.cpp:9
+    ctx = ctx or default_context()
+    out = np.zeros(max(num_edges * max(num_masks, 0), 1), np.uint8)
+    _check(_lib.sc_precompute_masks(ctx.h, num_edges, num_masks, ratio, seed, _ptr(out)), "precompute_masks")
+    return DropEdgeMaskSet(num_masks, ratio, seed, out[:num_edges * num_masks].reshape(num_masks, num_edges))
+
+
+def select_mask(seed: int, part_index: int, epoch: int, num_masks: int) -> int:  # trainer.hpp:261-266
+    if num_masks < 1:
+        raise ValueError("select_mask: need at least one mask")
+    return int(_lib.sc_select_mask(seed, part_index, epoch, num_masks))
+
+
+def substream(seed: int, tag: str, *idx: int) -> int:  # rng.hpp:94-103
+    a = idx[0] if len(idx) > 0 else 0
+    b = idx[1] if len(idx) > 1 else 0
+    return int(_lib.sc_substream(seed, tag.encode(), len(idx), a, b))
+
+
+def param_count(in_dim: int, hidden: Sequence[int], num_classes: int) -> int:
+    h = np.ascontiguousarray(hidden, np.int32)
+    return int(_lib.sc_param_count(in_dim, _ptr(h), len(h), num_classes))
+
+
+def make_sage_model(in_dim: int, hidden: Sequence[int], num_classes: int, seed: int,
+                    ctx: Optional[Context] = None) -> np.ndarray:  # nn.hpp:73-102 (float)
+    ctx = ctx or default_context()
+    h = np.ascontiguousarray(hidden, np.int32)
+    out = np.zeros(param_count(in_dim, hidden, num_classes), np.float32)
+    _check(_lib.sc_init_params(ctx.h, in_dim, _ptr(h), len(h), num_classes, seed, _ptr(out)), "make_sage_model")
+    return out
+
+
+@dataclass
+class TrainConfig:  # trainer.hpp:20-33
+    layers: int = 2
+    hidden: List[int] = field(default_factory=lambda: [32])
+    epochs: int = 100
+    learning_rate: float = 0.01
+    loss: str = "softmax_ce"
+    reweight: str = "dar"
+    use_dropedge: bool = False
+    dropedge_k: int = 10
+    drop_ratio: float = 0.5
+    seed: int = 0
+    precision: str = "f32"
+    workers: int = 1
+    # B200 knobs
+    deterministic: bool = True
+    gemm: str = "auto"  # "auto" (tcgen05 where supported) | "simt"
+
+    def resolved_hidden(self) -> List[int]:  # trainer.cpp:12-19
+        if self.layers == 0:
+            return []
+        if len(self.hidden) == 1:
+            return [self.hidden[0]] * self.layers
+        if len(self.hidden) != self.layers:
+            raise ValueError("hidden dims must match layer count (or be a single value)")
+        return list(self.hidden)
+
+    def validate(self):  # trainer.cpp:21-36
+        if self.layers < 0:
+            raise ValueError("layers must be >= 0")
+        if self.epochs < 0:
+            raise ValueError("epochs must be >= 0")
+        if not self.learning_rate > 0.0:
+            raise ValueError("learning rate must be > 0")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.layers > 0 and not self.hidden:
+            raise ValueError("hidden dims required for layers > 0")
+        if any(h < 1 for h in self.hidden):
+            raise ValueError("hidden dims must be positive")
+        if self.use_dropedge:
+            if self.dropedge_k < 1:
+                raise ValueError("dropedge_k must be >= 1")
+            if not 0.0 <= self.drop_ratio < 1.0:
+                raise ValueError("drop_ratio must lie in [0, 1)")
+        if self.precision != "f32":
+            raise ValueError("sagecut_cuda trains in f32 (the reference's Precision::f32)")
+        self.resolved_hidden()
+
+
+@dataclass
+class EpochMetrics:  # trainer.hpp:38-46
+    epoch: int
+    train_loss: float
+    train_metric: float = 0.0
+    val_metric: float = 0.0
+    test_metric: float = 0.0
+    grad_norm: float = 0.0
+    comm_floats: int = 0
+
+
+class CoFreeTrainer:
+    """The state of train_cofree_impl (trainer.hpp:202-313) on one rank."""
+
+    def __init__(self, g: Graph, part: VertexCutPartition, config: TrainConfig, rank: int = 0, world: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        config.validate()
+        self.g, self.part, self.config = g, part, config
+        self.hidden = np.ascontiguousarray(config.resolved_hidden(), np.int32)
+        c = _TrainConfigC(len(self.hidden), self.hidden.ctypes.data if len(self.hidden) else None,
+                          config.learning_rate, _LOSSES[config.loss], _SCHEMES[config.reweight],
+                          int(config.use_dropedge), config.dropedge_k, config.drop_ratio, config.seed,
+                          int(config.deterministic), 1 if config.gemm == "simt" else 0)
+        h = _vp()
+        _check(_lib.sc_trainer_create(g.ctx.h, g.h, part.h, C.byref(c), rank, world, C.byref(h)), "train_cofree")
+        self.h = h
+        n = _i64()
+        _check(_lib.sc_trainer_param_count(self.h, C.byref(n)))
+        self.param_count = n.value
+        self.rank, self.world = rank, world
+        if world > 1:
+            if nccl_id is None:
+                raise ValueError("world > 1 needs the rank-0 NCCL unique id")
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            _check(_lib.sc_trainer_init_comm(self.h, buf), "init_comm")
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(_lib.sc_nccl_unique_id(buf), "nccl_unique_id")
+        return bytes(buf)
+
+    def step(self, epoch: int):
+        loss, gn = _f64(), _f64()
+        _check(_lib.sc_trainer_step(self.h, epoch, C.byref(loss), C.byref(gn)), "step")
+        return loss.value, gn.value
+
+    def step_async(self, epoch: int):
+        _check(_lib.sc_trainer_step_async(self.h, epoch), "step")
+
+    def last(self):
+        loss, gn = _f64(), _f64()
+        _check(_lib.sc_trainer_last(self.h, C.byref(loss), C.byref(gn)), "step")
+        return loss.value, gn.value
+
+    def params(self) -> np.ndarray:
+        out = np.zeros(self.param_count, np.float32)
+        _check(_lib.sc_trainer_get_params(self.h, _ptr(out)))
+        return out
+
+    def set_params(self, theta):
+        t = np.ascontiguousarray(theta, np.float32)
+        if t.size != self.param_count:
+            raise ValueError("set_params: wrong parameter count")
+        _check(_lib.sc_trainer_set_params(self.h, _ptr(t)))
+
+    def grads(self) -> np.ndarray:
+        out = np.zeros(self.param_count, np.float32)
+        _check(_lib.sc_trainer_get_grads(self.h, _ptr(out)))
+        return out
+
+    def part_grads(self, i: int) -> np.ndarray:
+        out = np.zeros(self.param_count, np.float32)
+        _check(_lib.sc_trainer_get_part_grads(self.h, i, _ptr(out)))
+        return out
+
+    def part_logits(self, i: int) -> np.ndarray:
+        nl = self.part.part_sizes(i)[0]
+        out = np.zeros((nl, self.g.num_classes), np.float32)
+        _check(_lib.sc_trainer_get_part_logits(self.h, i, _ptr(out)))
+        return out
+
+    def part_loss(self, i: int) -> float:
+        x = _f64()
+        _check(_lib.sc_trainer_get_part_loss(self.h, i, C.byref(x)))
+        return x.value
+
+    def part_mask(self, i: int) -> int:
+        x = _i32()
+        _check(_lib.sc_trainer_get_part_mask(self.h, i, C.byref(x)))
+        return x.value
+
+    def evaluate(self):
+        a, b, c = _f64(), _f64(), _f64()
+        _check(_lib.sc_trainer_evaluate(self.h, C.byref(a), C.byref(b), C.byref(c)), "evaluate")
+        return a.value, b.value, c.value
+
+    def profile(self, enable: bool = True):
+        _check(_lib.sc_trainer_profile(self.h, int(enable)))
+
+    def kernel_times(self):
+        cnt = _i32()
+        _check(_lib.sc_trainer_kernel_times(self.h, None, None, None, 0, C.byref(cnt)))
+        k = cnt.value
+        names = (C.c_char_p * k)()
+        ms = (_f64 * k)()
+        by = (_f64 * k)()
+        _check(_lib.sc_trainer_kernel_times(self.h, names, ms, by, k, C.byref(cnt)))
+        return {names[i].decode(): (ms[i], by[i]) for i in range(k)}
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.sc_trainer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+@dataclass
+class TrainResult:  # trainer.hpp:71-75
+    model: np.ndarray
+    metrics: List[EpochMetrics]
+
+
+def train_cofree(g: Graph, part: VertexCutPartition, config: TrainConfig, evaluate: bool = True) -> TrainResult:
+    """train_cofree (trainer.cpp:119 / trainer.hpp:202-313): per-epoch step, Adam,
+    and (like the reference) a full-graph evaluation after every epoch."""
+    t = CoFreeTrainer(g, part, config)
+    metrics = []
+    for epoch in range(config.epochs):
+        loss, gn = t.step(epoch)
+        tr, va, te = t.evaluate() if evaluate else (0.0, 0.0, 0.0)
+        metrics.append(EpochMetrics(epoch, loss, tr, va, te, gn, part.num_parts * t.param_count))
+    return TrainResult(t.params(), metrics)

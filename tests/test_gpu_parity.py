@@ -1,0 +1,246 @@
+"""Parity of the CUDA path (libsagecut_cuda.so through its C ABI) with the
+oracle restatement and the reference's golden vectors.
+
+Bar (north_star): partition assignments, duplication counts, reweighting
+factors and DropEdge masks bit-exact; logits, loss and gradients within 1e-4
+relative in fp32 over 5 training steps. "Relative" here is
+    ||x_gpu - x_ref||_2 / ||x_ref||_2 <= 1e-4   (logits, gradients, parameters)
+    |loss_gpu - loss_ref| / |loss_ref|  <= 1e-5
+with the oracle in the reference's f32 mode as x_ref.
+"""
+import numpy as np
+import pytest
+
+from cpu_libs import oracle
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def sc():
+    from paper_2308_03209_b200 import sagecut
+    return sagecut
+
+
+@pytest.fixture(scope="module")
+def O():
+    return oracle()
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def gpu_graph(sc, og, d=None):
+    g, _ = sc.build_graph(og.n, og.edges())
+    if d:
+        tr, va, te = og.masks()
+        g.set_data(og.features(d).astype(np.float32), og.labels(), int(og.labels().max()) + 1, tr, va, te)
+    return g
+
+
+def check_partition(sc, g, gp, op, full=True):
+    np.testing.assert_array_equal(gp.edge_assignment, op.assignment())
+    st, ost = sc.replication_stats(gp, g), op.stats()
+    np.testing.assert_array_equal(st.per_node_rf, ost["per_node_rf"])
+    assert (st.rf, st.edge_balance, st.node_balance, st.duplicated_nodes) == \
+        (ost["rf"], ost["edge_balance"], ost["node_balance"], ost["duplicated_nodes"])
+    for scheme in ("dar", "vanilla_inv", "none"):
+        gw = sc.compute_weights(scheme, g, gp).per_part
+        ow = op.weights(scheme)
+        for a, b in zip(gw, ow):
+            np.testing.assert_array_equal(a, b)
+    if full:
+        for i in range(gp.num_parts):
+            a, b = gp.part(i), op.part(i)
+            np.testing.assert_array_equal(a.nodes, b.nodes)
+            np.testing.assert_array_equal(a.edges, b.edges)
+            np.testing.assert_array_equal(a.edge_global_ids, b.edge_gids)
+            np.testing.assert_array_equal(a.local_degrees, b.local_deg)
+            np.testing.assert_array_equal(a.adj_offsets, b.offsets)
+            np.testing.assert_array_equal(a.adj_neighbors, b.nbrs)
+            np.testing.assert_array_equal(a.adj_edge_ids, b.eids)
+            np.testing.assert_array_equal(a.global_to_local, b.g2l)
+
+
+# ---------------------------------------------------------------- graph ingest
+def test_build_graph_matches_reference(sc, O, golden):
+    k = golden("karate")
+    g, rep = sc.build_graph(int(k["n"]), k["edges"])
+    np.testing.assert_array_equal(g.edges(), k["edges"])
+    off, nb, ei, dg = g.csr()
+    np.testing.assert_array_equal(off, k["offsets"])
+    np.testing.assert_array_equal(nb, k["nbrs"])
+    np.testing.assert_array_equal(ei, k["eids"])
+    np.testing.assert_array_equal(dg, k["degrees"])
+    # raw edges with self-loops, reversed pairs and duplicates (graph.cpp:14-30)
+    rng = np.random.default_rng(5)
+    raw = rng.integers(0, 300, size=(5000, 2)).astype(np.int32)
+    raw[::17, 1] = raw[::17, 0]
+    og = O.graph_build(310, raw)
+    g2, rep2 = sc.build_graph(310, raw)
+    np.testing.assert_array_equal(g2.edges(), og.edges())
+    for a, b in zip(g2.csr(), og.csr()):
+        np.testing.assert_array_equal(a, b)
+    assert rep2.dropped_self_loops == int((raw[:, 0] == raw[:, 1]).sum())
+    with pytest.raises(ValueError, match="out of range"):
+        sc.build_graph(10, np.array([[0, 10]], np.int32))
+    g0, _ = sc.build_graph(5, np.zeros((0, 2), np.int32))  # empty graph
+    assert g0.num_edges() == 0
+
+
+# ---------------------------------------------------------------- vertex cut
+@pytest.mark.parametrize("algo", ["random", "dbh"])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8, 16])
+def test_partitions_bit_exact(sc, O, algo, p):
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    g = gpu_graph(sc, og)
+    for seed in (0, 3):
+        fn = sc.partition_random if algo == "random" else sc.partition_dbh
+        check_partition(sc, g, fn(g, p, seed), og.partition(algo, p, seed))
+
+
+def test_partition_goldens_and_isolated_nodes(sc, O, golden):
+    k = golden("karate")
+    g, _ = sc.build_graph(int(k["n"]), k["edges"])
+    for p in (1, 2, 4, 8):
+        gp = sc.partition_random(g, p, 0)
+        np.testing.assert_array_equal(gp.edge_assignment, k[f"random_p{p}_assign"])
+        np.testing.assert_array_equal(sc.replication_stats(gp, g).per_node_rf, k[f"random_p{p}_per_node_rf"])
+    # isolated nodes go round-robin (partition.cpp:45-50); some parts empty
+    raw = np.array([[0, 1], [1, 2], [5, 6]], np.int32)
+    og = O.graph_build(12, raw)
+    g2, _ = sc.build_graph(12, raw)
+    for p in (2, 3, 7):
+        a = np.arange(3, dtype=np.int32) % p
+        check_partition(sc, g2, sc.build_vertex_cut(g2, p, a), og.build_vertex_cut(p, a))
+    with pytest.raises(ValueError, match="invalid part"):
+        sc.build_vertex_cut(g2, 2, np.array([0, 1, 2], np.int32))
+    with pytest.raises(ValueError, match="num_parts"):
+        sc.partition_random(g2, 0, 1)
+
+
+# ---------------------------------------------------------------- DropEdge masks
+@pytest.mark.parametrize("m", [0, 1, 2, 7, 13, 100, 1000, 100003])
+def test_masks_bit_exact(sc, O, m):
+    for ratio in (0.0, 0.1, 0.5, 0.9):
+        for seed in (0, 3, 12345):
+            a = sc.precompute_masks(m, 4, ratio, seed).masks
+            b = O.precompute_masks(m, 4, ratio, seed)
+            np.testing.assert_array_equal(a, b)
+
+
+def test_masks_golden_and_errors(sc, golden):
+    s = golden("sbm200")
+    np.testing.assert_array_equal(sc.precompute_masks(100, 10, 0.5, 3).masks, s["masks_100_10_05_3"])
+    with pytest.raises(ValueError, match="at least one mask"):
+        sc.precompute_masks(10, 0, 0.5, 1)
+    with pytest.raises(ValueError, match="ratio"):
+        sc.precompute_masks(10, 3, 1.0, 1)
+
+
+def test_masks_large_partition(sc, O):
+    """A products-sized partition edge count (7.75M): keep count exact and equal to the oracle."""
+    m = 7_748_473
+    a = sc.precompute_masks(m, 2, 0.5, sc.substream(0, "dropedge", 0)).masks
+    b = O.precompute_masks(m, 2, 0.5, O.substream(0, "dropedge", 0))
+    np.testing.assert_array_equal(a, b)
+    assert int(a[0].sum()) == int(np.ceil(0.5 * m))
+
+
+def test_init_params(sc, golden):
+    s = golden("sbm200")
+    np.testing.assert_array_equal(sc.make_sage_model(8, [16, 16], 4, 1), s["init_8_16_16_4_seed1_f32"].astype(np.float32))
+
+
+# ---------------------------------------------------------------- training step
+def run_traj(sc, O, og, algo, p, pseed, d, steps=5, **cfg):
+    g = gpu_graph(sc, og, d)
+    gp = (sc.partition_random if algo == "random" else sc.partition_dbh)(g, p, pseed)
+    op = og.partition(algo, p, pseed)
+    C = g.num_classes
+    ocfg = dict(cfg)
+    tcfg = sc.TrainConfig(layers=len(cfg["hidden"]), hidden=cfg["hidden"], learning_rate=cfg.get("lr", 0.01),
+                          loss=cfg.get("loss", "softmax_ce"), reweight=cfg.get("reweight", "dar"),
+                          use_dropedge=cfg.get("dropedge", False), dropedge_k=cfg.get("k", 10),
+                          drop_ratio=cfg.get("ratio", 0.5), seed=cfg.get("seed", 0),
+                          gemm=cfg.get("gemm", "auto"))
+    for key in ("gemm",):
+        ocfg.pop(key, None)
+    t = sc.CoFreeTrainer(g, gp, tcfg)
+    to = op.trainer(f32=True, **ocfg)
+    np.testing.assert_array_equal(t.params(), to.params().astype(np.float32))
+    worst = {}
+    for e in range(steps):
+        loss, gn = t.step(e)
+        ol, ogn = to.step(e)
+        worst["loss"] = max(worst.get("loss", 0), abs(loss - ol) / abs(ol))
+        worst["gnorm"] = max(worst.get("gnorm", 0), abs(gn - ogn) / abs(ogn))
+        assert [t.part_mask(i) for i in range(p)] == [to.part_mask(i) for i in range(p)]
+        lg = np.concatenate([t.part_logits(i).ravel() for i in range(p)])
+        olg = np.concatenate([to.part_logits(i, C).ravel() for i in range(p)])
+        worst["logits"] = max(worst.get("logits", 0), rel(lg, olg))
+        worst["grads"] = max(worst.get("grads", 0), rel(t.grads(), to.gathered()))
+        worst["params"] = max(worst.get("params", 0), rel(t.params(), to.params()))
+        for i in range(p):
+            worst["part_loss"] = max(worst.get("part_loss", 0),
+                                     abs(t.part_loss(i) - to.part_loss(i)) / max(abs(to.part_loss(i)), 1e-30))
+    return worst, t, to
+
+
+def assert_within(worst):
+    assert worst["loss"] <= 1e-5, worst
+    assert worst["gnorm"] <= REL, worst
+    assert worst["logits"] <= REL, worst
+    assert worst["grads"] <= REL, worst
+    assert worst["params"] <= REL, worst
+
+
+@pytest.mark.parametrize("gemm", ["simt", "auto"])
+@pytest.mark.parametrize("de", [False, True])
+def test_sbm200_trajectory(sc, O, gemm, de):
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    worst, t, to = run_traj(sc, O, og, "random", 8, 3, 8, hidden=[16, 16], lr=0.01, dropedge=de, seed=1, gemm=gemm)
+    print(worst)
+    assert_within(worst)
+    np.testing.assert_allclose(t.evaluate(), to.eval(), atol=0.02)
+
+
+def test_sbm200_bce_vanilla_dbh(sc, O):
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    assert_within(run_traj(sc, O, og, "random", 8, 3, 8, hidden=[16, 16], loss="bce", seed=1)[0])
+    assert_within(run_traj(sc, O, og, "random", 8, 3, 8, hidden=[16, 16], reweight="vanilla_inv", seed=1)[0])
+    assert_within(run_traj(sc, O, og, "dbh", 4, 3, 8, hidden=[16, 16, 16], lr=0.02, dropedge=True, k=4, ratio=0.3,
+                           seed=5)[0])
+
+
+def test_edge_cases(sc, O):
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    # zero-layer model (pure feature classifier), p = 1, K = 1, ratio 0
+    assert_within(run_traj(sc, O, og, "random", 1, 3, 8, hidden=[], seed=2)[0])
+    assert_within(run_traj(sc, O, og, "random", 16, 1, 8, hidden=[12], dropedge=True, k=1, ratio=0.0, seed=2)[0])
+    # odd widths exercise the scalar aggregation path and GEMM tails
+    assert_within(run_traj(sc, O, og, "random", 3, 1, 8, hidden=[7, 5], dropedge=True, k=3, ratio=0.7, seed=4)[0])
+
+
+def test_config0_er10k(sc, O, golden):
+    """configs[0]: ER 10k nodes / 200k edges, 64 feats, 2 x 32, p = 4, DropEdge."""
+    z = golden("er10k")
+    og = O.graph_sbm(10000, 4, 0.004, 0.004, 64, 1.0, 0)
+    worst, t, to = run_traj(sc, O, og, "random", 4, 0, 64, hidden=[32, 32], lr=0.01, dropedge=True, seed=0)
+    print(worst)
+    assert_within(worst)
+    # and against the reference's own trajectory (golden)
+    np.testing.assert_allclose(t.params(), z["traj_params"][-1], rtol=0, atol=1e-4 * np.abs(z["traj_params"][-1]).max())
+
+
+def test_trainer_errors(sc, O):
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    g = gpu_graph(sc, og)  # no features attached
+    gp = sc.partition_random(g, 2, 0)
+    with pytest.raises(ValueError, match="features"):
+        sc.CoFreeTrainer(g, gp, sc.TrainConfig(layers=1, hidden=[4]))
