@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark: one CoFree-GNN training epoch (all p vertex-cut partitions:
+forward, weighted loss, backward, gradient exchange, Adam) on B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config products|reddit|er10k]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Metric (BASELINE.json): epoch time and aggregated edges/s,
+    edges/s = L * sum_i kept_CSR_entries_i / epoch_time
+(forward directed edge traversals; with DropEdge only kept entries count),
+plus the aggregation (SpMM) kernel's fraction of the measured HBM roofline.
+
+Scaling: the partition count p is FIXED (8 for the products/reddit shapes)
+and the p partitions are spread over the N GPUs (partition i on rank i % N),
+so total work is constant as N grows ("strong"). The only cross-GPU traffic is
+the per-epoch gradient all-reduce (NCCL) inside libsagecut_cuda.so.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref = the unmodified reference sources built behind the Eigen shim;
+falls back to the oracle port) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # configs[2]: the headline (products-shaped, 3-layer GraphSAGE 256, DropEdge p=0.5)
+    "products": dict(workload="ogbn-products-shaped synthetic (BASELINE configs[2])", nodes=2_449_029,
+                     pairs=62_000_000, feats=100, classes=47, layers=3, hidden=256, parts=8, dropedge=True, k=10,
+                     ratio=0.5, lr=3e-3),
+    # configs[1]: Reddit-shaped; 114.6M directed = 57.3M undirected edges; SAGE (no GCN in the reference)
+    "reddit": dict(workload="Reddit-shaped synthetic (BASELINE configs[1])", nodes=232_965, pairs=57_400_000,
+                   feats=602, classes=41, layers=2, hidden=256, parts=8, dropedge=False, k=10, ratio=0.5, lr=1e-2),
+    # configs[0]: ER 10k / 200k, 64 feats, 2 layers (reference default hidden 32), p = 4
+    "er10k": dict(workload="Erdos-Renyi 10k/200k (BASELINE configs[0])", nodes=10_000, pairs=200_000, feats=64,
+                  classes=4, layers=2, hidden=32, parts=4, dropedge=False, k=10, ratio=0.5, lr=1e-2),
+}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------- data
+def synth_host(cfg, seed=0, scale=1.0):
+    """O(E) seeded synthetic graph of the config's shape (never the reference's O(n^2) generators).
+    Uniform random endpoint pairs (canonicalised/deduped by build_graph), labels uniform, features
+    one-hot(label) + N(0, 1) (synth.cpp:91-97 convention), 60/20/20 split."""
+    rng = np.random.default_rng(seed)
+    n = max(int(cfg["nodes"] * scale), 16)
+    m = max(int(cfg["pairs"] * scale), 16)
+    uv = rng.integers(0, n, size=(m, 2), dtype=np.int32)
+    labels = rng.integers(0, cfg["classes"], size=n, dtype=np.int32)
+    feats = rng.standard_normal((n, cfg["feats"]), dtype=np.float32)
+    feats[np.arange(n), labels % cfg["feats"]] += 1.0
+    perm = rng.permutation(n)
+    tr = np.zeros(n, np.uint8)
+    va = np.zeros(n, np.uint8)
+    te = np.zeros(n, np.uint8)
+    n_tr, n_va = n * 6 // 10, n * 2 // 10
+    tr[perm[:n_tr]] = 1
+    va[perm[n_tr:n_tr + n_va]] = 1
+    te[perm[n_tr + n_va:]] = 1
+    return n, uv, feats, labels, tr, va, te
+
+
+def kept_entries(sizes_m, cfg):
+    """sum_i CSR entries kept per epoch: every DropEdge mask keeps exactly ceil((1-r) m_i) edges."""
+    if cfg["dropedge"]:
+        return sum(2 * math.ceil((1.0 - cfg["ratio"]) * m) for m in sizes_m)
+    return sum(2 * m for m in sizes_m)
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index=0):
+        self.samples, self.proc, self.gpu = [], None, gpu_index
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(name):
+    """Per-launch DRAM bytes of the kernel from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- CPU reference
+def cpu_reference_sample(cfg, steps, warmup, scale=None):
+    """The reference's own training epoch (train_cofree_impl minus the per-epoch eval) on a bounded
+    sample of the same workload shape, all host threads (workers = min(p, nproc))."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cpu_libs
+
+    kind = "reference"
+    try:
+        lib = cpu_libs.reference()
+    except (FileNotFoundError, OSError):
+        lib, kind = cpu_libs.oracle(), "port"
+    if scale is None:
+        scale = min(1.0, 50_000 / cfg["nodes"])
+    n, uv, feats, labels, tr, va, te = synth_host(cfg, seed=0, scale=scale)
+    g = lib.graph_build(n, uv)
+    g.set_data(feats, labels, cfg["classes"], tr, va, te)
+    part = g.partition("random", cfg["parts"], 0)
+    cores = min(cfg["parts"], os.cpu_count() or 1)
+    t = part.trainer([cfg["hidden"]] * cfg["layers"], lr=cfg["lr"], dropedge=cfg["dropedge"], k=cfg["k"],
+                     ratio=cfg["ratio"], seed=1, f32=True, workers=cores)
+    kept = kept_entries([part.sizes(i)[1] for i in range(cfg["parts"])], cfg)
+    for e in range(warmup):
+        t.step(e)
+    t0 = time.perf_counter()
+    for e in range(steps):
+        t.step(warmup + e)
+    sec = (time.perf_counter() - t0) / max(steps, 1)
+    value = cfg["layers"] * kept / sec
+    sample = (f"{n} nodes / {g.m} edges (scale {scale:.4f} of the config, same avg degree, feats, layers, hidden, "
+              f"p, DropEdge), {steps} epoch(s) after {warmup} warm-up, no per-epoch eval")
+    blas = None
+    if kind == "reference":
+        try:
+            blas = bool(lib.lib.ref_blas_active())
+        except Exception:
+            pass
+    return dict(value=value, unit="edges/s", cores=cores, kind=kind, sample=sample, epoch_s=sec,
+                gemm_backend=("OpenBLAS sgemm, 1 thread/worker" if blas else "shim loop GEMM") if kind == "reference"
+                else "oracle loops")
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    res = cpu_reference_sample(cfg, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": "aggregated_edges_per_s", "value": res["value"], "unit": "edges/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["epoch_s"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"] + " [bounded CPU sample]", "partitions": cfg["parts"],
+                       "layers": cfg["layers"], "hidden": cfg["hidden"], "feats": cfg["feats"],
+                       "classes": cfg["classes"], "dropedge": cfg["dropedge"]},
+            "cpu_baseline": {"value": res["value"], "unit": "edges/s", "cores": res["cores"], "kind": res["kind"],
+                             "sample": res["sample"], "gemm": res["gemm_backend"]},
+            "e2e": {"value": res["value"], "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_gpu_arm(args, cfg):
+    rank, world, local = dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    from paper_2308_03209_b200 import sagecut as sc
+
+    ctx = sc.Context(local)
+    t_setup = time.perf_counter()
+    # identical seeded synthetic inputs on every rank (generated on the host once per rank)
+    n, uv, feats, labels, tr, va, te = synth_host(cfg, seed=0)
+    g, rep = sc.build_graph(n, uv, ctx)
+    g.set_data(feats, labels, cfg["classes"], tr, va, te)
+    part = sc.partition_random(g, cfg["parts"], 0)
+    sizes_m = [part.part_sizes(i)[1] for i in range(cfg["parts"])]
+    kept = kept_entries(sizes_m, cfg)
+    nccl_id = None
+    if world > 1:
+        obj = [sc.CoFreeTrainer.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    tcfg = sc.TrainConfig(layers=cfg["layers"], hidden=[cfg["hidden"]], learning_rate=cfg["lr"],
+                          use_dropedge=cfg["dropedge"], dropedge_k=cfg["k"], drop_ratio=cfg["ratio"], seed=1,
+                          gemm=args.gemm)
+    trainer = sc.CoFreeTrainer(g, part, tcfg, rank=rank, world=world, nccl_id=nccl_id)
+    setup_s = time.perf_counter() - t_setup
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    epoch = 0
+    for _ in range(args.warmup):
+        trainer.step(epoch)
+        epoch += 1
+    # ---- timed region: K epochs, device events on the library's stream
+    trainer.profile(True)
+    barrier()
+    ctx.sync()
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clocks:
+        ctx.timer_start()
+        losses = []
+        prof = {}
+        for _ in range(args.steps):
+            losses.append(trainer.step(epoch)[0])
+            for k, (ms, by) in trainer.kernel_times().items():
+                a = prof.setdefault(k, [0.0, 0.0])
+                a[0] += ms
+                a[1] += by
+            epoch += 1
+        ms = ctx.timer_stop()
+    launches = ctx.launch_count() - launches0
+    trainer.profile(False)
+    barrier()
+    ms_step = max_over_ranks(ms / args.steps)
+    value = cfg["layers"] * kept / (ms_step / 1e3)
+
+    # ---- e2e: the public API with host buffers: per step H2D of the feature matrix from pinned
+    # host memory (the step's input), the epoch, and the D2H of loss / grad-norm.
+    pinned = torch.from_numpy(feats).pin_memory()
+    barrier()
+    ctx.sync()
+    ctx.timer_start()
+    for _ in range(args.steps):
+        g.set_features(None, host_ptr=pinned.data_ptr())
+        trainer.step(epoch)
+        epoch += 1
+    e2e_ms = max_over_ranks(ctx.timer_stop() / args.steps)
+    e2e_value = cfg["layers"] * kept / (e2e_ms / 1e3)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = measured_peaks()
+    spmm_ms = sum(prof.get(k, [0, 0])[0] for k in ("spmm_fwd", "spmm_bwd"))
+    spmm_bytes = sum(prof.get(k, [0, 0])[1] for k in ("spmm_fwd", "spmm_bwd"))
+    launches_spmm = 2 * cfg["layers"] * len(range(rank, cfg["parts"], world)) * args.steps
+    achieved = spmm_bytes / (spmm_ms / 1e3) / 1e9 if spmm_ms > 0 else 0.0
+    total_prof = sum(v[0] for v in prof.values())
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "share": v[0] / total_prof if total_prof else None,
+                   "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 and v[1] > 0 else None}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    dominant = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(cfg, steps=1, warmup=0)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the baseline must not sink the GPU line
+            cpu = {"value": None, "unit": "edges/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
+    line = {
+        "metric": "aggregated_edges_per_s", "value": value, "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "nodes": g.num_nodes, "edges": g.num_edges(),
+                   "feats": cfg["feats"], "classes": cfg["classes"], "layers": cfg["layers"],
+                   "hidden": cfg["hidden"], "partitions": cfg["parts"], "partitioner": "random vertex cut",
+                   "dropedge": f"p={cfg['ratio']} K={cfg['k']}" if cfg["dropedge"] else None,
+                   "kept_csr_entries_per_epoch": kept, "parallelism": f"dp{world} over {cfg['parts']} fixed partitions",
+                   "gemm": args.gemm, "l2": "inputs > L2 (each activation matrix is n_i x 256 fp32 = 2.5 GB)"},
+        "epoch_ms": ms_step,
+        "roofline": {"kernel": "spmm (masked mean aggregation fwd + transposed bwd)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None,
+                     "traffic": ncu_traffic("spmm"), "launches": launches_spmm,
+                     "bytes_per_launch": spmm_bytes / max(launches_spmm, 1),
+                     "share_of_step": spmm_ms / total_prof if total_prof else None},
+        "dominant_kernel": dominant,
+        "kernels": kernels,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(feats.nbytes), "d2h_bytes_per_step": 16},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "setup_s": setup_s,
+        "loss_first_last": [losses[0], losses[-1]] if losses else None,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
+    ap.add_argument("--gemm", default="auto", choices=["auto", "simt"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_gpu_arm(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -53,6 +53,10 @@ sc_status sc_ctx_destroy(sc_ctx* ctx);
 sc_status sc_ctx_sync(sc_ctx* ctx);
 /* Kernel launches issued by this library on ctx since creation (counter). */
 int64_t sc_ctx_launch_count(sc_ctx* ctx);
+/* CUDA-event timer on ctx's stream: start records an event, stop records a
+ * second one, synchronizes, and returns the elapsed device time. */
+sc_status sc_ctx_timer_start(sc_ctx* ctx);
+sc_status sc_ctx_timer_stop(sc_ctx* ctx, double* ms);
 
 /* ---- graph (proj/include/sagecut/graph.hpp:53-96, proj/src/graph.cpp) ---- */
 /* build_graph (graph.cpp:8-64): drop self-loops, canonicalise u<v, sort,

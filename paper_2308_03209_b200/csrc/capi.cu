@@ -75,6 +75,10 @@ sc_status sc_ctx_destroy(sc_ctx* ctx) {
         if (!ctx) return;
         set_device(ctx);
         cudaStreamSynchronize(ctx->stream);
+        if (ctx->t0) {
+            cudaEventDestroy(ctx->t0);
+            cudaEventDestroy(ctx->t1);
+        }
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -83,6 +87,27 @@ sc_status sc_ctx_sync(sc_ctx* ctx) {
     return guard([&] { SC_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
 int64_t sc_ctx_launch_count(sc_ctx*) { return sc::g_launches; }
+sc_status sc_ctx_timer_start(sc_ctx* ctx) {
+    return guard([&] {
+        set_device(ctx);
+        if (!ctx->t0) {
+            SC_CUDA(cudaEventCreate(&ctx->t0));
+            SC_CUDA(cudaEventCreate(&ctx->t1));
+        }
+        SC_CUDA(cudaEventRecord(ctx->t0, ctx->stream));
+    });
+}
+sc_status sc_ctx_timer_stop(sc_ctx* ctx, double* ms) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && ctx->t0, "sc_ctx_timer_stop: timer not started");
+        set_device(ctx);
+        SC_CUDA(cudaEventRecord(ctx->t1, ctx->stream));
+        SC_CUDA(cudaEventSynchronize(ctx->t1));
+        float f = 0.f;
+        SC_CUDA(cudaEventElapsedTime(&f, ctx->t0, ctx->t1));
+        *ms = f;
+    });
+}
 
 // ---- graph ----
 sc_status sc_build_graph_dev(sc_ctx* ctx, int32_t n, const int32_t* raw_dev, int64_t m_raw, sc_graph** out,

@@ -76,6 +76,7 @@ struct sc_ctx {
     sc::DevBuf<unsigned char> cub_tmp;  // CUB temp storage (grow-only)
     sc::DevBuf<unsigned char> scratch;  // misc scratch (grow-only)
     int64_t launches = 0;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
     void* temp(size_t bytes) {
         cub_tmp.ensure(bytes < 256 ? 256 : bytes);
         return cub_tmp.get();

@@ -231,7 +231,18 @@ struct Rows {
     const int32_t* nbrs;
     const uint32_t* bits;
     const int32_t* nodes;  // local -> global row (features / labels); null = identity
+    int64_t nnz;           // CSR slots
+    int64_t kept;          // CSR slots kept by the selected DropEdge mask
 };
+
+// Algorithmic HBM bytes of one aggregation launch: offsets,
+// neighbour ids, mask bits, inv_deg (fwd) or ReLU-mask rows (bwd), one gathered
+// fp32 row per kept slot, and the output rows.
+double spmm_bytes(const Rows& R, int H, bool bwd) {
+    double b = 8.0 * (R.n + 1) + 4.0 * R.nnz + (R.bits ? (R.nnz + 7) / 8 : 0) + 4.0 * H * R.kept + 4.0 * H * R.n;
+    b += bwd ? 4.0 * H * R.n : 4.0 * R.n;
+    return b;
+}
 
 // sage_forward (nn.hpp:192-242). Writes logits; keeps the cache in t's buffers.
 void forward(sc_trainer* t, const Rows& R, float* logits) {
@@ -251,7 +262,7 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
                  kEpiRelu, nullptr);
         P.end(s);
         // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
-        P.begin("spmm_fwd", 0.0, s);
+        P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
         spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->inv.get(), t->MSG[l].get(), t->MEAN[l].get(), s);
         P.end(s);
         // h' = mean U_L^T + h U_R^T   (nn.hpp:233-234)
@@ -304,7 +315,7 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
                  t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get());
         P.end(s);
         // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
-        P.begin("spmm_bwd", 0.0, s);
+        P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
         spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s);
         P.end(s);
         // dW = dz^T h_in   (:289)
@@ -337,7 +348,9 @@ void run_partition(sc_trainer* t, int i, int epoch) {
         st.chosen = static_cast<int>(rng.next_below(uint64_t(t->K)));
         bits = st.bits.get() + int64_t(st.chosen) * st.words;
     }
-    const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get()};
+    const int64_t kept =
+        bits ? 2 * static_cast<int64_t>(std::ceil((1.0 - t->ratio) * static_cast<double>(pd.m_local))) : st.nnz;
+    const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept};
     forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
     if (t->loss == 0)
@@ -405,7 +418,7 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
     sc_graph* g = t->g;
     ensure_rows(t, g->n);
     if (t->eval_logits.size() < size_t(g->n) * t->C) t->eval_logits.alloc(size_t(g->n) * t->C);
-    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr};
+    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m};
     const bool was = t->prof.enabled;
     t->prof.enabled = false;
     forward(t, R, t->eval_logits.get());

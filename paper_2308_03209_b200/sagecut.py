@@ -58,6 +58,8 @@ _sig("sc_ctx_create", [C.c_int, _pp])
 _sig("sc_ctx_destroy", [_vp])
 _sig("sc_ctx_sync", [_vp])
 _sig("sc_ctx_launch_count", [_vp], _i64)
+_sig("sc_ctx_timer_start", [_vp])
+_sig("sc_ctx_timer_stop", [_vp, C.POINTER(_f64)])
 _sig("sc_build_graph", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i64)])
 _sig("sc_build_graph_dev", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i64)])
 _sig("sc_graph_set_data", [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp])
@@ -142,6 +144,14 @@ class Context:
     def launch_count(self) -> int:
         return int(_lib.sc_ctx_launch_count(self.h))
 
+    def timer_start(self):
+        _check(_lib.sc_ctx_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        ms = _f64()
+        _check(_lib.sc_ctx_timer_stop(self.h, C.byref(ms)))
+        return ms.value
+
     def close(self):
         if getattr(self, "h", None):
             _lib.sc_ctx_destroy(self.h)
@@ -203,9 +213,13 @@ class Graph:
                                       _ptr(te)), "set_data")
         self.dim, self.num_classes = f.shape[1], int(num_classes)
 
-    def set_features(self, features, device_ptr: Optional[int] = None):
+    def set_features(self, features, device_ptr: Optional[int] = None, host_ptr: Optional[int] = None):
+        """Replace the n x d feature matrix (same shape) from a numpy array, a host
+        pointer (pinned memory -> async DMA), or a device pointer."""
         if device_ptr is not None:
             _check(_lib.sc_graph_set_features(self.h, _vp(device_ptr), 1))
+        elif host_ptr is not None:
+            _check(_lib.sc_graph_set_features(self.h, _vp(host_ptr), 0))
         else:
             f = np.ascontiguousarray(features, np.float32)
             _check(_lib.sc_graph_set_features(self.h, _ptr(f), 0))

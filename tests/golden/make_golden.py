@@ -29,6 +29,9 @@ import sys
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+# Goldens use the shim's plain loop GEMM (k-ascending sums, no BLAS blocking) so
+# the oracle restatement can be pinned to them at ~1 ulp.
+os.environ["SAGECUT_REF_NO_BLAS"] = "1"
 sys.path.insert(0, os.path.dirname(HERE))
 from cpu_libs import reference  # noqa: E402
 
