@@ -67,7 +67,7 @@ sc_status sc_build_graph(sc_ctx* ctx, int32_t num_nodes, const int32_t* raw_uv, 
 sc_status sc_build_graph_dev(sc_ctx* ctx, int32_t num_nodes, const int32_t* raw_uv_dev, int64_t m_raw,
                              sc_graph** out, int64_t* dropped_self_loops, int64_t* merged_duplicates);
 /* Attach features (fp32 n x d), class ids, and the train/val/test masks
- * (Graph::features/labels/num_classes/*_mask). Host buffers. */
+ * (Graph::features, labels, num_classes, train/val/test_mask). Host buffers. */
 sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, const int32_t* labels,
                             int32_t num_classes, const uint8_t* train, const uint8_t* val, const uint8_t* test);
 /* Replace only the features (e.g. a new batch of the same graph). Host or device source. */
@@ -161,6 +161,17 @@ sc_status sc_trainer_profile(sc_trainer* t, int32_t enable);
 sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms, double* bytes, int32_t cap,
                                   int32_t* count);
 sc_status sc_trainer_destroy(sc_trainer* t);
+
+/* ---- diagnostics (kernel-level parity tests) ------------------------------- */
+/* C[M x N] = A1[rows1] B1' (+ A2 B2') with epilogue epi (0 none, 1 relu,
+ * 2 row-scale by `scale`), through the tcgen05 bf16x3 kernel (mode 0) or the
+ * fp32 SIMT kernel (mode 1). B' = B^T when b_nn == 0 (B is N x K), B when
+ * b_nn == 1 (B is K x N). A1 has a1_rows rows of lda1 floats; rows1 (length
+ * M, optional) gathers them. All buffers are host memory. */
+sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t K1, const float* A1,
+                        int64_t a1_rows, int64_t lda1, const int32_t* rows1, const float* B1, int64_t ldb1,
+                        int32_t b1_nn, int32_t K2, const float* A2, int64_t lda2, const float* B2, int64_t ldb2,
+                        int32_t b2_nn, int32_t epi, const float* scale, float* C);
 
 #ifdef __cplusplus
 }

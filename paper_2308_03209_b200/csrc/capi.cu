@@ -518,6 +518,47 @@ sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms,
         *count = k;
     });
 }
+sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t K1, const float* A1,
+                        int64_t a1_rows, int64_t lda1, const int32_t* rows1, const float* B1, int64_t ldb1,
+                        int32_t b1_nn, int32_t K2, const float* A2, int64_t lda2, const float* B2, int64_t ldb2,
+                        int32_t b2_nn, int32_t epi, const float* scale, float* C) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && A1 && B1 && C && M >= 0 && N >= 1 && K1 >= 1, "sc_debug_gemm: bad arguments");
+        set_device(ctx);
+        cudaStream_t s = ctx->stream;
+        auto up = [&](const void* h, size_t bytes) {
+            DevBuf<unsigned char> d(std::max<size_t>(bytes, 16));
+            if (bytes) SC_CUDA(cudaMemcpyAsync(d.get(), h, bytes, cudaMemcpyHostToDevice, s));
+            return d;
+        };
+        auto dA1 = up(A1, sizeof(float) * a1_rows * lda1);
+        auto dB1 = up(B1, sizeof(float) * (b1_nn ? int64_t(K1) * ldb1 : int64_t(N) * ldb1));
+        DevBuf<unsigned char> dR1, dA2, dB2, dS;
+        if (rows1) dR1 = up(rows1, sizeof(int32_t) * M);
+        if (K2 > 0) {
+            dA2 = up(A2, sizeof(float) * M * lda2);
+            dB2 = up(B2, sizeof(float) * (b2_nn ? int64_t(K2) * ldb2 : int64_t(N) * ldb2));
+        }
+        if (epi == kEpiRowScale) dS = up(scale, sizeof(float) * M);
+        DevBuf<float> dC(std::max<int64_t>(M * N, 1));
+        const MatA a1{reinterpret_cast<const float*>(dA1.get()), lda1,
+                      rows1 ? reinterpret_cast<const int32_t*>(dR1.get()) : nullptr, K1};
+        const MatB b1{reinterpret_cast<const float*>(dB1.get()), ldb1, b1_nn != 0};
+        const MatA a2{reinterpret_cast<const float*>(dA2.get()), lda2, nullptr, K2};
+        const MatB b2{reinterpret_cast<const float*>(dB2.get()), ldb2, b2_nn != 0};
+        const float* sc = epi == kEpiRowScale ? reinterpret_cast<const float*>(dS.get()) : nullptr;
+        if (mode == 0) {
+            DevBuf<uint8_t> img;
+            gemm_bf16x3(a1, b1, K2 > 0 ? &a2 : nullptr, K2 > 0 ? &b2 : nullptr, dC.get(), N, M, N, epi, sc, img, s);
+            SC_CUDA(cudaStreamSynchronize(s));
+        } else {
+            gemm_nt(a1, b1, K2 > 0 ? &a2 : nullptr, K2 > 0 ? &b2 : nullptr, dC.get(), N, M, N, epi, sc, s);
+        }
+        d2h(C, dC.get(), M * N, s);
+        SC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 sc_status sc_trainer_destroy(sc_trainer* t) {
     return guard([&] {
         if (!t) return;

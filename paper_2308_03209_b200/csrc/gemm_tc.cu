@@ -1,15 +1,425 @@
-// gemm_tc.cu — tensor-core GEMM path (tcgen05, sm_100a). v0: dispatch only.
+// gemm_tc.cu — fp32-grade GEMMs on the 5th-gen tensor cores (tcgen05, sm_100a).
+//
+//   C[M x N] = A1 op(B1) (+ A2 op(B2)),  M huge (partition rows), N <= 256.
+//
+// Precision: the reference's f32 mode needs ~fp32 products (1e-4 relative over
+// 5 Adam steps). Each fp32 operand x is split into bf16 hi = rn(x) and
+// lo = rn(x - hi) (|x - hi - lo| <= 2^-17 |x|) and the product is
+// hi*hi + hi*lo + lo*hi (three kind::f16 MMAs, fp32 accumulation in TMEM);
+// the dropped lo*lo term is <= 2^-16 relative. This "bf16x3" runs at 1/3 of
+// the bf16 tensor rate, 2x faster than 3xTF32 on the half-rate tf32 pipe.
+//
+// Kernel structure (persistent, one CTA per SM, 288 threads):
+//   warps 0-3  producers: A tile (128 rows x 64 k) fp32 from HBM (optionally
+//              row-gathered), split to hi/lo, stored into the canonical
+//              K-major SWIZZLE_128B smem layout; thread 0 also issues one
+//              cp.async.bulk of the pre-split, pre-swizzled B k-block image.
+//   warp 8     TMEM allocator + single-thread MMA issuer (tcgen05.mma,
+//              tcgen05.commit -> mbarriers).
+//   warps 4-7  epilogue: tcgen05.ld accumulator rows -> ReLU / row-scale ->
+//              global fp32 rows. Two TMEM accumulator buffers (2 x 256 cols)
+//              so tile t's epilogue overlaps tile t+1's main loop.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+
 #include "gemm_tc.cuh"
 #include "internal.hpp"
 #include "trainer.hpp"
 
 namespace sc {
+namespace tc {
 
-void TcGemm::init(sc_trainer* t) { enabled = t->gemm_mode == 0 && false; }
+constexpr int kBM = 128;          // UMMA M (cta_group::1)
+constexpr int kBK = 64;           // k per stage: 64 bf16 = 128 B = one SW128 row
+constexpr int kStages = 2;
+constexpr int kMaxN = 256;
+constexpr int kProducers = 128;   // warps 0-3
+constexpr int kEpilogue = 128;    // warps 4-7
+constexpr int kThreads = kProducers + kEpilogue + 32;  // + warp 8
+constexpr int kATile = kBM * 128;        // bytes of one (hi or lo) A tile
+constexpr int kBTileMax = kMaxN * 128;   // bytes of one (hi or lo) B tile
+constexpr int kStageBytes = 2 * kATile + 2 * kBTileMax;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+struct Src {
+    const float* a;
+    const int32_t* rows;  // optional gather
+    int64_t lda;
+    int32_t K;            // valid k
+    int32_t kblocks;      // ceil(K / 64)
+    const uint8_t* bimg;  // pre-split B image: kblocks x [hi tile | lo tile], each n_pad x 128 B
+};
+
+struct Params {
+    Src src[2];
+    int nsrc;
+    int64_t M;
+    int32_t N, n_pad;
+    float* C;
+    int64_t ldc;
+    int epi;
+    const float* row_scale;
+    int64_t tiles;
+};
+
+// ---- PTX helpers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (tcgen05 format):
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46)
+// = 1024 B between 8-row core groups, version 1 at [46,48), swizzle mode 2
+// (128 B) at [61,64).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(1) << 16) |
+           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+           (static_cast<uint64_t>(2) << 61);
+}
+// Instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A bf16 (7-9 = 1),
+// B bf16 (10-12 = 1), both K-major, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// fp32 -> (hi, lo) bf16 pair; packs two elements per 32-bit word.
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
+    hi = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+    lo = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+}
+
+// Byte offset of (row, 16-byte chunk c) in a K-major SW128 tile.
+__host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t c) {
+    return (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4);
+}
+
+// ---- the kernel ----------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full = bars;                   // [kStages]
+    uint64_t* empty = bars + kStages;        // [kStages]
+    uint64_t* tfull = bars + 2 * kStages;    // [2]
+    uint64_t* tempty = bars + 2 * kStages + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t btile = static_cast<uint32_t>(p.n_pad) * 128u;
+
+    if (warp == 8) {
+        if (lane == 0) {
+            for (int s = 0; s < kStages; ++s) {
+                mbar_init(&full[s], kProducers);
+                mbar_init(&empty[s], 1);
+            }
+            for (int s = 0; s < 2; ++s) {
+                mbar_init(&tfull[s], 1);
+                mbar_init(&tempty[s], kEpilogue);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    int kb_total = 0;
+    for (int s = 0; s < p.nsrc; ++s) kb_total += p.src[s].kblocks;
+
+    if (warp < 4) {
+        // ================= producers =================
+        const int tid = threadIdx.x;
+        uint32_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            const int64_t m0 = tile * kBM;
+            for (int s = 0; s < p.nsrc; ++s) {
+                const Src& S = p.src[s];
+                for (int kb = 0; kb < S.kblocks; ++kb, ++it) {
+                    const int stage = it % kStages;
+                    const uint32_t phase = (it / kStages) & 1;
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* st = smem + stage * kStageBytes;
+                    uint8_t* a_hi = st;
+                    uint8_t* a_lo = st + kATile;
+                    uint8_t* b_hi = st + 2 * kATile;
+                    if (tid == 0) {
+                        mbar_expect_tx(&full[stage], 2 * btile);
+                        bulk_g2s(b_hi, S.bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile, &full[stage]);
+                    }
+                    const int k0 = kb * kBK;
+#pragma unroll 2
+                    for (int j = 0; j < (kBM * 8) / kProducers; ++j) {
+                        const int idx = tid + j * kProducers;
+                        const int r = idx >> 3, c = idx & 7;
+                        const int64_t row = m0 + r;
+                        const int k = k0 + c * 8;
+                        float v[8];
+                        if (row < p.M && k + 8 <= S.K) {
+                            const int64_t grow = S.rows ? S.rows[row] : row;
+                            const float4* src = reinterpret_cast<const float4*>(S.a + grow * S.lda + k);
+                            const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
+                            v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+                            v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+                        } else if (row < p.M && k < S.K) {
+                            const int64_t grow = S.rows ? S.rows[row] : row;
+                            const float* src = S.a + grow * S.lda;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) v[q] = (k + q < S.K) ? __ldg(src + k + q) : 0.f;
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) v[q] = 0.f;
+                        }
+                        uint4 hi, lo;
+                        split2(v[0], v[1], hi.x, lo.x);
+                        split2(v[2], v[3], hi.y, lo.y);
+                        split2(v[4], v[5], hi.z, lo.z);
+                        split2(v[6], v[7], hi.w, lo.w);
+                        const uint32_t off = sw128_off(r, c);
+                        *reinterpret_cast<uint4*>(a_hi + off) = hi;
+                        *reinterpret_cast<uint4*>(a_lo + off) = lo;
+                    }
+                    fence_proxy_async();
+                    mbar_arrive(&full[stage]);
+                }
+            }
+        }
+    } else if (warp == 8) {
+        // ================= MMA issuer =================
+        const uint32_t idesc = idesc_bf16(kBM, p.n_pad);
+        uint32_t it = 0, t = 0;
+        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
+            const uint32_t acc = t & 1;
+            const uint32_t d_tmem = tmem_base + acc * 256;
+            mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (int kbg = 0; kbg < kb_total; ++kbg, ++it) {
+                const int stage = it % kStages;
+                mbar_wait(&full[stage], (it / kStages) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint8_t* st = smem + stage * kStageBytes;
+                    const uint64_t ahi = desc_sw128(smem_u32(st)), alo = desc_sw128(smem_u32(st + kATile));
+                    const uint64_t bhi = desc_sw128(smem_u32(st + 2 * kATile));
+                    const uint64_t blo = desc_sw128(smem_u32(st + 2 * kATile + btile));
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;  // 16 bf16 = 32 B along K
+                        mma_bf16(d_tmem, ahi + adv, bhi + adv, idesc, (kbg | k) ? 1u : 0u);
+                        mma_bf16(d_tmem, ahi + adv, blo + adv, idesc, 1u);
+                        mma_bf16(d_tmem, alo + adv, bhi + adv, idesc, 1u);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (kbg == kb_total - 1) mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ================= epilogue (warps 4-7) =================
+        const int ew = warp - 4;  // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
+        uint32_t t = 0;
+        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
+            const uint32_t acc = t & 1;
+            mbar_wait(&tfull[acc], (t >> 1) & 1);
+            tc_fence_after();
+            const int64_t row = tile * kBM + ew * 32 + lane;
+            const bool live = row < p.M;
+            const float sc = (p.epi == kEpiRowScale && live) ? p.row_scale[row] : 1.f;
+            float* crow = p.C + row * p.ldc;
+            for (int c0 = 0; c0 < p.n_pad; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
+                if (!live) continue;
+                float v[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    float x = __uint_as_float(r[q]);
+                    if (p.epi == kEpiRelu) x = fmaxf(x, 0.f);
+                    else if (p.epi == kEpiRowScale) x = sc * x;
+                    v[q] = x;
+                }
+                if (c0 + 32 <= p.N && (p.ldc & 3) == 0) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        reinterpret_cast<float4*>(crow + c0)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                                                                              v[4 * q + 3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q)
+                        if (c0 + q < p.N) crow[c0 + q] = v[q];
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+// ---- B image prep: fp32 B (NT [N x K] or NN [K x N]) -> per k-block
+// [hi tile | lo tile], each n_pad rows x 64 k bf16 in the SW128 K-major layout.
+__global__ void prep_b_kernel(const float* __restrict__ B, int64_t ldb, int nn, int32_t N, int32_t K, int32_t n_pad,
+                              int32_t kblocks, uint8_t* img) {
+    const int64_t total = int64_t(kblocks) * n_pad * 8;  // 16-byte chunks per (hi) image
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t kb = static_cast<int32_t>(i / (int64_t(n_pad) * 8));
+        const int32_t rem = static_cast<int32_t>(i % (int64_t(n_pad) * 8));
+        const int32_t n = rem >> 3, c = rem & 7;
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int32_t k = kb * kBK + c * 8 + q;
+            v[q] = (n < N && k < K) ? (nn ? B[int64_t(k) * ldb + n] : B[int64_t(n) * ldb + k]) : 0.f;
+        }
+        uint4 hi, lo;
+        split2(v[0], v[1], hi.x, lo.x);
+        split2(v[2], v[3], hi.y, lo.y);
+        split2(v[4], v[5], hi.z, lo.z);
+        split2(v[6], v[7], hi.w, lo.w);
+        uint8_t* base = img + int64_t(kb) * 2 * n_pad * 128;
+        const uint32_t off = sw128_off(n, c);
+        *reinterpret_cast<uint4*>(base + off) = hi;
+        *reinterpret_cast<uint4*>(base + int64_t(n_pad) * 128 + off) = lo;
+    }
+}
+
+}  // namespace tc
+
+// ---- host side -------------------------------------------------------------------
+namespace {
+bool tc_supported(const MatA& a1, const MatA* a2, int32_t N) {
+    auto ok = [](const MatA& a) {
+        return (a.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(a.ptr) % 16) == 0 && a.K >= 1;
+    };
+    return N >= 1 && N <= tc::kMaxN && ok(a1) && (!a2 || ok(*a2));
+}
+}  // namespace
+
+void TcGemm::init(sc_trainer* t) {
+    enabled = t->gemm_mode == 0;
+    if (enabled) {
+        SC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::kSmemBytes));
+    }
+}
+
+void gemm_bf16x3(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
+                 int32_t N, int epi, const float* row_scale, DevBuf<uint8_t>& bimg, cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::kSmemBytes));
+        attr_set = true;
+    }
+    tc::Params p{};
+    const int32_t n_pad = std::max(16, (N + 15) / 16 * 16);
+    p.nsrc = a2 ? 2 : 1;
+    const MatA* as[2] = {&a1, a2};
+    const MatB* bs[2] = {&b1, b2};
+    int64_t img_bytes = 0;
+    int32_t kbs[2] = {0, 0};
+    for (int i = 0; i < p.nsrc; ++i) {
+        kbs[i] = (as[i]->K + tc::kBK - 1) / tc::kBK;
+        img_bytes += int64_t(kbs[i]) * 2 * n_pad * 128;
+    }
+    bimg.ensure(static_cast<size_t>(img_bytes));
+    int64_t off = 0;
+    for (int i = 0; i < p.nsrc; ++i) {
+        const int64_t chunks = int64_t(kbs[i]) * n_pad * 8;
+        tc::prep_b_kernel<<<grid_for(chunks, 256), 256, 0, s>>>(bs[i]->ptr, bs[i]->ld, bs[i]->nn ? 1 : 0, N,
+                                                                as[i]->K, n_pad, kbs[i], bimg.get() + off);
+        SC_LAUNCH_CHECK();
+        count_launch();
+        p.src[i] = tc::Src{as[i]->ptr, as[i]->rows, as[i]->ld, as[i]->K, kbs[i], bimg.get() + off};
+        off += int64_t(kbs[i]) * 2 * n_pad * 128;
+    }
+    p.M = M;
+    p.N = N;
+    p.n_pad = n_pad;
+    p.C = C;
+    p.ldc = ldc;
+    p.epi = epi;
+    p.row_scale = row_scale;
+    p.tiles = (M + tc::kBM - 1) / tc::kBM;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, num_sms()));
+    tc::gemm_bf16x3_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(p);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
 
 void TcGemm::nt(sc_trainer* t, const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc,
                 int64_t M, int32_t N, int epi, const float* row_scale) {
-    gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, t->ctx->stream);
+    if (enabled && tc_supported(a1, a2, N))
+        gemm_bf16x3(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, bimg, t->ctx->stream);
+    else
+        gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, t->ctx->stream);
 }
 
 }  // namespace sc

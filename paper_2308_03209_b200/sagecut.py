@@ -109,6 +109,32 @@ _sig("sc_trainer_profile", [_vp, _i32])
 _sig("sc_trainer_kernel_times", [_vp, C.POINTER(C.c_char_p), C.POINTER(_f64), C.POINTER(_f64), _i32,
                                  C.POINTER(_i32)])
 _sig("sc_trainer_destroy", [_vp])
+_sig("sc_debug_gemm", [_vp, _i32, _i64, _i32, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _i64, _vp,
+                       _i64, _i32, _i32, _vp, _vp])
+
+
+def debug_gemm(A1, B1, b1_nn=False, rows1=None, A2=None, B2=None, b2_nn=False, epi=0, scale=None, simt=False,
+               N=None, ctx: Optional["Context"] = None) -> np.ndarray:
+    """Kernel-level hook: C = A1[rows1] op(B1) (+ A2 op(B2)), epilogue 0/1(relu)/2(row scale)."""
+    ctx = ctx or default_context()
+    A1 = np.ascontiguousarray(A1, np.float32)
+    B1 = np.ascontiguousarray(B1, np.float32)
+    K1 = B1.shape[0] if b1_nn else B1.shape[1]
+    N = N or (B1.shape[1] if b1_nn else B1.shape[0])
+    r1 = None if rows1 is None else np.ascontiguousarray(rows1, np.int32)
+    M = len(r1) if r1 is not None else A1.shape[0]
+    K2, A2p, B2p, lda2, ldb2 = 0, None, None, 0, 0
+    if A2 is not None:
+        A2 = np.ascontiguousarray(A2, np.float32)
+        B2 = np.ascontiguousarray(B2, np.float32)
+        K2 = B2.shape[0] if b2_nn else B2.shape[1]
+        A2p, B2p, lda2, ldb2 = A2, B2, A2.shape[1], B2.shape[1]
+    sc = None if scale is None else np.ascontiguousarray(scale, np.float32)
+    C = np.zeros((M, N), np.float32)
+    _check(_lib.sc_debug_gemm(ctx.h, 1 if simt else 0, M, N, K1, _ptr(A1), A1.shape[0], A1.shape[1], _ptr(r1),
+                              _ptr(B1), B1.shape[1], int(b1_nn), K2, _ptr(A2p), lda2, _ptr(B2p), ldb2, int(b2_nn),
+                              epi, _ptr(sc), _ptr(C)), "debug_gemm")
+    return C
 
 
 def _check(status: int, what: str = ""):
