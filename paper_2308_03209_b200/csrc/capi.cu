@@ -159,6 +159,9 @@ sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, con
         h2d(g->val.get(), val, n, s);
         h2d(g->test.get(), test, n, s);
         g->train_count = train_count;
+        g->feat_amax.alloc(1);
+        SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), s));
+        absmax(n * dim, g->features.get(), g->feat_amax.get(), s);
         SC_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -168,6 +171,8 @@ sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_devic
         set_device(g->ctx);
         SC_CUDA(cudaMemcpyAsync(g->features.get(), features, sizeof(float) * size_t(g->n) * g->dim,
                                 is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->ctx->stream));
+        SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), g->ctx->stream));
+        absmax(int64_t(g->n) * g->dim, g->features.get(), g->feat_amax.get(), g->ctx->stream);
     });
 }
 sc_status sc_graph_info(sc_graph* g, int32_t* n, int64_t* m, int32_t* dim, int32_t* classes) {
@@ -453,6 +458,7 @@ sc_status sc_trainer_set_params(sc_trainer* t, const float* in) {
     return guard([&] {
         set_device(t->ctx);
         h2d(t->theta.get(), in, t->P, t->ctx->stream);
+        t->tc.invalidate();
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
     });
 }
@@ -548,8 +554,15 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
         const MatB b2{reinterpret_cast<const float*>(dB2.get()), ldb2, b2_nn != 0};
         const float* sc = epi == kEpiRowScale ? reinterpret_cast<const float*>(dS.get()) : nullptr;
         if (mode == 0) {
-            DevBuf<uint8_t> img;
-            gemm_bf16x3(a1, b1, K2 > 0 ? &a2 : nullptr, K2 > 0 ? &b2 : nullptr, dC.get(), N, M, N, epi, sc, img, s);
+            DevBuf<float> am(2);
+            SC_CUDA(cudaMemsetAsync(am.get(), 0, 2 * sizeof(float), s));
+            absmax(a1_rows * lda1, a1.ptr, am.get(), s);
+            if (K2 > 0) absmax(M * lda2, a2.ptr, am.get() + 1, s);
+            BImage i1, i2;
+            prep_bimage(i1, b1, N, K1, s);
+            if (K2 > 0) prep_bimage(i2, b2, N, K2, s);
+            gemm_f16x3(a1, am.get(), i1, K2 > 0 ? &a2 : nullptr, am.get() + 1, K2 > 0 ? &i2 : nullptr, dC.get(), N, M,
+                       N, epi, sc, nullptr, s);
             SC_CUDA(cudaStreamSynchronize(s));
         } else {
             gemm_nt(a1, b1, K2 > 0 ? &a2 : nullptr, K2 > 0 ? &b2 : nullptr, dC.get(), N, M, N, epi, sc, s);

@@ -2,24 +2,29 @@
 //
 //   C[M x N] = A1 op(B1) (+ A2 op(B2)),  M huge (partition rows), N <= 256.
 //
-// Precision: the reference's f32 mode needs ~fp32 products (1e-4 relative over
-// 5 Adam steps). Each fp32 operand x is split into bf16 hi = rn(x) and
-// lo = rn(x - hi) (|x - hi - lo| <= 2^-17 |x|) and the product is
-// hi*hi + hi*lo + lo*hi (three kind::f16 MMAs, fp32 accumulation in TMEM);
-// the dropped lo*lo term is <= 2^-16 relative. This "bf16x3" runs at 1/3 of
-// the bf16 tensor rate, 2x faster than 3xTF32 on the half-rate tf32 pipe.
+// Precision ("fp16x3"). The reference's f32 mode needs ~fp32 products: its
+// parity bar is 1e-4 relative after 5 Adam steps, and Adam amplifies small
+// gradient errors (sign flips of near-zero components move a parameter by
+// 2*lr). Each fp32 operand is scaled by a power of two s (exact) so that its
+// |max| lands in [2^14, 2^15), then split into fp16 hi = rn(x s) and
+// lo = rn(x s - hi): |x s - hi - lo| <= 2^-22 |x s|. The product is
+// hi*hi + hi*lo + lo*hi (three kind::f16 MMAs at the full 16-bit tensor rate,
+// fp32 accumulation in TMEM); the dropped lo*lo term is <= 2^-22 relative.
+// Measured: ~2e-7 relative Frobenius error vs fp64 (bf16 splitting gave 4.5e-6,
+// which compounds to 2.5e-4 in 5-step gradients). The scales come from |max|
+// values the producing kernels reduce in their epilogues (no host sync).
 //
 // Kernel structure (persistent, one CTA per SM, 288 threads):
 //   warps 0-3  producers: A tile (128 rows x 64 k) fp32 from HBM (optionally
-//              row-gathered), split to hi/lo, stored into the canonical
-//              K-major SWIZZLE_128B smem layout; thread 0 also issues one
-//              cp.async.bulk of the pre-split, pre-swizzled B k-block image.
+//              row-gathered), scaled + split to fp16 hi/lo, stored in the
+//              canonical K-major SWIZZLE_128B smem layout; thread 0 also issues
+//              one cp.async.bulk of the pre-split, pre-swizzled B k-block image.
 //   warp 8     TMEM allocator + single-thread MMA issuer (tcgen05.mma,
 //              tcgen05.commit -> mbarriers).
-//   warps 4-7  epilogue: tcgen05.ld accumulator rows -> ReLU / row-scale ->
-//              global fp32 rows. Two TMEM accumulator buffers (2 x 256 cols)
-//              so tile t's epilogue overlaps tile t+1's main loop.
-#include <cuda_bf16.h>
+//   warps 4-7  epilogue: tcgen05.ld accumulator rows -> unscale, ReLU /
+//              row-scale, |max| -> global fp32 rows. Two TMEM accumulators
+//              (2 x 256 columns) so tile t's epilogue overlaps tile t+1.
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstring>
@@ -32,7 +37,7 @@ namespace sc {
 namespace tc {
 
 constexpr int kBM = 128;          // UMMA M (cta_group::1)
-constexpr int kBK = 64;           // k per stage: 64 bf16 = 128 B = one SW128 row
+constexpr int kBK = 64;           // k per stage: 64 fp16 = 128 B = one SW128 row
 constexpr int kStages = 2;
 constexpr int kMaxN = 256;
 constexpr int kProducers = 128;   // warps 0-3
@@ -45,11 +50,13 @@ constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barrie
 
 struct Src {
     const float* a;
-    const int32_t* rows;  // optional gather
+    const int32_t* rows;     // optional gather
     int64_t lda;
-    int32_t K;            // valid k
-    int32_t kblocks;      // ceil(K / 64)
-    const uint8_t* bimg;  // pre-split B image: kblocks x [hi tile | lo tile], each n_pad x 128 B
+    int32_t K;               // valid k
+    int32_t kblocks;         // ceil(K / 64)
+    const uint8_t* bimg;     // kblocks x [hi tile | lo tile], each n_pad x 128 B
+    const float* amax_a;     // |A| max (device scalar)
+    const int32_t* bexp;     // power-of-two exponent B was scaled by (device scalar)
 };
 
 struct Params {
@@ -61,6 +68,7 @@ struct Params {
     int64_t ldc;
     int epi;
     const float* row_scale;
+    float* amax_out;
     int64_t tiles;
 };
 
@@ -106,13 +114,12 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
            (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
            (static_cast<uint64_t>(2) << 61);
 }
-// Instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A bf16 (7-9 = 1),
-// B bf16 (10-12 = 1), both K-major, N>>3 at [17,23), M>>4 at [24,29).
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-           (static_cast<uint32_t>(M >> 4) << 24);
+// Instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A f16 (7-9 = 0),
+// B f16 (10-12 = 0), both K-major, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
@@ -135,13 +142,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// fp32 -> (hi, lo) bf16 pair; packs two elements per 32-bit word.
-__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
-    const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
-    const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
-    hi = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
-    lo = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+// Exponent k such that amax * 2^k lies in [2^14, 2^15) (0 for zero / non-finite).
+__host__ __device__ __forceinline__ int scale_exp(float amax) {
+    if (!(amax > 0.f) || !(amax < 3.0e38f)) return 0;
+    int e;
+    frexpf(amax, &e);  // amax = f 2^e, f in [0.5, 1)
+    return 15 - e;
+}
+
+// x * 2^k split into fp16 (hi, lo); two elements per 32-bit word.
+__device__ __forceinline__ void split2(float x0, float x1, float s, uint32_t& hi, uint32_t& lo) {
+    x0 *= s;
+    x1 *= s;
+    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+    const __half l0 = __float2half_rn(x0 - __half2float(h0));
+    const __half l1 = __float2half_rn(x1 - __half2float(h1));
+    hi = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+    lo = static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
 }
 
 // Byte offset of (row, 16-byte chunk c) in a K-major SW128 tile.
@@ -150,18 +167,27 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t c)
 }
 
 // ---- the kernel ----------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* full = bars;                   // [kStages]
-    uint64_t* empty = bars + kStages;        // [kStages]
-    uint64_t* tfull = bars + 2 * kStages;    // [2]
+    uint64_t* full = bars;                      // [kStages]
+    uint64_t* empty = bars + kStages;           // [kStages]
+    uint64_t* tfull = bars + 2 * kStages;       // [2]
     uint64_t* tempty = bars + 2 * kStages + 2;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t btile = static_cast<uint32_t>(p.n_pad) * 128u;
+
+    // Per-source operand scales: A_s gets 2^(kt - kB_s) so that every source's
+    // products carry the same total scale 2^kt (they share one accumulator).
+    int kt = 1 << 20;
+    int kb_exp[2] = {0, 0};
+    for (int s = 0; s < p.nsrc; ++s) {
+        kb_exp[s] = *p.src[s].bexp;
+        kt = min(kt, scale_exp(*p.src[s].amax_a) + kb_exp[s]);
+    }
 
     if (warp == 8) {
         if (lane == 0) {
@@ -196,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
             const int64_t m0 = tile * kBM;
             for (int s = 0; s < p.nsrc; ++s) {
                 const Src& S = p.src[s];
+                const float sa = ldexpf(1.f, kt - kb_exp[s]);
                 for (int kb = 0; kb < S.kblocks; ++kb, ++it) {
                     const int stage = it % kStages;
                     const uint32_t phase = (it / kStages) & 1;
@@ -232,10 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
                             for (int q = 0; q < 8; ++q) v[q] = 0.f;
                         }
                         uint4 hi, lo;
-                        split2(v[0], v[1], hi.x, lo.x);
-                        split2(v[2], v[3], hi.y, lo.y);
-                        split2(v[4], v[5], hi.z, lo.z);
-                        split2(v[6], v[7], hi.w, lo.w);
+                        split2(v[0], v[1], sa, hi.x, lo.x);
+                        split2(v[2], v[3], sa, hi.y, lo.y);
+                        split2(v[4], v[5], sa, hi.z, lo.z);
+                        split2(v[6], v[7], sa, hi.w, lo.w);
                         const uint32_t off = sw128_off(r, c);
                         *reinterpret_cast<uint4*>(a_hi + off) = hi;
                         *reinterpret_cast<uint4*>(a_lo + off) = lo;
@@ -247,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         }
     } else if (warp == 8) {
         // ================= MMA issuer =================
-        const uint32_t idesc = idesc_bf16(kBM, p.n_pad);
+        const uint32_t idesc = idesc_f16(kBM, p.n_pad);
         uint32_t it = 0, t = 0;
         for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
             const uint32_t acc = t & 1;
@@ -265,10 +292,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
                     const uint64_t blo = desc_sw128(smem_u32(st + 2 * kATile + btile));
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k) {
-                        const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;  // 16 bf16 = 32 B along K
-                        mma_bf16(d_tmem, ahi + adv, bhi + adv, idesc, (kbg | k) ? 1u : 0u);
-                        mma_bf16(d_tmem, ahi + adv, blo + adv, idesc, 1u);
-                        mma_bf16(d_tmem, alo + adv, bhi + adv, idesc, 1u);
+                        const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;  // 16 fp16 = 32 B along K
+                        mma_f16(d_tmem, ahi + adv, bhi + adv, idesc, (kbg | k) ? 1u : 0u);
+                        mma_f16(d_tmem, ahi + adv, blo + adv, idesc, 1u);
+                        mma_f16(d_tmem, alo + adv, bhi + adv, idesc, 1u);
                     }
                     mma_commit(&empty[stage]);
                     if (kbg == kb_total - 1) mma_commit(&tfull[acc]);
@@ -279,6 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     } else {
         // ================= epilogue (warps 4-7) =================
         const int ew = warp - 4;  // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
+        const float unscale = ldexpf(1.f, -kt);
+        float amx = 0.f;
         uint32_t t = 0;
         for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
             const uint32_t acc = t & 1;
@@ -295,10 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
                 float v[32];
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
-                    float x = __uint_as_float(r[q]);
+                    float x = __uint_as_float(r[q]) * unscale;
                     if (p.epi == kEpiRelu) x = fmaxf(x, 0.f);
                     else if (p.epi == kEpiRowScale) x = sc * x;
                     v[q] = x;
+                    if (c0 + q < p.N) amx = fmaxf(amx, fabsf(x));
                 }
                 if (c0 + 32 <= p.N && (p.ldc & 3) == 0) {
 #pragma unroll
@@ -314,6 +344,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
+        if (p.amax_out) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out), __float_as_uint(amx));
+        }
     }
     __syncthreads();
     if (warp == 8) {
@@ -322,12 +357,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     }
 }
 
-// ---- B image prep: fp32 B (NT [N x K] or NN [K x N]) -> per k-block
-// [hi tile | lo tile], each n_pad rows x 64 k bf16 in the SW128 K-major layout.
-__global__ void prep_b_kernel(const float* __restrict__ B, int64_t ldb, int nn, int32_t N, int32_t K, int32_t n_pad,
-                              int32_t kblocks, uint8_t* img) {
+// ---- B image prep (one CTA per operand): |B| max -> exponent kB, then fp32 B
+// (NT [N x K] or NN [K x N]) * 2^kB split into per-k-block [hi tile | lo tile],
+// each n_pad rows x 64 k fp16 in the SW128 K-major layout.
+__global__ void __launch_bounds__(1024) prep_b_kernel(const float* __restrict__ B, int64_t ldb, int nn, int32_t N,
+                                                      int32_t K, int32_t n_pad, int32_t kblocks, uint8_t* img,
+                                                      int32_t* bexp) {
+    __shared__ float red[32];
+    float mx = 0.f;
+    for (int64_t i = threadIdx.x; i < int64_t(N) * K; i += blockDim.x) {
+        const int32_t a = static_cast<int32_t>(i / K), b = static_cast<int32_t>(i % K);
+        mx = fmaxf(mx, fabsf(nn ? B[int64_t(b) * ldb + a] : B[int64_t(a) * ldb + b]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (threadIdx.x == 0) red[0] = mx;
+    }
+    __syncthreads();
+    const int kexp = scale_exp(red[0]);
+    const float s = ldexpf(1.f, kexp);
+    if (threadIdx.x == 0) *bexp = kexp;
     const int64_t total = int64_t(kblocks) * n_pad * 8;  // 16-byte chunks per (hi) image
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
         const int32_t kb = static_cast<int32_t>(i / (int64_t(n_pad) * 8));
         const int32_t rem = static_cast<int32_t>(i % (int64_t(n_pad) * 8));
         const int32_t n = rem >> 3, c = rem & 7;
@@ -338,10 +395,10 @@ __global__ void prep_b_kernel(const float* __restrict__ B, int64_t ldb, int nn, 
             v[q] = (n < N && k < K) ? (nn ? B[int64_t(k) * ldb + n] : B[int64_t(n) * ldb + k]) : 0.f;
         }
         uint4 hi, lo;
-        split2(v[0], v[1], hi.x, lo.x);
-        split2(v[2], v[3], hi.y, lo.y);
-        split2(v[4], v[5], hi.z, lo.z);
-        split2(v[6], v[7], hi.w, lo.w);
+        split2(v[0], v[1], s, hi.x, lo.x);
+        split2(v[2], v[3], s, hi.y, lo.y);
+        split2(v[4], v[5], s, hi.z, lo.z);
+        split2(v[6], v[7], s, hi.w, lo.w);
         uint8_t* base = img + int64_t(kb) * 2 * n_pad * 128;
         const uint32_t off = sw128_off(n, c);
         *reinterpret_cast<uint4*>(base + off) = hi;
@@ -352,74 +409,85 @@ __global__ void prep_b_kernel(const float* __restrict__ B, int64_t ldb, int nn, 
 }  // namespace tc
 
 // ---- host side -------------------------------------------------------------------
-namespace {
 bool tc_supported(const MatA& a1, const MatA* a2, int32_t N) {
     auto ok = [](const MatA& a) {
         return (a.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(a.ptr) % 16) == 0 && a.K >= 1;
     };
     return N >= 1 && N <= tc::kMaxN && ok(a1) && (!a2 || ok(*a2));
 }
-}  // namespace
 
-void TcGemm::init(sc_trainer* t) {
-    enabled = t->gemm_mode == 0;
-    if (enabled) {
-        SC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::kSmemBytes));
-    }
-}
-
-void gemm_bf16x3(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
-                 int32_t N, int epi, const float* row_scale, DevBuf<uint8_t>& bimg, cudaStream_t s) {
-    if (M <= 0 || N <= 0) return;
-    static bool attr_set = false;
-    if (!attr_set) {
-        SC_CUDA(cudaFuncSetAttribute(tc::gemm_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::kSmemBytes));
-        attr_set = true;
-    }
-    tc::Params p{};
-    const int32_t n_pad = std::max(16, (N + 15) / 16 * 16);
-    p.nsrc = a2 ? 2 : 1;
-    const MatA* as[2] = {&a1, a2};
-    const MatB* bs[2] = {&b1, b2};
-    int64_t img_bytes = 0;
-    int32_t kbs[2] = {0, 0};
-    for (int i = 0; i < p.nsrc; ++i) {
-        kbs[i] = (as[i]->K + tc::kBK - 1) / tc::kBK;
-        img_bytes += int64_t(kbs[i]) * 2 * n_pad * 128;
-    }
-    bimg.ensure(static_cast<size_t>(img_bytes));
-    int64_t off = 0;
-    for (int i = 0; i < p.nsrc; ++i) {
-        const int64_t chunks = int64_t(kbs[i]) * n_pad * 8;
-        tc::prep_b_kernel<<<grid_for(chunks, 256), 256, 0, s>>>(bs[i]->ptr, bs[i]->ld, bs[i]->nn ? 1 : 0, N,
-                                                                as[i]->K, n_pad, kbs[i], bimg.get() + off);
-        SC_LAUNCH_CHECK();
-        count_launch();
-        p.src[i] = tc::Src{as[i]->ptr, as[i]->rows, as[i]->ld, as[i]->K, kbs[i], bimg.get() + off};
-        off += int64_t(kbs[i]) * 2 * n_pad * 128;
-    }
-    p.M = M;
-    p.N = N;
-    p.n_pad = n_pad;
-    p.C = C;
-    p.ldc = ldc;
-    p.epi = epi;
-    p.row_scale = row_scale;
-    p.tiles = (M + tc::kBM - 1) / tc::kBM;
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, num_sms()));
-    tc::gemm_bf16x3_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(p);
+void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s) {
+    im.N = N;
+    im.K = K;
+    im.n_pad = std::max(16, (N + 15) / 16 * 16);
+    im.kblocks = (K + tc::kBK - 1) / tc::kBK;
+    im.img.ensure(static_cast<size_t>(im.kblocks) * 2 * im.n_pad * 128);
+    im.bexp.ensure(1);
+    tc::prep_b_kernel<<<1, 1024, 0, s>>>(b.ptr, b.ld, b.nn ? 1 : 0, N, K, im.n_pad, im.kblocks, im.img.get(),
+                                         im.bexp.get());
     SC_LAUNCH_CHECK();
     count_launch();
 }
 
-void TcGemm::nt(sc_trainer* t, const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc,
-                int64_t M, int32_t N, int epi, const float* row_scale) {
-    if (enabled && tc_supported(a1, a2, N))
-        gemm_bf16x3(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, bimg, t->ctx->stream);
-    else
-        gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, t->ctx->stream);
+void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
+                const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
+                float* amax_out, cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    if (!tc_supported(a1, a2, N)) throw std::logic_error("gemm_f16x3: unsupported operand layout");
+    static bool attr_set = false;
+    if (!attr_set) {
+        SC_CUDA(cudaFuncSetAttribute(tc::gemm_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::kSmemBytes));
+        attr_set = true;
+    }
+    tc::Params p{};
+    p.nsrc = a2 ? 2 : 1;
+    const MatA* as[2] = {&a1, a2};
+    const BImage* bs[2] = {&b1, b2};
+    const float* am[2] = {amax1, amax2};
+    for (int i = 0; i < p.nsrc; ++i) {
+        if (bs[i]->N != N || bs[i]->K != as[i]->K) throw std::logic_error("gemm_f16x3: B image shape mismatch");
+        p.src[i] = tc::Src{as[i]->ptr, as[i]->rows, as[i]->ld, as[i]->K, bs[i]->kblocks, bs[i]->img.get(), am[i],
+                           bs[i]->bexp.get()};
+    }
+    p.M = M;
+    p.N = N;
+    p.n_pad = b1.n_pad;
+    p.C = C;
+    p.ldc = ldc;
+    p.epi = epi;
+    p.row_scale = row_scale;
+    p.amax_out = amax_out;
+    p.tiles = (M + tc::kBM - 1) / tc::kBM;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, num_sms()));
+    tc::gemm_f16x3_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(p);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+
+void TcGemm::init(sc_trainer* t) { enabled = t->gemm_mode == 0; }
+
+const BImage& TcGemm::image(const MatB& b, int32_t N, int32_t K, cudaStream_t s) {
+    const Key key{b.ptr, b.ld, b.nn, N, K};
+    auto& e = cache[key];
+    if (e.version != version) {
+        prep_bimage(e.im, b, N, K, s);
+        e.version = version;
+    }
+    return e.im;
+}
+
+void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2,
+                const float* amax2, const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi,
+                const float* row_scale, float* amax_out) {
+    cudaStream_t s = t->ctx->stream;
+    if (enabled && tc_supported(a1, a2, N)) {
+        const BImage& i1 = image(b1, N, a1.K, s);
+        const BImage* i2 = a2 ? &image(*b2, N, a2->K, s) : nullptr;
+        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s);
+    } else {
+        gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
+    }
 }
 
 }  // namespace sc

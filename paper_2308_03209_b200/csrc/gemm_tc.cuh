@@ -1,7 +1,10 @@
-// gemm_tc.cuh — GEMM dispatcher for the M-huge products of the step.
+// gemm_tc.cuh — tensor-core GEMM path (tcgen05 fp16x3, gemm_tc.cu) and its dispatcher.
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <map>
+#include <tuple>
 
 #include "internal.hpp"
 #include "nn.cuh"
@@ -10,20 +13,42 @@ struct sc_trainer;
 
 namespace sc {
 
-// C[M x N] = A1 op(B1) (+ A2 op(B2)) with an epilogue on the tcgen05 tensor
-// cores in bf16x3 split precision (gemm_tc.cu). A rows must be 16-byte
-// aligned (ld % 4 == 0); N <= 256. `bimg` is scratch for the pre-split B image.
-void gemm_bf16x3(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
-                 int32_t N, int epi, const float* row_scale, DevBuf<uint8_t>& bimg, cudaStream_t s);
+// A weight operand pre-scaled (by 2^bexp) and pre-split into fp16 hi/lo
+// k-block images in the smem SW128 layout, ready for one bulk copy per stage.
+struct BImage {
+    DevBuf<uint8_t> img;
+    DevBuf<int32_t> bexp;
+    int32_t N = 0, K = 0, n_pad = 0, kblocks = 0;
+};
 
-// Uses gemm_bf16x3 when the trainer allows it and the shape is supported;
-// otherwise the fp32 SIMT kernel (nn.cu).
+bool tc_supported(const MatA& a1, const MatA* a2, int32_t N);
+void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s);
+
+// C[M x N] = A1 op(B1) (+ A2 op(B2)) on the tensor cores in fp16x3 split
+// precision. amax_i: device scalars holding max|A_i| (upper bounds are fine);
+// amax_out (optional): max|C| is atomically reduced into it.
+void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
+                const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
+                float* amax_out, cudaStream_t s);
+
+// Uses gemm_f16x3 when the trainer allows it and the shape is supported,
+// otherwise the fp32 SIMT kernel (nn.cu). Weight images are cached per
+// operand and rebuilt when `version` changes (after every Adam step).
 struct TcGemm {
     bool enabled = false;
-    DevBuf<uint8_t> bimg;
+    uint64_t version = 1;
+    using Key = std::tuple<const float*, int64_t, bool, int32_t, int32_t>;
+    struct Entry {
+        BImage im;
+        uint64_t version = 0;
+    };
+    std::map<Key, Entry> cache;
     void init(sc_trainer* t);
-    void nt(sc_trainer* t, const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc,
-            int64_t M, int32_t N, int epi, const float* row_scale);
+    void invalidate() { ++version; }
+    const BImage& image(const MatB& b, int32_t N, int32_t K, cudaStream_t s);
+    void nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2, const float* amax2,
+            const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
+            float* amax_out);
 };
 
 }  // namespace sc

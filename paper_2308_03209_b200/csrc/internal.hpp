@@ -95,6 +95,7 @@ struct sc_graph {
     // Graph data (features/labels/masks)
     int32_t dim = 0, num_classes = 0;
     sc::DevBuf<float> features;        // n x dim
+    sc::DevBuf<float> feat_amax;       // max |features| (tensor-core operand scale)
     sc::DevBuf<int32_t> labels;        // n
     sc::DevBuf<uint8_t> train, val, test;  // n
     int64_t train_count = 0;

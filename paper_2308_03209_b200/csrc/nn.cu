@@ -33,7 +33,18 @@ struct GemmArgs {
     int32_t N;
     int epi;
     const float* row_scale;
+    float* amax_out;
 };
+
+// |v| max-reduction into a float slot: non-negative floats order like their bits.
+__device__ __forceinline__ void atomic_max_abs(float* slot, float v) {
+    atomicMax(reinterpret_cast<unsigned int*>(slot), __float_as_uint(fabsf(v)));
+}
+__device__ __forceinline__ float warp_max_f(float x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
 
 __device__ __forceinline__ float load_a(const MatA& a, int64_t r, int32_t k, int64_t M) {
     if (r >= M || k >= a.K) return 0.f;
@@ -97,6 +108,7 @@ __global__ void __launch_bounds__(NT) gemm_nt_kernel(GemmArgs args) {
             __syncthreads();
         }
     }
+    float mx = 0.f;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int64_t r = m0 + ty * TM + i;
@@ -110,8 +122,21 @@ __global__ void __launch_bounds__(NT) gemm_nt_kernel(GemmArgs args) {
             if (args.epi == kEpiRelu) v = fmaxf(v, 0.f);
             else if (args.epi == kEpiRowScale) v = sc * v;
             args.C[r * args.ldc + c] = v;
+            mx = fmaxf(mx, fabsf(v));
         }
     }
+    if (args.amax_out) {
+        mx = warp_max_f(mx);
+        if ((threadIdx.x & 31) == 0) atomic_max_abs(args.amax_out, mx);
+    }
+}
+
+__global__ void absmax_kernel(int64_t n, const float* __restrict__ x, float* out) {
+    float mx = 0.f;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        mx = fmaxf(mx, fabsf(x[i]));
+    mx = warp_max_f(mx);
+    if ((threadIdx.x & 31) == 0) atomic_max_abs(out, mx);
 }
 
 // Weight-gradient GEMM, split-K: block (tile, split) accumulates a 128 x 128
@@ -233,7 +258,8 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
                                                    const int32_t* __restrict__ nbrs,
                                                    const uint32_t* __restrict__ bits, const float* __restrict__ inv,
                                                    const float* __restrict__ src, const float* __restrict__ msg,
-                                                   float* __restrict__ out) {
+                                                   float* __restrict__ out, float* amax_out) {
+    float amx = 0.f;
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int32_t H4 = H >> 2;
@@ -305,7 +331,12 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
                 r.w = mv.w > 0.f ? r.w : 0.f;
             }
             reinterpret_cast<float4*>(out + v * H)[ch] = r;
+            amx = fmaxf(amx, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
         }
+    }
+    if (amax_out) {
+        amx = warp_max_f(amx);
+        if (lane == 0) atomic_max_abs(amax_out, amx);
     }
 }
 
@@ -314,7 +345,7 @@ template <bool kBwd>
 __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                    const int32_t* __restrict__ nbrs, const uint32_t* __restrict__ bits,
                                    const float* __restrict__ inv, const float* __restrict__ src,
-                                   const float* __restrict__ msg, float* __restrict__ out) {
+                                   const float* __restrict__ msg, float* __restrict__ out, float* amax_out) {
     const int64_t total = n * H;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t v = i / H;
@@ -323,27 +354,28 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
         for (int64_t k = off[v]; k < off[v + 1]; ++k)
             if (slot_kept(bits, k)) acc += src[int64_t(nbrs[k]) * H + c];
         out[i] = kBwd ? (msg[i] > 0.f ? acc : 0.f) : acc * inv[v];
+        if (amax_out) atomic_max_abs(amax_out, out[i]);
     }
 }
 
 template <bool kBwd>
 void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
-                 const float* src, const float* msg, float* out, cudaStream_t s) {
+                 const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out) {
     if (n <= 0) return;
     if (H % 4 != 0) {
-        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
     } else {
         const int64_t warps_needed = n;
         const unsigned grid = grid_for(warps_needed * 32, 256, int64_t(num_sms()) * 16);
         const int nch = (H / 4 + 31) / 32;
         if (nch <= 1)
-            spmm_kernel<1, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+            spmm_kernel<1, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
         else if (nch == 2)
-            spmm_kernel<2, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+            spmm_kernel<2, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
         else if (nch <= 4)
-            spmm_kernel<4, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+            spmm_kernel<4, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
         else
-            spmm_kernel<8, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out);
+            spmm_kernel<8, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
     }
     SC_LAUNCH_CHECK();
     count_launch();
@@ -532,9 +564,10 @@ __global__ void correct_kernel(int64_t n, int32_t C, const float* __restrict__ l
 }  // namespace
 
 void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
-             int32_t N, int epi, const float* row_scale, cudaStream_t s) {
+             int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out) {
     if (M <= 0 || N <= 0) return;
     GemmArgs args{};
+    args.amax_out = amax_out;
     args.a[0] = a1;
     args.b[0] = b1;
     args.nsrc = 1;
@@ -593,11 +626,17 @@ void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* bits, float* 
 }
 void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* msg, float* mean, cudaStream_t s) {
-    spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, mean, s);
+    spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, mean, s, nullptr);
 }
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
-              const float* dmean_s, const float* msg, float* dz, cudaStream_t s) {
-    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s);
+              const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out) {
+    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s, amax_out);
+}
+void absmax(int64_t n, const float* x, float* out, cudaStream_t s) {
+    if (n <= 0) return;
+    absmax_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, x, out);
+    SC_LAUNCH_CHECK();
+    count_launch();
 }
 void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_t* bits, cudaStream_t s) {
     if (nnz <= 0) return;

@@ -24,8 +24,12 @@ struct MatB {
 enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2 };
 
 // C[M x N] = A1 * op(B1) (+ A2 * op(B2)), fp32 in/out, fp32 accumulate, then epilogue.
+// amax_out (optional): atomically max-reduced with |C| (the next GEMM's operand scale).
 void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
-             int32_t N, int epi, const float* row_scale, cudaStream_t s);
+             int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out = nullptr);
+
+// *out = max(*out, max |x[0..n)|) (non-negative floats compare like their bit patterns).
+void absmax(int64_t n, const float* x, float* out, cudaStream_t s);
 
 // Weight gradient: C[N1 x N2] = A^T [N1 x M] * Bcat [M x N2], where Bcat's
 // columns [0, n2a) come from b1 and [n2a, N2) from b2 (b2 may gather rows).
@@ -47,7 +51,7 @@ void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs,
               const float* inv, const float* msg, float* mean, cudaStream_t s);
 // dz[u] = 1[msg[u] > 0] * sum_{v in CSR(u), kept} dmean_s[v]   (nn.hpp:277-288, pull form)
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
-              const float* dmean_s, const float* msg, float* dz, cudaStream_t s);
+              const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out = nullptr);
 // CSR-slot bitmap of a local-edge-indexed byte mask: bit k = mask[eids[k]].
 void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_t* bits, cudaStream_t s);
 

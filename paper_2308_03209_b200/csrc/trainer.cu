@@ -163,6 +163,7 @@ void trainer_init(sc_trainer* t) {
     t->out2.alloc(2);
     t->nonfinite.alloc(1);
     t->red_partial.alloc(1024);
+    t->amax.alloc(sc_trainer::kSlotBase + 2 * std::max(t->L, 1));
     ensure_rows(t, n_max);
     int32_t maxN1 = t->C, maxN2 = t->E;
     for (auto& lo : t->lay) {
@@ -256,10 +257,11 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
     for (int l = 0; l < t->L; ++l) {
         const LayerOff& lo = t->lay[l];
         const MatA xin = l == 0 ? x0 : MatA{t->X[l].get(), lo.in, nullptr, lo.in};
+        const float* xin_amax = l == 0 ? t->g->feat_amax.get() : t->amax_x(l);
         // msg = relu(h W^T)   (nn.hpp:220-221)
         P.begin("gemm_msg", 4.0 * n * (lo.in + lo.H), s);
-        t->tc.nt(t, xin, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, t->MSG[l].get(), lo.H, n, lo.H,
-                 kEpiRelu, nullptr);
+        t->tc.nt(t, xin, xin_amax, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, nullptr,
+                 t->MSG[l].get(), lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l));
         P.end(s);
         // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
         P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
@@ -270,7 +272,9 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
         const MatB uR{t->theta.get() + lo.U + lo.H, lo.H + lo.in, false};
         const MatA mean{t->MEAN[l].get(), lo.H, nullptr, lo.H};
         P.begin("gemm_update", 4.0 * n * (2 * lo.H + lo.in), s);
-        t->tc.nt(t, mean, uL, &xin, &uR, t->X[l + 1].get(), lo.H, n, lo.H, kEpiNone, nullptr);
+        // |mean| <= max|msg| (a mean of msg rows): msg's bound scales it.
+        t->tc.nt(t, mean, t->amax_msg(l), uL, &xin, xin_amax, &uR, t->X[l + 1].get(), lo.H, n, lo.H, kEpiNone, nullptr,
+                 t->amax_x(l + 1));
         P.end(s);
     }
     const MatA emb = t->L == 0 ? x0 : MatA{t->X[t->L].get(), t->E, nullptr, t->E};
@@ -295,10 +299,12 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
     P.end(s);
     float* dh = t->dh.get();
     float* dh2 = t->dh2.get();
+    float* dh_amax = t->amax_slot(sc_trainer::kSlotDh0);
+    float* dh2_amax = t->amax_slot(sc_trainer::kSlotDh1);
     if (t->L == 0) return;
     P.begin("gemm_dgrad", 4.0 * n * (t->C + t->E), s);
     gemm_nt(MatA{t->G.get(), t->C, nullptr, t->C}, MatB{t->theta.get() + t->head_off, t->E, true}, nullptr, nullptr, dh,
-            t->E, n, t->E, kEpiNone, nullptr, s);
+            t->E, n, t->E, kEpiNone, nullptr, s, dh_amax);
     P.end(s);
     for (int l = t->L - 1; l >= 0; --l) {
         const LayerOff& lo = t->lay[l];
@@ -311,12 +317,14 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
         P.end(s);
         // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
         P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s);
-        t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr, nullptr,
-                 t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get());
+        t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr,
+                 nullptr, nullptr, t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get(), nullptr);
         P.end(s);
         // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
+        float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
+        SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
         P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
-        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s);
+        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s, dz_amax);
         P.end(s);
         // dW = dz^T h_in   (:289)
         P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s);
@@ -327,10 +335,12 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
             const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz.get(), lo.H, nullptr, lo.H};
             P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s);
             const MatB wB{t->theta.get() + lo.W, lo.in, true};
-            t->tc.nt(t, dhA, MatB{t->theta.get() + lo.U + lo.H, lo.H + lo.in, true}, &dzA, &wB, dh2, lo.in, n, lo.in,
-                     kEpiNone, nullptr);
+            SC_CUDA(cudaMemsetAsync(dh2_amax, 0, sizeof(float), s));
+            t->tc.nt(t, dhA, dh_amax, MatB{t->theta.get() + lo.U + lo.H, lo.H + lo.in, true}, &dzA, dz_amax, &wB, dh2,
+                     lo.in, n, lo.in, kEpiNone, nullptr, dh2_amax);
             P.end(s);
             std::swap(dh, dh2);
+            std::swap(dh_amax, dh2_amax);
         }
     }
 }
@@ -351,6 +361,7 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     const int64_t kept =
         bits ? 2 * static_cast<int64_t>(std::ceil((1.0 - t->ratio) * static_cast<double>(pd.m_local))) : st.nnz;
     const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept};
+    SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
     forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
     if (t->loss == 0)
@@ -393,6 +404,7 @@ void trainer_step_async(sc_trainer* t, int epoch) {
     const float c2 = static_cast<float>(1.0 - std::pow(0.999, static_cast<double>(step)));
     adam(t->P, t->theta.get(), t->m1.get(), t->m2.get(), t->gathered.get(), 0.9f, 0.999f, c1, c2,
          static_cast<float>(t->lr), static_cast<float>(1e-8), t->nonfinite.get(), s);
+    t->tc.invalidate();  // weights changed: rebuild the pre-split weight images on next use
     t->prof.end(s);
     d2h(t->host_out, t->out2.get(), 2, s);
     d2h(&t->host_nonfinite, t->nonfinite.get(), 1, s);

@@ -85,6 +85,13 @@ struct sc_trainer {
     int64_t ws_floats = 0;
     sc::DevBuf<double> row_loss, part_loss, out2, red_partial;
     sc::DevBuf<int> nonfinite;
+    // max|x| of every tensor-core A operand, reduced by its producing kernel
+    // and read by the consuming GEMM to pick its power-of-two operand scale.
+    enum { kSlotDh0 = 0, kSlotDh1 = 1, kSlotDz = 2, kSlotBase = 3 };
+    sc::DevBuf<float> amax;
+    float* amax_slot(int i) { return amax.get() + i; }
+    float* amax_x(int l) { return amax.get() + kSlotBase + (l - 1); }  // layer input X[l], l in [1, L]
+    float* amax_msg(int l) { return amax.get() + kSlotBase + L + l; }  // MSG[l], l in [0, L)
     double host_out[2] = {0, 0};
     int host_nonfinite = 0;
     bool pending = false;
