@@ -172,6 +172,12 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
                         int64_t a1_rows, int64_t lda1, const int32_t* rows1, const float* B1, int64_t ldb1,
                         int32_t b1_nn, int32_t K2, const float* A2, int64_t lda2, const float* B2, int64_t ldb2,
                         int32_t b2_nn, int32_t epi, const float* scale, float* C);
+/* Weight-gradient product C[N1 x (N2a + N2b)] = A^T [B1 | B2[rows2]] over M
+ * rows: tcgen05 fp16x3 split-K (mode 0) or fp32 SIMT split-K (mode 1).
+ * A: M x N1, B1: M x N2a, B2: b2_rows x N2b (optional), rows2: M gather
+ * indices into B2 (optional). Host buffers. */
+sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A, int32_t N1, const float* B1,
+                           int32_t N2a, const float* B2, int64_t b2_rows, int32_t N2b, const int32_t* rows2, float* C);
 
 #ifdef __cplusplus
 }

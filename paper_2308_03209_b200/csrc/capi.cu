@@ -572,6 +572,40 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
     });
 }
 
+sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A, int32_t N1, const float* B1,
+                           int32_t N2a, const float* B2, int64_t b2_rows, int32_t N2b, const int32_t* rows2, float* C) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && A && B1 && C && M >= 0 && N1 >= 1 && N2a >= 1, "sc_debug_gemm_tn: bad arguments");
+        set_device(ctx);
+        cudaStream_t s = ctx->stream;
+        const int32_t N2 = N2a + (B2 ? N2b : 0);
+        DevBuf<float> dA(std::max<int64_t>(M * N1, 1)), dB1(std::max<int64_t>(M * N2a, 1));
+        DevBuf<float> dB2(std::max<int64_t>(B2 ? b2_rows * N2b : 1, 1)), dC(int64_t(N1) * N2);
+        DevBuf<int32_t> dR(std::max<int64_t>(rows2 ? M : 1, 1));
+        h2d(dA.get(), A, M * N1, s);
+        h2d(dB1.get(), B1, M * N2a, s);
+        if (B2) h2d(dB2.get(), B2, b2_rows * N2b, s);
+        if (rows2) h2d(dR.get(), rows2, M, s);
+        const MatT a{dA.get(), N1, nullptr, N1}, b1{dB1.get(), N2a, nullptr, N2a};
+        const MatT b2{dB2.get(), N2b, rows2 ? dR.get() : nullptr, N2b};
+        const int64_t wsf = std::max<int64_t>(gemm_tn_workspace_floats(N1, N2), int64_t(256) * N1 * N2);
+        DevBuf<float> ws(wsf);
+        if (mode == 0) {
+            DevBuf<float> am(3);
+            SC_CUDA(cudaMemsetAsync(am.get(), 0, 3 * sizeof(float), s));
+            absmax(M * N1, dA.get(), am.get(), s);
+            absmax(M * N2a, dB1.get(), am.get() + 1, s);
+            if (B2) absmax(b2_rows * N2b, dB2.get(), am.get() + 2, s);
+            gemm_tn_f16x3(a, am.get(), b1, am.get() + 1, B2 ? &b2 : nullptr, am.get() + 2, M, dC.get(), N2, ws.get(),
+                          wsf, s);
+        } else {
+            gemm_tn(a, b1, B2 ? &b2 : nullptr, M, dC.get(), N2, ws.get(), wsf, s);
+        }
+        d2h(C, dC.get(), int64_t(N1) * N2, s);
+        SC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 sc_status sc_trainer_destroy(sc_trainer* t) {
     return guard([&] {
         if (!t) return;

@@ -406,9 +406,324 @@ __global__ void __launch_bounds__(1024) prep_b_kernel(const float* __restrict__ 
     }
 }
 
+// =============================================================================
+// Weight-gradient GEMM:  C[N1 x N2] = A^T Bcat,  A [M x N1], Bcat = [B1 | B2]
+// [M x N2], K = M (partition rows, millions). The MMA's "M" is N1 (tiles of
+// 128), its "N" is N2 (tiles of <= 256), its K runs over rows. Row-major
+// activations are MN-major operands, so the producers copy rows straight
+// into the MN-major SWIZZLE_128B layout (scaled + fp16x3 split on the way).
+// Split-K over rows; inside a CTA the TMEM accumulator is drained every
+// kChunkKb k-blocks into an fp32 partial (the tensor-core accumulate is not
+// round-to-nearest, so long K runs in TMEM would bias the sum); splits are
+// summed in a fixed order afterwards (deterministic).
+// =============================================================================
+constexpr int kChunkKb = 16;                 // 1024 rows per TMEM accumulation
+constexpr int kTnBTile = kMaxN * 128;        // bytes of one B' (hi or lo) tile: 256 cols x 64 k x 2 B
+
+struct TnB {
+    const float* ptr;
+    int64_t ld;
+    const int32_t* rows;
+    int32_t cols;
+    const float* amax;
+};
+struct TnParams {
+    const float* a;
+    int64_t lda;
+    int32_t N1;
+    const float* amax_a;
+    TnB b[2];
+    int nb;          // number of B sources
+    int32_t n2a;     // columns of B1 (B2 follows)
+    int32_t N2;
+    int64_t M;
+    int64_t rows_per_split;
+    int32_t tiles1, tiles2;
+    float* ws;       // [splits][N1][N2] fp32 partials
+    uint32_t lbo, sbo;  // MN-major descriptor strides (bytes)
+};
+
+// MN-major SW128 descriptor: LBO = stride between 64-element MN atoms,
+// SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(lbo >> 4) << 16) |
+           (static_cast<uint64_t>(sbo >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+           (static_cast<uint64_t>(2) << 61);
+}
+// kind::f16, D f32, A/B f16, A and B MN-major (bits 15, 16).
+__host__ __device__ constexpr uint32_t idesc_f16_mn(int M, int N) {
+    return (1u << 4) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+// Byte offset of (mn, k) 16-byte chunk (8 consecutive mn at one k) in an
+// MN-major SW128 tile laid out [mn_atom][k_atom][8 k rows][128 B]:
+// mn atom = 64 elements, k atom = 8 rows, each atom 1024 B.
+__device__ __forceinline__ uint32_t mn_sw128_off(uint32_t mn, uint32_t k) {
+    return (mn >> 6) * 8192 + (k >> 3) * 1024 + (k & 7) * 128 + ((((mn & 63) >> 3) ^ (k & 7)) << 4);
+}
+
+__device__ __forceinline__ float tn_load(const TnB& b, int64_t row, int32_t c) {
+    const int64_t g = b.rows ? b.rows[row] : row;
+    return __ldg(b.ptr + g * b.ld + c);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int kTnStage = 2 * kATile + 2 * kTnBTile;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTnStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = bars + 2 * kStages + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    const int tiles = p.tiles1 * p.tiles2;
+    const int split = blockIdx.x / tiles, tile = blockIdx.x % tiles;
+    const int32_t n10 = (tile / p.tiles2) * kBM, n20 = (tile % p.tiles2) * kMaxN;
+    const int32_t nb = min(kMaxN, p.N2 - n20);
+    const int32_t nb_pad = (nb + 15) / 16 * 16;
+    const int64_t r0 = int64_t(split) * p.rows_per_split;
+    const int64_t r1 = min(p.M, r0 + p.rows_per_split);
+    const int kblocks = r1 > r0 ? static_cast<int>((r1 - r0 + kBK - 1) / kBK) : 0;
+    const int nchunks = (kblocks + kChunkKb - 1) / kChunkKb;
+
+    const int ka = scale_exp(*p.amax_a);
+    int kbx = scale_exp(*p.b[0].amax);
+    if (p.nb > 1) kbx = min(kbx, scale_exp(*p.b[1].amax));
+    const float sa = ldexpf(1.f, ka), sb = ldexpf(1.f, kbx);
+
+    if (warp == 8) {
+        if (lane == 0) {
+            for (int s = 0; s < kStages; ++s) {
+                mbar_init(&full[s], kProducers);
+                mbar_init(&empty[s], 1);
+            }
+            for (int s = 0; s < 2; ++s) {
+                mbar_init(&tfull[s], 1);
+                mbar_init(&tempty[s], kEpilogue);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < 4) {
+        // ===== producers: rows k0..k0+63 of A[:, n10:n10+128] and Bcat[:, n20:n20+nb_pad]
+        const int tid = threadIdx.x;
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int stage = kb % kStages;
+            mbar_wait(&empty[stage], ((kb / kStages) & 1) ^ 1);
+            uint8_t* st = smem + stage * kTnStage;
+            uint8_t* a_hi = st;
+            uint8_t* a_lo = st + kATile;
+            uint8_t* b_hi = st + 2 * kATile;
+            uint8_t* b_lo = b_hi + kTnBTile;
+            const int64_t k0 = r0 + int64_t(kb) * kBK;
+            // A': 64 rows x 16 chunks of 8 columns = 1024 chunks; 8 per thread.
+            for (int j = 0; j < 8; ++j) {
+                const int idx = tid + j * kProducers;
+                const int kr = idx >> 4, ch = idx & 15;
+                const int64_t row = k0 + kr;
+                const int32_t c = n10 + ch * 8;
+                float v[8];
+                if (row < r1 && c + 8 <= p.N1 && (p.lda & 3) == 0) {
+                    const float4* src = reinterpret_cast<const float4*>(p.a + row * p.lda + c);
+                    const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
+                    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+                    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        v[q] = (row < r1 && c + q < p.N1) ? __ldg(p.a + row * p.lda + c + q) : 0.f;
+                }
+                uint4 hi, lo;
+                split2(v[0], v[1], sa, hi.x, lo.x);
+                split2(v[2], v[3], sa, hi.y, lo.y);
+                split2(v[4], v[5], sa, hi.z, lo.z);
+                split2(v[6], v[7], sa, hi.w, lo.w);
+                const uint32_t off = mn_sw128_off(ch * 8, kr);
+                *reinterpret_cast<uint4*>(a_hi + off) = hi;
+                *reinterpret_cast<uint4*>(a_lo + off) = lo;
+            }
+            // B': 64 rows x (nb_pad / 8) chunks.
+            const int bch = nb_pad >> 3;
+            for (int idx = tid; idx < 64 * bch; idx += kProducers) {
+                const int kr = idx / bch, ch = idx % bch;
+                const int64_t row = k0 + kr;
+                const int32_t c = n20 + ch * 8;
+                float v[8];
+                const bool in_b1 = c + 8 <= p.n2a;
+                const bool in_b2 = c >= p.n2a && c + 8 <= p.N2;
+                const TnB& B = in_b1 ? p.b[0] : p.b[1];
+                const int32_t cc = in_b1 ? c : c - p.n2a;
+                const int64_t g = (row < r1 && (in_b1 || in_b2)) ? (B.rows ? B.rows[row] : row) : 0;
+                if (row < r1 && (in_b1 || in_b2) && (B.ld & 3) == 0 && (cc & 3) == 0) {
+                    const float4* src = reinterpret_cast<const float4*>(B.ptr + g * B.ld + cc);
+                    const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
+                    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+                    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int32_t cq = c + q;
+                        v[q] = (row >= r1 || cq >= p.N2) ? 0.f
+                               : cq < p.n2a            ? tn_load(p.b[0], row, cq)
+                                                       : tn_load(p.b[1], row, cq - p.n2a);
+                    }
+                }
+                uint4 hi, lo;
+                split2(v[0], v[1], sb, hi.x, lo.x);
+                split2(v[2], v[3], sb, hi.y, lo.y);
+                split2(v[4], v[5], sb, hi.z, lo.z);
+                split2(v[6], v[7], sb, hi.w, lo.w);
+                const uint32_t off = mn_sw128_off(ch * 8, kr);
+                *reinterpret_cast<uint4*>(b_hi + off) = hi;
+                *reinterpret_cast<uint4*>(b_lo + off) = lo;
+            }
+            fence_proxy_async();
+            mbar_arrive(&full[stage]);
+        }
+    } else if (warp == 8) {
+        // ===== MMA issuer
+        const uint32_t idesc = idesc_f16_mn(kBM, nb_pad);
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            const uint32_t acc = chunk & 1;
+            const uint32_t d_tmem = tmem_base + acc * 256;
+            mbar_wait(&tempty[acc], ((chunk >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const int kb_end = min(kblocks, (chunk + 1) * kChunkKb);
+            for (int kb = chunk * kChunkKb; kb < kb_end; ++kb) {
+                const int stage = kb % kStages;
+                mbar_wait(&full[stage], (kb / kStages) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint8_t* st = smem + stage * kTnStage;
+                    const uint32_t ahi = smem_u32(st), alo = smem_u32(st + kATile);
+                    const uint32_t bhi = smem_u32(st + 2 * kATile), blo = smem_u32(st + 2 * kATile + kTnBTile);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        const uint32_t adv = k * 2048;  // 16 rows = 2 K atoms of 1024 B
+                        const uint64_t dah = desc_mn_sw128(ahi + adv, p.lbo, p.sbo);
+                        const uint64_t dal = desc_mn_sw128(alo + adv, p.lbo, p.sbo);
+                        const uint64_t dbh = desc_mn_sw128(bhi + adv, p.lbo, p.sbo);
+                        const uint64_t dbl = desc_mn_sw128(blo + adv, p.lbo, p.sbo);
+                        const uint32_t first = (kb == chunk * kChunkKb && k == 0) ? 0u : 1u;
+                        mma_f16(d_tmem, dah, dbh, idesc, first);
+                        mma_f16(d_tmem, dah, dbl, idesc, 1u);
+                        mma_f16(d_tmem, dal, dbh, idesc, 1u);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (kb == kb_end - 1) mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ===== epilogue: drain each chunk into the fp32 partial ws[split]
+        const int ew = warp - 4;
+        const int32_t m = n10 + ew * 32 + lane;  // output row (N1 index)
+        const bool live = m < p.N1;
+        const float unscale = ldexpf(1.f, -(ka + kbx));
+        float* out = p.ws + (int64_t(split) * p.N1 + (live ? m : 0)) * p.N2 + n20;
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            const uint32_t acc = chunk & 1;
+            mbar_wait(&tfull[acc], (chunk >> 1) & 1);
+            tc_fence_after();
+            for (int c0 = 0; c0 < nb_pad; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
+                if (!live) continue;
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    if (c0 + q >= nb) break;
+                    const float x = __uint_as_float(r[q]) * unscale;
+                    out[c0 + q] = chunk == 0 ? x : out[c0 + q] + x;
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+        if (nchunks == 0 && live)
+            for (int c = 0; c < nb; ++c) out[c] = 0.f;
+    }
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+__global__ void tn_reduce_kernel(int32_t S, int32_t N1, int32_t N2, const float* ws, float* C, int64_t ldc) {
+    const int64_t total = int64_t(N1) * N2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int32_t s = 0; s < S; ++s) acc += ws[int64_t(s) * total + i];
+        C[(i / N2) * ldc + (i % N2)] = acc;
+    }
+}
+
 }  // namespace tc
 
 // ---- host side -------------------------------------------------------------------
+constexpr int kTnSmemBytes = tc::kStages * (2 * tc::kATile + 2 * tc::kTnBTile) + 1024 + 256;
+
+int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M) {
+    const int32_t tiles = ((N1 + tc::kBM - 1) / tc::kBM) * ((N2 + tc::kMaxN - 1) / tc::kMaxN);
+    int64_t s = std::max<int64_t>(1, num_sms() / tiles);
+    s = std::min<int64_t>(s, (M + 4095) / 4096);  // >= 4096 rows per split
+    return static_cast<int32_t>(std::max<int64_t>(s, 1));
+}
+
+void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
+                   const float* amax_b2, int64_t M, float* C, int64_t ldc, float* ws, int64_t ws_floats,
+                   cudaStream_t s) {
+    const int32_t N1 = a.cols, N2 = b1.cols + (b2 ? b2->cols : 0);
+    if (N1 <= 0 || N2 <= 0) return;
+    if (M <= 0) {
+        for (int32_t r = 0; r < N1; ++r) SC_CUDA(cudaMemsetAsync(C + int64_t(r) * ldc, 0, sizeof(float) * N2, s));
+        return;
+    }
+    static bool attr_set = false;
+    if (!attr_set) {
+        SC_CUDA(cudaFuncSetAttribute(tc::gemm_tn_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kTnSmemBytes));
+        attr_set = true;
+    }
+    tc::TnParams p{};
+    p.a = a.ptr;
+    p.lda = a.ld;
+    p.N1 = N1;
+    p.amax_a = amax_a;
+    p.b[0] = tc::TnB{b1.ptr, b1.ld, b1.rows, b1.cols, amax_b1};
+    p.nb = b2 ? 2 : 1;
+    if (b2) p.b[1] = tc::TnB{b2->ptr, b2->ld, b2->rows, b2->cols, amax_b2};
+    p.n2a = b1.cols;
+    p.N2 = N2;
+    p.M = M;
+    const int32_t S = tn_f16x3_splits(N1, N2, M);
+    if (int64_t(S) * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn_f16x3: workspace too small");
+    p.rows_per_split = ((M + S - 1) / S + tc::kBK - 1) / tc::kBK * tc::kBK;
+    p.tiles1 = (N1 + tc::kBM - 1) / tc::kBM;
+    p.tiles2 = (N2 + tc::kMaxN - 1) / tc::kMaxN;
+    p.ws = ws;
+    p.lbo = 8192;  // MN-major: stride between 64-element MN atoms ([mn_atom][k_atom] layout)
+    p.sbo = 1024;  // stride between 8-row K groups (validated against fp64 in tests/test_gpu_gemm.py)
+    const unsigned grid = static_cast<unsigned>(S * p.tiles1 * p.tiles2);
+    tc::gemm_tn_f16x3_kernel<<<grid, tc::kThreads, kTnSmemBytes, s>>>(p);
+    SC_LAUNCH_CHECK();
+    tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
+    SC_LAUNCH_CHECK();
+    count_launch(2);
+}
 bool tc_supported(const MatA& a1, const MatA* a2, int32_t N) {
     auto ok = [](const MatA& a) {
         return (a.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(a.ptr) % 16) == 0 && a.K >= 1;
@@ -488,6 +803,14 @@ void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b
     } else {
         gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
     }
+}
+
+void TcGemm::tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1,
+                const MatT* b2, const float* amax_b2, int64_t M, float* C, int64_t ldc) {
+    if (enabled)
+        gemm_tn_f16x3(a, amax_a, b1, amax_b1, b2, amax_b2, M, C, ldc, t->ws.get(), t->ws_floats, t->ctx->stream);
+    else
+        gemm_tn(a, b1, b2, M, C, ldc, t->ws.get(), t->ws_floats, t->ctx->stream);
 }
 
 }  // namespace sc

@@ -31,6 +31,14 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
                 float* amax_out, cudaStream_t s);
 
+// Weight gradient C[N1 x N2] = A^T [B1 | B2] (K = M rows) on the tensor cores,
+// fp16x3, split-K with a fixed-order reduction (deterministic). ws needs
+// tn_f16x3_splits(N1, N2, M) * N1 * N2 floats.
+int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M);
+void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
+                   const float* amax_b2, int64_t M, float* C, int64_t ldc, float* ws, int64_t ws_floats,
+                   cudaStream_t s);
+
 // Uses gemm_f16x3 when the trainer allows it and the shape is supported,
 // otherwise the fp32 SIMT kernel (nn.cu). Weight images are cached per
 // operand and rebuilt when `version` changes (after every Adam step).
@@ -49,6 +57,8 @@ struct TcGemm {
     void nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2, const float* amax2,
             const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
             float* amax_out);
+    void tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
+            const float* amax_b2, int64_t M, float* C, int64_t ldc);
 };
 
 }  // namespace sc

@@ -145,6 +145,10 @@ void trainer_init(sc_trainer* t) {
         st.scale.alloc(std::max<int64_t>(st.n, 1));
         compute_weights_device(vc, t->reweight, i, st.w.get());
         loss_weights(t, i);
+        // |dloss/dlogits| <= scale = w / normalizer (|softmax - onehot|, |sigmoid - y| <= 1)
+        st.g_amax.alloc(1);
+        SC_CUDA(cudaMemsetAsync(st.g_amax.get(), 0, sizeof(float), s));
+        absmax(st.n, st.scale.get(), st.g_amax.get(), s);
         st.logits.alloc(std::max<int64_t>(st.n * t->C, 1));
         if (t->use_dropedge) {
             st.words = (st.nnz + 31) / 32;
@@ -234,6 +238,7 @@ struct Rows {
     const int32_t* nodes;  // local -> global row (features / labels); null = identity
     int64_t nnz;           // CSR slots
     int64_t kept;          // CSR slots kept by the selected DropEdge mask
+    const float* g_amax;   // bound on max|dloss/dlogits| (= max loss scale)
 };
 
 // Algorithmic HBM bytes of one aggregation launch: offsets,
@@ -294,8 +299,10 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
     const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L].get(), t->E, nullptr, t->E};
     // head grad = G^T emb ; dh = G head   (:259-260)
     P.begin("wgrad", 4.0 * n * (t->C + t->E), s);
-    gemm_tn(MatT{t->G.get(), t->C, nullptr, t->C}, embt, nullptr, n, slot + t->head_off, t->E, t->ws.get(), t->ws_floats,
-            s);
+    const float* x0_amax = t->g->feat_amax.get();
+    const float* emb_amax = t->L == 0 ? x0_amax : t->amax_x(t->L);
+    t->tc.tn(t, MatT{t->G.get(), t->C, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
+             slot + t->head_off, t->E);
     P.end(s);
     float* dh = t->dh.get();
     float* dh2 = t->dh2.get();
@@ -313,7 +320,8 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
         // dU = dh^T [mean | h_in]   (:271-272)
         const MatT meant{t->MEAN[l].get(), lo.H, nullptr, lo.H};
         P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), s);
-        gemm_tn(dht, meant, &xint, n, slot + lo.U, lo.H + lo.in, t->ws.get(), t->ws_floats, s);
+        const float* xin_amax = l == 0 ? x0_amax : t->amax_x(l);
+        t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, slot + lo.U, lo.H + lo.in);
         P.end(s);
         // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
         P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s);
@@ -328,8 +336,8 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
         P.end(s);
         // dW = dz^T h_in   (:289)
         P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s);
-        gemm_tn(MatT{t->dz.get(), lo.H, nullptr, lo.H}, xint, nullptr, n, slot + lo.W, lo.in, t->ws.get(), t->ws_floats,
-                s);
+        t->tc.tn(t, MatT{t->dz.get(), lo.H, nullptr, lo.H}, dz_amax, xint, xin_amax, nullptr, nullptr, n, slot + lo.W,
+                 lo.in);
         P.end(s);
         if (l > 0) {  // dh = dh U_R + dz W   (:275, :290); layer 0's is unused
             const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz.get(), lo.H, nullptr, lo.H};
@@ -360,7 +368,7 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     }
     const int64_t kept =
         bits ? 2 * static_cast<int64_t>(std::ceil((1.0 - t->ratio) * static_cast<double>(pd.m_local))) : st.nnz;
-    const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept};
+    const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get()};
     SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
     forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
@@ -430,7 +438,7 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
     sc_graph* g = t->g;
     ensure_rows(t, g->n);
     if (t->eval_logits.size() < size_t(g->n) * t->C) t->eval_logits.alloc(size_t(g->n) * t->C);
-    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m};
+    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr};
     const bool was = t->prof.enabled;
     t->prof.enabled = false;
     forward(t, R, t->eval_logits.get());

@@ -26,6 +26,7 @@ struct PartState {
     DevBuf<uint32_t> bits; // K CSR-slot bitmaps
     int64_t words = 0;
     DevBuf<float> logits;  // n x C, last step
+    DevBuf<float> g_amax;  // bound on max|dloss/dlogits| (tensor-core operand scale)
     int chosen = -1;
 };
 

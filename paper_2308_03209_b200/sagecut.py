@@ -113,6 +113,27 @@ _sig("sc_debug_gemm", [_vp, _i32, _i64, _i32, _i32, _vp, _i64, _i64, _vp, _vp, _
                        _i64, _i32, _i32, _vp, _vp])
 
 
+_sig("sc_debug_gemm_tn", [_vp, _i32, _i64, _vp, _i32, _vp, _i32, _vp, _i64, _i32, _vp, _vp])
+
+
+def debug_gemm_tn(A, B1, B2=None, rows2=None, simt=False, ctx: Optional["Context"] = None) -> np.ndarray:
+    """Kernel-level hook: C = A^T [B1 | B2[rows2]] (weight-gradient shape, K = rows)."""
+    ctx = ctx or default_context()
+    A = np.ascontiguousarray(A, np.float32)
+    B1 = np.ascontiguousarray(B1, np.float32)
+    M, N1 = A.shape
+    N2a = B1.shape[1]
+    b2p, b2r, n2b = None, 0, 0
+    if B2 is not None:
+        B2 = np.ascontiguousarray(B2, np.float32)
+        b2p, b2r, n2b = B2, B2.shape[0], B2.shape[1]
+    r2 = None if rows2 is None else np.ascontiguousarray(rows2, np.int32)
+    C = np.zeros((N1, N2a + n2b), np.float32)
+    _check(_lib.sc_debug_gemm_tn(ctx.h, 1 if simt else 0, M, _ptr(A), N1, _ptr(B1), N2a, _ptr(b2p), b2r, n2b,
+                                 _ptr(r2), _ptr(C)), "debug_gemm_tn")
+    return C
+
+
 def debug_gemm(A1, B1, b1_nn=False, rows1=None, A2=None, B2=None, b2_nn=False, epi=0, scale=None, simt=False,
                N=None, ctx: Optional["Context"] = None) -> np.ndarray:
     """Kernel-level hook: C = A1[rows1] op(B1) (+ A2 op(B2)), epilogue 0/1(relu)/2(row scale)."""

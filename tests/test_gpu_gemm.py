@@ -77,3 +77,37 @@ def test_f16x3_scaling_extreme_magnitudes(sc, sa, sb, sa2):
     e = rel(C, ref)
     print(sa, sb, sa2, e)
     assert e <= 2e-6
+
+
+TN_CASES = [  # M, N1, N2a, N2b, gather
+    (5000, 256, 256, 0, False),
+    (70_000, 256, 256, 100, True),
+    (3000, 47, 256, 0, False),
+    (1234, 16, 16, 8, True),
+    (9999, 32, 32, 64, False),
+    (300_000, 256, 256, 0, False),
+]
+
+
+@pytest.mark.parametrize("case", TN_CASES, ids=[str(c) for c in TN_CASES])
+def test_tn_f16x3_matches_fp64(sc, case):
+    """Weight-gradient shape (K = rows): fp16x3 split-K with periodic TMEM drains."""
+    M, N1, N2a, N2b, gather = case
+    rng = np.random.default_rng(M + N1)
+    A = rng.standard_normal((M, N1)).astype(np.float32) * 1e-3
+    B1 = rng.standard_normal((M, N2a)).astype(np.float32)
+    B2 = rows = None
+    ref = A.astype(np.float64).T @ B1.astype(np.float64)
+    if N2b:
+        B2 = rng.standard_normal((M + 11, N2b)).astype(np.float32) * 3.0
+        rows = rng.integers(0, M + 11, size=M).astype(np.int32) if gather else None
+        b2 = B2[rows] if gather else B2[:M]
+        ref = np.concatenate([ref, A.astype(np.float64).T @ b2.astype(np.float64)], axis=1)
+        if not gather:
+            B2 = B2[:M]
+    C_tc = sc.debug_gemm_tn(A, B1, B2, rows)
+    C_simt = sc.debug_gemm_tn(A, B1, B2, rows, simt=True)
+    e_tc, e_simt = rel(C_tc, ref), rel(C_simt, ref)
+    print(f"TN {case}: tcgen05 fp16x3 rel err {e_tc:.2e}, simt fp32 {e_simt:.2e}")
+    assert e_simt <= 1e-5
+    assert e_tc <= 1e-5
