@@ -14,14 +14,15 @@
 // which compounds to 2.5e-4 in 5-step gradients). The scales come from |max|
 // values the producing kernels reduce in their epilogues (no host sync).
 //
-// Kernel structure (persistent, one CTA per SM, 288 threads):
-//   warps 0-3  producers: A tile (128 rows x 64 k) fp32 from HBM (optionally
+// Kernel structure (persistent, one CTA per SM, 416 threads):
+//   warps 0-7  producers: A tile (128 rows x 64 k) fp32 from HBM (optionally
 //              row-gathered), scaled + split to fp16 hi/lo, stored in the
 //              canonical K-major SWIZZLE_128B smem layout; thread 0 also issues
 //              one cp.async.bulk of the pre-split, pre-swizzled B k-block image.
-//   warp 8     TMEM allocator + single-thread MMA issuer (tcgen05.mma,
+//              Loads run two pipeline iterations ahead in registers.
+//   warp 12    TMEM allocator + single-thread MMA issuer (tcgen05.mma,
 //              tcgen05.commit -> mbarriers).
-//   warps 4-7  epilogue: tcgen05.ld accumulator rows -> unscale, ReLU /
+//   warps 8-11 epilogue: tcgen05.ld accumulator rows -> unscale, ReLU /
 //              row-scale, |max| -> global fp32 rows. Two TMEM accumulators
 //              (2 x 256 columns) so tile t's epilogue overlaps tile t+1.
 #include <cuda_fp16.h>
@@ -40,13 +41,22 @@ constexpr int kBM = 128;          // UMMA M (cta_group::1)
 constexpr int kBK = 64;           // k per stage: 64 fp16 = 128 B = one SW128 row
 constexpr int kStages = 2;
 constexpr int kMaxN = 256;
-constexpr int kProducers = 128;   // warps 0-3
-constexpr int kEpilogue = 128;    // warps 4-7
-constexpr int kThreads = kProducers + kEpilogue + 32;  // + warp 8
+constexpr int kProducerWarps = 8; // warps 0-7: operand producers
+constexpr int kProducers = kProducerWarps * 32;
+constexpr int kEpilogue = 128;    // warps 8-11: epilogue (warp % 4 selects the TMEM lane quarter)
+constexpr int kMmaWarp = kProducerWarps + 4;  // warp 12: TMEM allocator + MMA issuer
+constexpr int kThreads = kProducers + kEpilogue + 32;
 constexpr int kATile = kBM * 128;        // bytes of one (hi or lo) A tile
-constexpr int kBTileMax = kMaxN * 128;   // bytes of one (hi or lo) B tile
-constexpr int kStageBytes = 2 * kATile + 2 * kBTileMax;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+// The NT (activation x weight) kernel streams 32-deep k-stages in the
+// SWIZZLE_64B layout (64 B rows) so four stages fit: the weight k-block image
+// arrives by bulk copy from L2 and needs the deeper pipeline to stay hidden.
+constexpr int kNtBK = 32;
+constexpr int kNtStages = 4;
+constexpr int kNtATile = kBM * 64;
+constexpr int kNtBTileMax = kMaxN * 64;
+constexpr int kNtStageBytes = 2 * kNtATile + 2 * kNtBTileMax;
+constexpr int kNtSmemBytes = kNtStages * kNtStageBytes + 1024 + 256 + 4 * 32 * 33 * 4;  // + epilogue staging
+constexpr int kNtRing = 4;  // producer register ring depth (pipeline iterations in flight)
 
 struct Src {
     const float* a;
@@ -54,7 +64,7 @@ struct Src {
     int64_t lda;
     int32_t K;               // valid k
     int32_t kblocks;         // ceil(K / 64)
-    const uint8_t* bimg;     // kblocks x [hi tile | lo tile], each n_pad x 128 B
+    const uint8_t* bimg;     // kblocks x [hi tile | lo tile], each n_pad x 64 B (32 k, SW64)
     const float* amax_a;     // |A| max (device scalar)
     const int32_t* bexp;     // power-of-two exponent B was scaled by (device scalar)
 };
@@ -152,33 +162,117 @@ __host__ __device__ __forceinline__ int scale_exp(float amax) {
 
 // x * 2^k split into fp16 (hi, lo); two elements per 32-bit word.
 __device__ __forceinline__ void split2(float x0, float x1, float s, uint32_t& hi, uint32_t& lo) {
-    x0 *= s;
-    x1 *= s;
-    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
-    const __half l0 = __float2half_rn(x0 - __half2float(h0));
-    const __half l1 = __float2half_rn(x1 - __half2float(h1));
-    hi = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
-    lo = static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+    // packed conversions (F2FP / HADD2.F32): 2 elements per instruction
+    const float2 xs = make_float2(x0 * s, x1 * s);
+    const __half2 h = __float22half2_rn(xs);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __float22half2_rn(make_float2(xs.x - hf.x, xs.y - hf.y));
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
+// K-major SWIZZLE_64B descriptor: 8-row core groups of 512 B (SBO), swizzle mode 4.
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(1) << 16) |
+           (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+           (static_cast<uint64_t>(4) << 61);
+}
+// Byte offset of (row, 16-byte chunk c in 0..3) in a K-major SW64 tile
+// (Swizzle<2,4,3>: chunk bits [4,6) ^= address bits [7,9)).
+__host__ __device__ __forceinline__ uint32_t sw64_off(uint32_t row, uint32_t c) {
+    return (row >> 3) * 512 + (row & 7) * 64 + ((c ^ ((row >> 1) & 3)) << 4);
+}
 // Byte offset of (row, 16-byte chunk c) in a K-major SW128 tile.
 __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t c) {
     return (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4);
 }
 
 // ---- the kernel ----------------------------------------------------------------
+// Producer-side operand loads for one pipeline iteration (tile, source, k-block):
+// every load of the stage is issued before any is consumed (4 chunks of 8 fp32
+// per thread), and the loop keeps two iterations of loads in flight.
+struct NtLoad {
+    float4 x[2][2];
+};
+
+__device__ __forceinline__ void nt_decode(const Params& p, int64_t it, int kb_total, int64_t& m0, int& src,
+                                          int& kb) {
+    const int64_t tl = it / kb_total;
+    int kbg = static_cast<int>(it - tl * kb_total);
+    m0 = (blockIdx.x + tl * gridDim.x) * kBM;
+    src = 0;
+    if (p.nsrc > 1 && kbg >= p.src[0].kblocks) {
+        kbg -= p.src[0].kblocks;
+        src = 1;
+    }
+    kb = kbg;
+}
+
+__device__ __forceinline__ void nt_issue(const Params& p, int tid, int64_t it, int64_t n_it, int kb_total,
+                                         NtLoad& L) {
+    if (it >= n_it) return;
+    int64_t m0;
+    int src, kb;
+    nt_decode(p, it, kb_total, m0, src, kb);
+    const Src& S = p.src[src];
+    const int k0 = kb * kNtBK;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int idx = tid + j * kProducers;
+        const int r = idx >> 2, c = idx & 3;
+        const int64_t row = m0 + r;
+        const int k = k0 + c * 8;
+        if (row < p.M && k + 8 <= S.K) {
+            const int64_t grow = S.rows ? __ldg(S.rows + row) : row;
+            const float4* src4 = reinterpret_cast<const float4*>(S.a + grow * S.lda + k);
+            L.x[j][0] = __ldg(src4);
+            L.x[j][1] = __ldg(src4 + 1);
+        } else {
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = 0.f;
+            if (row < p.M && k < S.K) {
+                const int64_t grow = S.rows ? __ldg(S.rows + row) : row;
+                const float* src1 = S.a + grow * S.lda;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (k + q < S.K) v[q] = __ldg(src1 + k + q);
+            }
+            L.x[j][0] = make_float4(v[0], v[1], v[2], v[3]);
+            L.x[j][1] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+    }
+}
+
+__device__ __forceinline__ void nt_store(int tid, float sa, const NtLoad& L, uint8_t* a_hi, uint8_t* a_lo) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int idx = tid + j * kProducers;
+        const int r = idx >> 2, c = idx & 3;
+        uint4 hi, lo;
+        split2(L.x[j][0].x, L.x[j][0].y, sa, hi.x, lo.x);
+        split2(L.x[j][0].z, L.x[j][0].w, sa, hi.y, lo.y);
+        split2(L.x[j][1].x, L.x[j][1].y, sa, hi.z, lo.z);
+        split2(L.x[j][1].z, L.x[j][1].w, sa, hi.w, lo.w);
+        const uint32_t off = sw64_off(r, c);
+        *reinterpret_cast<uint4*>(a_hi + off) = hi;
+        *reinterpret_cast<uint4*>(a_lo + off) = lo;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* full = bars;                      // [kStages]
-    uint64_t* empty = bars + kStages;           // [kStages]
-    uint64_t* tfull = bars + 2 * kStages;       // [2]
-    uint64_t* tempty = bars + 2 * kStages + 2;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    // align to 1024 B with pointer arithmetic on the shared array (keeps the shared address space)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kNtStages * kNtStageBytes);
+    uint64_t* full = bars;                      // [kNtStages]
+    uint64_t* empty = bars + kNtStages;           // [kNtStages]
+    uint64_t* tfull = bars + 2 * kNtStages;       // [2]
+    uint64_t* tempty = bars + 2 * kNtStages + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kNtStages + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t btile = static_cast<uint32_t>(p.n_pad) * 128u;
+    const uint32_t btile = static_cast<uint32_t>(p.n_pad) * 64u;
 
     // Per-source operand scales: A_s gets 2^(kt - kB_s) so that every source's
     // products carry the same total scale 2^kt (they share one accumulator).
@@ -189,9 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
         kt = min(kt, scale_exp(*p.src[s].amax_a) + kb_exp[s]);
     }
 
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         if (lane == 0) {
-            for (int s = 0; s < kStages; ++s) {
+            for (int s = 0; s < kNtStages; ++s) {
                 mbar_init(&full[s], kProducers);
                 mbar_init(&empty[s], 1);
             }
@@ -213,66 +307,43 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
 
     int kb_total = 0;
     for (int s = 0; s < p.nsrc; ++s) kb_total += p.src[s].kblocks;
+    const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
-    if (warp < 4) {
+    if (warp < kProducerWarps) {
         // ================= producers =================
         const int tid = threadIdx.x;
-        uint32_t it = 0;
-        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-            const int64_t m0 = tile * kBM;
-            for (int s = 0; s < p.nsrc; ++s) {
-                const Src& S = p.src[s];
-                const float sa = ldexpf(1.f, kt - kb_exp[s]);
-                for (int kb = 0; kb < S.kblocks; ++kb, ++it) {
-                    const int stage = it % kStages;
-                    const uint32_t phase = (it / kStages) & 1;
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* st = smem + stage * kStageBytes;
-                    uint8_t* a_hi = st;
-                    uint8_t* a_lo = st + kATile;
-                    uint8_t* b_hi = st + 2 * kATile;
-                    if (tid == 0) {
-                        mbar_expect_tx(&full[stage], 2 * btile);
-                        bulk_g2s(b_hi, S.bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile, &full[stage]);
-                    }
-                    const int k0 = kb * kBK;
-#pragma unroll 2
-                    for (int j = 0; j < (kBM * 8) / kProducers; ++j) {
-                        const int idx = tid + j * kProducers;
-                        const int r = idx >> 3, c = idx & 7;
-                        const int64_t row = m0 + r;
-                        const int k = k0 + c * 8;
-                        float v[8];
-                        if (row < p.M && k + 8 <= S.K) {
-                            const int64_t grow = S.rows ? S.rows[row] : row;
-                            const float4* src = reinterpret_cast<const float4*>(S.a + grow * S.lda + k);
-                            const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
-                            v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-                            v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-                        } else if (row < p.M && k < S.K) {
-                            const int64_t grow = S.rows ? S.rows[row] : row;
-                            const float* src = S.a + grow * S.lda;
+        const int64_t n_it = my_tiles * kb_total;
+        const float sa0 = ldexpf(1.f, kt - kb_exp[0]), sa1 = ldexpf(1.f, kt - kb_exp[1]);
+        NtLoad L[kNtRing];
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) v[q] = (k + q < S.K) ? __ldg(src + k + q) : 0.f;
-                        } else {
+        for (int d = 0; d < kNtRing; ++d) nt_issue(p, tid, d, n_it, kb_total, L[d]);
+        auto produce = [&](int64_t it, const NtLoad& L) {
+            const int stage = static_cast<int>(it % kNtStages);
+            const uint32_t phase = static_cast<uint32_t>((it / kNtStages) & 1);
+            int64_t m0;
+            int src, kb;
+            nt_decode(p, it, kb_total, m0, src, kb);
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* st = smem + stage * kNtStageBytes;
+            if (tid == 0) {
+                mbar_expect_tx(&full[stage], 2 * btile);
+                bulk_g2s(st + 2 * kNtATile, p.src[src].bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile,
+                         &full[stage]);
+            }
+            nt_store(tid, src ? sa1 : sa0, L, st, st + kNtATile);
+            fence_proxy_async();
+            mbar_arrive(&full[stage]);
+        };
+        for (int64_t it = 0; it < n_it; it += kNtRing) {
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) v[q] = 0.f;
-                        }
-                        uint4 hi, lo;
-                        split2(v[0], v[1], sa, hi.x, lo.x);
-                        split2(v[2], v[3], sa, hi.y, lo.y);
-                        split2(v[4], v[5], sa, hi.z, lo.z);
-                        split2(v[6], v[7], sa, hi.w, lo.w);
-                        const uint32_t off = sw128_off(r, c);
-                        *reinterpret_cast<uint4*>(a_hi + off) = hi;
-                        *reinterpret_cast<uint4*>(a_lo + off) = lo;
-                    }
-                    fence_proxy_async();
-                    mbar_arrive(&full[stage]);
+            for (int d = 0; d < kNtRing; ++d) {
+                if (it + d < n_it) {
+                    produce(it + d, L[d]);
+                    nt_issue(p, tid, it + d + kNtRing, n_it, kb_total, L[d]);
                 }
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
         const uint32_t idesc = idesc_f16(kBM, p.n_pad);
         uint32_t it = 0, t = 0;
@@ -282,16 +353,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
             mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
             tc_fence_after();
             for (int kbg = 0; kbg < kb_total; ++kbg, ++it) {
-                const int stage = it % kStages;
-                mbar_wait(&full[stage], (it / kStages) & 1);
+                const int stage = it % kNtStages;
+                mbar_wait(&full[stage], (it / kNtStages) & 1);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint8_t* st = smem + stage * kStageBytes;
-                    const uint64_t ahi = desc_sw128(smem_u32(st)), alo = desc_sw128(smem_u32(st + kATile));
-                    const uint64_t bhi = desc_sw128(smem_u32(st + 2 * kATile));
-                    const uint64_t blo = desc_sw128(smem_u32(st + 2 * kATile + btile));
+                    const uint8_t* st = smem + stage * kNtStageBytes;
+                    const uint64_t ahi = desc_sw64(smem_u32(st)), alo = desc_sw64(smem_u32(st + kNtATile));
+                    const uint64_t bhi = desc_sw64(smem_u32(st + 2 * kNtATile));
+                    const uint64_t blo = desc_sw64(smem_u32(st + 2 * kNtATile + btile));
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
+                    for (int k = 0; k < kNtBK / 16; ++k) {
                         const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;  // 16 fp16 = 32 B along K
                         mma_f16(d_tmem, ahi + adv, bhi + adv, idesc, (kbg | k) ? 1u : 0u);
                         mma_f16(d_tmem, ahi + adv, blo + adv, idesc, 1u);
@@ -304,42 +375,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
             }
         }
     } else {
-        // ================= epilogue (warps 4-7) =================
-        const int ew = warp - 4;  // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
+        // ================= epilogue (warps 8-11) =================
+        const int ew = warp & 3;  // TMEM lanes 32*ew .. 32*ew+31
         const float unscale = ldexpf(1.f, -kt);
+        float* stg = reinterpret_cast<float*>(smem + kNtStages * kNtStageBytes + 256) + ew * (32 * 33);
         float amx = 0.f;
         uint32_t t = 0;
         for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
             const uint32_t acc = t & 1;
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
-            const int64_t row = tile * kBM + ew * 32 + lane;
+            const int64_t row0 = tile * kBM + ew * 32;  // this warp's 32 output rows
+            const int64_t row = row0 + lane;
             const bool live = row < p.M;
             const float sc = (p.epi == kEpiRowScale && live) ? p.row_scale[row] : 1.f;
-            float* crow = p.C + row * p.ldc;
+            const int rows_here = p.M - row0 < 32 ? static_cast<int>(p.M - row0) : 32;
             for (int c0 = 0; c0 < p.n_pad; c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
-                if (!live) continue;
-                float v[32];
+                // lane owns row `row`; transpose through smem so each store is a full 128 B row segment
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
                     float x = __uint_as_float(r[q]) * unscale;
                     if (p.epi == kEpiRelu) x = fmaxf(x, 0.f);
                     else if (p.epi == kEpiRowScale) x = sc * x;
-                    v[q] = x;
-                    if (c0 + q < p.N) amx = fmaxf(amx, fabsf(x));
+                    if (live && c0 + q < p.N) amx = fmaxf(amx, fabsf(x));
+                    stg[lane * 33 + q] = x;
                 }
-                if (c0 + 32 <= p.N && (p.ldc & 3) == 0) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        reinterpret_cast<float4*>(crow + c0)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2],
-                                                                              v[4 * q + 3]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 32; ++q)
-                        if (c0 + q < p.N) crow[c0 + q] = v[q];
+                __syncwarp();
+                const int col = c0 + lane;
+                if (col < p.N) {
+                    float* cbase = p.C + row0 * p.ldc + col;
+                    for (int rr = 0; rr < rows_here; ++rr) cbase[rr * p.ldc] = stg[rr * 33 + lane];
                 }
+                __syncwarp();
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
@@ -351,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
         }
     }
     __syncthreads();
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
     }
@@ -359,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
 
 // ---- B image prep (one CTA per operand): |B| max -> exponent kB, then fp32 B
 // (NT [N x K] or NN [K x N]) * 2^kB split into per-k-block [hi tile | lo tile],
-// each n_pad rows x 64 k fp16 in the SW128 K-major layout.
+// each n_pad rows x 32 k fp16 in the SW64 K-major layout.
 __global__ void __launch_bounds__(1024) prep_b_kernel(const float* __restrict__ B, int64_t ldb, int nn, int32_t N,
                                                       int32_t K, int32_t n_pad, int32_t kblocks, uint8_t* img,
                                                       int32_t* bexp) {
@@ -383,15 +452,15 @@ __global__ void __launch_bounds__(1024) prep_b_kernel(const float* __restrict__ 
     const int kexp = scale_exp(red[0]);
     const float s = ldexpf(1.f, kexp);
     if (threadIdx.x == 0) *bexp = kexp;
-    const int64_t total = int64_t(kblocks) * n_pad * 8;  // 16-byte chunks per (hi) image
+    const int64_t total = int64_t(kblocks) * n_pad * 4;  // 16-byte chunks per (hi) image
     for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
-        const int32_t kb = static_cast<int32_t>(i / (int64_t(n_pad) * 8));
-        const int32_t rem = static_cast<int32_t>(i % (int64_t(n_pad) * 8));
-        const int32_t n = rem >> 3, c = rem & 7;
+        const int32_t kb = static_cast<int32_t>(i / (int64_t(n_pad) * 4));
+        const int32_t rem = static_cast<int32_t>(i % (int64_t(n_pad) * 4));
+        const int32_t n = rem >> 2, c = rem & 3;
         float v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int32_t k = kb * kBK + c * 8 + q;
+            const int32_t k = kb * kNtBK + c * 8 + q;
             v[q] = (n < N && k < K) ? (nn ? B[int64_t(k) * ldb + n] : B[int64_t(n) * ldb + k]) : 0.f;
         }
         uint4 hi, lo;
@@ -399,10 +468,10 @@ __global__ void __launch_bounds__(1024) prep_b_kernel(const float* __restrict__ 
         split2(v[2], v[3], s, hi.y, lo.y);
         split2(v[4], v[5], s, hi.z, lo.z);
         split2(v[6], v[7], s, hi.w, lo.w);
-        uint8_t* base = img + int64_t(kb) * 2 * n_pad * 128;
-        const uint32_t off = sw128_off(n, c);
+        uint8_t* base = img + int64_t(kb) * 2 * n_pad * 64;
+        const uint32_t off = sw64_off(n, c);
         *reinterpret_cast<uint4*>(base + off) = hi;
-        *reinterpret_cast<uint4*>(base + int64_t(n_pad) * 128 + off) = lo;
+        *reinterpret_cast<uint4*>(base + int64_t(n_pad) * 64 + off) = lo;
     }
 }
 
@@ -467,9 +536,85 @@ __device__ __forceinline__ float tn_load(const TnB& b, int64_t row, int32_t c) {
     return __ldg(b.ptr + g * b.ld + c);
 }
 
+// TN producer loads for one 64-row k-block: A' (4 chunks of 8 columns per
+// thread) and B' (up to 8 chunks), all issued before any is consumed.
+struct TnLoad {
+    float4 a[4][2];
+    float4 b[8][2];
+};
+
+__device__ __forceinline__ void tn_load8(const float* base, int64_t ld, const int32_t* rows, int64_t row, int32_t c,
+                                         int32_t cols, bool row_ok, float4 (&out)[2]) {
+    if (row_ok && c + 8 <= cols && (ld & 3) == 0 && (c & 3) == 0) {
+        const int64_t g = rows ? __ldg(rows + row) : row;
+        const float4* s4 = reinterpret_cast<const float4*>(base + g * ld + c);
+        out[0] = __ldg(s4);
+        out[1] = __ldg(s4 + 1);
+    } else {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = 0.f;
+        if (row_ok) {
+            const int64_t g = rows ? __ldg(rows + row) : row;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (c + q < cols) v[q] = __ldg(base + g * ld + c + q);
+        }
+        out[0] = make_float4(v[0], v[1], v[2], v[3]);
+        out[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+}
+
+__device__ __forceinline__ void tn_issue(const TnParams& p, int tid, int kb, int kblocks, int64_t r0, int64_t r1,
+                                         int32_t n10, int32_t n20, int bch, TnLoad& L) {
+    if (kb >= kblocks) return;
+    const int64_t k0 = r0 + int64_t(kb) * kBK;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int idx = tid + j * kProducers;
+        const int kr = idx >> 4, ch = idx & 15;
+        tn_load8(p.a, p.lda, nullptr, k0 + kr, n10 + ch * 8, p.N1, k0 + kr < r1, L.a[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int idx = tid + j * kProducers;
+        if (idx >= 64 * bch) break;
+        const int kr = idx / bch, ch = idx % bch;
+        const int64_t row = k0 + kr;
+        const int32_t c = n20 + ch * 8;
+        const bool ok = row < r1;
+        if (c + 8 <= p.n2a) {
+            tn_load8(p.b[0].ptr, p.b[0].ld, p.b[0].rows, row, c, p.n2a, ok, L.b[j]);
+        } else if (c >= p.n2a) {
+            tn_load8(p.b[1].ptr, p.b[1].ld, p.b[1].rows, row, c - p.n2a, p.N2 - p.n2a, ok, L.b[j]);
+        } else {  // chunk straddles B1 | B2
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int32_t cq = c + q;
+                v[q] = (!ok || cq >= p.N2) ? 0.f : cq < p.n2a ? tn_load(p.b[0], row, cq) : tn_load(p.b[1], row, cq - p.n2a);
+            }
+            L.b[j][0] = make_float4(v[0], v[1], v[2], v[3]);
+            L.b[j][1] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+    }
+}
+
+__device__ __forceinline__ void store_chunk(const float4 (&x)[2], float s, uint8_t* hi_base, uint8_t* lo_base,
+                                            uint32_t off) {
+    uint4 hi, lo;
+    split2(x[0].x, x[0].y, s, hi.x, lo.x);
+    split2(x[0].z, x[0].w, s, hi.y, lo.y);
+    split2(x[1].x, x[1].y, s, hi.z, lo.z);
+    split2(x[1].z, x[1].w, s, hi.w, lo.w);
+    *reinterpret_cast<uint4*>(hi_base + off) = hi;
+    *reinterpret_cast<uint4*>(lo_base + off) = lo;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align to 1024 B with pointer arithmetic on the shared array (keeps the shared address space)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int kTnStage = 2 * kATile + 2 * kTnBTile;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTnStage);
     uint64_t* full = bars;
@@ -494,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     if (p.nb > 1) kbx = min(kbx, scale_exp(*p.b[1].amax));
     const float sa = ldexpf(1.f, ka), sb = ldexpf(1.f, kbx);
 
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         if (lane == 0) {
             for (int s = 0; s < kStages; ++s) {
                 mbar_init(&full[s], kProducers);
@@ -516,9 +661,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp < 4) {
-        // ===== producers: rows k0..k0+63 of A[:, n10:n10+128] and Bcat[:, n20:n20+nb_pad]
+    if (warp < kProducerWarps) {
+        // ===== producers: rows of A[:, n10:n10+128] and Bcat[:, n20:n20+nb_pad], one stage ahead in registers
         const int tid = threadIdx.x;
+        const int bch = nb_pad >> 3;
+        TnLoad L;
+        tn_issue(p, tid, 0, kblocks, r0, r1, n10, n20, bch, L);
         for (int kb = 0; kb < kblocks; ++kb) {
             const int stage = kb % kStages;
             mbar_wait(&empty[stage], ((kb / kStages) & 1) ^ 1);
@@ -527,72 +675,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             uint8_t* a_lo = st + kATile;
             uint8_t* b_hi = st + 2 * kATile;
             uint8_t* b_lo = b_hi + kTnBTile;
-            const int64_t k0 = r0 + int64_t(kb) * kBK;
-            // A': 64 rows x 16 chunks of 8 columns = 1024 chunks; 8 per thread.
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int idx = tid + j * kProducers;
+                store_chunk(L.a[j], sa, a_hi, a_lo, mn_sw128_off((idx & 15) * 8, idx >> 4));
+            }
+#pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int idx = tid + j * kProducers;
-                const int kr = idx >> 4, ch = idx & 15;
-                const int64_t row = k0 + kr;
-                const int32_t c = n10 + ch * 8;
-                float v[8];
-                if (row < r1 && c + 8 <= p.N1 && (p.lda & 3) == 0) {
-                    const float4* src = reinterpret_cast<const float4*>(p.a + row * p.lda + c);
-                    const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
-                    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-                    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        v[q] = (row < r1 && c + q < p.N1) ? __ldg(p.a + row * p.lda + c + q) : 0.f;
-                }
-                uint4 hi, lo;
-                split2(v[0], v[1], sa, hi.x, lo.x);
-                split2(v[2], v[3], sa, hi.y, lo.y);
-                split2(v[4], v[5], sa, hi.z, lo.z);
-                split2(v[6], v[7], sa, hi.w, lo.w);
-                const uint32_t off = mn_sw128_off(ch * 8, kr);
-                *reinterpret_cast<uint4*>(a_hi + off) = hi;
-                *reinterpret_cast<uint4*>(a_lo + off) = lo;
-            }
-            // B': 64 rows x (nb_pad / 8) chunks.
-            const int bch = nb_pad >> 3;
-            for (int idx = tid; idx < 64 * bch; idx += kProducers) {
-                const int kr = idx / bch, ch = idx % bch;
-                const int64_t row = k0 + kr;
-                const int32_t c = n20 + ch * 8;
-                float v[8];
-                const bool in_b1 = c + 8 <= p.n2a;
-                const bool in_b2 = c >= p.n2a && c + 8 <= p.N2;
-                const TnB& B = in_b1 ? p.b[0] : p.b[1];
-                const int32_t cc = in_b1 ? c : c - p.n2a;
-                const int64_t g = (row < r1 && (in_b1 || in_b2)) ? (B.rows ? B.rows[row] : row) : 0;
-                if (row < r1 && (in_b1 || in_b2) && (B.ld & 3) == 0 && (cc & 3) == 0) {
-                    const float4* src = reinterpret_cast<const float4*>(B.ptr + g * B.ld + cc);
-                    const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
-                    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-                    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int32_t cq = c + q;
-                        v[q] = (row >= r1 || cq >= p.N2) ? 0.f
-                               : cq < p.n2a            ? tn_load(p.b[0], row, cq)
-                                                       : tn_load(p.b[1], row, cq - p.n2a);
-                    }
-                }
-                uint4 hi, lo;
-                split2(v[0], v[1], sb, hi.x, lo.x);
-                split2(v[2], v[3], sb, hi.y, lo.y);
-                split2(v[4], v[5], sb, hi.z, lo.z);
-                split2(v[6], v[7], sb, hi.w, lo.w);
-                const uint32_t off = mn_sw128_off(ch * 8, kr);
-                *reinterpret_cast<uint4*>(b_hi + off) = hi;
-                *reinterpret_cast<uint4*>(b_lo + off) = lo;
+                if (idx >= 64 * bch) break;
+                store_chunk(L.b[j], sb, b_hi, b_lo, mn_sw128_off((idx % bch) * 8, idx / bch));
             }
             fence_proxy_async();
             mbar_arrive(&full[stage]);
+            tn_issue(p, tid, kb + 1, kblocks, r0, r1, n10, n20, bch, L);
         }
-    } else if (warp == 8) {
+    } else if (warp == kMmaWarp) {
         // ===== MMA issuer
         const uint32_t idesc = idesc_f16_mn(kBM, nb_pad);
         for (int chunk = 0; chunk < nchunks; ++chunk) {
@@ -629,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         }
     } else {
         // ===== epilogue: drain each chunk into the fp32 partial ws[split]
-        const int ew = warp - 4;
+        const int ew = warp & 3;
         const int32_t m = n10 + ew * 32 + lane;  // output row (N1 index)
         const bool live = m < p.N1;
         const float unscale = ldexpf(1.f, -(ka + kbx));
@@ -656,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             for (int c = 0; c < nb; ++c) out[c] = 0.f;
     }
     __syncthreads();
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
     }
@@ -735,8 +833,8 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
     im.N = N;
     im.K = K;
     im.n_pad = std::max(16, (N + 15) / 16 * 16);
-    im.kblocks = (K + tc::kBK - 1) / tc::kBK;
-    im.img.ensure(static_cast<size_t>(im.kblocks) * 2 * im.n_pad * 128);
+    im.kblocks = (K + tc::kNtBK - 1) / tc::kNtBK;
+    im.img.ensure(static_cast<size_t>(im.kblocks) * 2 * im.n_pad * 64);
     im.bexp.ensure(1);
     tc::prep_b_kernel<<<1, 1024, 0, s>>>(b.ptr, b.ld, b.nn ? 1 : 0, N, K, im.n_pad, im.kblocks, im.img.get(),
                                          im.bexp.get());
@@ -752,7 +850,7 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     static bool attr_set = false;
     if (!attr_set) {
         SC_CUDA(cudaFuncSetAttribute(tc::gemm_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::kSmemBytes));
+                                     tc::kNtSmemBytes));
         attr_set = true;
     }
     tc::Params p{};
@@ -775,7 +873,7 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.amax_out = amax_out;
     p.tiles = (M + tc::kBM - 1) / tc::kBM;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, num_sms()));
-    tc::gemm_f16x3_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(p);
+    tc::gemm_f16x3_kernel<<<grid, tc::kThreads, tc::kNtSmemBytes, s>>>(p);
     SC_LAUNCH_CHECK();
     count_launch();
 }
