@@ -1,0 +1,321 @@
+// sagecut_b200.hpp — C++ drop-in facade over libsagecut_cuda.so.
+//
+// Mirrors the reference's C++ API for the CoFree-GNN training path
+// (namespace sagecut in /root/reference/proj/include/sagecut/*.hpp) on top of
+// the C ABI in sagecut_cuda.h, so a caller such as the reference CLI
+// (proj/tools/main.cpp: run_partition :299-318, run_train :430-446) switches
+// by changing the namespace and include. Graph / partition state stays on the
+// device; the by-value structs below are host copies made on request.
+//
+// Differences from the reference, by design:
+//   * Graph holds a device handle (features fp32 row-major, no Eigen);
+//   * precision is always f32 (the reference's Precision::f32 path);
+//   * train_cofree's per-epoch evaluation is optional (TrainConfig::evaluate).
+// Errors: the reference's exception types and message texts are rethrown
+// (std::invalid_argument, std::runtime_error, std::logic_error).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sagecut_cuda.h"
+
+namespace sagecut_b200 {
+
+using NodeId = std::int32_t;  // graph.hpp:12
+using EdgeId = std::int32_t;  // graph.hpp:13
+
+struct Edge {  // graph.hpp:15-19
+    NodeId u = 0;
+    NodeId v = 0;
+};
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(sc_status st) {
+    if (st == SC_OK) return;
+    const std::string msg = sc_last_error();
+    switch (st) {
+        case SC_EINVAL: throw std::invalid_argument(msg);
+        case SC_ERUNTIME: throw std::runtime_error(msg);
+        case SC_EINTERNAL: throw std::logic_error(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+class Context {
+public:
+    explicit Context(int device = 0) { check(sc_ctx_create(device, &h_)); }
+    ~Context() { sc_ctx_destroy(h_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    sc_ctx* get() const { return h_; }
+
+private:
+    sc_ctx* h_ = nullptr;
+};
+
+struct ValidationReport {  // graph.hpp:43-48
+    std::int64_t dropped_self_loops = 0;
+    std::int64_t merged_duplicate_edges = 0;
+};
+
+// sagecut::Graph (graph.hpp:53-80) with its storage on the device.
+class Graph {
+public:
+    Graph() = default;
+    Graph(Context& ctx, sc_graph* h) : ctx_(&ctx), h_(h, &sc_graph_destroy) { refresh(); }
+    sc_graph* get() const { return h_.get(); }
+    Context& context() const { return *ctx_; }
+    NodeId num_nodes = 0;
+    int num_classes = 0;
+    int feature_dim = 0;
+    std::size_t num_edges() const { return static_cast<std::size_t>(m_); }
+    std::vector<Edge> edges() const {
+        std::vector<Edge> e(num_edges());
+        check(sc_graph_copy_edges(get(), reinterpret_cast<std::int32_t*>(e.data())));
+        return e;
+    }
+    std::vector<NodeId> degrees() const {
+        std::vector<NodeId> d(static_cast<std::size_t>(num_nodes));
+        check(sc_graph_copy_csr(get(), nullptr, nullptr, nullptr, d.data()));
+        return d;
+    }
+    // features: num_nodes x dim row-major; labels: class ids; masks: 0/1 per node
+    void set_data(const std::vector<float>& features, int dim, const std::vector<NodeId>& labels, int classes,
+                  const std::vector<std::uint8_t>& train, const std::vector<std::uint8_t>& val,
+                  const std::vector<std::uint8_t>& test) {
+        check(sc_graph_set_data(get(), features.data(), dim, labels.data(), classes, train.data(), val.data(),
+                                test.data()));
+        refresh();
+    }
+
+private:
+    void refresh() {
+        std::int32_t d = 0, c = 0;
+        check(sc_graph_info(get(), &num_nodes, &m_, &d, &c));
+        feature_dim = d;
+        num_classes = c;
+    }
+    Context* ctx_ = nullptr;
+    std::shared_ptr<sc_graph> h_;
+    std::int64_t m_ = 0;
+};
+
+// build_graph (graph.cpp:8-64), on the device.
+inline std::pair<Graph, ValidationReport> build_graph(Context& ctx, NodeId num_nodes, const std::vector<Edge>& raw) {
+    sc_graph* h = nullptr;
+    ValidationReport rep;
+    check(sc_build_graph(ctx.get(), num_nodes, reinterpret_cast<const std::int32_t*>(raw.data()),
+                         static_cast<std::int64_t>(raw.size()), &h, &rep.dropped_self_loops,
+                         &rep.merged_duplicate_edges));
+    return {Graph(ctx, h), rep};
+}
+
+struct PartSubgraph {  // partition.hpp:14-31 (host copy)
+    std::vector<NodeId> nodes;
+    std::vector<NodeId> global_to_local;
+    std::vector<Edge> edges;
+    std::vector<EdgeId> edge_global_ids;
+    std::vector<NodeId> local_degrees;
+    std::vector<std::int64_t> adj_offsets;  // int64: >2^31 CSR entries fit
+    std::vector<NodeId> adj_neighbors;
+    std::vector<EdgeId> adj_edge_ids;
+    NodeId num_local_nodes() const { return static_cast<NodeId>(nodes.size()); }
+};
+
+// sagecut::VertexCutPartition (partition.hpp:35-40), device resident.
+class VertexCutPartition {
+public:
+    VertexCutPartition() = default;
+    VertexCutPartition(const Graph& g, sc_vcut* h) : g_(&g), h_(h, &sc_vcut_destroy) {
+        check(sc_vcut_num_parts(h, &num_parts));
+    }
+    sc_vcut* get() const { return h_.get(); }
+    int num_parts = 0;
+    std::vector<int> edge_assignment() const {
+        std::vector<int> a(g_->num_edges());
+        check(sc_vcut_assignment(get(), a.data()));
+        return a;
+    }
+    PartSubgraph part(int i) const {
+        std::int64_t nl = 0, ne = 0;
+        check(sc_vcut_part_sizes(get(), i, &nl, &ne));
+        PartSubgraph s;
+        s.nodes.resize(nl);
+        s.global_to_local.resize(static_cast<std::size_t>(g_->num_nodes));
+        s.edges.resize(ne);
+        s.edge_global_ids.resize(ne);
+        s.local_degrees.resize(nl);
+        s.adj_offsets.resize(nl + 1);
+        s.adj_neighbors.resize(2 * ne);
+        s.adj_edge_ids.resize(2 * ne);
+        check(sc_vcut_part_copy(get(), i, s.nodes.data(), reinterpret_cast<std::int32_t*>(s.edges.data()),
+                                s.edge_global_ids.data(), s.local_degrees.data(), s.adj_offsets.data(),
+                                s.adj_neighbors.data(), s.adj_edge_ids.data(), s.global_to_local.data()));
+        return s;
+    }
+
+private:
+    const Graph* g_ = nullptr;
+    std::shared_ptr<sc_vcut> h_;
+};
+
+// partition.cpp:92-114, 22-90
+inline VertexCutPartition partition_random(const Graph& g, int num_parts, std::uint64_t seed) {
+    sc_vcut* h = nullptr;
+    check(sc_partition_random(g.get(), num_parts, seed, &h));
+    return VertexCutPartition(g, h);
+}
+inline VertexCutPartition partition_dbh(const Graph& g, int num_parts, std::uint64_t seed) {
+    sc_vcut* h = nullptr;
+    check(sc_partition_dbh(g.get(), num_parts, seed, &h));
+    return VertexCutPartition(g, h);
+}
+inline VertexCutPartition build_vertex_cut(const Graph& g, int num_parts, const std::vector<int>& edge_assignment) {
+    if (edge_assignment.size() != g.num_edges())
+        throw std::invalid_argument("edge assignment length does not match edge count");
+    sc_vcut* h = nullptr;
+    check(sc_build_vertex_cut(g.get(), num_parts, edge_assignment.data(), &h));
+    return VertexCutPartition(g, h);
+}
+
+struct ReplicationStats {  // partition.hpp:50-56
+    double rf = 0.0;
+    std::vector<int> per_node_rf;
+    double edge_balance = 0.0;
+    double node_balance = 0.0;
+    std::int64_t duplicated_nodes = 0;
+};
+inline ReplicationStats replication_stats(const VertexCutPartition& part, const Graph& g) {  // partition.cpp:310
+    ReplicationStats s;
+    s.per_node_rf.resize(static_cast<std::size_t>(g.num_nodes));
+    check(sc_replication_stats(part.get(), s.per_node_rf.data(), &s.rf, &s.edge_balance, &s.node_balance,
+                               &s.duplicated_nodes));
+    return s;
+}
+
+enum class ReweightScheme { dar, vanilla_inv, none };  // reweight.hpp:10
+struct NodeWeights {                                    // reweight.hpp:15-19
+    ReweightScheme scheme = ReweightScheme::none;
+    std::vector<std::vector<double>> per_part;
+};
+inline NodeWeights compute_weights(ReweightScheme scheme, const Graph& g, const VertexCutPartition& part) {
+    (void)g;
+    std::vector<std::int64_t> sizes(static_cast<std::size_t>(part.num_parts));
+    std::int64_t total = 0;
+    for (int i = 0; i < part.num_parts; ++i) {
+        check(sc_vcut_part_sizes(part.get(), i, &sizes[i], nullptr));
+        total += sizes[i];
+    }
+    std::vector<double> flat(static_cast<std::size_t>(total));
+    check(sc_compute_weights(part.get(), static_cast<int>(scheme), flat.data()));
+    NodeWeights w;
+    w.scheme = scheme;
+    std::int64_t off = 0;
+    for (auto sz : sizes) {
+        w.per_part.emplace_back(flat.begin() + off, flat.begin() + off + sz);
+        off += sz;
+    }
+    return w;
+}
+
+struct DropEdgeMaskSet {  // dropedge.hpp:13-18
+    int num_masks = 0;
+    double ratio = 0.0;
+    std::uint64_t seed = 0;
+    std::vector<std::vector<std::uint8_t>> masks;
+};
+inline DropEdgeMaskSet precompute_masks(Context& ctx, std::size_t num_edges, int num_masks, double ratio,
+                                        std::uint64_t seed) {  // dropedge.cpp:9
+    std::vector<std::uint8_t> flat(num_edges * static_cast<std::size_t>(num_masks > 0 ? num_masks : 0) + 1);
+    check(sc_precompute_masks(ctx.get(), static_cast<std::int64_t>(num_edges), num_masks, ratio, seed, flat.data()));
+    DropEdgeMaskSet s{num_masks, ratio, seed, {}};
+    for (int k = 0; k < num_masks; ++k)
+        s.masks.emplace_back(flat.begin() + k * num_edges, flat.begin() + (k + 1) * num_edges);
+    return s;
+}
+// select_mask for partition i at an epoch (trainer.hpp:261-266).
+inline int select_mask(std::uint64_t seed, std::uint64_t part, std::uint64_t epoch, int num_masks) {
+    if (num_masks < 1) throw std::invalid_argument("select_mask: need at least one mask");
+    return sc_select_mask(seed, part, epoch, num_masks);
+}
+
+enum class LossKind { softmax_ce, bce };  // nn.hpp:296
+
+struct TrainConfig {  // trainer.hpp:20-33
+    int layers = 2;
+    std::vector<int> hidden = {32};
+    int epochs = 100;
+    double learning_rate = 0.01;
+    LossKind loss = LossKind::softmax_ce;
+    ReweightScheme reweight = ReweightScheme::dar;
+    bool use_dropedge = false;
+    int dropedge_k = 10;
+    double drop_ratio = 0.5;
+    std::uint64_t seed = 0;
+    bool evaluate = true;       // per-epoch full-graph metrics (trainer.hpp:306)
+    bool deterministic = true;  // ascending-partition gradient sum
+};
+
+inline std::vector<int> resolved_hidden_dims(const TrainConfig& c) {  // trainer.cpp:12-19
+    if (c.layers == 0) return {};
+    if (c.hidden.size() == 1) return std::vector<int>(static_cast<std::size_t>(c.layers), c.hidden.front());
+    if (c.hidden.size() != static_cast<std::size_t>(c.layers))
+        throw std::invalid_argument("hidden dims must match layer count (or be a single value)");
+    return c.hidden;
+}
+
+struct EpochMetrics {  // trainer.hpp:38-46
+    int epoch = 0;
+    double train_loss = 0.0, train_metric = 0.0, val_metric = 0.0, test_metric = 0.0, grad_norm = 0.0;
+    std::uint64_t comm_floats = 0;
+};
+struct TrainResult {  // trainer.hpp:71-75 (model as the flat for_each_matrix vector)
+    std::vector<float> model;
+    std::vector<EpochMetrics> metrics;
+};
+
+// train_cofree (trainer.cpp:119 / trainer.hpp:202-313) on one GPU; for a
+// multi-GPU run create one sc_trainer per rank through the C ABI.
+inline TrainResult train_cofree(const Graph& g, const VertexCutPartition& part, const TrainConfig& c) {
+    if (c.epochs < 0) throw std::invalid_argument("epochs must be >= 0");
+    const std::vector<int> hidden = resolved_hidden_dims(c);
+    sc_train_config cfg{};
+    cfg.layers = static_cast<std::int32_t>(hidden.size());
+    cfg.hidden = hidden.data();
+    cfg.learning_rate = c.learning_rate;
+    cfg.loss = c.loss == LossKind::softmax_ce ? 0 : 1;
+    cfg.reweight = static_cast<std::int32_t>(c.reweight);
+    cfg.use_dropedge = c.use_dropedge ? 1 : 0;
+    cfg.dropedge_k = c.dropedge_k;
+    cfg.drop_ratio = c.drop_ratio;
+    cfg.seed = c.seed;
+    cfg.deterministic = c.deterministic ? 1 : 0;
+    cfg.gemm = 0;
+    sc_trainer* t = nullptr;
+    check(sc_trainer_create(g.context().get(), g.get(), part.get(), &cfg, 0, 1, &t));
+    std::unique_ptr<sc_trainer, sc_status (*)(sc_trainer*)> guard(t, &sc_trainer_destroy);
+    std::int64_t P = 0;
+    check(sc_trainer_param_count(t, &P));
+    TrainResult res;
+    for (int e = 0; e < c.epochs; ++e) {
+        EpochMetrics m;
+        m.epoch = e;
+        check(sc_trainer_step(t, e, &m.train_loss, &m.grad_norm));
+        if (c.evaluate) check(sc_trainer_evaluate(t, &m.train_metric, &m.val_metric, &m.test_metric));
+        m.comm_floats = static_cast<std::uint64_t>(part.num_parts) * static_cast<std::uint64_t>(P);
+        res.metrics.push_back(m);
+    }
+    res.model.resize(static_cast<std::size_t>(P));
+    check(sc_trainer_get_params(t, res.model.data()));
+    return res;
+}
+
+}  // namespace sagecut_b200
