@@ -482,7 +482,9 @@ sc_status sc_trainer_get_part_logits(sc_trainer* t, int32_t part, float* out) {
         REQUIRE_ARG(part >= 0 && part < t->p, "bad part index");
         REQUIRE_ARG(part % t->world == t->rank, "partition is not trained on this rank");
         set_device(t->ctx);
-        d2h(out, t->ps[part].logits.get(), t->ps[part].n * t->C, t->ctx->stream);
+        if (t->ps[part].n > 0)
+            SC_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * t->C, t->ps[part].logits.get(), sizeof(float) * t->Cp,
+                                      sizeof(float) * t->C, t->ps[part].n, cudaMemcpyDeviceToHost, t->ctx->stream));
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
     });
 }

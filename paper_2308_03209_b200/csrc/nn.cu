@@ -413,15 +413,15 @@ __device__ __forceinline__ double warp_sum_d(double x) {
     return x;
 }
 
-__global__ void softmax_ce_kernel(int64_t n, int32_t C, const float* __restrict__ logits,
+__global__ void softmax_ce_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
                                   const int32_t* __restrict__ labels, const int32_t* __restrict__ rows,
                                   const double* __restrict__ w, const float* __restrict__ scale, float* G,
                                   double* row_loss) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
-        const float* z = logits + r * C;
-        float* g = G + r * C;
+        const float* z = logits + r * ld;
+        float* g = G + r * ld;
         const double wr = w[r];
         if (wr == 0.0) {  // nn.hpp:330 rows with zero weight contribute nothing
             for (int32_t c = lane; c < C; c += 32) g[c] = 0.f;
@@ -442,14 +442,15 @@ __global__ void softmax_ce_kernel(int64_t n, int32_t C, const float* __restrict_
     }
 }
 
-__global__ void bce_kernel(int64_t n, int32_t C, const float* __restrict__ logits, const int32_t* __restrict__ labels,
+__global__ void bce_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
+                           const int32_t* __restrict__ labels,
                            const int32_t* __restrict__ rows, const double* __restrict__ w,
                            const float* __restrict__ scale, float* G, double* row_loss) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
-        const float* z = logits + r * C;
-        float* g = G + r * C;
+        const float* z = logits + r * ld;
+        float* g = G + r * ld;
         const double wr = w[r];
         if (wr == 0.0) {
             for (int32_t c = lane; c < C; c += 32) g[c] = 0.f;
@@ -545,13 +546,14 @@ __global__ void adam_kernel(int64_t P, float* theta, float* m1, float* m2, const
     }
 }
 
-__global__ void correct_kernel(int64_t n, int32_t C, const float* __restrict__ logits, const int32_t* __restrict__ labels,
+__global__ void correct_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
+                               const int32_t* __restrict__ labels,
                                const uint8_t* __restrict__ mask, unsigned long long* out) {
     unsigned long long corr = 0, tot = 0;
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
         if (!mask[r]) continue;
         ++tot;
-        const float* z = logits + r * C;
+        const float* z = logits + r * ld;
         int32_t best = 0;
         for (int32_t c = 1; c < C; ++c)
             if (z[c] > z[best]) best = c;
@@ -644,17 +646,17 @@ void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_
     SC_LAUNCH_CHECK();
     count_launch();
 }
-void softmax_ce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
+void softmax_ce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
                 const float* scale, float* G, double* row_loss, cudaStream_t s) {
     if (n <= 0) return;
-    softmax_ce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, logits, labels, rows, w, scale, G, row_loss);
+    softmax_ce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
     SC_LAUNCH_CHECK();
     count_launch();
 }
-void bce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
+void bce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
          const float* scale, float* G, double* row_loss, cudaStream_t s) {
     if (n <= 0) return;
-    bce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, logits, labels, rows, w, scale, G, row_loss);
+    bce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
     SC_LAUNCH_CHECK();
     count_launch();
 }
@@ -682,10 +684,10 @@ void adam(int64_t P, float* theta, float* m1, float* m2, const float* g, float b
     SC_LAUNCH_CHECK();
     count_launch();
 }
-void count_correct(int64_t n, int32_t C, const float* logits, const int32_t* labels, const uint8_t* mask,
+void count_correct(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const uint8_t* mask,
                    unsigned long long* out, cudaStream_t s) {
     if (n <= 0) return;
-    correct_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, C, logits, labels, mask, out);
+    correct_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, C, ld, logits, labels, mask, out);
     SC_LAUNCH_CHECK();
     count_launch();
 }

@@ -57,9 +57,10 @@ void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_
 
 // Loss + dloss/dlogits (nn.hpp:317-378). Rows with w == 0 get zero gradient.
 // row_loss[r] = w * (lse - z_y) (CE) in f64; scale[r] = (float)(w / normalizer).
-void softmax_ce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows,
+// ld: row stride of logits and G (>= C)
+void softmax_ce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows,
                 const double* w, const float* scale, float* G, double* row_loss, cudaStream_t s);
-void bce(int64_t n, int32_t C, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
+void bce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
          const float* scale, float* G, double* row_loss, cudaStream_t s);
 // Deterministic f64 sum of x[0..n), divided by `divisor`, into *out (fixed-shape two-pass reduction).
 void sum_f64(int64_t n, const double* x, double* partial, double* out, double divisor, cudaStream_t s);
@@ -75,7 +76,7 @@ void adam(int64_t P, float* theta, float* m1, float* m2, const float* g, float b
           float lr, float eps, const int* nonfinite, cudaStream_t s);
 
 // Accuracy of argmax(logits) over masked rows (trainer.cpp:66-97, multi-class).
-void count_correct(int64_t n, int32_t C, const float* logits, const int32_t* labels, const uint8_t* mask,
+void count_correct(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const uint8_t* mask,
                    unsigned long long* correct_and_total, cudaStream_t s);
 
 }  // namespace sc

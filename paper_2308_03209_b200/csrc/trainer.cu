@@ -97,6 +97,7 @@ void trainer_init(sc_trainer* t) {
     t->normalizer = static_cast<double>(g->train_count);
     t->d = g->dim;
     t->C = g->num_classes;
+    t->Cp = (t->C + 3) / 4 * 4;  // logits / dlogits row stride: 16-byte rows for the tensor-core kernels
     t->p = vc->p;
     // flat parameter layout (for_each_matrix order)
     int64_t off = 0;
@@ -149,7 +150,7 @@ void trainer_init(sc_trainer* t) {
         st.g_amax.alloc(1);
         SC_CUDA(cudaMemsetAsync(st.g_amax.get(), 0, sizeof(float), s));
         absmax(st.n, st.scale.get(), st.g_amax.get(), s);
-        st.logits.alloc(std::max<int64_t>(st.n * t->C, 1));
+        st.logits.alloc(std::max<int64_t>(st.n * t->Cp, 1));
         if (t->use_dropedge) {
             st.words = (st.nnz + 31) / 32;
             st.bits.alloc(std::max<int64_t>(st.words * t->K, 1));
@@ -219,7 +220,7 @@ void ensure_rows(sc_trainer* t, int64_t n) {
         t->MEAN[l].alloc(n * t->lay[l].H);
     }
     t->inv.alloc(n);
-    t->G.alloc(n * t->C);
+    t->G.alloc(n * t->Cp);
     t->dh.alloc(n * maxW);
     t->dh2.alloc(n * maxW);
     t->dmean.alloc(n * maxH);
@@ -284,8 +285,9 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
     }
     const MatA emb = t->L == 0 ? x0 : MatA{t->X[t->L].get(), t->E, nullptr, t->E};
     P.begin("gemm_head", 4.0 * n * (t->E + t->C), s);
-    gemm_nt(emb, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, logits, t->C, n, t->C, kEpiNone,
-            nullptr, s);
+    const float* emb_amax = t->L == 0 ? t->g->feat_amax.get() : t->amax_x(t->L);
+    t->tc.nt(t, emb, emb_amax, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, nullptr, logits,
+             t->Cp, n, t->C, kEpiNone, nullptr, nullptr);
     P.end(s);
 }
 
@@ -301,7 +303,7 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
     P.begin("wgrad", 4.0 * n * (t->C + t->E), s);
     const float* x0_amax = t->g->feat_amax.get();
     const float* emb_amax = t->L == 0 ? x0_amax : t->amax_x(t->L);
-    t->tc.tn(t, MatT{t->G.get(), t->C, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
+    t->tc.tn(t, MatT{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
              slot + t->head_off, t->E);
     P.end(s);
     float* dh = t->dh.get();
@@ -310,8 +312,8 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
     float* dh2_amax = t->amax_slot(sc_trainer::kSlotDh1);
     if (t->L == 0) return;
     P.begin("gemm_dgrad", 4.0 * n * (t->C + t->E), s);
-    gemm_nt(MatA{t->G.get(), t->C, nullptr, t->C}, MatB{t->theta.get() + t->head_off, t->E, true}, nullptr, nullptr, dh,
-            t->E, n, t->E, kEpiNone, nullptr, s, dh_amax);
+    t->tc.nt(t, MatA{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, MatB{t->theta.get() + t->head_off, t->E, true},
+             nullptr, nullptr, nullptr, dh, t->E, n, t->E, kEpiNone, nullptr, dh_amax);
     P.end(s);
     for (int l = t->L - 1; l >= 0; --l) {
         const LayerOff& lo = t->lay[l];
@@ -373,10 +375,10 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
     if (t->loss == 0)
-        softmax_ce(st.n, t->C, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
+        softmax_ce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
                    t->G.get(), t->row_loss.get(), s);
     else
-        bce(st.n, t->C, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(), t->G.get(),
+        bce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(), t->G.get(),
             t->row_loss.get(), s);
     sum_f64(st.n, t->row_loss.get(), t->red_partial.get(), t->part_loss.get() + i, t->normalizer, s);
     t->prof.end(s);
@@ -437,7 +439,7 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
     cudaStream_t s = t->ctx->stream;
     sc_graph* g = t->g;
     ensure_rows(t, g->n);
-    if (t->eval_logits.size() < size_t(g->n) * t->C) t->eval_logits.alloc(size_t(g->n) * t->C);
+    if (t->eval_logits.size() < size_t(g->n) * t->Cp) t->eval_logits.alloc(size_t(g->n) * t->Cp);
     const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr};
     const bool was = t->prof.enabled;
     t->prof.enabled = false;
@@ -445,9 +447,9 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
     t->prof.enabled = was;
     DevBuf<unsigned long long> cnt(6);
     SC_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-    count_correct(g->n, t->C, t->eval_logits.get(), g->labels.get(), g->train.get(), cnt.get(), s);
-    count_correct(g->n, t->C, t->eval_logits.get(), g->labels.get(), g->val.get(), cnt.get() + 2, s);
-    count_correct(g->n, t->C, t->eval_logits.get(), g->labels.get(), g->test.get(), cnt.get() + 4, s);
+    count_correct(g->n, t->C, t->Cp, t->eval_logits.get(), g->labels.get(), g->train.get(), cnt.get(), s);
+    count_correct(g->n, t->C, t->Cp, t->eval_logits.get(), g->labels.get(), g->val.get(), cnt.get() + 2, s);
+    count_correct(g->n, t->C, t->Cp, t->eval_logits.get(), g->labels.get(), g->test.get(), cnt.get() + 4, s);
     unsigned long long h[6];
     d2h(h, cnt.get(), 6, s);
     SC_CUDA(cudaStreamSynchronize(s));

@@ -69,7 +69,7 @@ struct sc_trainer {
     uint64_t seed = 0;
     int deterministic = 1, gemm_mode = 0;
     // dims
-    int d = 0, C = 0, E = 0, p = 0;
+    int d = 0, C = 0, Cp = 0, E = 0, p = 0;
     std::vector<sc::LayerOff> lay;
     int64_t head_off = 0, P = 0;
     double normalizer = 1.0;
