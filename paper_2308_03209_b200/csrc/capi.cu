@@ -160,6 +160,7 @@ sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, con
         h2d(g->test.get(), test, n, s);
         g->train_count = train_count;
         g->feat_amax.alloc(1);
+        ++g->feat_version;
         SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), s));
         absmax(n * dim, g->features.get(), g->feat_amax.get(), s);
         SC_CUDA(cudaStreamSynchronize(s));
@@ -171,6 +172,7 @@ sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_devic
         set_device(g->ctx);
         SC_CUDA(cudaMemcpyAsync(g->features.get(), features, sizeof(float) * size_t(g->n) * g->dim,
                                 is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->ctx->stream));
+        ++g->feat_version;
         SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), g->ctx->stream));
         absmax(int64_t(g->n) * g->dim, g->features.get(), g->feat_amax.get(), g->ctx->stream);
     });
@@ -581,21 +583,24 @@ sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A,
         set_device(ctx);
         cudaStream_t s = ctx->stream;
         const int32_t N2 = N2a + (B2 ? N2b : 0);
-        DevBuf<float> dA(std::max<int64_t>(M * N1, 1)), dB1(std::max<int64_t>(M * N2a, 1));
+        const int32_t lda = (N1 + 3) / 4 * 4;  // 16-byte rows, as the trainer's buffers are
+        DevBuf<float> dA(std::max<int64_t>(M * lda, 1)), dB1(std::max<int64_t>(M * N2a, 1));
         DevBuf<float> dB2(std::max<int64_t>(B2 ? b2_rows * N2b : 1, 1)), dC(int64_t(N1) * N2);
         DevBuf<int32_t> dR(std::max<int64_t>(rows2 ? M : 1, 1));
-        h2d(dA.get(), A, M * N1, s);
+        if (M > 0)
+            SC_CUDA(cudaMemcpy2DAsync(dA.get(), sizeof(float) * lda, A, sizeof(float) * N1, sizeof(float) * N1, M,
+                                      cudaMemcpyHostToDevice, s));
         h2d(dB1.get(), B1, M * N2a, s);
         if (B2) h2d(dB2.get(), B2, b2_rows * N2b, s);
         if (rows2) h2d(dR.get(), rows2, M, s);
-        const MatT a{dA.get(), N1, nullptr, N1}, b1{dB1.get(), N2a, nullptr, N2a};
+        const MatT a{dA.get(), lda, nullptr, N1}, b1{dB1.get(), N2a, nullptr, N2a};
         const MatT b2{dB2.get(), N2b, rows2 ? dR.get() : nullptr, N2b};
         const int64_t wsf = std::max<int64_t>(gemm_tn_workspace_floats(N1, N2), int64_t(256) * N1 * N2);
         DevBuf<float> ws(wsf);
         if (mode == 0) {
             DevBuf<float> am(3);
             SC_CUDA(cudaMemsetAsync(am.get(), 0, 3 * sizeof(float), s));
-            absmax(M * N1, dA.get(), am.get(), s);
+            absmax(M * lda, dA.get(), am.get(), s);
             absmax(M * N2a, dB1.get(), am.get() + 1, s);
             if (B2) absmax(b2_rows * N2b, dB2.get(), am.get() + 2, s);
             gemm_tn_f16x3(a, am.get(), b1, am.get() + 1, B2 ? &b2 : nullptr, am.get() + 2, M, dC.get(), N2, ws.get(),

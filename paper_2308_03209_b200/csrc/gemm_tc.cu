@@ -1,31 +1,35 @@
 // gemm_tc.cu — fp32-grade GEMMs on the 5th-gen tensor cores (tcgen05, sm_100a).
 //
-//   C[M x N] = A1 op(B1) (+ A2 op(B2)),  M huge (partition rows), N <= 256.
+//   NT:  C[M x N] = A1 op(B1) (+ A2 op(B2)), M huge (partition rows), N <= 256
+//        (forward msg / update / head, backward dgrad)
+//   TN:  C[N1 x N2] = A^T [B1 | B2], K = M rows (weight gradients)
 //
 // Precision ("fp16x3"). The reference's f32 mode needs ~fp32 products: its
 // parity bar is 1e-4 relative after 5 Adam steps, and Adam amplifies small
-// gradient errors (sign flips of near-zero components move a parameter by
-// 2*lr). Each fp32 operand is scaled by a power of two s (exact) so that its
+// gradient errors. Each fp32 operand is scaled by a power of two (exact) so its
 // |max| lands in [2^14, 2^15), then split into fp16 hi = rn(x s) and
-// lo = rn(x s - hi): |x s - hi - lo| <= 2^-22 |x s|. The product is
+// lo = rn(x s - hi) (|x s - hi - lo| <= 2^-22 |x s|); the product is
 // hi*hi + hi*lo + lo*hi (three kind::f16 MMAs at the full 16-bit tensor rate,
-// fp32 accumulation in TMEM); the dropped lo*lo term is <= 2^-22 relative.
-// Measured: ~2e-7 relative Frobenius error vs fp64 (bf16 splitting gave 4.5e-6,
-// which compounds to 2.5e-4 in 5-step gradients). The scales come from |max|
-// values the producing kernels reduce in their epilogues (no host sync).
+// fp32 accumulation in TMEM). Measured ~1e-6 relative vs fp64 (bf16 splitting:
+// 4.5e-6, which compounded to 2.5e-4 in 5-step gradients). The |max| values
+// come from the kernels that produced each operand (no host sync).
 //
-// Kernel structure (persistent, one CTA per SM, 416 threads):
-//   warps 0-7  producers: A tile (128 rows x 64 k) fp32 from HBM (optionally
-//              row-gathered), scaled + split to fp16 hi/lo, stored in the
-//              canonical K-major SWIZZLE_128B smem layout; thread 0 also issues
-//              one cp.async.bulk of the pre-split, pre-swizzled B k-block image.
-//              Loads run two pipeline iterations ahead in registers.
-//   warp 12    TMEM allocator + single-thread MMA issuer (tcgen05.mma,
-//              tcgen05.commit -> mbarriers).
-//   warps 8-11 epilogue: tcgen05.ld accumulator rows -> unscale, ReLU /
-//              row-scale, |max| -> global fp32 rows. Two TMEM accumulators
-//              (2 x 256 columns) so tile t's epilogue overlaps tile t+1.
+// Data movement (both kernels, persistent/one CTA per SM, 448 threads):
+//   warp 13    loader: one cp.async.bulk (TMA bulk copy) per operand row slice,
+//              HBM -> fp32 staging ring in shared memory (optionally through a
+//              row gather, e.g. partition rows -> global feature rows)
+//   warps 0-7  converters: staging fp32 -> scaled fp16 hi/lo tiles in the
+//              canonical SWIZZLE_64B K-major (NT) or SWIZZLE_128B MN-major (TN)
+//              layout; NT thread 0 also bulk-copies the pre-split weight image
+//   warp 12    TMEM allocator + single-thread MMA issuer (tcgen05.mma/commit)
+//   warps 8-11 epilogue: tcgen05.ld -> unscale / ReLU / row-scale / |max| ->
+//              smem transpose -> coalesced stores (NT), or periodic TMEM drains
+//              into an fp32 split-K partial (TN)
+// Two TMEM accumulators (2 x 256 columns) let one tile's epilogue overlap the
+// next tile's main loop.
+#include <cuda.h>
 #include <cuda_fp16.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstring>
@@ -37,39 +41,53 @@
 namespace sc {
 namespace tc {
 
-constexpr int kBM = 128;          // UMMA M (cta_group::1)
-constexpr int kBK = 64;           // k per stage: 64 fp16 = 128 B = one SW128 row
-constexpr int kStages = 2;
+constexpr int kBM = 128;  // UMMA M (cta_group::1)
 constexpr int kMaxN = 256;
-constexpr int kProducerWarps = 8; // warps 0-7: operand producers
-constexpr int kProducers = kProducerWarps * 32;
-constexpr int kEpilogue = 128;    // warps 8-11: epilogue (warp % 4 selects the TMEM lane quarter)
-constexpr int kMmaWarp = kProducerWarps + 4;  // warp 12: TMEM allocator + MMA issuer
-constexpr int kThreads = kProducers + kEpilogue + 32;
-constexpr int kATile = kBM * 128;        // bytes of one (hi or lo) A tile
-// The NT (activation x weight) kernel streams 32-deep k-stages in the
-// SWIZZLE_64B layout (64 B rows) so four stages fit: the weight k-block image
-// arrives by bulk copy from L2 and needs the deeper pipeline to stay hidden.
+constexpr int kConvWarps = 8;
+constexpr int kConv = kConvWarps * 32;  // converter threads (warps 0-7)
+constexpr int kEpilogue = 128;          // warps 8-11 (warp % 4 = TMEM lane quarter)
+constexpr int kMmaWarp = 12;
+constexpr int kLoadWarp = 13;
+constexpr int kThreads = 14 * 32;
+
+// NT: 32-deep k-stages, fp16 SW64 tiles (64 B rows)
 constexpr int kNtBK = 32;
-constexpr int kNtStages = 4;
-constexpr int kNtATile = kBM * 64;
-constexpr int kNtBTileMax = kMaxN * 64;
-constexpr int kNtStageBytes = 2 * kNtATile + 2 * kNtBTileMax;
-constexpr int kNtSmemBytes = kNtStages * kNtStageBytes + 1024 + 256 + 4 * 32 * 33 * 4;  // + epilogue staging
-constexpr int kNtRing = 4;  // producer register ring depth (pipeline iterations in flight)
+constexpr int kNtStages = 3;                          // MMA operand stages
+constexpr int kNtStg = 3;                             // fp32 staging stages
+constexpr int kNtATile = kBM * 64;                    // one (hi or lo) A tile
+constexpr int kNtBTileMax = kMaxN * 64;               // one (hi or lo) B tile
+constexpr int kNtStage = 2 * kNtATile + 2 * kNtBTileMax;
+constexpr int kNtStgBytes = kBM * kNtBK * 4;          // 128 rows x 32 fp32
+constexpr int kNtEpiBytes = 4 * 32 * 33 * 4;          // epilogue transpose buffers
+constexpr int kNtBarOff = kNtStages * kNtStage + kNtStg * kNtStgBytes + kNtEpiBytes;
+constexpr int kNtSmemBytes = kNtBarOff + 256 + 1024;
+
+// TN: 32-row stages, fp16 MN-major SW128 tiles
+constexpr int kTnBK = 32;
+constexpr int kTnStages = 2;
+constexpr int kTnStg = 2;
+constexpr int kTnATile = kBM * kTnBK * 2;             // 128 cols x 32 rows fp16 = 8 KB
+constexpr int kTnBTile = kMaxN * kTnBK * 2;           // 256 cols x 32 rows fp16 = 16 KB
+constexpr int kTnStage = 2 * kTnATile + 2 * kTnBTile;
+constexpr int kTnStgA = kTnBK * kBM * 4;              // 32 rows x 128 fp32 = 16 KB
+constexpr int kTnStgB = kTnBK * kMaxN * 4;            // 32 rows x 256 fp32 = 32 KB
+constexpr int kTnBarOff = kTnStages * kTnStage + kTnStg * (kTnStgA + kTnStgB);
+constexpr int kTnSmemBytes = kTnBarOff + 256 + 1024;
+constexpr int kChunkKb = 32;                          // 1024 rows per TMEM accumulation (TN)
 
 struct Src {
+    CUtensorMap tmap;     // 2D map over A (box 32 k x 128 rows, fp32, OOB -> 0); unused when gathered
     const float* a;
-    const int32_t* rows;     // optional gather
+    const int32_t* rows;  // optional gather (per-row bulk copies)
     int64_t lda;
-    int32_t K;               // valid k
-    int32_t kblocks;         // ceil(K / 64)
-    const uint8_t* bimg;     // kblocks x [hi tile | lo tile], each n_pad x 64 B (32 k, SW64)
-    const float* amax_a;     // |A| max (device scalar)
-    const int32_t* bexp;     // power-of-two exponent B was scaled by (device scalar)
+    int32_t K;            // valid k (multiple of 4)
+    int32_t kblocks;      // ceil(K / 32)
+    const uint8_t* bimg;  // kblocks x [hi tile | lo tile], each n_pad x 64 B (32 k, SW64)
+    const float* amax_a;  // max|A| (device scalar)
+    const int32_t* bexp;  // power-of-two exponent B was scaled by (device scalar)
 };
 
-struct Params {
+struct alignas(64) Params {
     Src src[2];
     int nsrc;
     int64_t M;
@@ -115,15 +133,6 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// K-major, SWIZZLE_128B shared-memory matrix descriptor (tcgen05 format):
-// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46)
-// = 1024 B between 8-row core groups, version 1 at [46,48), swizzle mode 2
-// (128 B) at [61,64).
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
-    return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(1) << 16) |
-           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
-           (static_cast<uint64_t>(2) << 61);
-}
 // Instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A f16 (7-9 = 0),
 // B f16 (10-12 = 0), both K-major, N>>3 at [17,23), M>>4 at [24,29).
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
@@ -182,18 +191,37 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
 __host__ __device__ __forceinline__ uint32_t sw64_off(uint32_t row, uint32_t c) {
     return (row >> 3) * 512 + (row & 7) * 64 + ((c ^ ((row >> 1) & 3)) << 4);
 }
-// Byte offset of (row, 16-byte chunk c) in a K-major SW128 tile.
-__host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t c) {
-    return (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4);
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
 }
-
-// ---- the kernel ----------------------------------------------------------------
-// Producer-side operand loads for one pipeline iteration (tile, source, k-block):
-// every load of the stage is issued before any is consumed (4 chunks of 8 fp32
-// per thread), and the loop keeps two iterations of loads in flight.
-struct NtLoad {
-    float4 x[2][2];
-};
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void split8_store(const float4& x0, const float4& x1, float s, uint8_t* hi_base,
+                                             uint8_t* lo_base, uint32_t off) {
+    uint4 hi, lo;
+    split2(x0.x, x0.y, s, hi.x, lo.x);
+    split2(x0.z, x0.w, s, hi.y, lo.y);
+    split2(x1.x, x1.y, s, hi.z, lo.z);
+    split2(x1.z, x1.w, s, hi.w, lo.w);
+    *reinterpret_cast<uint4*>(hi_base + off) = hi;
+    *reinterpret_cast<uint4*>(lo_base + off) = lo;
+}
+// Zero the elements of an 8-wide chunk at or beyond `valid` (0..8).
+__device__ __forceinline__ void mask8(float4& x0, float4& x1, int valid) {
+    if (valid >= 8) return;
+    float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        if (q >= valid) v[q] = 0.f;
+    x0 = make_float4(v[0], v[1], v[2], v[3]);
+    x1 = make_float4(v[4], v[5], v[6], v[7]);
+}
 
 __device__ __forceinline__ void nt_decode(const Params& p, int64_t it, int kb_total, int64_t& m0, int& src,
                                           int& kb) {
@@ -208,68 +236,19 @@ __device__ __forceinline__ void nt_decode(const Params& p, int64_t it, int kb_to
     kb = kbg;
 }
 
-__device__ __forceinline__ void nt_issue(const Params& p, int tid, int64_t it, int64_t n_it, int kb_total,
-                                         NtLoad& L) {
-    if (it >= n_it) return;
-    int64_t m0;
-    int src, kb;
-    nt_decode(p, it, kb_total, m0, src, kb);
-    const Src& S = p.src[src];
-    const int k0 = kb * kNtBK;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int idx = tid + j * kProducers;
-        const int r = idx >> 2, c = idx & 3;
-        const int64_t row = m0 + r;
-        const int k = k0 + c * 8;
-        if (row < p.M && k + 8 <= S.K) {
-            const int64_t grow = S.rows ? __ldg(S.rows + row) : row;
-            const float4* src4 = reinterpret_cast<const float4*>(S.a + grow * S.lda + k);
-            L.x[j][0] = __ldg(src4);
-            L.x[j][1] = __ldg(src4 + 1);
-        } else {
-            float v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = 0.f;
-            if (row < p.M && k < S.K) {
-                const int64_t grow = S.rows ? __ldg(S.rows + row) : row;
-                const float* src1 = S.a + grow * S.lda;
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (k + q < S.K) v[q] = __ldg(src1 + k + q);
-            }
-            L.x[j][0] = make_float4(v[0], v[1], v[2], v[3]);
-            L.x[j][1] = make_float4(v[4], v[5], v[6], v[7]);
-        }
-    }
-}
-
-__device__ __forceinline__ void nt_store(int tid, float sa, const NtLoad& L, uint8_t* a_hi, uint8_t* a_lo) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int idx = tid + j * kProducers;
-        const int r = idx >> 2, c = idx & 3;
-        uint4 hi, lo;
-        split2(L.x[j][0].x, L.x[j][0].y, sa, hi.x, lo.x);
-        split2(L.x[j][0].z, L.x[j][0].w, sa, hi.y, lo.y);
-        split2(L.x[j][1].x, L.x[j][1].y, sa, hi.z, lo.z);
-        split2(L.x[j][1].z, L.x[j][1].w, sa, hi.w, lo.w);
-        const uint32_t off = sw64_off(r, c);
-        *reinterpret_cast<uint4*>(a_hi + off) = hi;
-        *reinterpret_cast<uint4*>(a_lo + off) = lo;
-    }
-}
-
 __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
-    extern __shared__ uint8_t smem_raw[];
-    // align to 1024 B with pointer arithmetic on the shared array (keeps the shared address space)
+    extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kNtStages * kNtStageBytes);
-    uint64_t* full = bars;                      // [kNtStages]
-    uint64_t* empty = bars + kNtStages;           // [kNtStages]
-    uint64_t* tfull = bars + 2 * kNtStages;       // [2]
-    uint64_t* tempty = bars + 2 * kNtStages + 2;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kNtStages + 4);
+    uint8_t* stg_base = smem + kNtStages * kNtStage;
+    float* epi_base = reinterpret_cast<float*>(stg_base + kNtStg * kNtStgBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kNtBarOff);
+    uint64_t* full = bars;                              // [kNtStages] converters -> MMA
+    uint64_t* empty = full + kNtStages;                 // [kNtStages] MMA -> converters
+    uint64_t* sfull = empty + kNtStages;                // [kNtStg] loader (tx) -> converters
+    uint64_t* sempty = sfull + kNtStg;                  // [kNtStg] converters -> loader
+    uint64_t* tfull = sempty + kNtStg;                  // [2] MMA -> epilogue
+    uint64_t* tempty = tfull + 2;                       // [2] epilogue -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t btile = static_cast<uint32_t>(p.n_pad) * 64u;
@@ -286,8 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
     if (warp == kMmaWarp) {
         if (lane == 0) {
             for (int s = 0; s < kNtStages; ++s) {
-                mbar_init(&full[s], kProducers);
+                mbar_init(&full[s], kConv);
                 mbar_init(&empty[s], 1);
+            }
+            for (int s = 0; s < kNtStg; ++s) {
+                mbar_init(&sfull[s], 1);
+                mbar_init(&sempty[s], kConv);
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
@@ -308,40 +291,83 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
     int kb_total = 0;
     for (int s = 0; s < p.nsrc; ++s) kb_total += p.src[s].kblocks;
     const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int64_t n_it = my_tiles * kb_total;
 
-    if (warp < kProducerWarps) {
-        // ================= producers =================
-        const int tid = threadIdx.x;
-        const int64_t n_it = my_tiles * kb_total;
-        const float sa0 = ldexpf(1.f, kt - kb_exp[0]), sa1 = ldexpf(1.f, kt - kb_exp[1]);
-        NtLoad L[kNtRing];
-#pragma unroll
-        for (int d = 0; d < kNtRing; ++d) nt_issue(p, tid, d, n_it, kb_total, L[d]);
-        auto produce = [&](int64_t it, const NtLoad& L) {
-            const int stage = static_cast<int>(it % kNtStages);
-            const uint32_t phase = static_cast<uint32_t>((it / kNtStages) & 1);
+    if (warp == kLoadWarp) {
+        // ================= loader: row slices HBM -> fp32 staging =================
+        int64_t grow[4] = {0, 0, 0, 0};  // rows lane + 32 j of the current tile (gathered)
+        for (int64_t it = 0; it < n_it; ++it) {
+            const int slot = static_cast<int>(it % kNtStg);
             int64_t m0;
             int src, kb;
             nt_decode(p, it, kb_total, m0, src, kb);
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* st = smem + stage * kNtStageBytes;
-            if (tid == 0) {
-                mbar_expect_tx(&full[stage], 2 * btile);
-                bulk_g2s(st + 2 * kNtATile, p.src[src].bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile,
-                         &full[stage]);
-            }
-            nt_store(tid, src ? sa1 : sa0, L, st, st + kNtATile);
-            fence_proxy_async();
-            mbar_arrive(&full[stage]);
-        };
-        for (int64_t it = 0; it < n_it; it += kNtRing) {
+            const Src& S = p.src[src];
+            if (kb == 0 && S.rows) {  // new tile or source: gathered global rows of this tile
 #pragma unroll
-            for (int d = 0; d < kNtRing; ++d) {
-                if (it + d < n_it) {
-                    produce(it + d, L[d]);
-                    nt_issue(p, tid, it + d + kNtRing, n_it, kb_total, L[d]);
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t row = m0 + lane + 32 * j;
+                    grow[j] = row < p.M ? (S.rows ? static_cast<int64_t>(__ldg(S.rows + row)) : row) : -1;
                 }
             }
+            const int k0 = kb * kNtBK;
+            uint8_t* dst = stg_base + slot * kNtStgBytes;
+            mbar_wait(&sempty[slot], ((it / kNtStg) & 1) ^ 1);
+            if (!S.rows) {
+                // one 2D TMA per stage: box 32 k x 128 rows; out-of-range rows / k are zero-filled
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&sfull[slot], kNtStgBytes);
+                    tma_load_2d(dst, &S.tmap, k0, static_cast<int32_t>(m0), &sfull[slot]);
+                }
+            } else {
+                // gathered rows: one bulk copy per row slice (whole 16 B units; rows are padded to
+                // ld >= round_up(K, 4); the tail is masked by the converters)
+                const uint32_t bytes = static_cast<uint32_t>(min(kNtBK, ((S.K + 3) & ~3) - k0)) * 4u;
+                const int64_t nvalid = p.M - m0 < kBM ? p.M - m0 : kBM;
+                if (lane == 0) mbar_arrive_expect_tx(&sfull[slot], static_cast<uint32_t>(nvalid) * bytes);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (grow[j] >= 0)
+                        bulk_g2s(dst + (lane + 32 * j) * (kNtBK * 4), S.a + grow[j] * S.lda + k0, bytes, &sfull[slot]);
+            }
+        }
+    } else if (warp < kConvWarps) {
+        // ================= converters: staging fp32 -> scaled fp16 hi/lo (SW64) =================
+        const int tid = threadIdx.x;
+        const float sa0 = ldexpf(1.f, kt - kb_exp[0]), sa1 = ldexpf(1.f, kt - kb_exp[1]);
+        for (int64_t it = 0; it < n_it; ++it) {
+            const int stage = static_cast<int>(it % kNtStages), slot = static_cast<int>(it % kNtStg);
+            int64_t m0;
+            int src, kb;
+            nt_decode(p, it, kb_total, m0, src, kb);
+            const Src& S = p.src[src];
+            const int k0 = kb * kNtBK;
+            uint8_t* st = smem + stage * kNtStage;
+            const uint8_t* sg = stg_base + slot * kNtStgBytes;
+            mbar_wait(&empty[stage], ((it / kNtStages) & 1) ^ 1);
+            if (tid == 0) {
+                mbar_expect_tx(&full[stage], 2 * btile);
+                bulk_g2s(st + 2 * kNtATile, S.bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile, &full[stage]);
+            }
+            mbar_wait(&sfull[slot], (it / kNtStg) & 1);
+            const float sa = src ? sa1 : sa0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int idx = tid + j * kConv;
+                const int r = idx >> 2, c = idx & 3;
+                float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+                const int valid = m0 + r < p.M ? min(8, S.K - (k0 + c * 8)) : 0;
+                if (valid > 0) {
+                    const float4* q = reinterpret_cast<const float4*>(sg + r * (kNtBK * 4) + c * 32);
+                    x0 = q[0];
+                    x1 = q[1];
+                    mask8(x0, x1, valid);
+                }
+                split8_store(x0, x1, sa, st, st + kNtATile, sw64_off(r, c));
+            }
+            fence_proxy_async();
+            mbar_arrive(&full[stage]);
+            mbar_arrive(&sempty[slot]);
         }
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
@@ -357,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
                 mbar_wait(&full[stage], (it / kNtStages) & 1);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint8_t* st = smem + stage * kNtStageBytes;
+                    const uint8_t* st = smem + stage * kNtStage;
                     const uint64_t ahi = desc_sw64(smem_u32(st)), alo = desc_sw64(smem_u32(st + kNtATile));
                     const uint64_t bhi = desc_sw64(smem_u32(st + 2 * kNtATile));
                     const uint64_t blo = desc_sw64(smem_u32(st + 2 * kNtATile + btile));
@@ -378,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
         // ================= epilogue (warps 8-11) =================
         const int ew = warp & 3;  // TMEM lanes 32*ew .. 32*ew+31
         const float unscale = ldexpf(1.f, -kt);
-        float* stg = reinterpret_cast<float*>(smem + kNtStages * kNtStageBytes + 256) + ew * (32 * 33);
+        float* stg = epi_base + ew * (32 * 33);
         float amx = 0.f;
         uint32_t t = 0;
         for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
@@ -479,16 +505,13 @@ __global__ void __launch_bounds__(1024) prep_b_kernel(const float* __restrict__ 
 // Weight-gradient GEMM:  C[N1 x N2] = A^T Bcat,  A [M x N1], Bcat = [B1 | B2]
 // [M x N2], K = M (partition rows, millions). The MMA's "M" is N1 (tiles of
 // 128), its "N" is N2 (tiles of <= 256), its K runs over rows. Row-major
-// activations are MN-major operands, so the producers copy rows straight
-// into the MN-major SWIZZLE_128B layout (scaled + fp16x3 split on the way).
-// Split-K over rows; inside a CTA the TMEM accumulator is drained every
-// kChunkKb k-blocks into an fp32 partial (the tensor-core accumulate is not
+// activations are MN-major operands, so row slices are bulk-copied straight to
+// staging and converted into the MN-major SWIZZLE_128B layout. Split-K over
+// rows; inside a CTA the TMEM accumulator is drained every kChunkKb k-blocks
+// (1024 rows) into an fp32 partial (the tensor-core accumulate is not
 // round-to-nearest, so long K runs in TMEM would bias the sum); splits are
 // summed in a fixed order afterwards (deterministic).
 // =============================================================================
-constexpr int kChunkKb = 16;                 // 1024 rows per TMEM accumulation
-constexpr int kTnBTile = kMaxN * 128;        // bytes of one B' (hi or lo) tile: 256 cols x 64 k x 2 B
-
 struct TnB {
     const float* ptr;
     int64_t ld;
@@ -509,11 +532,10 @@ struct TnParams {
     int64_t rows_per_split;
     int32_t tiles1, tiles2;
     float* ws;       // [splits][N1][N2] fp32 partials
-    uint32_t lbo, sbo;  // MN-major descriptor strides (bytes)
 };
 
 // MN-major SW128 descriptor: LBO = stride between 64-element MN atoms,
-// SBO = stride between 8-row K groups.
+// SBO = stride between 8-row K groups (validated against fp64 in tests).
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(lbo >> 4) << 16) |
            (static_cast<uint64_t>(sbo >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
@@ -524,126 +546,52 @@ __host__ __device__ constexpr uint32_t idesc_f16_mn(int M, int N) {
     return (1u << 4) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
            (static_cast<uint32_t>(M >> 4) << 24);
 }
-// Byte offset of (mn, k) 16-byte chunk (8 consecutive mn at one k) in an
-// MN-major SW128 tile laid out [mn_atom][k_atom][8 k rows][128 B]:
-// mn atom = 64 elements, k atom = 8 rows, each atom 1024 B.
-__device__ __forceinline__ uint32_t mn_sw128_off(uint32_t mn, uint32_t k) {
-    return (mn >> 6) * 8192 + (k >> 3) * 1024 + (k & 7) * 128 + ((((mn & 63) >> 3) ^ (k & 7)) << 4);
-}
-
-__device__ __forceinline__ float tn_load(const TnB& b, int64_t row, int32_t c) {
-    const int64_t g = b.rows ? b.rows[row] : row;
-    return __ldg(b.ptr + g * b.ld + c);
-}
-
-// TN producer loads for one 64-row k-block: A' (4 chunks of 8 columns per
-// thread) and B' (up to 8 chunks), all issued before any is consumed.
-struct TnLoad {
-    float4 a[4][2];
-    float4 b[8][2];
-};
-
-__device__ __forceinline__ void tn_load8(const float* base, int64_t ld, const int32_t* rows, int64_t row, int32_t c,
-                                         int32_t cols, bool row_ok, float4 (&out)[2]) {
-    if (row_ok && c + 8 <= cols && (ld & 3) == 0 && (c & 3) == 0) {
-        const int64_t g = rows ? __ldg(rows + row) : row;
-        const float4* s4 = reinterpret_cast<const float4*>(base + g * ld + c);
-        out[0] = __ldg(s4);
-        out[1] = __ldg(s4 + 1);
-    } else {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = 0.f;
-        if (row_ok) {
-            const int64_t g = rows ? __ldg(rows + row) : row;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (c + q < cols) v[q] = __ldg(base + g * ld + c + q);
-        }
-        out[0] = make_float4(v[0], v[1], v[2], v[3]);
-        out[1] = make_float4(v[4], v[5], v[6], v[7]);
-    }
-}
-
-__device__ __forceinline__ void tn_issue(const TnParams& p, int tid, int kb, int kblocks, int64_t r0, int64_t r1,
-                                         int32_t n10, int32_t n20, int bch, TnLoad& L) {
-    if (kb >= kblocks) return;
-    const int64_t k0 = r0 + int64_t(kb) * kBK;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int idx = tid + j * kProducers;
-        const int kr = idx >> 4, ch = idx & 15;
-        tn_load8(p.a, p.lda, nullptr, k0 + kr, n10 + ch * 8, p.N1, k0 + kr < r1, L.a[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int idx = tid + j * kProducers;
-        if (idx >= 64 * bch) break;
-        const int kr = idx / bch, ch = idx % bch;
-        const int64_t row = k0 + kr;
-        const int32_t c = n20 + ch * 8;
-        const bool ok = row < r1;
-        if (c + 8 <= p.n2a) {
-            tn_load8(p.b[0].ptr, p.b[0].ld, p.b[0].rows, row, c, p.n2a, ok, L.b[j]);
-        } else if (c >= p.n2a) {
-            tn_load8(p.b[1].ptr, p.b[1].ld, p.b[1].rows, row, c - p.n2a, p.N2 - p.n2a, ok, L.b[j]);
-        } else {  // chunk straddles B1 | B2
-            float v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int32_t cq = c + q;
-                v[q] = (!ok || cq >= p.N2) ? 0.f : cq < p.n2a ? tn_load(p.b[0], row, cq) : tn_load(p.b[1], row, cq - p.n2a);
-            }
-            L.b[j][0] = make_float4(v[0], v[1], v[2], v[3]);
-            L.b[j][1] = make_float4(v[4], v[5], v[6], v[7]);
-        }
-    }
-}
-
-__device__ __forceinline__ void store_chunk(const float4 (&x)[2], float s, uint8_t* hi_base, uint8_t* lo_base,
-                                            uint32_t off) {
-    uint4 hi, lo;
-    split2(x[0].x, x[0].y, s, hi.x, lo.x);
-    split2(x[0].z, x[0].w, s, hi.y, lo.y);
-    split2(x[1].x, x[1].y, s, hi.z, lo.z);
-    split2(x[1].z, x[1].w, s, hi.w, lo.w);
-    *reinterpret_cast<uint4*>(hi_base + off) = hi;
-    *reinterpret_cast<uint4*>(lo_base + off) = lo;
+// Byte offset of the 16-byte chunk (8 consecutive mn at one k) in an MN-major
+// SW128 tile of 32 k rows laid out [mn_atom][k_atom(4)][8 k rows][128 B].
+constexpr uint32_t kTnLbo = 4 * 1024;  // MN atom stride
+constexpr uint32_t kTnSbo = 1024;      // K group stride
+__device__ __forceinline__ uint32_t mn_off(uint32_t mn, uint32_t k) {
+    return (mn >> 6) * kTnLbo + (k >> 3) * kTnSbo + (k & 7) * 128 + ((((mn & 63) >> 3) ^ (k & 7)) << 4);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    // align to 1024 B with pointer arithmetic on the shared array (keeps the shared address space)
+    extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    constexpr int kTnStage = 2 * kATile + 2 * kTnBTile;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTnStage);
+    uint8_t* stg_base = smem + kTnStages * kTnStage;  // kTnStg x [A' rows | B' rows]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTnBarOff);
     uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
-    uint64_t* tempty = bars + 2 * kStages + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    uint64_t* empty = full + kTnStages;
+    uint64_t* sfull = empty + kTnStages;
+    uint64_t* sempty = sfull + kTnStg;
+    uint64_t* tfull = sempty + kTnStg;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     const int tiles = p.tiles1 * p.tiles2;
     const int split = blockIdx.x / tiles, tile = blockIdx.x % tiles;
     const int32_t n10 = (tile / p.tiles2) * kBM, n20 = (tile % p.tiles2) * kMaxN;
-    const int32_t nb = min(kMaxN, p.N2 - n20);
+    const int32_t na = min(kBM, p.N1 - n10);    // valid A' columns
+    const int32_t nb = min(kMaxN, p.N2 - n20);  // valid B' columns
     const int32_t nb_pad = (nb + 15) / 16 * 16;
     const int64_t r0 = int64_t(split) * p.rows_per_split;
     const int64_t r1 = min(p.M, r0 + p.rows_per_split);
-    const int kblocks = r1 > r0 ? static_cast<int>((r1 - r0 + kBK - 1) / kBK) : 0;
+    const int kblocks = r1 > r0 ? static_cast<int>((r1 - r0 + kTnBK - 1) / kTnBK) : 0;
     const int nchunks = (kblocks + kChunkKb - 1) / kChunkKb;
 
     const int ka = scale_exp(*p.amax_a);
     int kbx = scale_exp(*p.b[0].amax);
     if (p.nb > 1) kbx = min(kbx, scale_exp(*p.b[1].amax));
-    const float sa = ldexpf(1.f, ka), sb = ldexpf(1.f, kbx);
 
     if (warp == kMmaWarp) {
         if (lane == 0) {
-            for (int s = 0; s < kStages; ++s) {
-                mbar_init(&full[s], kProducers);
+            for (int s = 0; s < kTnStages; ++s) {
+                mbar_init(&full[s], kConv);
                 mbar_init(&empty[s], 1);
+            }
+            for (int s = 0; s < kTnStg; ++s) {
+                mbar_init(&sfull[s], 1);
+                mbar_init(&sempty[s], kConv);
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
@@ -661,37 +609,99 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp < kProducerWarps) {
-        // ===== producers: rows of A[:, n10:n10+128] and Bcat[:, n20:n20+nb_pad], one stage ahead in registers
-        const int tid = threadIdx.x;
-        const int bch = nb_pad >> 3;
-        TnLoad L;
-        tn_issue(p, tid, 0, kblocks, r0, r1, n10, n20, bch, L);
+    if (warp == kLoadWarp) {
+        // ================= loader: lane l copies row k0 + l of A' and B' into staging =================
+        // Byte counts are whole 16 B units: rows are padded (ld >= round_up(cols, 4)); tails masked later.
+        const uint32_t a_bytes = static_cast<uint32_t>((na + 3) & ~3) * 4u;
+        const int32_t b1_end = min(n20 + nb, p.n2a);                  // B1 columns [n20, b1_end)
+        const int32_t b2_beg = max(n20, p.n2a);                       // B2 columns [b2_beg, n20 + nb)
+        const uint32_t b1_bytes = b1_end > n20 ? static_cast<uint32_t>((b1_end - n20 + 3) & ~3) * 4u : 0u;
+        const uint32_t b2_bytes =
+            p.nb > 1 && n20 + nb > b2_beg ? static_cast<uint32_t>((n20 + nb - b2_beg + 3) & ~3) * 4u : 0u;
+        auto gidx = [&](const TnB& B, int64_t row) -> int64_t {
+            return B.rows ? static_cast<int64_t>(__ldg(B.rows + row)) : row;
+        };
+        int64_t g1 = 0, g2 = 0;
+        if (kblocks > 0 && r0 + lane < r1) {
+            g1 = gidx(p.b[0], r0 + lane);
+            if (b2_bytes) g2 = gidx(p.b[1], r0 + lane);
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
-            const int stage = kb % kStages;
-            mbar_wait(&empty[stage], ((kb / kStages) & 1) ^ 1);
-            uint8_t* st = smem + stage * kTnStage;
-            uint8_t* a_hi = st;
-            uint8_t* a_lo = st + kATile;
-            uint8_t* b_hi = st + 2 * kATile;
-            uint8_t* b_lo = b_hi + kTnBTile;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int idx = tid + j * kProducers;
-                store_chunk(L.a[j], sa, a_hi, a_lo, mn_sw128_off((idx & 15) * 8, idx >> 4));
+            const int slot = kb % kTnStg;
+            const int64_t k0 = r0 + int64_t(kb) * kTnBK;
+            const int64_t row = k0 + lane;
+            const bool ok = row < r1;
+            // prefetch next k-block's gather indices
+            int64_t n1 = 0, n2 = 0;
+            if (kb + 1 < kblocks && row + kTnBK < r1) {
+                n1 = gidx(p.b[0], row + kTnBK);
+                if (b2_bytes) n2 = gidx(p.b[1], row + kTnBK);
             }
+            const int64_t nvalid = r1 - k0 < kTnBK ? r1 - k0 : kTnBK;
+            mbar_wait(&sempty[slot], ((kb / kTnStg) & 1) ^ 1);
+            if (lane == 0)
+                mbar_arrive_expect_tx(&sfull[slot], static_cast<uint32_t>(nvalid) * (a_bytes + b1_bytes + b2_bytes));
+            __syncwarp();
+            uint8_t* sa = stg_base + slot * (kTnStgA + kTnStgB);
+            uint8_t* sb = sa + kTnStgA;
+            if (ok) {
+                bulk_g2s(sa + lane * (kBM * 4), p.a + row * p.lda + n10, a_bytes, &sfull[slot]);
+                if (b1_bytes) bulk_g2s(sb + lane * (kMaxN * 4), p.b[0].ptr + g1 * p.b[0].ld + n20, b1_bytes, &sfull[slot]);
+                if (b2_bytes)
+                    bulk_g2s(sb + lane * (kMaxN * 4) + (b2_beg - n20) * 4, p.b[1].ptr + g2 * p.b[1].ld + (b2_beg - p.n2a),
+                             b2_bytes, &sfull[slot]);
+            }
+            g1 = n1;
+            g2 = n2;
+        }
+    } else if (warp < kConvWarps) {
+        // ================= converters: staging -> MN-major fp16 hi/lo =================
+        const int tid = threadIdx.x;
+        const float sa_ = ldexpf(1.f, ka), sb_ = ldexpf(1.f, kbx);
+        const int bch = nb_pad >> 3;
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int stage = kb % kTnStages, slot = kb % kTnStg;
+            const int64_t k0 = r0 + int64_t(kb) * kTnBK;
+            const int rows_ok = r1 - k0 < kTnBK ? static_cast<int>(r1 - k0) : kTnBK;
+            uint8_t* st = smem + stage * kTnStage;
+            const uint8_t* sga = stg_base + slot * (kTnStgA + kTnStgB);
+            const uint8_t* sgb = sga + kTnStgA;
+            mbar_wait(&empty[stage], ((kb / kTnStages) & 1) ^ 1);
+            mbar_wait(&sfull[slot], (kb / kTnStg) & 1);
+            // A': 32 rows x 16 chunks of 8 columns
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int idx = tid + j * kProducers;
-                if (idx >= 64 * bch) break;
-                store_chunk(L.b[j], sb, b_hi, b_lo, mn_sw128_off((idx % bch) * 8, idx / bch));
+            for (int j = 0; j < 2; ++j) {
+                const int idx = tid + j * kConv;
+                const int kr = idx >> 4, ch = idx & 15;
+                float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+                const int valid = kr < rows_ok ? min(8, na - ch * 8) : 0;
+                if (valid > 0) {
+                    const float4* q = reinterpret_cast<const float4*>(sga + kr * (kBM * 4) + ch * 32);
+                    x0 = q[0];
+                    x1 = q[1];
+                    mask8(x0, x1, valid);
+                }
+                split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
+            }
+            // B': 32 rows x bch chunks
+            for (int idx = tid; idx < kTnBK * bch; idx += kConv) {
+                const int kr = idx / bch, ch = idx % bch;
+                float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+                const int valid = kr < rows_ok ? min(8, nb - ch * 8) : 0;
+                if (valid > 0) {
+                    const float4* q = reinterpret_cast<const float4*>(sgb + kr * (kMaxN * 4) + ch * 32);
+                    x0 = q[0];
+                    x1 = q[1];
+                    mask8(x0, x1, valid);
+                }
+                split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + kTnBTile, mn_off(ch * 8, kr));
             }
             fence_proxy_async();
             mbar_arrive(&full[stage]);
-            tn_issue(p, tid, kb + 1, kblocks, r0, r1, n10, n20, bch, L);
+            mbar_arrive(&sempty[slot]);
         }
     } else if (warp == kMmaWarp) {
-        // ===== MMA issuer
+        // ================= MMA issuer =================
         const uint32_t idesc = idesc_f16_mn(kBM, nb_pad);
         for (int chunk = 0; chunk < nchunks; ++chunk) {
             const uint32_t acc = chunk & 1;
@@ -700,20 +710,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             tc_fence_after();
             const int kb_end = min(kblocks, (chunk + 1) * kChunkKb);
             for (int kb = chunk * kChunkKb; kb < kb_end; ++kb) {
-                const int stage = kb % kStages;
-                mbar_wait(&full[stage], (kb / kStages) & 1);
+                const int stage = kb % kTnStages;
+                mbar_wait(&full[stage], (kb / kTnStages) & 1);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint8_t* st = smem + stage * kTnStage;
-                    const uint32_t ahi = smem_u32(st), alo = smem_u32(st + kATile);
-                    const uint32_t bhi = smem_u32(st + 2 * kATile), blo = smem_u32(st + 2 * kATile + kTnBTile);
+                    const uint32_t ahi = smem_u32(st), alo = smem_u32(st + kTnATile);
+                    const uint32_t bhi = smem_u32(st + 2 * kTnATile), blo = smem_u32(st + 2 * kTnATile + kTnBTile);
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        const uint32_t adv = k * 2048;  // 16 rows = 2 K atoms of 1024 B
-                        const uint64_t dah = desc_mn_sw128(ahi + adv, p.lbo, p.sbo);
-                        const uint64_t dal = desc_mn_sw128(alo + adv, p.lbo, p.sbo);
-                        const uint64_t dbh = desc_mn_sw128(bhi + adv, p.lbo, p.sbo);
-                        const uint64_t dbl = desc_mn_sw128(blo + adv, p.lbo, p.sbo);
+                    for (int k = 0; k < kTnBK / 16; ++k) {
+                        const uint32_t adv = k * 2 * kTnSbo;  // 16 rows = 2 K groups
+                        const uint64_t dah = desc_mn_sw128(ahi + adv, kTnLbo, kTnSbo);
+                        const uint64_t dal = desc_mn_sw128(alo + adv, kTnLbo, kTnSbo);
+                        const uint64_t dbh = desc_mn_sw128(bhi + adv, kTnLbo, kTnSbo);
+                        const uint64_t dbl = desc_mn_sw128(blo + adv, kTnLbo, kTnSbo);
                         const uint32_t first = (kb == chunk * kChunkKb && k == 0) ? 0u : 1u;
                         mma_f16(d_tmem, dah, dbh, idesc, first);
                         mma_f16(d_tmem, dah, dbl, idesc, 1u);
@@ -726,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             }
         }
     } else {
-        // ===== epilogue: drain each chunk into the fp32 partial ws[split]
+        // ================= epilogue: drain each chunk into the fp32 partial ws[split] =================
         const int ew = warp & 3;
         const int32_t m = n10 + ew * 32 + lane;  // output row (N1 index)
         const bool live = m < p.N1;
@@ -772,11 +782,10 @@ __global__ void tn_reduce_kernel(int32_t S, int32_t N1, int32_t N2, const float*
 }  // namespace tc
 
 // ---- host side -------------------------------------------------------------------
-constexpr int kTnSmemBytes = tc::kStages * (2 * tc::kATile + 2 * tc::kTnBTile) + 1024 + 256;
 
 int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M) {
     const int32_t tiles = ((N1 + tc::kBM - 1) / tc::kBM) * ((N2 + tc::kMaxN - 1) / tc::kMaxN);
-    int64_t s = std::max<int64_t>(1, num_sms() / tiles);
+    int64_t s = std::max<int64_t>(1, num_sms() / tiles);  // one wave of persistent-sized CTAs
     s = std::min<int64_t>(s, (M + 4095) / 4096);  // >= 4096 rows per split
     return static_cast<int32_t>(std::max<int64_t>(s, 1));
 }
@@ -793,7 +802,7 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     static bool attr_set = false;
     if (!attr_set) {
         SC_CUDA(cudaFuncSetAttribute(tc::gemm_tn_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kTnSmemBytes));
+                                     tc::kTnSmemBytes));
         attr_set = true;
     }
     tc::TnParams p{};
@@ -809,24 +818,30 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     p.M = M;
     const int32_t S = tn_f16x3_splits(N1, N2, M);
     if (int64_t(S) * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn_f16x3: workspace too small");
-    p.rows_per_split = ((M + S - 1) / S + tc::kBK - 1) / tc::kBK * tc::kBK;
+    p.rows_per_split = ((M + S - 1) / S + tc::kTnBK - 1) / tc::kTnBK * tc::kTnBK;
     p.tiles1 = (N1 + tc::kBM - 1) / tc::kBM;
     p.tiles2 = (N2 + tc::kMaxN - 1) / tc::kMaxN;
     p.ws = ws;
-    p.lbo = 8192;  // MN-major: stride between 64-element MN atoms ([mn_atom][k_atom] layout)
-    p.sbo = 1024;  // stride between 8-row K groups (validated against fp64 in tests/test_gpu_gemm.py)
     const unsigned grid = static_cast<unsigned>(S * p.tiles1 * p.tiles2);
-    tc::gemm_tn_f16x3_kernel<<<grid, tc::kThreads, kTnSmemBytes, s>>>(p);
+    tc::gemm_tn_f16x3_kernel<<<grid, tc::kThreads, tc::kTnSmemBytes, s>>>(p);
     SC_LAUNCH_CHECK();
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();
     count_launch(2);
 }
 bool tc_supported(const MatA& a1, const MatA* a2, int32_t N) {
+    // rows are fetched in whole 16 B units by bulk copies: 16 B aligned rows (ld % 4 == 0)
     auto ok = [](const MatA& a) {
-        return (a.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(a.ptr) % 16) == 0 && a.K >= 1;
+        return (a.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(a.ptr) % 16) == 0 && a.K >= 1 && a.ld >= a.K;
     };
     return N >= 1 && N <= tc::kMaxN && ok(a1) && (!a2 || ok(*a2));
+}
+
+bool tn_supported(const MatT& a, const MatT& b1, const MatT* b2) {
+    auto ok = [](const MatT& x) {
+        return (x.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x.ptr) % 16) == 0 && x.ld >= x.cols;
+    };
+    return ok(a) && ok(b1) && (!b2 || (ok(*b2) && b1.cols % 4 == 0));
 }
 
 void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s) {
@@ -841,6 +856,31 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
     SC_LAUNCH_CHECK();
     count_launch();
 }
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        SC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+// 2D fp32 map over a row-major [rows x cols] matrix with row stride ld, box {box_c, box_r}.
+void encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_c,
+               uint32_t box_r) {
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+    const cuuint32_t box[2] = {box_c, box_r};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+}  // namespace
 
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
@@ -860,8 +900,16 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     const float* am[2] = {amax1, amax2};
     for (int i = 0; i < p.nsrc; ++i) {
         if (bs[i]->N != N || bs[i]->K != as[i]->K) throw std::logic_error("gemm_f16x3: B image shape mismatch");
-        p.src[i] = tc::Src{as[i]->ptr, as[i]->rows, as[i]->ld, as[i]->K, bs[i]->kblocks, bs[i]->img.get(), am[i],
-                           bs[i]->bexp.get()};
+        tc::Src& S = p.src[i];
+        S.a = as[i]->ptr;
+        S.rows = as[i]->rows;
+        S.lda = as[i]->ld;
+        S.K = as[i]->K;
+        S.kblocks = bs[i]->kblocks;
+        S.bimg = bs[i]->img.get();
+        S.amax_a = am[i];
+        S.bexp = bs[i]->bexp.get();
+        if (!S.rows) encode_2d(&S.tmap, S.a, M, S.K, S.lda, tc::kNtBK, tc::kBM);
     }
     p.M = M;
     p.N = N;
@@ -905,7 +953,7 @@ void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b
 
 void TcGemm::tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1,
                 const MatT* b2, const float* amax_b2, int64_t M, float* C, int64_t ldc) {
-    if (enabled)
+    if (enabled && tn_supported(a, b1, b2))
         gemm_tn_f16x3(a, amax_a, b1, amax_b1, b2, amax_b2, M, C, ldc, t->ws.get(), t->ws_floats, t->ctx->stream);
     else
         gemm_tn(a, b1, b2, M, C, ldc, t->ws.get(), t->ws_floats, t->ctx->stream);

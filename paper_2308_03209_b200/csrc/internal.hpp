@@ -96,6 +96,7 @@ struct sc_graph {
     int32_t dim = 0, num_classes = 0;
     sc::DevBuf<float> features;        // n x dim
     sc::DevBuf<float> feat_amax;       // max |features| (tensor-core operand scale)
+    uint64_t feat_version = 0;         // bumped whenever the features change
     sc::DevBuf<int32_t> labels;        // n
     sc::DevBuf<uint8_t> train, val, test;  // n
     int64_t train_count = 0;

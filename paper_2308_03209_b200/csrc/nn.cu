@@ -131,6 +131,14 @@ __global__ void __launch_bounds__(NT) gemm_nt_kernel(GemmArgs args) {
     }
 }
 
+__global__ void gather_rows_kernel(int64_t n, int32_t d, const int32_t* __restrict__ rows, const float* __restrict__ src,
+                                   float* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * d; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / d;
+        dst[i] = src[int64_t(rows[r]) * d + (i - r * d)];
+    }
+}
+
 __global__ void absmax_kernel(int64_t n, const float* __restrict__ x, float* out) {
     float mx = 0.f;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
@@ -633,6 +641,12 @@ void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs,
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
               const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out) {
     spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s, amax_out);
+}
+void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s) {
+    if (n <= 0) return;
+    gather_rows_kernel<<<grid_for(n * d, 256), 256, 0, s>>>(n, d, rows, src, dst);
+    SC_LAUNCH_CHECK();
+    count_launch();
 }
 void absmax(int64_t n, const float* x, float* out, cudaStream_t s) {
     if (n <= 0) return;

@@ -151,6 +151,7 @@ void trainer_init(sc_trainer* t) {
         SC_CUDA(cudaMemsetAsync(st.g_amax.get(), 0, sizeof(float), s));
         absmax(st.n, st.scale.get(), st.g_amax.get(), s);
         st.logits.alloc(std::max<int64_t>(st.n * t->Cp, 1));
+        st.x0.alloc(std::max<int64_t>(st.n * t->d, 1));
         if (t->use_dropedge) {
             st.words = (st.nnz + 31) / 32;
             st.bits.alloc(std::max<int64_t>(st.words * t->K, 1));
@@ -240,6 +241,7 @@ struct Rows {
     int64_t nnz;           // CSR slots
     int64_t kept;          // CSR slots kept by the selected DropEdge mask
     const float* g_amax;   // bound on max|dloss/dlogits| (= max loss scale)
+    const float* x0;       // layer-0 input rows (contiguous n x d; the partition's gathered features)
 };
 
 // Algorithmic HBM bytes of one aggregation launch: offsets,
@@ -259,7 +261,7 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
     P.begin("inv_degree", double(n) * 12 + double(R.offsets ? 8 : 0) * n, s);
     inv_degree(n, R.offsets, R.bits, t->inv.get(), s);
     P.end(s);
-    const MatA x0{t->g->features.get(), t->d, R.nodes, t->d};
+    const MatA x0{R.x0, t->d, nullptr, t->d};
     for (int l = 0; l < t->L; ++l) {
         const LayerOff& lo = t->lay[l];
         const MatA xin = l == 0 ? x0 : MatA{t->X[l].get(), lo.in, nullptr, lo.in};
@@ -296,8 +298,7 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
     cudaStream_t s = t->ctx->stream;
     Profiler& P = t->prof;
     const int64_t n = R.n;
-    const MatA x0{t->g->features.get(), t->d, R.nodes, t->d};
-    const MatT x0t{t->g->features.get(), t->d, R.nodes, t->d};
+    const MatT x0t{R.x0, t->d, nullptr, t->d};
     const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L].get(), t->E, nullptr, t->E};
     // head grad = G^T emb ; dh = G head   (:259-260)
     P.begin("wgrad", 4.0 * n * (t->C + t->E), s);
@@ -370,7 +371,14 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     }
     const int64_t kept =
         bits ? 2 * static_cast<int64_t>(std::ceil((1.0 - t->ratio) * static_cast<double>(pd.m_local))) : st.nnz;
-    const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get()};
+    if (st.x0_version != t->g->feat_version) {  // the partition's feature rows, contiguous (train_cofree :225-227)
+        t->prof.begin("gather_x0", 8.0 * st.n * t->d, s);
+        gather_rows(st.n, t->d, pd.nodes.get(), t->g->features.get(), st.x0.get(), s);
+        t->prof.end(s);
+        st.x0_version = t->g->feat_version;
+    }
+    const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get(),
+                 st.x0.get()};
     SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
     forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
@@ -440,7 +448,8 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
     sc_graph* g = t->g;
     ensure_rows(t, g->n);
     if (t->eval_logits.size() < size_t(g->n) * t->Cp) t->eval_logits.alloc(size_t(g->n) * t->Cp);
-    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr};
+    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr,
+                 g->features.get()};
     const bool was = t->prof.enabled;
     t->prof.enabled = false;
     forward(t, R, t->eval_logits.get());

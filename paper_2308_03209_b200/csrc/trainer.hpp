@@ -27,6 +27,8 @@ struct PartState {
     int64_t words = 0;
     DevBuf<float> logits;  // n x C, last step
     DevBuf<float> g_amax;  // bound on max|dloss/dlogits| (tensor-core operand scale)
+    DevBuf<float> x0;      // layer-0 input: this partition's feature rows (n x d), gathered once per
+    uint64_t x0_version = 0;  // feature version, so the GEMMs stream contiguous rows
     int chosen = -1;
 };
 
