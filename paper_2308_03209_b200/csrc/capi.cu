@@ -557,7 +557,7 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
         const MatA a2{reinterpret_cast<const float*>(dA2.get()), lda2, nullptr, K2};
         const MatB b2{reinterpret_cast<const float*>(dB2.get()), ldb2, b2_nn != 0};
         const float* sc = epi == kEpiRowScale ? reinterpret_cast<const float*>(dS.get()) : nullptr;
-        if (mode == 0) {
+        if (mode == 0 && tc_supported(a1, K2 > 0 ? &a2 : nullptr, N)) {
             DevBuf<float> am(2);
             SC_CUDA(cudaMemsetAsync(am.get(), 0, 2 * sizeof(float), s));
             absmax(a1_rows * lda1, a1.ptr, am.get(), s);
@@ -597,7 +597,7 @@ sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A,
         const MatT b2{dB2.get(), N2b, rows2 ? dR.get() : nullptr, N2b};
         const int64_t wsf = std::max<int64_t>(gemm_tn_workspace_floats(N1, N2), int64_t(256) * N1 * N2);
         DevBuf<float> ws(wsf);
-        if (mode == 0) {
+        if (mode == 0 && tn_supported(a, b1, B2 ? &b2 : nullptr)) {
             DevBuf<float> am(3);
             SC_CUDA(cudaMemsetAsync(am.get(), 0, 3 * sizeof(float), s));
             absmax(M * lda, dA.get(), am.get(), s);

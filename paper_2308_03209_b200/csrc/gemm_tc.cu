@@ -74,11 +74,11 @@ constexpr int kTnStgB = kTnBK * kMaxN * 4;            // 32 rows x 256 fp32 = 32
 constexpr int kTnBarOff = kTnStages * kTnStage + kTnStg * (kTnStgA + kTnStgB);
 constexpr int kTnSmemBytes = kTnBarOff + 256 + 1024;
 constexpr int kChunkKb = 32;                          // 1024 rows per TMEM accumulation (TN)
+constexpr int kTnBox = kTnBK * 128;                   // one 32-column x 32-row fp32 TMA box
 
 struct Src {
-    CUtensorMap tmap;     // 2D map over A (box 32 k x 128 rows, fp32, OOB -> 0); unused when gathered
+    CUtensorMap tmap;     // 2D map over A (box 32 k x 128 rows, fp32, SWIZZLE_128B, OOB -> 0)
     const float* a;
-    const int32_t* rows;  // optional gather (per-row bulk copies)
     int64_t lda;
     int32_t K;            // valid k (multiple of 4)
     int32_t kblocks;      // ceil(K / 32)
@@ -294,45 +294,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
     const int64_t n_it = my_tiles * kb_total;
 
     if (warp == kLoadWarp) {
-        // ================= loader: row slices HBM -> fp32 staging =================
-        int64_t grow[4] = {0, 0, 0, 0};  // rows lane + 32 j of the current tile (gathered)
+        // ================= loader: one 2D TMA per stage, HBM -> fp32 staging =================
+        // box 32 k (128 B) x 128 rows, SWIZZLE_128B; out-of-range rows / k are zero-filled
         for (int64_t it = 0; it < n_it; ++it) {
             const int slot = static_cast<int>(it % kNtStg);
             int64_t m0;
             int src, kb;
             nt_decode(p, it, kb_total, m0, src, kb);
-            const Src& S = p.src[src];
-            if (kb == 0 && S.rows) {  // new tile or source: gathered global rows of this tile
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int64_t row = m0 + lane + 32 * j;
-                    grow[j] = row < p.M ? (S.rows ? static_cast<int64_t>(__ldg(S.rows + row)) : row) : -1;
-                }
-            }
-            const int k0 = kb * kNtBK;
-            uint8_t* dst = stg_base + slot * kNtStgBytes;
             mbar_wait(&sempty[slot], ((it / kNtStg) & 1) ^ 1);
-            if (!S.rows) {
-                // one 2D TMA per stage: box 32 k x 128 rows; out-of-range rows / k are zero-filled
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&sfull[slot], kNtStgBytes);
-                    tma_load_2d(dst, &S.tmap, k0, static_cast<int32_t>(m0), &sfull[slot]);
-                }
-            } else {
-                // gathered rows: one bulk copy per row slice (whole 16 B units; rows are padded to
-                // ld >= round_up(K, 4); the tail is masked by the converters)
-                const uint32_t bytes = static_cast<uint32_t>(min(kNtBK, ((S.K + 3) & ~3) - k0)) * 4u;
-                const int64_t nvalid = p.M - m0 < kBM ? p.M - m0 : kBM;
-                if (lane == 0) mbar_arrive_expect_tx(&sfull[slot], static_cast<uint32_t>(nvalid) * bytes);
-                __syncwarp();
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (grow[j] >= 0)
-                        bulk_g2s(dst + (lane + 32 * j) * (kNtBK * 4), S.a + grow[j] * S.lda + k0, bytes, &sfull[slot]);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&sfull[slot], kNtStgBytes);
+                tma_load_2d(stg_base + slot * kNtStgBytes, &p.src[src].tmap, kb * kNtBK, static_cast<int32_t>(m0),
+                            &sfull[slot]);
             }
+            __syncwarp();
         }
     } else if (warp < kConvWarps) {
         // ================= converters: staging fp32 -> scaled fp16 hi/lo (SW64) =================
+        // Row-fastest mapping: 8 consecutive threads read the same chunk of 8 different rows, which
+        // the 128 B swizzle spreads over distinct banks (conflict-free loads and SW64 stores).
         const int tid = threadIdx.x;
         const float sa0 = ldexpf(1.f, kt - kb_exp[0]), sa1 = ldexpf(1.f, kt - kb_exp[1]);
         for (int64_t it = 0; it < n_it; ++it) {
@@ -341,7 +321,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
             int src, kb;
             nt_decode(p, it, kb_total, m0, src, kb);
             const Src& S = p.src[src];
-            const int k0 = kb * kNtBK;
             uint8_t* st = smem + stage * kNtStage;
             const uint8_t* sg = stg_base + slot * kNtStgBytes;
             mbar_wait(&empty[stage], ((it / kNtStages) & 1) ^ 1);
@@ -354,15 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int idx = tid + j * kConv;
-                const int r = idx >> 2, c = idx & 3;
-                float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
-                const int valid = m0 + r < p.M ? min(8, S.K - (k0 + c * 8)) : 0;
-                if (valid > 0) {
-                    const float4* q = reinterpret_cast<const float4*>(sg + r * (kNtBK * 4) + c * 32);
-                    x0 = q[0];
-                    x1 = q[1];
-                    mask8(x0, x1, valid);
-                }
+                const int r = idx & 127, c = idx >> 7;  // row, 8-float chunk (0..3)
+                const uint8_t* rowp = sg + r * (kNtBK * 4);
+                float4 x0 = *reinterpret_cast<const float4*>(rowp + (((2 * c) ^ (r & 7)) << 4));
+                float4 x1 = *reinterpret_cast<const float4*>(rowp + (((2 * c + 1) ^ (r & 7)) << 4));
                 split8_store(x0, x1, sa, st, st + kNtATile, sw64_off(r, c));
             }
             fence_proxy_async();
@@ -519,7 +493,8 @@ struct TnB {
     int32_t cols;
     const float* amax;
 };
-struct TnParams {
+struct alignas(64) TnParams {
+    CUtensorMap tm_a, tm_b1, tm_b2;  // 2D fp32 maps, box 32 columns x 32 rows, SWIZZLE_128B
     const float* a;
     int64_t lda;
     int32_t N1;
@@ -610,52 +585,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == kLoadWarp) {
-        // ================= loader: lane l copies row k0 + l of A' and B' into staging =================
-        // Byte counts are whole 16 B units: rows are padded (ld >= round_up(cols, 4)); tails masked later.
-        const uint32_t a_bytes = static_cast<uint32_t>((na + 3) & ~3) * 4u;
-        const int32_t b1_end = min(n20 + nb, p.n2a);                  // B1 columns [n20, b1_end)
-        const int32_t b2_beg = max(n20, p.n2a);                       // B2 columns [b2_beg, n20 + nb)
-        const uint32_t b1_bytes = b1_end > n20 ? static_cast<uint32_t>((b1_end - n20 + 3) & ~3) * 4u : 0u;
-        const uint32_t b2_bytes =
-            p.nb > 1 && n20 + nb > b2_beg ? static_cast<uint32_t>((n20 + nb - b2_beg + 3) & ~3) * 4u : 0u;
-        auto gidx = [&](const TnB& B, int64_t row) -> int64_t {
-            return B.rows ? static_cast<int64_t>(__ldg(B.rows + row)) : row;
-        };
-        int64_t g1 = 0, g2 = 0;
-        if (kblocks > 0 && r0 + lane < r1) {
-            g1 = gidx(p.b[0], r0 + lane);
-            if (b2_bytes) g2 = gidx(p.b[1], r0 + lane);
-        }
+        // ================= loader: 2D TMA boxes (32 columns x 32 rows, SWIZZLE_128B) -> staging =================
+        // A' needs ceil(na/32) boxes, B' ceil(nb/32) (from B1 or B2; n2a is a multiple of 32).
+        const int a_boxes = (na + 31) >> 5, b_boxes = (nb + 31) >> 5;
+        const uint32_t bytes = static_cast<uint32_t>(a_boxes + b_boxes) * kTnBox;
         for (int kb = 0; kb < kblocks; ++kb) {
             const int slot = kb % kTnStg;
-            const int64_t k0 = r0 + int64_t(kb) * kTnBK;
-            const int64_t row = k0 + lane;
-            const bool ok = row < r1;
-            // prefetch next k-block's gather indices
-            int64_t n1 = 0, n2 = 0;
-            if (kb + 1 < kblocks && row + kTnBK < r1) {
-                n1 = gidx(p.b[0], row + kTnBK);
-                if (b2_bytes) n2 = gidx(p.b[1], row + kTnBK);
-            }
-            const int64_t nvalid = r1 - k0 < kTnBK ? r1 - k0 : kTnBK;
+            const int32_t k0 = static_cast<int32_t>(r0 + int64_t(kb) * kTnBK);
             mbar_wait(&sempty[slot], ((kb / kTnStg) & 1) ^ 1);
-            if (lane == 0)
-                mbar_arrive_expect_tx(&sfull[slot], static_cast<uint32_t>(nvalid) * (a_bytes + b1_bytes + b2_bytes));
-            __syncwarp();
             uint8_t* sa = stg_base + slot * (kTnStgA + kTnStgB);
             uint8_t* sb = sa + kTnStgA;
-            if (ok) {
-                bulk_g2s(sa + lane * (kBM * 4), p.a + row * p.lda + n10, a_bytes, &sfull[slot]);
-                if (b1_bytes) bulk_g2s(sb + lane * (kMaxN * 4), p.b[0].ptr + g1 * p.b[0].ld + n20, b1_bytes, &sfull[slot]);
-                if (b2_bytes)
-                    bulk_g2s(sb + lane * (kMaxN * 4) + (b2_beg - n20) * 4, p.b[1].ptr + g2 * p.b[1].ld + (b2_beg - p.n2a),
-                             b2_bytes, &sfull[slot]);
+            if (lane == 0) mbar_arrive_expect_tx(&sfull[slot], bytes);
+            __syncwarp();
+            if (lane < a_boxes) tma_load_2d(sa + lane * kTnBox, &p.tm_a, n10 + 32 * lane, k0, &sfull[slot]);
+            if (lane < b_boxes) {
+                const int32_t c = n20 + 32 * lane;
+                if (c < p.n2a) tma_load_2d(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[slot]);
+                else tma_load_2d(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[slot]);
             }
-            g1 = n1;
-            g2 = n2;
         }
     } else if (warp < kConvWarps) {
-        // ================= converters: staging -> MN-major fp16 hi/lo =================
+        // ================= converters: swizzled staging -> MN-major fp16 hi/lo =================
+        // Row-fastest mapping (idx & 31 = row): 8 consecutive threads read the same logical chunk
+        // of 8 rows, which the 128 B swizzle spreads over distinct banks.
         const int tid = threadIdx.x;
         const float sa_ = ldexpf(1.f, ka), sb_ = ldexpf(1.f, kbx);
         const int bch = nb_pad >> 3;
@@ -672,26 +624,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int idx = tid + j * kConv;
-                const int kr = idx >> 4, ch = idx & 15;
+                const int kr = idx & 31, ch = idx >> 5;
                 float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
                 const int valid = kr < rows_ok ? min(8, na - ch * 8) : 0;
                 if (valid > 0) {
-                    const float4* q = reinterpret_cast<const float4*>(sga + kr * (kBM * 4) + ch * 32);
-                    x0 = q[0];
-                    x1 = q[1];
+                    const uint8_t* rowp = sga + (ch >> 2) * kTnBox + kr * 128;
+                    x0 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3)) ^ (kr & 7)) << 4));
+                    x1 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3) + 1) ^ (kr & 7)) << 4));
                     mask8(x0, x1, valid);
                 }
                 split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
             }
-            // B': 32 rows x bch chunks
-            for (int idx = tid; idx < kTnBK * bch; idx += kConv) {
-                const int kr = idx / bch, ch = idx % bch;
+            // B': 32 rows x bch (<= 32) chunks
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int idx = tid + j * kConv;
+                const int kr = idx & 31, ch = idx >> 5;
+                if (ch >= bch) continue;
                 float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
                 const int valid = kr < rows_ok ? min(8, nb - ch * 8) : 0;
                 if (valid > 0) {
-                    const float4* q = reinterpret_cast<const float4*>(sgb + kr * (kMaxN * 4) + ch * 32);
-                    x0 = q[0];
-                    x1 = q[1];
+                    const uint8_t* rowp = sgb + (ch >> 2) * kTnBox + kr * 128;
+                    x0 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3)) ^ (kr & 7)) << 4));
+                    x1 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3) + 1) ^ (kr & 7)) << 4));
                     mask8(x0, x1, valid);
                 }
                 split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + kTnBTile, mn_off(ch * 8, kr));
@@ -783,6 +738,31 @@ __global__ void tn_reduce_kernel(int32_t S, int32_t N1, int32_t N2, const float*
 
 // ---- host side -------------------------------------------------------------------
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        SC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+// 2D fp32 map over a row-major [rows x cols] matrix with row stride ld, box {box_c, box_r}.
+void encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_c,
+               uint32_t box_r, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+    const cuuint32_t box[2] = {box_c, box_r};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+}  // namespace
+
 int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M) {
     const int32_t tiles = ((N1 + tc::kBM - 1) / tc::kBM) * ((N2 + tc::kMaxN - 1) / tc::kMaxN);
     int64_t s = std::max<int64_t>(1, num_sms() / tiles);  // one wave of persistent-sized CTAs
@@ -811,6 +791,9 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     p.N1 = N1;
     p.amax_a = amax_a;
     p.b[0] = tc::TnB{b1.ptr, b1.ld, b1.rows, b1.cols, amax_b1};
+    encode_2d(&p.tm_a, a.ptr, M, N1, a.ld, 32, tc::kTnBK);
+    encode_2d(&p.tm_b1, b1.ptr, M, b1.cols, b1.ld, 32, tc::kTnBK);
+    if (b2) encode_2d(&p.tm_b2, b2->ptr, M, b2->cols, b2->ld, 32, tc::kTnBK);
     p.nb = b2 ? 2 : 1;
     if (b2) p.b[1] = tc::TnB{b2->ptr, b2->ld, b2->rows, b2->cols, amax_b2};
     p.n2a = b1.cols;
@@ -831,17 +814,20 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
 }
 bool tc_supported(const MatA& a1, const MatA* a2, int32_t N) {
     // rows are fetched in whole 16 B units by bulk copies: 16 B aligned rows (ld % 4 == 0)
+    // operands stream through 2D TMA (no row gathers): 16 B aligned rows
     auto ok = [](const MatA& a) {
-        return (a.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(a.ptr) % 16) == 0 && a.K >= 1 && a.ld >= a.K;
+        return !a.rows && (a.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(a.ptr) % 16) == 0 && a.K >= 1 &&
+               a.ld >= a.K;
     };
     return N >= 1 && N <= tc::kMaxN && ok(a1) && (!a2 || ok(*a2));
 }
 
 bool tn_supported(const MatT& a, const MatT& b1, const MatT* b2) {
     auto ok = [](const MatT& x) {
-        return (x.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x.ptr) % 16) == 0 && x.ld >= x.cols;
+        return !x.rows && (x.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x.ptr) % 16) == 0 && x.ld >= x.cols;
     };
-    return ok(a) && ok(b1) && (!b2 || (ok(*b2) && b1.cols % 4 == 0));
+    // B' boxes are 32 columns wide and come from one source each
+    return ok(a) && ok(b1) && (!b2 || (ok(*b2) && b1.cols % 32 == 0));
 }
 
 void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s) {
@@ -857,30 +843,6 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
     count_launch();
 }
 
-namespace {
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        SC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
-        if (!f || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    }();
-    return fn;
-}
-// 2D fp32 map over a row-major [rows x cols] matrix with row stride ld, box {box_c, box_r}.
-void encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_c,
-               uint32_t box_r) {
-    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
-    const cuuint32_t box[2] = {box_c, box_r};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-}
-}  // namespace
 
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
@@ -902,14 +864,13 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
         if (bs[i]->N != N || bs[i]->K != as[i]->K) throw std::logic_error("gemm_f16x3: B image shape mismatch");
         tc::Src& S = p.src[i];
         S.a = as[i]->ptr;
-        S.rows = as[i]->rows;
         S.lda = as[i]->ld;
         S.K = as[i]->K;
         S.kblocks = bs[i]->kblocks;
         S.bimg = bs[i]->img.get();
         S.amax_a = am[i];
         S.bexp = bs[i]->bexp.get();
-        if (!S.rows) encode_2d(&S.tmap, S.a, M, S.K, S.lda, tc::kNtBK, tc::kBM);
+        encode_2d(&S.tmap, S.a, M, S.K, S.lda, tc::kNtBK, tc::kBM);
     }
     p.M = M;
     p.N = N;

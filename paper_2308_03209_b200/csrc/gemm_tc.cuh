@@ -14,7 +14,7 @@ struct sc_trainer;
 namespace sc {
 
 // A weight operand pre-scaled (by 2^bexp) and pre-split into fp16 hi/lo
-// k-block images in the smem SW128 layout, ready for one bulk copy per stage.
+// k-block images (32 k, SW64 K-major layout), ready for one bulk copy per stage.
 struct BImage {
     DevBuf<uint8_t> img;
     DevBuf<int32_t> bexp;
@@ -22,6 +22,7 @@ struct BImage {
 };
 
 bool tc_supported(const MatA& a1, const MatA* a2, int32_t N);
+bool tn_supported(const MatT& a, const MatT& b1, const MatT* b2);
 void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s);
 
 // C[M x N] = A1 op(B1) (+ A2 op(B2)) on the tensor cores in fp16x3 split
