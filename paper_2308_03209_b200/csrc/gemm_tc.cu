@@ -71,7 +71,8 @@ constexpr int kTnBTile = kMaxN * kTnBK * 2;           // 256 cols x 32 rows fp16
 constexpr int kTnStage = 2 * kTnATile + 2 * kTnBTile;
 constexpr int kTnStgA = kTnBK * kBM * 4;              // 32 rows x 128 fp32 = 16 KB
 constexpr int kTnStgB = kTnBK * kMaxN * 4;            // 32 rows x 256 fp32 = 32 KB
-constexpr int kTnBarOff = kTnStages * kTnStage + kTnStg * (kTnStgA + kTnStgB);
+constexpr int kTnEpiOff = kTnStages * kTnStage + kTnStg * (kTnStgA + kTnStgB);
+constexpr int kTnBarOff = kTnEpiOff + 4 * 32 * 33 * 4;  // + drain transpose buffers
 constexpr int kTnSmemBytes = kTnBarOff + 256 + 1024;
 constexpr int kChunkKb = 32;                          // 1024 rows per TMEM accumulation (TN)
 constexpr int kTnBox = kTnBK * 128;                   // one 32-column x 32-row fp32 TMA box
@@ -692,11 +693,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         }
     } else {
         // ================= epilogue: drain each chunk into the fp32 partial ws[split] =================
+        // Each warp owns 32 output rows (TMEM lanes); a 32 x 32 block is transposed through smem so
+        // every read-modify-write of the partial touches one contiguous 128 B row segment.
         const int ew = warp & 3;
-        const int32_t m = n10 + ew * 32 + lane;  // output row (N1 index)
-        const bool live = m < p.N1;
+        const int32_t m0w = n10 + ew * 32;  // first output row (N1 index) of this warp
+        const int rows_here = p.N1 - m0w < 32 ? max(0, p.N1 - m0w) : 32;
         const float unscale = ldexpf(1.f, -(ka + kbx));
-        float* out = p.ws + (int64_t(split) * p.N1 + (live ? m : 0)) * p.N2 + n20;
+        float* stg = reinterpret_cast<float*>(smem + kTnEpiOff) + ew * (32 * 33);
+        float* outw = p.ws + (int64_t(split) * p.N1 + m0w) * p.N2 + n20;
         for (int chunk = 0; chunk < nchunks; ++chunk) {
             const uint32_t acc = chunk & 1;
             mbar_wait(&tfull[acc], (chunk >> 1) & 1);
@@ -704,19 +708,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             for (int c0 = 0; c0 < nb_pad; c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
-                if (!live) continue;
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    if (c0 + q >= nb) break;
-                    const float x = __uint_as_float(r[q]) * unscale;
-                    out[c0 + q] = chunk == 0 ? x : out[c0 + q] + x;
+                for (int q = 0; q < 32; ++q) stg[lane * 33 + q] = __uint_as_float(r[q]) * unscale;
+                __syncwarp();
+                const int col = c0 + lane;
+                if (col < nb) {
+                    float* o = outw + col;
+                    float prev[32];
+                    // all 32 loads in flight before any store (the stores could alias them otherwise)
+#pragma unroll
+                    for (int rr = 0; rr < 32; ++rr)
+                        prev[rr] = (chunk > 0 && rr < rows_here) ? o[int64_t(rr) * p.N2] : 0.f;
+#pragma unroll
+                    for (int rr = 0; rr < 32; ++rr)
+                        if (rr < rows_here) o[int64_t(rr) * p.N2] = prev[rr] + stg[rr * 33 + lane];
                 }
+                __syncwarp();
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
-        if (nchunks == 0 && live)
-            for (int c = 0; c < nb; ++c) out[c] = 0.f;
+        if (nchunks == 0)
+            for (int rr = 0; rr < rows_here; ++rr)
+                for (int c = lane; c < nb; c += 32) outw[int64_t(rr) * p.N2 + c] = 0.f;
     }
     __syncthreads();
     if (warp == kMmaWarp) {
