@@ -162,6 +162,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// (slot, phase) of a circular mbarrier pipeline, advanced without divisions.
+struct Ring {
+    int idx = 0;
+    uint32_t phase = 0;
+    __device__ __forceinline__ void next(int n) {
+        if (++idx == n) {
+            idx = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
 // Exponent k such that amax * 2^k lies in [2^14, 2^15) (0 for zero / non-finite).
 __host__ __device__ __forceinline__ int scale_exp(float amax) {
     if (!(amax > 0.f) || !(amax < 3.0e38f)) return 0;
@@ -224,18 +236,6 @@ __device__ __forceinline__ void mask8(float4& x0, float4& x1, int valid) {
     x1 = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-__device__ __forceinline__ void nt_decode(const Params& p, int64_t it, int kb_total, int64_t& m0, int& src,
-                                          int& kb) {
-    const int64_t tl = it / kb_total;
-    int kbg = static_cast<int>(it - tl * kb_total);
-    m0 = (blockIdx.x + tl * gridDim.x) * kBM;
-    src = 0;
-    if (p.nsrc > 1 && kbg >= p.src[0].kblocks) {
-        kbg -= p.src[0].kblocks;
-        src = 1;
-    }
-    kb = kbg;
-}
 
 __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -291,74 +291,72 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
 
     int kb_total = 0;
     for (int s = 0; s < p.nsrc; ++s) kb_total += p.src[s].kblocks;
-    const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const int64_t n_it = my_tiles * kb_total;
 
     if (warp == kLoadWarp) {
         // ================= loader: one 2D TMA per stage, HBM -> fp32 staging =================
         // box 32 k (128 B) x 128 rows, SWIZZLE_128B; out-of-range rows / k are zero-filled
-        for (int64_t it = 0; it < n_it; ++it) {
-            const int slot = static_cast<int>(it % kNtStg);
-            int64_t m0;
-            int src, kb;
-            nt_decode(p, it, kb_total, m0, src, kb);
-            mbar_wait(&sempty[slot], ((it / kNtStg) & 1) ^ 1);
-            if (lane == 0) {
-                mbar_arrive_expect_tx(&sfull[slot], kNtStgBytes);
-                tma_load_2d(stg_base + slot * kNtStgBytes, &p.src[src].tmap, kb * kNtBK, static_cast<int32_t>(m0),
-                            &sfull[slot]);
-            }
-            __syncwarp();
-        }
+        Ring ring;
+        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x)
+            for (int src = 0; src < p.nsrc; ++src)
+                for (int kb = 0; kb < p.src[src].kblocks; ++kb, ring.next(kNtStg)) {
+                    mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&sfull[ring.idx], kNtStgBytes);
+                        tma_load_2d(stg_base + ring.idx * kNtStgBytes, &p.src[src].tmap, kb * kNtBK,
+                                    static_cast<int32_t>(tile * kBM), &sfull[ring.idx]);
+                    }
+                    __syncwarp();
+                }
     } else if (warp < kConvWarps) {
         // ================= converters: staging fp32 -> scaled fp16 hi/lo (SW64) =================
         // Row-fastest mapping: 8 consecutive threads read the same chunk of 8 different rows, which
         // the 128 B swizzle spreads over distinct banks (conflict-free loads and SW64 stores).
         const int tid = threadIdx.x;
         const float sa0 = ldexpf(1.f, kt - kb_exp[0]), sa1 = ldexpf(1.f, kt - kb_exp[1]);
-        for (int64_t it = 0; it < n_it; ++it) {
-            const int stage = static_cast<int>(it % kNtStages), slot = static_cast<int>(it % kNtStg);
-            int64_t m0;
-            int src, kb;
-            nt_decode(p, it, kb_total, m0, src, kb);
-            const Src& S = p.src[src];
-            uint8_t* st = smem + stage * kNtStage;
-            const uint8_t* sg = stg_base + slot * kNtStgBytes;
-            mbar_wait(&empty[stage], ((it / kNtStages) & 1) ^ 1);
-            if (tid == 0) {
-                mbar_expect_tx(&full[stage], 2 * btile);
-                bulk_g2s(st + 2 * kNtATile, S.bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile, &full[stage]);
-            }
-            mbar_wait(&sfull[slot], (it / kNtStg) & 1);
-            const float sa = src ? sa1 : sa0;
+        Ring mr, sr;  // MMA-operand ring, staging ring
+        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x)
+            for (int src = 0; src < p.nsrc; ++src) {
+                const Src& S = p.src[src];
+                const float sa = src ? sa1 : sa0;
+                for (int kb = 0; kb < S.kblocks; ++kb, mr.next(kNtStages), sr.next(kNtStg)) {
+                    uint8_t* st = smem + mr.idx * kNtStage;
+                    const uint8_t* sg = stg_base + sr.idx * kNtStgBytes;
+                    mbar_wait(&empty[mr.idx], mr.phase ^ 1);
+                    if (tid == 0) {
+                        mbar_expect_tx(&full[mr.idx], 2 * btile);
+                        bulk_g2s(st + 2 * kNtATile, S.bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile,
+                                 &full[mr.idx]);
+                    }
+                    mbar_wait(&sfull[sr.idx], sr.phase);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int idx = tid + j * kConv;
-                const int r = idx & 127, c = idx >> 7;  // row, 8-float chunk (0..3)
-                const uint8_t* rowp = sg + r * (kNtBK * 4);
-                float4 x0 = *reinterpret_cast<const float4*>(rowp + (((2 * c) ^ (r & 7)) << 4));
-                float4 x1 = *reinterpret_cast<const float4*>(rowp + (((2 * c + 1) ^ (r & 7)) << 4));
-                split8_store(x0, x1, sa, st, st + kNtATile, sw64_off(r, c));
+                    for (int j = 0; j < 2; ++j) {
+                        const int idx = tid + j * kConv;
+                        const int r = idx & 127, c = idx >> 7;  // row, 8-float chunk (0..3)
+                        const uint8_t* rowp = sg + r * (kNtBK * 4);
+                        float4 x0 = *reinterpret_cast<const float4*>(rowp + (((2 * c) ^ (r & 7)) << 4));
+                        float4 x1 = *reinterpret_cast<const float4*>(rowp + (((2 * c + 1) ^ (r & 7)) << 4));
+                        split8_store(x0, x1, sa, st, st + kNtATile, sw64_off(r, c));
+                    }
+                    fence_proxy_async();
+                    mbar_arrive(&full[mr.idx]);
+                    mbar_arrive(&sempty[sr.idx]);
+                }
             }
-            fence_proxy_async();
-            mbar_arrive(&full[stage]);
-            mbar_arrive(&sempty[slot]);
-        }
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
         const uint32_t idesc = idesc_f16(kBM, p.n_pad);
-        uint32_t it = 0, t = 0;
+        Ring mr;
+        uint32_t t = 0;
         for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
             const uint32_t acc = t & 1;
             const uint32_t d_tmem = tmem_base + acc * 256;
             mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
             tc_fence_after();
-            for (int kbg = 0; kbg < kb_total; ++kbg, ++it) {
-                const int stage = it % kNtStages;
-                mbar_wait(&full[stage], (it / kNtStages) & 1);
+            for (int kbg = 0; kbg < kb_total; ++kbg, mr.next(kNtStages)) {
+                mbar_wait(&full[mr.idx], mr.phase);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint8_t* st = smem + stage * kNtStage;
+                    const uint8_t* st = smem + mr.idx * kNtStage;
                     const uint64_t ahi = desc_sw64(smem_u32(st)), alo = desc_sw64(smem_u32(st + kNtATile));
                     const uint64_t bhi = desc_sw64(smem_u32(st + 2 * kNtATile));
                     const uint64_t blo = desc_sw64(smem_u32(st + 2 * kNtATile + btile));
@@ -369,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
                         mma_f16(d_tmem, ahi + adv, blo + adv, idesc, 1u);
                         mma_f16(d_tmem, alo + adv, bhi + adv, idesc, 1u);
                     }
-                    mma_commit(&empty[stage]);
+                    mma_commit(&empty[mr.idx]);
                     if (kbg == kb_total - 1) mma_commit(&tfull[acc]);
                 }
                 __syncwarp();
