@@ -550,7 +550,8 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
             dB2 = up(B2, sizeof(float) * (b2_nn ? int64_t(K2) * ldb2 : int64_t(N) * ldb2));
         }
         if (epi == kEpiRowScale) dS = up(scale, sizeof(float) * M);
-        DevBuf<float> dC(std::max<int64_t>(M * N, 1));
+        const int64_t ldc = (N + 3) / 4 * 4;  // 16-byte output rows, as the trainer's buffers are
+        DevBuf<float> dC(std::max<int64_t>(M * ldc, 1));
         const MatA a1{reinterpret_cast<const float*>(dA1.get()), lda1,
                       rows1 ? reinterpret_cast<const int32_t*>(dR1.get()) : nullptr, K1};
         const MatB b1{reinterpret_cast<const float*>(dB1.get()), ldb1, b1_nn != 0};
@@ -565,13 +566,15 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
             BImage i1, i2;
             prep_bimage(i1, b1, N, K1, s);
             if (K2 > 0) prep_bimage(i2, b2, N, K2, s);
-            gemm_f16x3(a1, am.get(), i1, K2 > 0 ? &a2 : nullptr, am.get() + 1, K2 > 0 ? &i2 : nullptr, dC.get(), N, M,
-                       N, epi, sc, nullptr, s);
+            gemm_f16x3(a1, am.get(), i1, K2 > 0 ? &a2 : nullptr, am.get() + 1, K2 > 0 ? &i2 : nullptr, dC.get(), ldc,
+                       M, N, epi, sc, nullptr, s);
             SC_CUDA(cudaStreamSynchronize(s));
         } else {
-            gemm_nt(a1, b1, K2 > 0 ? &a2 : nullptr, K2 > 0 ? &b2 : nullptr, dC.get(), N, M, N, epi, sc, s);
+            gemm_nt(a1, b1, K2 > 0 ? &a2 : nullptr, K2 > 0 ? &b2 : nullptr, dC.get(), ldc, M, N, epi, sc, s);
         }
-        d2h(C, dC.get(), M * N, s);
+        if (M > 0)
+            SC_CUDA(cudaMemcpy2DAsync(C, sizeof(float) * N, dC.get(), sizeof(float) * ldc, sizeof(float) * N, M,
+                                      cudaMemcpyDeviceToHost, s));
         SC_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -49,6 +49,12 @@ constexpr int kEpilogue = 128;          // warps 8-11 (warp % 4 = TMEM lane quar
 constexpr int kMmaWarp = 12;
 constexpr int kLoadWarp = 13;
 constexpr int kThreads = 14 * 32;
+// NT uses 8 epilogue warps (warps 8-15: two per TMEM lane quarter, even / odd
+// 32-column chunks), then the MMA and loader warps.
+constexpr int kNtEpiWarps = 8;
+constexpr int kNtMmaWarp = 16;
+constexpr int kNtLoadWarp = 17;
+constexpr int kNtThreads = 18 * 32;
 
 // NT: 32-deep k-stages, fp16 SW64 tiles (64 B rows)
 constexpr int kNtBK = 32;
@@ -58,7 +64,8 @@ constexpr int kNtATile = kBM * 64;                    // one (hi or lo) A tile
 constexpr int kNtBTileMax = kMaxN * 64;               // one (hi or lo) B tile
 constexpr int kNtStage = 2 * kNtATile + 2 * kNtBTileMax;
 constexpr int kNtStgBytes = kBM * kNtBK * 4;          // 128 rows x 32 fp32
-constexpr int kNtEpiBytes = 4 * 32 * 33 * 4;          // epilogue transpose buffers
+constexpr int kNtEpiBuf = 32 * 32 * 4;                // one 32 x 32 fp32 output box (SW128)
+constexpr int kNtEpiBytes = kNtEpiWarps * kNtEpiBuf;  // one store box per epilogue warp
 constexpr int kNtBarOff = kNtStages * kNtStage + kNtStg * kNtStgBytes + kNtEpiBytes;
 constexpr int kNtSmemBytes = kNtBarOff + 256 + 1024;
 
@@ -90,6 +97,7 @@ struct Src {
 
 struct alignas(64) Params {
     Src src[2];
+    CUtensorMap tmap_c;   // 2D map over C (box 32 cols x 32 rows, fp32, SWIZZLE_128B; stores clip at M, N)
     int nsrc;
     int64_t M;
     int32_t N, n_pad;
@@ -211,6 +219,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -237,7 +256,8 @@ __device__ __forceinline__ void mask8(float4& x0, float4& x1, int valid) {
 }
 
 
-__global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
+template <int EPI, bool AMAX>
+__global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stg_base = smem + kNtStages * kNtStage;
@@ -263,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
         kt = min(kt, scale_exp(*p.src[s].amax_a) + kb_exp[s]);
     }
 
-    if (warp == kMmaWarp) {
+    if (warp == kNtMmaWarp) {
         if (lane == 0) {
             for (int s = 0; s < kNtStages; ++s) {
                 mbar_init(&full[s], kConv);
@@ -275,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
-                mbar_init(&tempty[s], kEpilogue);
+                mbar_init(&tempty[s], kNtEpiWarps * 32);
             }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
@@ -292,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
     int kb_total = 0;
     for (int s = 0; s < p.nsrc; ++s) kb_total += p.src[s].kblocks;
 
-    if (warp == kLoadWarp) {
+    if (warp == kNtLoadWarp) {
         // ================= loader: one 2D TMA per stage, HBM -> fp32 staging =================
         // box 32 k (128 B) x 128 rows, SWIZZLE_128B; out-of-range rows / k are zero-filled
         Ring ring;
@@ -342,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
                     mbar_arrive(&sempty[sr.idx]);
                 }
             }
-    } else if (warp == kMmaWarp) {
+    } else if (warp == kNtMmaWarp) {
         // ================= MMA issuer =================
         const uint32_t idesc = idesc_f16(kBM, p.n_pad);
         Ring mr;
@@ -374,10 +394,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
             }
         }
     } else {
-        // ================= epilogue (warps 8-11) =================
-        const int ew = warp & 3;  // TMEM lanes 32*ew .. 32*ew+31
+        // ================= epilogue (warps 8-15) =================
+        // tcgen05.ld (lane = row) -> unscale / ReLU / row-scale / |max| -> SW128 smem box -> TMA store
+        // (the store clips rows >= M and columns >= N). n_pad is a multiple of 32 and the B image
+        // is zero beyond N, as are TMA-filled A rows beyond M, so every chunk is full and padded
+        // entries are exactly 0 (they cannot raise |max|).
+        const int ew = warp & 3;                    // TMEM lanes 32*ew .. 32*ew+31
+        const int half = (warp - kConvWarps) >> 2;  // even / odd 32-column chunks
         const float unscale = ldexpf(1.f, -kt);
-        float* stg = epi_base + ew * (32 * 33);
+        uint8_t* box = reinterpret_cast<uint8_t*>(epi_base) + (warp - kConvWarps) * kNtEpiBuf;
         float amx = 0.f;
         uint32_t t = 0;
         for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
@@ -385,41 +410,43 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_f16x3_kernel(const __grid_co
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
             const int64_t row0 = tile * kBM + ew * 32;  // this warp's 32 output rows
-            const int64_t row = row0 + lane;
-            const bool live = row < p.M;
-            const float sc = (p.epi == kEpiRowScale && live) ? p.row_scale[row] : 1.f;
-            const int rows_here = p.M - row0 < 32 ? static_cast<int>(p.M - row0) : 32;
-            for (int c0 = 0; c0 < p.n_pad; c0 += 32) {
+            float sc = 1.f;
+            if (EPI == kEpiRowScale && row0 + lane < p.M) sc = p.row_scale[row0 + lane];
+            for (int c0 = half * 32; c0 < p.n_pad; c0 += 64) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
-                // lane owns row `row`; transpose through smem so each store is a full 128 B row segment
+                if (lane == 0) bulk_wait_read<0>();  // the previous store has read the box
+                __syncwarp();
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    float x = __uint_as_float(r[q]) * unscale;
-                    if (p.epi == kEpiRelu) x = fmaxf(x, 0.f);
-                    else if (p.epi == kEpiRowScale) x = sc * x;
-                    if (live && c0 + q < p.N) amx = fmaxf(amx, fabsf(x));
-                    stg[lane * 33 + q] = x;
+                for (int j = 0; j < 8; ++j) {
+                    float x[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        float v = __uint_as_float(r[4 * j + q]) * unscale;
+                        if (EPI == kEpiRelu) v = fmaxf(v, 0.f);
+                        if (EPI == kEpiRowScale) v = sc * v;
+                        if (AMAX) amx = fmaxf(amx, fabsf(v));
+                        x[q] = v;
+                    }
+                    *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                        make_float4(x[0], x[1], x[2], x[3]);
                 }
+                fence_proxy_async();
                 __syncwarp();
-                const int col = c0 + lane;
-                if (col < p.N) {
-                    float* cbase = p.C + row0 * p.ldc + col;
-                    for (int rr = 0; rr < rows_here; ++rr) cbase[rr * p.ldc] = stg[rr * 33 + lane];
-                }
-                __syncwarp();
+                if (lane == 0 && row0 < p.M) tma_store_2d(&p.tmap_c, box, c0, static_cast<int32_t>(row0));
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
-        if (p.amax_out) {
+        if (lane == 0) bulk_wait_read<0>();
+        if (AMAX) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
             if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out), __float_as_uint(amx));
         }
     }
     __syncthreads();
-    if (warp == kMmaWarp) {
+    if (warp == kNtMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
     }
@@ -834,6 +861,11 @@ bool tc_supported(const MatA& a1, const MatA* a2, int32_t N) {
     return N >= 1 && N <= tc::kMaxN && ok(a1) && (!a2 || ok(*a2));
 }
 
+bool tc_out_supported(const float* C, int64_t ldc) {
+    // C is written by 2D TMA stores: 16 B aligned base and rows
+    return (reinterpret_cast<uintptr_t>(C) % 16) == 0 && (ldc % 4) == 0;
+}
+
 bool tn_supported(const MatT& a, const MatT& b1, const MatT* b2) {
     auto ok = [](const MatT& x) {
         return !x.rows && (x.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x.ptr) % 16) == 0 && x.ld >= x.cols;
@@ -845,7 +877,7 @@ bool tn_supported(const MatT& a, const MatT& b1, const MatT* b2) {
 void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s) {
     im.N = N;
     im.K = K;
-    im.n_pad = std::max(16, (N + 15) / 16 * 16);
+    im.n_pad = (N + 31) / 32 * 32;  // whole 32-column TMEM chunks in the epilogue
     im.kblocks = (K + tc::kNtBK - 1) / tc::kNtBK;
     im.img.ensure(static_cast<size_t>(im.kblocks) * 2 * im.n_pad * 64);
     im.bexp.ensure(1);
@@ -860,13 +892,8 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
                 float* amax_out, cudaStream_t s) {
     if (M <= 0 || N <= 0) return;
-    if (!tc_supported(a1, a2, N)) throw std::logic_error("gemm_f16x3: unsupported operand layout");
-    static bool attr_set = false;
-    if (!attr_set) {
-        SC_CUDA(cudaFuncSetAttribute(tc::gemm_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::kNtSmemBytes));
-        attr_set = true;
-    }
+    if (!tc_supported(a1, a2, N) || !tc_out_supported(C, ldc))
+        throw std::logic_error("gemm_f16x3: unsupported operand layout");
     tc::Params p{};
     p.nsrc = a2 ? 2 : 1;
     const MatA* as[2] = {&a1, a2};
@@ -884,6 +911,7 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
         S.bexp = bs[i]->bexp.get();
         encode_2d(&S.tmap, S.a, M, S.K, S.lda, tc::kNtBK, tc::kBM);
     }
+    encode_2d(&p.tmap_c, C, M, N, ldc, 32, 32);
     p.M = M;
     p.N = N;
     p.n_pad = b1.n_pad;
@@ -894,7 +922,19 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.amax_out = amax_out;
     p.tiles = (M + tc::kBM - 1) / tc::kBM;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, num_sms()));
-    tc::gemm_f16x3_kernel<<<grid, tc::kThreads, tc::kNtSmemBytes, s>>>(p);
+    auto launch = [&](auto kernel) {
+        SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kNtSmemBytes));
+        kernel<<<grid, tc::kNtThreads, tc::kNtSmemBytes, s>>>(p);
+    };
+    const bool amax = amax_out != nullptr;
+    switch (epi) {
+        case kEpiNone: amax ? launch(tc::gemm_f16x3_kernel<kEpiNone, true>) : launch(tc::gemm_f16x3_kernel<kEpiNone, false>); break;
+        case kEpiRelu: amax ? launch(tc::gemm_f16x3_kernel<kEpiRelu, true>) : launch(tc::gemm_f16x3_kernel<kEpiRelu, false>); break;
+        case kEpiRowScale:
+            amax ? launch(tc::gemm_f16x3_kernel<kEpiRowScale, true>) : launch(tc::gemm_f16x3_kernel<kEpiRowScale, false>);
+            break;
+        default: throw std::logic_error("gemm_f16x3: bad epilogue");
+    }
     SC_LAUNCH_CHECK();
     count_launch();
 }
@@ -915,7 +955,7 @@ void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b
                 const float* amax2, const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi,
                 const float* row_scale, float* amax_out) {
     cudaStream_t s = t->ctx->stream;
-    if (enabled && tc_supported(a1, a2, N)) {
+    if (enabled && tc_supported(a1, a2, N) && tc_out_supported(C, ldc)) {
         const BImage& i1 = image(b1, N, a1.K, s);
         const BImage* i2 = a2 ? &image(*b2, N, a2->K, s) : nullptr;
         gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s);

@@ -22,6 +22,7 @@ struct BImage {
 };
 
 bool tc_supported(const MatA& a1, const MatA* a2, int32_t N);
+bool tc_out_supported(const float* C, int64_t ldc);
 bool tn_supported(const MatT& a, const MatT& b1, const MatT* b2);
 void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s);
 
