@@ -32,7 +32,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "gemm_tc.cuh"
 #include "internal.hpp"
@@ -58,16 +60,10 @@ constexpr int kNtThreads = 18 * 32;
 
 // NT: 32-deep k-stages, fp16 SW64 tiles (64 B rows)
 constexpr int kNtBK = 32;
-constexpr int kNtStages = 3;                          // MMA operand stages
-constexpr int kNtStg = 3;                             // fp32 staging stages
 constexpr int kNtATile = kBM * 64;                    // one (hi or lo) A tile
-constexpr int kNtBTileMax = kMaxN * 64;               // one (hi or lo) B tile
-constexpr int kNtStage = 2 * kNtATile + 2 * kNtBTileMax;
 constexpr int kNtStgBytes = kBM * kNtBK * 4;          // 128 rows x 32 fp32
 constexpr int kNtEpiBuf = 32 * 32 * 4;                // one 32 x 32 fp32 output box (SW128)
 constexpr int kNtEpiBytes = kNtEpiWarps * kNtEpiBuf;  // one store box per epilogue warp
-constexpr int kNtBarOff = kNtStages * kNtStage + kNtStg * kNtStgBytes + kNtEpiBytes;
-constexpr int kNtSmemBytes = kNtBarOff + 256 + 1024;
 
 // TN: 32-row stages, fp16 MN-major SW128 tiles
 constexpr int kTnBK = 32;
@@ -91,6 +87,7 @@ struct Src {
     int32_t K;            // valid k (multiple of 4)
     int32_t kblocks;      // ceil(K / 32)
     const uint8_t* bimg;  // kblocks x [hi tile | lo tile], each n_pad x 64 B (32 k, SW64)
+    CUtensorMap tmap_b;   // the same image as 2D [kblocks * 2 * n_pad rows x 64 B] (pair kernel: half-tile boxes)
     const float* amax_a;  // max|A| (device scalar)
     const int32_t* bexp;  // power-of-two exponent B was scaled by (device scalar)
 };
@@ -256,23 +253,129 @@ __device__ __forceinline__ void mask8(float4& x0, float4& x1, int valid) {
 }
 
 
-template <int EPI, bool AMAX>
+// ---- CTA-pair (cta_group::2) helpers ----------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+// Arrive on a barrier of either CTA of the cluster. Default (.release.cta) semantics, as the
+// tensor-core pipelines use: the data it publishes was written to the arriving CTA's own shared
+// memory and made visible to the async proxy by fence.proxy.async beforehand.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2D TMA issued by either CTA of a pair; completion bytes are counted on the leader's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                                 uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
+        : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void mma_f16_g(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (PAIR)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    else
+        mma_f16(d_tmem, a, b, idesc, acc);
+}
+// MMA completion -> barrier at the same offset in both CTAs of the pair (or the local one).
+template <bool PAIR>
+__device__ __forceinline__ void mma_commit_g(uint64_t* bar) {
+    if constexpr (PAIR)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(bar)),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
+    else
+        mma_commit(bar);
+}
+template <bool PAIR>
+__device__ __forceinline__ void tmem_alloc_g(uint32_t* slot) {
+    if constexpr (PAIR) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+}
+template <bool PAIR>
+__device__ __forceinline__ void tmem_dealloc_g(uint32_t base) {
+    if constexpr (PAIR)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(512));
+    else
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(512));
+}
+
+// Shared-memory plan of the NT kernel. PAIR: a CTA pair (cluster of 2, cta_group::2)
+// computes a 256-row tile with one M=256 MMA stream; each CTA converts its own
+// 128 A rows and holds half of the weight image's rows, so the per-SM operand
+// bytes (TMA in, tensor-core reads) drop by a third and the freed shared memory
+// deepens both rings.
+template <bool PAIR>
+struct NtCfg {
+    static constexpr int kStages = PAIR ? 4 : 3;                    // MMA operand stages
+    static constexpr int kStg = PAIR ? 4 : 3;                       // fp32 staging stages
+    static constexpr int kBTile = (PAIR ? kMaxN / 2 : kMaxN) * 64;  // one (hi or lo) B tile, this CTA's rows
+    static constexpr int kStage = 2 * kNtATile + 2 * kBTile;
+    static constexpr int kStgOff = kStages * kStage;
+    static constexpr int kEpiOff = kStgOff + kStg * kNtStgBytes;
+    static constexpr int kBarOff = kEpiOff + kNtEpiBytes;
+    static constexpr int kSmem = kBarOff + 256 + 1024;
+    static constexpr int kRows = PAIR ? 2 * kBM : kBM;              // output rows per tile
+};
+static_assert(NtCfg<true>::kSmem <= 232448 && NtCfg<false>::kSmem <= 232448, "NT shared memory");
+
+template <int EPI, bool AMAX, bool PAIR>
 __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
+    using Cfg = NtCfg<PAIR>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* stg_base = smem + kNtStages * kNtStage;
-    float* epi_base = reinterpret_cast<float*>(stg_base + kNtStg * kNtStgBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kNtBarOff);
-    uint64_t* full = bars;                              // [kNtStages] converters -> MMA
-    uint64_t* empty = full + kNtStages;                 // [kNtStages] MMA -> converters
-    uint64_t* sfull = empty + kNtStages;                // [kNtStg] loader (tx) -> converters
-    uint64_t* sempty = sfull + kNtStg;                  // [kNtStg] converters -> loader
-    uint64_t* tfull = sempty + kNtStg;                  // [2] MMA -> epilogue
-    uint64_t* tempty = tfull + 2;                       // [2] epilogue -> MMA
+    uint8_t* stg_base = smem + Cfg::kStgOff;
+    uint8_t* epi_base = smem + Cfg::kEpiOff;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
+    uint64_t* full = bars;                              // [kStages] converters + B TMA -> MMA (leader's)
+    uint64_t* empty = full + Cfg::kStages;              // [kStages] MMA -> converters
+    uint64_t* sfull = empty + Cfg::kStages;             // [kStg] loader (tx) -> converters
+    uint64_t* sempty = sfull + Cfg::kStg;               // [kStg] converters -> loader
+    uint64_t* tfull = sempty + Cfg::kStg;               // [2] MMA -> epilogue
+    uint64_t* tempty = tfull + 2;                       // [2] epilogue -> MMA (leader's)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t btile = static_cast<uint32_t>(p.n_pad) * 64u;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int64_t tile0 = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
+    const int64_t tstep = PAIR ? (gridDim.x >> 1) : gridDim.x;
+    const int32_t nloc = PAIR ? (p.n_pad >> 1) : p.n_pad;  // weight rows held by this CTA
+    const uint32_t bh = static_cast<uint32_t>(nloc) * 64u;  // bytes of one local (hi or lo) B tile
 
     // Per-source operand scales: A_s gets 2^(kt - kB_s) so that every source's
     // products carry the same total scale 2^kt (they share one accumulator).
@@ -285,29 +388,31 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
 
     if (warp == kNtMmaWarp) {
         if (lane == 0) {
-            for (int s = 0; s < kNtStages; ++s) {
-                mbar_init(&full[s], kConv);
+            for (int s = 0; s < Cfg::kStages; ++s) {
+                mbar_init(&full[s], kConvWarps * (PAIR ? 2 : 1));
                 mbar_init(&empty[s], 1);
             }
-            for (int s = 0; s < kNtStg; ++s) {
+            for (int s = 0; s < Cfg::kStg; ++s) {
                 mbar_init(&sfull[s], 1);
-                mbar_init(&sempty[s], kConv);
+                mbar_init(&sempty[s], kConvWarps);
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
-                mbar_init(&tempty[s], kNtEpiWarps * 32);
+                mbar_init(&tempty[s], kNtEpiWarps * (PAIR ? 2 : 1));
             }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncwarp();
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        tmem_alloc_g<PAIR>(tmem_slot);
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync();  // peer barriers initialised before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // the pair's leader (rank 0) owns the barriers the MMA issuer waits on
+    const uint32_t full_l = PAIR ? mapa(smem_u32(full), 0) : smem_u32(full);
+    const uint32_t tempty_l = PAIR ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
 
     int kb_total = 0;
     for (int s = 0; s < p.nsrc; ++s) kb_total += p.src[s].kblocks;
@@ -316,14 +421,14 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
         // ================= loader: one 2D TMA per stage, HBM -> fp32 staging =================
         // box 32 k (128 B) x 128 rows, SWIZZLE_128B; out-of-range rows / k are zero-filled
         Ring ring;
-        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x)
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
             for (int src = 0; src < p.nsrc; ++src)
-                for (int kb = 0; kb < p.src[src].kblocks; ++kb, ring.next(kNtStg)) {
+                for (int kb = 0; kb < p.src[src].kblocks; ++kb, ring.next(Cfg::kStg)) {
                     mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
                     if (lane == 0) {
                         mbar_arrive_expect_tx(&sfull[ring.idx], kNtStgBytes);
                         tma_load_2d(stg_base + ring.idx * kNtStgBytes, &p.src[src].tmap, kb * kNtBK,
-                                    static_cast<int32_t>(tile * kBM), &sfull[ring.idx]);
+                                    static_cast<int32_t>(tile * Cfg::kRows + rank * kBM), &sfull[ring.idx]);
                     }
                     __syncwarp();
                 }
@@ -331,21 +436,31 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
         // ================= converters: staging fp32 -> scaled fp16 hi/lo (SW64) =================
         // Row-fastest mapping: 8 consecutive threads read the same chunk of 8 different rows, which
         // the 128 B swizzle spreads over distinct banks (conflict-free loads and SW64 stores).
+        // Thread 0 also fetches this CTA's rows of the stage's weight image.
         const int tid = threadIdx.x;
         const float sa0 = ldexpf(1.f, kt - kb_exp[0]), sa1 = ldexpf(1.f, kt - kb_exp[1]);
         Ring mr, sr;  // MMA-operand ring, staging ring
-        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x)
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
             for (int src = 0; src < p.nsrc; ++src) {
                 const Src& S = p.src[src];
                 const float sa = src ? sa1 : sa0;
-                for (int kb = 0; kb < S.kblocks; ++kb, mr.next(kNtStages), sr.next(kNtStg)) {
-                    uint8_t* st = smem + mr.idx * kNtStage;
+                for (int kb = 0; kb < S.kblocks; ++kb, mr.next(Cfg::kStages), sr.next(Cfg::kStg)) {
+                    uint8_t* st = smem + mr.idx * Cfg::kStage;
                     const uint8_t* sg = stg_base + sr.idx * kNtStgBytes;
                     mbar_wait(&empty[mr.idx], mr.phase ^ 1);
                     if (tid == 0) {
-                        mbar_expect_tx(&full[mr.idx], 2 * btile);
-                        bulk_g2s(st + 2 * kNtATile, S.bimg + static_cast<int64_t>(kb) * 2 * btile, 2 * btile,
-                                 &full[mr.idx]);
+                        if constexpr (PAIR) {
+                            // image rows: [kb][plane][n_pad]; this CTA's half starts at rank * nloc
+                            const uint32_t fb = full_l + mr.idx * 8;
+                            if (rank == 0) mbar_expect_tx(&full[mr.idx], 4 * bh);  // both halves, hi + lo
+                            const int32_t r0 = (kb * 2) * p.n_pad + static_cast<int32_t>(rank) * nloc;
+                            tma_load_2d_pair(st + 2 * kNtATile, &S.tmap_b, 0, r0, fb);
+                            tma_load_2d_pair(st + 2 * kNtATile + bh, &S.tmap_b, 0, r0 + p.n_pad, fb);
+                        } else {
+                            mbar_expect_tx(&full[mr.idx], 2 * bh);
+                            bulk_g2s(st + 2 * kNtATile, S.bimg + static_cast<int64_t>(kb) * 2 * bh, 2 * bh,
+                                     &full[mr.idx]);
+                        }
                     }
                     mbar_wait(&sfull[sr.idx], sr.phase);
 #pragma unroll
@@ -358,39 +473,49 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                         split8_store(x0, x1, sa, st, st + kNtATile, sw64_off(r, c));
                     }
                     fence_proxy_async();
-                    mbar_arrive(&full[mr.idx]);
-                    mbar_arrive(&sempty[sr.idx]);
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (PAIR) mbar_arrive_cluster(full_l + mr.idx * 8);
+                        else mbar_arrive(&full[mr.idx]);
+                        mbar_arrive(&sempty[sr.idx]);
+                    }
                 }
             }
     } else if (warp == kNtMmaWarp) {
-        // ================= MMA issuer =================
-        const uint32_t idesc = idesc_f16(kBM, p.n_pad);
-        Ring mr;
-        uint32_t t = 0;
-        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
-            const uint32_t acc = t & 1;
-            const uint32_t d_tmem = tmem_base + acc * 256;
-            mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
-            tc_fence_after();
-            for (int kbg = 0; kbg < kb_total; ++kbg, mr.next(kNtStages)) {
-                mbar_wait(&full[mr.idx], mr.phase);
+        // ================= MMA issuer (the pair's leader only) =================
+        if (PAIR && rank != 0) {
+            // the peer's tensor core work is issued by the leader
+        } else {
+            const uint32_t idesc = idesc_f16(Cfg::kRows, p.n_pad);
+            Ring mr;
+            uint32_t t = 0;
+            for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t) {
+                const uint32_t acc = t & 1;
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                if constexpr (PAIR) mbar_wait_cluster(&tempty[acc], ((t >> 1) & 1) ^ 1);
+                else mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint8_t* st = smem + mr.idx * kNtStage;
-                    const uint64_t ahi = desc_sw64(smem_u32(st)), alo = desc_sw64(smem_u32(st + kNtATile));
-                    const uint64_t bhi = desc_sw64(smem_u32(st + 2 * kNtATile));
-                    const uint64_t blo = desc_sw64(smem_u32(st + 2 * kNtATile + btile));
+                for (int kbg = 0; kbg < kb_total; ++kbg, mr.next(Cfg::kStages)) {
+                    if constexpr (PAIR) mbar_wait_cluster(&full[mr.idx], mr.phase);
+                    else mbar_wait(&full[mr.idx], mr.phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint8_t* st = smem + mr.idx * Cfg::kStage;
+                        const uint64_t ahi = desc_sw64(smem_u32(st)), alo = desc_sw64(smem_u32(st + kNtATile));
+                        const uint64_t bhi = desc_sw64(smem_u32(st + 2 * kNtATile));
+                        const uint64_t blo = desc_sw64(smem_u32(st + 2 * kNtATile + bh));
 #pragma unroll
-                    for (int k = 0; k < kNtBK / 16; ++k) {
-                        const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;  // 16 fp16 = 32 B along K
-                        mma_f16(d_tmem, ahi + adv, bhi + adv, idesc, (kbg | k) ? 1u : 0u);
-                        mma_f16(d_tmem, ahi + adv, blo + adv, idesc, 1u);
-                        mma_f16(d_tmem, alo + adv, bhi + adv, idesc, 1u);
+                        for (int k = 0; k < kNtBK / 16; ++k) {
+                            const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;  // 16 fp16 = 32 B along K
+                            mma_f16_g<PAIR>(d_tmem, ahi + adv, bhi + adv, idesc, (kbg | k) ? 1u : 0u);
+                            mma_f16_g<PAIR>(d_tmem, ahi + adv, blo + adv, idesc, 1u);
+                            mma_f16_g<PAIR>(d_tmem, alo + adv, bhi + adv, idesc, 1u);
+                        }
+                        mma_commit_g<PAIR>(&empty[mr.idx]);
+                        if (kbg == kb_total - 1) mma_commit_g<PAIR>(&tfull[acc]);
                     }
-                    mma_commit(&empty[mr.idx]);
-                    if (kbg == kb_total - 1) mma_commit(&tfull[acc]);
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
     } else {
@@ -402,14 +527,14 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
         const int ew = warp & 3;                    // TMEM lanes 32*ew .. 32*ew+31
         const int half = (warp - kConvWarps) >> 2;  // even / odd 32-column chunks
         const float unscale = ldexpf(1.f, -kt);
-        uint8_t* box = reinterpret_cast<uint8_t*>(epi_base) + (warp - kConvWarps) * kNtEpiBuf;
+        uint8_t* box = epi_base + (warp - kConvWarps) * kNtEpiBuf;
         float amx = 0.f;
         uint32_t t = 0;
-        for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++t) {
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t) {
             const uint32_t acc = t & 1;
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
-            const int64_t row0 = tile * kBM + ew * 32;  // this warp's 32 output rows
+            const int64_t row0 = tile * Cfg::kRows + rank * kBM + ew * 32;  // this warp's 32 output rows
             float sc = 1.f;
             if (EPI == kEpiRowScale && row0 + lane < p.M) sc = p.row_scale[row0 + lane];
             for (int c0 = half * 32; c0 < p.n_pad; c0 += 64) {
@@ -436,7 +561,11 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                 if (lane == 0 && row0 < p.M) tma_store_2d(&p.tmap_c, box, c0, static_cast<int32_t>(row0));
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (PAIR) mbar_arrive_cluster(tempty_l + acc * 8);
+                else mbar_arrive(&tempty[acc]);
+            }
         }
         if (lane == 0) bulk_wait_read<0>();
         if (AMAX) {
@@ -445,10 +574,12 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
             if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out), __float_as_uint(amx));
         }
     }
-    __syncthreads();
+    tc_fence_before();
+    if constexpr (PAIR) cluster_sync();  // no remote arrivals / tensor-core work left in flight
+    else __syncthreads();
     if (warp == kNtMmaWarp) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+        tmem_dealloc_g<PAIR>(tmem_base);
     }
 }
 
@@ -800,6 +931,26 @@ void encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, 
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
+// 2D map over a pre-split weight image viewed as [rows x 32 fp16] (64 B rows, already
+// in SW64 order, copied verbatim), box = `box_rows` rows.
+void encode_img(CUtensorMap* map, const uint8_t* img, int64_t rows, uint32_t box_rows) {
+    const cuuint64_t gdim[2] = {32, static_cast<cuuint64_t>(rows)};
+    const cuuint64_t gstride[1] = {64};
+    const cuuint32_t box[2] = {32, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint8_t*>(img), gdim, gstride,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (image) failed (" + std::to_string(int(r)) + ")");
+}
+// NT GEMMs run on CTA pairs (cta_group::2) unless SC_NT_PAIR=0.
+bool nt_pair_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SC_NT_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 }  // namespace
 
 int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M) {
@@ -920,18 +1071,54 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.epi = epi;
     p.row_scale = row_scale;
     p.amax_out = amax_out;
-    p.tiles = (M + tc::kBM - 1) / tc::kBM;
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, num_sms()));
-    auto launch = [&](auto kernel) {
-        SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kNtSmemBytes));
-        kernel<<<grid, tc::kNtThreads, tc::kNtSmemBytes, s>>>(p);
+    const bool pair = nt_pair_enabled();
+    if (pair)
+        for (int i = 0; i < p.nsrc; ++i)
+            encode_img(&p.src[i].tmap_b, bs[i]->img.get(), int64_t(bs[i]->kblocks) * 2 * bs[i]->n_pad, bs[i]->n_pad / 2);
+    const int64_t rows_per_tile = pair ? 2 * tc::kBM : tc::kBM;
+    p.tiles = (M + rows_per_tile - 1) / rows_per_tile;
+    auto launch = [&](auto kernel, int smem_bytes) {
+        SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        cfg.blockDim = dim3(tc::kNtThreads);
+        cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes);
+        cfg.stream = s;
+        if (pair) {
+            const int64_t pairs = std::min<int64_t>(p.tiles, std::max(1, num_sms() / 2));
+            cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        } else {
+            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(p.tiles, num_sms())));
+        }
+        SC_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
     };
+    auto dispatch = [&](auto epi_tag, auto amax_tag) {
+        constexpr int E = decltype(epi_tag)::value;
+        constexpr bool A = decltype(amax_tag)::value;
+        if (pair) launch(tc::gemm_f16x3_kernel<E, A, true>, tc::NtCfg<true>::kSmem);
+        else launch(tc::gemm_f16x3_kernel<E, A, false>, tc::NtCfg<false>::kSmem);
+    };
+    using T = std::true_type;
+    using F = std::false_type;
     const bool amax = amax_out != nullptr;
     switch (epi) {
-        case kEpiNone: amax ? launch(tc::gemm_f16x3_kernel<kEpiNone, true>) : launch(tc::gemm_f16x3_kernel<kEpiNone, false>); break;
-        case kEpiRelu: amax ? launch(tc::gemm_f16x3_kernel<kEpiRelu, true>) : launch(tc::gemm_f16x3_kernel<kEpiRelu, false>); break;
+        case kEpiNone:
+            amax ? dispatch(std::integral_constant<int, kEpiNone>{}, T{})
+                 : dispatch(std::integral_constant<int, kEpiNone>{}, F{});
+            break;
+        case kEpiRelu:
+            amax ? dispatch(std::integral_constant<int, kEpiRelu>{}, T{})
+                 : dispatch(std::integral_constant<int, kEpiRelu>{}, F{});
+            break;
         case kEpiRowScale:
-            amax ? launch(tc::gemm_f16x3_kernel<kEpiRowScale, true>) : launch(tc::gemm_f16x3_kernel<kEpiRowScale, false>);
+            amax ? dispatch(std::integral_constant<int, kEpiRowScale>{}, T{})
+                 : dispatch(std::integral_constant<int, kEpiRowScale>{}, F{});
             break;
         default: throw std::logic_error("gemm_f16x3: bad epilogue");
     }
