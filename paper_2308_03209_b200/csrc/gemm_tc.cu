@@ -47,7 +47,6 @@ constexpr int kBM = 128;  // UMMA M (cta_group::1)
 constexpr int kMaxN = 256;
 constexpr int kConvWarps = 8;
 constexpr int kConv = kConvWarps * 32;  // converter threads (warps 0-7)
-constexpr int kEpilogue = 128;          // warps 8-11 (warp % 4 = TMEM lane quarter)
 constexpr int kMmaWarp = 12;
 constexpr int kLoadWarp = 13;
 constexpr int kThreads = 14 * 32;
@@ -67,16 +66,8 @@ constexpr int kNtEpiBytes = kNtEpiWarps * kNtEpiBuf;  // one store box per epilo
 
 // TN: 32-row stages, fp16 MN-major SW128 tiles
 constexpr int kTnBK = 32;
-constexpr int kTnStages = 2;
-constexpr int kTnStg = 2;
 constexpr int kTnATile = kBM * kTnBK * 2;             // 128 cols x 32 rows fp16 = 8 KB
-constexpr int kTnBTile = kMaxN * kTnBK * 2;           // 256 cols x 32 rows fp16 = 16 KB
-constexpr int kTnStage = 2 * kTnATile + 2 * kTnBTile;
 constexpr int kTnStgA = kTnBK * kBM * 4;              // 32 rows x 128 fp32 = 16 KB
-constexpr int kTnStgB = kTnBK * kMaxN * 4;            // 32 rows x 256 fp32 = 32 KB
-constexpr int kTnEpiOff = kTnStages * kTnStage + kTnStg * (kTnStgA + kTnStgB);
-constexpr int kTnBarOff = kTnEpiOff + 4 * 32 * 33 * 4;  // + drain transpose buffers
-constexpr int kTnSmemBytes = kTnBarOff + 256 + 1024;
 constexpr int kChunkKb = 32;                          // 1024 rows per TMEM accumulation (TN)
 constexpr int kTnBox = kTnBK * 128;                   // one 32-column x 32-row fp32 TMA box
 
@@ -686,26 +677,56 @@ __device__ __forceinline__ uint32_t mn_off(uint32_t mn, uint32_t k) {
     return (mn >> 6) * kTnLbo + (k >> 3) * kTnSbo + (k & 7) * 128 + ((((mn & 63) >> 3) ^ (k & 7)) << 4);
 }
 
+// Shared-memory plan of the TN kernel. PAIR: a CTA pair (cta_group::2) owns a
+// 256-column slice of A' (M = 256, 128 per CTA) and splits the B' tile's columns
+// between its two CTAs, so each B' element is converted once per pair instead
+// of once per 128-column A' tile, and per-SM conversion work drops by a third.
+template <bool PAIR>
+struct TnCfg {
+    static constexpr int kStages = PAIR ? 3 : 2;
+    static constexpr int kStg = PAIR ? 3 : 2;
+    static constexpr int kBLoc = PAIR ? kMaxN / 2 : kMaxN;  // B' columns held per CTA
+    static constexpr int kBTile = kBLoc * kTnBK * 2;        // one (hi or lo) B' tile
+    static constexpr int kStage = 2 * kTnATile + 2 * kBTile;
+    static constexpr int kStgB = kTnBK * kBLoc * 4;
+    static constexpr int kStgSlot = kTnStgA + kStgB;
+    static constexpr int kStgOff = kStages * kStage;
+    static constexpr int kEpiOff = kStgOff + kStg * kStgSlot;
+    static constexpr int kBarOff = kEpiOff + 4 * 32 * 33 * 4;  // + drain transpose buffers
+    static constexpr int kSmem = kBarOff + 256 + 1024;
+    static constexpr int kACols = PAIR ? 2 * kBM : kBM;      // A' columns per tile
+};
+static_assert(TnCfg<true>::kSmem <= 232448 && TnCfg<false>::kSmem <= 232448, "TN shared memory");
+
+template <bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
+    using Cfg = TnCfg<PAIR>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* stg_base = smem + kTnStages * kTnStage;  // kTnStg x [A' rows | B' rows]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTnBarOff);
-    uint64_t* full = bars;
-    uint64_t* empty = full + kTnStages;
-    uint64_t* sfull = empty + kTnStages;
-    uint64_t* sempty = sfull + kTnStg;
-    uint64_t* tfull = sempty + kTnStg;
-    uint64_t* tempty = tfull + 2;
+    uint8_t* stg_base = smem + Cfg::kStgOff;  // kStg x [A' rows | B' rows]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
+    uint64_t* full = bars;                     // [kStages] converters -> MMA (leader's)
+    uint64_t* empty = full + Cfg::kStages;     // [kStages] MMA -> converters
+    uint64_t* sfull = empty + Cfg::kStages;    // [kStg] loader (tx) -> converters
+    uint64_t* sempty = sfull + Cfg::kStg;      // [kStg] converters -> loader
+    uint64_t* tfull = sempty + Cfg::kStg;      // [2] MMA -> epilogue
+    uint64_t* tempty = tfull + 2;              // [2] epilogue -> MMA (leader's)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int unit = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
     const int tiles = p.tiles1 * p.tiles2;
-    const int split = blockIdx.x / tiles, tile = blockIdx.x % tiles;
-    const int32_t n10 = (tile / p.tiles2) * kBM, n20 = (tile % p.tiles2) * kMaxN;
-    const int32_t na = min(kBM, p.N1 - n10);    // valid A' columns
-    const int32_t nb = min(kMaxN, p.N2 - n20);  // valid B' columns
-    const int32_t nb_pad = (nb + 15) / 16 * 16;
+    const int split = unit / tiles, tile = unit % tiles;
+    const int32_t n10 = (tile / p.tiles2) * Cfg::kACols + static_cast<int32_t>(rank) * kBM;  // this CTA's A' cols
+    const int32_t n20 = (tile % p.tiles2) * kMaxN;                                           // tile's B' cols
+    const int32_t na = max(0, min(kBM, p.N1 - n10));  // valid A' columns of this CTA
+    const int32_t nb = min(kMaxN, p.N2 - n20);        // valid B' columns of the tile
+    // MMA N; a pair splits it into two 32-column-aligned halves (TMA boxes never straddle B1 | B2)
+    const int32_t nb_pad = PAIR ? (nb + 63) / 64 * 64 : (nb + 15) / 16 * 16;
+    const int32_t nloc = PAIR ? nb_pad / 2 : nb_pad;                  // B' columns held by this CTA
+    const int32_t nb0 = n20 + static_cast<int32_t>(rank) * nloc;      // first of them
+    const int32_t nbl = max(0, min(nloc, nb - static_cast<int32_t>(rank) * nloc));  // valid ones
     const int64_t r0 = int64_t(split) * p.rows_per_split;
     const int64_t r1 = min(p.M, r0 + p.rows_per_split);
     const int kblocks = r1 > r0 ? static_cast<int>((r1 - r0 + kTnBK - 1) / kTnBK) : 0;
@@ -717,48 +738,49 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
 
     if (warp == kMmaWarp) {
         if (lane == 0) {
-            for (int s = 0; s < kTnStages; ++s) {
-                mbar_init(&full[s], kConv);
+            for (int s = 0; s < Cfg::kStages; ++s) {
+                mbar_init(&full[s], kConvWarps * (PAIR ? 2 : 1));
                 mbar_init(&empty[s], 1);
             }
-            for (int s = 0; s < kTnStg; ++s) {
+            for (int s = 0; s < Cfg::kStg; ++s) {
                 mbar_init(&sfull[s], 1);
-                mbar_init(&sempty[s], kConv);
+                mbar_init(&sempty[s], kConvWarps);
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
-                mbar_init(&tempty[s], kEpilogue);
+                mbar_init(&tempty[s], 4 * (PAIR ? 2 : 1));
             }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncwarp();
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        tmem_alloc_g<PAIR>(tmem_slot);
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t full_l = PAIR ? mapa(smem_u32(full), 0) : smem_u32(full);
+    const uint32_t tempty_l = PAIR ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
 
     if (warp == kLoadWarp) {
         // ================= loader: 2D TMA boxes (32 columns x 32 rows, SWIZZLE_128B) -> staging =================
-        // A' needs ceil(na/32) boxes, B' ceil(nb/32) (from B1 or B2; n2a is a multiple of 32).
-        const int a_boxes = (na + 31) >> 5, b_boxes = (nb + 31) >> 5;
+        // A' needs ceil(na/32) boxes, B' ceil(nbl/32) (each from B1 or B2; n2a is a multiple of 32).
+        const int a_boxes = (na + 31) >> 5, b_boxes = (nbl + 31) >> 5;
         const uint32_t bytes = static_cast<uint32_t>(a_boxes + b_boxes) * kTnBox;
-        for (int kb = 0; kb < kblocks; ++kb) {
-            const int slot = kb % kTnStg;
+        Ring ring;
+        for (int kb = 0; kb < kblocks; ++kb, ring.next(Cfg::kStg)) {
             const int32_t k0 = static_cast<int32_t>(r0 + int64_t(kb) * kTnBK);
-            mbar_wait(&sempty[slot], ((kb / kTnStg) & 1) ^ 1);
-            uint8_t* sa = stg_base + slot * (kTnStgA + kTnStgB);
+            mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
+            uint8_t* sa = stg_base + ring.idx * Cfg::kStgSlot;
             uint8_t* sb = sa + kTnStgA;
-            if (lane == 0) mbar_arrive_expect_tx(&sfull[slot], bytes);
+            if (lane == 0) mbar_arrive_expect_tx(&sfull[ring.idx], bytes);
             __syncwarp();
-            if (lane < a_boxes) tma_load_2d(sa + lane * kTnBox, &p.tm_a, n10 + 32 * lane, k0, &sfull[slot]);
+            if (lane < a_boxes) tma_load_2d(sa + lane * kTnBox, &p.tm_a, n10 + 32 * lane, k0, &sfull[ring.idx]);
             if (lane < b_boxes) {
-                const int32_t c = n20 + 32 * lane;
-                if (c < p.n2a) tma_load_2d(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[slot]);
-                else tma_load_2d(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[slot]);
+                const int32_t c = nb0 + 32 * lane;
+                if (c < p.n2a) tma_load_2d(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[ring.idx]);
+                else tma_load_2d(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[ring.idx]);
             }
         }
     } else if (warp < kConvWarps) {
@@ -767,16 +789,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         // of 8 rows, which the 128 B swizzle spreads over distinct banks.
         const int tid = threadIdx.x;
         const float sa_ = ldexpf(1.f, ka), sb_ = ldexpf(1.f, kbx);
-        const int bch = nb_pad >> 3;
-        for (int kb = 0; kb < kblocks; ++kb) {
-            const int stage = kb % kTnStages, slot = kb % kTnStg;
+        const int bch = nloc >> 3;
+        Ring mr, sr;
+        for (int kb = 0; kb < kblocks; ++kb, mr.next(Cfg::kStages), sr.next(Cfg::kStg)) {
             const int64_t k0 = r0 + int64_t(kb) * kTnBK;
             const int rows_ok = r1 - k0 < kTnBK ? static_cast<int>(r1 - k0) : kTnBK;
-            uint8_t* st = smem + stage * kTnStage;
-            const uint8_t* sga = stg_base + slot * (kTnStgA + kTnStgB);
+            uint8_t* st = smem + mr.idx * Cfg::kStage;
+            const uint8_t* sga = stg_base + sr.idx * Cfg::kStgSlot;
             const uint8_t* sgb = sga + kTnStgA;
-            mbar_wait(&empty[stage], ((kb / kTnStages) & 1) ^ 1);
-            mbar_wait(&sfull[slot], (kb / kTnStg) & 1);
+            mbar_wait(&empty[mr.idx], mr.phase ^ 1);
+            mbar_wait(&sfull[sr.idx], sr.phase);
             // A': 32 rows x 16 chunks of 8 columns
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
@@ -792,59 +814,65 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 }
                 split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
             }
-            // B': 32 rows x bch (<= 32) chunks
+            // B': 32 rows x bch chunks (this CTA's columns)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < Cfg::kBLoc / 64; ++j) {
                 const int idx = tid + j * kConv;
                 const int kr = idx & 31, ch = idx >> 5;
                 if (ch >= bch) continue;
                 float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
-                const int valid = kr < rows_ok ? min(8, nb - ch * 8) : 0;
+                const int valid = kr < rows_ok ? min(8, nbl - ch * 8) : 0;
                 if (valid > 0) {
                     const uint8_t* rowp = sgb + (ch >> 2) * kTnBox + kr * 128;
                     x0 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3)) ^ (kr & 7)) << 4));
                     x1 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3) + 1) ^ (kr & 7)) << 4));
                     mask8(x0, x1, valid);
                 }
-                split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + kTnBTile, mn_off(ch * 8, kr));
+                split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile, mn_off(ch * 8, kr));
             }
             fence_proxy_async();
-            mbar_arrive(&full[stage]);
-            mbar_arrive(&sempty[slot]);
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (PAIR) mbar_arrive_cluster(full_l + mr.idx * 8);
+                else mbar_arrive(&full[mr.idx]);
+                mbar_arrive(&sempty[sr.idx]);
+            }
         }
     } else if (warp == kMmaWarp) {
-        // ================= MMA issuer =================
-        const uint32_t idesc = idesc_f16_mn(kBM, nb_pad);
-        for (int chunk = 0; chunk < nchunks; ++chunk) {
-            const uint32_t acc = chunk & 1;
-            const uint32_t d_tmem = tmem_base + acc * 256;
-            mbar_wait(&tempty[acc], ((chunk >> 1) & 1) ^ 1);
-            tc_fence_after();
-            const int kb_end = min(kblocks, (chunk + 1) * kChunkKb);
-            for (int kb = chunk * kChunkKb; kb < kb_end; ++kb) {
-                const int stage = kb % kTnStages;
-                mbar_wait(&full[stage], (kb / kTnStages) & 1);
+        // ================= MMA issuer (the pair's leader only) =================
+        if (!PAIR || rank == 0) {
+            const uint32_t idesc = idesc_f16_mn(Cfg::kACols, nb_pad);
+            Ring mr;
+            for (int chunk = 0; chunk < nchunks; ++chunk) {
+                const uint32_t acc = chunk & 1;
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                mbar_wait(&tempty[acc], ((chunk >> 1) & 1) ^ 1);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint8_t* st = smem + stage * kTnStage;
-                    const uint32_t ahi = smem_u32(st), alo = smem_u32(st + kTnATile);
-                    const uint32_t bhi = smem_u32(st + 2 * kTnATile), blo = smem_u32(st + 2 * kTnATile + kTnBTile);
+                const int kb_end = min(kblocks, (chunk + 1) * kChunkKb);
+                for (int kb = chunk * kChunkKb; kb < kb_end; ++kb, mr.next(Cfg::kStages)) {
+                    mbar_wait(&full[mr.idx], mr.phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint8_t* st = smem + mr.idx * Cfg::kStage;
+                        const uint32_t ahi = smem_u32(st), alo = smem_u32(st + kTnATile);
+                        const uint32_t bhi = smem_u32(st + 2 * kTnATile), blo = smem_u32(st + 2 * kTnATile + Cfg::kBTile);
 #pragma unroll
-                    for (int k = 0; k < kTnBK / 16; ++k) {
-                        const uint32_t adv = k * 2 * kTnSbo;  // 16 rows = 2 K groups
-                        const uint64_t dah = desc_mn_sw128(ahi + adv, kTnLbo, kTnSbo);
-                        const uint64_t dal = desc_mn_sw128(alo + adv, kTnLbo, kTnSbo);
-                        const uint64_t dbh = desc_mn_sw128(bhi + adv, kTnLbo, kTnSbo);
-                        const uint64_t dbl = desc_mn_sw128(blo + adv, kTnLbo, kTnSbo);
-                        const uint32_t first = (kb == chunk * kChunkKb && k == 0) ? 0u : 1u;
-                        mma_f16(d_tmem, dah, dbh, idesc, first);
-                        mma_f16(d_tmem, dah, dbl, idesc, 1u);
-                        mma_f16(d_tmem, dal, dbh, idesc, 1u);
+                        for (int k = 0; k < kTnBK / 16; ++k) {
+                            const uint32_t adv = k * 2 * kTnSbo;  // 16 rows = 2 K groups
+                            const uint64_t dah = desc_mn_sw128(ahi + adv, kTnLbo, kTnSbo);
+                            const uint64_t dal = desc_mn_sw128(alo + adv, kTnLbo, kTnSbo);
+                            const uint64_t dbh = desc_mn_sw128(bhi + adv, kTnLbo, kTnSbo);
+                            const uint64_t dbl = desc_mn_sw128(blo + adv, kTnLbo, kTnSbo);
+                            const uint32_t first = (kb == chunk * kChunkKb && k == 0) ? 0u : 1u;
+                            mma_f16_g<PAIR>(d_tmem, dah, dbh, idesc, first);
+                            mma_f16_g<PAIR>(d_tmem, dah, dbl, idesc, 1u);
+                            mma_f16_g<PAIR>(d_tmem, dal, dbh, idesc, 1u);
+                        }
+                        mma_commit_g<PAIR>(&empty[mr.idx]);
+                        if (kb == kb_end - 1) mma_commit_g<PAIR>(&tfull[acc]);
                     }
-                    mma_commit(&empty[stage]);
-                    if (kb == kb_end - 1) mma_commit(&tfull[acc]);
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
     } else {
@@ -853,9 +881,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         // every read-modify-write of the partial touches one contiguous 128 B row segment.
         const int ew = warp & 3;
         const int32_t m0w = n10 + ew * 32;  // first output row (N1 index) of this warp
-        const int rows_here = p.N1 - m0w < 32 ? max(0, p.N1 - m0w) : 32;
+        const int rows_here = max(0, min(32, p.N1 - m0w));
         const float unscale = ldexpf(1.f, -(ka + kbx));
-        float* stg = reinterpret_cast<float*>(smem + kTnEpiOff) + ew * (32 * 33);
+        float* stg = reinterpret_cast<float*>(smem + Cfg::kEpiOff) + ew * (32 * 33);
         float* outw = p.ws + (int64_t(split) * p.N1 + m0w) * p.N2 + n20;
         for (int chunk = 0; chunk < nchunks; ++chunk) {
             const uint32_t acc = chunk & 1;
@@ -882,16 +910,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 __syncwarp();
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (PAIR) mbar_arrive_cluster(tempty_l + acc * 8);
+                else mbar_arrive(&tempty[acc]);
+            }
         }
         if (nchunks == 0)
             for (int rr = 0; rr < rows_here; ++rr)
                 for (int c = lane; c < nb; c += 32) outw[int64_t(rr) * p.N2 + c] = 0.f;
     }
-    __syncthreads();
+    tc_fence_before();
+    if constexpr (PAIR) cluster_sync();
+    else __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+        tmem_dealloc_g<PAIR>(tmem_base);
     }
 }
 
@@ -953,10 +987,24 @@ bool nt_pair_enabled() {
 }
 }  // namespace
 
+namespace {
+// Weight-gradient GEMMs with more than 128 A' columns run on CTA pairs unless SC_TN_PAIR=0.
+bool tn_use_pair(int32_t N1) {
+    static const bool on = [] {
+        const char* e = std::getenv("SC_TN_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on && N1 > tc::kBM;
+}
+}  // namespace
+
 int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M) {
-    const int32_t tiles = ((N1 + tc::kBM - 1) / tc::kBM) * ((N2 + tc::kMaxN - 1) / tc::kMaxN);
-    int64_t s = std::max<int64_t>(1, num_sms() / tiles);  // one wave of persistent-sized CTAs
-    s = std::min<int64_t>(s, (M + 4095) / 4096);  // >= 4096 rows per split
+    const bool pair = tn_use_pair(N1);
+    const int32_t acols = pair ? 2 * tc::kBM : tc::kBM;
+    const int32_t units = ((N1 + acols - 1) / acols) * ((N2 + tc::kMaxN - 1) / tc::kMaxN);
+    const int32_t slots = pair ? std::max(1, num_sms() / 2) : num_sms();  // CTAs (pairs) resident at once
+    int64_t s = std::max<int64_t>(1, slots / units);  // one wave of persistent-sized CTAs
+    s = std::min<int64_t>(s, (M + 4095) / 4096);       // >= 4096 rows per split
     return static_cast<int32_t>(std::max<int64_t>(s, 1));
 }
 
@@ -969,12 +1017,7 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
         for (int32_t r = 0; r < N1; ++r) SC_CUDA(cudaMemsetAsync(C + int64_t(r) * ldc, 0, sizeof(float) * N2, s));
         return;
     }
-    static bool attr_set = false;
-    if (!attr_set) {
-        SC_CUDA(cudaFuncSetAttribute(tc::gemm_tn_f16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::kTnSmemBytes));
-        attr_set = true;
-    }
+    const bool pair = tn_use_pair(N1);
     tc::TnParams p{};
     p.a = a.ptr;
     p.lda = a.ld;
@@ -992,11 +1035,31 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     const int32_t S = tn_f16x3_splits(N1, N2, M);
     if (int64_t(S) * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn_f16x3: workspace too small");
     p.rows_per_split = ((M + S - 1) / S + tc::kTnBK - 1) / tc::kTnBK * tc::kTnBK;
-    p.tiles1 = (N1 + tc::kBM - 1) / tc::kBM;
+    const int32_t acols = pair ? 2 * tc::kBM : tc::kBM;
+    p.tiles1 = (N1 + acols - 1) / acols;
     p.tiles2 = (N2 + tc::kMaxN - 1) / tc::kMaxN;
     p.ws = ws;
-    const unsigned grid = static_cast<unsigned>(S * p.tiles1 * p.tiles2);
-    tc::gemm_tn_f16x3_kernel<<<grid, tc::kThreads, tc::kTnSmemBytes, s>>>(p);
+    const int64_t units = int64_t(S) * p.tiles1 * p.tiles2;
+    auto launch = [&](auto kernel, int smem_bytes) {
+        SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3(static_cast<unsigned>(pair ? 2 * units : units));
+        cfg.blockDim = dim3(tc::kThreads);
+        cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes);
+        cfg.stream = s;
+        if (pair) {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        }
+        SC_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
+    };
+    if (pair) launch(tc::gemm_tn_f16x3_kernel<true>, tc::TnCfg<true>::kSmem);
+    else launch(tc::gemm_tn_f16x3_kernel<false>, tc::TnCfg<false>::kSmem);
     SC_LAUNCH_CHECK();
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();

@@ -86,6 +86,11 @@ TN_CASES = [  # M, N1, N2a, N2b, gather
     (1234, 16, 16, 8, True),
     (9999, 32, 32, 64, False),
     (300_000, 256, 256, 0, False),
+    # CTA-pair shapes (N1 > 128): partial second CTA, two A' tiles, B1 | B2 seams inside a half
+    (4100, 200, 256, 100, False),
+    (6000, 384, 256, 0, False),
+    (2048, 129, 32, 48, False),
+    (40_000, 256, 256, 256, False),
 ]
 
 
