@@ -178,13 +178,13 @@ __host__ __device__ __forceinline__ int scale_exp(float amax) {
     return 15 - e;
 }
 
-// x * 2^k split into fp16 (hi, lo); two elements per 32-bit word.
+// x * 2^k split into fp16 (hi, lo); two elements per 32-bit word. Packed fp32x2 arithmetic
+// (FMUL2 / FFMA2) and packed conversions (F2FP); x s - hi is exact in fp32.
 __device__ __forceinline__ void split2(float x0, float x1, float s, uint32_t& hi, uint32_t& lo) {
-    // packed conversions (F2FP / HADD2.F32): 2 elements per instruction
-    const float2 xs = make_float2(x0 * s, x1 * s);
+    const float2 xs = __fmul2_rn(make_float2(x0, x1), make_float2(s, s));
     const __half2 h = __float22half2_rn(xs);
-    const float2 hf = __half22float2(h);
-    const __half2 l = __float22half2_rn(make_float2(xs.x - hf.x, xs.y - hf.y));
+    const float2 d = __ffma2_rn(__half22float2(h), make_float2(-1.f, -1.f), xs);
+    const __half2 l = __float22half2_rn(d);
     hi = *reinterpret_cast<const uint32_t*>(&h);
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
@@ -217,6 +217,42 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// L2 eviction-priority policies (createpolicy) for streamed operands and L2-resident partials.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_l2hint(float* ptr, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_v4_l2hint(float* ptr, float a, float b, float c, float d, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(a), "f"(b), "f"(c),
+                 "f"(d), "l"(pol)
+                 : "memory");
+}
+// fire-and-forget fp32 adds performed at L2 (round-to-nearest)
+__device__ __forceinline__ void red_add_v4_l2hint(float* ptr, float a, float b, float c, float d, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(a), "f"(b),
+                 "f"(c), "f"(d), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_l2hint(float* ptr, float a, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(a), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                                 uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -692,7 +728,7 @@ struct TnCfg {
     static constexpr int kStgSlot = kTnStgA + kStgB;
     static constexpr int kStgOff = kStages * kStage;
     static constexpr int kEpiOff = kStgOff + kStg * kStgSlot;
-    static constexpr int kBarOff = kEpiOff + 4 * 32 * 33 * 4;  // + drain transpose buffers
+    static constexpr int kBarOff = kEpiOff;
     static constexpr int kSmem = kBarOff + 256 + 1024;
     static constexpr int kACols = PAIR ? 2 * kBM : kBM;      // A' columns per tile
 };
@@ -768,6 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         // A' needs ceil(na/32) boxes, B' ceil(nbl/32) (each from B1 or B2; n2a is a multiple of 32).
         const int a_boxes = (na + 31) >> 5, b_boxes = (nbl + 31) >> 5;
         const uint32_t bytes = static_cast<uint32_t>(a_boxes + b_boxes) * kTnBox;
+        const uint64_t pol_b = l2_evict_first();
         Ring ring;
         for (int kb = 0; kb < kblocks; ++kb, ring.next(Cfg::kStg)) {
             const int32_t k0 = static_cast<int32_t>(r0 + int64_t(kb) * kTnBK);
@@ -777,10 +814,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             if (lane == 0) mbar_arrive_expect_tx(&sfull[ring.idx], bytes);
             __syncwarp();
             if (lane < a_boxes) tma_load_2d(sa + lane * kTnBox, &p.tm_a, n10 + 32 * lane, k0, &sfull[ring.idx]);
-            if (lane < b_boxes) {
+            if (lane < b_boxes) {  // B' columns are read by this CTA only: stream them through L2
                 const int32_t c = nb0 + 32 * lane;
-                if (c < p.n2a) tma_load_2d(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[ring.idx]);
-                else tma_load_2d(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[ring.idx]);
+                if (c < p.n2a) tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[ring.idx], pol_b);
+                else tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[ring.idx], pol_b);
             }
         }
     } else if (warp < kConvWarps) {
@@ -799,36 +836,53 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             const uint8_t* sgb = sga + kTnStgA;
             mbar_wait(&empty[mr.idx], mr.phase ^ 1);
             mbar_wait(&sfull[sr.idx], sr.phase);
-            // A': 32 rows x 16 chunks of 8 columns
+            // A': 32 rows x 16 chunks of 8 columns; B': 32 rows x bch chunks (this CTA's columns).
+            // Interior stages (all rows and columns valid) skip the masking.
+            const bool whole = rows_ok == kTnBK && na == kBM && nbl == nloc;  // block-uniform
+            auto load8 = [&](const uint8_t* sg, int kr, int ch, int valid, float4& x0, float4& x1) {
+                const uint8_t* rowp = sg + (ch >> 2) * kTnBox + kr * 128;
+                x0 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3)) ^ (kr & 7)) << 4));
+                x1 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3) + 1) ^ (kr & 7)) << 4));
+                if (valid < 8) mask8(x0, x1, valid);
+            };
+            if (whole) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int idx = tid + j * kConv;
-                const int kr = idx & 31, ch = idx >> 5;
-                float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
-                const int valid = kr < rows_ok ? min(8, na - ch * 8) : 0;
-                if (valid > 0) {
-                    const uint8_t* rowp = sga + (ch >> 2) * kTnBox + kr * 128;
-                    x0 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3)) ^ (kr & 7)) << 4));
-                    x1 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3) + 1) ^ (kr & 7)) << 4));
-                    mask8(x0, x1, valid);
+                for (int j = 0; j < 2; ++j) {
+                    const int idx = tid + j * kConv;
+                    const int kr = idx & 31, ch = idx >> 5;
+                    float4 x0, x1;
+                    load8(sga, kr, ch, 8, x0, x1);
+                    split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
                 }
-                split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
-            }
-            // B': 32 rows x bch chunks (this CTA's columns)
 #pragma unroll
-            for (int j = 0; j < Cfg::kBLoc / 64; ++j) {
-                const int idx = tid + j * kConv;
-                const int kr = idx & 31, ch = idx >> 5;
-                if (ch >= bch) continue;
-                float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
-                const int valid = kr < rows_ok ? min(8, nbl - ch * 8) : 0;
-                if (valid > 0) {
-                    const uint8_t* rowp = sgb + (ch >> 2) * kTnBox + kr * 128;
-                    x0 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3)) ^ (kr & 7)) << 4));
-                    x1 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3) + 1) ^ (kr & 7)) << 4));
-                    mask8(x0, x1, valid);
+                for (int j = 0; j < Cfg::kBLoc / 64; ++j) {
+                    const int idx = tid + j * kConv;
+                    const int kr = idx & 31, ch = idx >> 5;
+                    if (ch >= bch) continue;
+                    float4 x0, x1;
+                    load8(sgb, kr, ch, 8, x0, x1);
+                    split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile, mn_off(ch * 8, kr));
                 }
-                split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile, mn_off(ch * 8, kr));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int idx = tid + j * kConv;
+                    const int kr = idx & 31, ch = idx >> 5;
+                    float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+                    const int valid = kr < rows_ok ? min(8, na - ch * 8) : 0;
+                    if (valid > 0) load8(sga, kr, ch, valid, x0, x1);
+                    split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
+                }
+#pragma unroll
+                for (int j = 0; j < Cfg::kBLoc / 64; ++j) {
+                    const int idx = tid + j * kConv;
+                    const int kr = idx & 31, ch = idx >> 5;
+                    if (ch >= bch) continue;
+                    float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+                    const int valid = kr < rows_ok ? min(8, nbl - ch * 8) : 0;
+                    if (valid > 0) load8(sgb, kr, ch, valid, x0, x1);
+                    split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile, mn_off(ch * 8, kr));
+                }
             }
             fence_proxy_async();
             __syncwarp();
@@ -877,14 +931,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         }
     } else {
         // ================= epilogue: drain each chunk into the fp32 partial ws[split] =================
-        // Each warp owns 32 output rows (TMEM lanes); a 32 x 32 block is transposed through smem so
-        // every read-modify-write of the partial touches one contiguous 128 B row segment.
+        // Lane = output row (TMEM lane). The first chunk stores, later chunks add with fire-and-forget
+        // vector reductions performed in L2 (red.global.add.v4.f32). Every partial element is owned
+        // by one thread, and same-address operations of a thread stay in program order, so the sum
+        // over chunks is evaluated in a fixed order (deterministic).
         const int ew = warp & 3;
         const int32_t m0w = n10 + ew * 32;  // first output row (N1 index) of this warp
         const int rows_here = max(0, min(32, p.N1 - m0w));
         const float unscale = ldexpf(1.f, -(ka + kbx));
-        float* stg = reinterpret_cast<float*>(smem + Cfg::kEpiOff) + ew * (32 * 33);
         float* outw = p.ws + (int64_t(split) * p.N1 + m0w) * p.N2 + n20;
+        float* orow = outw + int64_t(lane) * p.N2;
+        const bool vec = (p.N2 & 3) == 0;  // 16-byte aligned partial rows
+        const uint64_t pol_ws = l2_evict_last();  // the partials stay in L2 while operands stream past
         for (int chunk = 0; chunk < nchunks; ++chunk) {
             const uint32_t acc = chunk & 1;
             mbar_wait(&tfull[acc], (chunk >> 1) & 1);
@@ -892,22 +950,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             for (int c0 = 0; c0 < nb_pad; c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
+                if (lane >= rows_here || c0 >= nb) continue;
+                float* o = orow + c0;
+                if (vec && c0 + 32 <= nb) {
 #pragma unroll
-                for (int q = 0; q < 32; ++q) stg[lane * 33 + q] = __uint_as_float(r[q]) * unscale;
-                __syncwarp();
-                const int col = c0 + lane;
-                if (col < nb) {
-                    float* o = outw + col;
-                    float prev[32];
-                    // all 32 loads in flight before any store (the stores could alias them otherwise)
+                    for (int j = 0; j < 8; ++j) {
+                        const float x0 = __uint_as_float(r[4 * j]) * unscale, x1 = __uint_as_float(r[4 * j + 1]) * unscale;
+                        const float x2 = __uint_as_float(r[4 * j + 2]) * unscale, x3 = __uint_as_float(r[4 * j + 3]) * unscale;
+                        if (chunk == 0) st_v4_l2hint(o + 4 * j, x0, x1, x2, x3, pol_ws);
+                        else red_add_v4_l2hint(o + 4 * j, x0, x1, x2, x3, pol_ws);
+                    }
+                } else {
+                    const int nv = min(32, nb - c0);
 #pragma unroll
-                    for (int rr = 0; rr < 32; ++rr)
-                        prev[rr] = (chunk > 0 && rr < rows_here) ? o[int64_t(rr) * p.N2] : 0.f;
-#pragma unroll
-                    for (int rr = 0; rr < 32; ++rr)
-                        if (rr < rows_here) o[int64_t(rr) * p.N2] = prev[rr] + stg[rr * 33 + lane];
+                    for (int q = 0; q < 32; ++q) {
+                        if (q >= nv) break;
+                        const float x = __uint_as_float(r[q]) * unscale;
+                        if (chunk == 0) st_l2hint(o + q, x, pol_ws);
+                        else red_add_l2hint(o + q, x, pol_ws);
+                    }
                 }
-                __syncwarp();
             }
             tc_fence_before();
             __syncwarp();

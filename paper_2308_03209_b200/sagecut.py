@@ -18,7 +18,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsagecut_cuda.so")
+# SC_LIB: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("SC_LIB") or os.path.join(_HERE, "libsagecut_cuda.so")
 
 SC_OK, SC_EINVAL, SC_ERUNTIME, SC_EINTERNAL, SC_ECUDA, SC_ENCCL = range(6)
 

@@ -22,6 +22,14 @@ if which == "nt":
         t0 = time.perf_counter()
         sc.debug_gemm(A, B, epi=1)
         print("nt wall", time.perf_counter() - t0)
+elif which == "tn512":  # the update layer's dU = dh^T [mean | h] shape (N2 = 512)
+    A = rng.standard_normal((M, 256), dtype=np.float32)
+    B = rng.standard_normal((M, 256), dtype=np.float32)
+    B2 = rng.standard_normal((M, 256), dtype=np.float32)
+    for _ in range(2):
+        t0 = time.perf_counter()
+        sc.debug_gemm_tn(A, B, B2)
+        print("tn512 wall", time.perf_counter() - t0)
 else:
     A = rng.standard_normal((M, 256), dtype=np.float32)
     B = rng.standard_normal((M, 256), dtype=np.float32)
