@@ -475,7 +475,8 @@ sc_status sc_trainer_get_part_grads(sc_trainer* t, int32_t part, float* out) {
     return guard([&] {
         REQUIRE_ARG(part >= 0 && part < t->p, "bad part index");
         set_device(t->ctx);
-        d2h(out, t->slots.get() + int64_t(part) * t->P, t->P, t->ctx->stream);
+        for (int b = 0; b < t->nb(); ++b)  // bucket-major slots -> one flat parameter-ordered vector
+            d2h(out + t->b_off[b], t->slot_ptr(b, part), t->b_len(b), t->ctx->stream);
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
     });
 }

@@ -505,14 +505,27 @@ __global__ void sum_f64_final_kernel(const double* partial, int nb, double* out,
     }
 }
 
-__global__ void gather_kernel(int64_t P, int32_t p, const float* __restrict__ slots, float* gathered, double* partial,
-                              int* nonfinite) {
+// Gradient slots are bucket-major (one bucket per parameter matrix, in
+// for_each_matrix order): bucket b holds pp consecutive per-partition copies of
+// its len_b floats, so one all-gather per (round, bucket) exchanges a
+// contiguous range. Element k of bucket b for partition i lives at
+// b_off[b] * pp + i * len_b + (k - b_off[b]).
+__global__ void gather_kernel(int64_t P, int32_t p, int32_t pp, int32_t nb, const int64_t* __restrict__ b_off,
+                              const float* __restrict__ slots, float* gathered, double* partial, int* nonfinite) {
     __shared__ double sh[kRedThreads];
     double acc = 0.0;
     bool bad = false;
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < P; k += int64_t(gridDim.x) * blockDim.x) {
-        float g = slots[k];
-        for (int32_t i = 1; i < p; ++i) g += slots[int64_t(i) * P + k];
+        int32_t lo = 0, hi = nb - 1;  // last bucket with b_off <= k
+        while (lo < hi) {
+            const int32_t mid = (lo + hi + 1) >> 1;
+            if (b_off[mid] <= k) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t o = b_off[lo], len = b_off[lo + 1] - o;
+        const float* src = slots + o * pp + (k - o);
+        float g = src[0];
+        for (int32_t i = 1; i < p; ++i) g += src[int64_t(i) * len];  // ascending partition order (trainer.hpp:79-94)
         gathered[k] = g;
         bad |= !isfinite(g);
         acc += static_cast<double>(g) * static_cast<double>(g);
@@ -681,9 +694,9 @@ void sum_f64(int64_t n, const double* x, double* partial, double* out, double di
     SC_LAUNCH_CHECK();
     count_launch(2);
 }
-void gather_grads(int64_t P, int32_t p, const float* slots, float* gathered, double* partial, int* nonfinite,
-                  cudaStream_t s) {
-    gather_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(P, p, slots, gathered, partial, nonfinite);
+void gather_grads(int64_t P, int32_t p, int32_t pp, int32_t nb, const int64_t* b_off, const float* slots,
+                  float* gathered, double* partial, int* nonfinite, cudaStream_t s) {
+    gather_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(P, p, pp, nb, b_off, slots, gathered, partial, nonfinite);
     SC_LAUNCH_CHECK();
     count_launch();
 }

@@ -68,10 +68,12 @@ void bce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* l
 // Deterministic f64 sum of x[0..n), divided by `divisor`, into *out (fixed-shape two-pass reduction).
 void sum_f64(int64_t n, const double* x, double* partial, double* out, double divisor, cudaStream_t s);
 
-// gathered[k] = sum_{i < p} slots[i][k] in ascending i (trainer.hpp:79-94);
-// f64 sum of squares + non-finite flag for grad_norm / adam_step's check.
-void gather_grads(int64_t P, int32_t p, const float* slots, float* gathered, double* partial, int* nonfinite,
-                  cudaStream_t s);
+// gathered[k] = sum_{i < p} slot_i[k] in ascending i (trainer.hpp:79-94) over
+// bucket-major slots (bucket b = parameter matrix b holds pp >= p per-partition
+// copies; b_off: nb + 1 device offsets, the last = P); f64 sum of squares +
+// non-finite flag for grad_norm / adam_step's check.
+void gather_grads(int64_t P, int32_t p, int32_t pp, int32_t nb, const int64_t* b_off, const float* slots,
+                  float* gathered, double* partial, int* nonfinite, cudaStream_t s);
 // out[0] = sqrt(sum partial) (grad_norm), out[1] = sum part_loss[0..p) in order.
 void finalize_step(const double* partial, const double* part_loss, int32_t p, double* out, cudaStream_t s);
 // Adam (nn.hpp:400-432); skipped entirely when *nonfinite is set.

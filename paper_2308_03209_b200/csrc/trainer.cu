@@ -1,8 +1,9 @@
 // trainer.cu — train_cofree_impl (proj/include/sagecut/trainer.hpp:202-313) on
 // the device: one rank per GPU owns partitions i with i % world == rank, runs
-// their forward / loss / backward back to back on one stream, exchanges the
-// per-partition gradient slots with one NCCL all-reduce, then every rank sums
-// the slots in ascending partition order (the reference's gather_gradients,
+// their forward / loss / backward back to back on one stream, all-gathers each
+// per-partition gradient bucket (one parameter matrix) over NCCL on a comm
+// stream as soon as backward produces it, then every rank sums the slots in
+// ascending partition order (the reference's gather_gradients,
 // trainer.hpp:79-94) and applies the same Adam step.
 #include <nccl.h>
 
@@ -73,6 +74,9 @@ using namespace sc;
 
 sc_trainer::~sc_trainer() {
     if (comm) ncclCommDestroy(comm);
+    for (cudaEvent_t e : xfer_events) cudaEventDestroy(e);
+    if (comm_done) cudaEventDestroy(comm_done);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
 }
 
 namespace sc {
@@ -121,7 +125,19 @@ void trainer_init(sc_trainer* t) {
     t->m1.alloc(t->P);
     t->m2.alloc(t->P);
     t->gathered.alloc(t->P);
-    t->slots.alloc(int64_t(t->p) * t->P);
+    // gradient buckets: one per matrix, for_each_matrix order (W_l, U_l, ..., head)
+    t->b_off.clear();
+    for (const LayerOff& lo : t->lay) {
+        t->b_off.push_back(lo.W);
+        t->b_off.push_back(lo.U);
+    }
+    t->b_off.push_back(t->head_off);
+    t->b_off.push_back(t->P);
+    t->b_off_dev.alloc(t->b_off.size());
+    SC_CUDA(cudaMemcpyAsync(t->b_off_dev.get(), t->b_off.data(), t->b_off.size() * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, s));
+    t->pp = (t->p + t->world - 1) / t->world * t->world;
+    t->slots.alloc(int64_t(t->pp) * t->P);
     SC_CUDA(cudaMemsetAsync(t->m1.get(), 0, t->m1.bytes(), s));
     SC_CUDA(cudaMemsetAsync(t->m2.get(), 0, t->m2.bytes(), s));
     SC_CUDA(cudaMemsetAsync(t->slots.get(), 0, t->slots.bytes(), s));
@@ -165,7 +181,8 @@ void trainer_init(sc_trainer* t) {
             SC_CUDA(cudaStreamSynchronize(s));
         }
     }
-    t->part_loss.alloc(t->p);
+    t->part_loss.alloc(t->pp);
+    SC_CUDA(cudaMemsetAsync(t->part_loss.get(), 0, t->part_loss.bytes(), s));
     t->out2.alloc(2);
     t->nonfinite.alloc(1);
     t->red_partial.alloc(1024);
@@ -293,8 +310,10 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
     P.end(s);
 }
 
-// sage_backward (nn.hpp:246-293) into one gradient slot.
-void backward(sc_trainer* t, const Rows& R, float* slot) {
+// sage_backward (nn.hpp:246-293) into partition i's gradient slot; each
+// finished bucket is handed to the comm stream (exchange round i / world).
+void backward(sc_trainer* t, const Rows& R, int i) {
+    const int round = i / t->world;
     cudaStream_t s = t->ctx->stream;
     Profiler& P = t->prof;
     const int64_t n = R.n;
@@ -305,8 +324,9 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
     const float* x0_amax = t->g->feat_amax.get();
     const float* emb_amax = t->L == 0 ? x0_amax : t->amax_x(t->L);
     t->tc.tn(t, MatT{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
-             slot + t->head_off, t->E);
+             t->slot_ptr(2 * t->L, i), t->E);
     P.end(s);
+    exchange_bucket(t, 2 * t->L, round);
     float* dh = t->dh.get();
     float* dh2 = t->dh2.get();
     float* dh_amax = t->amax_slot(sc_trainer::kSlotDh0);
@@ -324,8 +344,9 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
         const MatT meant{t->MEAN[l].get(), lo.H, nullptr, lo.H};
         P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), s);
         const float* xin_amax = l == 0 ? x0_amax : t->amax_x(l);
-        t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, slot + lo.U, lo.H + lo.in);
+        t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, t->slot_ptr(2 * l + 1, i), lo.H + lo.in);
         P.end(s);
+        exchange_bucket(t, 2 * l + 1, round);
         // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
         P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s);
         t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr,
@@ -339,9 +360,10 @@ void backward(sc_trainer* t, const Rows& R, float* slot) {
         P.end(s);
         // dW = dz^T h_in   (:289)
         P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s);
-        t->tc.tn(t, MatT{t->dz.get(), lo.H, nullptr, lo.H}, dz_amax, xint, xin_amax, nullptr, nullptr, n, slot + lo.W,
-                 lo.in);
+        t->tc.tn(t, MatT{t->dz.get(), lo.H, nullptr, lo.H}, dz_amax, xint, xin_amax, nullptr, nullptr, n,
+                 t->slot_ptr(2 * l, i), lo.in);
         P.end(s);
+        exchange_bucket(t, 2 * l, round);
         if (l > 0) {  // dh = dh U_R + dz W   (:275, :290); layer 0's is unused
             const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz.get(), lo.H, nullptr, lo.H};
             P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s);
@@ -390,31 +412,42 @@ void run_partition(sc_trainer* t, int i, int epoch) {
             t->row_loss.get(), s);
     sum_f64(st.n, t->row_loss.get(), t->red_partial.get(), t->part_loss.get() + i, t->normalizer, s);
     t->prof.end(s);
-    backward(t, R, t->slots.get() + int64_t(i) * t->P);
+    exchange_bucket(t, -1, i / t->world);
+    backward(t, R, i);
 }
 
 void trainer_step_async(sc_trainer* t, int epoch) {
     cudaStream_t s = t->ctx->stream;
     t->prof.records.clear();
     t->prof.used = 0;
-    // Slots and losses of partitions owned by other ranks arrive via the all-reduce.
-    if (t->world > 1) {
-        SC_CUDA(cudaMemsetAsync(t->slots.get(), 0, t->slots.bytes(), s));
-        SC_CUDA(cudaMemsetAsync(t->part_loss.get(), 0, t->part_loss.bytes(), s));
+    if (t->world > 1 && !t->comm)
+        throw std::invalid_argument("sc_trainer_init_comm must be called before stepping with world > 1");
+    // Exchange round j trains partition j*world + rank on every rank; each
+    // finished gradient bucket (and the partition loss) is all-gathered on the
+    // comm stream while the rest of backward runs. Every slot has exactly one
+    // writer, so the exchange moves bits and the ordered sum below is bitwise
+    // the reference's single-process gather for any GPU count.
+    t->xfer_used = 0;
+    const int rounds = t->pp / t->world;
+    for (int j = 0; j < rounds; ++j) {
+        const int i = j * t->world + t->rank;
+        if (i < t->p) {
+            run_partition(t, i, epoch);
+        } else {  // no partition this round (p % world != 0): same collective sequence, padding slots
+            exchange_bucket(t, -1, j);
+            for (int b = t->nb() - 1; b >= 0; --b) exchange_bucket(t, b, j);
+        }
     }
-    for (int i : t->local) run_partition(t, i, epoch);
-    if (t->world > 1) {
-        if (!t->comm) throw std::invalid_argument("sc_trainer_init_comm must be called before stepping with world > 1");
-        t->prof.begin("allreduce", 4.0 * t->p * t->P, s);
-        SC_NCCL(ncclGroupStart());
-        SC_NCCL(ncclAllReduce(t->slots.get(), t->slots.get(), size_t(t->p) * t->P, ncclFloat32, ncclSum, t->comm, s));
-        SC_NCCL(ncclAllReduce(t->part_loss.get(), t->part_loss.get(), size_t(t->p), ncclFloat64, ncclSum, t->comm, s));
-        SC_NCCL(ncclGroupEnd());
+    if (t->world > 1) {  // exposed tail of the exchange: the last buckets' all-gathers
+        t->prof.begin("exchange_tail", 4.0 * t->p * t->P, s);
+        SC_CUDA(cudaEventRecord(t->comm_done, t->comm_stream));
+        SC_CUDA(cudaStreamWaitEvent(s, t->comm_done, 0));
         t->prof.end(s);
     }
     SC_CUDA(cudaMemsetAsync(t->nonfinite.get(), 0, 4, s));
     t->prof.begin("gather_adam", 4.0 * t->P * (t->p + 6), s);
-    gather_grads(t->P, t->p, t->slots.get(), t->gathered.get(), t->red_partial.get(), t->nonfinite.get(), s);
+    gather_grads(t->P, t->p, t->pp, t->nb(), t->b_off_dev.get(), t->slots.get(), t->gathered.get(),
+                 t->red_partial.get(), t->nonfinite.get(), s);
     finalize_step(t->red_partial.get(), t->part_loss.get(), t->p, t->out2.get(), s);
     // adam_step (nn.hpp:400-432): corrections in f64, cast to float
     const int64_t step = t->adam_step + 1;
@@ -474,6 +507,31 @@ void trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
     std::memcpy(uid.internal, id, 128);
     SC_CUDA(cudaSetDevice(t->ctx->device));
     SC_NCCL(ncclCommInitRank(&t->comm, t->world, uid, t->rank));
+    if (!t->comm_stream) SC_CUDA(cudaStreamCreateWithFlags(&t->comm_stream, cudaStreamNonBlocking));
+    if (!t->comm_done) SC_CUDA(cudaEventCreateWithFlags(&t->comm_done, cudaEventDisableTiming));
+}
+
+void exchange_bucket(sc_trainer* t, int b, int round) {
+    if (t->world == 1) return;
+    cudaStream_t s = t->ctx->stream;
+    if (t->xfer_used == t->xfer_events.size()) {
+        cudaEvent_t e;
+        SC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        t->xfer_events.push_back(e);
+    }
+    cudaEvent_t ev = t->xfer_events[t->xfer_used++];
+    SC_CUDA(cudaEventRecord(ev, s));
+    SC_CUDA(cudaStreamWaitEvent(t->comm_stream, ev, 0));
+    const int first = round * t->world;  // the round's partitions first .. first + world - 1 are contiguous
+    if (b < 0) {
+        double* base = t->part_loss.get() + first;
+        SC_NCCL(ncclAllGather(base + t->rank, base, 1, ncclFloat64, t->comm, t->comm_stream));
+    } else {
+        const int64_t len = t->b_len(b);
+        float* base = t->slot_ptr(b, first);
+        SC_NCCL(ncclAllGather(base + int64_t(t->rank) * len, base, size_t(len), ncclFloat32, t->comm,
+                              t->comm_stream));
+    }
 }
 
 void nccl_unique_id(uint8_t out[128]) {

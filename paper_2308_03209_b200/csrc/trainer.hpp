@@ -76,7 +76,19 @@ struct sc_trainer {
     int64_t head_off = 0, P = 0;
     double normalizer = 1.0;
     // parameters / optimizer / gradients
-    sc::DevBuf<float> theta, m1, m2, gathered, slots;
+    sc::DevBuf<float> theta, m1, m2, gathered;
+    // Per-partition gradient slots, bucket-major: bucket b (= parameter matrix
+    // b in for_each_matrix order: W_0, U_0, ..., W_{L-1}, U_{L-1}, head) holds
+    // pp = ceil(p / world) * world consecutive copies of its b_len[b] floats,
+    // one per partition, so the copies of one exchange round
+    // (partitions j*world .. j*world + world-1) are one contiguous range.
+    sc::DevBuf<float> slots;
+    int pp = 0;
+    std::vector<int64_t> b_off;      // nb + 1 offsets into the flat parameter vector
+    sc::DevBuf<int64_t> b_off_dev;
+    int nb() const { return static_cast<int>(b_off.size()) - 1; }
+    int64_t b_len(int b) const { return b_off[b + 1] - b_off[b]; }
+    float* slot_ptr(int b, int i) { return slots.get() + b_off[b] * pp + int64_t(i) * b_len(b); }
     int64_t adam_step = 0;
     // partitions
     std::vector<int> local;
@@ -102,6 +114,10 @@ struct sc_trainer {
     sc::TcGemm tc;
     sc::Profiler prof;
     ncclComm_t comm = nullptr;
+    cudaStream_t comm_stream = nullptr;      // gradient exchange, overlapped with backward
+    std::vector<cudaEvent_t> xfer_events;    // compute -> comm stream hand-offs (reused per step)
+    size_t xfer_used = 0;
+    cudaEvent_t comm_done = nullptr;
     ~sc_trainer();
 };
 
@@ -114,5 +130,8 @@ void trainer_step_async(sc_trainer* t, int epoch);
 void trainer_finish(sc_trainer* t, double* loss, double* gnorm);
 void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te);
 void trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
+// Exchange bucket b (or the losses, b = -1) of exchange round j across ranks
+// on the comm stream once the compute stream has produced it.
+void exchange_bucket(sc_trainer* t, int b, int round);
 void nccl_unique_id(uint8_t out[128]);
 }  // namespace sc
