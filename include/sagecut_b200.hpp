@@ -15,7 +15,9 @@
 // (std::invalid_argument, std::runtime_error, std::logic_error).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -161,10 +163,39 @@ public:
                                 s.adj_neighbors.data(), s.adj_edge_ids.data(), s.global_to_local.data()));
         return s;
     }
+    std::vector<std::string> warnings() const {  // partition.hpp:36
+        std::int64_t need = 0;
+        check(sc_vcut_warnings(get(), nullptr, 0, &need));
+        std::string buf(static_cast<std::size_t>(need), '\0');
+        check(sc_vcut_warnings(get(), buf.data(), need, &need));
+        buf.resize(std::strlen(buf.c_str()));
+        std::vector<std::string> out;
+        std::size_t a = 0;
+        while (!buf.empty() && a <= buf.size()) {
+            const std::size_t b = std::min(buf.find('\n', a), buf.size());
+            out.push_back(buf.substr(a, b - a));
+            a = b + 1;
+        }
+        return out;
+    }
 
 private:
     const Graph* g_ = nullptr;
     std::shared_ptr<sc_vcut> h_;
+};
+
+// partition.hpp:41-52 (host copy)
+struct EdgeCutPartition {
+    int num_parts = 0;
+    std::vector<int> node_assignment;
+    std::vector<std::vector<EdgeId>> kept_edges;
+    std::vector<EdgeId> cut_edges;
+    std::vector<std::vector<NodeId>> halo_sets;
+    std::size_t total_halo() const {
+        std::size_t h = 0;
+        for (const auto& s : halo_sets) h += s.size();
+        return h;
+    }
 };
 
 // partition.cpp:92-114, 22-90
@@ -176,6 +207,53 @@ inline VertexCutPartition partition_random(const Graph& g, int num_parts, std::u
 inline VertexCutPartition partition_dbh(const Graph& g, int num_parts, std::uint64_t seed) {
     sc_vcut* h = nullptr;
     check(sc_partition_dbh(g.get(), num_parts, seed, &h));
+    return VertexCutPartition(g, h);
+}
+// partition.cpp:116-201 (same assignment and warnings; O(E log E))
+inline VertexCutPartition partition_ne(const Graph& g, int num_parts, std::uint64_t seed, double balance_slack = 1.1) {
+    sc_vcut* h = nullptr;
+    check(sc_partition_ne(g.get(), num_parts, seed, balance_slack, &h));
+    return VertexCutPartition(g, h);
+}
+// partition.cpp:203-231
+inline EdgeCutPartition edge_cut_from_assignment(const Graph& g, int num_parts, std::vector<int> node_assignment) {
+    if (node_assignment.size() != static_cast<std::size_t>(g.num_nodes))
+        throw std::invalid_argument("node assignment length does not match node count");
+    const std::size_t p = static_cast<std::size_t>(std::max(num_parts, 1));
+    std::vector<std::int64_t> kept(p), halo(p);
+    std::int64_t ncut = 0;
+    check(sc_edge_cut_from_assignment(g.get(), num_parts, node_assignment.data(), kept.data(), &ncut, halo.data(),
+                                      nullptr, nullptr, nullptr));
+    std::int64_t nh = 0;
+    for (auto x : halo) nh += x;
+    std::vector<std::int32_t> kept_ids(g.num_edges() - static_cast<std::size_t>(ncut)), halo_nodes(nh);
+    EdgeCutPartition ec;
+    ec.num_parts = num_parts;
+    ec.cut_edges.resize(static_cast<std::size_t>(ncut));
+    check(sc_edge_cut_from_assignment(g.get(), num_parts, node_assignment.data(), kept.data(), &ncut, halo.data(),
+                                      kept_ids.data(), ec.cut_edges.data(), halo_nodes.data()));
+    std::size_t ka = 0, ha = 0;
+    for (int i = 0; i < num_parts; ++i) {
+        ec.kept_edges.emplace_back(kept_ids.begin() + ka, kept_ids.begin() + ka + kept[i]);
+        ec.halo_sets.emplace_back(halo_nodes.begin() + ha, halo_nodes.begin() + ha + halo[i]);
+        ka += kept[i];
+        ha += halo[i];
+    }
+    ec.node_assignment = std::move(node_assignment);
+    return ec;
+}
+// partition.cpp:233-278
+inline EdgeCutPartition partition_edge_cut_greedy(const Graph& g, int num_parts, std::uint64_t seed) {
+    std::vector<int> na(static_cast<std::size_t>(g.num_nodes));
+    check(sc_partition_edge_cut_greedy(g.get(), num_parts, seed, na.data()));
+    return edge_cut_from_assignment(g, num_parts, std::move(na));
+}
+// partition.cpp:280-308
+inline VertexCutPartition edge_cut_to_vertex_cut(const Graph& g, const EdgeCutPartition& ec, std::uint64_t seed) {
+    if (ec.node_assignment.size() != static_cast<std::size_t>(g.num_nodes))
+        throw std::invalid_argument("edge cut does not match graph");
+    sc_vcut* h = nullptr;
+    check(sc_edge_cut_to_vertex_cut(g.get(), ec.num_parts, ec.node_assignment.data(), seed, &h));
     return VertexCutPartition(g, h);
 }
 inline VertexCutPartition build_vertex_cut(const Graph& g, int num_parts, const std::vector<int>& edge_assignment) {

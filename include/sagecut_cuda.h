@@ -85,6 +85,27 @@ sc_status sc_partition_random(sc_graph* g, int32_t num_parts, uint64_t seed, sc_
 sc_status sc_partition_dbh(sc_graph* g, int32_t num_parts, uint64_t seed, sc_vcut** out);
 /* build_vertex_cut (partition.cpp:22-90) from a caller-supplied assignment. */
 sc_status sc_build_vertex_cut(sc_graph* g, int32_t num_parts, const int32_t* edge_assignment, sc_vcut** out);
+/* partition_ne (partition.cpp:116-201), output-identical: greedy neighbour
+ * expansion with a lazy-deletion (unassigned-degree, id) min-heap instead of
+ * the reference's boundary rescan. Overshoot reports -> sc_vcut_warnings. */
+sc_status sc_partition_ne(sc_graph* g, int32_t num_parts, uint64_t seed, double balance_slack, sc_vcut** out);
+/* partition_edge_cut_greedy (partition.cpp:233-278): node -> part (n, host). */
+sc_status sc_partition_edge_cut_greedy(sc_graph* g, int32_t num_parts, uint64_t seed, int32_t* node_assignment);
+/* edge_cut_from_assignment (partition.cpp:203-231): kept_counts[p] (may be
+ * NULL), *num_cut, halo_counts[p] (may be NULL); when non-NULL, kept_edges
+ * (m - num_cut: kept_edges part-major, each ascending), cut_edges (num_cut,
+ * ascending) and halo_nodes (sum halo_counts: halo_sets part-major, each
+ * ascending). Call once with NULL lists to size them. */
+sc_status sc_edge_cut_from_assignment(sc_graph* g, int32_t num_parts, const int32_t* node_assignment,
+                                      int64_t* kept_counts, int64_t* num_cut, int64_t* halo_counts,
+                                      int32_t* kept_edges, int32_t* cut_edges, int32_t* halo_nodes);
+/* edge_cut_to_vertex_cut (partition.cpp:280-308) of the edge cut induced by
+ * node_assignment (n, host). */
+sc_status sc_edge_cut_to_vertex_cut(sc_graph* g, int32_t num_parts, const int32_t* node_assignment, uint64_t seed,
+                                    sc_vcut** out);
+/* VertexCutPartition::warnings joined by '\n' (NUL-terminated, truncated to
+ * cap); *needed = full length + 1. */
+sc_status sc_vcut_warnings(sc_vcut* vc, char* buf, int64_t cap, int64_t* needed);
 sc_status sc_vcut_num_parts(sc_vcut* vc, int32_t* num_parts);
 sc_status sc_vcut_assignment(sc_vcut* vc, int32_t* out);
 sc_status sc_vcut_part_sizes(sc_vcut* vc, int32_t part, int64_t* n_local, int64_t* n_edges);

@@ -392,6 +392,55 @@ void* ref_build_vertex_cut(void* gp, int p, const std::int32_t* assign) {
         return nullptr;
     return out;
 }
+void* ref_partition_ne(void* gp, int p, std::uint64_t seed, double slack, char* wbuf, std::int64_t cap) {
+    VertexCutPartition* out = nullptr;
+    if (guard([&] {
+            out = new VertexCutPartition(partition_ne(*static_cast<Graph*>(gp), p, seed, slack));
+            std::string j;
+            for (const auto& x : out->warnings) j += (j.empty() ? "" : "\n") + x;
+            if (wbuf && cap > 0) {
+                std::strncpy(wbuf, j.c_str(), static_cast<std::size_t>(cap - 1));
+                wbuf[cap - 1] = 0;
+            }
+        }))
+        return nullptr;
+    return out;
+}
+int ref_edge_cut_greedy(void* gp, int p, std::uint64_t seed, std::int32_t* node_assign) {
+    return guard([&] {
+        const EdgeCutPartition ec = partition_edge_cut_greedy(*static_cast<Graph*>(gp), p, seed);
+        for (std::size_t v = 0; v < ec.node_assignment.size(); ++v) node_assign[v] = ec.node_assignment[v];
+    });
+}
+int ref_edge_cut_stats(void* gp, int p, const std::int32_t* na, std::int64_t* kept_counts, std::int64_t* num_cut,
+                       std::int64_t* halo_counts, std::int32_t* cut_edges, std::int32_t* halo_nodes) {
+    return guard([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        const EdgeCutPartition ec =
+            edge_cut_from_assignment(g, p, std::vector<int>(na, na + static_cast<std::size_t>(g.num_nodes)));
+        *num_cut = static_cast<std::int64_t>(ec.cut_edges.size());
+        for (int i = 0; i < p; ++i) {
+            kept_counts[i] = static_cast<std::int64_t>(ec.kept_edges[static_cast<std::size_t>(i)].size());
+            halo_counts[i] = static_cast<std::int64_t>(ec.halo_sets[static_cast<std::size_t>(i)].size());
+        }
+        if (cut_edges)
+            for (std::size_t k = 0; k < ec.cut_edges.size(); ++k) cut_edges[k] = static_cast<std::int32_t>(ec.cut_edges[k]);
+        if (halo_nodes)
+            for (const auto& h : ec.halo_sets)
+                for (const auto v : h) *halo_nodes++ = static_cast<std::int32_t>(v);
+    });
+}
+void* ref_edge_cut_to_vertex_cut(void* gp, int p, const std::int32_t* na, std::uint64_t seed) {
+    VertexCutPartition* out = nullptr;
+    if (guard([&] {
+            const Graph& g = *static_cast<Graph*>(gp);
+            const EdgeCutPartition ec =
+                edge_cut_from_assignment(g, p, std::vector<int>(na, na + static_cast<std::size_t>(g.num_nodes)));
+            out = new VertexCutPartition(edge_cut_to_vertex_cut(g, ec, seed));
+        }))
+        return nullptr;
+    return out;
+}
 void ref_partition_free(void* pp) { delete static_cast<VertexCutPartition*>(pp); }
 void ref_partition_assignment(void* pp, std::int32_t* out) {
     auto* vc = static_cast<VertexCutPartition*>(pp);

@@ -308,6 +308,169 @@ VCut partition_dbh(const Graph& g, int p, u64 seed) {  // :102-114
     return build_vertex_cut(g, p, std::move(a));
 }
 
+// partition.cpp:116-201 — greedy neighbour expansion, restated as the
+// reference's literal boundary scan (O(picks x |boundary|); small graphs only).
+VCut partition_ne(const Graph& g, int p, u64 /*seed*/, double slack, std::vector<std::string>& warnings) {
+    if (p < 1) throw std::invalid_argument("num_parts must be >= 1");
+    if (slack < 1.0) throw std::invalid_argument("partition_ne: balance_slack must be >= 1");
+    const std::size_t m = g.edges.size();
+    const std::size_t target = (m + static_cast<std::size_t>(p) - 1) / static_cast<std::size_t>(p);
+    std::vector<i32> assign(m, p - 1);
+    std::vector<std::uint8_t> done(m, 0), in_b(static_cast<std::size_t>(g.n), 0);
+    std::vector<i32> deg(g.degrees);
+    std::vector<i32> boundary;
+    std::size_t left = m;
+    i32 lowest = 0;
+    for (int part = 0; part + 1 < p && left > 0; ++part) {
+        boundary.clear();
+        std::fill(in_b.begin(), in_b.end(), 0);
+        std::size_t filled = 0;
+        while (filled < target && left > 0) {
+            i32 pick = -1, best = INT32_MAX;
+            std::size_t keep = 0;
+            for (std::size_t b = 0; b < boundary.size(); ++b) {  // :143-157
+                const i32 v = boundary[b];
+                if (deg[v] == 0) {
+                    in_b[v] = 0;
+                    continue;
+                }
+                boundary[keep++] = v;
+                if (deg[v] < best || (deg[v] == best && v < pick)) {
+                    best = deg[v];
+                    pick = v;
+                }
+            }
+            boundary.resize(keep);
+            if (pick < 0) {  // :159-165 lowest-id node with unassigned edges
+                while (lowest < g.n && deg[lowest] == 0) ++lowest;
+                if (lowest >= g.n) break;
+                pick = lowest;
+            } else {
+                in_b[pick] = 0;
+                boundary.erase(std::find(boundary.begin(), boundary.end(), pick));
+            }
+            for (i32 k = g.offsets[pick]; k < g.offsets[pick + 1]; ++k) {  // :170-186
+                const i32 e = g.eids[k];
+                if (done[e]) continue;
+                done[e] = 1;
+                assign[e] = part;
+                ++filled;
+                --left;
+                const i32 o = g.nbrs[k];
+                --deg[pick];
+                --deg[o];
+                if (!in_b[o] && deg[o] > 0) {
+                    in_b[o] = 1;
+                    boundary.push_back(o);
+                }
+            }
+        }
+        const auto limit = static_cast<std::size_t>(slack * static_cast<double>(target));  // :188-193
+        if (filled > limit)
+            warnings.push_back("part " + std::to_string(part) + " overshoot: " + std::to_string(filled) +
+                               " edges > slack limit " + std::to_string(limit));
+    }
+    return build_vertex_cut(g, p, std::move(assign));
+}
+
+// partition.cpp:203-231 — kept / cut edges and ascending halo sets.
+struct ECut {
+    int p = 0;
+    std::vector<i32> node_assign;
+    std::vector<std::vector<i32>> kept, halo;
+    std::vector<i32> cut;
+};
+ECut edge_cut_from_assignment(const Graph& g, int p, std::vector<i32> na) {
+    if (p < 1) throw std::invalid_argument("num_parts must be >= 1");
+    if (na.size() != static_cast<std::size_t>(g.n))
+        throw std::invalid_argument("node assignment length does not match node count");
+    for (i32 a : na)
+        if (a < 0 || a >= p) throw std::invalid_argument("node assignment references an invalid part");
+    ECut ec;
+    ec.p = p;
+    ec.node_assign = std::move(na);
+    ec.kept.resize(p);
+    ec.halo.resize(p);
+    for (std::size_t e = 0; e < g.edges.size(); ++e) {
+        const auto [u, v] = g.edges[e];
+        const i32 pu = ec.node_assign[u], pv = ec.node_assign[v];
+        if (pu == pv) {
+            ec.kept[pu].push_back(static_cast<i32>(e));
+        } else {
+            ec.cut.push_back(static_cast<i32>(e));
+            ec.halo[pv].push_back(u);
+            ec.halo[pu].push_back(v);
+        }
+    }
+    for (auto& h : ec.halo) {
+        std::sort(h.begin(), h.end());
+        h.erase(std::unique(h.begin(), h.end()), h.end());
+    }
+    return ec;
+}
+
+// partition.cpp:233-278 — seeded BFS region growing (restart: uniform pick
+// among the unassigned nodes in ascending id order).
+ECut partition_edge_cut_greedy(const Graph& g, int p, u64 seed) {
+    if (p < 1) throw std::invalid_argument("num_parts must be >= 1");
+    const std::size_t n = static_cast<std::size_t>(g.n);
+    Rng rng(substream(seed, "partition.edge_cut"));
+    std::vector<i32> a(n, -1);
+    const std::size_t base = n / static_cast<std::size_t>(p), rem = n % static_cast<std::size_t>(p);
+    std::size_t assigned = 0;
+    for (int part = 0; part < p && assigned < n; ++part) {
+        const std::size_t target = base + (static_cast<std::size_t>(part) < rem ? 1 : 0);
+        std::size_t size = 0;
+        std::vector<i32> q;
+        std::size_t head = 0;
+        while (size < target && assigned < n) {
+            if (head == q.size()) {
+                std::vector<i32> free_nodes;
+                for (i32 v = 0; v < g.n; ++v)
+                    if (a[v] < 0) free_nodes.push_back(v);
+                const i32 start = free_nodes[static_cast<std::size_t>(rng.next_below(free_nodes.size()))];
+                a[start] = part;
+                ++size;
+                ++assigned;
+                q.push_back(start);
+                continue;
+            }
+            const i32 v = q[head++];
+            for (i32 k = g.offsets[v]; k < g.offsets[v + 1]; ++k) {
+                if (size >= target) break;
+                const i32 u = g.nbrs[k];
+                if (a[u] >= 0) continue;
+                a[u] = part;
+                ++size;
+                ++assigned;
+                q.push_back(u);
+            }
+        }
+    }
+    return edge_cut_from_assignment(g, p, std::move(a));
+}
+
+// partition.cpp:280-308
+VCut edge_cut_to_vertex_cut(const Graph& g, const ECut& ec, u64 seed) {
+    if (ec.node_assign.size() != static_cast<std::size_t>(g.n))
+        throw std::invalid_argument("edge cut does not match graph");
+    std::vector<i32> a(g.edges.size(), -1);
+    for (int part = 0; part < ec.p; ++part)
+        for (i32 e : ec.kept[part]) a[e] = part;
+    i32 anchor = -1;
+    if (!ec.cut.empty()) {
+        const auto& first = g.edges[*std::min_element(ec.cut.begin(), ec.cut.end())];
+        anchor = std::min(first.first, first.second);
+    }
+    Rng rng(substream(seed, "partition.ec2vc"));
+    for (i32 e : ec.cut) {
+        const auto [u, v] = g.edges[e];
+        const i32 keep = (u == anchor || v == anchor) ? anchor : ((rng.next_u64() & 1u) ? u : v);
+        a[e] = ec.node_assign[keep];
+    }
+    return build_vertex_cut(g, ec.p, std::move(a));
+}
+
 // ---- reweight.cpp:23-81 -----------------------------------------------------------
 std::vector<std::vector<double>> weights(const Graph& g, const VCut& vc, int scheme) {
     std::vector<std::vector<double>> w;
@@ -950,7 +1113,11 @@ void* or_partition(void* gp, int algo, int p, uint64_t seed) {
             const Graph& g = *static_cast<Graph*>(gp);
             if (algo == 0) out = new VCut(partition_random(g, p, seed));
             else if (algo == 1) out = new VCut(partition_dbh(g, p, seed));
-            else throw std::invalid_argument("oracle: only random (0) and dbh (1) are restated");
+            else if (algo == 2) {
+                std::vector<std::string> w;
+                out = new VCut(partition_ne(g, p, seed, 1.1, w));
+            } else if (algo == 3) out = new VCut(edge_cut_to_vertex_cut(g, partition_edge_cut_greedy(g, p, seed), seed));
+            else throw std::invalid_argument("oracle: unknown partition algorithm");
         }))
         return nullptr;
     return out;
@@ -960,6 +1127,59 @@ void* or_build_vertex_cut(void* gp, int p, const int32_t* assign) {
     if (guard([&] {
             const Graph& g = *static_cast<Graph*>(gp);
             out = new VCut(build_vertex_cut(g, p, std::vector<i32>(assign, assign + g.edges.size())));
+        }))
+        return nullptr;
+    return out;
+}
+// partition_ne with an explicit balance_slack; warnings joined by '\n' into
+// wbuf (cap bytes, NUL-terminated).
+void* or_partition_ne(void* gp, int p, uint64_t seed, double slack, char* wbuf, int64_t cap) {
+    VCut* out = nullptr;
+    if (guard([&] {
+            std::vector<std::string> w;
+            out = new VCut(partition_ne(*static_cast<Graph*>(gp), p, seed, slack, w));
+            std::string j;
+            for (const auto& x : w) j += (j.empty() ? "" : "\n") + x;
+            if (wbuf && cap > 0) {
+                std::strncpy(wbuf, j.c_str(), static_cast<std::size_t>(cap - 1));
+                wbuf[cap - 1] = 0;
+            }
+        }))
+        return nullptr;
+    return out;
+}
+int or_edge_cut_greedy(void* gp, int p, uint64_t seed, int32_t* node_assign) {
+    return guard([&] {
+        const ECut ec = partition_edge_cut_greedy(*static_cast<Graph*>(gp), p, seed);
+        std::memcpy(node_assign, ec.node_assign.data(), ec.node_assign.size() * 4);
+    });
+}
+// kept_counts[p], num_cut, halo_counts[p]; cut_edges (num_cut) and halo_nodes
+// (sum halo_counts, part-major, ascending) when non-null.
+int or_edge_cut_stats(void* gp, int p, const int32_t* na, int64_t* kept_counts, int64_t* num_cut,
+                      int64_t* halo_counts, int32_t* cut_edges, int32_t* halo_nodes) {
+    return guard([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        const ECut ec = edge_cut_from_assignment(g, p, std::vector<i32>(na, na + g.n));
+        *num_cut = static_cast<int64_t>(ec.cut.size());
+        for (int i = 0; i < p; ++i) {
+            kept_counts[i] = static_cast<int64_t>(ec.kept[i].size());
+            halo_counts[i] = static_cast<int64_t>(ec.halo[i].size());
+        }
+        if (cut_edges) std::memcpy(cut_edges, ec.cut.data(), ec.cut.size() * 4);
+        if (halo_nodes)
+            for (const auto& h : ec.halo) {
+                std::memcpy(halo_nodes, h.data(), h.size() * 4);
+                halo_nodes += h.size();
+            }
+    });
+}
+void* or_edge_cut_to_vertex_cut(void* gp, int p, const int32_t* na, uint64_t seed) {
+    VCut* out = nullptr;
+    if (guard([&] {
+            const Graph& g = *static_cast<Graph*>(gp);
+            out = new VCut(edge_cut_to_vertex_cut(g, edge_cut_from_assignment(g, p, std::vector<i32>(na, na + g.n)),
+                                                  seed));
         }))
         return nullptr;
     return out;

@@ -46,7 +46,13 @@ int or_graph_set_data(void* g, const float* features, int d, const int32_t* labe
                       const uint8_t* train, const uint8_t* val, const uint8_t* test);
 
 /* partition.cpp */
-void* or_partition(void* g, int algo /*0 random, 1 dbh*/, int p, uint64_t seed);
+void* or_partition(void* g, int algo /*0 random, 1 dbh, 2 ne (slack 1.1), 3 edge-cut greedy -> ec2vc*/, int p,
+                   uint64_t seed);
+void* or_partition_ne(void* g, int p, uint64_t seed, double slack, char* warnings, int64_t cap);
+int or_edge_cut_greedy(void* g, int p, uint64_t seed, int32_t* node_assign);
+int or_edge_cut_stats(void* g, int p, const int32_t* node_assign, int64_t* kept_counts, int64_t* num_cut,
+                      int64_t* halo_counts, int32_t* cut_edges, int32_t* halo_nodes);
+void* or_edge_cut_to_vertex_cut(void* g, int p, const int32_t* node_assign, uint64_t seed);
 void* or_build_vertex_cut(void* g, int p, const int32_t* assign);
 void or_partition_free(void* p);
 void or_partition_assignment(void* p, int32_t* out);

@@ -250,6 +250,65 @@ sc_status sc_build_vertex_cut(sc_graph* g, int32_t p, const int32_t* assign, sc_
         *out = build_vertex_cut_device(g, p, std::move(a)).release();
     });
 }
+sc_status sc_partition_ne(sc_graph* g, int32_t p, uint64_t seed, double balance_slack, sc_vcut** out) {
+    return guard([&] {
+        REQUIRE_ARG(g && out, "sc_partition_ne: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        REQUIRE_ARG(balance_slack >= 1.0, "partition_ne: balance_slack must be >= 1");
+        (void)seed;  // growth order is fully fixed by the tie-break rules (partition.cpp:123)
+        set_device(g->ctx);
+        std::vector<std::string> warnings;
+        const std::vector<int32_t> a = ne_assign_host(g, p, balance_slack, warnings);
+        DevBuf<int32_t> d(std::max<int64_t>(g->m, 1));
+        h2d(d.get(), a.data(), g->m, g->ctx->stream);
+        auto vc = build_vertex_cut_device(g, p, std::move(d));
+        vc->warnings = std::move(warnings);
+        *out = vc.release();
+    });
+}
+sc_status sc_partition_edge_cut_greedy(sc_graph* g, int32_t p, uint64_t seed, int32_t* node_assignment) {
+    return guard([&] {
+        REQUIRE_ARG(g && (node_assignment || g->n == 0), "sc_partition_edge_cut_greedy: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        set_device(g->ctx);
+        const std::vector<int32_t> a = edge_cut_greedy_host(g, p, seed);
+        std::copy(a.begin(), a.end(), node_assignment);
+    });
+}
+sc_status sc_edge_cut_from_assignment(sc_graph* g, int32_t p, const int32_t* node_assignment, int64_t* kept_counts,
+                                      int64_t* num_cut, int64_t* halo_counts, int32_t* kept_edges, int32_t* cut_edges,
+                                      int32_t* halo_nodes) {
+    return guard([&] {
+        REQUIRE_ARG(g && num_cut && (node_assignment || g->n == 0), "sc_edge_cut_from_assignment: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        set_device(g->ctx);
+        edge_cut_stats_device(g, p, node_assignment, kept_counts, num_cut, halo_counts, kept_edges, cut_edges,
+                              halo_nodes);
+    });
+}
+sc_status sc_edge_cut_to_vertex_cut(sc_graph* g, int32_t p, const int32_t* node_assignment, uint64_t seed,
+                                    sc_vcut** out) {
+    return guard([&] {
+        REQUIRE_ARG(g && out && (node_assignment || g->n == 0), "sc_edge_cut_to_vertex_cut: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        set_device(g->ctx);
+        DevBuf<int32_t> a(std::max<int64_t>(g->m, 1));
+        ec2vc_assign_device(g, p, node_assignment, seed, a.get());
+        *out = build_vertex_cut_device(g, p, std::move(a)).release();
+    });
+}
+sc_status sc_vcut_warnings(sc_vcut* vc, char* buf, int64_t cap, int64_t* needed) {
+    return guard([&] {
+        std::string j;
+        for (const auto& w : vc->warnings) j += (j.empty() ? "" : "\n") + w;
+        if (needed) *needed = static_cast<int64_t>(j.size()) + 1;
+        if (buf && cap > 0) {
+            const size_t k = std::min<size_t>(j.size(), size_t(cap - 1));
+            std::memcpy(buf, j.data(), k);
+            buf[k] = 0;
+        }
+    });
+}
 sc_status sc_vcut_num_parts(sc_vcut* vc, int32_t* p) {
     return guard([&] { *p = vc->p; });
 }

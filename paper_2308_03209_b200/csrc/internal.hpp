@@ -120,6 +120,7 @@ struct sc_vcut {
     sc::DevBuf<int32_t> g2l;           // p x n, -1 where absent
     sc::DevBuf<int32_t> per_node_rf;   // n
     std::vector<PartDev> parts;
+    std::vector<std::string> warnings; // VertexCutPartition::warnings (partition_ne overshoot reports)
 };
 
 namespace sc {
@@ -132,6 +133,13 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
 void assign_random(sc_graph* g, int32_t p, uint64_t seed, int32_t* assign);
 void assign_dbh(sc_graph* g, int32_t p, uint64_t seed, int32_t* assign);
 void compute_weights_device(sc_vcut* vc, int scheme, int32_t part, double* out_dev);
+// partition_seq.cu (partition.cpp:116-308)
+std::vector<int32_t> ne_assign_host(sc_graph* g, int32_t p, double slack, std::vector<std::string>& warnings);
+std::vector<int32_t> edge_cut_greedy_host(sc_graph* g, int32_t p, uint64_t seed);
+void ec2vc_assign_device(sc_graph* g, int32_t p, const int32_t* node_assign_host, uint64_t seed, int32_t* assign_dev);
+void edge_cut_stats_device(sc_graph* g, int32_t p, const int32_t* node_assign_host, int64_t* kept_counts,
+                           int64_t* num_cut, int64_t* halo_counts, int32_t* kept_edges_host, int32_t* cut_edges_host,
+                           int32_t* halo_nodes_host);
 // dropedge.cu
 void precompute_masks_device(sc_ctx* ctx, int64_t m, int32_t k, double ratio, uint64_t seed, uint8_t* out_dev);
 // init

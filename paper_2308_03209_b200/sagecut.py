@@ -78,6 +78,11 @@ _sig("sc_vcut_part_sizes", [_vp, _i32, C.POINTER(_i64), C.POINTER(_i64)])
 _sig("sc_vcut_part_copy", [_vp, _i32] + [_vp] * 8)
 _sig("sc_replication_stats", [_vp, _vp, C.POINTER(_f64), C.POINTER(_f64), C.POINTER(_f64), C.POINTER(_i64)])
 _sig("sc_vcut_destroy", [_vp])
+_sig("sc_partition_ne", [_vp, _i32, _u64, _f64, _pp])
+_sig("sc_partition_edge_cut_greedy", [_vp, _i32, _u64, _vp])
+_sig("sc_edge_cut_from_assignment", [_vp, _i32, _vp, _vp, C.POINTER(_i64), _vp, _vp, _vp, _vp])
+_sig("sc_edge_cut_to_vertex_cut", [_vp, _i32, _vp, _u64, _pp])
+_sig("sc_vcut_warnings", [_vp, C.c_char_p, _i64, C.POINTER(_i64)])
 _sig("sc_compute_weights", [_vp, _i32, _vp])
 _sig("sc_precompute_masks", [_vp, _i64, _i32, _f64, _u64, _vp])
 _sig("sc_select_mask", [_u64, _u64, _u64, _i32], _i32)
@@ -358,6 +363,15 @@ class VertexCutPartition:
     def parts(self) -> List[PartSubgraph]:
         return [self.part(i) for i in range(self.num_parts)]
 
+    @property
+    def warnings(self) -> List[str]:  # VertexCutPartition::warnings (partition.hpp:36)
+        need = _i64()
+        _check(_lib.sc_vcut_warnings(self.h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(int(need.value))
+        _check(_lib.sc_vcut_warnings(self.h, buf, len(buf), C.byref(need)))
+        w = buf.value.decode()
+        return w.split("\n") if w else []
+
     def __del__(self):
         if getattr(self, "h", None):
             _lib.sc_vcut_destroy(self.h)
@@ -373,6 +387,60 @@ def partition_random(g: Graph, num_parts: int, seed: int) -> VertexCutPartition:
 def partition_dbh(g: Graph, num_parts: int, seed: int) -> VertexCutPartition:  # partition.cpp:102
     h = _vp()
     _check(_lib.sc_partition_dbh(g.h, num_parts, seed, C.byref(h)), "partition_dbh")
+    return VertexCutPartition(h, g)
+
+
+def partition_ne(g: Graph, num_parts: int, seed: int, balance_slack: float = 1.1) -> VertexCutPartition:
+    """partition_ne (partition.cpp:116-201): same assignment as the reference, O(E log E)."""
+    h = _vp()
+    _check(_lib.sc_partition_ne(g.h, num_parts, seed, float(balance_slack), C.byref(h)), "partition_ne")
+    return VertexCutPartition(h, g)
+
+
+@dataclass
+class EdgeCutPartition:  # partition.hpp:41-52
+    num_parts: int
+    node_assignment: np.ndarray
+    kept_edges: List[np.ndarray]
+    cut_edges: np.ndarray
+    halo_sets: List[np.ndarray]
+
+    def total_halo(self) -> int:
+        return int(sum(len(h) for h in self.halo_sets))
+
+
+def edge_cut_from_assignment(g: Graph, num_parts: int, node_assignment) -> EdgeCutPartition:  # partition.cpp:203
+    na = np.ascontiguousarray(node_assignment, np.int32)
+    if len(na) != g.num_nodes:
+        raise ValueError("node assignment length does not match node count")
+    kept = np.zeros(max(num_parts, 1), np.int64)
+    halo = np.zeros(max(num_parts, 1), np.int64)
+    ncut = _i64()
+    _check(_lib.sc_edge_cut_from_assignment(g.h, num_parts, _ptr(na), _ptr(kept), C.byref(ncut), _ptr(halo), None,
+                                            None, None), "edge_cut_from_assignment")
+    kept_ids = np.zeros(g.num_edges() - ncut.value, np.int32)
+    cut = np.zeros(ncut.value, np.int32)
+    nodes = np.zeros(int(halo.sum()), np.int32)
+    _check(_lib.sc_edge_cut_from_assignment(g.h, num_parts, _ptr(na), _ptr(kept), C.byref(ncut), _ptr(halo),
+                                            _ptr(kept_ids), _ptr(cut), _ptr(nodes)), "edge_cut_from_assignment")
+    kb = np.concatenate([[0], np.cumsum(kept[:num_parts])])
+    hb = np.concatenate([[0], np.cumsum(halo[:num_parts])])
+    return EdgeCutPartition(num_parts, na, [kept_ids[kb[i]:kb[i + 1]] for i in range(num_parts)], cut,
+                            [nodes[hb[i]:hb[i + 1]] for i in range(num_parts)])
+
+
+def partition_edge_cut_greedy(g: Graph, num_parts: int, seed: int) -> EdgeCutPartition:  # partition.cpp:233
+    na = np.zeros(g.num_nodes, np.int32)
+    _check(_lib.sc_partition_edge_cut_greedy(g.h, num_parts, seed, _ptr(na)), "partition_edge_cut_greedy")
+    return edge_cut_from_assignment(g, num_parts, na)
+
+
+def edge_cut_to_vertex_cut(g: Graph, ec: EdgeCutPartition, seed: int) -> VertexCutPartition:  # partition.cpp:280
+    na = np.ascontiguousarray(ec.node_assignment, np.int32)
+    if len(na) != g.num_nodes:
+        raise ValueError("edge cut does not match graph")
+    h = _vp()
+    _check(_lib.sc_edge_cut_to_vertex_cut(g.h, ec.num_parts, _ptr(na), seed, C.byref(h)), "edge_cut_to_vertex_cut")
     return VertexCutPartition(h, g)
 
 

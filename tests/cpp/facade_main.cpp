@@ -50,6 +50,18 @@ int main(int argc, char** argv) {
         for (auto b : masks.masks[0]) std::printf(" %d", int(b));
         std::printf("\n");
 
+        // greedy partitioners (partition.cpp:116-308) through the facade
+        const auto ne = sb::partition_ne(g, p, 0, 1.0);
+        std::printf("ne");
+        for (int a : ne.edge_assignment()) std::printf(" %d", a);
+        std::printf("\nne_warnings %zu\n", ne.warnings().size());
+        const auto ec = sb::partition_edge_cut_greedy(g, p, 5);
+        std::printf("ec_nodes");
+        for (int a : ec.node_assignment) std::printf(" %d", a);
+        std::printf("\nec_cut %zu\nec_halo %zu\nec2vc", ec.cut_edges.size(), ec.total_halo());
+        for (int a : sb::edge_cut_to_vertex_cut(g, ec, 5).edge_assignment()) std::printf(" %d", a);
+        std::printf("\n");
+
         sb::TrainConfig cfg;
         cfg.layers = 2;
         cfg.hidden = {16};

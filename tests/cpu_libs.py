@@ -77,6 +77,12 @@ class CpuLib:
         f("graph_set_data").argtypes = [_p, _f32p, C.c_int, _i32p, C.c_int, _u8p, _u8p, _u8p]
         f("partition").restype = _p
         f("partition").argtypes = [_p, C.c_int, C.c_int, C.c_uint64]
+        f("partition_ne").restype = _p
+        f("partition_ne").argtypes = [_p, C.c_int, C.c_uint64, C.c_double, C.c_char_p, C.c_int64]
+        f("edge_cut_greedy").argtypes = [_p, C.c_int, C.c_uint64, _i32p]
+        f("edge_cut_stats").argtypes = [_p, C.c_int, _i32p, _p, _p, _p, _p, _p]
+        f("edge_cut_to_vertex_cut").restype = _p
+        f("edge_cut_to_vertex_cut").argtypes = [_p, C.c_int, _i32p, C.c_uint64]
         f("build_vertex_cut").restype = _p
         f("build_vertex_cut").argtypes = [_p, C.c_int, _i32p]
         f("partition_free").argtypes = [_p]
@@ -224,6 +230,40 @@ class Graph:
         algo_id = {"random": 0, "dbh": 1, "ne": 2, "ec2vc": 3}[algo]
         h = self.lib._f("partition")(self.h, algo_id, p, seed)
         return Partition(self, self.lib._checked_handle(h, f"partition_{algo}"), p)
+
+    def partition_ne(self, p, seed, slack=1.1):
+        """partition_ne with its warnings (partition.cpp:116-201)."""
+        buf = C.create_string_buffer(1 << 16)
+        h = self.lib._f("partition_ne")(self.h, p, seed, slack, buf, len(buf))
+        part = Partition(self, self.lib._checked_handle(h, "partition_ne"), p)
+        w = buf.value.decode()
+        return part, (w.split("\n") if w else [])
+
+    def edge_cut_greedy(self, p, seed):
+        """partition_edge_cut_greedy's node assignment (partition.cpp:233-278)."""
+        out = np.zeros(self.n, np.int32)
+        self.lib._check(self.lib._f("edge_cut_greedy")(self.h, p, seed, out), "edge_cut_greedy")
+        return out
+
+    def edge_cut(self, p, node_assign):
+        """edge_cut_from_assignment (partition.cpp:203-231): kept counts, cut edges, halo sets."""
+        na = np.ascontiguousarray(node_assign, np.int32)
+        kept = np.zeros(p, np.int64)
+        halo = np.zeros(p, np.int64)
+        ncut = C.c_int64()
+        f = self.lib._f("edge_cut_stats")
+        self.lib._check(f(self.h, p, na, kept.ctypes.data_as(_p), C.byref(ncut), halo.ctypes.data_as(_p), None, None),
+                        "edge_cut_stats")
+        cut = np.zeros(ncut.value, np.int32)
+        nodes = np.zeros(int(halo.sum()), np.int32)
+        self.lib._check(f(self.h, p, na, kept.ctypes.data_as(_p), C.byref(ncut), halo.ctypes.data_as(_p),
+                          cut.ctypes.data_as(_p), nodes.ctypes.data_as(_p)), "edge_cut_stats")
+        bounds = np.concatenate([[0], np.cumsum(halo)])
+        return kept, cut, [nodes[bounds[i]:bounds[i + 1]] for i in range(p)]
+
+    def edge_cut_to_vertex_cut(self, p, node_assign, seed):
+        h = self.lib._f("edge_cut_to_vertex_cut")(self.h, p, np.ascontiguousarray(node_assign, np.int32), seed)
+        return Partition(self, self.lib._checked_handle(h, "edge_cut_to_vertex_cut"), p)
 
     def build_vertex_cut(self, p, assign):
         h = self.lib._f("build_vertex_cut")(self.h, p, np.ascontiguousarray(assign, np.int32))

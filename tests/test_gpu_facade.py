@@ -45,4 +45,12 @@ def test_cpp_facade_matches_oracle(tmp_path):
     np.testing.assert_allclose(np.array(res["loss"].split(), float), ref_loss, rtol=1e-5)
     theta = np.array(res["params"].split(), float)
     assert np.linalg.norm(theta - t.params()) / np.linalg.norm(t.params()) <= 1e-4
+    ne, warn = og.partition_ne(p, 0, 1.0)
+    assert [int(x) for x in res["ne"].split()] == ne.assignment().tolist()
+    assert int(res["ne_warnings"]) == len(warn)
+    na = og.edge_cut_greedy(p, 5)
+    assert [int(x) for x in res["ec_nodes"].split()] == na.tolist()
+    kept, cut, halo = og.edge_cut(p, na)
+    assert int(res["ec_cut"]) == len(cut) and int(res["ec_halo"]) == sum(len(h) for h in halo)
+    assert [int(x) for x in res["ec2vc"].split()] == og.edge_cut_to_vertex_cut(p, na, 5).assignment().tolist()
     assert res["error"].startswith("invalid_argument num_parts must be >= 1")
