@@ -1277,11 +1277,13 @@ void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b
 }
 
 void TcGemm::tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1,
-                const MatT* b2, const float* amax_b2, int64_t M, float* C, int64_t ldc) {
+                const MatT* b2, const float* amax_b2, int64_t M, float* C, int64_t ldc, cudaStream_t s, float* ws) {
+    if (!s) s = t->ctx->stream;
+    if (!ws) ws = t->ws.get();
     if (enabled && tn_supported(a, b1, b2))
-        gemm_tn_f16x3(a, amax_a, b1, amax_b1, b2, amax_b2, M, C, ldc, t->ws.get(), t->ws_floats, t->ctx->stream);
+        gemm_tn_f16x3(a, amax_a, b1, amax_b1, b2, amax_b2, M, C, ldc, ws, t->ws_floats, s);
     else
-        gemm_tn(a, b1, b2, M, C, ldc, t->ws.get(), t->ws_floats, t->ctx->stream);
+        gemm_tn(a, b1, b2, M, C, ldc, ws, t->ws_floats, s);
 }
 
 }  // namespace sc

@@ -59,8 +59,9 @@ struct TcGemm {
     void nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2, const float* amax2,
             const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
             float* amax_out);
+    // s / ws: stream and split-K workspace (default: the context stream, t->ws)
     void tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
-            const float* amax_b2, int64_t M, float* C, int64_t ldc);
+            const float* amax_b2, int64_t M, float* C, int64_t ldc, cudaStream_t s = nullptr, float* ws = nullptr);
 };
 
 }  // namespace sc

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -72,8 +73,19 @@ Profiler::~Profiler() {
 
 using namespace sc;
 
+cudaEvent_t sc_trainer::fork_event() {
+    if (fork_used == fork_events.size()) {
+        cudaEvent_t e;
+        SC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        fork_events.push_back(e);
+    }
+    return fork_events[fork_used++ % fork_events.size()];
+}
+
 sc_trainer::~sc_trainer() {
     if (comm) ncclCommDestroy(comm);
+    for (cudaEvent_t e : fork_events) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
     for (cudaEvent_t e : xfer_events) cudaEventDestroy(e);
     if (comm_done) cudaEventDestroy(comm_done);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -195,6 +207,13 @@ void trainer_init(sc_trainer* t) {
     }
     t->ws_floats = gemm_tn_workspace_floats(maxN1, maxN2);
     t->ws.alloc(t->ws_floats);
+    if (const char* o = std::getenv("SC_OVERLAP")) t->overlap = std::atoi(o) != 0;
+    if (t->overlap) {
+        t->ws_side.alloc(t->ws_floats);
+        int least = 0, greatest = 0;
+        SC_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        SC_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, greatest));
+    }
     t->tc.init(t);
     SC_CUDA(cudaStreamSynchronize(s));
 }
@@ -315,23 +334,36 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
 void backward(sc_trainer* t, const Rows& R, int i) {
     const int round = i / t->world;
     cudaStream_t s = t->ctx->stream;
+    // side stream for the weight-gradient GEMMs that need only dh (see trainer.hpp)
+    cudaStream_t w = t->overlap ? t->side : s;
+    float* ws_w = t->overlap ? t->ws_side.get() : t->ws.get();
+    auto hand_off = [&](cudaStream_t from, cudaStream_t to) {
+        if (from == to) return;
+        cudaEvent_t ev = t->fork_event();
+        SC_CUDA(cudaEventRecord(ev, from));
+        SC_CUDA(cudaStreamWaitEvent(to, ev, 0));
+    };
     Profiler& P = t->prof;
     const int64_t n = R.n;
     const MatT x0t{R.x0, t->d, nullptr, t->d};
     const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L].get(), t->E, nullptr, t->E};
-    // head grad = G^T emb ; dh = G head   (:259-260)
-    P.begin("wgrad", 4.0 * n * (t->C + t->E), s);
+    // head grad = G^T emb (side) ; dh = G head (main)   (:259-260)
+    hand_off(s, w);
+    P.begin("wgrad", 4.0 * n * (t->C + t->E), w);
     const float* x0_amax = t->g->feat_amax.get();
     const float* emb_amax = t->L == 0 ? x0_amax : t->amax_x(t->L);
     t->tc.tn(t, MatT{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
-             t->slot_ptr(2 * t->L, i), t->E);
-    P.end(s);
-    exchange_bucket(t, 2 * t->L, round);
+             t->slot_ptr(2 * t->L, i), t->E, w, ws_w);
+    P.end(w);
+    exchange_bucket(t, 2 * t->L, round, w);
     float* dh = t->dh.get();
     float* dh2 = t->dh2.get();
     float* dh_amax = t->amax_slot(sc_trainer::kSlotDh0);
     float* dh2_amax = t->amax_slot(sc_trainer::kSlotDh1);
-    if (t->L == 0) return;
+    if (t->L == 0) {
+        hand_off(w, s);
+        return;
+    }
     P.begin("gemm_dgrad", 4.0 * n * (t->C + t->E), s);
     t->tc.nt(t, MatA{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, MatB{t->theta.get() + t->head_off, t->E, true},
              nullptr, nullptr, nullptr, dh, t->E, n, t->E, kEpiNone, nullptr, dh_amax);
@@ -340,18 +372,21 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         const LayerOff& lo = t->lay[l];
         const MatT xint = l == 0 ? x0t : MatT{t->X[l].get(), lo.in, nullptr, lo.in};
         const MatT dht{dh, lo.H, nullptr, lo.H};
-        // dU = dh^T [mean | h_in]   (:271-272)
         const MatT meant{t->MEAN[l].get(), lo.H, nullptr, lo.H};
-        P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), s);
         const float* xin_amax = l == 0 ? x0_amax : t->amax_x(l);
-        t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, t->slot_ptr(2 * l + 1, i), lo.H + lo.in);
-        P.end(s);
-        exchange_bucket(t, 2 * l + 1, round);
         // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
         P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s);
         t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr,
                  nullptr, nullptr, t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get(), nullptr);
         P.end(s);
+        // dU = dh^T [mean | h_in] (:271-272) on the side stream: tensor-bound, it
+        // shares the SMs with the HBM-bound transposed aggregation below
+        hand_off(s, w);
+        P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), w);
+        t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, t->slot_ptr(2 * l + 1, i), lo.H + lo.in,
+                 w, ws_w);
+        P.end(w);
+        exchange_bucket(t, 2 * l + 1, round, w);
         // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
         float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
         SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
@@ -375,6 +410,7 @@ void backward(sc_trainer* t, const Rows& R, int i) {
             std::swap(dh, dh2);
             std::swap(dh_amax, dh2_amax);
         }
+        hand_off(w, s);  // dU(l) read the old dh / dh_amax, which the next layer overwrites
     }
 }
 
@@ -428,6 +464,7 @@ void trainer_step_async(sc_trainer* t, int epoch) {
     // writer, so the exchange moves bits and the ordered sum below is bitwise
     // the reference's single-process gather for any GPU count.
     t->xfer_used = 0;
+    t->fork_used = 0;
     const int rounds = t->pp / t->world;
     for (int j = 0; j < rounds; ++j) {
         const int i = j * t->world + t->rank;
@@ -511,9 +548,9 @@ void trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
     if (!t->comm_done) SC_CUDA(cudaEventCreateWithFlags(&t->comm_done, cudaEventDisableTiming));
 }
 
-void exchange_bucket(sc_trainer* t, int b, int round) {
+void exchange_bucket(sc_trainer* t, int b, int round, cudaStream_t producer) {
     if (t->world == 1) return;
-    cudaStream_t s = t->ctx->stream;
+    cudaStream_t s = producer ? producer : t->ctx->stream;
     if (t->xfer_used == t->xfer_events.size()) {
         cudaEvent_t e;
         SC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

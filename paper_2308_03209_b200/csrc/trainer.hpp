@@ -96,7 +96,16 @@ struct sc_trainer {
     // activations (rows_cap rows)
     int64_t rows_cap = 0;
     std::vector<sc::DevBuf<float>> X, MSG, MEAN;
-    sc::DevBuf<float> inv, G, dh, dh2, dmean, dz, eval_logits, ws;
+    sc::DevBuf<float> inv, G, dh, dh2, dmean, dz, eval_logits, ws, ws_side;
+    // Backward runs the weight-gradient GEMMs that only need dh (head: G^T emb;
+    // update: dh^T [mean | h]) on a high-priority side stream, concurrently with
+    // the dgrad -> transposed aggregation -> dW chain on the main stream
+    // (SC_OVERLAP=0 keeps everything on the main stream).
+    bool overlap = true;
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> fork_events;
+    size_t fork_used = 0;
+    cudaEvent_t fork_event();
     int64_t ws_floats = 0;
     sc::DevBuf<double> row_loss, part_loss, out2, red_partial;
     sc::DevBuf<int> nonfinite;
@@ -132,6 +141,6 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te);
 void trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
 // Exchange bucket b (or the losses, b = -1) of exchange round j across ranks
 // on the comm stream once the compute stream has produced it.
-void exchange_bucket(sc_trainer* t, int b, int round);
+void exchange_bucket(sc_trainer* t, int b, int round, cudaStream_t producer = nullptr);
 void nccl_unique_id(uint8_t out[128]);
 }  // namespace sc
