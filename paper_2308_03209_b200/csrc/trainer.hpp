@@ -99,9 +99,11 @@ struct sc_trainer {
     sc::DevBuf<float> inv, G, dh, dh2, dmean, dz, eval_logits, ws, ws_side;
     // Backward runs the weight-gradient GEMMs that only need dh (head: G^T emb;
     // update: dh^T [mean | h]) on a high-priority side stream, concurrently with
-    // the dgrad -> transposed aggregation -> dW chain on the main stream
-    // (SC_OVERLAP=0 keeps everything on the main stream).
-    bool overlap = true;
+    // the dgrad -> transposed aggregation -> dW chain on the main stream.
+    // Opt-in (SC_OVERLAP=1): on B200 the two contend for HBM and the epoch
+    // gains <1 % (profiles/r01_overlap_ab.txt), while the aggregation's own
+    // duration, and so its roofline figure, doubles.
+    bool overlap = false;
     cudaStream_t side = nullptr;
     std::vector<cudaEvent_t> fork_events;
     size_t fork_used = 0;
