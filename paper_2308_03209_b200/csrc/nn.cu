@@ -450,6 +450,63 @@ __global__ void softmax_ce_kernel(int64_t n, int32_t C, int32_t ld, const float*
     }
 }
 
+// Thread per row for C <= 4 * NV (the bench's 47 classes: 12 float4 per row):
+// the row lives in registers, max / sum-exp run sequentially in column order
+// exactly like nn.hpp:333-336, and the gradient row is written with 16-byte
+// stores (padding columns zeroed). Warp-per-row above handles wide C.
+template <int NV>
+__global__ void __launch_bounds__(128) softmax_ce_rows_kernel(int64_t n, int32_t C, int32_t ld,
+                                                              const float* __restrict__ logits,
+                                                              const int32_t* __restrict__ labels,
+                                                              const int32_t* __restrict__ rows,
+                                                              const double* __restrict__ w,
+                                                              const float* __restrict__ scale, float* __restrict__ G,
+                                                              double* __restrict__ row_loss) {
+    const int32_t nv = ld >> 2;  // float4 per (padded) row
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
+        float4* g = reinterpret_cast<float4*>(G + r * ld);
+        const double wr = w[r];
+        if (wr == 0.0) {  // nn.hpp:330
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+                if (j < nv) g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            row_loss[r] = 0.0;
+            continue;
+        }
+        const float4* zr = reinterpret_cast<const float4*>(logits + r * ld);
+        float z[4 * NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const float4 v = j < nv ? __ldg(zr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+            z[4 * j] = v.x;
+            z[4 * j + 1] = v.y;
+            z[4 * j + 2] = v.z;
+            z[4 * j + 3] = v.w;
+        }
+        const int32_t y = labels[rows ? rows[r] : r];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4 * NV; ++c)
+            if (c < C) mx = fmaxf(mx, z[c]);
+        float se = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4 * NV; ++c)
+            if (c < C) se += expf(z[c] - mx);
+        const float lse = mx + logf(se);
+        const float sc = scale[r];
+        float zy = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4 * NV; ++c) {
+            if (c == y) zy = z[c];
+            z[c] = c < C ? sc * (expf(z[c] - lse) - (c == y ? 1.f : 0.f)) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            if (j < nv) g[j] = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
+        row_loss[r] = wr * static_cast<double>(lse - zy);
+    }
+}
+
 __global__ void bce_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
                            const int32_t* __restrict__ labels,
                            const int32_t* __restrict__ rows, const double* __restrict__ w,
@@ -676,7 +733,20 @@ void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_
 void softmax_ce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
                 const float* scale, float* G, double* row_loss, cudaStream_t s) {
     if (n <= 0) return;
-    softmax_ce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
+    const bool vec = ld % 4 == 0 && reinterpret_cast<uintptr_t>(logits) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(G) % 16 == 0;
+    const unsigned grid = grid_for(n, 128);
+    if (vec && ld <= 16)
+        softmax_ce_rows_kernel<4><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
+    else if (vec && ld <= 32)
+        softmax_ce_rows_kernel<8><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
+    else if (vec && ld <= 48)
+        softmax_ce_rows_kernel<12><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
+    else if (vec && ld <= 64)
+        softmax_ce_rows_kernel<16><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
+    else
+        softmax_ce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G,
+                                                                  row_loss);
     SC_LAUNCH_CHECK();
     count_launch();
 }

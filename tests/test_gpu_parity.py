@@ -244,3 +244,23 @@ def test_trainer_errors(sc, O):
     gp = sc.partition_random(g, 2, 0)
     with pytest.raises(ValueError, match="features"):
         sc.CoFreeTrainer(g, gp, sc.TrainConfig(layers=1, hidden=[4]))
+
+
+@pytest.mark.parametrize("C", [13, 47, 61, 90])
+def test_many_classes(sc, O, C):
+    """Products-like widths: d = 100 features, C classes (softmax row kernel for C <= 64, warp
+    kernel above), 2 x 64 SAGE with DropEdge, 3 steps against the oracle."""
+    rng = np.random.default_rng(C)
+    n = 3000
+    og = O.graph_build(n, rng.integers(0, n, size=(30000, 2), dtype=np.int32))
+    lab = rng.integers(0, C, size=n).astype(np.int32)
+    f = rng.standard_normal((n, 100)).astype(np.float32)
+    f[np.arange(n), lab % 100] += 1.0
+    perm = rng.permutation(n)
+    tr = np.zeros(n, np.uint8)
+    va = np.zeros(n, np.uint8)
+    te = np.zeros(n, np.uint8)
+    tr[perm[:1800]], va[perm[1800:2400]], te[perm[2400:]] = 1, 1, 1
+    og.set_data(f, lab, C, tr, va, te)
+    worst, _, _ = run_traj(sc, O, og, "random", 4, 1, 100, steps=3, hidden=[64, 64], dropedge=True, seed=3)
+    assert_within(worst)
