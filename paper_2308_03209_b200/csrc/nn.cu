@@ -254,93 +254,124 @@ __global__ void inv_degree_kernel(int64_t n, const int64_t* __restrict__ off, co
         int32_t d = 0;
         if (!bits) {
             d = static_cast<int32_t>(b - a);
-        } else {
-            for (int64_t k = a; k < b; ++k) d += slot_kept(bits, k) ? 1 : 0;
+        } else {  // popcount of the row's slot range, word by word (hub rows span many words)
+            for (int64_t k = a; k < b;) {
+                const int64_t wbase = k & ~int64_t(31);
+                const int lo = static_cast<int>(k - wbase);
+                const int hi = static_cast<int>(min(b - wbase, int64_t(32)));
+                uint32_t word = __ldg(bits + (k >> 5));
+                word >>= lo;
+                if (hi - lo < 32) word &= (1u << (hi - lo)) - 1u;
+                d += __popc(word);
+                k = wbase + hi;
+            }
         }
         inv[v] = d > 0 ? 1.f / static_cast<float>(d) : 0.f;
     }
 }
 
+// Sum of the kept source rows over CSR slots [a, b) in slot order (the
+// reference's order); lanes own float4 column chunks, up to 4 row loads in flight.
+template <int NCH>
+__device__ __forceinline__ void gather_rows_sum(int64_t a, int64_t b, int lane, int32_t H, int32_t H4,
+                                                const int32_t* __restrict__ nbrs, const uint32_t* __restrict__ bits,
+                                                const float* __restrict__ src, float4 (&acc)[NCH]) {
+    for (int64_t base = a; base < b; base += 32) {
+        const int64_t k = base + lane;
+        const bool valid = k < b;
+        const int32_t nb = valid ? __ldg(nbrs + k) : 0;
+        const bool kept = valid && slot_kept(bits, k);
+        unsigned ballot = __ballot_sync(0xffffffffu, kept);
+        while (ballot) {
+            int32_t u[4];
+            int cnt = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (ballot) {
+                    const int sl = __ffs(ballot) - 1;
+                    ballot &= ballot - 1;
+                    u[q] = __shfl_sync(0xffffffffu, nb, sl);
+                    ++cnt;
+                } else {
+                    u[q] = -1;
+                }
+            }
+            float4 vals[4][NCH];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const int32_t ch = lane + 32 * c;
+                    if (q < cnt && ch < H4)
+                        vals[q][c] = __ldg(reinterpret_cast<const float4*>(src + int64_t(u[q]) * H) + ch);
+                    else
+                        vals[q][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < cnt)
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        acc[c].x += vals[q][c].x;
+                        acc[c].y += vals[q][c].y;
+                        acc[c].z += vals[q][c].z;
+                        acc[c].w += vals[q][c].w;
+                    }
+        }
+    }
+}
+
+// Output row v: forward mean = inv[v] * sum (nn.hpp:229); backward dz =
+// 1[msg > 0] * sum (nn.hpp:287-288). Returns max|out| of the lane's chunks.
+template <int NCH, bool kBwd>
+__device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int32_t H4, const float* __restrict__ inv,
+                                            const float* __restrict__ msg, float* __restrict__ out,
+                                            const float4 (&acc)[NCH]) {
+    float amx = 0.f;
+    const float s = kBwd ? 1.f : inv[v];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        const int32_t ch = lane + 32 * c;
+        if (ch >= H4) continue;
+        float4 r = acc[c];
+        if (!kBwd) {
+            r.x *= s;
+            r.y *= s;
+            r.z *= s;
+            r.w *= s;
+        } else {
+            const float4 mv = __ldg(reinterpret_cast<const float4*>(msg + v * H) + ch);
+            r.x = mv.x > 0.f ? r.x : 0.f;
+            r.y = mv.y > 0.f ? r.y : 0.f;
+            r.z = mv.z > 0.f ? r.z : 0.f;
+            r.w = mv.w > 0.f ? r.w : 0.f;
+        }
+        reinterpret_cast<float4*>(out + v * H)[ch] = r;
+        amx = fmaxf(amx, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
+    }
+    return amx;
+}
+
+// Warp per row over rows with at most `max_slots` CSR slots (heavier rows go
+// through the segmented path below).
 template <int NCH, bool kBwd>
 __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                    const int32_t* __restrict__ nbrs,
                                                    const uint32_t* __restrict__ bits, const float* __restrict__ inv,
                                                    const float* __restrict__ src, const float* __restrict__ msg,
-                                                   float* __restrict__ out, float* amax_out) {
+                                                   float* __restrict__ out, float* amax_out, int64_t max_slots) {
     float amx = 0.f;
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int32_t H4 = H >> 2;
     for (int64_t v = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += warps) {
+        const int64_t a = off[v], b = off[v + 1];
+        if (b - a > max_slots) continue;
         float4 acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int64_t a = off[v], b = off[v + 1];
-        for (int64_t base = a; base < b; base += 32) {
-            const int64_t k = base + lane;
-            const bool valid = k < b;
-            const int32_t nb = valid ? __ldg(nbrs + k) : 0;
-            const bool kept = valid && slot_kept(bits, k);
-            unsigned ballot = __ballot_sync(0xffffffffu, kept);
-            // Add kept neighbours in CSR order; up to 4 row loads in flight.
-            while (ballot) {
-                int32_t u[4];
-                int cnt = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (ballot) {
-                        const int sl = __ffs(ballot) - 1;
-                        ballot &= ballot - 1;
-                        u[q] = __shfl_sync(0xffffffffu, nb, sl);
-                        ++cnt;
-                    } else {
-                        u[q] = -1;
-                    }
-                }
-                float4 vals[4][NCH];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) {
-                        const int32_t ch = lane + 32 * c;
-                        if (q < cnt && ch < H4)
-                            vals[q][c] = __ldg(reinterpret_cast<const float4*>(src + int64_t(u[q]) * H) + ch);
-                        else
-                            vals[q][c] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (q < cnt)
-#pragma unroll
-                        for (int c = 0; c < NCH; ++c) {
-                            acc[c].x += vals[q][c].x;
-                            acc[c].y += vals[q][c].y;
-                            acc[c].z += vals[q][c].z;
-                            acc[c].w += vals[q][c].w;
-                        }
-            }
-        }
-        const float s = kBwd ? 1.f : inv[v];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int32_t ch = lane + 32 * c;
-            if (ch >= H4) continue;
-            float4 r = acc[c];
-            if (!kBwd) {
-                r.x *= s;
-                r.y *= s;
-                r.z *= s;
-                r.w *= s;
-            } else {
-                const float4 mv = __ldg(reinterpret_cast<const float4*>(msg + v * H) + ch);
-                r.x = mv.x > 0.f ? r.x : 0.f;
-                r.y = mv.y > 0.f ? r.y : 0.f;
-                r.z = mv.z > 0.f ? r.z : 0.f;
-                r.w = mv.w > 0.f ? r.w : 0.f;
-            }
-            reinterpret_cast<float4*>(out + v * H)[ch] = r;
-            amx = fmaxf(amx, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
-        }
+        gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
+        amx = fmaxf(amx, finish_row<NCH, kBwd>(v, lane, H, H4, inv, msg, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -348,7 +379,90 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
     }
 }
 
-// Scalar fallback for H % 4 != 0 (tests with odd widths): thread per (row, col).
+// Skewed degrees (hubs): a row with more than kHeavySlots slots is cut into
+// kSegSlots-slot segments, one warp each, whose partial sums are then added in
+// segment order by one warp per row (deterministic; the association differs
+// from the reference's single running sum only for these rows).
+template <int NCH>
+__global__ void __launch_bounds__(256) spmm_segments_kernel(int32_t nseg, int32_t H, const int64_t* __restrict__ off,
+                                                            const int32_t* __restrict__ nbrs,
+                                                            const uint32_t* __restrict__ bits,
+                                                            const int32_t* __restrict__ seg_row,
+                                                            const int64_t* __restrict__ seg_begin,
+                                                            const float* __restrict__ src, float* __restrict__ partial) {
+    const int lane = threadIdx.x & 31;
+    const int32_t H4 = H >> 2;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t sg = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); sg < nseg; sg += warps) {
+        const int64_t a = seg_begin[sg];
+        const int64_t b = min(a + int64_t(kSegSlots), off[seg_row[sg] + 1]);
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+            if (lane + 32 * c < H4) reinterpret_cast<float4*>(partial + sg * H)[lane + 32 * c] = acc[c];
+    }
+}
+
+template <int NCH, bool kBwd>
+__global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int32_t H,
+                                                                const int32_t* __restrict__ rows,
+                                                                const int32_t* __restrict__ seg_first,
+                                                                const float* __restrict__ partial,
+                                                                const float* __restrict__ inv,
+                                                                const float* __restrict__ msg, float* __restrict__ out,
+                                                                float* amax_out) {
+    const int lane = threadIdx.x & 31;
+    const int32_t H4 = H >> 2;
+    float amx = 0.f;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t h = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); h < nh; h += warps) {
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int32_t sg = seg_first[h]; sg < seg_first[h + 1]; ++sg)
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+                if (lane + 32 * c < H4) {
+                    const float4 p = reinterpret_cast<const float4*>(partial + int64_t(sg) * H)[lane + 32 * c];
+                    acc[c].x += p.x;
+                    acc[c].y += p.y;
+                    acc[c].z += p.z;
+                    acc[c].w += p.w;
+                }
+        amx = fmaxf(amx, finish_row<NCH, kBwd>(rows[h], lane, H, H4, inv, msg, out, acc));
+    }
+    if (amax_out) {
+        amx = warp_max_f(amx);
+        if (lane == 0) atomic_max_abs(amax_out, amx);
+    }
+}
+
+__global__ void heavy_count_kernel(int32_t nh, const int32_t* __restrict__ rows, const int64_t* __restrict__ off,
+                                   int32_t* __restrict__ nseg) {
+    for (int64_t h = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; h < nh; h += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t d = off[rows[h] + 1] - off[rows[h]];
+        nseg[h] = static_cast<int32_t>((d + kSegSlots - 1) / kSegSlots);
+    }
+}
+__global__ void heavy_fill_kernel(int32_t nh, const int32_t* __restrict__ rows, const int64_t* __restrict__ off,
+                                  const int32_t* __restrict__ seg_first, int32_t* __restrict__ seg_row,
+                                  int64_t* __restrict__ seg_begin) {
+    for (int64_t h = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; h < nh; h += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t v = rows[h];
+        for (int32_t sg = seg_first[h], j = 0; sg < seg_first[h + 1]; ++sg, ++j) {
+            seg_row[sg] = v;
+            seg_begin[sg] = off[v] + int64_t(j) * kSegSlots;
+        }
+    }
+}
+struct IsHeavy {
+    const int64_t* off;
+    __device__ bool operator()(int64_t v) const { return off[v + 1] - off[v] > kHeavySlots; }
+};
+
 template <bool kBwd>
 __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                    const int32_t* __restrict__ nbrs, const uint32_t* __restrict__ bits,
@@ -366,27 +480,42 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
     }
 }
 
-template <bool kBwd>
-void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
-                 const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out) {
-    if (n <= 0) return;
-    if (H % 4 != 0) {
-        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
-    } else {
-        const int64_t warps_needed = n;
-        const unsigned grid = grid_for(warps_needed * 32, 256, int64_t(num_sms()) * 16);
-        const int nch = (H / 4 + 31) / 32;
-        if (nch <= 1)
-            spmm_kernel<1, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
-        else if (nch == 2)
-            spmm_kernel<2, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
-        else if (nch <= 4)
-            spmm_kernel<4, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
-        else
-            spmm_kernel<8, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
-    }
+template <int NCH, bool kBwd>
+void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
+              const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv,
+              float* partial) {
+    const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 16);
+    const bool heavy = hv && hv->nh > 0;
+    spmm_kernel<NCH, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out,
+                                                heavy ? int64_t(kHeavySlots) : INT64_MAX);
     SC_LAUNCH_CHECK();
     count_launch();
+    if (!heavy) return;
+    spmm_segments_kernel<NCH><<<grid_for(int64_t(hv->nseg) * 32, 256, int64_t(num_sms()) * 16), 256, 0, s>>>(
+        hv->nseg, H, off, nbrs, bits, hv->seg_row.get(), hv->seg_begin.get(), src, partial);
+    SC_LAUNCH_CHECK();
+    spmm_heavy_finish_kernel<NCH, kBwd><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
+        hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, msg, out, amax_out);
+    SC_LAUNCH_CHECK();
+    count_launch(2);
+}
+
+template <bool kBwd>
+void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
+                 const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out,
+                 const HeavyRows* hv, float* partial) {
+    if (n <= 0) return;
+    if (H % 4 != 0) {  // scalar fallback: thread per output element (any H, any degree)
+        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
+        SC_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
+    const int nch = (H / 4 + 31) / 32;
+    if (nch <= 1) spmm_vec<1, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
+    else if (nch == 2) spmm_vec<2, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
+    else if (nch <= 4) spmm_vec<4, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
+    else spmm_vec<8, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
 }
 
 __global__ void mask_bits_kernel(int64_t nnz, const int32_t* __restrict__ eids, const uint8_t* __restrict__ mask,
@@ -705,12 +834,56 @@ void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* bits, float* 
     count_launch();
 }
 void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits, const float* inv,
-              const float* msg, float* mean, cudaStream_t s) {
-    spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, mean, s, nullptr);
+              const float* msg, float* mean, cudaStream_t s, const HeavyRows* hv, float* partial) {
+    spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, mean, s, nullptr, hv, partial);
 }
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
-              const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out) {
-    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s, amax_out);
+              const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out, const HeavyRows* hv,
+              float* partial) {
+    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s, amax_out, hv, partial);
+}
+
+void build_heavy_rows(sc_ctx* ctx, int64_t n, const int64_t* off, HeavyRows& hv) {
+    cudaStream_t s = ctx->stream;
+    hv.nh = hv.nseg = 0;
+    if (n <= 0) return;
+    DevBuf<int32_t> cnt(1);
+    hv.rows.alloc(1);
+    IsHeavy pred{off};
+    cub::CountingInputIterator<int64_t> it(0);
+    // pass 1: count heavy rows
+    cub::TransformInputIterator<bool, IsHeavy, cub::CountingInputIterator<int64_t>> flags(it, pred);
+    DevBuf<int32_t> idx(n);
+    cub::CountingInputIterator<int32_t> ids(0);
+    size_t tmp = 0;
+    SC_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, ids, flags, idx.get(), cnt.get(), n, s));
+    SC_CUDA(cub::DeviceSelect::Flagged(ctx->temp(tmp), tmp, ids, flags, idx.get(), cnt.get(), n, s));
+    int32_t nh = 0;
+    d2h(&nh, cnt.get(), 1, s);
+    SC_CUDA(cudaStreamSynchronize(s));
+    count_launch(1);
+    if (nh == 0) return;
+    hv.rows.alloc(nh);
+    SC_CUDA(cudaMemcpyAsync(hv.rows.get(), idx.get(), sizeof(int32_t) * nh, cudaMemcpyDeviceToDevice, s));
+    hv.seg_first.alloc(nh + 1);
+    DevBuf<int32_t> nseg(nh + 1);
+    heavy_count_kernel<<<grid_for(nh, 256), 256, 0, s>>>(nh, hv.rows.get(), off, nseg.get());
+    SC_LAUNCH_CHECK();
+    SC_CUDA(cudaMemsetAsync(nseg.get() + nh, 0, sizeof(int32_t), s));
+    tmp = 0;
+    SC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nseg.get(), hv.seg_first.get(), nh + 1, s));
+    SC_CUDA(cub::DeviceScan::ExclusiveSum(ctx->temp(tmp), tmp, nseg.get(), hv.seg_first.get(), nh + 1, s));
+    int32_t total = 0;
+    d2h(&total, hv.seg_first.get() + nh, 1, s);
+    SC_CUDA(cudaStreamSynchronize(s));
+    hv.seg_row.alloc(total);
+    hv.seg_begin.alloc(total);
+    heavy_fill_kernel<<<grid_for(nh, 256), 256, 0, s>>>(nh, hv.rows.get(), off, hv.seg_first.get(), hv.seg_row.get(),
+                                                        hv.seg_begin.get());
+    SC_LAUNCH_CHECK();
+    count_launch(3);
+    hv.nh = nh;
+    hv.nseg = total;
 }
 void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s) {
     if (n <= 0) return;

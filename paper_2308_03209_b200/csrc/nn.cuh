@@ -5,7 +5,23 @@
 
 #include <cstdint>
 
+#include "internal.hpp"
+
 namespace sc {
+
+// Aggregation rows with more than kHeavySlots CSR slots (skewed degrees) are
+// split into kSegSlots-slot segments so no single warp walks a hub row.
+constexpr int64_t kHeavySlots = 4096;
+constexpr int64_t kSegSlots = 1024;
+struct HeavyRows {
+    DevBuf<int32_t> rows;       // nh heavy rows, ascending
+    DevBuf<int32_t> seg_first;  // nh + 1: segments of row h are [seg_first[h], seg_first[h+1])
+    DevBuf<int32_t> seg_row;    // nseg
+    DevBuf<int64_t> seg_begin;  // nseg: first CSR slot of the segment
+    int32_t nh = 0, nseg = 0;
+};
+// Heavy-row table of a CSR (offsets on the device).
+void build_heavy_rows(sc_ctx* ctx, int64_t n, const int64_t* offsets, HeavyRows& hv);
 
 // A operand of a row-major GEMM: A[r][k] = ptr[(rows ? rows[r] : r) * ld + k].
 struct MatA {
@@ -49,12 +65,16 @@ int64_t gemm_tn_workspace_floats(int32_t N1, int32_t N2);
 
 // Per-node inverse masked degree (nn.hpp:174-188, 209-215): inv = d > 0 ? 1/d : 0.
 void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* mask_bits, float* inv, cudaStream_t s);
-// mean[v] = inv[v] * sum_{k in CSR(v), kept} msg[nbr_k]   (nn.hpp:222-230)
+// mean[v] = inv[v] * sum_{k in CSR(v), kept} msg[nbr_k]   (nn.hpp:222-230).
+// hv (optional): the CSR's heavy rows, aggregated through `partial`
+// (hv->nseg x H floats).
 void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
-              const float* inv, const float* msg, float* mean, cudaStream_t s);
+              const float* inv, const float* msg, float* mean, cudaStream_t s, const HeavyRows* hv = nullptr,
+              float* partial = nullptr);
 // dz[u] = 1[msg[u] > 0] * sum_{v in CSR(u), kept} dmean_s[v]   (nn.hpp:277-288, pull form)
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
-              const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out = nullptr);
+              const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out = nullptr,
+              const HeavyRows* hv = nullptr, float* partial = nullptr);
 // CSR-slot bitmap of a local-edge-indexed byte mask: bit k = mask[eids[k]].
 void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_t* bits, cudaStream_t s);
 

@@ -179,6 +179,7 @@ void trainer_init(sc_trainer* t) {
         SC_CUDA(cudaMemsetAsync(st.g_amax.get(), 0, sizeof(float), s));
         absmax(st.n, st.scale.get(), st.g_amax.get(), s);
         st.logits.alloc(std::max<int64_t>(st.n * t->Cp, 1));
+        build_heavy_rows(t->ctx, st.n, pd.offsets.get(), st.heavy);
         st.x0.alloc(std::max<int64_t>(st.n * t->d, 1));
         if (t->use_dropedge) {
             st.words = (st.nnz + 31) / 32;
@@ -200,6 +201,11 @@ void trainer_init(sc_trainer* t) {
     t->red_partial.alloc(1024);
     t->amax.alloc(sc_trainer::kSlotBase + 2 * std::max(t->L, 1));
     ensure_rows(t, n_max);
+    int64_t max_seg = 0;
+    for (int i : t->local) max_seg = std::max<int64_t>(max_seg, t->ps[i].heavy.nseg);
+    int32_t maxH = 1;
+    for (auto& lo : t->lay) maxH = std::max(maxH, lo.H);
+    if (max_seg) t->heavy_ws.alloc(max_seg * maxH);
     int32_t maxN1 = t->C, maxN2 = t->E;
     for (auto& lo : t->lay) {
         maxN1 = std::max(maxN1, lo.H);
@@ -278,6 +284,7 @@ struct Rows {
     int64_t kept;          // CSR slots kept by the selected DropEdge mask
     const float* g_amax;   // bound on max|dloss/dlogits| (= max loss scale)
     const float* x0;       // layer-0 input rows (contiguous n x d; the partition's gathered features)
+    const HeavyRows* hv;   // hub rows (segmented aggregation)
 };
 
 // Algorithmic HBM bytes of one aggregation launch: offsets,
@@ -309,7 +316,8 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
         P.end(s);
         // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
         P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
-        spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->inv.get(), t->MSG[l].get(), t->MEAN[l].get(), s);
+        spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->inv.get(), t->MSG[l].get(), t->MEAN[l].get(), s, R.hv,
+                 t->heavy_ws.get());
         P.end(s);
         // h' = mean U_L^T + h U_R^T   (nn.hpp:233-234)
         const MatB uL{t->theta.get() + lo.U, lo.H + lo.in, false};
@@ -391,7 +399,8 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
         SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
         P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
-        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s, dz_amax);
+        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s, dz_amax, R.hv,
+                 t->heavy_ws.get());
         P.end(s);
         // dW = dz^T h_in   (:289)
         P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s);
@@ -436,7 +445,7 @@ void run_partition(sc_trainer* t, int i, int epoch) {
         st.x0_version = t->g->feat_version;
     }
     const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get(),
-                 st.x0.get()};
+                 st.x0.get(), &st.heavy};
     SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
     forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
@@ -518,8 +527,15 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
     sc_graph* g = t->g;
     ensure_rows(t, g->n);
     if (t->eval_logits.size() < size_t(g->n) * t->Cp) t->eval_logits.alloc(size_t(g->n) * t->Cp);
+    if (!t->eval_heavy_built) {
+        build_heavy_rows(t->ctx, g->n, g->offsets.get(), t->eval_heavy);
+        t->eval_heavy_built = true;
+        int32_t maxH = 1;
+        for (auto& lo : t->lay) maxH = std::max(maxH, lo.H);
+        if (size_t(t->eval_heavy.nseg) * maxH > t->heavy_ws.size()) t->heavy_ws.alloc(size_t(t->eval_heavy.nseg) * maxH);
+    }
     const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr,
-                 g->features.get()};
+                 g->features.get(), &t->eval_heavy};
     const bool was = t->prof.enabled;
     t->prof.enabled = false;
     forward(t, R, t->eval_logits.get());

@@ -29,6 +29,7 @@ struct PartState {
     DevBuf<float> g_amax;  // bound on max|dloss/dlogits| (tensor-core operand scale)
     DevBuf<float> x0;      // layer-0 input: this partition's feature rows (n x d), gathered once per
     uint64_t x0_version = 0;  // feature version, so the GEMMs stream contiguous rows
+    HeavyRows heavy;          // hub rows of the local CSR (segmented aggregation)
     int chosen = -1;
 };
 
@@ -97,6 +98,9 @@ struct sc_trainer {
     int64_t rows_cap = 0;
     std::vector<sc::DevBuf<float>> X, MSG, MEAN;
     sc::DevBuf<float> inv, G, dh, dh2, dmean, dz, eval_logits, ws, ws_side;
+    sc::DevBuf<float> heavy_ws;   // segment partial sums of the heavy-row aggregation
+    sc::HeavyRows eval_heavy;     // heavy rows of the full graph (evaluate_splits)
+    bool eval_heavy_built = false;
     // Backward runs the weight-gradient GEMMs that only need dh (head: G^T emb;
     // update: dh^T [mean | h]) on a high-priority side stream, concurrently with
     // the dgrad -> transposed aggregation -> dW chain on the main stream.

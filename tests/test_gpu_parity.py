@@ -264,3 +264,26 @@ def test_many_classes(sc, O, C):
     og.set_data(f, lab, C, tr, va, te)
     worst, _, _ = run_traj(sc, O, og, "random", 4, 1, 100, steps=3, hidden=[64, 64], dropedge=True, seed=3)
     assert_within(worst)
+
+
+def test_skewed_degree_hubs(sc, O):
+    """Hub rows above kHeavySlots (4096 CSR slots) take the segmented aggregation path
+    (forward, transposed backward, full-graph eval); trajectories stay within tolerance."""
+    rng = np.random.default_rng(5)
+    n = 20000
+    hub = np.stack([np.zeros(14000, np.int64), rng.choice(np.arange(1, n), 14000, replace=False)], 1)
+    hub2 = np.stack([np.full(9000, 7), rng.choice(np.arange(8, n), 9000, replace=False)], 1)
+    e = np.concatenate([hub, hub2, rng.integers(0, n, size=(60000, 2))]).astype(np.int32)
+    og = O.graph_build(n, e)
+    C = 6
+    lab = rng.integers(0, C, size=n).astype(np.int32)
+    f = rng.standard_normal((n, 16)).astype(np.float32)
+    f[np.arange(n), lab] += 1.0
+    tr = (rng.random(n) < 0.6).astype(np.uint8)
+    va = ((1 - tr) * (rng.random(n) < 0.5)).astype(np.uint8)
+    te = (1 - tr - va).astype(np.uint8)
+    og.set_data(f, lab, C, tr, va, te)
+    for de in (False, True):
+        worst, t, to = run_traj(sc, O, og, "random", 2, 1, 16, steps=3, hidden=[32, 32], dropedge=de, seed=4)
+        assert_within(worst)
+        np.testing.assert_allclose(t.evaluate(), to.eval(), atol=0.01)
