@@ -44,6 +44,12 @@ CONFIGS = {
     # configs[1]: Reddit-shaped; 114.6M directed = 57.3M undirected edges; SAGE (no GCN in the reference)
     "reddit": dict(workload="Reddit-shaped synthetic (BASELINE configs[1])", nodes=232_965, pairs=57_400_000,
                    feats=602, classes=41, layers=2, hidden=256, parts=8, dropedge=False, k=10, ratio=0.5, lr=1e-2),
+    # configs[3]: power-law R-MAT (a,b,c,d) = (0.57,0.19,0.19,0.05), 20M nodes / 1B edge samples, 128 feats,
+    # 3 x 256 SAGE (47 classes: the survey's choice). Full size needs > 180 GB at N = 1 (activations of
+    # ~7.5M-row partitions plus the 1B-edge graph); --scale 0.25 (5M / 250M) is the default single-GPU size.
+    "rmat": dict(workload="power-law R-MAT synthetic (BASELINE configs[3])", nodes=20_000_000, pairs=1_000_000_000,
+                 feats=128, classes=47, layers=3, hidden=256, parts=8, dropedge=False, k=10, ratio=0.5, lr=3e-3,
+                 rmat=(0.57, 0.19, 0.19, 0.05), default_scale=0.25),
     # configs[0]: ER 10k / 200k, 64 feats, 2 layers (reference default hidden 32), p = 4
     "er10k": dict(workload="Erdos-Renyi 10k/200k (BASELINE configs[0])", nodes=10_000, pairs=200_000, feats=64,
                   classes=4, layers=2, hidden=32, parts=4, dropedge=False, k=10, ratio=0.5, lr=1e-2),
@@ -62,6 +68,9 @@ def synth_host(cfg, seed=0, scale=1.0):
     rng = np.random.default_rng(seed)
     n = max(int(cfg["nodes"] * scale), 16)
     m = max(int(cfg["pairs"] * scale), 16)
+    if "rmat" in cfg:
+        feats, labels, tr, va, te = synth_data(n, cfg, seed)
+        return n, rmat_edges(n, m, cfg["rmat"], seed).numpy(), feats, labels, tr, va, te
     uv = rng.integers(0, n, size=(m, 2), dtype=np.int32)
     labels = rng.integers(0, cfg["classes"], size=n, dtype=np.int32)
     feats = rng.standard_normal((n, cfg["feats"]), dtype=np.float32)
@@ -75,6 +84,47 @@ def synth_host(cfg, seed=0, scale=1.0):
     va[perm[n_tr:n_tr + n_va]] = 1
     te[perm[n_tr + n_va:]] = 1
     return n, uv, feats, labels, tr, va, te
+
+
+def rmat_edges(n, m, abcd, seed=0, device=None):
+    """R-MAT edge samples (Chakrabarti et al.): each endpoint bit picks a quadrant with probabilities
+    (a, b, c, d) over 2^L >= n ids, ids folded into [0, n) and randomly relabelled (hubs spread out).
+    O(m log n); generated on the GPU with torch when `device` is given (input synthesis only)."""
+    import torch
+    a, b, c, _ = abcd
+    L = max(1, int(math.ceil(math.log2(n))))
+    gen = torch.Generator(device=device or "cpu").manual_seed(seed)
+    perm = torch.randperm(n, generator=gen, device=device or "cpu").to(torch.int64)
+    out = torch.empty((m, 2), dtype=torch.int32, device=device or "cpu")
+    chunk = 1 << 25
+    for s0 in range(0, m, chunk):
+        k = min(chunk, m - s0)
+        u = torch.zeros(k, dtype=torch.int64, device=device or "cpu")
+        v = torch.zeros_like(u)
+        for _ in range(L):
+            r = torch.rand(k, generator=gen, device=device or "cpu")
+            ub = r >= a + b                              # quadrants c, d: row bit 1
+            vb = ((r >= a) & (r < a + b)) | (r >= a + b + c)  # quadrants b, d: column bit 1
+            u = (u << 1) | ub.to(torch.int64)
+            v = (v << 1) | vb.to(torch.int64)
+        out[s0:s0 + k, 0] = perm[u % n].to(torch.int32)
+        out[s0:s0 + k, 1] = perm[v % n].to(torch.int32)
+    return out
+
+
+def synth_data(n, cfg, seed=0):
+    """labels uniform, features one-hot(label) + N(0, 1), 60/20/20 split (synth.cpp:91-97 convention)."""
+    rng = np.random.default_rng(seed + 1)
+    labels = rng.integers(0, cfg["classes"], size=n, dtype=np.int32)
+    feats = rng.standard_normal((n, cfg["feats"]), dtype=np.float32)
+    feats[np.arange(n), labels % cfg["feats"]] += 1.0
+    perm = rng.permutation(n)
+    tr, va, te = (np.zeros(n, np.uint8) for _ in range(3))
+    n_tr, n_va = n * 6 // 10, n * 2 // 10
+    tr[perm[:n_tr]] = 1
+    va[perm[n_tr:n_tr + n_va]] = 1
+    te[perm[n_tr + n_va:]] = 1
+    return feats, labels, tr, va, te
 
 
 def kept_entries(sizes_m, cfg):
@@ -220,12 +270,26 @@ def run_gpu_arm(args, cfg):
 
     ctx = sc.Context(local)
     t_setup = time.perf_counter()
-    # identical seeded synthetic inputs on every rank (generated on the host once per rank)
-    n, uv, feats, labels, tr, va, te = synth_host(cfg, seed=0)
-    g, rep = sc.build_graph(n, uv, ctx)
+    # identical seeded synthetic inputs on every rank (generated once per rank)
+    scale = args.scale if args.scale is not None else cfg.get("default_scale", 1.0)
+    if "rmat" in cfg:  # R-MAT edges are sampled on the device and handed over as a device edge list
+        n = max(int(cfg["nodes"] * scale), 16)
+        uv_dev = rmat_edges(n, max(int(cfg["pairs"] * scale), 16), cfg["rmat"], seed=0, device=f"cuda:{local}")
+        torch.cuda.synchronize()  # generated on torch's stream; the library reads it on its own
+        feats, labels, tr, va, te = synth_data(n, cfg, 0)
+        g, rep = sc.build_graph_device(n, uv_dev.data_ptr(), uv_dev.shape[0], ctx)
+        del uv_dev
+        torch.cuda.empty_cache()
+    else:
+        n, uv, feats, labels, tr, va, te = synth_host(cfg, seed=0, scale=scale)
+        g, rep = sc.build_graph(n, uv, ctx)
     g.set_data(feats, labels, cfg["classes"], tr, va, te)
     part = sc.partition_random(g, cfg["parts"], 0)
     sizes_m = [part.part_sizes(i)[1] for i in range(cfg["parts"])]
+    deg = g.degrees()
+    degree_stats = {"max": int(deg.max()), "mean": float(deg.mean()), "p99": float(np.percentile(deg, 99)),
+                    "isolated": int((deg == 0).sum())}
+    del deg
     kept = kept_entries(sizes_m, cfg)
     nccl_id = None
     if world > 1:
@@ -314,10 +378,12 @@ def run_gpu_arm(args, cfg):
         "metric": "aggregated_edges_per_s", "value": value, "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "nodes": g.num_nodes, "edges": g.num_edges(),
+        "config": {"workload": cfg["workload"] + (f" [scale {scale}]" if scale != 1.0 else ""),
+                   "nodes": g.num_nodes, "edges": g.num_edges(),
                    "feats": cfg["feats"], "classes": cfg["classes"], "layers": cfg["layers"],
                    "hidden": cfg["hidden"], "partitions": cfg["parts"], "partitioner": "random vertex cut",
                    "dropedge": f"p={cfg['ratio']} K={cfg['k']}" if cfg["dropedge"] else None,
+                   "degrees": degree_stats, "rf": sc.replication_stats(part, g).rf,
                    "kept_csr_entries_per_epoch": kept, "parallelism": f"dp{world} over {cfg['parts']} fixed partitions",
                    "gemm": args.gemm, "l2": "inputs > L2 (each activation matrix is n_i x 256 fp32 = 2.5 GB)"},
         "epoch_ms": ms_step,
@@ -351,6 +417,8 @@ def main():
     ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
     ap.add_argument("--gemm", default="auto", choices=["auto", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", type=float, default=None,
+                    help="scale nodes and edges of the config (default 1; rmat: 0.25, see CONFIGS)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -256,6 +256,11 @@ class Graph:
         _check(_lib.sc_graph_copy_csr(self.h, _ptr(off), _ptr(nb), _ptr(ei), _ptr(dg)))
         return off, nb, ei, dg
 
+    def degrees(self) -> np.ndarray:
+        dg = np.zeros(self.num_nodes, np.int32)
+        _check(_lib.sc_graph_copy_csr(self.h, None, None, None, _ptr(dg)))
+        return dg
+
     def set_data(self, features, labels, num_classes, train_mask, val_mask, test_mask):
         f = np.ascontiguousarray(features, np.float32)
         if f.ndim != 2 or f.shape[0] != self.num_nodes:
