@@ -340,15 +340,20 @@ def run_gpu_arm(args, cfg):
     ms_step = max_over_ranks(ms / args.steps)
     value = cfg["layers"] * kept / (ms_step / 1e3)
 
-    # ---- e2e: the public API with host buffers: per step H2D of the feature matrix from pinned
-    # host memory (the step's input), the epoch, and the D2H of loss / grad-norm.
+    # ---- e2e: the public API with host buffers: every step's input (the feature matrix, from pinned
+    # host memory) is copied host -> device inside the timed region and the loss / grad-norm read back.
+    # Step k+1's copy (and its partitions' layer-0 row gathers) is staged on the library's copy
+    # stream while step k computes; step 0's copy is exposed.
     pinned = torch.from_numpy(feats).pin_memory()
     barrier()
     ctx.sync()
     ctx.timer_start()
-    for _ in range(args.steps):
-        g.set_features(None, host_ptr=pinned.data_ptr())
-        trainer.step(epoch)
+    trainer.stage_features(host_ptr=pinned.data_ptr())
+    for k in range(args.steps):
+        trainer.step_async(epoch)  # commits the staged features
+        if k + 1 < args.steps:
+            trainer.stage_features(host_ptr=pinned.data_ptr())
+        trainer.last()
         epoch += 1
     e2e_ms = max_over_ranks(ctx.timer_stop() / args.steps)
     e2e_value = cfg["layers"] * kept / (e2e_ms / 1e3)

@@ -169,6 +169,7 @@ sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, con
 sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_device) {
     return guard([&] {
         REQUIRE_ARG(g && features && g->dim > 0, "sc_graph_set_features: graph has no feature buffer");
+        REQUIRE_ARG(!g->staged, "sc_graph_set_features: features are staged for the next step");
         set_device(g->ctx);
         SC_CUDA(cudaMemcpyAsync(g->features.get(), features, sizeof(float) * size_t(g->n) * g->dim,
                                 is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->ctx->stream));
@@ -209,6 +210,14 @@ sc_status sc_graph_copy_csr(sc_graph* g, int64_t* offsets, int32_t* nbrs, int32_
         if (degrees) d2h(degrees, g->degrees.get(), g->n, s);
         SC_CUDA(cudaStreamSynchronize(s));
     });
+}
+sc_graph::~sc_graph() {
+    if (copy_stream) {
+        cudaStreamSynchronize(copy_stream);
+        cudaStreamDestroy(copy_stream);
+    }
+    if (staged_ev) cudaEventDestroy(staged_ev);
+    if (released_ev) cudaEventDestroy(released_ev);
 }
 sc_status sc_graph_destroy(sc_graph* g) {
     return guard([&] {
@@ -490,6 +499,13 @@ sc_status sc_trainer_step(sc_trainer* t, int32_t epoch, double* loss, double* gn
         set_device(t->ctx);
         trainer_step_async(t, epoch);
         trainer_finish(t, loss, gnorm);
+    });
+}
+sc_status sc_trainer_stage_features(sc_trainer* t, const float* features, int32_t is_device) {
+    return guard([&] {
+        REQUIRE_ARG(t && features, "sc_trainer_stage_features: null argument");
+        set_device(t->ctx);
+        trainer_stage_features(t, features, is_device != 0);
     });
 }
 sc_status sc_trainer_step_async(sc_trainer* t, int32_t epoch) {

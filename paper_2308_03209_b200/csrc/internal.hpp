@@ -100,6 +100,15 @@ struct sc_graph {
     sc::DevBuf<int32_t> labels;        // n
     sc::DevBuf<uint8_t> train, val, test;  // n
     int64_t train_count = 0;
+    // Staged next features (sc_trainer_stage_features): H2D on copy_stream into
+    // features_next while the current step runs; committed (buffers swapped)
+    // at the start of the next step. released: recorded on the compute stream
+    // at each commit, after the last use of the buffer that becomes _next.
+    sc::DevBuf<float> features_next, feat_amax_next;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t staged_ev = nullptr, released_ev = nullptr;
+    bool staged = false, released_recorded = false;
+    ~sc_graph();
 };
 
 // One PartSubgraph (partition.hpp:14-31), device resident.

@@ -461,8 +461,54 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     backward(t, R, i);
 }
 
+void trainer_stage_features(sc_trainer* t, const float* features, bool is_device) {
+    sc_graph* g = t->g;
+    if (g->dim == 0) throw std::invalid_argument("stage_features: graph has no feature buffer");
+    if (g->staged) throw std::invalid_argument("stage_features: features already staged (step first)");
+    if (!g->copy_stream) {
+        SC_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+        SC_CUDA(cudaEventCreateWithFlags(&g->staged_ev, cudaEventDisableTiming));
+        SC_CUDA(cudaEventCreateWithFlags(&g->released_ev, cudaEventDisableTiming));
+    }
+    cudaStream_t c = g->copy_stream;
+    const int64_t nd = int64_t(g->n) * g->dim;
+    g->features_next.ensure(std::max<int64_t>(nd, 1));
+    g->feat_amax_next.ensure(1);
+    if (g->released_recorded) SC_CUDA(cudaStreamWaitEvent(c, g->released_ev, 0));  // old buffer no longer read
+    SC_CUDA(cudaMemcpyAsync(g->features_next.get(), features, sizeof(float) * nd,
+                            is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c));
+    SC_CUDA(cudaMemsetAsync(g->feat_amax_next.get(), 0, sizeof(float), c));
+    absmax(nd, g->features_next.get(), g->feat_amax_next.get(), c);
+    for (int i : t->local) {  // the partitions' contiguous layer-0 rows (train_cofree :225-227)
+        PartState& st = t->ps[i];
+        st.x0_next.ensure(std::max<int64_t>(st.n * t->d, 1));
+        gather_rows(st.n, t->d, t->vc->parts[i].nodes.get(), g->features_next.get(), st.x0_next.get(), c);
+    }
+    SC_CUDA(cudaEventRecord(g->staged_ev, c));
+    g->staged = true;
+}
+
+void commit_staged_features(sc_trainer* t) {
+    sc_graph* g = t->g;
+    if (!g->staged) return;
+    cudaStream_t s = t->ctx->stream;
+    SC_CUDA(cudaStreamWaitEvent(s, g->staged_ev, 0));
+    std::swap(g->features, g->features_next);
+    std::swap(g->feat_amax, g->feat_amax_next);
+    ++g->feat_version;
+    for (int i : t->local) {
+        PartState& st = t->ps[i];
+        std::swap(st.x0, st.x0_next);
+        st.x0_version = g->feat_version;
+    }
+    SC_CUDA(cudaEventRecord(g->released_ev, s));  // everything that read the old buffers is enqueued before this
+    g->released_recorded = true;
+    g->staged = false;
+}
+
 void trainer_step_async(sc_trainer* t, int epoch) {
     cudaStream_t s = t->ctx->stream;
+    commit_staged_features(t);
     t->prof.records.clear();
     t->prof.used = 0;
     if (t->world > 1 && !t->comm)

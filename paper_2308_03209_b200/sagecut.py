@@ -102,6 +102,7 @@ _sig("sc_nccl_unique_id", [_vp])
 _sig("sc_trainer_init_comm", [_vp, _vp])
 _sig("sc_trainer_step", [_vp, _i32, C.POINTER(_f64), C.POINTER(_f64)])
 _sig("sc_trainer_step_async", [_vp, _i32])
+_sig("sc_trainer_stage_features", [_vp, _vp, _i32])
 _sig("sc_trainer_last", [_vp, C.POINTER(_f64), C.POINTER(_f64)])
 _sig("sc_trainer_param_count", [_vp, C.POINTER(_i64)])
 for _n in ("sc_trainer_get_params", "sc_trainer_set_params", "sc_trainer_get_grads"):
@@ -627,6 +628,19 @@ class CoFreeTrainer:
         loss, gn = _f64(), _f64()
         _check(_lib.sc_trainer_step(self.h, epoch, C.byref(loss), C.byref(gn)), "step")
         return loss.value, gn.value
+
+    def stage_features(self, features=None, host_ptr: Optional[int] = None, device_ptr: Optional[int] = None):
+        """Copy the next step's features (n x d) while the current step runs; the next step() uses them."""
+        if device_ptr is not None:
+            _check(_lib.sc_trainer_stage_features(self.h, _vp(device_ptr), 1), "stage_features")
+        elif host_ptr is not None:
+            _check(_lib.sc_trainer_stage_features(self.h, _vp(host_ptr), 0), "stage_features")
+        else:
+            f = np.ascontiguousarray(features, np.float32)
+            if f.shape != (self.g.num_nodes, self.g.dim):
+                raise ValueError("stage_features: features must be num_nodes x d")
+            self._staged = f  # keep the host buffer alive until the copy has run
+            _check(_lib.sc_trainer_stage_features(self.h, _ptr(f), 0), "stage_features")
 
     def step_async(self, epoch: int):
         _check(_lib.sc_trainer_step_async(self.h, epoch), "step")

@@ -292,3 +292,32 @@ def test_skewed_degree_hubs(sc, O):
         worst, t, to = run_traj(sc, O, og, "random", 2, 1, 16, steps=3, hidden=[32, 32], dropedge=de, seed=4)
         assert_within(worst)
         np.testing.assert_allclose(t.evaluate(), to.eval(), atol=0.01)
+
+
+def test_staged_features_match_set_features(sc, O):
+    """sc_trainer_stage_features (copy + x0 gathers overlapped with the running step) gives bitwise
+    the same trajectory as replacing the features synchronously before each step."""
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    rng = np.random.default_rng(0)
+    feats = [og.features(8).astype(np.float32) + rng.standard_normal((og.n, 8)).astype(np.float32) * 0.1 * k
+             for k in range(4)]
+    out = []
+    for staged in (False, True):
+        g = gpu_graph(sc, og, 8)
+        t = sc.CoFreeTrainer(g, sc.partition_random(g, 4, 3),
+                             sc.TrainConfig(layers=2, hidden=[16], use_dropedge=True, seed=1))
+        losses = []
+        if staged:
+            t.stage_features(feats[0])
+        for e in range(4):
+            if staged:
+                t.step_async(e)
+                if e + 1 < 4:
+                    t.stage_features(feats[e + 1])
+                losses.append(t.last())
+            else:
+                g.set_features(feats[e])
+                losses.append(t.step(e))
+        out.append((losses, t.params()))
+    assert out[0][0] == out[1][0]
+    np.testing.assert_array_equal(out[0][1], out[1][1])
