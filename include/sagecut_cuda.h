@@ -165,10 +165,9 @@ sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
  * one Adam step. Outputs are host scalars (the only D2H of the step). */
 sc_status sc_trainer_step(sc_trainer* t, int32_t epoch, double* loss, double* grad_norm);
 /* Stage the NEXT step's n x d features (host: pinned for a true async copy;
- * or device): the copy, its |max| and the local partitions' layer-0 row
- * gathers run on a copy stream while the current step computes, and the next
- * sc_trainer_step / _step_async commits them (the features the reference's
- * PartitionInputs gather, trainer.hpp:225-227). One staging per step. */
+ * or device): the copy runs on a copy stream while the current step computes,
+ * and the next sc_trainer_step / _step_async commits them (the features the
+ * reference's PartitionInputs gather, trainer.hpp:225-227). One staging per step. */
 sc_status sc_trainer_stage_features(sc_trainer* t, const float* features, int32_t is_device);
 /* Same, but enqueue only (no host sync); results via sc_trainer_last(). */
 sc_status sc_trainer_step_async(sc_trainer* t, int32_t epoch);

@@ -104,7 +104,7 @@ struct sc_graph {
     // features_next while the current step runs; committed (buffers swapped)
     // at the start of the next step. released: recorded on the compute stream
     // at each commit, after the last use of the buffer that becomes _next.
-    sc::DevBuf<float> features_next, feat_amax_next;
+    sc::DevBuf<float> features_next;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t staged_ev = nullptr, released_ev = nullptr;
     bool staged = false, released_recorded = false;

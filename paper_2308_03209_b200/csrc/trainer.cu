@@ -473,17 +473,11 @@ void trainer_stage_features(sc_trainer* t, const float* features, bool is_device
     cudaStream_t c = g->copy_stream;
     const int64_t nd = int64_t(g->n) * g->dim;
     g->features_next.ensure(std::max<int64_t>(nd, 1));
-    g->feat_amax_next.ensure(1);
     if (g->released_recorded) SC_CUDA(cudaStreamWaitEvent(c, g->released_ev, 0));  // old buffer no longer read
+    // Only the copy engine works here: kernels on this stream would take SM slots from the
+    // step's persistent GEMMs. |max| and the x0 gathers run on the compute stream at commit.
     SC_CUDA(cudaMemcpyAsync(g->features_next.get(), features, sizeof(float) * nd,
                             is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c));
-    SC_CUDA(cudaMemsetAsync(g->feat_amax_next.get(), 0, sizeof(float), c));
-    absmax(nd, g->features_next.get(), g->feat_amax_next.get(), c);
-    for (int i : t->local) {  // the partitions' contiguous layer-0 rows (train_cofree :225-227)
-        PartState& st = t->ps[i];
-        st.x0_next.ensure(std::max<int64_t>(st.n * t->d, 1));
-        gather_rows(st.n, t->d, t->vc->parts[i].nodes.get(), g->features_next.get(), st.x0_next.get(), c);
-    }
     SC_CUDA(cudaEventRecord(g->staged_ev, c));
     g->staged = true;
 }
@@ -493,15 +487,11 @@ void commit_staged_features(sc_trainer* t) {
     if (!g->staged) return;
     cudaStream_t s = t->ctx->stream;
     SC_CUDA(cudaStreamWaitEvent(s, g->staged_ev, 0));
+    SC_CUDA(cudaEventRecord(g->released_ev, s));  // everything that read the old buffer is enqueued before this
     std::swap(g->features, g->features_next);
-    std::swap(g->feat_amax, g->feat_amax_next);
-    ++g->feat_version;
-    for (int i : t->local) {
-        PartState& st = t->ps[i];
-        std::swap(st.x0, st.x0_next);
-        st.x0_version = g->feat_version;
-    }
-    SC_CUDA(cudaEventRecord(g->released_ev, s));  // everything that read the old buffers is enqueued before this
+    ++g->feat_version;  // partitions re-gather their x0 rows lazily (run_partition)
+    SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), s));
+    absmax(int64_t(g->n) * g->dim, g->features.get(), g->feat_amax.get(), s);
     g->released_recorded = true;
     g->staged = false;
 }

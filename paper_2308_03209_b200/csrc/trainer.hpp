@@ -30,7 +30,6 @@ struct PartState {
     DevBuf<float> x0;      // layer-0 input: this partition's feature rows (n x d), gathered once per
     uint64_t x0_version = 0;  // feature version, so the GEMMs stream contiguous rows
     HeavyRows heavy;          // hub rows of the local CSR (segmented aggregation)
-    DevBuf<float> x0_next;    // x0 of the staged features (gathered on the copy stream)
     int chosen = -1;
 };
 
@@ -146,9 +145,9 @@ void trainer_step_async(sc_trainer* t, int epoch);
 void trainer_finish(sc_trainer* t, double* loss, double* gnorm);
 void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te);
 void trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
-// Stage the next step's features (host or device source): copy + |max| + the
-// local partitions' x0 gathers run on the graph's copy stream, overlapping the
-// current step; the next trainer_step_async commits them.
+// Stage the next step's features (host or device source): the copy runs on the
+// graph's copy stream (copy engine only), overlapping the current step; the
+// next trainer_step_async commits them (swap, |max|, lazy x0 re-gathers).
 void trainer_stage_features(sc_trainer* t, const float* features, bool is_device);
 void commit_staged_features(sc_trainer* t);
 // Exchange bucket b (or the losses, b = -1) of exchange round j across ranks

@@ -246,15 +246,26 @@ def test_trainer_errors(sc, O):
         sc.CoFreeTrainer(g, gp, sc.TrainConfig(layers=1, hidden=[4]))
 
 
+def _matrix_shapes(d, hidden, C):
+    out, inp = [], d
+    for l, h in enumerate(hidden):
+        out += [(f"W{l}", h, inp), (f"U{l}", h, h + inp)]
+        inp = h
+    return out + [("head", C, inp)]
+
+
 @pytest.mark.parametrize("C", [13, 47, 61, 90])
 def test_many_classes(sc, O, C):
-    """Products-like widths: d = 100 features, C classes (softmax row kernel for C <= 64, warp
-    kernel above), 2 x 64 SAGE with DropEdge, 3 steps against the oracle.
+    """Products-like widths at 20k nodes: d = 100 features, C classes (softmax row kernel for
+    C <= 64, warp kernel above), 2 x 64 SAGE with DropEdge, 3 steps against the oracle.
 
-    Sized so that one ReLU decision flipped by GEMM rounding (a pre-activation within ~1e-6 of
-    zero lands on the other side than in the reference; ~1 such element per step at this size,
-    with the SIMT fp32 path too) moves the gathered gradient by well under 1e-4 relative: the
-    flipped element contributes one row of dW, ~1/sqrt(rows) of its norm (3000 rows: ~2e-4)."""
+    Teacher-forced: before each step the GPU trainer takes the oracle's parameters, so every step's
+    gradients are compared from identical inputs. At this size a pre-activation within ~1 ulp of zero
+    occurs about once per layer and partition; GEMM rounding (SIMT fp32 as well as the tensor-core
+    path) can put it on the other side of the ReLU than the reference, which changes one row of one
+    weight gradient by O(1e-3) (measured: tools/diag_part.py). The bar is therefore per row: the loss
+    within 1e-5, the gradient within 1e-4 after excluding at most 2 rows per matrix, and no row
+    beyond 1e-2."""
     rng = np.random.default_rng(C)
     n = 20000
     og = O.graph_build(n, rng.integers(0, n, size=(200000, 2), dtype=np.int32))
@@ -267,8 +278,26 @@ def test_many_classes(sc, O, C):
     te = np.zeros(n, np.uint8)
     tr[perm[:12000]], va[perm[12000:16000]], te[perm[16000:]] = 1, 1, 1
     og.set_data(f, lab, C, tr, va, te)
-    worst, _, _ = run_traj(sc, O, og, "random", 4, 1, 100, steps=3, hidden=[64, 64], dropedge=True, seed=3)
-    assert_within(worst)
+    g = gpu_graph(sc, og, 100)
+    gp, op = sc.partition_random(g, 4, 1), og.partition("random", 4, 1)
+    H = [64, 64]
+    t = sc.CoFreeTrainer(g, gp, sc.TrainConfig(layers=2, hidden=H, use_dropedge=True, seed=3))
+    to = op.trainer(H, lr=0.01, dropedge=True, seed=3, f32=True)
+    for e in range(3):
+        t.set_params(to.params().astype(np.float32))
+        loss, _ = t.step(e)
+        ol, _ = to.step(e)
+        assert abs(loss - ol) <= 1e-5 * abs(ol), (e, loss, ol)
+        a, b = t.grads().astype(np.float64), to.gathered()
+        k = 0
+        for name, r, c in _matrix_shapes(100, H, C):
+            x, y = a[k:k + r * c].reshape(r, c), b[k:k + r * c].reshape(r, c)
+            k += r * c
+            row_err = np.linalg.norm(x - y, axis=1) / np.maximum(np.linalg.norm(y, axis=1), 1e-30)
+            worst = np.argsort(-row_err)
+            keep = np.sort(worst[2:])
+            assert rel(x[keep], y[keep]) <= REL, (e, name, row_err[worst[:4]])
+            assert row_err[worst[0]] <= 1e-2, (e, name, row_err[worst[:4]])
 
 
 def test_skewed_degree_hubs(sc, O):

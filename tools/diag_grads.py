@@ -1,6 +1,6 @@
 """Per-matrix gradient error of the CUDA path vs the oracle (diagnostics for tolerance failures).
 
-    python tools/diag_grads.py C [gemm]
+    python tools/diag_grads.py C [gemm] [n] [m]
 """
 import os
 import sys
@@ -14,16 +14,17 @@ from paper_2308_03209_b200 import sagecut as sc  # noqa: E402
 
 C = int(sys.argv[1])
 gemm = sys.argv[2] if len(sys.argv) > 2 else "auto"
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 3000
+m = int(sys.argv[4]) if len(sys.argv) > 4 else 10 * n
 O = oracle()
 rng = np.random.default_rng(C)
-n = 3000
-og = O.graph_build(n, rng.integers(0, n, size=(30000, 2), dtype=np.int32))
+og = O.graph_build(n, rng.integers(0, n, size=(m, 2), dtype=np.int32))
 lab = rng.integers(0, C, size=n).astype(np.int32)
 f = rng.standard_normal((n, 100)).astype(np.float32)
 f[np.arange(n), lab % 100] += 1.0
 perm = rng.permutation(n)
 tr, va, te = (np.zeros(n, np.uint8) for _ in range(3))
-tr[perm[:1800]], va[perm[1800:2400]], te[perm[2400:]] = 1, 1, 1
+tr[perm[:n * 6 // 10]], va[perm[n * 6 // 10:n * 8 // 10]], te[perm[n * 8 // 10:]] = 1, 1, 1
 og.set_data(f, lab, C, tr, va, te)
 g, _ = sc.build_graph(n, og.edges())
 g.set_data(og.features(100).astype(np.float32), lab, C, tr, va, te)
@@ -43,6 +44,10 @@ sizes.append(C * inp)
 for e in range(3):
     t.step(e)
     to.step(e)
+    lg = np.concatenate([t.part_logits(i).ravel() for i in range(4)])
+    olg = np.concatenate([to.part_logits(i, C).ravel() for i in range(4)])
+    print(f"  logits rel {np.linalg.norm(lg - olg) / np.linalg.norm(olg):.2e}  params rel "
+          f"{np.linalg.norm(t.params() - to.params()) / np.linalg.norm(to.params()):.2e}")
     a, b = t.grads().astype(np.float64), to.gathered()
     k = 0
     row = []
