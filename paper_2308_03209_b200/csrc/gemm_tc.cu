@@ -490,14 +490,20 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                         }
                     }
                     mbar_wait(&sfull[sr.idx], sr.phase);
+                    // all of the stage's shared loads first (4 x LDS.128 in flight), then convert
+                    float4 xv[2][2];
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         const int idx = tid + j * kConv;
                         const int r = idx & 127, c = idx >> 7;  // row, 8-float chunk (0..3)
                         const uint8_t* rowp = sg + r * (kNtBK * 4);
-                        float4 x0 = *reinterpret_cast<const float4*>(rowp + (((2 * c) ^ (r & 7)) << 4));
-                        float4 x1 = *reinterpret_cast<const float4*>(rowp + (((2 * c + 1) ^ (r & 7)) << 4));
-                        split8_store(x0, x1, sa, st, st + kNtATile, sw64_off(r, c));
+                        xv[j][0] = *reinterpret_cast<const float4*>(rowp + (((2 * c) ^ (r & 7)) << 4));
+                        xv[j][1] = *reinterpret_cast<const float4*>(rowp + (((2 * c + 1) ^ (r & 7)) << 4));
+                    }
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int idx = tid + j * kConv;
+                        split8_store(xv[j][0], xv[j][1], sa, st, st + kNtATile, sw64_off(idx & 127, idx >> 7));
                     }
                     fence_proxy_async();
                     __syncwarp();
@@ -846,22 +852,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 if (valid < 8) mask8(x0, x1, valid);
             };
             if (whole) {
+                // all of the stage's shared loads first (up to 8 x LDS.128 in flight), then convert
+                constexpr int kJB = Cfg::kBLoc / 64;
+                float4 xa[2][2], xb[kJB][2];
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                     const int idx = tid + j * kConv;
-                    const int kr = idx & 31, ch = idx >> 5;
-                    float4 x0, x1;
-                    load8(sga, kr, ch, 8, x0, x1);
-                    split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
+                    load8(sga, idx & 31, idx >> 5, 8, xa[j][0], xa[j][1]);
                 }
 #pragma unroll
-                for (int j = 0; j < Cfg::kBLoc / 64; ++j) {
+                for (int j = 0; j < kJB; ++j) {
+                    const int idx = tid + j * kConv;
+                    if ((idx >> 5) < bch) load8(sgb, idx & 31, idx >> 5, 8, xb[j][0], xb[j][1]);
+                }
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int idx = tid + j * kConv;
+                    split8_store(xa[j][0], xa[j][1], sa_, st, st + kTnATile, mn_off((idx >> 5) * 8, idx & 31));
+                }
+#pragma unroll
+                for (int j = 0; j < kJB; ++j) {
                     const int idx = tid + j * kConv;
                     const int kr = idx & 31, ch = idx >> 5;
-                    if (ch >= bch) continue;
-                    float4 x0, x1;
-                    load8(sgb, kr, ch, 8, x0, x1);
-                    split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile, mn_off(ch * 8, kr));
+                    if (ch < bch)
+                        split8_store(xb[j][0], xb[j][1], sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile,
+                                     mn_off(ch * 8, kr));
                 }
             } else {
 #pragma unroll
