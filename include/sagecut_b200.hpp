@@ -358,7 +358,44 @@ struct EpochMetrics {  // trainer.hpp:38-46
 struct TrainResult {  // trainer.hpp:71-75 (model as the flat for_each_matrix vector)
     std::vector<float> model;
     std::vector<EpochMetrics> metrics;
+    int in_dim = 0, num_classes = 0;  // model dims, for save_checkpoint
+    std::vector<int> hidden;
 };
+
+// checkpoint.cpp:44-57 (the model as SageModel<double>, "CFCK" format)
+inline void save_checkpoint(const TrainResult& r, const std::string& path) {
+    check(sc_save_checkpoint_params(r.model.data(), r.in_dim, r.hidden.data(), static_cast<std::int32_t>(r.hidden.size()),
+                                    r.num_classes, path.c_str()));
+}
+// checkpoint.cpp:59-84: the flat parameters, cast to f32
+inline std::vector<float> load_checkpoint(const std::string& path) {
+    std::int64_t n = 0;
+    check(sc_load_checkpoint_params(path.c_str(), nullptr, 0, &n));
+    std::vector<float> theta(static_cast<std::size_t>(n));
+    check(sc_load_checkpoint_params(path.c_str(), theta.data(), n, &n));
+    return theta;
+}
+// trainer.cpp:126-140
+inline void write_metrics_jsonl(const std::vector<EpochMetrics>& metrics, const std::string& path) {
+    std::vector<sc_epoch_metrics> rows;
+    for (const auto& m : metrics)
+        rows.push_back(sc_epoch_metrics{m.epoch, m.train_loss, m.train_metric, m.val_metric, m.test_metric,
+                                        m.grad_norm, m.comm_floats});
+    check(sc_write_metrics_jsonl(path.c_str(), static_cast<std::int32_t>(rows.size()), rows.data()));
+}
+// partition_io.cpp:12-29 / :31-56 / :58-68
+inline void save_partition(const VertexCutPartition& part, const std::string& path,
+                           const ReweightScheme* weights = nullptr) {
+    check(sc_save_partition(part.get(), path.c_str(), weights ? static_cast<std::int32_t>(*weights) : -1));
+}
+inline VertexCutPartition load_partition(const std::string& path, const Graph& g) {
+    sc_vcut* h = nullptr;
+    check(sc_load_partition(g.get(), path.c_str(), &h));
+    return VertexCutPartition(g, h);
+}
+inline void save_edge_cut(const Graph& g, const EdgeCutPartition& ec, const std::string& path) {
+    check(sc_save_edge_cut(g.get(), ec.num_parts, ec.node_assignment.data(), path.c_str()));
+}
 
 // train_cofree (trainer.cpp:119 / trainer.hpp:202-313) on one GPU; for a
 // multi-GPU run create one sc_trainer per rank through the C ABI.
@@ -391,6 +428,9 @@ inline TrainResult train_cofree(const Graph& g, const VertexCutPartition& part, 
         m.comm_floats = static_cast<std::uint64_t>(part.num_parts) * static_cast<std::uint64_t>(P);
         res.metrics.push_back(m);
     }
+    res.in_dim = g.feature_dim;
+    res.num_classes = g.num_classes;
+    res.hidden = hidden;
     res.model.resize(static_cast<std::size_t>(P));
     check(sc_trainer_get_params(t, res.model.data()));
     return res;

@@ -188,6 +188,36 @@ sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms,
                                   int32_t* count);
 sc_status sc_trainer_destroy(sc_trainer* t);
 
+/* ---- files (byte-compatible with the reference's writers) ------------------ */
+/* save_partition (partition_io.cpp:12-29): JSON {num_parts, edge_assignment,
+ * parts[{nodes[, weights]}][, weight_scheme]}, nlohmann dump(2). weight_scheme:
+ * -1 = no weights, else 0 dar / 1 vanilla_inv / 2 none (compute_weights). */
+sc_status sc_save_partition(sc_vcut* vc, const char* path, int32_t weight_scheme);
+/* load_partition (partition_io.cpp:31-56): rebuilds the vertex cut from the
+ * stored assignment and checks the stored node sets (SC_ERUNTIME on mismatch). */
+sc_status sc_load_partition(sc_graph* g, const char* path, sc_vcut** out);
+/* save_edge_cut (partition_io.cpp:58-68) of the edge cut induced by node_assignment. */
+sc_status sc_save_edge_cut(sc_graph* g, int32_t num_parts, const int32_t* node_assignment, const char* path);
+/* save_checkpoint (checkpoint.cpp:44-57) of the trainer's model as SageModel<double>
+ * ("CFCK", u64 L, per layer message + update, head; u64 rows, u64 cols, row-major f64 LE). */
+sc_status sc_trainer_save_checkpoint(sc_trainer* t, const char* path);
+/* load_checkpoint (checkpoint.cpp:59-84) into the trainer's parameters (cast to f32;
+ * SC_EINVAL when the shapes differ from the trainer's model). */
+sc_status sc_trainer_load_checkpoint(sc_trainer* t, const char* path);
+/* save_checkpoint of a flat f32 parameter vector (for_each_matrix order) with
+ * the model's dims; load: count = number of parameters (pass theta = NULL to
+ * size), values cast to f32 in the same order. */
+sc_status sc_save_checkpoint_params(const float* theta, int32_t in_dim, const int32_t* hidden, int32_t layers,
+                                    int32_t num_classes, const char* path);
+sc_status sc_load_checkpoint_params(const char* path, float* theta, int64_t cap, int64_t* count);
+typedef struct {         /* EpochMetrics (trainer.hpp:38-46) */
+    int32_t epoch;
+    double train_loss, train_metric, val_metric, test_metric, grad_norm;
+    uint64_t comm_floats;
+} sc_epoch_metrics;
+/* write_metrics_jsonl (trainer.cpp:126-140). */
+sc_status sc_write_metrics_jsonl(const char* path, int32_t n, const sc_epoch_metrics* rows);
+
 /* ---- diagnostics (kernel-level parity tests) ------------------------------- */
 /* C[M x N] = A1[rows1] B1' (+ A2 B2') with epilogue epi (0 none, 1 relu,
  * 2 row-scale by `scale`), through the tcgen05 bf16x3 kernel (mode 0) or the

@@ -23,11 +23,13 @@
 #include <thread>
 #include <vector>
 
+#include "sagecut/checkpoint.hpp"
 #include "sagecut/dropedge.hpp"
 #include "sagecut/graph.hpp"
 #include "sagecut/graph_io.hpp"
 #include "sagecut/nn.hpp"
 #include "sagecut/partition.hpp"
+#include "sagecut/partition_io.hpp"
 #include "sagecut/reweight.hpp"
 #include "sagecut/rng.hpp"
 #include "sagecut/synth.hpp"
@@ -521,6 +523,68 @@ std::int64_t ref_init_params(int in_dim, const int* hidden, int layers, int clas
         }
     });
     return count;
+}
+
+// ---- File formats (partition_io.cpp, checkpoint.cpp, trainer.cpp:126-140) --------
+// scheme: -1 no weights, else dar / vanilla_inv / none
+int ref_save_partition(void* gp, void* pp, const char* path, int scheme) {
+    return guard([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        const auto& part = *static_cast<VertexCutPartition*>(pp);
+        if (scheme < 0) {
+            save_partition(part, path);
+        } else {
+            const NodeWeights w = compute_weights(static_cast<ReweightScheme>(scheme), g, part);
+            save_partition(part, path, &w);
+        }
+    });
+}
+void* ref_load_partition(void* gp, const char* path) {
+    VertexCutPartition* out = nullptr;
+    if (guard([&] { out = new VertexCutPartition(load_partition(path, *static_cast<Graph*>(gp))); })) return nullptr;
+    return out;
+}
+int ref_save_edge_cut(void* gp, int p, const std::int32_t* na, const char* path) {
+    return guard([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        save_edge_cut(edge_cut_from_assignment(g, p, std::vector<int>(na, na + g.num_nodes)), path);
+    });
+}
+// theta: flat f32 parameters (for_each_matrix order) -> SageModel<double> (TrainResult::model) -> CFCK
+int ref_save_checkpoint_f32(const float* theta, int in_dim, const int* hidden, int layers, int classes,
+                            const char* path) {
+    return guard([&] {
+        auto m = make_sage_model<double>(in_dim, hidden_vec(hidden, layers), classes, 0);
+        std::vector<double> v(theta, theta + m.param_count());
+        unflatten(m, v.data());
+        save_checkpoint(m, path);
+    });
+}
+// flat f64 parameters of a CFCK file (count returned; -1 on error)
+std::int64_t ref_load_checkpoint(const char* path, double* out) {
+    std::int64_t count = -1;
+    guard([&] {
+        const auto m = load_checkpoint(path);
+        if (out) flatten(m, out);
+        count = static_cast<std::int64_t>(m.param_count());
+    });
+    return count;
+}
+// rows: n x 6 doubles (train_loss, train_metric, val_metric, test_metric, grad_norm, comm_floats) + epochs
+int ref_write_metrics(const char* path, int n, const int* epochs, const double* rows) {
+    return guard([&] {
+        std::vector<EpochMetrics> v(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            v[i].epoch = epochs[i];
+            v[i].train_loss = rows[6 * i];
+            v[i].train_metric = rows[6 * i + 1];
+            v[i].val_metric = rows[6 * i + 2];
+            v[i].test_metric = rows[6 * i + 3];
+            v[i].grad_norm = rows[6 * i + 4];
+            v[i].comm_floats = static_cast<std::uint64_t>(rows[6 * i + 5]);
+        }
+        write_metrics_jsonl(v, path);
+    });
 }
 
 // ---- Trainer -------------------------------------------------------------------

@@ -10,6 +10,7 @@
 
 #include "../../include/sagecut_cuda.h"
 #include "internal.hpp"
+#include "io.hpp"
 #include "trainer.hpp"
 
 namespace {
@@ -410,6 +411,189 @@ sc_status sc_compute_weights(sc_vcut* vc, int32_t scheme, double* out) {
             SC_CUDA(cudaStreamSynchronize(vc->g->ctx->stream));
             off += nl;
         }
+    });
+}
+
+// ---- files (partition_io.cpp, checkpoint.cpp, trainer.cpp:126-140) ----
+namespace {
+const char* const kSchemeNames[] = {"dar", "vanilla_inv", "none"};
+std::vector<std::vector<int32_t>> part_nodes_host(sc_vcut* vc) {
+    std::vector<std::vector<int32_t>> nodes(vc->p);
+    for (int32_t i = 0; i < vc->p; ++i) {
+        nodes[i].resize(vc->parts[i].n_local);
+        d2h(nodes[i].data(), vc->parts[i].nodes.get(), vc->parts[i].n_local, vc->g->ctx->stream);
+    }
+    SC_CUDA(cudaStreamSynchronize(vc->g->ctx->stream));
+    return nodes;
+}
+}  // namespace
+
+sc_status sc_save_partition(sc_vcut* vc, const char* path, int32_t weight_scheme) {
+    return guard([&] {
+        REQUIRE_ARG(vc && path, "sc_save_partition: null argument");
+        REQUIRE_ARG(weight_scheme >= -1 && weight_scheme <= 2, "sc_save_partition: bad weight scheme");
+        set_device(vc->g->ctx);
+        cudaStream_t s = vc->g->ctx->stream;
+        std::vector<int32_t> assign(vc->g->m);
+        d2h(assign.data(), vc->assign.get(), vc->g->m, s);
+        const auto nodes = part_nodes_host(vc);
+        std::vector<std::vector<double>> w;
+        if (weight_scheme >= 0) {
+            for (int32_t i = 0; i < vc->p; ++i) {
+                const int64_t nl = vc->parts[i].n_local;
+                DevBuf<double> wd(std::max<int64_t>(nl, 1));
+                compute_weights_device(vc, weight_scheme, i, wd.get());
+                w.emplace_back(nl);
+                d2h(w.back().data(), wd.get(), nl, s);
+                SC_CUDA(cudaStreamSynchronize(s));
+            }
+        }
+        write_partition_json(path, vc->p, assign, nodes, weight_scheme >= 0 ? &w : nullptr,
+                             weight_scheme >= 0 ? kSchemeNames[weight_scheme] : nullptr);
+    });
+}
+sc_status sc_load_partition(sc_graph* g, const char* path, sc_vcut** out) {
+    return guard([&] {
+        REQUIRE_ARG(g && path && out, "sc_load_partition: null argument");
+        set_device(g->ctx);
+        const std::string p(path);
+        int32_t np = 0;
+        std::vector<int32_t> assign;
+        std::vector<std::vector<int32_t>> stored;
+        read_partition_json(p, np, assign, stored);
+        if (int64_t(assign.size()) != g->m)  // partition_io.cpp:40-43
+            throw std::runtime_error(p + ": partition was built for " + std::to_string(assign.size()) +
+                                     " edges, graph has " + std::to_string(g->m));
+        REQUIRE_ARG(np >= 1, "num_parts must be >= 1");
+        for (int32_t a : assign)
+            REQUIRE_ARG(a >= 0 && a < np, "edge assignment references an invalid part");
+        DevBuf<int32_t> d(std::max<int64_t>(g->m, 1));
+        h2d(d.get(), assign.data(), g->m, g->ctx->stream);
+        auto vc = build_vertex_cut_device(g, np, std::move(d));
+        if (stored.size() != size_t(vc->p)) throw std::runtime_error(p + ": part count mismatch");
+        if (part_nodes_host(vc.get()) != stored)
+            throw std::runtime_error(p + ": stored node sets do not match this graph");
+        *out = vc.release();
+    });
+}
+sc_status sc_save_edge_cut(sc_graph* g, int32_t p, const int32_t* node_assignment, const char* path) {
+    return guard([&] {
+        REQUIRE_ARG(g && path && (node_assignment || g->n == 0), "sc_save_edge_cut: null argument");
+        REQUIRE_ARG(p >= 1, "num_parts must be >= 1");
+        set_device(g->ctx);
+        std::vector<int64_t> kept(p), halo(p);
+        int64_t ncut = 0;
+        edge_cut_stats_device(g, p, node_assignment, kept.data(), &ncut, halo.data(), nullptr, nullptr, nullptr);
+        int64_t nh = 0;
+        for (int64_t h : halo) nh += h;
+        std::vector<int32_t> cut(ncut), hn(nh);
+        edge_cut_stats_device(g, p, node_assignment, kept.data(), &ncut, halo.data(), nullptr, cut.data(), hn.data());
+        std::vector<std::vector<int32_t>> sets(p);
+        int64_t o = 0;
+        for (int32_t i = 0; i < p; ++i) {
+            sets[i].assign(hn.begin() + o, hn.begin() + o + halo[i]);
+            o += halo[i];
+        }
+        write_edge_cut_json(path, p, std::vector<int32_t>(node_assignment, node_assignment + g->n), cut, sets);
+    });
+}
+namespace {
+std::vector<std::pair<int64_t, int64_t>> model_shapes(sc_trainer* t) {  // for_each_matrix order
+    std::vector<std::pair<int64_t, int64_t>> sh;
+    for (const auto& lo : t->lay) {
+        sh.emplace_back(lo.H, lo.in);
+        sh.emplace_back(lo.H, lo.H + lo.in);
+    }
+    sh.emplace_back(t->C, t->E);
+    return sh;
+}
+}  // namespace
+sc_status sc_trainer_save_checkpoint(sc_trainer* t, const char* path) {
+    return guard([&] {
+        REQUIRE_ARG(t && path, "sc_trainer_save_checkpoint: null argument");
+        set_device(t->ctx);
+        trainer_finish(t, nullptr, nullptr);
+        std::vector<float> theta(t->P);
+        d2h(theta.data(), t->theta.get(), t->P, t->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+        std::vector<HostMatrix> mats;
+        int64_t k = 0;
+        for (const auto& [r, c] : model_shapes(t)) {  // TrainResult::model is SageModel<double>
+            HostMatrix m;
+            m.rows = uint64_t(r);
+            m.cols = uint64_t(c);
+            m.v.assign(theta.begin() + k, theta.begin() + k + r * c);
+            k += r * c;
+            mats.push_back(std::move(m));
+        }
+        write_checkpoint(path, mats);
+    });
+}
+sc_status sc_trainer_load_checkpoint(sc_trainer* t, const char* path) {
+    return guard([&] {
+        REQUIRE_ARG(t && path, "sc_trainer_load_checkpoint: null argument");
+        set_device(t->ctx);
+        trainer_finish(t, nullptr, nullptr);
+        const auto mats = read_checkpoint(path);
+        const auto sh = model_shapes(t);
+        REQUIRE_ARG(mats.size() == sh.size(), "load_checkpoint: layer count does not match the model");
+        std::vector<float> theta;
+        for (size_t i = 0; i < sh.size(); ++i) {
+            REQUIRE_ARG(mats[i].rows == uint64_t(sh[i].first) && mats[i].cols == uint64_t(sh[i].second),
+                        "load_checkpoint: matrix shape does not match the model");
+            for (double v : mats[i].v) theta.push_back(static_cast<float>(v));
+        }
+        h2d(t->theta.get(), theta.data(), t->P, t->ctx->stream);
+        t->tc.invalidate();
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+sc_status sc_save_checkpoint_params(const float* theta, int32_t in_dim, const int32_t* hidden, int32_t layers,
+                                    int32_t num_classes, const char* path) {
+    return guard([&] {
+        REQUIRE_ARG(theta && path && (hidden || layers == 0), "sc_save_checkpoint_params: null argument");
+        REQUIRE_ARG(layers >= 0 && in_dim >= 0 && num_classes >= 0, "sc_save_checkpoint_params: bad dims");
+        std::vector<HostMatrix> mats;
+        int64_t k = 0, in = in_dim;
+        auto add = [&](int64_t r, int64_t c) {
+            HostMatrix m;
+            m.rows = uint64_t(r);
+            m.cols = uint64_t(c);
+            m.v.assign(theta + k, theta + k + r * c);
+            k += r * c;
+            mats.push_back(std::move(m));
+        };
+        for (int32_t l = 0; l < layers; ++l) {
+            add(hidden[l], in);
+            add(hidden[l], hidden[l] + in);
+            in = hidden[l];
+        }
+        add(num_classes, in);
+        write_checkpoint(path, mats);
+    });
+}
+sc_status sc_load_checkpoint_params(const char* path, float* theta, int64_t cap, int64_t* count) {
+    return guard([&] {
+        REQUIRE_ARG(path && count, "sc_load_checkpoint_params: null argument");
+        const auto mats = read_checkpoint(path);
+        int64_t n = 0;
+        for (const auto& m : mats) n += int64_t(m.v.size());
+        *count = n;
+        if (!theta) return;
+        REQUIRE_ARG(cap >= n, "sc_load_checkpoint_params: output buffer too small");
+        int64_t k = 0;
+        for (const auto& m : mats)
+            for (double v : m.v) theta[k++] = static_cast<float>(v);
+    });
+}
+sc_status sc_write_metrics_jsonl(const char* path, int32_t n, const sc_epoch_metrics* rows) {
+    return guard([&] {
+        REQUIRE_ARG(path && (rows || n == 0), "sc_write_metrics_jsonl: null argument");
+        std::vector<EpochRow> v(n);
+        for (int32_t i = 0; i < n; ++i)
+            v[i] = EpochRow{rows[i].epoch, rows[i].train_loss, rows[i].train_metric, rows[i].val_metric,
+                            rows[i].test_metric, rows[i].grad_norm, rows[i].comm_floats};
+        write_metrics_jsonl(path, v);
     });
 }
 

@@ -83,6 +83,19 @@ _sig("sc_partition_edge_cut_greedy", [_vp, _i32, _u64, _vp])
 _sig("sc_edge_cut_from_assignment", [_vp, _i32, _vp, _vp, C.POINTER(_i64), _vp, _vp, _vp, _vp])
 _sig("sc_edge_cut_to_vertex_cut", [_vp, _i32, _vp, _u64, _pp])
 _sig("sc_vcut_warnings", [_vp, C.c_char_p, _i64, C.POINTER(_i64)])
+_sig("sc_save_partition", [_vp, C.c_char_p, _i32])
+_sig("sc_load_partition", [_vp, C.c_char_p, _pp])
+_sig("sc_save_edge_cut", [_vp, _i32, _vp, C.c_char_p])
+_sig("sc_trainer_save_checkpoint", [_vp, C.c_char_p])
+_sig("sc_trainer_load_checkpoint", [_vp, C.c_char_p])
+
+
+class _EpochMetricsC(C.Structure):
+    _fields_ = [("epoch", _i32), ("train_loss", _f64), ("train_metric", _f64), ("val_metric", _f64),
+                ("test_metric", _f64), ("grad_norm", _f64), ("comm_floats", _u64)]
+
+
+_sig("sc_write_metrics_jsonl", [C.c_char_p, _i32, _vp])
 _sig("sc_compute_weights", [_vp, _i32, _vp])
 _sig("sc_precompute_masks", [_vp, _i64, _i32, _f64, _u64, _vp])
 _sig("sc_select_mask", [_u64, _u64, _u64, _i32], _i32)
@@ -450,6 +463,34 @@ def edge_cut_to_vertex_cut(g: Graph, ec: EdgeCutPartition, seed: int) -> VertexC
     return VertexCutPartition(h, g)
 
 
+def save_partition(part: VertexCutPartition, path: str, weights: Optional[str] = None):
+    """save_partition (partition_io.cpp:12-29); `weights` names a reweight scheme to embed."""
+    _check(_lib.sc_save_partition(part.h, os.fsencode(path), -1 if weights is None else _SCHEMES[weights]),
+           "save_partition")
+
+
+def load_partition(path: str, g: Graph) -> VertexCutPartition:  # partition_io.cpp:31-56
+    h = _vp()
+    _check(_lib.sc_load_partition(g.h, os.fsencode(path), C.byref(h)), "load_partition")
+    return VertexCutPartition(h, g)
+
+
+def save_edge_cut(g: Graph, ec: "EdgeCutPartition", path: str):  # partition_io.cpp:58-68
+    na = np.ascontiguousarray(ec.node_assignment, np.int32)
+    _check(_lib.sc_save_edge_cut(g.h, ec.num_parts, _ptr(na), os.fsencode(path)), "save_edge_cut")
+
+
+def write_metrics_jsonl(metrics, path: str):
+    """write_metrics_jsonl (trainer.cpp:126-140); metrics: EpochMetrics-like objects or dicts."""
+    rows = (_EpochMetricsC * max(len(metrics), 1))()
+    for i, m in enumerate(metrics):
+        get = (lambda k: m[k]) if isinstance(m, dict) else (lambda k: getattr(m, k))
+        rows[i] = _EpochMetricsC(int(get("epoch")), float(get("train_loss")), float(get("train_metric")),
+                                 float(get("val_metric")), float(get("test_metric")), float(get("grad_norm")),
+                                 int(get("comm_floats")))
+    _check(_lib.sc_write_metrics_jsonl(os.fsencode(path), len(metrics), C.cast(rows, _vp)), "write_metrics_jsonl")
+
+
 def build_vertex_cut(g: Graph, num_parts: int, edge_assignment) -> VertexCutPartition:  # partition.cpp:22
     a = np.ascontiguousarray(edge_assignment, np.int32)
     if len(a) != g.num_edges():
@@ -641,6 +682,12 @@ class CoFreeTrainer:
                 raise ValueError("stage_features: features must be num_nodes x d")
             self._staged = f  # keep the host buffer alive until the copy has run
             _check(_lib.sc_trainer_stage_features(self.h, _ptr(f), 0), "stage_features")
+
+    def save_checkpoint(self, path: str):  # checkpoint.cpp:44-57 (model as SageModel<double>)
+        _check(_lib.sc_trainer_save_checkpoint(self.h, os.fsencode(path)), "save_checkpoint")
+
+    def load_checkpoint(self, path: str):  # checkpoint.cpp:59-84
+        _check(_lib.sc_trainer_load_checkpoint(self.h, os.fsencode(path)), "load_checkpoint")
 
     def step_async(self, epoch: int):
         _check(_lib.sc_trainer_step_async(self.h, epoch), "step")

@@ -70,6 +70,17 @@ int main(int argc, char** argv) {
         cfg.use_dropedge = true;
         cfg.seed = seed;
         const auto res = sb::train_cofree(g, part, cfg);
+        // file formats through the facade (partition_io.cpp, checkpoint.cpp, trainer.cpp:126-140)
+        if (argc > 2) {
+            const std::string dir = argv[2];
+            const sb::ReweightScheme dar = sb::ReweightScheme::dar;
+            sb::save_partition(part, dir + "/part.json", &dar);
+            const auto back = sb::load_partition(dir + "/part.json", g);
+            std::printf("reload_same %d\n", back.edge_assignment() == part.edge_assignment() ? 1 : 0);
+            sb::save_checkpoint(res, dir + "/model.ckpt");
+            std::printf("ckpt_same %d\n", sb::load_checkpoint(dir + "/model.ckpt") == res.model ? 1 : 0);
+            sb::write_metrics_jsonl(res.metrics, dir + "/metrics.jsonl");
+        }
         std::printf("loss");
         for (const auto& e : res.metrics) std::printf(" %.17g", e.train_loss);
         std::printf("\nparams");

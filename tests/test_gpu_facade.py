@@ -29,7 +29,7 @@ def test_cpp_facade_matches_oracle(tmp_path):
         fh.write("\n".join(" ".join(repr(float(x)) for x in row) for row in f) + "\n")
         for arr in (lab, tr, va, te):
             fh.write(" ".join(str(int(x)) for x in arr) + "\n")
-    out = subprocess.run([EXE, str(path)], capture_output=True, text=True, timeout=300)
+    out = subprocess.run([EXE, str(path), str(tmp_path)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     res = {ln.split(" ", 1)[0]: ln.split(" ", 1)[1] if " " in ln else "" for ln in out.stdout.strip().split("\n")}
     op = og.partition("random", p, 3)
@@ -53,4 +53,8 @@ def test_cpp_facade_matches_oracle(tmp_path):
     kept, cut, halo = og.edge_cut(p, na)
     assert int(res["ec_cut"]) == len(cut) and int(res["ec_halo"]) == sum(len(h) for h in halo)
     assert [int(x) for x in res["ec2vc"].split()] == og.edge_cut_to_vertex_cut(p, na, 5).assignment().tolist()
+    assert res["reload_same"] == "1" and res["ckpt_same"] == "1"
+    assert (tmp_path / "model.ckpt").read_bytes()[:4] == b"CFCK"
+    assert len((tmp_path / "metrics.jsonl").read_text().splitlines()) == epochs
+    assert '"weight_scheme": "dar"' in (tmp_path / "part.json").read_text()
     assert res["error"].startswith("invalid_argument num_parts must be >= 1")
