@@ -341,7 +341,8 @@ def run_gpu_arm(args, cfg):
     value = cfg["layers"] * kept / (ms_step / 1e3)
 
     # ---- e2e: the public API with host buffers: every step's input (the feature matrix, from pinned
-    # host memory) is copied host -> device inside the timed region and the loss / grad-norm read back.
+    # host memory) is copied host -> device inside the timed region and the loss, grad-norm (f64) and
+    # non-finite flag (i32) read back (20 bytes).
     # Step k+1's copy (and its partitions' layer-0 row gathers) is staged on the library's copy
     # stream while step k computes; step 0's copy is exposed.
     pinned = torch.from_numpy(feats).pin_memory()
@@ -402,7 +403,7 @@ def run_gpu_arm(args, cfg):
         "kernels": kernels,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(feats.nbytes), "d2h_bytes_per_step": 16},
+                "h2d_bytes_per_step": int(feats.nbytes), "d2h_bytes_per_step": 20},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "setup_s": setup_s,

@@ -86,6 +86,7 @@ sc_trainer::~sc_trainer() {
     if (comm) ncclCommDestroy(comm);
     for (cudaEvent_t e : fork_events) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    if (host) cudaFreeHost(host);
     for (cudaEvent_t e : xfer_events) cudaEventDestroy(e);
     if (comm_done) cudaEventDestroy(comm_done);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -197,6 +198,12 @@ void trainer_init(sc_trainer* t) {
     t->part_loss.alloc(t->pp);
     SC_CUDA(cudaMemsetAsync(t->part_loss.get(), 0, t->part_loss.bytes(), s));
     t->out2.alloc(2);
+    if (!t->host) {
+        void* h = nullptr;
+        SC_CUDA(cudaMallocHost(&h, sizeof(sc_trainer::HostOut)));
+        t->host = static_cast<sc_trainer::HostOut*>(h);
+        *t->host = sc_trainer::HostOut{{0, 0}, 0};
+    }
     t->nonfinite.alloc(1);
     t->red_partial.alloc(1024);
     t->amax.alloc(sc_trainer::kSlotBase + 2 * std::max(t->L, 1));
@@ -539,8 +546,8 @@ void trainer_step_async(sc_trainer* t, int epoch) {
          static_cast<float>(t->lr), static_cast<float>(1e-8), t->nonfinite.get(), s);
     t->tc.invalidate();  // weights changed: rebuild the pre-split weight images on next use
     t->prof.end(s);
-    d2h(t->host_out, t->out2.get(), 2, s);
-    d2h(&t->host_nonfinite, t->nonfinite.get(), 1, s);
+    d2h(t->host->out, t->out2.get(), 2, s);
+    d2h(&t->host->nonfinite, t->nonfinite.get(), 1, s);
     t->pending = true;
 }
 
@@ -549,10 +556,10 @@ void trainer_finish(sc_trainer* t, double* loss, double* gnorm) {
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
         t->pending = false;
         t->prof.collect();
-        if (t->host_nonfinite) throw std::invalid_argument("adam_step: non-finite gradient");
+        if (t->host->nonfinite) throw std::invalid_argument("adam_step: non-finite gradient");
         ++t->adam_step;
-        t->last_loss = t->host_out[1];
-        t->last_gnorm = t->host_out[0];
+        t->last_loss = t->host->out[1];
+        t->last_gnorm = t->host->out[0];
     }
     if (loss) *loss = t->last_loss;
     if (gnorm) *gnorm = t->last_gnorm;

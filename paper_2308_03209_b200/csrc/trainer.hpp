@@ -122,8 +122,14 @@ struct sc_trainer {
     float* amax_slot(int i) { return amax.get() + i; }
     float* amax_x(int l) { return amax.get() + kSlotBase + (l - 1); }  // layer input X[l], l in [1, L]
     float* amax_msg(int l) { return amax.get() + kSlotBase + L + l; }  // MSG[l], l in [0, L)
-    double host_out[2] = {0, 0};
-    int host_nonfinite = 0;
+    // Pinned (cudaMallocHost) read-back slots: a D2H into pageable memory would
+    // block the host until the whole step has run, so nothing (e.g. the next
+    // step's feature copy) could be enqueued behind it.
+    struct HostOut {
+        double out[2];
+        int nonfinite;
+    };
+    HostOut* host = nullptr;
     bool pending = false;
     double last_loss = 0, last_gnorm = 0;
     sc::TcGemm tc;
