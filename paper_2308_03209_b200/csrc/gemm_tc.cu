@@ -723,16 +723,10 @@ __device__ __forceinline__ uint32_t mn_off(uint32_t mn, uint32_t k) {
 // 256-column slice of A' (M = 256, 128 per CTA) and splits the B' tile's columns
 // between its two CTAs, so each B' element is converted once per pair instead
 // of once per 128-column A' tile, and per-SM conversion work drops by a third.
-// DIRECT: the converter warps load their fp32 rows from global memory straight
-// into registers (one k-block ahead) instead of through TMA-staged shared
-// memory. Staging cost 64 KB of shared-memory traffic per 32-row stage (TMA
-// write + converter read) on top of the 32 KB fp16 stores and 48 KB of MMA
-// operand reads, which saturated the SM's shared-memory bandwidth (ncu: L1
-// 80 %, converters stalled on LDS); the freed staging space deepens the ring.
-template <bool PAIR, bool DIRECT = false>
+template <bool PAIR>
 struct TnCfg {
-    static constexpr int kStages = DIRECT ? (PAIR ? 6 : 4) : (PAIR ? 3 : 2);
-    static constexpr int kStg = DIRECT ? 0 : (PAIR ? 3 : 2);
+    static constexpr int kStages = PAIR ? 3 : 2;
+    static constexpr int kStg = PAIR ? 3 : 2;
     static constexpr int kBLoc = PAIR ? kMaxN / 2 : kMaxN;  // B' columns held per CTA
     static constexpr int kBTile = kBLoc * kTnBK * 2;        // one (hi or lo) B' tile
     static constexpr int kStage = 2 * kTnATile + 2 * kBTile;
@@ -745,21 +739,10 @@ struct TnCfg {
     static constexpr int kACols = PAIR ? 2 * kBM : kBM;      // A' columns per tile
 };
 static_assert(TnCfg<true>::kSmem <= 232448 && TnCfg<false>::kSmem <= 232448, "TN shared memory");
-static_assert(TnCfg<true, true>::kSmem <= 232448, "TN shared memory");
 
-// Split 4 fp32 (scaled by s) into fp16 hi / lo halves of one 8-column chunk.
-__device__ __forceinline__ void split4_store(const float4& x, float s, uint8_t* hi_base, uint8_t* lo_base,
-                                             uint32_t off) {
-    uint2 hi, lo;
-    split2(x.x, x.y, s, hi.x, lo.x);
-    split2(x.z, x.w, s, hi.y, lo.y);
-    *reinterpret_cast<uint2*>(hi_base + off) = hi;
-    *reinterpret_cast<uint2*>(lo_base + off) = lo;
-}
-
-template <bool PAIR, bool DIRECT = false>
+template <bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
-    using Cfg = TnCfg<PAIR, DIRECT>;
+    using Cfg = TnCfg<PAIR>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stg_base = smem + Cfg::kStgOff;  // kStg x [A' rows | B' rows]
@@ -823,9 +806,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     const uint32_t tempty_l = PAIR ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
 
     if (warp == kLoadWarp) {
-        if constexpr (DIRECT) {
-            // converters fetch their own rows
-        } else {
         // ================= loader: 2D TMA boxes (32 columns x 32 rows, SWIZZLE_128B) -> staging =================
         // A' needs ceil(na/32) boxes, B' ceil(nbl/32) (each from B1 or B2; n2a is a multiple of 32).
         const int a_boxes = (na + 31) >> 5, b_boxes = (nbl + 31) >> 5;
@@ -844,79 +824,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 const int32_t c = nb0 + 32 * lane;
                 if (c < p.n2a) tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[ring.idx], pol_b);
                 else tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[ring.idx], pol_b);
-            }
-        }
-        }
-    } else if (DIRECT && warp < kConvWarps) {
-        // ================= converters, direct: global fp32 rows -> registers -> MN-major fp16 hi/lo ========
-        // Warp w owns rows 4w..4w+3 of each 32-row k-block; lane l owns columns 4l..4l+3 of each
-        // 128-column group (A': one group, B': kBLoc / 128 groups), so a warp-wide load is one
-        // contiguous 512 B row segment. Loads of k-block kb+1 are in flight while kb converts.
-        constexpr int kVB = Cfg::kBLoc / 128;
-        const float sa_ = ldexpf(1.f, ka), sb_ = ldexpf(1.f, kbx);
-        const int c4 = 4 * lane;  // column within a 128-column group
-        const float* a_col = p.a + n10 + c4;
-        const float* b_col[kVB];
-        int64_t b_ld[kVB];
-#pragma unroll
-        for (int v = 0; v < kVB; ++v) {
-            const int32_t cb = nb0 + 128 * v + c4;  // n2a is a multiple of 32: 4 columns never straddle B1 | B2
-            const bool first = cb < p.n2a;
-            b_col[v] = first ? p.b[0].ptr + cb : p.b[1].ptr + (cb - p.n2a);
-            b_ld[v] = first ? p.b[0].ld : p.b[1].ld;
-        }
-        const int a_valid = na - c4;  // columns of this lane's 4 that exist (<= 0: none)
-        int b_valid[kVB];
-#pragma unroll
-        for (int v = 0; v < kVB; ++v) b_valid[v] = nbl - 128 * v - c4;
-        auto ld4 = [](const float* q, int valid) {
-            if (valid >= 4) return __ldg(reinterpret_cast<const float4*>(q));
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid > 0) x.x = __ldg(q);
-            if (valid > 1) x.y = __ldg(q + 1);
-            if (valid > 2) x.z = __ldg(q + 2);
-            return x;
-        };
-        float4 ca[4], cb[4][kVB], na_[4], nb_[4][kVB];
-        auto fetch = [&](int kb, float4 (&xa)[4], float4 (&xb)[4][kVB]) {
-            const int64_t k0 = r0 + int64_t(kb) * kTnBK;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int64_t k = k0 + warp * 4 + i;
-                const bool row_ok = k < r1;
-                xa[i] = row_ok ? ld4(a_col + k * p.lda, a_valid) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int v = 0; v < kVB; ++v)
-                    xb[i][v] = row_ok ? ld4(b_col[v] + k * b_ld[v], b_valid[v]) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        };
-        if (kblocks > 0) fetch(0, ca, cb);
-        Ring mr;
-        for (int kb = 0; kb < kblocks; ++kb, mr.next(Cfg::kStages)) {
-            if (kb + 1 < kblocks) fetch(kb + 1, na_, nb_);
-            uint8_t* st = smem + mr.idx * Cfg::kStage;
-            mbar_wait(&empty[mr.idx], mr.phase ^ 1);
-            const uint32_t half = static_cast<uint32_t>(c4 & 4) << 1;  // 0 or 8 bytes within the 16 B chunk
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int kr = warp * 4 + i;
-                split4_store(ca[i], sa_, st, st + kTnATile, mn_off(c4 & ~7, kr) + half);
-#pragma unroll
-                for (int v = 0; v < kVB; ++v)
-                    split4_store(cb[i][v], sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile,
-                                 mn_off(128 * v + (c4 & ~7), kr) + half);
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                if constexpr (PAIR) mbar_arrive_cluster(full_l + mr.idx * 8);
-                else mbar_arrive(&full[mr.idx]);
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                ca[i] = na_[i];
-#pragma unroll
-                for (int v = 0; v < kVB; ++v) cb[i][v] = nb_[i][v];
             }
         }
     } else if (warp < kConvWarps) {
@@ -1228,16 +1135,8 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
         }
         SC_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
     };
-    static const bool direct = [] {
-        const char* e = std::getenv("SC_TN_DIRECT");
-        return e ? std::atoi(e) != 0 : true;
-    }();
-    if (pair) {  // (single-CTA tiles hold 256 B' columns: too many registers to prefetch directly)
-        if (direct) launch(tc::gemm_tn_f16x3_kernel<true, true>, tc::TnCfg<true, true>::kSmem);
-        else launch(tc::gemm_tn_f16x3_kernel<true, false>, tc::TnCfg<true, false>::kSmem);
-    } else {
-        launch(tc::gemm_tn_f16x3_kernel<false, false>, tc::TnCfg<false, false>::kSmem);
-    }
+    if (pair) launch(tc::gemm_tn_f16x3_kernel<true>, tc::TnCfg<true>::kSmem);
+    else launch(tc::gemm_tn_f16x3_kernel<false>, tc::TnCfg<false>::kSmem);
     SC_LAUNCH_CHECK();
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();
