@@ -94,7 +94,6 @@ struct alignas(64) Params {
     int epi;
     const float* row_scale;
     float* amax_out;
-    uint32_t* relu_mask;  // optional (EPI == kEpiRelu): bit c of word [row][c / 32] = C[row][c] > 0
     int64_t tiles;
 };
 
@@ -576,17 +575,13 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
                 if (lane == 0) bulk_wait_read<0>();  // the previous store has read the box
                 __syncwarp();
-                uint32_t pos = 0;  // ReLU sign bits of this row's 32 columns
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     float x[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         float v = __uint_as_float(r[4 * j + q]) * unscale;
-                        if (EPI == kEpiRelu) {
-                            v = fmaxf(v, 0.f);
-                            pos |= (v > 0.f ? 1u : 0u) << (4 * j + q);
-                        }
+                        if (EPI == kEpiRelu) v = fmaxf(v, 0.f);
                         if (EPI == kEpiRowScale) v = sc * v;
                         if (AMAX) amx = fmaxf(amx, fabsf(v));
                         x[q] = v;
@@ -594,8 +589,6 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                     *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
                         make_float4(x[0], x[1], x[2], x[3]);
                 }
-                if (EPI == kEpiRelu && p.relu_mask && row0 + lane < p.M)
-                    p.relu_mask[(row0 + lane) * (p.n_pad >> 5) + (c0 >> 5)] = pos;
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0 && row0 < p.M) tma_store_2d(&p.tmap_c, box, c0, static_cast<int32_t>(row0));
@@ -1188,7 +1181,7 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
 
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-                float* amax_out, cudaStream_t s, uint32_t* relu_mask) {
+                float* amax_out, cudaStream_t s) {
     if (M <= 0 || N <= 0) return;
     if (!tc_supported(a1, a2, N) || !tc_out_supported(C, ldc))
         throw std::logic_error("gemm_f16x3: unsupported operand layout");
@@ -1218,7 +1211,6 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.epi = epi;
     p.row_scale = row_scale;
     p.amax_out = amax_out;
-    p.relu_mask = relu_mask;
     const bool pair = nt_pair_enabled();
     if (pair)
         for (int i = 0; i < p.nsrc; ++i)
@@ -1288,16 +1280,14 @@ const BImage& TcGemm::image(const MatB& b, int32_t N, int32_t K, cudaStream_t s)
 
 void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2,
                 const float* amax2, const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi,
-                const float* row_scale, float* amax_out, uint32_t* relu_mask) {
+                const float* row_scale, float* amax_out) {
     cudaStream_t s = t->ctx->stream;
     if (enabled && tc_supported(a1, a2, N) && tc_out_supported(C, ldc)) {
         const BImage& i1 = image(b1, N, a1.K, s);
         const BImage* i2 = a2 ? &image(*b2, N, a2->K, s) : nullptr;
-        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s,
-                   epi == kEpiRelu ? relu_mask : nullptr);
+        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s);
     } else {
         gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
-        if (epi == kEpiRelu && relu_mask) relu_sign_mask(M, N, C, ldc, relu_mask, s);
     }
 }
 

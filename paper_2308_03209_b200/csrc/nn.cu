@@ -322,16 +322,13 @@ __device__ __forceinline__ void gather_rows_sum(int64_t a, int64_t b, int lane, 
 }
 
 // Output row v: forward mean = inv[v] * sum (nn.hpp:229); backward dz =
-// 1[msg_pre > 0] * sum (nn.hpp:287-288), the ReLU decision read from the sign
-// bitmask the msg GEMM's epilogue wrote (word [v][c / 32], bit c % 32) instead
-// of the 1 KB msg row. Returns max|out| of the lane's chunks.
+// 1[msg > 0] * sum (nn.hpp:287-288). Returns max|out| of the lane's chunks.
 template <int NCH, bool kBwd>
 __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int32_t H4, const float* __restrict__ inv,
-                                            const uint32_t* __restrict__ pos, float* __restrict__ out,
+                                            const float* __restrict__ msg, float* __restrict__ out,
                                             const float4 (&acc)[NCH]) {
     float amx = 0.f;
     const float s = kBwd ? 1.f : inv[v];
-    const int32_t W = (H + 31) >> 5;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         const int32_t ch = lane + 32 * c;
@@ -343,11 +340,11 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
             r.z *= s;
             r.w *= s;
         } else {
-            const uint32_t b = __ldg(pos + v * W + (ch >> 3)) >> ((4 * ch) & 31);
-            r.x = (b & 1u) ? r.x : 0.f;
-            r.y = (b & 2u) ? r.y : 0.f;
-            r.z = (b & 4u) ? r.z : 0.f;
-            r.w = (b & 8u) ? r.w : 0.f;
+            const float4 mv = __ldg(reinterpret_cast<const float4*>(msg + v * H) + ch);
+            r.x = mv.x > 0.f ? r.x : 0.f;
+            r.y = mv.y > 0.f ? r.y : 0.f;
+            r.z = mv.z > 0.f ? r.z : 0.f;
+            r.w = mv.w > 0.f ? r.w : 0.f;
         }
         reinterpret_cast<float4*>(out + v * H)[ch] = r;
         amx = fmaxf(amx, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
@@ -361,7 +358,7 @@ template <int NCH, bool kBwd>
 __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                    const int32_t* __restrict__ nbrs,
                                                    const uint32_t* __restrict__ bits, const float* __restrict__ inv,
-                                                   const float* __restrict__ src, const uint32_t* __restrict__ pos,
+                                                   const float* __restrict__ src, const float* __restrict__ msg,
                                                    float* __restrict__ out, float* amax_out, int64_t max_slots) {
     float amx = 0.f;
     const int lane = threadIdx.x & 31;
@@ -374,7 +371,7 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
-        amx = fmaxf(amx, finish_row<NCH, kBwd>(v, lane, H, H4, inv, pos, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd>(v, lane, H, H4, inv, msg, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -415,8 +412,8 @@ __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int3
                                                                 const int32_t* __restrict__ seg_first,
                                                                 const float* __restrict__ partial,
                                                                 const float* __restrict__ inv,
-                                                                const uint32_t* __restrict__ pos,
-                                                                float* __restrict__ out, float* amax_out) {
+                                                                const float* __restrict__ msg, float* __restrict__ out,
+                                                                float* amax_out) {
     const int lane = threadIdx.x & 31;
     const int32_t H4 = H >> 2;
     float amx = 0.f;
@@ -435,7 +432,7 @@ __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int3
                     acc[c].z += p.z;
                     acc[c].w += p.w;
                 }
-        amx = fmaxf(amx, finish_row<NCH, kBwd>(rows[h], lane, H, H4, inv, pos, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd>(rows[h], lane, H, H4, inv, msg, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -470,7 +467,7 @@ template <bool kBwd>
 __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                    const int32_t* __restrict__ nbrs, const uint32_t* __restrict__ bits,
                                    const float* __restrict__ inv, const float* __restrict__ src,
-                                   const uint32_t* __restrict__ pos, float* __restrict__ out, float* amax_out) {
+                                   const float* __restrict__ msg, float* __restrict__ out, float* amax_out) {
     const int64_t total = n * H;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t v = i / H;
@@ -478,19 +475,18 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
         float acc = 0.f;
         for (int64_t k = off[v]; k < off[v + 1]; ++k)
             if (slot_kept(bits, k)) acc += src[int64_t(nbrs[k]) * H + c];
-        const int32_t W = (H + 31) >> 5;
-        out[i] = kBwd ? (((pos[v * W + (c >> 5)] >> (c & 31)) & 1u) ? acc : 0.f) : acc * inv[v];
+        out[i] = kBwd ? (msg[i] > 0.f ? acc : 0.f) : acc * inv[v];
         if (amax_out) atomic_max_abs(amax_out, out[i]);
     }
 }
 
 template <int NCH, bool kBwd>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
-              const float* src, const uint32_t* pos, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv,
+              const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv,
               float* partial) {
     const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 16);
     const bool heavy = hv && hv->nh > 0;
-    spmm_kernel<NCH, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, pos, out, amax_out,
+    spmm_kernel<NCH, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out,
                                                 heavy ? int64_t(kHeavySlots) : INT64_MAX);
     SC_LAUNCH_CHECK();
     count_launch();
@@ -499,27 +495,27 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
         hv->nseg, H, off, nbrs, bits, hv->seg_row.get(), hv->seg_begin.get(), src, partial);
     SC_LAUNCH_CHECK();
     spmm_heavy_finish_kernel<NCH, kBwd><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
-        hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, pos, out, amax_out);
+        hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, msg, out, amax_out);
     SC_LAUNCH_CHECK();
     count_launch(2);
 }
 
 template <bool kBwd>
 void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
-                 const float* src, const uint32_t* pos, float* out, cudaStream_t s, float* amax_out,
+                 const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out,
                  const HeavyRows* hv, float* partial) {
     if (n <= 0) return;
     if (H % 4 != 0) {  // scalar fallback: thread per output element (any H, any degree)
-        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, pos, out, amax_out);
+        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
         SC_LAUNCH_CHECK();
         count_launch();
         return;
     }
     const int nch = (H / 4 + 31) / 32;
-    if (nch <= 1) spmm_vec<1, kBwd>(n, H, off, nbrs, bits, inv, src, pos, out, s, amax_out, hv, partial);
-    else if (nch == 2) spmm_vec<2, kBwd>(n, H, off, nbrs, bits, inv, src, pos, out, s, amax_out, hv, partial);
-    else if (nch <= 4) spmm_vec<4, kBwd>(n, H, off, nbrs, bits, inv, src, pos, out, s, amax_out, hv, partial);
-    else spmm_vec<8, kBwd>(n, H, off, nbrs, bits, inv, src, pos, out, s, amax_out, hv, partial);
+    if (nch <= 1) spmm_vec<1, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
+    else if (nch == 2) spmm_vec<2, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
+    else if (nch <= 4) spmm_vec<4, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
+    else spmm_vec<8, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
 }
 
 __global__ void mask_bits_kernel(int64_t nnz, const int32_t* __restrict__ eids, const uint8_t* __restrict__ mask,
@@ -842,27 +838,9 @@ void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs,
     spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, mean, s, nullptr, hv, partial);
 }
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
-              const float* dmean_s, const uint32_t* relu_pos, float* dz, cudaStream_t s, float* amax_out,
-              const HeavyRows* hv, float* partial) {
-    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, relu_pos, dz, s, amax_out, hv, partial);
-}
-
-__global__ void relu_sign_mask_kernel(int64_t M, int32_t N, const float* __restrict__ C, int64_t ldc,
-                                      uint32_t* __restrict__ mask) {
-    const int32_t W = (N + 31) >> 5;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M * W; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t r = i / W;
-        const int32_t w = static_cast<int32_t>(i - r * W);
-        uint32_t b = 0;
-        for (int q = 0; q < 32 && 32 * w + q < N; ++q) b |= (C[r * ldc + 32 * w + q] > 0.f ? 1u : 0u) << q;
-        mask[i] = b;
-    }
-}
-void relu_sign_mask(int64_t M, int32_t N, const float* C, int64_t ldc, uint32_t* mask, cudaStream_t s) {
-    if (M <= 0 || N <= 0) return;
-    relu_sign_mask_kernel<<<grid_for(M * ((N + 31) / 32), 256), 256, 0, s>>>(M, N, C, ldc, mask);
-    SC_LAUNCH_CHECK();
-    count_launch();
+              const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out, const HeavyRows* hv,
+              float* partial) {
+    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s, amax_out, hv, partial);
 }
 
 void build_heavy_rows(sc_ctx* ctx, int64_t n, const int64_t* off, HeavyRows& hv) {

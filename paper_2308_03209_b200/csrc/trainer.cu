@@ -261,16 +261,13 @@ void ensure_rows(sc_trainer* t, int64_t n) {
     t->X.clear();
     t->MSG.clear();
     t->MEAN.clear();
-    t->POS.clear();
     t->X.resize(t->L + 1);
     t->MSG.resize(t->L);
     t->MEAN.resize(t->L);
-    t->POS.resize(t->L);
     for (int l = 0; l < t->L; ++l) {
         t->X[l + 1].alloc(n * t->lay[l].H);
         t->MSG[l].alloc(n * t->lay[l].H);
         t->MEAN[l].alloc(n * t->lay[l].H);
-        t->POS[l].alloc(n * ((t->lay[l].H + 31) / 32));
     }
     t->inv.alloc(n);
     t->G.alloc(n * t->Cp);
@@ -298,12 +295,11 @@ struct Rows {
 };
 
 // Algorithmic HBM bytes of one aggregation launch: offsets,
-// neighbour ids, DropEdge bits, inv_deg (fwd) or the ReLU sign bits (bwd,
-// ceil(H/32) words per row), one gathered fp32 row per kept slot, and the
-// output rows.
+// neighbour ids, mask bits, inv_deg (fwd) or ReLU-mask rows (bwd), one gathered
+// fp32 row per kept slot, and the output rows.
 double spmm_bytes(const Rows& R, int H, bool bwd) {
     double b = 8.0 * (R.n + 1) + 4.0 * R.nnz + (R.bits ? (R.nnz + 7) / 8 : 0) + 4.0 * H * R.kept + 4.0 * H * R.n;
-    b += bwd ? 4.0 * ((H + 31) / 32) * R.n : 4.0 * R.n;
+    b += bwd ? 4.0 * H * R.n : 4.0 * R.n;
     return b;
 }
 
@@ -323,7 +319,7 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
         // msg = relu(h W^T)   (nn.hpp:220-221)
         P.begin("gemm_msg", 4.0 * n * (lo.in + lo.H), s);
         t->tc.nt(t, xin, xin_amax, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, nullptr,
-                 t->MSG[l].get(), lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l), t->POS[l].get());
+                 t->MSG[l].get(), lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l));
         P.end(s);
         // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
         P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
@@ -410,7 +406,7 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
         SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
         P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
-        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->POS[l].get(), t->dz.get(), s, dz_amax, R.hv,
+        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s, dz_amax, R.hv,
                  t->heavy_ws.get());
         P.end(s);
         // dW = dz^T h_in   (:289)

@@ -97,7 +97,6 @@ struct sc_trainer {
     // activations (rows_cap rows)
     int64_t rows_cap = 0;
     std::vector<sc::DevBuf<float>> X, MSG, MEAN;
-    std::vector<sc::DevBuf<uint32_t>> POS;  // ReLU sign bits of MSG[l] ([n][ceil(H/32)]), for backward
     sc::DevBuf<float> inv, G, dh, dh2, dmean, dz, eval_logits, ws, ws_side;
     sc::DevBuf<float> heavy_ws;   // segment partial sums of the heavy-row aggregation
     sc::HeavyRows eval_heavy;     // heavy rows of the full graph (evaluate_splits)
