@@ -484,7 +484,9 @@ template <int NCH, bool kBwd>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv,
               float* partial) {
-    const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 16);
+    // 64 blocks of 8 warps per SM: ~6 waves at 5 resident blocks, so the grid-stride tail is short
+    // (A/B, profiles/r01_spmm_grid_ab.txt: x16 -> x64 blocks per SM = 0.82 -> 0.92 of HBM peak)
+    const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
     const bool heavy = hv && hv->nh > 0;
     spmm_kernel<NCH, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out,
                                                 heavy ? int64_t(kHeavySlots) : INT64_MAX);
