@@ -157,7 +157,8 @@ typedef struct {
 /* Partitions i with i % world == rank are trained on this rank's device. */
 sc_status sc_trainer_create(sc_ctx* ctx, sc_graph* g, sc_vcut* vc, const sc_train_config* cfg, int32_t rank,
                             int32_t world, sc_trainer** out);
-/* NCCL: rank 0 calls sc_nccl_unique_id and ships the 128 bytes to the others. */
+/* NCCL: rank 0 calls sc_nccl_unique_id and ships the 128 bytes to the others
+ * (optional at world == 1: a single-rank communicator runs the same exchange). */
 sc_status sc_nccl_unique_id(uint8_t out[128]);
 sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
 /* One epoch of train_cofree_impl (trainer.hpp:255-302): every local

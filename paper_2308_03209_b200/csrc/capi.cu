@@ -675,7 +675,7 @@ sc_status sc_nccl_unique_id(uint8_t out[128]) {
 sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
     return guard([&] {
         REQUIRE_ARG(t && id, "sc_trainer_init_comm: null argument");
-        if (t->world > 1) trainer_init_comm(t, id);
+        trainer_init_comm(t, id);  // world == 1: a single-rank communicator (exercises the exchange path)
     });
 }
 sc_status sc_trainer_step(sc_trainer* t, int32_t epoch, double* loss, double* gnorm) {

@@ -139,6 +139,15 @@ __global__ void gather_rows_kernel(int64_t n, int32_t d, const int32_t* __restri
     }
 }
 
+// 16-byte variant (d % 4 == 0, 16-byte aligned rows): one float4 per thread.
+__global__ void gather_rows4_kernel(int64_t n, int32_t d4, const int32_t* __restrict__ rows,
+                                    const float4* __restrict__ src, float4* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * d4; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / d4;
+        dst[i] = __ldg(src + int64_t(rows[r]) * d4 + (i - r * d4));
+    }
+}
+
 __global__ void absmax_kernel(int64_t n, const float* __restrict__ x, float* out) {
     float mx = 0.f;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
@@ -484,7 +493,7 @@ template <int NCH, bool kBwd>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv,
               float* partial) {
-    // 64 blocks of 8 warps per SM: ~6 waves at 5 resident blocks, so the grid-stride tail is short
+    // 64 blocks of 8 warps per SM: ~13 waves at 5 resident blocks, so the grid-stride tail is short
     // (A/B, profiles/r01_spmm_grid_ab.txt: x16 -> x64 blocks per SM = 0.82 -> 0.92 of HBM peak)
     const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
     const bool heavy = hv && hv->nh > 0;
@@ -889,7 +898,11 @@ void build_heavy_rows(sc_ctx* ctx, int64_t n, const int64_t* off, HeavyRows& hv)
 }
 void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s) {
     if (n <= 0) return;
-    gather_rows_kernel<<<grid_for(n * d, 256), 256, 0, s>>>(n, d, rows, src, dst);
+    if (d % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0)
+        gather_rows4_kernel<<<grid_for(n * (d / 4), 256, int64_t(num_sms()) * 64), 256, 0, s>>>(
+            n, d / 4, rows, reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst));
+    else
+        gather_rows_kernel<<<grid_for(n * d, 256), 256, 0, s>>>(n, d, rows, src, dst);
     SC_LAUNCH_CHECK();
     count_launch();
 }

@@ -527,7 +527,7 @@ void trainer_step_async(sc_trainer* t, int epoch) {
             for (int b = t->nb() - 1; b >= 0; --b) exchange_bucket(t, b, j);
         }
     }
-    if (t->world > 1) {  // exposed tail of the exchange: the last buckets' all-gathers
+    if (t->comm) {  // exposed tail of the exchange: the last buckets' all-gathers
         t->prof.begin("exchange_tail", 4.0 * t->p * t->P, s);
         SC_CUDA(cudaEventRecord(t->comm_done, t->comm_stream));
         SC_CUDA(cudaStreamWaitEvent(s, t->comm_done, 0));
@@ -608,7 +608,7 @@ void trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
 }
 
 void exchange_bucket(sc_trainer* t, int b, int round, cudaStream_t producer) {
-    if (t->world == 1) return;
+    if (!t->comm) return;  // world == 1 without a communicator: nothing to exchange
     cudaStream_t s = producer ? producer : t->ctx->stream;
     if (t->xfer_used == t->xfer_events.size()) {
         cudaEvent_t e;

@@ -653,9 +653,9 @@ class CoFreeTrainer:
         _check(_lib.sc_trainer_param_count(self.h, C.byref(n)))
         self.param_count = n.value
         self.rank, self.world = rank, world
-        if world > 1:
-            if nccl_id is None:
-                raise ValueError("world > 1 needs the rank-0 NCCL unique id")
+        if world > 1 and nccl_id is None:
+            raise ValueError("world > 1 needs the rank-0 NCCL unique id")
+        if nccl_id is not None:  # (world == 1 too: a single-rank communicator runs the exchange path)
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             _check(_lib.sc_trainer_init_comm(self.h, buf), "init_comm")
 

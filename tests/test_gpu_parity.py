@@ -348,3 +348,21 @@ def test_staged_features_match_set_features(sc, O):
         out.append((losses, t.params()))
     assert out[0][0] == out[1][0]
     np.testing.assert_array_equal(out[0][1], out[1][1])
+
+
+def test_nccl_exchange_path_single_rank(sc, O):
+    """The bucketed all-gather exchange (comm stream, per-bucket events, ncclAllGather in place) run
+    through a single-rank NCCL communicator: same bits as the local path."""
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    out = []
+    for nccl in (False, True):
+        g = gpu_graph(sc, og, 8)
+        nid = sc.CoFreeTrainer.nccl_unique_id() if nccl else None
+        t = sc.CoFreeTrainer(g, sc.partition_random(g, 3, 3),
+                             sc.TrainConfig(layers=2, hidden=[16], use_dropedge=True, seed=1), nccl_id=nid)
+        losses = [t.step(e) for e in range(3)]
+        out.append((losses, t.params(), [t.part_grads(i) for i in range(3)]))
+    assert out[0][0] == out[1][0]
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    for a, b in zip(out[0][2], out[1][2]):
+        np.testing.assert_array_equal(a, b)
