@@ -436,4 +436,17 @@ inline TrainResult train_cofree(const Graph& g, const VertexCutPartition& part, 
     return res;
 }
 
+// train_full_graph (trainer.hpp:164-200): the p = 1 vertex cut (every edge in part 0, local ids =
+// global ids) trained with unit loss weights and no DropEdge — the reference's degeneracy
+// (test_trainer.cpp:69-79) — on the same device trainer.
+inline TrainResult train_full_graph(const Graph& g, const TrainConfig& c) {
+    const VertexCutPartition part = build_vertex_cut(g, 1, std::vector<int>(g.num_edges(), 0));
+    TrainConfig fc = c;
+    fc.reweight = ReweightScheme::none;
+    fc.use_dropedge = false;
+    TrainResult r = train_cofree(g, part, fc);
+    for (auto& m : r.metrics) m.comm_floats = 0;
+    return r;
+}
+
 }  // namespace sagecut_b200

@@ -623,6 +623,23 @@ double ref_trainer_time_part_step(void* t, int i, int epoch, int reps) {
 
 // The reference's own end-to-end entry point (trainer.cpp:119), for
 // cross-checking the step-wise harness above.
+// the reference's train_full_graph (trainer.cpp:114-117 -> trainer.hpp:164-200)
+int ref_train_full_graph(void* gp, const int* hidden, int layers, double lr, int loss, std::uint64_t seed, int f32,
+                         int epochs, double* final_params, double* losses, double* gnorms, double* metrics) {
+    return guard([&] {
+        const auto cfg = make_config(hidden, layers, lr, loss, 0, 0, 10, 0.5, seed, f32, 1, epochs);
+        const auto res = train_full_graph(*static_cast<Graph*>(gp), cfg);
+        flatten(res.model, final_params);
+        for (std::size_t e = 0; e < res.metrics.size(); ++e) {
+            losses[e] = res.metrics[e].train_loss;
+            gnorms[e] = res.metrics[e].grad_norm;
+            metrics[3 * e] = res.metrics[e].train_metric;
+            metrics[3 * e + 1] = res.metrics[e].val_metric;
+            metrics[3 * e + 2] = res.metrics[e].test_metric;
+        }
+    });
+}
+
 int ref_train_cofree(void* gp, void* pp, const int* hidden, int layers, double lr, int loss, int reweight,
                      int use_dropedge, int k, double ratio, std::uint64_t seed, int f32, int workers, int epochs,
                      double* final_params, double* losses, double* gnorms, double* metrics /* epochs x 3 */) {

@@ -767,6 +767,19 @@ class TrainResult:  # trainer.hpp:71-75
     metrics: List[EpochMetrics]
 
 
+def train_full_graph(g: Graph, config: TrainConfig, evaluate: bool = True) -> TrainResult:
+    """train_full_graph (trainer.hpp:164-200): the whole graph as one partition — every edge in
+    part 0, local ids = global ids, unit loss weights on the train mask, no DropEdge — through the
+    same device trainer (the reference's p = 1 degeneracy, test_trainer.cpp:69-79)."""
+    from dataclasses import replace
+    part = build_vertex_cut(g, 1, np.zeros(g.num_edges(), np.int32))
+    cfg = replace(config, reweight="none", use_dropedge=False)
+    res = train_cofree(g, part, cfg, evaluate)
+    for m in res.metrics:
+        m.comm_floats = 0  # nothing is exchanged (trainer.hpp:197)
+    return res
+
+
 def train_cofree(g: Graph, part: VertexCutPartition, config: TrainConfig, evaluate: bool = True) -> TrainResult:
     """train_cofree (trainer.cpp:119 / trainer.hpp:202-313): per-epoch step, Adam,
     and (like the reference) a full-graph evaluation after every epoch."""

@@ -8,6 +8,8 @@ relative in fp32 over 5 training steps. "Relative" here is
     |loss_gpu - loss_ref| / |loss_ref|  <= 1e-5
 with the oracle in the reference's f32 mode as x_ref.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -366,3 +368,31 @@ def test_nccl_exchange_path_single_rank(sc, O):
     np.testing.assert_array_equal(out[0][1], out[1][1])
     for a, b in zip(out[0][2], out[1][2]):
         np.testing.assert_array_equal(a, b)
+
+
+def test_train_full_graph_matches_reference(sc):
+    """train_full_graph (trainer.hpp:164-200) against the reference's own, 5 epochs in f32."""
+    import ctypes as C
+    from cpu_libs import REF_SO, reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    R = reference()
+    rg = R.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    O = oracle()
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    g = gpu_graph(sc, og, 8)
+    hidden = np.array([16, 16], np.int32)
+    epochs = 5
+    P = len(R.init_params(8, [16, 16], 4, 1, f32=True))
+    theta, L, G, M = np.zeros(P), np.zeros(epochs), np.zeros(epochs), np.zeros(3 * epochs)
+    fn = R.lib.ref_train_full_graph
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_int, C.c_int] + [C.c_void_p] * 4
+    assert fn(rg.h, hidden.ctypes.data, 2, 0.01, 0, 1, 1, epochs, theta.ctypes.data, L.ctypes.data, G.ctypes.data,
+              M.ctypes.data) == 0
+    res = sc.train_full_graph(g, sc.TrainConfig(layers=2, hidden=[16, 16], learning_rate=0.01, seed=1,
+                                                epochs=epochs, use_dropedge=True))  # DropEdge is ignored, as in the reference
+    np.testing.assert_allclose([m.train_loss for m in res.metrics], L, rtol=1e-5)
+    assert rel(res.model, theta) <= REL
+    np.testing.assert_allclose([[m.train_metric, m.val_metric, m.test_metric] for m in res.metrics],
+                               M.reshape(epochs, 3), atol=0.02)
+    assert all(m.comm_floats == 0 for m in res.metrics)
