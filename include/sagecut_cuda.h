@@ -149,8 +149,10 @@ typedef struct {
     int32_t dropedge_k;
     double drop_ratio;
     uint64_t seed;
-    int32_t deterministic;   /* 1: ascending-partition gradient sum (bitwise
-                                invariant to GPU count); 0: local sum + allreduce */
+    int32_t deterministic;   /* accepted for API compatibility: the exchange all-gathers
+                                per-partition slots and sums them in ascending partition
+                                order, which is always bitwise invariant to the GPU count
+                                and costs the same bytes as a reduction at p = world */
     int32_t gemm;            /* 0: auto (tcgen05 where shapes allow), 1: SIMT fp32 only */
 } sc_train_config;
 
