@@ -330,6 +330,21 @@ __device__ __forceinline__ void mma_f16_g(uint32_t d_tmem, uint64_t a, uint64_t 
     else
         mma_f16(d_tmem, a, b, idesc, acc);
 }
+// A operand from TMEM (K-major: lane = M row, K packed two fp16 per 32-bit column), B from smem.
+__device__ __forceinline__ void mma_f16_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                                uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // MMA completion -> barrier at the same offset in both CTAs of the pair (or the local one).
 template <bool PAIR>
 __device__ __forceinline__ void mma_commit_g(uint64_t* bar) {
@@ -711,6 +726,10 @@ __host__ __device__ constexpr uint32_t idesc_f16_mn(int M, int N) {
     return (1u << 4) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
            (static_cast<uint32_t>(M >> 4) << 24);
 }
+// Same with A K-major (A read from TMEM), B MN-major.
+__host__ __device__ constexpr uint32_t idesc_f16_at(int M, int N) {
+    return (1u << 4) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
 // Byte offset of the 16-byte chunk (8 consecutive mn at one k) in an MN-major
 // SW128 tile of 32 k rows laid out [mn_atom][k_atom(4)][8 k rows][128 B].
 constexpr uint32_t kTnLbo = 4 * 1024;  // MN atom stride
@@ -723,13 +742,22 @@ __device__ __forceinline__ uint32_t mn_off(uint32_t mn, uint32_t k) {
 // 256-column slice of A' (M = 256, 128 per CTA) and splits the B' tile's columns
 // between its two CTAs, so each B' element is converted once per pair instead
 // of once per 128-column A' tile, and per-SM conversion work drops by a third.
-template <bool PAIR>
+// AT (pairs only): the A' operand lives in TMEM instead of shared memory. The
+// converters write its fp16 hi / lo halves with tcgen05.st (TMEM lane = A'
+// column = output row) and the MMAs read A from TMEM, which removes the A'
+// fp16 stores and two thirds of the MMA operand reads from the SM's shared-
+// memory bandwidth (the TN kernel's limit). TMEM then holds one 256-column
+// accumulator plus kStages 32-column A' stages (hi 16 + lo 16), so the
+// accumulator is single-buffered: the MMAs wait for each 1024-row drain.
+template <bool PAIR, bool AT = false>
 struct TnCfg {
-    static constexpr int kStages = PAIR ? 3 : 2;
+    static constexpr int kStages = AT ? 6 : (PAIR ? 3 : 2);
     static constexpr int kStg = PAIR ? 3 : 2;
+    static constexpr int kAcc = AT ? 1 : 2;                  // TMEM accumulators
+    static constexpr int kChunk = AT ? 2 * kChunkKb : kChunkKb;  // k-blocks per accumulation
     static constexpr int kBLoc = PAIR ? kMaxN / 2 : kMaxN;  // B' columns held per CTA
     static constexpr int kBTile = kBLoc * kTnBK * 2;        // one (hi or lo) B' tile
-    static constexpr int kStage = 2 * kTnATile + 2 * kBTile;
+    static constexpr int kStage = (AT ? 0 : 2 * kTnATile) + 2 * kBTile;  // smem per stage
     static constexpr int kStgB = kTnBK * kBLoc * 4;
     static constexpr int kStgSlot = kTnStgA + kStgB;
     static constexpr int kStgOff = kStages * kStage;
@@ -739,10 +767,12 @@ struct TnCfg {
     static constexpr int kACols = PAIR ? 2 * kBM : kBM;      // A' columns per tile
 };
 static_assert(TnCfg<true>::kSmem <= 232448 && TnCfg<false>::kSmem <= 232448, "TN shared memory");
+static_assert(TnCfg<true, true>::kSmem <= 232448 && 256 + 32 * TnCfg<true, true>::kStages <= 512, "TN (A in TMEM)");
 
-template <bool PAIR>
+template <bool PAIR, bool AT = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
-    using Cfg = TnCfg<PAIR>;
+    static_assert(!AT || PAIR, "A in TMEM needs the CTA-pair layout");
+    using Cfg = TnCfg<PAIR, AT>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stg_base = smem + Cfg::kStgOff;  // kStg x [A' rows | B' rows]
@@ -772,8 +802,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     const int64_t r0 = int64_t(split) * p.rows_per_split;
     const int64_t r1 = min(p.M, r0 + p.rows_per_split);
     const int kblocks = r1 > r0 ? static_cast<int>((r1 - r0 + kTnBK - 1) / kTnBK) : 0;
-    const int nchunks = (kblocks + kChunkKb - 1) / kChunkKb;
+    const int nchunks = (kblocks + Cfg::kChunk - 1) / Cfg::kChunk;
 
+    constexpr int kBOff = AT ? 0 : 2 * kTnATile;  // B' hi / lo tiles within a stage
     const int ka = scale_exp(*p.amax_a);
     int kbx = scale_exp(*p.b[0].amax);
     if (p.nb > 1) kbx = min(kbx, scale_exp(*p.b[1].amax));
@@ -788,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 mbar_init(&sfull[s], 1);
                 mbar_init(&sempty[s], kConvWarps);
             }
-            for (int s = 0; s < 2; ++s) {
+            for (int s = 0; s < Cfg::kAcc; ++s) {
                 mbar_init(&tfull[s], 1);
                 mbar_init(&tempty[s], 4 * (PAIR ? 2 : 1));
             }
@@ -851,12 +882,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 x1 = *reinterpret_cast<const float4*>(rowp + (((2 * (ch & 3) + 1) ^ (kr & 7)) << 4));
                 if (valid < 8) mask8(x0, x1, valid);
             };
+            if constexpr (AT) {
+                // A' -> TMEM: warp w owns TMEM lane quarter w & 3 (A' columns 32q .. 32q+31, one per
+                // lane) and k rows 16 (w >> 2) .. +15 of the stage. Column-wise reads of the row-major
+                // staging are conflict-free (one 128 B row per instruction, swizzled chunks).
+                const int q = warp & 3, kh = warp >> 2;
+                const int m = 32 * q + lane;
+                const uint8_t* box = sga + q * kTnBox + (((lane & 3)) << 2);
+                float x[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int kr = 16 * kh + i;
+                    const float v = *reinterpret_cast<const float*>(box + kr * 128 + ((((lane >> 2) ^ (kr & 7))) << 4));
+                    x[i] = (whole || (kr < rows_ok && m < na)) ? v : 0.f;
+                }
+                uint32_t hi[8], lo[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) split2(x[2 * j], x[2 * j + 1], sa_, hi[j], lo[j]);
+                const uint32_t tcol = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + 256 + mr.idx * 32 + 8 * kh;
+                tmem_st8(tcol, hi);
+                tmem_st8(tcol + 16, lo);
+            }
             if (whole) {
                 // all of the stage's shared loads first (up to 8 x LDS.128 in flight), then convert
                 constexpr int kJB = Cfg::kBLoc / 64;
                 float4 xa[2][2], xb[kJB][2];
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
+                    if constexpr (AT) break;
                     const int idx = tid + j * kConv;
                     load8(sga, idx & 31, idx >> 5, 8, xa[j][0], xa[j][1]);
                 }
@@ -867,6 +920,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 }
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
+                    if constexpr (AT) break;
                     const int idx = tid + j * kConv;
                     split8_store(xa[j][0], xa[j][1], sa_, st, st + kTnATile, mn_off((idx >> 5) * 8, idx & 31));
                 }
@@ -875,12 +929,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                     const int idx = tid + j * kConv;
                     const int kr = idx & 31, ch = idx >> 5;
                     if (ch < bch)
-                        split8_store(xb[j][0], xb[j][1], sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile,
+                        split8_store(xb[j][0], xb[j][1], sb_, st + kBOff, st + kBOff + Cfg::kBTile,
                                      mn_off(ch * 8, kr));
                 }
             } else {
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
+                    if constexpr (AT) break;
                     const int idx = tid + j * kConv;
                     const int kr = idx & 31, ch = idx >> 5;
                     float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
@@ -896,8 +951,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                     float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
                     const int valid = kr < rows_ok ? min(8, nbl - ch * 8) : 0;
                     if (valid > 0) load8(sgb, kr, ch, valid, x0, x1);
-                    split8_store(x0, x1, sb_, st + 2 * kTnATile, st + 2 * kTnATile + Cfg::kBTile, mn_off(ch * 8, kr));
+                    split8_store(x0, x1, sb_, st + kBOff, st + kBOff + Cfg::kBTile, mn_off(ch * 8, kr));
                 }
+            }
+            if constexpr (AT) {
+                tmem_wait_st();   // the A' stage is in TMEM
+                tc_fence_before();
             }
             fence_proxy_async();
             __syncwarp();
@@ -910,32 +969,39 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer (the pair's leader only) =================
         if (!PAIR || rank == 0) {
-            const uint32_t idesc = idesc_f16_mn(Cfg::kACols, nb_pad);
+            const uint32_t idesc = AT ? idesc_f16_at(Cfg::kACols, nb_pad) : idesc_f16_mn(Cfg::kACols, nb_pad);
             Ring mr;
             for (int chunk = 0; chunk < nchunks; ++chunk) {
-                const uint32_t acc = chunk & 1;
+                const uint32_t acc = chunk % Cfg::kAcc;
                 const uint32_t d_tmem = tmem_base + acc * 256;
-                mbar_wait(&tempty[acc], ((chunk >> 1) & 1) ^ 1);
+                mbar_wait(&tempty[acc], ((chunk / Cfg::kAcc) & 1) ^ 1);
                 tc_fence_after();
-                const int kb_end = min(kblocks, (chunk + 1) * kChunkKb);
-                for (int kb = chunk * kChunkKb; kb < kb_end; ++kb, mr.next(Cfg::kStages)) {
+                const int kb_end = min(kblocks, (chunk + 1) * Cfg::kChunk);
+                for (int kb = chunk * Cfg::kChunk; kb < kb_end; ++kb, mr.next(Cfg::kStages)) {
                     mbar_wait(&full[mr.idx], mr.phase);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint8_t* st = smem + mr.idx * Cfg::kStage;
                         const uint32_t ahi = smem_u32(st), alo = smem_u32(st + kTnATile);
-                        const uint32_t bhi = smem_u32(st + 2 * kTnATile), blo = smem_u32(st + 2 * kTnATile + Cfg::kBTile);
+                        const uint32_t bhi = smem_u32(st + kBOff), blo = smem_u32(st + kBOff + Cfg::kBTile);
 #pragma unroll
                         for (int k = 0; k < kTnBK / 16; ++k) {
                             const uint32_t adv = k * 2 * kTnSbo;  // 16 rows = 2 K groups
-                            const uint64_t dah = desc_mn_sw128(ahi + adv, kTnLbo, kTnSbo);
-                            const uint64_t dal = desc_mn_sw128(alo + adv, kTnLbo, kTnSbo);
                             const uint64_t dbh = desc_mn_sw128(bhi + adv, kTnLbo, kTnSbo);
                             const uint64_t dbl = desc_mn_sw128(blo + adv, kTnLbo, kTnSbo);
-                            const uint32_t first = (kb == chunk * kChunkKb && k == 0) ? 0u : 1u;
-                            mma_f16_g<PAIR>(d_tmem, dah, dbh, idesc, first);
-                            mma_f16_g<PAIR>(d_tmem, dah, dbl, idesc, 1u);
-                            mma_f16_g<PAIR>(d_tmem, dal, dbh, idesc, 1u);
+                            const uint32_t first = (kb == chunk * Cfg::kChunk && k == 0) ? 0u : 1u;
+                            if constexpr (AT) {  // 16 k = 8 TMEM columns; lo plane 16 columns after hi
+                                const uint32_t tah = tmem_base + 256 + mr.idx * 32 + k * 8;
+                                mma_f16_ts_pair(d_tmem, tah, dbh, idesc, first);
+                                mma_f16_ts_pair(d_tmem, tah, dbl, idesc, 1u);
+                                mma_f16_ts_pair(d_tmem, tah + 16, dbh, idesc, 1u);
+                            } else {
+                                const uint64_t dah = desc_mn_sw128(ahi + adv, kTnLbo, kTnSbo);
+                                const uint64_t dal = desc_mn_sw128(alo + adv, kTnLbo, kTnSbo);
+                                mma_f16_g<PAIR>(d_tmem, dah, dbh, idesc, first);
+                                mma_f16_g<PAIR>(d_tmem, dah, dbl, idesc, 1u);
+                                mma_f16_g<PAIR>(d_tmem, dal, dbh, idesc, 1u);
+                            }
                         }
                         mma_commit_g<PAIR>(&empty[mr.idx]);
                         if (kb == kb_end - 1) mma_commit_g<PAIR>(&tfull[acc]);
@@ -959,8 +1025,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         const bool vec = (p.N2 & 3) == 0;  // 16-byte aligned partial rows
         const uint64_t pol_ws = l2_evict_last();  // the partials stay in L2 while operands stream past
         for (int chunk = 0; chunk < nchunks; ++chunk) {
-            const uint32_t acc = chunk & 1;
-            mbar_wait(&tfull[acc], (chunk >> 1) & 1);
+            const uint32_t acc = chunk % Cfg::kAcc;
+            mbar_wait(&tfull[acc], (chunk / Cfg::kAcc) & 1);
             tc_fence_after();
             for (int c0 = 0; c0 < nb_pad; c0 += 32) {
                 uint32_t r[32];
@@ -1135,8 +1201,13 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
         }
         SC_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
     };
-    if (pair) launch(tc::gemm_tn_f16x3_kernel<true>, tc::TnCfg<true>::kSmem);
-    else launch(tc::gemm_tn_f16x3_kernel<false>, tc::TnCfg<false>::kSmem);
+    static const bool a_tmem = [] {
+        const char* e = std::getenv("SC_TN_ATMEM");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    if (pair && a_tmem) launch(tc::gemm_tn_f16x3_kernel<true, true>, tc::TnCfg<true, true>::kSmem);
+    else if (pair) launch(tc::gemm_tn_f16x3_kernel<true, false>, tc::TnCfg<true, false>::kSmem);
+    else launch(tc::gemm_tn_f16x3_kernel<false, false>, tc::TnCfg<false, false>::kSmem);
     SC_LAUNCH_CHECK();
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();
