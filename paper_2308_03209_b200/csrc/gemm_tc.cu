@@ -762,7 +762,8 @@ struct TnCfg {
     static constexpr int kStgSlot = kTnStgA + kStgB;
     static constexpr int kStgOff = kStages * kStage;
     static constexpr int kEpiOff = kStgOff + kStg * kStgSlot;
-    static constexpr int kBarOff = kEpiOff;
+    static constexpr int kEpiPitch = 33;                     // drain transpose tile: 32 x 33 floats per warp
+    static constexpr int kBarOff = kEpiOff + 4 * 32 * kEpiPitch * 4;
     static constexpr int kSmem = kBarOff + 256 + 1024;
     static constexpr int kACols = PAIR ? 2 * kBM : kBM;      // A' columns per tile
 };
@@ -1024,6 +1025,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
         float* orow = outw + int64_t(lane) * p.N2;
         const bool vec = (p.N2 & 3) == 0;  // 16-byte aligned partial rows
         const uint64_t pol_ws = l2_evict_last();  // the partials stay in L2 while operands stream past
+        float* tbuf = reinterpret_cast<float*>(smem + Cfg::kEpiOff) + ew * 32 * Cfg::kEpiPitch;
         for (int chunk = 0; chunk < nchunks; ++chunk) {
             const uint32_t acc = chunk % Cfg::kAcc;
             mbar_wait(&tfull[acc], (chunk / Cfg::kAcc) & 1);
@@ -1031,17 +1033,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
             for (int c0 = 0; c0 < nb_pad; c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
-                if (lane >= rows_here || c0 >= nb) continue;
-                float* o = orow + c0;
+                if (c0 >= nb) continue;  // warp-uniform
                 if (vec && c0 + 32 <= nb) {
+                    // Transpose the warp's 32 x 32 block through shared memory so each vector
+                    // reduction covers 4 row segments of 128 contiguous bytes instead of 32
+                    // scattered 16-byte pieces (8x fewer L2 transactions per drain).
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float x0 = __uint_as_float(r[4 * j]) * unscale, x1 = __uint_as_float(r[4 * j + 1]) * unscale;
-                        const float x2 = __uint_as_float(r[4 * j + 2]) * unscale, x3 = __uint_as_float(r[4 * j + 3]) * unscale;
-                        if (chunk == 0) st_v4_l2hint(o + 4 * j, x0, x1, x2, x3, pol_ws);
-                        else red_add_v4_l2hint(o + 4 * j, x0, x1, x2, x3, pol_ws);
+                    for (int q = 0; q < 32; ++q) tbuf[lane * Cfg::kEpiPitch + q] = __uint_as_float(r[q]) * unscale;
+                    __syncwarp();
+#pragma unroll
+                    for (int rr = 0; rr < 8; ++rr) {
+                        const int row = 4 * rr + (lane >> 3), c = (lane & 7) * 4;
+                        const float* t = tbuf + row * Cfg::kEpiPitch + c;
+                        float* o = outw + int64_t(row) * p.N2 + c0 + c;
+                        if (row < rows_here) {
+                            if (chunk == 0) st_v4_l2hint(o, t[0], t[1], t[2], t[3], pol_ws);
+                            else red_add_v4_l2hint(o, t[0], t[1], t[2], t[3], pol_ws);
+                        }
                     }
-                } else {
+                    __syncwarp();
+                } else if (lane < rows_here) {
+                    float* o = orow + c0;
                     const int nv = min(32, nb - c0);
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
