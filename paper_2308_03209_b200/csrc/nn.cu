@@ -896,8 +896,25 @@ void build_heavy_rows(sc_ctx* ctx, int64_t n, const int64_t* off, HeavyRows& hv)
     hv.nh = nh;
     hv.nseg = total;
 }
-void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s) {
+__global__ void gather_rows_pad_kernel(int64_t n, int32_t d, int32_t dp, const int32_t* __restrict__ rows,
+                                       const float* __restrict__ src, float* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * dp; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / dp;
+        const int32_t c = static_cast<int32_t>(i - r * dp);
+        dst[i] = c < d ? __ldg(src + int64_t(rows[r]) * d + c) : 0.f;
+    }
+}
+
+void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s,
+                 int32_t dst_ld) {
     if (n <= 0) return;
+    if (dst_ld > d) {  // padded destination rows (zeros beyond d)
+        gather_rows_pad_kernel<<<grid_for(n * dst_ld, 256, int64_t(num_sms()) * 64), 256, 0, s>>>(n, d, dst_ld, rows,
+                                                                                                   src, dst);
+        SC_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
     if (d % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0)
         gather_rows4_kernel<<<grid_for(n * (d / 4), 256, int64_t(num_sms()) * 64), 256, 0, s>>>(
             n, d / 4, rows, reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst));

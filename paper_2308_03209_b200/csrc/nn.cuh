@@ -44,8 +44,9 @@ enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2 };
 void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
              int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out = nullptr);
 
-// dst[j] = src[rows[j]] for n rows of width d (row-major).
-void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s);
+// dst[r][:] = src[rows[r]][:] (n x d); dst_ld > d pads each destination row with zeros.
+void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s,
+                 int32_t dst_ld = 0);
 
 // *out = max(*out, max |x[0..n)|) (non-negative floats compare like their bit patterns).
 void absmax(int64_t n, const float* x, float* out, cudaStream_t s);

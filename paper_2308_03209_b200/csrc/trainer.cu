@@ -113,6 +113,7 @@ void trainer_init(sc_trainer* t) {
     cudaStream_t s = t->ctx->stream;
     t->normalizer = static_cast<double>(g->train_count);
     t->d = g->dim;
+    t->dp = (t->d + 3) / 4 * 4;
     t->C = g->num_classes;
     t->Cp = (t->C + 3) / 4 * 4;  // logits / dlogits row stride: 16-byte rows for the tensor-core kernels
     t->p = vc->p;
@@ -181,7 +182,7 @@ void trainer_init(sc_trainer* t) {
         absmax(st.n, st.scale.get(), st.g_amax.get(), s);
         st.logits.alloc(std::max<int64_t>(st.n * t->Cp, 1));
         build_heavy_rows(t->ctx, st.n, pd.offsets.get(), st.heavy);
-        st.x0.alloc(std::max<int64_t>(st.n * t->d, 1));
+        st.x0.alloc(std::max<int64_t>(st.n * t->dp, 1));
         if (t->use_dropedge) {
             st.words = (st.nnz + 31) / 32;
             st.bits.alloc(std::max<int64_t>(st.words * t->K, 1));
@@ -290,7 +291,8 @@ struct Rows {
     int64_t nnz;           // CSR slots
     int64_t kept;          // CSR slots kept by the selected DropEdge mask
     const float* g_amax;   // bound on max|dloss/dlogits| (= max loss scale)
-    const float* x0;       // layer-0 input rows (contiguous n x d; the partition's gathered features)
+    const float* x0;       // layer-0 input rows (the partition's gathered features)
+    int64_t x0_ld;         // their pitch (dp for gathered rows: zero-padded to 16 bytes)
     const HeavyRows* hv;   // hub rows (segmented aggregation)
 };
 
@@ -311,7 +313,7 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
     P.begin("inv_degree", double(n) * 12 + double(R.offsets ? 8 : 0) * n, s);
     inv_degree(n, R.offsets, R.bits, t->inv.get(), s);
     P.end(s);
-    const MatA x0{R.x0, t->d, nullptr, t->d};
+    const MatA x0{R.x0, R.x0_ld, nullptr, t->d};
     for (int l = 0; l < t->L; ++l) {
         const LayerOff& lo = t->lay[l];
         const MatA xin = l == 0 ? x0 : MatA{t->X[l].get(), lo.in, nullptr, lo.in};
@@ -360,7 +362,7 @@ void backward(sc_trainer* t, const Rows& R, int i) {
     };
     Profiler& P = t->prof;
     const int64_t n = R.n;
-    const MatT x0t{R.x0, t->d, nullptr, t->d};
+    const MatT x0t{R.x0, R.x0_ld, nullptr, t->d};
     const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L].get(), t->E, nullptr, t->E};
     // head grad = G^T emb (side) ; dh = G head (main)   (:259-260)
     hand_off(s, w);
@@ -447,12 +449,12 @@ void run_partition(sc_trainer* t, int i, int epoch) {
         bits ? 2 * static_cast<int64_t>(std::ceil((1.0 - t->ratio) * static_cast<double>(pd.m_local))) : st.nnz;
     if (st.x0_version != t->g->feat_version) {  // the partition's feature rows, contiguous (train_cofree :225-227)
         t->prof.begin("gather_x0", 8.0 * st.n * t->d, s);
-        gather_rows(st.n, t->d, pd.nodes.get(), t->g->features.get(), st.x0.get(), s);
+        gather_rows(st.n, t->d, pd.nodes.get(), t->g->features.get(), st.x0.get(), s, t->dp);
         t->prof.end(s);
         st.x0_version = t->g->feat_version;
     }
     const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get(),
-                 st.x0.get(), &st.heavy};
+                 st.x0.get(), t->dp, &st.heavy};
     SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
     forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
@@ -578,7 +580,7 @@ void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
         if (size_t(t->eval_heavy.nseg) * maxH > t->heavy_ws.size()) t->heavy_ws.alloc(size_t(t->eval_heavy.nseg) * maxH);
     }
     const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr,
-                 g->features.get(), &t->eval_heavy};
+                 g->features.get(), g->dim, &t->eval_heavy};
     const bool was = t->prof.enabled;
     t->prof.enabled = false;
     forward(t, R, t->eval_logits.get());

@@ -73,6 +73,7 @@ struct sc_trainer {
     int deterministic = 1, gemm_mode = 0;
     // dims
     int d = 0, C = 0, Cp = 0, E = 0, p = 0;
+    int dp = 0;  // x0 row pitch: d rounded up to 4 floats (16-byte rows for the TMA-fed GEMMs)
     std::vector<sc::LayerOff> lay;
     int64_t head_off = 0, P = 0;
     double normalizer = 1.0;

@@ -396,3 +396,22 @@ def test_train_full_graph_matches_reference(sc):
     np.testing.assert_allclose([[m.train_metric, m.val_metric, m.test_metric] for m in res.metrics],
                                M.reshape(epochs, 3), atol=0.02)
     assert all(m.comm_floats == 0 for m in res.metrics)
+
+
+@pytest.mark.parametrize("d", [37, 602])
+def test_unaligned_feature_width(sc, O, d):
+    """d % 4 != 0 (Reddit's 602): the partitions' layer-0 rows are gathered into 16-byte padded
+    rows so the layer-0 GEMMs stay on the tensor-core path; 5 steps against the oracle."""
+    rng = np.random.default_rng(d)
+    n = 2000
+    og = O.graph_build(n, rng.integers(0, n, size=(16000, 2), dtype=np.int32))
+    C = 5
+    lab = rng.integers(0, C, size=n).astype(np.int32)
+    f = rng.standard_normal((n, d)).astype(np.float32)
+    f[np.arange(n), lab] += 1.0
+    tr = (rng.random(n) < 0.6).astype(np.uint8)
+    va = ((1 - tr) * (rng.random(n) < 0.5)).astype(np.uint8)
+    te = (1 - tr - va).astype(np.uint8)
+    og.set_data(f, lab, C, tr, va, te)
+    worst, t, to = run_traj(sc, O, og, "random", 4, 1, d, hidden=[32, 32], dropedge=True, seed=2)
+    assert_within(worst)
