@@ -401,7 +401,10 @@ def test_train_full_graph_matches_reference(sc):
 @pytest.mark.parametrize("d", [37, 602])
 def test_unaligned_feature_width(sc, O, d):
     """d % 4 != 0 (Reddit's 602): the partitions' layer-0 rows are gathered into 16-byte padded
-    rows so the layer-0 GEMMs stay on the tensor-core path; 5 steps against the oracle."""
+    rows so the layer-0 GEMMs stay on the tensor-core path. Teacher-forced (the GPU trainer takes
+    the oracle's parameters before each step): with hundreds of near-zero-gradient weights on the
+    noise features, Adam's first steps move every parameter by ~lr * sign(g), so free-running
+    trajectories of any two non-bitwise implementations drift apart by O(lr) on a few of them."""
     rng = np.random.default_rng(d)
     n = 2000
     og = O.graph_build(n, rng.integers(0, n, size=(16000, 2), dtype=np.int32))
@@ -413,5 +416,16 @@ def test_unaligned_feature_width(sc, O, d):
     va = ((1 - tr) * (rng.random(n) < 0.5)).astype(np.uint8)
     te = (1 - tr - va).astype(np.uint8)
     og.set_data(f, lab, C, tr, va, te)
-    worst, t, to = run_traj(sc, O, og, "random", 4, 1, d, hidden=[32, 32], dropedge=True, seed=2)
-    assert_within(worst)
+    g = gpu_graph(sc, og, d)
+    t = sc.CoFreeTrainer(g, sc.partition_random(g, 4, 1), sc.TrainConfig(layers=2, hidden=[32, 32],
+                                                                          use_dropedge=True, seed=2))
+    to = og.partition("random", 4, 1).trainer([32, 32], lr=0.01, dropedge=True, seed=2, f32=True)
+    for e in range(3):
+        t.set_params(to.params().astype(np.float32))
+        loss, _ = t.step(e)
+        ol, _ = to.step(e)
+        assert abs(loss - ol) <= 1e-5 * abs(ol), (e, loss, ol)
+        lg = np.concatenate([t.part_logits(i).ravel() for i in range(4)])
+        olg = np.concatenate([to.part_logits(i, C).ravel() for i in range(4)])
+        assert rel(lg, olg) <= REL, (e, rel(lg, olg))
+        assert rel(t.grads(), to.gathered()) <= REL, (e, rel(t.grads(), to.gathered()))
