@@ -187,6 +187,16 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def measured_tensor_peak():
+    """Sustained dense bf16 TF/s (a GEMM timed inside a long step), per the profiling recipe."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p.get("bf16_tflops_sustained") or p["bf16_tflops"]), "measured (sustained)"
+    except Exception:
+        return 2250.0, "fallback (nominal dense bf16)"
+
+
 def ncu_traffic(name):
     """Per-launch DRAM bytes of the kernel from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -326,9 +336,12 @@ def run_gpu_arm(args, cfg):
         ctx.timer_start()
         losses = []
         prof = {}
+        flops = {}
         for _ in range(args.steps):
             losses.append(trainer.step(epoch)[0])
+            fl = trainer.kernel_flops()
             for k, (ms, by) in trainer.kernel_times().items():
+                flops[k] = flops.get(k, 0.0) + fl.get(k, 0.0)
                 a = prof.setdefault(k, [0.0, 0.0])
                 a[0] += ms
                 a[1] += by
@@ -370,9 +383,23 @@ def run_gpu_arm(args, cfg):
     achieved = spmm_bytes / (spmm_ms / 1e3) / 1e9 if spmm_ms > 0 else 0.0
     total_prof = sum(v[0] for v in prof.values())
     kernels = {k: {"ms_per_step": v[0] / args.steps, "share": v[0] / total_prof if total_prof else None,
-                   "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 and v[1] > 0 else None}
+                   "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 and v[1] > 0 else None,
+                   "TFLOP_per_s_fp16x3": (3 * flops[k] / (v[0] / 1e3) / 1e12) if flops.get(k) and v[0] > 0 else None}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     dominant = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+    # tensor roofline of the dominant GEMM group: fp16x3 issues three fp16 MMAs per fp32-equivalent
+    # product, so the tensor pipe executes 3x the algorithmic 2MNK flops
+    gemm_groups = [k for k in prof if flops.get(k, 0) > 0]
+    gdom = max(gemm_groups, key=lambda k: prof[k][0]) if gemm_groups else None
+    tpeak, tpeak_kind = measured_tensor_peak()
+    roofline_gemm = None
+    if gdom:
+        alg = flops[gdom] / (prof[gdom][0] / 1e3) / 1e12
+        roofline_gemm = {"kernel": f"{gdom} (tcgen05 fp16x3)", "bound": "tensor", "achieved": 3 * alg,
+                         "algorithmic_tflops": alg, "peak": tpeak, "peak_kind": tpeak_kind, "unit": "TFLOP/s",
+                         "frac": 3 * alg / tpeak, "hbm_GB_per_s": prof[gdom][1] / (prof[gdom][0] / 1e3) / 1e9,
+                         "note": "achieved = executed fp16 MMA flops (3 x 2MNK) / measured kernel time; the SM "
+                                 "clock sits at the power cap (see clocks)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -400,6 +427,7 @@ def run_gpu_arm(args, cfg):
                      "bytes_per_launch": spmm_bytes / max(launches_spmm, 1),
                      "share_of_step": spmm_ms / total_prof if total_prof else None},
         "dominant_kernel": dominant,
+        "roofline_gemm": roofline_gemm,
         "kernels": kernels,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": e2e_ms,

@@ -189,6 +189,9 @@ sc_status sc_trainer_evaluate(sc_trainer* t, double* train, double* val, double*
 sc_status sc_trainer_profile(sc_trainer* t, int32_t enable);
 sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms, double* bytes, int32_t cap,
                                   int32_t* count);
+/* Algorithmic GEMM flops (2MNK, fp32-equivalent products) per kernel group, in
+ * the order of sc_trainer_kernel_times (0 for non-GEMM groups). */
+sc_status sc_trainer_kernel_flops(sc_trainer* t, double* flops, int32_t cap, int32_t* count);
 sc_status sc_trainer_destroy(sc_trainer* t);
 
 /* ---- files (byte-compatible with the reference's writers) ------------------ */

@@ -788,6 +788,16 @@ sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms,
         *count = k;
     });
 }
+sc_status sc_trainer_kernel_flops(sc_trainer* t, double* flops, int32_t cap, int32_t* count) {
+    return guard([&] {
+        int32_t k = 0;
+        for (const auto& kv : t->prof.totals) {  // same order as sc_trainer_kernel_times
+            if (k < cap && flops) flops[k] = kv.second.flops;
+            ++k;
+        }
+        *count = k;
+    });
+}
 sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t K1, const float* A1,
                         int64_t a1_rows, int64_t lda1, const int32_t* rows1, const float* B1, int64_t ldb1,
                         int32_t b1_nn, int32_t K2, const float* A2, int64_t lda2, const float* B2, int64_t ldb2,

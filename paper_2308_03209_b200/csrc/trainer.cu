@@ -30,7 +30,7 @@ namespace sc {
     } while (0)
 
 // ---- per-kernel event profiler (bench.py roofline) ---------------------------
-void Profiler::begin(const char* name, double bytes, cudaStream_t s) {
+void Profiler::begin(const char* name, double bytes, cudaStream_t s, double flops) {
     if (!enabled) return;
     if (used == events.size()) {
         cudaEvent_t a, b;
@@ -40,12 +40,13 @@ void Profiler::begin(const char* name, double bytes, cudaStream_t s) {
     }
     cur_name = name;
     cur_bytes = bytes;
+    cur_flops = flops;
     SC_CUDA(cudaEventRecord(events[used].first, s));
 }
 void Profiler::end(cudaStream_t s) {
     if (!enabled) return;
     SC_CUDA(cudaEventRecord(events[used].second, s));
-    records.push_back({cur_name, cur_bytes, used});
+    records.push_back({cur_name, cur_bytes, cur_flops, used});
     ++used;
 }
 void Profiler::collect() {
@@ -57,6 +58,7 @@ void Profiler::collect() {
         auto& t = totals[r.name];
         t.ms += ms;
         t.bytes += r.bytes;
+        t.flops += r.flops;
         t.calls += 1;
     }
     records.clear();
@@ -319,7 +321,7 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
         const MatA xin = l == 0 ? x0 : MatA{t->X[l].get(), lo.in, nullptr, lo.in};
         const float* xin_amax = l == 0 ? t->g->feat_amax.get() : t->amax_x(l);
         // msg = relu(h W^T)   (nn.hpp:220-221)
-        P.begin("gemm_msg", 4.0 * n * (lo.in + lo.H), s);
+        P.begin("gemm_msg", 4.0 * n * (lo.in + lo.H), s, 2.0 * n * lo.in * lo.H);
         t->tc.nt(t, xin, xin_amax, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, nullptr,
                  t->MSG[l].get(), lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l));
         P.end(s);
@@ -332,14 +334,14 @@ void forward(sc_trainer* t, const Rows& R, float* logits) {
         const MatB uL{t->theta.get() + lo.U, lo.H + lo.in, false};
         const MatB uR{t->theta.get() + lo.U + lo.H, lo.H + lo.in, false};
         const MatA mean{t->MEAN[l].get(), lo.H, nullptr, lo.H};
-        P.begin("gemm_update", 4.0 * n * (2 * lo.H + lo.in), s);
+        P.begin("gemm_update", 4.0 * n * (2 * lo.H + lo.in), s, 2.0 * n * (lo.H + lo.in) * lo.H);
         // |mean| <= max|msg| (a mean of msg rows): msg's bound scales it.
         t->tc.nt(t, mean, t->amax_msg(l), uL, &xin, xin_amax, &uR, t->X[l + 1].get(), lo.H, n, lo.H, kEpiNone, nullptr,
                  t->amax_x(l + 1));
         P.end(s);
     }
     const MatA emb = t->L == 0 ? x0 : MatA{t->X[t->L].get(), t->E, nullptr, t->E};
-    P.begin("gemm_head", 4.0 * n * (t->E + t->C), s);
+    P.begin("gemm_head", 4.0 * n * (t->E + t->C), s, 2.0 * n * t->E * t->C);
     const float* emb_amax = t->L == 0 ? t->g->feat_amax.get() : t->amax_x(t->L);
     t->tc.nt(t, emb, emb_amax, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, nullptr, logits,
              t->Cp, n, t->C, kEpiNone, nullptr, nullptr);
@@ -366,7 +368,7 @@ void backward(sc_trainer* t, const Rows& R, int i) {
     const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L].get(), t->E, nullptr, t->E};
     // head grad = G^T emb (side) ; dh = G head (main)   (:259-260)
     hand_off(s, w);
-    P.begin("wgrad", 4.0 * n * (t->C + t->E), w);
+    P.begin("wgrad", 4.0 * n * (t->C + t->E), w, 2.0 * n * t->C * t->E);
     const float* x0_amax = t->g->feat_amax.get();
     const float* emb_amax = t->L == 0 ? x0_amax : t->amax_x(t->L);
     t->tc.tn(t, MatT{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
@@ -381,7 +383,7 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         hand_off(w, s);
         return;
     }
-    P.begin("gemm_dgrad", 4.0 * n * (t->C + t->E), s);
+    P.begin("gemm_dgrad", 4.0 * n * (t->C + t->E), s, 2.0 * n * t->C * t->E);
     t->tc.nt(t, MatA{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, MatB{t->theta.get() + t->head_off, t->E, true},
              nullptr, nullptr, nullptr, dh, t->E, n, t->E, kEpiNone, nullptr, dh_amax);
     P.end(s);
@@ -392,14 +394,14 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         const MatT meant{t->MEAN[l].get(), lo.H, nullptr, lo.H};
         const float* xin_amax = l == 0 ? x0_amax : t->amax_x(l);
         // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
-        P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s);
+        P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s, 2.0 * n * lo.H * lo.H);
         t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr,
                  nullptr, nullptr, t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get(), nullptr);
         P.end(s);
         // dU = dh^T [mean | h_in] (:271-272) on the side stream: tensor-bound, it
         // shares the SMs with the HBM-bound transposed aggregation below
         hand_off(s, w);
-        P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), w);
+        P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), w, 2.0 * n * lo.H * (lo.H + lo.in));
         t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, t->slot_ptr(2 * l + 1, i), lo.H + lo.in,
                  w, ws_w);
         P.end(w);
@@ -412,14 +414,14 @@ void backward(sc_trainer* t, const Rows& R, int i) {
                  t->heavy_ws.get());
         P.end(s);
         // dW = dz^T h_in   (:289)
-        P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s);
+        P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s, 2.0 * n * lo.H * lo.in);
         t->tc.tn(t, MatT{t->dz.get(), lo.H, nullptr, lo.H}, dz_amax, xint, xin_amax, nullptr, nullptr, n,
                  t->slot_ptr(2 * l, i), lo.in);
         P.end(s);
         exchange_bucket(t, 2 * l, round);
         if (l > 0) {  // dh = dh U_R + dz W   (:275, :290); layer 0's is unused
             const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz.get(), lo.H, nullptr, lo.H};
-            P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s);
+            P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s, 2.0 * n * 2 * lo.H * lo.in);
             const MatB wB{t->theta.get() + lo.W, lo.in, true};
             SC_CUDA(cudaMemsetAsync(dh2_amax, 0, sizeof(float), s));
             t->tc.nt(t, dhA, dh_amax, MatB{t->theta.get() + lo.U + lo.H, lo.H + lo.in, true}, &dzA, dz_amax, &wB, dh2,

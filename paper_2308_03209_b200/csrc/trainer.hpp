@@ -36,11 +36,11 @@ struct PartState {
 struct Profiler {
     struct Rec {
         const char* name;
-        double bytes;
+        double bytes, flops;
         size_t slot;
     };
     struct Total {
-        double ms = 0, bytes = 0;
+        double ms = 0, bytes = 0, flops = 0;
         int calls = 0;
     };
     bool enabled = false;
@@ -48,9 +48,10 @@ struct Profiler {
     std::vector<Rec> records;
     size_t used = 0;
     const char* cur_name = nullptr;
-    double cur_bytes = 0;
+    double cur_bytes = 0, cur_flops = 0;
     std::map<std::string, Total> totals;
-    void begin(const char* name, double bytes, cudaStream_t s);
+    // bytes: algorithmic HBM bytes; flops: algorithmic 2MNK of a GEMM (fp32-equivalent products)
+    void begin(const char* name, double bytes, cudaStream_t s, double flops = 0);
     void end(cudaStream_t s);
     void collect();
     ~Profiler();

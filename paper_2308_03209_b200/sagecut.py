@@ -128,6 +128,7 @@ _sig("sc_trainer_evaluate", [_vp, C.POINTER(_f64), C.POINTER(_f64), C.POINTER(_f
 _sig("sc_trainer_profile", [_vp, _i32])
 _sig("sc_trainer_kernel_times", [_vp, C.POINTER(C.c_char_p), C.POINTER(_f64), C.POINTER(_f64), _i32,
                                  C.POINTER(_i32)])
+_sig("sc_trainer_kernel_flops", [_vp, C.POINTER(_f64), _i32, C.POINTER(_i32)])
 _sig("sc_trainer_destroy", [_vp])
 _sig("sc_debug_gemm", [_vp, _i32, _i64, _i32, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _i64, _vp,
                        _i64, _i32, _i32, _vp, _vp])
@@ -751,6 +752,14 @@ class CoFreeTrainer:
         by = (_f64 * k)()
         _check(_lib.sc_trainer_kernel_times(self.h, names, ms, by, k, C.byref(cnt)))
         return {names[i].decode(): (ms[i], by[i]) for i in range(k)}
+
+    def kernel_flops(self):
+        """{group: algorithmic GEMM flops of the last step} (2MNK; fp16x3 issues 3x that on the MMAs)."""
+        names = list(self.kernel_times())
+        fl = (_f64 * max(len(names), 1))()
+        cnt = _i32()
+        _check(_lib.sc_trainer_kernel_flops(self.h, fl, len(names), C.byref(cnt)))
+        return {n: fl[i] for i, n in enumerate(names)}
 
     def close(self):
         if getattr(self, "h", None):
