@@ -164,7 +164,6 @@ void trainer_init(sc_trainer* t) {
     t->local.clear();
     for (int i = t->rank; i < t->p; i += t->world) t->local.push_back(i);
     t->ps.resize(t->p);
-    DevBuf<double> wtmp;
     for (int i = 0; i < t->p; ++i) {
         PartState& st = t->ps[i];
         const PartDev& pd = vc->parts[i];
