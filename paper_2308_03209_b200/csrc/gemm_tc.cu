@@ -14,19 +14,19 @@
 // 4.5e-6, which compounded to 2.5e-4 in 5-step gradients). The |max| values
 // come from the kernels that produced each operand (no host sync).
 //
-// Data movement (both kernels, persistent/one CTA per SM, 448 threads):
-//   warp 13    loader: one cp.async.bulk (TMA bulk copy) per operand row slice,
-//              HBM -> fp32 staging ring in shared memory (optionally through a
-//              row gather, e.g. partition rows -> global feature rows)
-//   warps 0-7  converters: staging fp32 -> scaled fp16 hi/lo tiles in the
-//              canonical SWIZZLE_64B K-major (NT) or SWIZZLE_128B MN-major (TN)
-//              layout; NT thread 0 also bulk-copies the pre-split weight image
-//   warp 12    TMEM allocator + single-thread MMA issuer (tcgen05.mma/commit)
-//   warps 8-11 epilogue: tcgen05.ld -> unscale / ReLU / row-scale / |max| ->
-//              smem transpose -> coalesced stores (NT), or periodic TMEM drains
-//              into an fp32 split-K partial (TN)
-// Two TMEM accumulators (2 x 256 columns) let one tile's epilogue overlap the
-// next tile's main loop.
+// Data movement (persistent, one CTA (pair) per SM (pair)):
+//   loader warp      2D TMA boxes HBM -> fp32 staging ring in shared memory
+//   converter warps  staging fp32 -> scaled fp16 hi/lo tiles in the canonical
+//                    SWIZZLE_64B K-major (NT) or SWIZZLE_128B MN-major (TN)
+//                    layout; TN CTA pairs write the A' halves to TMEM instead;
+//                    NT thread 0 also bulk-copies the pre-split weight image
+//   MMA warp         TMEM allocator + single-thread MMA issuer (tcgen05.mma/commit)
+//   epilogue warps   tcgen05.ld -> unscale / ReLU / row-scale / |max| -> smem
+//                    transpose -> TMA stores (NT), or periodic TMEM drains into
+//                    an fp32 split-K partial (TN)
+// NT: 8 converter + 8 epilogue warps, two TMEM accumulators (2 x 256 columns) so
+// one tile's epilogue overlaps the next tile's main loop. TN: TnCfg (8 or 16
+// converter warps, 4 epilogue warps).
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -47,9 +47,6 @@ constexpr int kBM = 128;  // UMMA M (cta_group::1)
 constexpr int kMaxN = 256;
 constexpr int kConvWarps = 8;
 constexpr int kConv = kConvWarps * 32;  // converter threads (warps 0-7)
-constexpr int kMmaWarp = 12;
-constexpr int kLoadWarp = 13;
-constexpr int kThreads = 14 * 32;
 // NT uses 8 epilogue warps (warps 8-15: two per TMEM lane quarter, even / odd
 // 32-column chunks), then the MMA and loader warps.
 constexpr int kNtEpiWarps = 8;
@@ -343,6 +340,17 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8])
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
                  "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                  : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[N]) {
+    static_assert(N == 4 || N == 8, "tmem_st: 4 or 8 columns");
+    if constexpr (N == 8) {
+        tmem_st8(taddr, v);
+    } else {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+                     "r"(v[2]), "r"(v[3])
+                     : "memory");
+    }
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // MMA completion -> barrier at the same offset in both CTAs of the pair (or the local one).
@@ -754,6 +762,10 @@ struct TnCfg {
     static constexpr int kStages = AT ? 6 : (PAIR ? 3 : 2);
     static constexpr int kStg = PAIR ? 3 : 2;
     static constexpr int kAcc = AT ? 1 : 2;                  // TMEM accumulators
+    // warp roles: converters 0 .. kCW-1, epilogue kCW .. kCW+3, MMA issuer, TMA loader
+    static constexpr int kCW = AT ? 16 : kConvWarps;
+    static constexpr int kC = kCW * 32;
+    static constexpr int kMma = kCW + 4, kLoad = kCW + 5, kThr = (kCW + 6) * 32;
     static constexpr int kChunk = AT ? 2 * kChunkKb : kChunkKb;  // k-blocks per accumulation
     static constexpr int kBLoc = PAIR ? kMaxN / 2 : kMaxN;  // B' columns held per CTA
     static constexpr int kBTile = kBLoc * kTnBK * 2;        // one (hi or lo) B' tile
@@ -771,7 +783,7 @@ static_assert(TnCfg<true>::kSmem <= 232448 && TnCfg<false>::kSmem <= 232448, "TN
 static_assert(TnCfg<true, true>::kSmem <= 232448 && 256 + 32 * TnCfg<true, true>::kStages <= 512, "TN (A in TMEM)");
 
 template <bool PAIR, bool AT = false>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
+__global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
     static_assert(!AT || PAIR, "A in TMEM needs the CTA-pair layout");
     using Cfg = TnCfg<PAIR, AT>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -810,15 +822,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     int kbx = scale_exp(*p.b[0].amax);
     if (p.nb > 1) kbx = min(kbx, scale_exp(*p.b[1].amax));
 
-    if (warp == kMmaWarp) {
+    if (warp == Cfg::kMma) {
         if (lane == 0) {
             for (int s = 0; s < Cfg::kStages; ++s) {
-                mbar_init(&full[s], kConvWarps * (PAIR ? 2 : 1));
+                mbar_init(&full[s], Cfg::kCW * (PAIR ? 2 : 1));
                 mbar_init(&empty[s], 1);
             }
             for (int s = 0; s < Cfg::kStg; ++s) {
                 mbar_init(&sfull[s], 1);
-                mbar_init(&sempty[s], kConvWarps);
+                mbar_init(&sempty[s], Cfg::kCW);
             }
             for (int s = 0; s < Cfg::kAcc; ++s) {
                 mbar_init(&tfull[s], 1);
@@ -837,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     const uint32_t full_l = PAIR ? mapa(smem_u32(full), 0) : smem_u32(full);
     const uint32_t tempty_l = PAIR ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
 
-    if (warp == kLoadWarp) {
+    if (warp == Cfg::kLoad) {
         // ================= loader: 2D TMA boxes (32 columns x 32 rows, SWIZZLE_128B) -> staging =================
         // A' needs ceil(na/32) boxes, B' ceil(nbl/32) (each from B1 or B2; n2a is a multiple of 32).
         const int a_boxes = (na + 31) >> 5, b_boxes = (nbl + 31) >> 5;
@@ -858,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 else tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[ring.idx], pol_b);
             }
         }
-    } else if (warp < kConvWarps) {
+    } else if (warp < Cfg::kCW) {
         // ================= converters: swizzled staging -> MN-major fp16 hi/lo =================
         // Row-fastest mapping (idx & 31 = row): 8 consecutive threads read the same logical chunk
         // of 8 rows, which the 128 B swizzle spreads over distinct banks.
@@ -887,47 +899,50 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 // A' -> TMEM: warp w owns TMEM lane quarter w & 3 (A' columns 32q .. 32q+31, one per
                 // lane) and k rows 16 (w >> 2) .. +15 of the stage. Column-wise reads of the row-major
                 // staging are conflict-free (one 128 B row per instruction, swizzled chunks).
+                constexpr int kRows = kTnBK / (Cfg::kCW / 4);  // k rows per warp (8 with 16 converter warps)
                 const int q = warp & 3, kh = warp >> 2;
                 const int m = 32 * q + lane;
                 const uint8_t* box = sga + q * kTnBox + (((lane & 3)) << 2);
-                float x[16];
+                float x[kRows];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int kr = 16 * kh + i;
+                for (int i = 0; i < kRows; ++i) {
+                    const int kr = kRows * kh + i;
                     const float v = *reinterpret_cast<const float*>(box + kr * 128 + ((((lane >> 2) ^ (kr & 7))) << 4));
                     x[i] = (whole || (kr < rows_ok && m < na)) ? v : 0.f;
                 }
-                uint32_t hi[8], lo[8];
+                uint32_t hi[kRows / 2], lo[kRows / 2];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) split2(x[2 * j], x[2 * j + 1], sa_, hi[j], lo[j]);
-                const uint32_t tcol = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + 256 + mr.idx * 32 + 8 * kh;
-                tmem_st8(tcol, hi);
-                tmem_st8(tcol + 16, lo);
+                for (int j = 0; j < kRows / 2; ++j) split2(x[2 * j], x[2 * j + 1], sa_, hi[j], lo[j]);
+                const uint32_t tcol =
+                    tmem_base + (static_cast<uint32_t>(32 * q) << 16) + 256 + mr.idx * 32 + (kRows / 2) * kh;
+                tmem_st<kRows / 2>(tcol, hi);
+                tmem_st<kRows / 2>(tcol + 16, lo);
             }
             if (whole) {
                 // all of the stage's shared loads first (up to 8 x LDS.128 in flight), then convert
-                constexpr int kJB = Cfg::kBLoc / 64;
-                float4 xa[2][2], xb[kJB][2];
+                constexpr int kJB = (4 * Cfg::kBLoc + Cfg::kC - 1) / Cfg::kC;  // B' items (row, 8 cols) per thread
+                constexpr int kJA = (4 * kBM + Cfg::kC - 1) / Cfg::kC;         // A' items (smem path)
+                float4 xa[kJA][2], xb[kJB][2];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < kJA; ++j) {
                     if constexpr (AT) break;
-                    const int idx = tid + j * kConv;
+                    const int idx = tid + j * Cfg::kC;
                     load8(sga, idx & 31, idx >> 5, 8, xa[j][0], xa[j][1]);
                 }
 #pragma unroll
                 for (int j = 0; j < kJB; ++j) {
-                    const int idx = tid + j * kConv;
+                    const int idx = tid + j * Cfg::kC;
                     if ((idx >> 5) < bch) load8(sgb, idx & 31, idx >> 5, 8, xb[j][0], xb[j][1]);
                 }
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < kJA; ++j) {
                     if constexpr (AT) break;
-                    const int idx = tid + j * kConv;
+                    const int idx = tid + j * Cfg::kC;
                     split8_store(xa[j][0], xa[j][1], sa_, st, st + kTnATile, mn_off((idx >> 5) * 8, idx & 31));
                 }
 #pragma unroll
                 for (int j = 0; j < kJB; ++j) {
-                    const int idx = tid + j * kConv;
+                    const int idx = tid + j * Cfg::kC;
                     const int kr = idx & 31, ch = idx >> 5;
                     if (ch < bch)
                         split8_store(xb[j][0], xb[j][1], sb_, st + kBOff, st + kBOff + Cfg::kBTile,
@@ -935,9 +950,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < (4 * kBM + Cfg::kC - 1) / Cfg::kC; ++j) {
                     if constexpr (AT) break;
-                    const int idx = tid + j * kConv;
+                    const int idx = tid + j * Cfg::kC;
                     const int kr = idx & 31, ch = idx >> 5;
                     float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
                     const int valid = kr < rows_ok ? min(8, na - ch * 8) : 0;
@@ -945,8 +960,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                     split8_store(x0, x1, sa_, st, st + kTnATile, mn_off(ch * 8, kr));
                 }
 #pragma unroll
-                for (int j = 0; j < Cfg::kBLoc / 64; ++j) {
-                    const int idx = tid + j * kConv;
+                for (int j = 0; j < (4 * Cfg::kBLoc + Cfg::kC - 1) / Cfg::kC; ++j) {
+                    const int idx = tid + j * Cfg::kC;
                     const int kr = idx & 31, ch = idx >> 5;
                     if (ch >= bch) continue;
                     float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
@@ -967,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
                 mbar_arrive(&sempty[sr.idx]);
             }
         }
-    } else if (warp == kMmaWarp) {
+    } else if (warp == Cfg::kMma) {
         // ================= MMA issuer (the pair's leader only) =================
         if (!PAIR || rank == 0) {
             const uint32_t idesc = AT ? idesc_f16_at(Cfg::kACols, nb_pad) : idesc_f16_mn(Cfg::kACols, nb_pad);
@@ -1078,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tn_f16x3_kernel(const __grid
     tc_fence_before();
     if constexpr (PAIR) cluster_sync();
     else __syncthreads();
-    if (warp == kMmaWarp) {
+    if (warp == Cfg::kMma) {
         tc_fence_after();
         tmem_dealloc_g<PAIR>(tmem_base);
     }
@@ -1195,12 +1210,12 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     p.tiles2 = (N2 + tc::kMaxN - 1) / tc::kMaxN;
     p.ws = ws;
     const int64_t units = int64_t(S) * p.tiles1 * p.tiles2;
-    auto launch = [&](auto kernel, int smem_bytes) {
+    auto launch = [&](auto kernel, int smem_bytes, int threads) {
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
         cudaLaunchConfig_t cfg{};
         cudaLaunchAttribute attr[1];
         cfg.gridDim = dim3(static_cast<unsigned>(pair ? 2 * units : units));
-        cfg.blockDim = dim3(tc::kThreads);
+        cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes);
         cfg.stream = s;
         if (pair) {
@@ -1217,9 +1232,12 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
         const char* e = std::getenv("SC_TN_ATMEM");
         return e ? std::atoi(e) != 0 : true;
     }();
-    if (pair && a_tmem) launch(tc::gemm_tn_f16x3_kernel<true, true>, tc::TnCfg<true, true>::kSmem);
-    else if (pair) launch(tc::gemm_tn_f16x3_kernel<true, false>, tc::TnCfg<true, false>::kSmem);
-    else launch(tc::gemm_tn_f16x3_kernel<false, false>, tc::TnCfg<false, false>::kSmem);
+    if (pair && a_tmem)
+        launch(tc::gemm_tn_f16x3_kernel<true, true>, tc::TnCfg<true, true>::kSmem, tc::TnCfg<true, true>::kThr);
+    else if (pair)
+        launch(tc::gemm_tn_f16x3_kernel<true, false>, tc::TnCfg<true, false>::kSmem, tc::TnCfg<true, false>::kThr);
+    else
+        launch(tc::gemm_tn_f16x3_kernel<false, false>, tc::TnCfg<false, false>::kSmem, tc::TnCfg<false, false>::kThr);
     SC_LAUNCH_CHECK();
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();
