@@ -763,7 +763,7 @@ struct TnCfg {
     static constexpr int kStg = PAIR ? 3 : 2;
     static constexpr int kAcc = AT ? 1 : 2;                  // TMEM accumulators
     // warp roles: converters 0 .. kCW-1, epilogue kCW .. kCW+3, MMA issuer, TMA loader
-    static constexpr int kCW = AT ? 16 : kConvWarps;
+    static constexpr int kCW = kConvWarps;  // (16 with A' in TMEM measured 2 % slower: converters are not the limit)
     static constexpr int kC = kCW * 32;
     static constexpr int kMma = kCW + 4, kLoad = kCW + 5, kThr = (kCW + 6) * 32;
     static constexpr int kChunk = AT ? 2 * kChunkKb : kChunkKb;  // k-blocks per accumulation
