@@ -639,34 +639,29 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
     }
 }
 
-// ---- B image prep (one CTA per operand): |B| max -> exponent kB, then fp32 B
+// ---- B image prep (two grid-wide passes): |B| max -> exponent kB, then fp32 B
 // (NT [N x K] or NN [K x N]) * 2^kB split into per-k-block [hi tile | lo tile],
 // each n_pad rows x 32 k fp16 in the SW64 K-major layout.
-__global__ void __launch_bounds__(1024) prep_b_kernel(const float* __restrict__ B, int64_t ldb, int nn, int32_t N,
-                                                      int32_t K, int32_t n_pad, int32_t kblocks, uint8_t* img,
-                                                      int32_t* bexp) {
-    __shared__ float red[32];
+__global__ void prep_b_amax_kernel(const float* __restrict__ B, int64_t ldb, int nn, int32_t N, int32_t K,
+                                   float* amax) {
     float mx = 0.f;
-    for (int64_t i = threadIdx.x; i < int64_t(N) * K; i += blockDim.x) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(N) * K;
+         i += int64_t(gridDim.x) * blockDim.x) {
         const int32_t a = static_cast<int32_t>(i / K), b = static_cast<int32_t>(i % K);
         mx = fmaxf(mx, fabsf(nn ? B[int64_t(b) * ldb + a] : B[int64_t(a) * ldb + b]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (threadIdx.x == 0) red[0] = mx;
-    }
-    __syncthreads();
-    const int kexp = scale_exp(red[0]);
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(amax), __float_as_uint(mx));
+}
+__global__ void prep_b_split_kernel(const float* __restrict__ B, int64_t ldb, int nn, int32_t N, int32_t K,
+                                    int32_t n_pad, int32_t kblocks, const float* amax, uint8_t* img,
+                                    int32_t* bexp) {
+    const int kexp = scale_exp(*amax);
     const float s = ldexpf(1.f, kexp);
-    if (threadIdx.x == 0) *bexp = kexp;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *bexp = kexp;
     const int64_t total = int64_t(kblocks) * n_pad * 4;  // 16-byte chunks per (hi) image
-    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int32_t kb = static_cast<int32_t>(i / (int64_t(n_pad) * 4));
         const int32_t rem = static_cast<int32_t>(i % (int64_t(n_pad) * 4));
         const int32_t n = rem >> 2, c = rem & 3;
@@ -1273,10 +1268,17 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
     im.kblocks = (K + tc::kNtBK - 1) / tc::kNtBK;
     im.img.ensure(static_cast<size_t>(im.kblocks) * 2 * im.n_pad * 64);
     im.bexp.ensure(1);
-    tc::prep_b_kernel<<<1, 1024, 0, s>>>(b.ptr, b.ld, b.nn ? 1 : 0, N, K, im.n_pad, im.kblocks, im.img.get(),
-                                         im.bexp.get());
+    im.amax.ensure(1);
+    SC_CUDA(cudaMemsetAsync(im.amax.get(), 0, sizeof(float), s));
+    const int64_t nk = int64_t(N) * K;
+    tc::prep_b_amax_kernel<<<grid_for(nk, 256, 64), 256, 0, s>>>(b.ptr, b.ld, b.nn ? 1 : 0, N, K, im.amax.get());
     SC_LAUNCH_CHECK();
-    count_launch();
+    const int64_t chunks = int64_t(im.kblocks) * im.n_pad * 4;
+    tc::prep_b_split_kernel<<<grid_for(chunks, 256), 256, 0, s>>>(b.ptr, b.ld, b.nn ? 1 : 0, N, K, im.n_pad,
+                                                                  im.kblocks, im.amax.get(), im.img.get(),
+                                                                  im.bexp.get());
+    SC_LAUNCH_CHECK();
+    count_launch(2);
 }
 
 

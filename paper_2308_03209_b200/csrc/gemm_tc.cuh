@@ -18,6 +18,7 @@ namespace sc {
 struct BImage {
     DevBuf<uint8_t> img;
     DevBuf<int32_t> bexp;
+    DevBuf<float> amax;  // max |B| (prep scratch)
     int32_t N = 0, K = 0, n_pad = 0, kblocks = 0;
 };
 
