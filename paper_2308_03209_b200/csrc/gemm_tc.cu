@@ -32,6 +32,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -715,6 +716,7 @@ struct alignas(64) TnParams {
     int64_t rows_per_split;
     int32_t tiles1, tiles2;
     float* ws;       // [splits][N1][N2] fp32 partials
+    unsigned long long* trace;  // optional (SC_TN_TRACE=1): per-role wait / total cycles, summed over CTAs
 };
 
 // MN-major SW128 descriptor: LBO = stride between 64-element MN atoms,
@@ -777,6 +779,19 @@ struct TnCfg {
 static_assert(TnCfg<true>::kSmem <= 232448 && TnCfg<false>::kSmem <= 232448, "TN shared memory");
 static_assert(TnCfg<true, true>::kSmem <= 232448 && 256 + 32 * TnCfg<true, true>::kStages <= 512, "TN (A in TMEM)");
 
+// Diagnostics (build with -DSC_TN_TRACE_BUILD, run with SC_TN_TRACE=1): cycles each
+// role spends in its barrier waits, summed over CTAs and printed per launch.
+#ifdef SC_TN_TRACE_BUILD
+#define TN_TIMED_WAIT(acc_var, call)                                              \
+    do {                                                                          \
+        const long long t0_ = p.trace ? clock64() : 0;                            \
+        call;                                                                     \
+        if (p.trace) acc_var += static_cast<unsigned long long>(clock64() - t0_); \
+    } while (0)
+#else
+#define TN_TIMED_WAIT(acc_var, call) call
+#endif
+
 template <bool PAIR, bool AT = false>
 __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
     static_assert(!AT || PAIR, "A in TMEM needs the CTA-pair layout");
@@ -795,6 +810,10 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+#ifdef SC_TN_TRACE_BUILD
+    unsigned long long w_a = 0, w_b = 0;  // diagnostics: wait cycles of this thread's role
+    const long long t_start = p.trace ? clock64() : 0;
+#endif
     const int unit = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
     const int tiles = p.tiles1 * p.tiles2;
     const int split = unit / tiles, tile = unit % tiles;
@@ -853,7 +872,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
         Ring ring;
         for (int kb = 0; kb < kblocks; ++kb, ring.next(Cfg::kStg)) {
             const int32_t k0 = static_cast<int32_t>(r0 + int64_t(kb) * kTnBK);
-            mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
+            TN_TIMED_WAIT(w_a, mbar_wait(&sempty[ring.idx], ring.phase ^ 1));
             uint8_t* sa = stg_base + ring.idx * Cfg::kStgSlot;
             uint8_t* sb = sa + kTnStgA;
             if (lane == 0) mbar_arrive_expect_tx(&sfull[ring.idx], bytes);
@@ -879,8 +898,8 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
             uint8_t* st = smem + mr.idx * Cfg::kStage;
             const uint8_t* sga = stg_base + sr.idx * Cfg::kStgSlot;
             const uint8_t* sgb = sga + kTnStgA;
-            mbar_wait(&empty[mr.idx], mr.phase ^ 1);
-            mbar_wait(&sfull[sr.idx], sr.phase);
+            TN_TIMED_WAIT(w_a, mbar_wait(&empty[mr.idx], mr.phase ^ 1));
+            TN_TIMED_WAIT(w_b, mbar_wait(&sfull[sr.idx], sr.phase));
             // A': 32 rows x 16 chunks of 8 columns; B': 32 rows x bch chunks (this CTA's columns).
             // Interior stages (all rows and columns valid) skip the masking.
             const bool whole = rows_ok == kTnBK && na == kBM && nbl == nloc;  // block-uniform
@@ -985,11 +1004,11 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
             for (int chunk = 0; chunk < nchunks; ++chunk) {
                 const uint32_t acc = chunk % Cfg::kAcc;
                 const uint32_t d_tmem = tmem_base + acc * 256;
-                mbar_wait(&tempty[acc], ((chunk / Cfg::kAcc) & 1) ^ 1);
+                TN_TIMED_WAIT(w_b, mbar_wait(&tempty[acc], ((chunk / Cfg::kAcc) & 1) ^ 1));
                 tc_fence_after();
                 const int kb_end = min(kblocks, (chunk + 1) * Cfg::kChunk);
                 for (int kb = chunk * Cfg::kChunk; kb < kb_end; ++kb, mr.next(Cfg::kStages)) {
-                    mbar_wait(&full[mr.idx], mr.phase);
+                    TN_TIMED_WAIT(w_a, mbar_wait(&full[mr.idx], mr.phase));
                     tc_fence_after();
                     if (lane == 0) {
                         const uint8_t* st = smem + mr.idx * Cfg::kStage;
@@ -1038,7 +1057,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
         float* tbuf = reinterpret_cast<float*>(smem + Cfg::kEpiOff) + ew * 32 * Cfg::kEpiPitch;
         for (int chunk = 0; chunk < nchunks; ++chunk) {
             const uint32_t acc = chunk % Cfg::kAcc;
-            mbar_wait(&tfull[acc], (chunk / Cfg::kAcc) & 1);
+            TN_TIMED_WAIT(w_a, mbar_wait(&tfull[acc], (chunk / Cfg::kAcc) & 1));
             tc_fence_after();
             for (int c0 = 0; c0 < nb_pad; c0 += 32) {
                 uint32_t r[32];
@@ -1085,6 +1104,17 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
             for (int rr = 0; rr < rows_here; ++rr)
                 for (int c = lane; c < nb; c += 32) outw[int64_t(rr) * p.N2 + c] = 0.f;
     }
+#ifdef SC_TN_TRACE_BUILD
+    if (p.trace && lane == 0) {  // roles: 0 converters, 1 epilogue, 2 MMA, 3 loader
+        const int role = warp < Cfg::kCW ? 0 : warp < Cfg::kCW + 4 ? 1 : warp == Cfg::kMma ? 2 : 3;
+        if (role != 2 || !PAIR || rank == 0) {
+            atomicAdd(p.trace + 4 * role + 0, w_a);
+            atomicAdd(p.trace + 4 * role + 1, w_b);
+            atomicAdd(p.trace + 4 * role + 2, static_cast<unsigned long long>(clock64() - t_start));
+            atomicAdd(p.trace + 4 * role + 3, 1ull);
+        }
+    }
+#endif
     tc_fence_before();
     if constexpr (PAIR) cluster_sync();
     else __syncthreads();
@@ -1204,6 +1234,16 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     p.tiles1 = (N1 + acols - 1) / acols;
     p.tiles2 = (N2 + tc::kMaxN - 1) / tc::kMaxN;
     p.ws = ws;
+    static const bool trace = [] {
+        const char* e = std::getenv("SC_TN_TRACE");
+        return e && std::atoi(e) != 0;
+    }();
+    static DevBuf<unsigned long long> trace_buf;
+    if (trace) {
+        trace_buf.ensure(16);
+        SC_CUDA(cudaMemsetAsync(trace_buf.get(), 0, 16 * sizeof(unsigned long long), s));
+        p.trace = trace_buf.get();
+    }
     const int64_t units = int64_t(S) * p.tiles1 * p.tiles2;
     auto launch = [&](auto kernel, int smem_bytes, int threads) {
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
@@ -1234,6 +1274,18 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     else
         launch(tc::gemm_tn_f16x3_kernel<false, false>, tc::TnCfg<false, false>::kSmem, tc::TnCfg<false, false>::kThr);
     SC_LAUNCH_CHECK();
+    if (trace) {  // per role: mean over warps of (wait A, wait B, total) cycles
+        unsigned long long h[16];
+        SC_CUDA(cudaMemcpyAsync(h, trace_buf.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+        SC_CUDA(cudaStreamSynchronize(s));
+        const char* names[4] = {"conv(empty,sfull)", "epi(tfull,-)", "mma(full,tempty)", "load(sempty,-)"};
+        std::fprintf(stderr, "TN trace M=%lld N1=%d N2=%d:", static_cast<long long>(M), N1, N2);
+        for (int r = 0; r < 4; ++r) {
+            const double c = h[4 * r + 3] ? double(h[4 * r + 3]) : 1.0;
+            std::fprintf(stderr, " %s %.0f/%.0f of %.0f;", names[r], h[4 * r] / c, h[4 * r + 1] / c, h[4 * r + 2] / c);
+        }
+        std::fprintf(stderr, "\n");
+    }
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();
     count_launch(2);
