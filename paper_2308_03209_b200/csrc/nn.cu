@@ -647,51 +647,6 @@ __global__ void __launch_bounds__(128) softmax_ce_rows_kernel(int64_t n, int32_t
     }
 }
 
-// Same arithmetic, with the block's 128 rows staged through shared memory so the
-// global loads and gradient stores are fully coalesced (LD = padded row length,
-// a multiple of 4; the tile pitch LD + 1 keeps the per-row reads conflict-free).
-template <int LD>
-__global__ void __launch_bounds__(128) softmax_ce_tile_kernel(int64_t n, int32_t C,
-                                                              const float* __restrict__ logits,
-                                                              const int32_t* __restrict__ labels,
-                                                              const int32_t* __restrict__ rows,
-                                                              const double* __restrict__ w,
-                                                              const float* __restrict__ scale, float* __restrict__ G,
-                                                              double* __restrict__ row_loss) {
-    constexpr int P = LD + 1;
-    __shared__ float tile[128 * P];
-    for (int64_t r0 = int64_t(blockIdx.x) * 128; r0 < n; r0 += int64_t(gridDim.x) * 128) {
-        const int nr = static_cast<int>(min(int64_t(128), n - r0));
-        const float* src = logits + r0 * LD;
-        for (int i = threadIdx.x; i < nr * LD; i += 128) tile[(i / LD) * P + (i % LD)] = __ldg(src + i);
-        __syncthreads();
-        if (threadIdx.x < nr) {
-            const int64_t r = r0 + threadIdx.x;
-            float* z = tile + threadIdx.x * P;
-            const double wr = w[r];
-            if (wr == 0.0) {  // nn.hpp:330
-                for (int c = 0; c < LD; ++c) z[c] = 0.f;
-                row_loss[r] = 0.0;
-            } else {
-                const int32_t y = labels[rows ? rows[r] : r];
-                float mx = -INFINITY;
-                for (int c = 0; c < C; ++c) mx = fmaxf(mx, z[c]);
-                float se = 0.f;
-                for (int c = 0; c < C; ++c) se += expf(z[c] - mx);  // column order, nn.hpp:333-336
-                const float lse = mx + logf(se);
-                const float sc = scale[r];
-                const float zy = z[y];
-                for (int c = 0; c < LD; ++c) z[c] = c < C ? sc * (expf(z[c] - lse) - (c == y ? 1.f : 0.f)) : 0.f;
-                row_loss[r] = wr * static_cast<double>(lse - zy);
-            }
-        }
-        __syncthreads();
-        float* dst = G + r0 * LD;
-        for (int i = threadIdx.x; i < nr * LD; i += 128) dst[i] = tile[(i / LD) * P + (i % LD)];
-        __syncthreads();
-    }
-}
-
 __global__ void bce_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
                            const int32_t* __restrict__ labels,
                            const int32_t* __restrict__ rows, const double* __restrict__ w,
@@ -986,12 +941,7 @@ void softmax_ce(int64_t n, int32_t C, int32_t ld, const float* logits, const int
     const bool vec = ld % 4 == 0 && reinterpret_cast<uintptr_t>(logits) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(G) % 16 == 0;
     const unsigned grid = grid_for(n, 128);
-    const unsigned tiles = grid_for(n, 128, int64_t(num_sms()) * 8);
-    if (ld == 48)  // the 47-class products head
-        softmax_ce_tile_kernel<48><<<tiles, 128, 0, s>>>(n, C, logits, labels, rows, w, scale, G, row_loss);
-    else if (ld == 64)
-        softmax_ce_tile_kernel<64><<<tiles, 128, 0, s>>>(n, C, logits, labels, rows, w, scale, G, row_loss);
-    else if (vec && ld <= 16)
+    if (vec && ld <= 16)
         softmax_ce_rows_kernel<4><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
     else if (vec && ld <= 32)
         softmax_ce_rows_kernel<8><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
