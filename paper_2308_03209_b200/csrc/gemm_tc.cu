@@ -46,14 +46,10 @@ namespace tc {
 
 constexpr int kBM = 128;  // UMMA M (cta_group::1)
 constexpr int kMaxN = 256;
-constexpr int kConvWarps = 8;
-constexpr int kConv = kConvWarps * 32;  // converter threads (warps 0-7)
-// NT uses 8 epilogue warps (warps 8-15: two per TMEM lane quarter, even / odd
+constexpr int kConvWarps = 8;  // TN converter warps (NT: NtCfg::kCW)
+// NT uses 8 epilogue warps (after the converters: two per TMEM lane quarter, even / odd
 // 32-column chunks), then the MMA and loader warps.
 constexpr int kNtEpiWarps = 8;
-constexpr int kNtMmaWarp = 16;
-constexpr int kNtLoadWarp = 17;
-constexpr int kNtThreads = 18 * 32;
 
 // NT: 32-deep k-stages, fp16 SW64 tiles (64 B rows)
 constexpr int kNtBK = 32;
@@ -393,6 +389,11 @@ __device__ __forceinline__ void tmem_dealloc_g(uint32_t base) {
 // deepens both rings.
 template <bool PAIR>
 struct NtCfg {
+    // warp roles: converters 0 .. kCW-1, epilogue kCW .. kCW+7, MMA issuer, TMA loader
+    // (16 converter warps measured ~1 % slower than 8: the converters are not the limit)
+    static constexpr int kCW = 8;
+    static constexpr int kC = kCW * 32;
+    static constexpr int kMma = kCW + kNtEpiWarps, kLoad = kMma + 1, kThr = (kLoad + 1) * 32;
     static constexpr int kStages = PAIR ? 4 : 3;                    // MMA operand stages
     static constexpr int kStg = PAIR ? 4 : 3;                       // fp32 staging stages
     static constexpr int kBTile = (PAIR ? kMaxN / 2 : kMaxN) * 64;  // one (hi or lo) B tile, this CTA's rows
@@ -406,7 +407,7 @@ struct NtCfg {
 static_assert(NtCfg<true>::kSmem <= 232448 && NtCfg<false>::kSmem <= 232448, "NT shared memory");
 
 template <int EPI, bool AMAX, bool PAIR>
-__global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
     using Cfg = NtCfg<PAIR>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -437,15 +438,15 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
         kt = min(kt, scale_exp(*p.src[s].amax_a) + kb_exp[s]);
     }
 
-    if (warp == kNtMmaWarp) {
+    if (warp == Cfg::kMma) {
         if (lane == 0) {
             for (int s = 0; s < Cfg::kStages; ++s) {
-                mbar_init(&full[s], kConvWarps * (PAIR ? 2 : 1));
+                mbar_init(&full[s], Cfg::kCW * (PAIR ? 2 : 1));
                 mbar_init(&empty[s], 1);
             }
             for (int s = 0; s < Cfg::kStg; ++s) {
                 mbar_init(&sfull[s], 1);
-                mbar_init(&sempty[s], kConvWarps);
+                mbar_init(&sempty[s], Cfg::kCW);
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
     int kb_total = 0;
     for (int s = 0; s < p.nsrc; ++s) kb_total += p.src[s].kblocks;
 
-    if (warp == kNtLoadWarp) {
+    if (warp == Cfg::kLoad) {
         // ================= loader: one 2D TMA per stage, HBM -> fp32 staging =================
         // box 32 k (128 B) x 128 rows, SWIZZLE_128B; out-of-range rows / k are zero-filled
         Ring ring;
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                     }
                     __syncwarp();
                 }
-    } else if (warp < kConvWarps) {
+    } else if (warp < Cfg::kCW) {
         // ================= converters: staging fp32 -> scaled fp16 hi/lo (SW64) =================
         // Row-fastest mapping: 8 consecutive threads read the same chunk of 8 different rows, which
         // the 128 B swizzle spreads over distinct banks (conflict-free loads and SW64 stores).
@@ -515,18 +516,19 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                     }
                     mbar_wait(&sfull[sr.idx], sr.phase);
                     // all of the stage's shared loads first (4 x LDS.128 in flight), then convert
-                    float4 xv[2][2];
+                    constexpr int kItems = 4 * kBM / Cfg::kC;  // (row, 8-float chunk) items per thread
+                    float4 xv[kItems][2];
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const int idx = tid + j * kConv;
+                    for (int j = 0; j < kItems; ++j) {
+                        const int idx = tid + j * Cfg::kC;
                         const int r = idx & 127, c = idx >> 7;  // row, 8-float chunk (0..3)
                         const uint8_t* rowp = sg + r * (kNtBK * 4);
                         xv[j][0] = *reinterpret_cast<const float4*>(rowp + (((2 * c) ^ (r & 7)) << 4));
                         xv[j][1] = *reinterpret_cast<const float4*>(rowp + (((2 * c + 1) ^ (r & 7)) << 4));
                     }
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const int idx = tid + j * kConv;
+                    for (int j = 0; j < kItems; ++j) {
+                        const int idx = tid + j * Cfg::kC;
                         split8_store(xv[j][0], xv[j][1], sa, st, st + kNtATile, sw64_off(idx & 127, idx >> 7));
                     }
                     fence_proxy_async();
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
                     }
                 }
             }
-    } else if (warp == kNtMmaWarp) {
+    } else if (warp == Cfg::kMma) {
         // ================= MMA issuer (the pair's leader only) =================
         if (PAIR && rank != 0) {
             // the peer's tensor core work is issued by the leader
@@ -582,9 +584,9 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
         // is zero beyond N, as are TMA-filled A rows beyond M, so every chunk is full and padded
         // entries are exactly 0 (they cannot raise |max|).
         const int ew = warp & 3;                    // TMEM lanes 32*ew .. 32*ew+31
-        const int half = (warp - kConvWarps) >> 2;  // even / odd 32-column chunks
+        const int half = (warp - Cfg::kCW) >> 2;  // even / odd 32-column chunks
         const float unscale = ldexpf(1.f, -kt);
-        uint8_t* box = epi_base + (warp - kConvWarps) * kNtEpiBuf;
+        uint8_t* box = epi_base + (warp - Cfg::kCW) * kNtEpiBuf;
         float amx = 0.f;
         uint32_t t = 0;
         for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t) {
@@ -634,7 +636,7 @@ __global__ void __launch_bounds__(kNtThreads, 1) gemm_f16x3_kernel(const __grid_
     tc_fence_before();
     if constexpr (PAIR) cluster_sync();  // no remote arrivals / tensor-core work left in flight
     else __syncthreads();
-    if (warp == kNtMmaWarp) {
+    if (warp == Cfg::kMma) {
         tc_fence_after();
         tmem_dealloc_g<PAIR>(tmem_base);
     }
@@ -1376,7 +1378,7 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
         cudaLaunchConfig_t cfg{};
         cudaLaunchAttribute attr[1];
-        cfg.blockDim = dim3(tc::kNtThreads);
+        cfg.blockDim = dim3(pair ? tc::NtCfg<true>::kThr : tc::NtCfg<false>::kThr);
         cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes);
         cfg.stream = s;
         if (pair) {
