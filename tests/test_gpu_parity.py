@@ -429,3 +429,20 @@ def test_unaligned_feature_width(sc, O, d):
         olg = np.concatenate([to.part_logits(i, C).ravel() for i in range(4)])
         assert rel(lg, olg) <= REL, (e, rel(lg, olg))
         assert rel(t.grads(), to.gathered()) <= REL, (e, rel(t.grads(), to.gathered()))
+
+
+def test_more_partitions_than_edges(sc, O, golden):
+    """Karate club (78 edges) cut into 100 parts: most partitions are empty or hold only isolated
+    round-robin nodes; every kernel must accept n_i = 0 and m_i = 0 and the trajectory must match."""
+    k = golden("karate")
+    og = O.graph_build(int(k["n"]), k["edges"])
+    n = og.n
+    rng = np.random.default_rng(3)
+    lab = rng.integers(0, 3, size=n).astype(np.int32)
+    f = rng.standard_normal((n, 8)).astype(np.float32)
+    tr = np.ones(n, np.uint8)
+    z = np.zeros(n, np.uint8)
+    og.set_data(f, lab, 3, tr, z, z)
+    for de in (False, True):
+        worst, _, _ = run_traj(sc, O, og, "random", 100, 1, 8, steps=3, hidden=[16], dropedge=de, seed=5)
+        assert_within(worst)
