@@ -348,6 +348,7 @@ def run_gpu_arm(args, cfg):
             epoch += 1
         ms = ctx.timer_stop()
     launches = ctx.launch_count() - launches0
+    free_b, total_b = torch.cuda.mem_get_info(local)  # device memory in use (graph, partitions, trainer)
     trainer.profile(False)
     barrier()
     ms_step = max_over_ranks(ms / args.steps)
@@ -435,6 +436,7 @@ def run_gpu_arm(args, cfg):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "setup_s": setup_s,
+        "hbm_used_gb": round((total_b - free_b) / 1e9, 1),
         "loss_first_last": [losses[0], losses[-1]] if losses else None,
     }
     print(json.dumps(line), flush=True)
