@@ -162,7 +162,7 @@ def test_init_params(sc, golden):
 # ---------------------------------------------------------------- training step
 def run_traj(sc, O, og, algo, p, pseed, d, steps=5, **cfg):
     g = gpu_graph(sc, og, d)
-    gp = (sc.partition_random if algo == "random" else sc.partition_dbh)(g, p, pseed)
+    gp = {"random": sc.partition_random, "dbh": sc.partition_dbh, "ne": sc.partition_ne}[algo](g, p, pseed)
     op = og.partition(algo, p, pseed)
     C = g.num_classes
     ocfg = dict(cfg)
@@ -446,3 +446,10 @@ def test_more_partitions_than_edges(sc, O, golden):
     for de in (False, True):
         worst, _, _ = run_traj(sc, O, og, "random", 100, 1, 8, steps=3, hidden=[16], dropedge=de, seed=5)
         assert_within(worst)
+
+
+def test_ne_partition_trajectory(sc, O):
+    """Training on an NE vertex cut (low replication, unbalanced parts) matches the oracle."""
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    worst, _, _ = run_traj(sc, O, og, "ne", 4, 0, 8, hidden=[16, 16], dropedge=True, seed=1)
+    assert_within(worst)
