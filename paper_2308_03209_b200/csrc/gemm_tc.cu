@@ -89,7 +89,6 @@ struct alignas(64) Params {
     const float* row_scale;
     float* amax_out;
     int64_t tiles;
-    LossEpi loss;  // kEpiSoftmaxCE only
 };
 
 // ---- PTX helpers -------------------------------------------------------------
@@ -383,49 +382,6 @@ __device__ __forceinline__ void tmem_dealloc_g(uint32_t base) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(512));
 }
 
-// One row of the fused softmax-CE epilogue; z = the row's logits (C <= 64) from two
-// 32-column TMEM chunks.
-__device__ __forceinline__ void softmax_ce_row(const LossEpi& L, int64_t row, int32_t C, const uint32_t (&ra)[32],
-                                               const uint32_t (&rb)[32], float unscale) {
-    float4* g = reinterpret_cast<float4*>(L.G + row * L.ldg);
-    const int nv = static_cast<int>(L.ldg >> 2);
-    const double wr = L.w[row];
-    if (wr == 0.0) {  // nn.hpp:330
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (j < nv) g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        L.row_loss[row] = 0.0;
-        return;
-    }
-    // the logits in place (no second 64-float copy: the epilogue runs at <= 112 registers)
-    auto zval = [&](int c) { return __uint_as_float(c < 32 ? ra[c] : rb[c - 32]) * unscale; };
-    const int32_t y = L.labels[L.label_rows ? L.label_rows[row] : row];
-    float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < 64; ++c)
-        if (c < C) mx = fmaxf(mx, zval(c));
-    float se = 0.f;
-#pragma unroll
-    for (int c = 0; c < 64; ++c)
-        if (c < C) se += expf(zval(c) - mx);
-    const float lse = mx + logf(se);
-    const float sc = L.scale[row];
-    float zy = 0.f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        float q[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int c = 4 * j + e;
-            const float z = zval(c);
-            if (c == y) zy = z;
-            q[e] = c < C ? sc * (expf(z - lse) - (c == y ? 1.f : 0.f)) : 0.f;
-        }
-        if (j < nv) g[j] = make_float4(q[0], q[1], q[2], q[3]);
-    }
-    L.row_loss[row] = wr * static_cast<double>(lse - zy);
-}
-
 // Shared-memory plan of the NT kernel. PAIR: a CTA pair (cluster of 2, cta_group::2)
 // computes a 256-row tile with one M=256 MMA stream; each CTA converts its own
 // 128 A rows and holds half of the weight image's rows, so the per-SM operand
@@ -662,23 +618,6 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0 && row0 < p.M) tma_store_2d(&p.tmap_c, box, c0, static_cast<int32_t>(row0));
-            }
-            if constexpr (EPI == kEpiSoftmaxCE) {
-                // The whole logits row (n_pad <= 64) is in this lane's TMEM lane: the even-chunk warps
-                // read both 32-column chunks and run the row's softmax-CE in registers, in column
-                // order exactly like nn.cu:softmax_ce_rows_kernel (same logits values, same bits).
-                if (half == 0) {
-                    uint32_t ra[32], rb[32];
-                    tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16), ra);
-                    if (p.n_pad > 32) {
-                        tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + 32, rb);
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) rb[q] = 0u;
-                    }
-                    const int64_t row = row0 + lane;
-                    if (row < p.M) softmax_ce_row(p.loss, row, p.N, ra, rb, unscale);
-                }
             }
             tc_fence_before();
             __syncwarp();
@@ -1399,7 +1338,7 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
 
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-                float* amax_out, cudaStream_t s, const LossEpi* loss) {
+                float* amax_out, cudaStream_t s) {
     if (M <= 0 || N <= 0) return;
     if (!tc_supported(a1, a2, N) || !tc_out_supported(C, ldc))
         throw std::logic_error("gemm_f16x3: unsupported operand layout");
@@ -1429,12 +1368,6 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.epi = epi;
     p.row_scale = row_scale;
     p.amax_out = amax_out;
-    if (epi == kEpiSoftmaxCE) {
-        if (!loss || N > 64 || amax_out || (loss->ldg % 4) != 0 ||
-            (reinterpret_cast<uintptr_t>(loss->G) % 16) != 0)
-            throw std::logic_error("gemm_f16x3: fused softmax-CE needs C <= 64 and 16-byte gradient rows");
-        p.loss = *loss;
-    }
     const bool pair = nt_pair_enabled();
     if (pair)
         for (int i = 0; i < p.nsrc; ++i)
@@ -1484,7 +1417,6 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
             amax ? dispatch(std::integral_constant<int, kEpiRowScale>{}, T{})
                  : dispatch(std::integral_constant<int, kEpiRowScale>{}, F{});
             break;
-        case kEpiSoftmaxCE: dispatch(std::integral_constant<int, kEpiSoftmaxCE>{}, F{}); break;
         default: throw std::logic_error("gemm_f16x3: bad epilogue");
     }
     SC_LAUNCH_CHECK();
@@ -1503,22 +1435,17 @@ const BImage& TcGemm::image(const MatB& b, int32_t N, int32_t K, cudaStream_t s)
     return e.im;
 }
 
-bool TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2,
+void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2,
                 const float* amax2, const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi,
-                const float* row_scale, float* amax_out, const LossEpi* loss) {
+                const float* row_scale, float* amax_out) {
     cudaStream_t s = t->ctx->stream;
-    const bool fuse_ok = epi != kEpiSoftmaxCE ||
-                         (loss && N <= 64 && !amax_out && (loss->ldg % 4) == 0 &&
-                          (reinterpret_cast<uintptr_t>(loss->G) % 16) == 0);
-    if (enabled && fuse_ok && tc_supported(a1, a2, N) && tc_out_supported(C, ldc)) {
+    if (enabled && tc_supported(a1, a2, N) && tc_out_supported(C, ldc)) {
         const BImage& i1 = image(b1, N, a1.K, s);
         const BImage* i2 = a2 ? &image(*b2, N, a2->K, s) : nullptr;
-        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s, loss);
-        return true;
+        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s);
+    } else {
+        gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
     }
-    // SIMT path: the caller runs the loss kernel itself when the epilogue could not be fused
-    gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi == kEpiSoftmaxCE ? kEpiNone : epi, row_scale, s, amax_out);
-    return epi != kEpiSoftmaxCE;
 }
 
 void TcGemm::tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1,

@@ -32,7 +32,7 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
 // amax_out (optional): max|C| is atomically reduced into it.
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-                float* amax_out, cudaStream_t s, const LossEpi* loss = nullptr);
+                float* amax_out, cudaStream_t s);
 
 // Weight gradient C[N1 x N2] = A^T [B1 | B2] (K = M rows) on the tensor cores,
 // fp16x3, split-K with a fixed-order reduction (deterministic). ws needs
@@ -57,11 +57,9 @@ struct TcGemm {
     void init(sc_trainer* t);
     void invalidate() { ++version; }
     const BImage& image(const MatB& b, int32_t N, int32_t K, cudaStream_t s);
-    // returns false only for kEpiSoftmaxCE when the fused epilogue could not run (the caller
-    // then computes the loss itself from the logits)
-    bool nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2, const float* amax2,
+    void nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2, const float* amax2,
             const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-            float* amax_out, const LossEpi* loss = nullptr);
+            float* amax_out);
     // s / ws: stream and split-K workspace (default: the context stream, t->ws)
     void tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
             const float* amax_b2, int64_t M, float* C, int64_t ldc, cudaStream_t s = nullptr, float* ws = nullptr);

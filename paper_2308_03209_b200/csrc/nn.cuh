@@ -37,20 +37,7 @@ struct MatB {
     bool nn = false;
 };
 
-enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2, kEpiSoftmaxCE = 3 };
-
-// Fused softmax-CE (nn.hpp:317-345) in the head GEMM's epilogue (kEpiSoftmaxCE):
-// per row r of the logits: G[r] = scale[r] * (softmax - onehot(label)), row_loss[r]
-// = w[r] * (lse - z_y); rows with w == 0 get G = 0, loss 0.
-struct LossEpi {
-    const int32_t* labels = nullptr;
-    const int32_t* label_rows = nullptr;  // local -> global row for labels (nullable)
-    const double* w = nullptr;
-    const float* scale = nullptr;
-    float* G = nullptr;
-    int64_t ldg = 0;
-    double* row_loss = nullptr;
-};
+enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2 };
 
 // C[M x N] = A1 * op(B1) (+ A2 * op(B2)), fp32 in/out, fp32 accumulate, then epilogue.
 // amax_out (optional): atomically max-reduced with |C| (the next GEMM's operand scale).

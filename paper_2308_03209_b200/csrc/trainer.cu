@@ -306,10 +306,8 @@ double spmm_bytes(const Rows& R, int H, bool bwd) {
     return b;
 }
 
-// sage_forward (nn.hpp:192-242). Writes logits; keeps the cache in t's buffers. With `loss`
-// the head GEMM also runs softmax-CE in its epilogue (nn.hpp:317-345); returns false when it
-// could not (the caller then runs the loss kernel on the logits).
-bool forward(sc_trainer* t, const Rows& R, float* logits, const LossEpi* loss = nullptr) {
+// sage_forward (nn.hpp:192-242). Writes logits; keeps the cache in t's buffers.
+void forward(sc_trainer* t, const Rows& R, float* logits) {
     cudaStream_t s = t->ctx->stream;
     Profiler& P = t->prof;
     const int64_t n = R.n;
@@ -344,11 +342,9 @@ bool forward(sc_trainer* t, const Rows& R, float* logits, const LossEpi* loss = 
     const MatA emb = t->L == 0 ? x0 : MatA{t->X[t->L].get(), t->E, nullptr, t->E};
     P.begin("gemm_head", 4.0 * n * (t->E + t->C), s, 2.0 * n * t->E * t->C);
     const float* emb_amax = t->L == 0 ? t->g->feat_amax.get() : t->amax_x(t->L);
-    const bool fused =
-        t->tc.nt(t, emb, emb_amax, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, nullptr,
-                 logits, t->Cp, n, t->C, loss ? kEpiSoftmaxCE : kEpiNone, nullptr, nullptr, loss);
+    t->tc.nt(t, emb, emb_amax, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, nullptr, logits,
+             t->Cp, n, t->C, kEpiNone, nullptr, nullptr);
     P.end(s);
-    return fused && loss;
 }
 
 // sage_backward (nn.hpp:246-293) into partition i's gradient slot; each
@@ -461,19 +457,9 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get(),
                  st.x0.get(), t->dp, &st.heavy};
     SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
-    LossEpi le;  // softmax-CE fused into the head GEMM's epilogue where the tensor-core path runs
-    le.labels = t->g->labels.get();
-    le.label_rows = pd.nodes.get();
-    le.w = st.w.get();
-    le.scale = st.scale.get();
-    le.G = t->G.get();
-    le.ldg = t->Cp;
-    le.row_loss = t->row_loss.get();
-    const bool fused = forward(t, R, st.logits.get(), t->loss == 0 && st.n > 0 ? &le : nullptr);
+    forward(t, R, st.logits.get());
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
-    if (fused)
-        ;  // G and the per-row losses came out of the head GEMM
-    else if (t->loss == 0)
+    if (t->loss == 0)
         softmax_ce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
                    t->G.get(), t->row_loss.get(), s);
     else
