@@ -116,3 +116,16 @@ def test_tn_f16x3_matches_fp64(sc, case):
     print(f"TN {case}: tcgen05 fp16x3 rel err {e_tc:.2e}, simt fp32 {e_simt:.2e}")
     assert e_simt <= 1e-5
     assert e_tc <= 1e-5
+
+
+def test_tn_smem_operand_path_subprocess():
+    """The CTA-pair weight-gradient kernel with the A' operand in shared memory (SC_TN_ATMEM=0,
+    read once per process) passes the same fp64 checks."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SC_TN_ATMEM="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_gemm.py"), "-q", "-k",
+                        "test_tn_f16x3_matches_fp64"], capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -453,3 +453,18 @@ def test_ne_partition_trajectory(sc, O):
     og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
     worst, _, _ = run_traj(sc, O, og, "ne", 4, 0, 8, hidden=[16, 16], dropedge=True, seed=1)
     assert_within(worst)
+
+
+def test_side_stream_overlap_path(sc, O, monkeypatch):
+    """SC_OVERLAP=1 (dh-only weight gradients on a high-priority side stream, opt-in) gives the same
+    bits as the single-stream schedule."""
+    og = O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    out = []
+    for ov in ("0", "1"):
+        monkeypatch.setenv("SC_OVERLAP", ov)  # read when the trainer is created
+        g = gpu_graph(sc, og, 8)
+        t = sc.CoFreeTrainer(g, sc.partition_random(g, 4, 3),
+                             sc.TrainConfig(layers=2, hidden=[16], use_dropedge=True, seed=1))
+        out.append(([t.step(e) for e in range(3)], t.params()))
+    assert out[0][0] == out[1][0]
+    np.testing.assert_array_equal(out[0][1], out[1][1])
