@@ -89,6 +89,7 @@ struct alignas(64) Params {
     const float* row_scale;
     float* amax_out;
     int64_t tiles;
+    unsigned long long* trace;  // optional (SC_TN_TRACE_BUILD + SC_TN_TRACE=1), as TnParams::trace
 };
 
 // ---- PTX helpers -------------------------------------------------------------
@@ -406,6 +407,19 @@ struct NtCfg {
 };
 static_assert(NtCfg<true>::kSmem <= 232448 && NtCfg<false>::kSmem <= 232448, "NT shared memory");
 
+// Diagnostics (build with -DSC_TN_TRACE_BUILD, run with SC_TN_TRACE=1): cycles each
+// role spends in its barrier waits, summed over CTAs and printed per launch (TN and NT).
+#ifdef SC_TN_TRACE_BUILD
+#define TN_TIMED_WAIT(acc_var, call)                                              \
+    do {                                                                          \
+        const long long t0_ = p.trace ? clock64() : 0;                            \
+        call;                                                                     \
+        if (p.trace) acc_var += static_cast<unsigned long long>(clock64() - t0_); \
+    } while (0)
+#else
+#define TN_TIMED_WAIT(acc_var, call) call
+#endif
+
 template <int EPI, bool AMAX, bool PAIR>
 __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const __grid_constant__ Params p) {
     using Cfg = NtCfg<PAIR>;
@@ -424,6 +438,10 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+#ifdef SC_TN_TRACE_BUILD
+    unsigned long long w_a = 0, w_b = 0;
+    const long long t_start = p.trace ? clock64() : 0;
+#endif
     const int64_t tile0 = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
     const int64_t tstep = PAIR ? (gridDim.x >> 1) : gridDim.x;
     const int32_t nloc = PAIR ? (p.n_pad >> 1) : p.n_pad;  // weight rows held by this CTA
@@ -476,7 +494,7 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
         for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
             for (int src = 0; src < p.nsrc; ++src)
                 for (int kb = 0; kb < p.src[src].kblocks; ++kb, ring.next(Cfg::kStg)) {
-                    mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
+                    TN_TIMED_WAIT(w_a, mbar_wait(&sempty[ring.idx], ring.phase ^ 1));
                     if (lane == 0) {
                         mbar_arrive_expect_tx(&sfull[ring.idx], kNtStgBytes);
                         tma_load_2d(stg_base + ring.idx * kNtStgBytes, &p.src[src].tmap, kb * kNtBK,
@@ -499,7 +517,7 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                 for (int kb = 0; kb < S.kblocks; ++kb, mr.next(Cfg::kStages), sr.next(Cfg::kStg)) {
                     uint8_t* st = smem + mr.idx * Cfg::kStage;
                     const uint8_t* sg = stg_base + sr.idx * kNtStgBytes;
-                    mbar_wait(&empty[mr.idx], mr.phase ^ 1);
+                    TN_TIMED_WAIT(w_a, mbar_wait(&empty[mr.idx], mr.phase ^ 1));
                     if (tid == 0) {
                         if constexpr (PAIR) {
                             // image rows: [kb][plane][n_pad]; this CTA's half starts at rank * nloc
@@ -514,7 +532,7 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                                      &full[mr.idx]);
                         }
                     }
-                    mbar_wait(&sfull[sr.idx], sr.phase);
+                    TN_TIMED_WAIT(w_b, mbar_wait(&sfull[sr.idx], sr.phase));
                     // all of the stage's shared loads first (4 x LDS.128 in flight), then convert
                     constexpr int kItems = 4 * kBM / Cfg::kC;  // (row, 8-float chunk) items per thread
                     float4 xv[kItems][2];
@@ -551,12 +569,12 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
             for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t) {
                 const uint32_t acc = t & 1;
                 const uint32_t d_tmem = tmem_base + acc * 256;
-                if constexpr (PAIR) mbar_wait_cluster(&tempty[acc], ((t >> 1) & 1) ^ 1);
-                else mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+                if constexpr (PAIR) TN_TIMED_WAIT(w_b, mbar_wait_cluster(&tempty[acc], ((t >> 1) & 1) ^ 1));
+                else TN_TIMED_WAIT(w_b, mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1));
                 tc_fence_after();
                 for (int kbg = 0; kbg < kb_total; ++kbg, mr.next(Cfg::kStages)) {
-                    if constexpr (PAIR) mbar_wait_cluster(&full[mr.idx], mr.phase);
-                    else mbar_wait(&full[mr.idx], mr.phase);
+                    if constexpr (PAIR) TN_TIMED_WAIT(w_a, mbar_wait_cluster(&full[mr.idx], mr.phase));
+                    else TN_TIMED_WAIT(w_a, mbar_wait(&full[mr.idx], mr.phase));
                     tc_fence_after();
                     if (lane == 0) {
                         const uint8_t* st = smem + mr.idx * Cfg::kStage;
@@ -591,7 +609,7 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
         uint32_t t = 0;
         for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t) {
             const uint32_t acc = t & 1;
-            mbar_wait(&tfull[acc], (t >> 1) & 1);
+            TN_TIMED_WAIT(w_a, mbar_wait(&tfull[acc], (t >> 1) & 1));
             tc_fence_after();
             const int64_t row0 = tile * Cfg::kRows + rank * kBM + ew * 32;  // this warp's 32 output rows
             float sc = 1.f;
@@ -599,7 +617,7 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
             for (int c0 = half * 32; c0 < p.n_pad; c0 += 64) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
-                if (lane == 0) bulk_wait_read<0>();  // the previous store has read the box
+                if (lane == 0) TN_TIMED_WAIT(w_b, bulk_wait_read<0>());  // the previous store has read the box
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -633,6 +651,17 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
             if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out), __float_as_uint(amx));
         }
     }
+#ifdef SC_TN_TRACE_BUILD
+    if (p.trace && lane == 0) {  // roles: 0 converters, 1 epilogue, 2 MMA, 3 loader
+        const int role = warp < Cfg::kCW ? 0 : warp < Cfg::kMma ? 1 : warp == Cfg::kMma ? 2 : 3;
+        if (role != 2 || !PAIR || rank == 0) {
+            atomicAdd(p.trace + 4 * role + 0, w_a);
+            atomicAdd(p.trace + 4 * role + 1, w_b);
+            atomicAdd(p.trace + 4 * role + 2, static_cast<unsigned long long>(clock64() - t_start));
+            atomicAdd(p.trace + 4 * role + 3, 1ull);
+        }
+    }
+#endif
     tc_fence_before();
     if constexpr (PAIR) cluster_sync();  // no remote arrivals / tensor-core work left in flight
     else __syncthreads();
@@ -781,18 +810,6 @@ struct TnCfg {
 static_assert(TnCfg<true>::kSmem <= 232448 && TnCfg<false>::kSmem <= 232448, "TN shared memory");
 static_assert(TnCfg<true, true>::kSmem <= 232448 && 256 + 32 * TnCfg<true, true>::kStages <= 512, "TN (A in TMEM)");
 
-// Diagnostics (build with -DSC_TN_TRACE_BUILD, run with SC_TN_TRACE=1): cycles each
-// role spends in its barrier waits, summed over CTAs and printed per launch.
-#ifdef SC_TN_TRACE_BUILD
-#define TN_TIMED_WAIT(acc_var, call)                                              \
-    do {                                                                          \
-        const long long t0_ = p.trace ? clock64() : 0;                            \
-        call;                                                                     \
-        if (p.trace) acc_var += static_cast<unsigned long long>(clock64() - t0_); \
-    } while (0)
-#else
-#define TN_TIMED_WAIT(acc_var, call) call
-#endif
 
 template <bool PAIR, bool AT = false>
 __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
@@ -1368,6 +1385,16 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.epi = epi;
     p.row_scale = row_scale;
     p.amax_out = amax_out;
+    static const bool trace = [] {
+        const char* e = std::getenv("SC_TN_TRACE");
+        return e && std::atoi(e) != 0;
+    }();
+    static DevBuf<unsigned long long> trace_buf;
+    if (trace) {
+        trace_buf.ensure(16);
+        SC_CUDA(cudaMemsetAsync(trace_buf.get(), 0, 16 * sizeof(unsigned long long), s));
+        p.trace = trace_buf.get();
+    }
     const bool pair = nt_pair_enabled();
     if (pair)
         for (int i = 0; i < p.nsrc; ++i)
@@ -1421,6 +1448,18 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     }
     SC_LAUNCH_CHECK();
     count_launch();
+    if (trace) {
+        unsigned long long h[16];
+        SC_CUDA(cudaMemcpyAsync(h, trace_buf.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+        SC_CUDA(cudaStreamSynchronize(s));
+        const char* names[4] = {"conv(empty,sfull)", "epi(tfull,boxwait)", "mma(full,tempty)", "load(sempty,-)"};
+        std::fprintf(stderr, "NT trace M=%lld N=%d K=%d+%d:", static_cast<long long>(M), N, a1.K, a2 ? a2->K : 0);
+        for (int r = 0; r < 4; ++r) {
+            const double c = h[4 * r + 3] ? double(h[4 * r + 3]) : 1.0;
+            std::fprintf(stderr, " %s %.0f/%.0f of %.0f;", names[r], h[4 * r] / c, h[4 * r + 1] / c, h[4 * r + 2] / c);
+        }
+        std::fprintf(stderr, "\n");
+    }
 }
 
 void TcGemm::init(sc_trainer* t) { enabled = t->gemm_mode == 0; }

@@ -22,6 +22,15 @@ if which == "nt":
         t0 = time.perf_counter()
         sc.debug_gemm(A, B, epi=1)
         print("nt wall", time.perf_counter() - t0)
+elif which == "nt512":  # the update GEMM's dual-source shape: [mean | h] U^T (K = 256 + 256)
+    A = rng.standard_normal((M, 256), dtype=np.float32)
+    A2 = rng.standard_normal((M, 256), dtype=np.float32)
+    B = rng.standard_normal((256, 256), dtype=np.float32)
+    B2 = rng.standard_normal((256, 256), dtype=np.float32)
+    for _ in range(2):
+        t0 = time.perf_counter()
+        sc.debug_gemm(A, B, A2=A2, B2=B2)
+        print("nt512 wall", time.perf_counter() - t0)
 elif which == "tn512":  # the update layer's dU = dh^T [mean | h] shape (N2 = 512)
     A = rng.standard_normal((M, 256), dtype=np.float32)
     B = rng.standard_normal((M, 256), dtype=np.float32)
