@@ -96,12 +96,21 @@ std::vector<HostMatrix> read_checkpoint(const std::string& path) {
     in.read(magic, 4);
     if (!in || std::memcmp(magic, "CFCK", 4) != 0)
         throw std::runtime_error(path + ": not a checkpoint file (bad magic)");
+    in.seekg(0, std::ios::end);
+    const uint64_t file_bytes = static_cast<uint64_t>(in.tellg());
+    in.seekg(4, std::ios::beg);
     const uint64_t layers = read_u64(in);
+    // Every matrix costs at least its 16-byte header, so a corrupt count or shape is rejected
+    // before anything is allocated from it.
+    if (layers > file_bytes / 32) throw std::runtime_error("checkpoint: truncated header");
     std::vector<HostMatrix> mats;
     for (uint64_t k = 0; k < 2 * layers + 1; ++k) {
         HostMatrix m;
         m.rows = read_u64(in);
         m.cols = read_u64(in);
+        const uint64_t left = file_bytes - static_cast<uint64_t>(in.tellg());
+        if (m.cols != 0 && m.rows > left / sizeof(double) / m.cols)
+            throw std::runtime_error("checkpoint: truncated matrix data");
         m.v.resize(static_cast<size_t>(m.rows * m.cols));
         in.read(reinterpret_cast<char*>(m.v.data()), static_cast<std::streamsize>(m.v.size() * sizeof(double)));
         if (!in) throw std::runtime_error("checkpoint: truncated matrix data");
