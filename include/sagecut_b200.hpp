@@ -98,7 +98,17 @@ public:
         refresh();
     }
 
+    // Graph::multilabels (graph.hpp:64): num_nodes x C row-major 0/1; replaces the class ids
+    // (bce training, micro-F1 evaluation). Call after set_data.
+    void set_multilabels(const std::vector<float>& targets, int classes) {
+        check(sc_graph_set_multilabels(get(), targets.data(), classes));
+        refresh();
+        multilabel_ = true;
+    }
+    bool is_multilabel() const { return multilabel_; }  // graph.hpp:74
+
 private:
+    bool multilabel_ = false;
     void refresh() {
         std::int32_t d = 0, c = 0;
         check(sc_graph_info(get(), &num_nodes, &m_, &d, &c));
@@ -355,9 +365,42 @@ struct EpochMetrics {  // trainer.hpp:38-46
     double train_loss = 0.0, train_metric = 0.0, val_metric = 0.0, test_metric = 0.0, grad_norm = 0.0;
     std::uint64_t comm_floats = 0;
 };
+enum class CommMode { cofree, halo_sync_model };  // trainer.hpp:48
+struct CommReport {                               // trainer.hpp:50-55
+    CommMode mode = CommMode::cofree;
+    std::uint64_t floats_per_iteration = 0;
+    std::uint64_t gradient_floats = 0;
+    std::uint64_t embedding_floats = 0;
+};
+// trainer.cpp:38-49
+inline CommReport comm_volume(CommMode mode, int num_parts, std::size_t param_count, std::size_t num_layers,
+                              std::size_t hidden_dim, std::size_t total_halo) {
+    CommReport r;
+    r.mode = mode;
+    check(sc_comm_volume(mode == CommMode::cofree ? 0 : 1, num_parts, param_count, num_layers, hidden_dim,
+                         total_halo, &r.floats_per_iteration, &r.gradient_floats, &r.embedding_floats));
+    return r;
+}
+struct CommAudit {  // trainer.hpp:61-67
+    std::vector<std::uint64_t> gradient_floats_per_epoch;
+    std::uint64_t embedding_floats = 0;
+};
+// partition.cpp:344-362
+inline double expected_rf_random(int num_parts, std::int64_t degree) {
+    double x = 0;
+    check(sc_expected_rf_random(num_parts, degree, &x));
+    return x;
+}
+inline double imbalance_lower_bound(int num_parts, std::int64_t max_degree, std::int64_t min_degree) {
+    double x = 0;
+    check(sc_imbalance_lower_bound(num_parts, max_degree, min_degree, &x));
+    return x;
+}
+
 struct TrainResult {  // trainer.hpp:71-75 (model as the flat for_each_matrix vector)
     std::vector<float> model;
     std::vector<EpochMetrics> metrics;
+    CommAudit audit;
     int in_dim = 0, num_classes = 0;  // model dims, for save_checkpoint
     std::vector<int> hidden;
 };
@@ -424,6 +467,10 @@ inline TrainResult train_cofree(const Graph& g, const VertexCutPartition& part, 
         EpochMetrics m;
         m.epoch = e;
         check(sc_trainer_step(t, e, &m.train_loss, &m.grad_norm));
+        std::uint64_t grad_floats = 0, emb_floats = 0;
+        check(sc_trainer_comm_audit(t, &grad_floats, &emb_floats));
+        res.audit.gradient_floats_per_epoch.push_back(grad_floats);
+        res.audit.embedding_floats += emb_floats;
         if (c.evaluate) check(sc_trainer_evaluate(t, &m.train_metric, &m.val_metric, &m.test_metric));
         m.comm_floats = static_cast<std::uint64_t>(part.num_parts) * static_cast<std::uint64_t>(P);
         res.metrics.push_back(m);
@@ -436,6 +483,17 @@ inline TrainResult train_cofree(const Graph& g, const VertexCutPartition& part, 
     return res;
 }
 
+// evaluate (trainer.cpp:101-112): full-graph metric of a trained model over one split mask
+// (accuracy, or micro-F1 on multi-label graphs), forward-only on the device.
+inline double evaluate(const TrainResult& model, const Graph& g, const std::vector<std::uint8_t>& mask) {
+    if (mask.size() != static_cast<std::size_t>(g.num_nodes))
+        throw std::invalid_argument("evaluate: mask length != node count");
+    double x = 0.0;
+    check(sc_evaluate(g.context().get(), g.get(), model.model.data(), model.hidden.data(),
+                      static_cast<std::int32_t>(model.hidden.size()), mask.data(), &x));
+    return x;
+}
+
 // train_full_graph (trainer.hpp:164-200): the p = 1 vertex cut (every edge in part 0, local ids =
 // global ids) trained with unit loss weights and no DropEdge — the reference's degeneracy
 // (test_trainer.cpp:69-79) — on the same device trainer.
@@ -446,6 +504,7 @@ inline TrainResult train_full_graph(const Graph& g, const TrainConfig& c) {
     fc.use_dropedge = false;
     TrainResult r = train_cofree(g, part, fc);
     for (auto& m : r.metrics) m.comm_floats = 0;
+    r.audit = CommAudit{};  // nothing crosses workers in full-graph training
     return r;
 }
 

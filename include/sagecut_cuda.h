@@ -70,6 +70,13 @@ sc_status sc_build_graph_dev(sc_ctx* ctx, int32_t num_nodes, const int32_t* raw_
  * (Graph::features, labels, num_classes, train/val/test_mask). Host buffers. */
 sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, const int32_t* labels,
                             int32_t num_classes, const uint8_t* train, const uint8_t* val, const uint8_t* test);
+/* Multi-label targets (Graph::multilabels, graph.hpp:64; load_labels' multi-label
+ * branch, graph_io.cpp:206-229): n x C row-major, every entry 0 or 1 (else SC_EINVAL
+ * "loss: bce targets must be 0 or 1", nn.hpp:366-367). Replaces the class ids;
+ * the graph then trains with bce only (softmax_ce -> "softmax_ce requires
+ * multi-class labels", trainer.hpp:207-208) and evaluates with micro-F1
+ * (trainer.cpp:72-87). Call after sc_graph_set_data (features + masks). */
+sc_status sc_graph_set_multilabels(sc_graph* g, const float* targets, int32_t num_classes);
 /* Replace only the features (e.g. a new batch of the same graph). Host or device source. */
 sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_device);
 sc_status sc_graph_info(sc_graph* g, int32_t* num_nodes, int64_t* num_edges, int32_t* dim, int32_t* num_classes);
@@ -109,6 +116,14 @@ sc_status sc_vcut_warnings(sc_vcut* vc, char* buf, int64_t cap, int64_t* needed)
 sc_status sc_vcut_num_parts(sc_vcut* vc, int32_t* num_parts);
 sc_status sc_vcut_assignment(sc_vcut* vc, int32_t* out);
 sc_status sc_vcut_part_sizes(sc_vcut* vc, int32_t part, int64_t* n_local, int64_t* n_edges);
+/* Partition ownership for multi-GPU training (one process per GPU): vertex cuts
+ * built on g after this call materialise only the parts i with
+ * i % world == rank (the ones that rank trains, trainer.hpp:283-288's worker
+ * assignment); every other part keeps its sizes (and its nodes' replication
+ * counts) but no device arrays, so a rank holds ~p/world partitions instead of
+ * all p. Accessing a part that is not held gives SC_EINVAL. Default: (0, 1). */
+sc_status sc_graph_set_part_ownership(sc_graph* g, int32_t rank, int32_t world);
+sc_status sc_vcut_part_held(sc_vcut* vc, int32_t part, int32_t* held);
 /* PartSubgraph fields (partition.hpp:14-31); any pointer may be NULL. */
 sc_status sc_vcut_part_copy(sc_vcut* vc, int32_t part, int32_t* nodes, int32_t* edges_uv, int32_t* edge_global_ids,
                             int32_t* local_degrees, int64_t* offsets, int32_t* neighbors, int32_t* edge_ids,
@@ -163,6 +178,20 @@ sc_status sc_trainer_create(sc_ctx* ctx, sc_graph* g, sc_vcut* vc, const sc_trai
  * (optional at world == 1: a single-rank communicator runs the same exchange). */
 sc_status sc_nccl_unique_id(uint8_t out[128]);
 sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
+/* Host transport for the gradient exchange, instead of NCCL (multi-process
+ * runs without a GPU per rank, e.g. several ranks time-sharing one device in
+ * tests, or any collective library the caller already runs). Called once per
+ * (exchange round, bucket) on the stepping thread with this rank's
+ * contribution in `send` (bytes_per_rank bytes, host) and must return, in
+ * `recv`, all ranks' contributions concatenated in rank order (an all-gather,
+ * world * bytes_per_rank bytes); kind 0 = one partition's f32 gradient bucket
+ * (bucket = parameter matrix in for_each_matrix order), kind 1 = the round's
+ * f64 partition losses (bucket = -1). Non-zero return = failure (SC_ERUNTIME).
+ * The bits moved are the same as over NCCL, so results stay bitwise
+ * independent of the rank count. fn = NULL restores NCCL. */
+typedef int32_t (*sc_exchange_fn)(void* user, int32_t kind, int32_t round, int32_t bucket, const void* send,
+                                  void* recv, int64_t bytes_per_rank);
+sc_status sc_trainer_set_exchange(sc_trainer* t, sc_exchange_fn fn, void* user);
 /* One epoch of train_cofree_impl (trainer.hpp:255-302): every local
  * partition's forward / loss / backward, the gradient exchange, grad_norm and
  * one Adam step. Outputs are host scalars (the only D2H of the step). */
@@ -185,6 +214,22 @@ sc_status sc_trainer_get_part_loss(sc_trainer* t, int32_t part, double* loss);
 sc_status sc_trainer_get_part_mask(sc_trainer* t, int32_t part, int32_t* mask_index);
 /* evaluate_splits (trainer.hpp:132-140): full-graph forward + accuracy. */
 sc_status sc_trainer_evaluate(sc_trainer* t, double* train, double* val, double* test);
+/* evaluate (trainer.cpp:101-112) of the trainer's current model over one split
+ * mask (n bytes, host): accuracy, or micro-F1 on multi-label graphs. SC_EINVAL
+ * "evaluate: empty mask" when no node is masked. */
+sc_status sc_trainer_evaluate_mask(sc_trainer* t, const uint8_t* mask, double* metric);
+/* evaluate (trainer.cpp:101-112) of a given model: flat f32 parameters in
+ * for_each_matrix order for in_dim = the graph's feature dim, hidden[layers],
+ * num_classes = the graph's classes; forward-only on the device. */
+sc_status sc_evaluate(sc_ctx* ctx, sc_graph* g, const float* theta, const int32_t* hidden, int32_t layers,
+                      const uint8_t* mask, double* metric);
+/* CommAudit (trainer.hpp:61-76, TrainResult::audit): parameter-gradient floats this
+ * rank's partitions handed to the exchange in the last step (p * |theta| at
+ * world 1) and node-embedding floats (always 0: none cross partitions). */
+sc_status sc_trainer_comm_audit(sc_trainer* t, uint64_t* gradient_floats, uint64_t* embedding_floats);
+/* GEMMs that ran on the fp32 SIMT kernels although the tensor-core path was
+ * enabled (operand layout not TMA-compatible), since the trainer was created. */
+sc_status sc_trainer_fallback_count(sc_trainer* t, int64_t* count);
 /* Per-kernel timing of the last step (CUDA events), for bench.py's roofline. */
 sc_status sc_trainer_profile(sc_trainer* t, int32_t enable);
 sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms, double* bytes, int32_t cap,
@@ -193,6 +238,17 @@ sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms,
  * the order of sc_trainer_kernel_times (0 for non-GEMM groups). */
 sc_status sc_trainer_kernel_flops(sc_trainer* t, double* flops, int32_t cap, int32_t* count);
 sc_status sc_trainer_destroy(sc_trainer* t);
+
+/* ---- analytic models (host only) ------------------------------------------- */
+/* comm_volume (trainer.cpp:38-49): mode 0 cofree (p * |theta| gradient floats per
+ * iteration), 1 halo_sync_model (+ 2 * L * total_halo * hidden embedding floats). */
+sc_status sc_comm_volume(int32_t mode, int32_t num_parts, uint64_t param_count, uint64_t num_layers,
+                         uint64_t hidden_dim, uint64_t total_halo, uint64_t* floats_per_iteration,
+                         uint64_t* gradient_floats, uint64_t* embedding_floats);
+/* expected_rf_random (partition.cpp:344-349): p (1 - (1 - 1/p)^degree). */
+sc_status sc_expected_rf_random(int32_t num_parts, int64_t degree, double* out);
+/* imbalance_lower_bound (partition.cpp:351-362). */
+sc_status sc_imbalance_lower_bound(int32_t num_parts, int64_t max_degree, int64_t min_degree, double* out);
 
 /* ---- files (byte-compatible with the reference's writers) ------------------ */
 /* save_partition (partition_io.cpp:12-29): JSON {num_parts, edge_assignment,

@@ -371,6 +371,49 @@ int ref_graph_set_data(void* gp, const float* features, int d, const std::int32_
     });
 }
 
+// A multi-label target matrix (n x C of 0/1 floats), as load_labels' multi-label
+// branch leaves the graph (graph_io.cpp:206-229): multilabels set, labels cleared.
+int ref_graph_set_multilabels(void* gp, const float* y, int classes) {
+    return guard([&] {
+        auto* g = static_cast<Graph*>(gp);
+        const auto n = static_cast<Eigen::Index>(g->num_nodes);
+        g->multilabels.resize(n, classes);
+        for (Eigen::Index r = 0; r < n; ++r)
+            for (int c = 0; c < classes; ++c) g->multilabels(r, c) = static_cast<double>(y[r * classes + c]);
+        g->num_classes = classes;
+        g->labels.clear();
+    });
+}
+
+// The reference's evaluate (trainer.cpp:101-112) of a flat f64 model.
+int ref_evaluate(void* gp, const double* theta, const int* hidden, int layers, const std::uint8_t* mask,
+                 double* out) {
+    return guard([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        auto model = make_sage_model<double>(g.features.cols(), hidden_vec(hidden, layers), g.num_classes, 0);
+        unflatten(model, theta);
+        *out = evaluate(model, g, std::span<const std::uint8_t>(mask, static_cast<std::size_t>(g.num_nodes)));
+    });
+}
+
+// comm_volume (trainer.cpp:38-49): out = {floats_per_iteration, gradient_floats, embedding_floats}
+int ref_comm_volume(int mode, int num_parts, std::uint64_t params, std::uint64_t layers, std::uint64_t hidden,
+                    std::uint64_t halo, std::uint64_t* out) {
+    return guard([&] {
+        const CommReport r = comm_volume(mode == 0 ? CommMode::cofree : CommMode::halo_sync_model, num_parts,
+                                         params, layers, hidden, halo);
+        out[0] = r.floats_per_iteration;
+        out[1] = r.gradient_floats;
+        out[2] = r.embedding_floats;
+    });
+}
+int ref_expected_rf_random(int p, std::int64_t degree, double* out) {
+    return guard([&] { *out = expected_rf_random(p, degree); });
+}
+int ref_imbalance_lower_bound(int p, std::int64_t max_degree, std::int64_t min_degree, double* out) {
+    return guard([&] { *out = imbalance_lower_bound(p, max_degree, min_degree); });
+}
+
 // ---- Partitioning (proj/src/partition.cpp) ---------------------------------------
 // algo: 0 random, 1 dbh, 2 ne, 3 edge-cut greedy -> ec2vc
 void* ref_partition(void* gp, int algo, int p, std::uint64_t seed) {
@@ -642,12 +685,18 @@ int ref_train_full_graph(void* gp, const int* hidden, int layers, double lr, int
 
 int ref_train_cofree(void* gp, void* pp, const int* hidden, int layers, double lr, int loss, int reweight,
                      int use_dropedge, int k, double ratio, std::uint64_t seed, int f32, int workers, int epochs,
-                     double* final_params, double* losses, double* gnorms, double* metrics /* epochs x 3 */) {
+                     double* final_params, double* losses, double* gnorms, double* metrics /* epochs x 3 */,
+                     std::uint64_t* audit /* epochs gradient floats + embedding floats, optional */) {
     return guard([&] {
         const auto cfg = make_config(hidden, layers, lr, loss, reweight, use_dropedge, k, ratio, seed, f32,
                                      workers, epochs);
         const auto res = train_cofree(*static_cast<Graph*>(gp), *static_cast<VertexCutPartition*>(pp), cfg);
         flatten(res.model, final_params);
+        if (audit) {
+            for (std::size_t e = 0; e < res.audit.gradient_floats_per_epoch.size(); ++e)
+                audit[e] = res.audit.gradient_floats_per_epoch[e];
+            audit[res.audit.gradient_floats_per_epoch.size()] = res.audit.embedding_floats;
+        }
         for (std::size_t e = 0; e < res.metrics.size(); ++e) {
             losses[e] = res.metrics[e].train_loss;
             gnorms[e] = res.metrics[e].grad_norm;

@@ -112,8 +112,11 @@ struct Graph {
     std::vector<double> features;  // n x d row-major
     int d = 0;
     std::vector<i32> labels;
+    std::vector<double> multilabels;  // n x C of 0/1 (graph.hpp:64); empty when multi-class
     int num_classes = 0;
     std::vector<std::uint8_t> train, val, test;
+    bool is_multilabel() const { return !multilabels.empty(); }  // graph.hpp:74
+    bool has_labels() const { return !labels.empty() || is_multilabel(); }  // graph.hpp:72
 };
 
 Graph build_graph(i32 n, std::vector<std::pair<i32, i32>> raw) {
@@ -829,6 +832,39 @@ Model<S> zeros_like(const Model<S>& m) {
     return z;
 }
 
+// trainer.cpp:66-97 metric_from_logits: micro-F1 (positives at logit > 0) for
+// multi-label graphs, else accuracy of the first arg-max; 0 for an empty mask.
+template <class S>
+double metric_from_logits(const Mat<S>& lg, const Graph& g, const std::uint8_t* mask) {
+    std::size_t masked = 0;
+    for (i32 v = 0; v < g.n; ++v) masked += mask[v];
+    if (masked == 0) return 0.0;
+    if (g.is_multilabel()) {
+        std::int64_t tp = 0, fp = 0, fn = 0;
+        for (i32 v = 0; v < g.n; ++v) {
+            if (!mask[v]) continue;
+            for (i64 c = 0; c < lg.c; ++c) {
+                const bool pred = static_cast<double>(lg(v, c)) > 0.0;
+                const bool truth = g.multilabels[static_cast<std::size_t>(v) * lg.c + c] != 0.0;
+                tp += pred && truth;
+                fp += pred && !truth;
+                fn += !pred && truth;
+            }
+        }
+        const std::int64_t denom = 2 * tp + fp + fn;
+        return denom == 0 ? 0.0 : 2.0 * static_cast<double>(tp) / static_cast<double>(denom);
+    }
+    std::size_t correct = 0;
+    for (i32 v = 0; v < g.n; ++v) {
+        if (!mask[v]) continue;
+        i64 best = 0;
+        for (i64 c = 1; c < lg.c; ++c)
+            if (static_cast<double>(lg(v, c)) > static_cast<double>(lg(v, best))) best = c;
+        correct += best == g.labels[v];
+    }
+    return static_cast<double>(correct) / static_cast<double>(masked);
+}
+
 struct TrainerBase {
     virtual ~TrainerBase() = default;
     virtual void step(int epoch, double* loss, double* gnorm) = 0;
@@ -886,8 +922,10 @@ struct Trainer final : TrainerBase {
             if (ratio < 0.0 || ratio >= 1.0) throw std::invalid_argument("drop_ratio must lie in [0, 1)");
         }
         if (g.features.empty()) throw std::invalid_argument("training requires node features");
-        if (g.labels.empty()) throw std::invalid_argument("training requires labels");
+        if (!g.has_labels()) throw std::invalid_argument("training requires labels");
         if (g.train.empty()) throw std::invalid_argument("training requires split masks");
+        if (loss_kind == 0 && g.labels.empty())  // trainer.hpp:207-208
+            throw std::invalid_argument("softmax_ce requires multi-class labels");
         std::size_t cnt = 0;  // train_node_count trainer.cpp:59-64
         for (auto t : g.train) cnt += t;
         if (cnt == 0) throw std::invalid_argument("training requires a non-empty train mask");
@@ -906,8 +944,14 @@ struct Trainer final : TrainerBase {
             for (std::size_t j = 0; j < s.nodes.size(); ++j) {
                 const i32 v = s.nodes[j];
                 for (int c = 0; c < g.d; ++c) in.x(j, c) = static_cast<S>(g.features[static_cast<std::size_t>(v) * g.d + c]);
-                in.y[j] = g.labels[v];
-                if (loss_kind == 1) in.t(j, g.labels[v]) = S(1);  // label_targets graph.cpp:91-98
+                if (!g.is_multilabel()) in.y[j] = g.labels[v];
+                if (loss_kind == 1) {  // label_targets graph.cpp:91-98: the multi-label matrix, or one-hot
+                    if (g.is_multilabel())
+                        for (int c = 0; c < g.num_classes; ++c)
+                            in.t(j, c) = static_cast<S>(g.multilabels[static_cast<std::size_t>(v) * g.num_classes + c]);
+                    else
+                        in.t(j, g.labels[v]) = S(1);
+                }
                 in.w[j] = g.train[v] ? W[i][j] : 0.0;
             }
             if (use_de) in.masks = precompute_masks(s.edges.size(), K, ratio, substream(seed, "dropedge", i));
@@ -991,21 +1035,9 @@ struct Trainer final : TrainerBase {
         for (std::size_t i = 0; i < x.d.size(); ++i) x.d[i] = static_cast<S>(g.features[i]);
         Cache<S> cache;
         const Mat<S> lg = forward(model, adj, x, nullptr, cache);
-        auto metric = [&](const std::vector<std::uint8_t>& mask) {
-            std::size_t masked = 0, correct = 0;
-            for (i32 v = 0; v < g.n; ++v) {
-                if (!mask[v]) continue;
-                ++masked;
-                i64 best = 0;
-                for (i64 c = 1; c < lg.c; ++c)
-                    if (static_cast<double>(lg(v, c)) > static_cast<double>(lg(v, best))) best = c;
-                correct += best == g.labels[v];
-            }
-            return masked ? static_cast<double>(correct) / static_cast<double>(masked) : 0.0;
-        };
-        *tr = metric(g.train);
-        *va = metric(g.val);
-        *te = metric(g.test);
+        *tr = metric_from_logits(lg, g, g.train.data());
+        *va = metric_from_logits(lg, g, g.val.data());
+        *te = metric_from_logits(lg, g, g.test.data());
     }
 
     double time_part(int i, int epoch, int reps) override {
@@ -1105,6 +1137,118 @@ int or_graph_set_data(void* gp, const float* features, int d, const int32_t* lab
         g->val.assign(val, val + n);
         g->test.assign(test, test + n);
     });
+}
+
+// load_labels' multi-label branch (graph_io.cpp:206-229): n x C 0/1 matrix, labels cleared.
+int or_graph_set_multilabels(void* gp, const float* y, int classes) {
+    return guard([&] {
+        auto* g = static_cast<Graph*>(gp);
+        const std::size_t k = static_cast<std::size_t>(g->n) * static_cast<std::size_t>(classes);
+        g->multilabels.resize(k);
+        for (std::size_t i = 0; i < k; ++i) {
+            if (y[i] != 0.f && y[i] != 1.f) throw std::invalid_argument("loss: bce targets must be 0 or 1");
+            g->multilabels[i] = static_cast<double>(y[i]);
+        }
+        g->num_classes = classes;
+        g->labels.clear();
+    });
+}
+
+// evaluate (trainer.cpp:101-112): SageModel<double> forward over the full graph,
+// then metric_from_logits on one split mask.
+int or_evaluate(void* gp, const double* theta, const int* hidden, int layers, const uint8_t* mask, double* out) {
+    return guard([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        if (g.features.empty() || !g.has_labels())
+            throw std::invalid_argument("evaluate: graph lacks features or labels");
+        std::size_t masked = 0;
+        for (i32 v = 0; v < g.n; ++v) masked += mask[v];
+        if (masked == 0) throw std::invalid_argument("evaluate: empty mask");
+        Model<double> m = make_model<double>(g.d, std::vector<int>(hidden, hidden + layers), g.num_classes, 0);
+        m.from_flat(theta);
+        const Adj adj{g.n, g.offsets.data(), g.nbrs.data(), g.eids.data(), g.edges.size()};
+        Mat<double> x(g.n, g.d);
+        x.d = g.features;
+        Cache<double> cache;
+        const Mat<double> lg = forward(m, adj, x, nullptr, cache);
+        *out = metric_from_logits(lg, g, mask);
+    });
+}
+
+// comm_volume (trainer.cpp:38-49); out = {floats_per_iteration, gradient_floats, embedding_floats}
+int or_comm_volume(int mode, int num_parts, uint64_t params, uint64_t layers, uint64_t hidden, uint64_t halo,
+                   uint64_t* out) {
+    return guard([&] {
+        if (num_parts < 1) throw std::invalid_argument("comm_volume: num_parts must be >= 1");
+        const uint64_t grad = static_cast<uint64_t>(num_parts) * params;
+        const uint64_t emb = mode == 1 ? 2ULL * layers * halo * hidden : 0ULL;
+        out[0] = grad + emb;
+        out[1] = grad;
+        out[2] = emb;
+    });
+}
+// expected_rf_random / imbalance_lower_bound (partition.cpp:344-362)
+int or_expected_rf_random(int p, int64_t degree, double* out) {
+    return guard([&] {
+        if (p < 1) throw std::invalid_argument("expected_rf_random: num_parts must be >= 1");
+        if (degree < 0) throw std::invalid_argument("expected_rf_random: degree must be >= 0");
+        const double pd = static_cast<double>(p);
+        *out = pd * (1.0 - std::pow(1.0 - 1.0 / pd, static_cast<double>(degree)));
+    });
+}
+int or_imbalance_lower_bound(int p, int64_t max_degree, int64_t min_degree, double* out) {
+    return guard([&] {
+        if (p < 1) throw std::invalid_argument("num_parts must be >= 1");
+        if (min_degree < 1) throw std::invalid_argument("imbalance_lower_bound: min_degree must be >= 1");
+        if (max_degree < min_degree) throw std::invalid_argument("imbalance_lower_bound: max_degree < min_degree");
+        if (p == 1) {
+            *out = 1.0;
+            return;
+        }
+        const double pd = static_cast<double>(p);
+        *out = (1.0 - std::pow(1.0 - 1.0 / pd, static_cast<double>(max_degree))) /
+               (1.0 - std::pow(1.0 - 1.0 / pd, static_cast<double>(min_degree)));
+    });
+}
+
+// The masked mean aggregation alone (nn.hpp:209-230) and its transpose
+// (nn.hpp:277-288), float, over a CSR with int64 offsets (any size). mask:
+// per local edge (eids index it) or null. Forward: out[v] = (sum over kept
+// CSR slots of src[nbr], from 0, in CSR order) * inv[v], inv = 1/(float)deg.
+// Backward (pull form of the scatter, same per-row order: CSR rows ascend):
+// out[u] = (msg[u] > 0) ? sum over kept slots of src[nbr] : 0, where src is
+// dmean already scaled by inv (the reference adds inv[v] * dmean[v]).
+// Rows are split across `threads` std::threads (rows are independent).
+void or_spmm(int bwd, int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const int32_t* eids,
+             const uint8_t* mask, const float* src, const float* msg, float* out, int threads) {
+    auto rows = [&](int64_t r0, int64_t r1) {
+        std::vector<float> acc(static_cast<std::size_t>(H));
+        for (int64_t v = r0; v < r1; ++v) {
+            std::fill(acc.begin(), acc.end(), 0.f);
+            int32_t deg = 0;
+            for (int64_t k = off[v]; k < off[v + 1]; ++k) {
+                if (mask && !mask[eids[k]]) continue;
+                ++deg;
+                const float* s = src + static_cast<int64_t>(nbrs[k]) * H;
+                for (int32_t c = 0; c < H; ++c) acc[c] += s[c];
+            }
+            float* o = out + v * H;
+            if (!bwd) {
+                const float inv = deg > 0 ? 1.f / static_cast<float>(deg) : 0.f;
+                for (int32_t c = 0; c < H; ++c) o[c] = acc[c] * inv;
+            } else {
+                const float* m = msg + v * H;
+                for (int32_t c = 0; c < H; ++c) o[c] = m[c] > 0.f ? acc[c] : 0.f;
+            }
+        }
+    };
+    if (threads <= 1) {
+        rows(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < threads; ++t) th.emplace_back(rows, n * t / threads, n * (t + 1) / threads);
+    for (auto& x : th) x.join();
 }
 
 void* or_partition(void* gp, int algo, int p, uint64_t seed) {

@@ -45,6 +45,19 @@ void or_graph_masks(void* g, uint8_t* train, uint8_t* val, uint8_t* test);
 int or_graph_set_data(void* g, const float* features, int d, const int32_t* labels, int classes,
                       const uint8_t* train, const uint8_t* val, const uint8_t* test);
 
+int or_graph_set_multilabels(void* g, const float* y, int classes);
+
+/* trainer.cpp:38-49, 101-112; partition.cpp:344-362 */
+int or_evaluate(void* g, const double* theta, const int* hidden, int layers, const uint8_t* mask, double* out);
+int or_comm_volume(int mode, int num_parts, uint64_t params, uint64_t layers, uint64_t hidden, uint64_t halo,
+                   uint64_t* out);
+int or_expected_rf_random(int p, int64_t degree, double* out);
+int or_imbalance_lower_bound(int p, int64_t max_degree, int64_t min_degree, double* out);
+
+/* nn.hpp:209-230 / 277-288: aggregation alone (float), int64 offsets */
+void or_spmm(int bwd, int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const int32_t* eids,
+             const uint8_t* mask, const float* src, const float* msg, float* out, int threads);
+
 /* partition.cpp */
 void* or_partition(void* g, int algo /*0 random, 1 dbh, 2 ne (slack 1.1), 3 edge-cut greedy -> ec2vc*/, int p,
                    uint64_t seed);

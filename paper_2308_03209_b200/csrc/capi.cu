@@ -3,6 +3,7 @@
 // Every entry point converts C++ exceptions into sc_status codes with the
 // reference's message text in sc_last_error(), the same taxonomy the
 // reference's CLI maps to exit codes (proj/tools/main.cpp:822-834).
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -160,11 +161,32 @@ sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, con
         h2d(g->val.get(), val, n, s);
         h2d(g->test.get(), test, n, s);
         g->train_count = train_count;
+        g->multilabel = false;  // class ids replace any multi-label matrix (load_labels, graph_io.cpp:230-241)
+        g->targets.release();
         g->feat_amax.alloc(1);
         ++g->feat_version;
         SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), s));
         absmax(n * dim, g->features.get(), g->feat_amax.get(), s);
         SC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+sc_status sc_graph_set_multilabels(sc_graph* g, const float* targets, int32_t classes) {
+    return guard([&] {
+        REQUIRE_ARG(g && targets, "sc_graph_set_multilabels: null argument");
+        REQUIRE_ARG(classes >= 1, "sc_graph_set_multilabels: num_classes must be positive");
+        REQUIRE_ARG(g->dim > 0, "sc_graph_set_multilabels: call sc_graph_set_data first");
+        set_device(g->ctx);
+        const int64_t k = int64_t(g->n) * classes;
+        std::vector<uint8_t> y(static_cast<size_t>(std::max<int64_t>(k, 1)));
+        for (int64_t i = 0; i < k; ++i) {  // bce_loss's target check (nn.hpp:366-367)
+            if (targets[i] != 0.f && targets[i] != 1.f) throw std::invalid_argument("loss: bce targets must be 0 or 1");
+            y[size_t(i)] = targets[i] != 0.f ? 1 : 0;
+        }
+        g->targets.alloc(std::max<int64_t>(k, 1));
+        h2d(g->targets.get(), y.data(), k, g->ctx->stream);
+        g->num_classes = classes;
+        g->multilabel = true;
+        SC_CUDA(cudaStreamSynchronize(g->ctx->stream));
     });
 }
 sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_device) {
@@ -177,6 +199,20 @@ sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_devic
         ++g->feat_version;
         SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), g->ctx->stream));
         absmax(int64_t(g->n) * g->dim, g->features.get(), g->feat_amax.get(), g->ctx->stream);
+    });
+}
+sc_status sc_graph_set_part_ownership(sc_graph* g, int32_t rank, int32_t world) {
+    return guard([&] {
+        REQUIRE_ARG(g, "sc_graph_set_part_ownership: null graph");
+        REQUIRE_ARG(world >= 1 && rank >= 0 && rank < world, "bad rank/world");
+        g->own_rank = rank;
+        g->own_world = world;
+    });
+}
+sc_status sc_vcut_part_held(sc_vcut* vc, int32_t part, int32_t* held) {
+    return guard([&] {
+        REQUIRE_ARG(vc && held && part >= 0 && part < vc->p, "sc_vcut_part_held: bad part index");
+        *held = vc->parts[part].held ? 1 : 0;
     });
 }
 sc_status sc_graph_info(sc_graph* g, int32_t* n, int64_t* m, int32_t* dim, int32_t* classes) {
@@ -342,14 +378,14 @@ sc_status sc_vcut_part_copy(sc_vcut* vc, int32_t part, int32_t* nodes, int32_t* 
         REQUIRE_ARG(vc && part >= 0 && part < vc->p, "sc_vcut_part_copy: bad part index");
         set_device(vc->g->ctx);
         cudaStream_t s = vc->g->ctx->stream;
-        const PartDev& pd = vc->parts[part];
+        const PartDev& pd = vc->held(part);
         if (nodes) d2h(nodes, pd.nodes.get(), pd.n_local, s);
         if (gids) d2h(gids, pd.edge_gids.get(), pd.m_local, s);
         if (local_deg) d2h(local_deg, pd.local_deg.get(), pd.n_local, s);
         if (offsets) d2h(offsets, pd.offsets.get(), pd.n_local + 1, s);
         if (nbrs) d2h(nbrs, pd.nbrs.get(), 2 * pd.m_local, s);
         if (eids) d2h(eids, pd.eids.get(), 2 * pd.m_local, s);
-        if (g2l) d2h(g2l, vc->g2l.get() + int64_t(part) * vc->g->n, vc->g->n, s);
+        if (g2l) d2h(g2l, vc->g2l.get() + pd.g2l_slot * vc->g->n, vc->g->n, s);
         std::vector<int32_t> u, v;
         if (edges_uv) {
             u.resize(pd.m_local);
@@ -420,8 +456,9 @@ const char* const kSchemeNames[] = {"dar", "vanilla_inv", "none"};
 std::vector<std::vector<int32_t>> part_nodes_host(sc_vcut* vc) {
     std::vector<std::vector<int32_t>> nodes(vc->p);
     for (int32_t i = 0; i < vc->p; ++i) {
-        nodes[i].resize(vc->parts[i].n_local);
-        d2h(nodes[i].data(), vc->parts[i].nodes.get(), vc->parts[i].n_local, vc->g->ctx->stream);
+        const PartDev& pd = vc->held(i);
+        nodes[i].resize(pd.n_local);
+        d2h(nodes[i].data(), pd.nodes.get(), pd.n_local, vc->g->ctx->stream);
     }
     SC_CUDA(cudaStreamSynchronize(vc->g->ctx->stream));
     return nodes;
@@ -544,6 +581,11 @@ sc_status sc_trainer_load_checkpoint(sc_trainer* t, const char* path) {
             for (double v : mats[i].v) theta.push_back(static_cast<float>(v));
         }
         h2d(t->theta.get(), theta.data(), t->P, t->ctx->stream);
+        // CFCK holds the model only (checkpoint.cpp:44-57): training resumes from
+        // fresh Adam state, as a reference run started from these weights would.
+        if (t->m1.size()) SC_CUDA(cudaMemsetAsync(t->m1.get(), 0, t->m1.bytes(), t->ctx->stream));
+        if (t->m2.size()) SC_CUDA(cudaMemsetAsync(t->m2.get(), 0, t->m2.bytes(), t->ctx->stream));
+        t->adam_step = 0;
         t->tc.invalidate();
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
     });
@@ -553,6 +595,8 @@ sc_status sc_save_checkpoint_params(const float* theta, int32_t in_dim, const in
     return guard([&] {
         REQUIRE_ARG(theta && path && (hidden || layers == 0), "sc_save_checkpoint_params: null argument");
         REQUIRE_ARG(layers >= 0 && in_dim >= 0 && num_classes >= 0, "sc_save_checkpoint_params: bad dims");
+        for (int32_t l = 0; l < layers; ++l)
+            REQUIRE_ARG(hidden[l] >= 1, "hidden dims must be positive");
         std::vector<HostMatrix> mats;
         int64_t k = 0, in = in_dim;
         auto add = [&](int64_t r, int64_t c) {
@@ -678,6 +722,13 @@ sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
         trainer_init_comm(t, id);  // world == 1: a single-rank communicator (exercises the exchange path)
     });
 }
+sc_status sc_trainer_set_exchange(sc_trainer* t, sc_exchange_fn fn, void* user) {
+    return guard([&] {
+        REQUIRE_ARG(t, "sc_trainer_set_exchange: null trainer");
+        t->xfn = fn;
+        t->xuser = user;
+    });
+}
 sc_status sc_trainer_step(sc_trainer* t, int32_t epoch, double* loss, double* gnorm) {
     return guard([&] {
         set_device(t->ctx);
@@ -717,7 +768,9 @@ sc_status sc_trainer_get_params(sc_trainer* t, float* out) {
 }
 sc_status sc_trainer_set_params(sc_trainer* t, const float* in) {
     return guard([&] {
+        REQUIRE_ARG(t && in, "sc_trainer_set_params: null argument");
         set_device(t->ctx);
+        trainer_finish(t, nullptr, nullptr);  // the pending step read the old parameters
         h2d(t->theta.get(), in, t->P, t->ctx->stream);
         t->tc.invalidate();
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
@@ -768,6 +821,93 @@ sc_status sc_trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te)
     return guard([&] {
         set_device(t->ctx);
         trainer_evaluate(t, tr, va, te);
+    });
+}
+sc_status sc_trainer_evaluate_mask(sc_trainer* t, const uint8_t* mask, double* metric) {
+    return guard([&] {
+        REQUIRE_ARG(t && mask && metric, "sc_trainer_evaluate_mask: null argument");
+        set_device(t->ctx);
+        const int64_t n = t->g->n;
+        int64_t masked = 0;
+        for (int64_t v = 0; v < n; ++v) masked += mask[v] ? 1 : 0;
+        if (masked == 0) throw std::invalid_argument("evaluate: empty mask");  // trainer.cpp:106-108
+        DevBuf<uint8_t> d(std::max<int64_t>(n, 1));
+        h2d(d.get(), mask, n, t->ctx->stream);
+        *metric = trainer_evaluate_mask(t, d.get());
+    });
+}
+sc_status sc_evaluate(sc_ctx* ctx, sc_graph* g, const float* theta, const int32_t* hidden, int32_t layers,
+                      const uint8_t* mask, double* metric) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && g && theta && mask && metric && (hidden || layers == 0), "sc_evaluate: null argument");
+        REQUIRE_ARG(layers >= 0, "layers must be >= 0");
+        set_device(ctx);
+        if (g->dim == 0 || g->num_classes == 0) throw std::invalid_argument("evaluate: graph lacks features or labels");
+        auto t = std::make_unique<sc_trainer>();
+        t->ctx = ctx;
+        t->g = g;
+        t->L = layers;
+        t->hidden.assign(hidden, hidden + layers);
+        trainer_init_eval_only(t.get());
+        h2d(t->theta.get(), theta, t->P, ctx->stream);
+        const int64_t n = g->n;
+        int64_t masked = 0;
+        for (int64_t v = 0; v < n; ++v) masked += mask[v] ? 1 : 0;
+        if (masked == 0) throw std::invalid_argument("evaluate: empty mask");
+        DevBuf<uint8_t> d(std::max<int64_t>(n, 1));
+        h2d(d.get(), mask, n, ctx->stream);
+        *metric = trainer_evaluate_mask(t.get(), d.get());
+    });
+}
+sc_status sc_trainer_comm_audit(sc_trainer* t, uint64_t* gradient_floats, uint64_t* embedding_floats) {
+    return guard([&] {
+        REQUIRE_ARG(t, "sc_trainer_comm_audit: null trainer");
+        trainer_finish(t, nullptr, nullptr);
+        if (gradient_floats) *gradient_floats = t->audit_floats;
+        if (embedding_floats) *embedding_floats = 0;  // no node embedding ever leaves a partition
+    });
+}
+sc_status sc_trainer_fallback_count(sc_trainer* t, int64_t* count) {
+    return guard([&] {
+        REQUIRE_ARG(t && count, "sc_trainer_fallback_count: null argument");
+        *count = t->tc.simt_fallbacks;
+    });
+}
+sc_status sc_comm_volume(int32_t mode, int32_t num_parts, uint64_t param_count, uint64_t num_layers,
+                         uint64_t hidden_dim, uint64_t total_halo, uint64_t* floats_per_iteration,
+                         uint64_t* gradient_floats, uint64_t* embedding_floats) {
+    return guard([&] {  // trainer.cpp:38-49
+        REQUIRE_ARG(mode == 0 || mode == 1, "comm_volume: unknown mode");
+        if (num_parts < 1) throw std::invalid_argument("comm_volume: num_parts must be >= 1");
+        const uint64_t grad = static_cast<uint64_t>(num_parts) * param_count;
+        const uint64_t emb = mode == 1 ? 2ULL * num_layers * total_halo * hidden_dim : 0ULL;
+        if (gradient_floats) *gradient_floats = grad;
+        if (embedding_floats) *embedding_floats = emb;
+        if (floats_per_iteration) *floats_per_iteration = grad + emb;
+    });
+}
+sc_status sc_expected_rf_random(int32_t num_parts, int64_t degree, double* out) {
+    return guard([&] {  // partition.cpp:344-349
+        REQUIRE_ARG(out, "sc_expected_rf_random: null out");
+        if (num_parts < 1) throw std::invalid_argument("expected_rf_random: num_parts must be >= 1");
+        if (degree < 0) throw std::invalid_argument("expected_rf_random: degree must be >= 0");
+        const double p = static_cast<double>(num_parts);
+        *out = p * (1.0 - std::pow(1.0 - 1.0 / p, static_cast<double>(degree)));
+    });
+}
+sc_status sc_imbalance_lower_bound(int32_t num_parts, int64_t max_degree, int64_t min_degree, double* out) {
+    return guard([&] {  // partition.cpp:351-362
+        REQUIRE_ARG(out, "sc_imbalance_lower_bound: null out");
+        if (num_parts < 1) throw std::invalid_argument("num_parts must be >= 1");
+        if (min_degree < 1) throw std::invalid_argument("imbalance_lower_bound: min_degree must be >= 1");
+        if (max_degree < min_degree) throw std::invalid_argument("imbalance_lower_bound: max_degree < min_degree");
+        if (num_parts == 1) {
+            *out = 1.0;
+            return;
+        }
+        const double p = static_cast<double>(num_parts);
+        *out = (1.0 - std::pow(1.0 - 1.0 / p, static_cast<double>(max_degree))) /
+               (1.0 - std::pow(1.0 - 1.0 / p, static_cast<double>(min_degree)));
     });
 }
 sc_status sc_trainer_profile(sc_trainer* t, int32_t enable) {

@@ -1483,6 +1483,7 @@ void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b
         const BImage* i2 = a2 ? &image(*b2, N, a2->K, s) : nullptr;
         gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s);
     } else {
+        if (enabled) ++simt_fallbacks;
         gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
     }
 }
@@ -1493,8 +1494,10 @@ void TcGemm::tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b
     if (!ws) ws = t->ws.get();
     if (enabled && tn_supported(a, b1, b2))
         gemm_tn_f16x3(a, amax_a, b1, amax_b1, b2, amax_b2, M, C, ldc, ws, t->ws_floats, s);
-    else
+    else {
+        if (enabled) ++simt_fallbacks;
         gemm_tn(a, b1, b2, M, C, ldc, ws, t->ws_floats, s);
+    }
 }
 
 }  // namespace sc

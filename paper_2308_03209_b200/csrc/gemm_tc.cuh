@@ -54,6 +54,9 @@ struct TcGemm {
         uint64_t version = 0;
     };
     std::map<Key, Entry> cache;
+    // GEMMs that ran on the fp32 SIMT kernels although the tensor-core path was
+    // enabled (operand layout not TMA-compatible): counted, never silent.
+    int64_t simt_fallbacks = 0;
     void init(sc_trainer* t);
     void invalidate() { ++version; }
     const BImage& image(const MatB& b, int32_t N, int32_t K, cudaStream_t s);

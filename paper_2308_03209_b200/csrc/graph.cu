@@ -397,10 +397,17 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
         SC_LAUNCH_CHECK();
         count_launch(4);
     }
-    // per-part local numbering (ascending global id)
-    vc->g2l.alloc(static_cast<size_t>(p) * std::max<int64_t>(n, 1));
-    vc->per_node_rf.alloc(std::max<int64_t>(n, 1));
+    // per-part local numbering (ascending global id); arrays only for the parts this rank holds
+    vc->own_rank = g->own_rank;
+    vc->own_world = g->own_world;
     vc->parts.resize(p);
+    int64_t nheld = 0;
+    for (int32_t i = 0; i < p; ++i) {
+        vc->parts[i].held = g->owns(i);
+        vc->parts[i].g2l_slot = vc->parts[i].held ? nheld++ : -1;
+    }
+    vc->g2l.alloc(static_cast<size_t>(std::max<int64_t>(nheld, 1)) * std::max<int64_t>(n, 1));
+    vc->per_node_rf.alloc(std::max<int64_t>(n, 1));
     std::vector<int32_t> n_local(p, 0);
     DevBuf<int32_t> total(1);
     for (int32_t i = 0; i < p; ++i) {
@@ -419,9 +426,10 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
         }
         PartDev& pd = vc->parts[i];
         pd.n_local = n_local[i];
+        if (!pd.held) continue;
         pd.nodes.alloc(std::max<int64_t>(pd.n_local, 1));
         if (n > 0) {
-            g2l_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, mem_i, scan.get(), vc->g2l.get() + i * n,
+            g2l_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, mem_i, scan.get(), vc->g2l.get() + pd.g2l_slot * n,
                                                               pd.nodes.get());
             SC_LAUNCH_CHECK();
             count_launch();
@@ -453,12 +461,17 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
         PartDev& pd = vc->parts[i];
         pd.m_local = counts[i];
         const int64_t mi = pd.m_local;
+        if (!pd.held) {
+            start += mi;
+            continue;
+        }
         pd.lu.alloc(std::max<int64_t>(mi, 1));
         pd.lv.alloc(std::max<int64_t>(mi, 1));
         pd.edge_gids.alloc(std::max<int64_t>(mi, 1));
         if (mi > 0) {
             local_edges_kernel<<<grid_for(mi, kBlock), kBlock, 0, s>>>(mi, perm.get() + start, g->eu.get(), g->ev.get(),
-                                                                       vc->g2l.get() + i * n, pd.lu.get(), pd.lv.get(),
+                                                                       vc->g2l.get() + pd.g2l_slot * n, pd.lu.get(),
+                                                                       pd.lv.get(),
                                                                        pd.edge_gids.get());
             SC_LAUNCH_CHECK();
             count_launch();
@@ -500,7 +513,7 @@ __global__ void weights_kernel(int64_t nl, int scheme, const int32_t* __restrict
 }  // namespace
 
 void compute_weights_device(sc_vcut* vc, int scheme, int32_t part, double* out_dev) {
-    const PartDev& pd = vc->parts[part];
+    const PartDev& pd = vc->held(part);
     if (pd.n_local == 0) return;
     DevBuf<int> err(1);
     cudaStream_t s = vc->g->ctx->stream;
@@ -517,18 +530,21 @@ void compute_weights_device(sc_vcut* vc, int scheme, int32_t part, double* out_d
 }
 
 // ---- make_sage_model init (nn.hpp:73-102) ----------------------------------------------
+// Draw k of the init stream goes to flat parameter k (matrices in for_each_matrix
+// order, each row-major); the matrix of k (its Glorot bound) is found by binary
+// search over the nmat + 1 matrix offsets, so any layer count works.
 namespace {
-struct InitSpec {
-    int32_t nmat;
-    int64_t start[17];  // flat offset of matrix k (<= 8 layers)
-    double bound[16];
-};
-__global__ void init_kernel(int64_t total, uint64_t s, InitSpec spec, float* out) {
+__global__ void init_kernel(int64_t total, uint64_t s, int32_t nmat, const int64_t* __restrict__ start,
+                            const double* __restrict__ bound, float* out) {
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
-        int mi = 0;
-        while (mi + 1 < spec.nmat && k >= spec.start[mi + 1]) ++mi;
+        int32_t lo = 0, hi = nmat - 1;  // last matrix with start <= k
+        while (lo < hi) {
+            const int32_t mid = (lo + hi + 1) >> 1;
+            if (start[mid] <= k) lo = mid;
+            else hi = mid - 1;
+        }
         const double r = u64_to_double(draw_u64(s, static_cast<uint64_t>(k)));
-        out[k] = static_cast<float>(spec.bound[mi] * (2.0 * r - 1.0));
+        out[k] = static_cast<float>(bound[lo] * (2.0 * r - 1.0));
     }
 }
 }  // namespace
@@ -536,16 +552,14 @@ __global__ void init_kernel(int64_t total, uint64_t s, InitSpec spec, float* out
 void init_params_device(sc_ctx* ctx, int32_t in_dim, const int32_t* hidden, int32_t layers, int32_t classes,
                         uint64_t seed, float* out_dev) {
     if (in_dim < 1 || classes < 1) throw std::invalid_argument("make_sage_model: dimensions must be positive");
-    if (layers > 7) throw std::invalid_argument("sagecut_cuda: at most 7 layers supported");
-    InitSpec spec{};
+    std::vector<int64_t> start;
+    std::vector<double> bound;
     int64_t off = 0;
     int64_t in = in_dim;
-    int k = 0;
     auto add = [&](int64_t r, int64_t c) {
-        spec.start[k] = off;
-        spec.bound[k] = std::sqrt(6.0 / static_cast<double>(r + c));
+        start.push_back(off);
+        bound.push_back(std::sqrt(6.0 / static_cast<double>(r + c)));
         off += r * c;
-        ++k;
     };
     for (int32_t l = 0; l < layers; ++l) {
         if (hidden[l] < 1) throw std::invalid_argument("make_sage_model: hidden dims must be positive");
@@ -554,11 +568,17 @@ void init_params_device(sc_ctx* ctx, int32_t in_dim, const int32_t* hidden, int3
         in = hidden[l];
     }
     add(classes, in);
-    spec.nmat = k;
-    spec.start[k] = off;
-    init_kernel<<<grid_for(off, kBlock), kBlock, 0, ctx->stream>>>(off, substream(seed, "init"), spec, out_dev);
+    const int32_t nmat = static_cast<int32_t>(start.size());
+    cudaStream_t s = ctx->stream;
+    DevBuf<int64_t> d_start(nmat);
+    DevBuf<double> d_bound(nmat);
+    h2d(d_start.get(), start.data(), nmat, s);
+    h2d(d_bound.get(), bound.data(), nmat, s);
+    init_kernel<<<grid_for(off, kBlock), kBlock, 0, s>>>(off, substream(seed, "init"), nmat, d_start.get(),
+                                                         d_bound.get(), out_dev);
     SC_LAUNCH_CHECK();
     count_launch();
+    SC_CUDA(cudaStreamSynchronize(s));  // the offset tables are freed on return
 }
 
 }  // namespace sc

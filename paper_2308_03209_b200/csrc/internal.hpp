@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
@@ -97,9 +98,16 @@ struct sc_graph {
     sc::DevBuf<float> features;        // n x dim
     sc::DevBuf<float> feat_amax;       // max |features| (tensor-core operand scale)
     uint64_t feat_version = 0;         // bumped whenever the features change
-    sc::DevBuf<int32_t> labels;        // n
+    sc::DevBuf<int32_t> labels;        // n (multi-class ids)
+    sc::DevBuf<uint8_t> targets;       // n x num_classes 0/1 (multi-label graphs, graph.hpp:64)
+    bool multilabel = false;           // Graph::is_multilabel (graph.hpp:74)
     sc::DevBuf<uint8_t> train, val, test;  // n
     int64_t train_count = 0;
+    // Partition ownership (sc_graph_set_part_ownership): vertex cuts built on this
+    // graph materialise only parts i with i % own_world == own_rank (the ones this
+    // rank trains); the others keep their sizes only. own_world 1 = every part.
+    int32_t own_rank = 0, own_world = 1;
+    bool owns(int32_t part) const { return own_world <= 1 || part % own_world == own_rank; }
     // Staged next features (sc_trainer_stage_features): H2D on copy_stream into
     // features_next while the current step runs; committed (buffers swapped)
     // at the start of the next step. released: recorded on the compute stream
@@ -114,6 +122,8 @@ struct sc_graph {
 // One PartSubgraph (partition.hpp:14-31), device resident.
 struct PartDev {
     int64_t n_local = 0, m_local = 0;
+    bool held = true;                       // arrays materialised on this rank (sc_graph_set_part_ownership)
+    int64_t g2l_slot = -1;                  // row of sc_vcut::g2l (held parts only)
     sc::DevBuf<int32_t> nodes;              // global ids ascending
     sc::DevBuf<int32_t> lu, lv;             // local endpoints, local-edge order
     sc::DevBuf<int32_t> edge_gids;          // global edge id per local edge
@@ -126,7 +136,13 @@ struct sc_vcut {
     sc_graph* g = nullptr;
     int32_t p = 0;
     sc::DevBuf<int32_t> assign;        // m
-    sc::DevBuf<int32_t> g2l;           // p x n, -1 where absent
+    sc::DevBuf<int32_t> g2l;           // held parts x n, -1 where absent (PartDev::g2l_slot)
+    int32_t own_rank = 0, own_world = 1;  // the graph's ownership when this cut was built
+    const PartDev& held(int32_t i) const {
+        if (!parts[i].held)
+            throw std::invalid_argument("partition " + std::to_string(i) + " is not held on this rank");
+        return parts[i];
+    }
     sc::DevBuf<int32_t> per_node_rf;   // n
     std::vector<PartDev> parts;
     std::vector<std::string> warnings; // VertexCutPartition::warnings (partition_ne overshoot reports)

@@ -555,6 +555,10 @@ __device__ __forceinline__ float warp_sum(float x) {
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
 }
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
 __device__ __forceinline__ double warp_sum_d(double x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -647,8 +651,11 @@ __global__ void __launch_bounds__(128) softmax_ce_rows_kernel(int64_t n, int32_t
     }
 }
 
+// targets (optional): the graph's n x C 0/1 multi-label matrix (graph.hpp:64);
+// without it the target row is the one-hot of the class id (label_targets,
+// graph.cpp:91-98).
 __global__ void bce_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
-                           const int32_t* __restrict__ labels,
+                           const int32_t* __restrict__ labels, const uint8_t* __restrict__ targets,
                            const int32_t* __restrict__ rows, const double* __restrict__ w,
                            const float* __restrict__ scale, float* G, double* row_loss) {
     const int lane = threadIdx.x & 31;
@@ -662,12 +669,14 @@ __global__ void bce_kernel(int64_t n, int32_t C, int32_t ld, const float* __rest
             if (lane == 0) row_loss[r] = 0.0;
             continue;
         }
-        const int32_t yl = labels[rows ? rows[r] : r];
+        const int64_t node = rows ? rows[r] : r;
+        const int32_t yl = targets ? -1 : labels[node];
+        const uint8_t* trow = targets ? targets + node * C : nullptr;
         const float sc = scale[r];
         double acc = 0.0;
         for (int32_t c = lane; c < C; c += 32) {
             const float zc = z[c];
-            const float y = c == yl ? 1.f : 0.f;  // label_targets: one-hot (graph.cpp:91-98)
+            const float y = trow ? static_cast<float>(trow[c]) : (c == yl ? 1.f : 0.f);
             const float sp = fmaxf(zc, 0.f) + log1pf(expf(-fabsf(zc)));
             acc += wr * static_cast<double>(sp - zc * y);
             const float sg = zc >= 0.f ? 1.f / (1.f + expf(-zc)) : expf(zc) / (1.f + expf(zc));
@@ -779,6 +788,36 @@ __global__ void correct_kernel(int64_t n, int32_t C, int32_t ld, const float* __
     }
     atomicAdd(&out[0], corr);
     atomicAdd(&out[1], tot);
+}
+
+// Micro-F1 counts over masked rows (trainer.cpp:72-87): prediction = logit > 0,
+// truth = target != 0; out[0..2] += (tp, fp, fn), out[3] += masked rows.
+__global__ void f1_counts_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
+                                 const uint8_t* __restrict__ targets, const uint8_t* __restrict__ mask,
+                                 unsigned long long* out) {
+    unsigned long long tp = 0, fp = 0, fn = 0, tot = 0;
+    const int64_t total = n * C;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / C;
+        const int32_t c = static_cast<int32_t>(i - r * C);
+        if (!mask[r]) continue;
+        tot += c == 0;
+        const bool pred = logits[r * ld + c] > 0.f;
+        const bool truth = targets[i] != 0;
+        tp += pred && truth;
+        fp += pred && !truth;
+        fn += !pred && truth;
+    }
+    tp = warp_sum_u64(tp);
+    fp = warp_sum_u64(fp);
+    fn = warp_sum_u64(fn);
+    tot = warp_sum_u64(tot);
+    if ((threadIdx.x & 31) == 0 && (tp | fp | fn | tot)) {
+        atomicAdd(&out[0], tp);
+        atomicAdd(&out[1], fp);
+        atomicAdd(&out[2], fn);
+        atomicAdd(&out[3], tot);
+    }
 }
 
 }  // namespace
@@ -901,7 +940,7 @@ __global__ void gather_rows_pad_kernel(int64_t n, int32_t d, int32_t dp, const i
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * dp; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = i / dp;
         const int32_t c = static_cast<int32_t>(i - r * dp);
-        dst[i] = c < d ? __ldg(src + int64_t(rows[r]) * d + c) : 0.f;
+        dst[i] = c < d ? __ldg(src + (rows ? int64_t(rows[r]) : r) * d + c) : 0.f;
     }
 }
 
@@ -955,10 +994,10 @@ void softmax_ce(int64_t n, int32_t C, int32_t ld, const float* logits, const int
     SC_LAUNCH_CHECK();
     count_launch();
 }
-void bce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
-         const float* scale, float* G, double* row_loss, cudaStream_t s) {
+void bce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const uint8_t* targets,
+         const int32_t* rows, const double* w, const float* scale, float* G, double* row_loss, cudaStream_t s) {
     if (n <= 0) return;
-    bce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
+    bce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, targets, rows, w, scale, G, row_loss);
     SC_LAUNCH_CHECK();
     count_launch();
 }
@@ -990,6 +1029,14 @@ void count_correct(int64_t n, int32_t C, int32_t ld, const float* logits, const 
                    unsigned long long* out, cudaStream_t s) {
     if (n <= 0) return;
     correct_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, C, ld, logits, labels, mask, out);
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+
+void f1_counts(int64_t n, int32_t C, int32_t ld, const float* logits, const uint8_t* targets, const uint8_t* mask,
+               unsigned long long* out, cudaStream_t s) {
+    if (n <= 0 || C <= 0) return;
+    f1_counts_kernel<<<grid_for(n * C, 256), 256, 0, s>>>(n, C, ld, logits, targets, mask, out);
     SC_LAUNCH_CHECK();
     count_launch();
 }

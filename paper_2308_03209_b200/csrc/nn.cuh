@@ -44,7 +44,8 @@ enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2 };
 void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
              int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out = nullptr);
 
-// dst[r][:] = src[rows[r]][:] (n x d); dst_ld > d pads each destination row with zeros.
+// dst[r][:] = src[rows[r]][:] (n x d); dst_ld > d pads each destination row with zeros
+// (and then rows may be null: identity).
 void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, float* dst, cudaStream_t s,
                  int32_t dst_ld = 0);
 
@@ -84,8 +85,9 @@ void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_
 // ld: row stride of logits and G (>= C)
 void softmax_ce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows,
                 const double* w, const float* scale, float* G, double* row_loss, cudaStream_t s);
-void bce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const int32_t* rows, const double* w,
-         const float* scale, float* G, double* row_loss, cudaStream_t s);
+// targets (optional): the graph's n x C 0/1 multi-label matrix, else one-hot of labels.
+void bce(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const uint8_t* targets,
+         const int32_t* rows, const double* w, const float* scale, float* G, double* row_loss, cudaStream_t s);
 // Deterministic f64 sum of x[0..n), divided by `divisor`, into *out (fixed-shape two-pass reduction).
 void sum_f64(int64_t n, const double* x, double* partial, double* out, double divisor, cudaStream_t s);
 
@@ -104,5 +106,9 @@ void adam(int64_t P, float* theta, float* m1, float* m2, const float* g, float b
 // Accuracy of argmax(logits) over masked rows (trainer.cpp:66-97, multi-class).
 void count_correct(int64_t n, int32_t C, int32_t ld, const float* logits, const int32_t* labels, const uint8_t* mask,
                    unsigned long long* correct_and_total, cudaStream_t s);
+
+// Micro-F1 counts (trainer.cpp:72-87): out[0..3] += (tp, fp, fn, masked rows).
+void f1_counts(int64_t n, int32_t C, int32_t ld, const float* logits, const uint8_t* targets, const uint8_t* mask,
+               unsigned long long* out, cudaStream_t s);
 
 }  // namespace sc

@@ -89,6 +89,7 @@ sc_trainer::~sc_trainer() {
     for (cudaEvent_t e : fork_events) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (host) cudaFreeHost(host);
+    if (xhost) cudaFreeHost(xhost);
     for (cudaEvent_t e : xfer_events) cudaEventDestroy(e);
     if (comm_done) cudaEventDestroy(comm_done);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -96,32 +97,19 @@ sc_trainer::~sc_trainer() {
 
 namespace sc {
 
-void trainer_init(sc_trainer* t) {
+namespace {
+// Model layout (SageModel::for_each_matrix order), parameters initialised by
+// make_sage_model, optimizer state, gradient buckets and the per-operand
+// |max| slots: everything but the partitions.
+void init_model(sc_trainer* t) {
     sc_graph* g = t->g;
-    sc_vcut* vc = t->vc;
-    if (!(t->lr > 0.0)) throw std::invalid_argument("learning rate must be > 0");
-    if (t->L < 0) throw std::invalid_argument("layers must be >= 0");
-    for (int h : t->hidden)
-        if (h < 1) throw std::invalid_argument("hidden dims must be positive");
-    if (t->use_dropedge) {
-        if (t->K < 1) throw std::invalid_argument("dropedge_k must be >= 1");
-        if (t->ratio < 0.0 || t->ratio >= 1.0) throw std::invalid_argument("drop_ratio must lie in [0, 1)");
-    }
-    if (g->dim == 0) throw std::invalid_argument("training requires node features");
-    if (g->num_classes == 0) throw std::invalid_argument("training requires labels");
-    if (g->train_count == 0) throw std::invalid_argument("training requires a non-empty train mask");
-    if (vc->g != g || vc->parts.empty()) throw std::invalid_argument("train_cofree: partition does not match graph");
-    if (t->world < 1 || t->rank < 0 || t->rank >= t->world) throw std::invalid_argument("bad rank/world");
-    cudaStream_t s = t->ctx->stream;
-    t->normalizer = static_cast<double>(g->train_count);
     t->d = g->dim;
     t->dp = (t->d + 3) / 4 * 4;
     t->C = g->num_classes;
     t->Cp = (t->C + 3) / 4 * 4;  // logits / dlogits row stride: 16-byte rows for the tensor-core kernels
-    t->p = vc->p;
-    // flat parameter layout (for_each_matrix order)
     int64_t off = 0;
     int in = t->d;
+    t->lay.clear();
     for (int l = 0; l < t->L; ++l) {
         LayerOff lo;
         lo.in = in;
@@ -138,6 +126,36 @@ void trainer_init(sc_trainer* t) {
     off += int64_t(t->C) * t->E;
     t->P = off;
     t->theta.alloc(t->P);
+    init_params_device(t->ctx, t->d, t->hidden.data(), t->L, t->C, t->seed, t->theta.get());
+    t->amax.alloc(sc_trainer::kSlotBase + 2 * std::max(t->L, 1));
+    t->tc.init(t);
+}
+}  // namespace
+
+void trainer_init(sc_trainer* t) {
+    sc_graph* g = t->g;
+    sc_vcut* vc = t->vc;
+    if (!(t->lr > 0.0)) throw std::invalid_argument("learning rate must be > 0");
+    if (t->L < 0) throw std::invalid_argument("layers must be >= 0");
+    for (int h : t->hidden)
+        if (h < 1) throw std::invalid_argument("hidden dims must be positive");
+    if (t->use_dropedge) {
+        if (t->K < 1) throw std::invalid_argument("dropedge_k must be >= 1");
+        if (t->ratio < 0.0 || t->ratio >= 1.0) throw std::invalid_argument("drop_ratio must lie in [0, 1)");
+    }
+    if (g->dim == 0) throw std::invalid_argument("training requires node features");
+    if (g->num_classes == 0) throw std::invalid_argument("training requires labels");
+    if (t->loss == 0 && g->multilabel)  // trainer.hpp:207-208
+        throw std::invalid_argument("softmax_ce requires multi-class labels");
+    if (vc->g != g || vc->parts.empty()) throw std::invalid_argument("train_cofree: partition does not match graph");
+    if (g->train_count == 0) throw std::invalid_argument("training requires a non-empty train mask");
+    if (t->world < 1 || t->rank < 0 || t->rank >= t->world) throw std::invalid_argument("bad rank/world");
+    for (int i = t->rank; i < vc->p; i += t->world)  // every partition this rank trains must be materialised
+        (void)vc->held(i);
+    cudaStream_t s = t->ctx->stream;
+    t->normalizer = static_cast<double>(g->train_count);
+    t->p = vc->p;
+    init_model(t);
     t->m1.alloc(t->P);
     t->m2.alloc(t->P);
     t->gathered.alloc(t->P);
@@ -157,7 +175,6 @@ void trainer_init(sc_trainer* t) {
     SC_CUDA(cudaMemsetAsync(t->m1.get(), 0, t->m1.bytes(), s));
     SC_CUDA(cudaMemsetAsync(t->m2.get(), 0, t->m2.bytes(), s));
     SC_CUDA(cudaMemsetAsync(t->slots.get(), 0, t->slots.bytes(), s));
-    init_params_device(t->ctx, t->d, t->hidden.data(), t->L, t->C, t->seed, t->theta.get());
 
     // per-partition inputs (trainer.hpp:218-243)
     int64_t n_max = 1, nnz_max = 1;
@@ -208,7 +225,6 @@ void trainer_init(sc_trainer* t) {
     }
     t->nonfinite.alloc(1);
     t->red_partial.alloc(1024);
-    t->amax.alloc(sc_trainer::kSlotBase + 2 * std::max(t->L, 1));
     ensure_rows(t, n_max);
     int64_t max_seg = 0;
     for (int i : t->local) max_seg = std::max<int64_t>(max_seg, t->ps[i].heavy.nseg);
@@ -229,8 +245,18 @@ void trainer_init(sc_trainer* t) {
         SC_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         SC_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, greatest));
     }
-    t->tc.init(t);
     SC_CUDA(cudaStreamSynchronize(s));
+}
+
+void trainer_init_eval_only(sc_trainer* t) {
+    sc_graph* g = t->g;
+    if (t->L < 0) throw std::invalid_argument("layers must be >= 0");
+    for (int h : t->hidden)
+        if (h < 1) throw std::invalid_argument("make_sage_model: hidden dims must be positive");
+    if (g->dim == 0 || g->num_classes == 0) throw std::invalid_argument("evaluate: graph lacks features or labels");
+    t->eval_only = true;
+    init_model(t);
+    SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
 }
 
 // loss weight = train_mask ? scheme weight : 0; scale = (float)(w / normalizer)
@@ -306,40 +332,58 @@ double spmm_bytes(const Rows& R, int H, bool bwd) {
     return b;
 }
 
-// sage_forward (nn.hpp:192-242). Writes logits; keeps the cache in t's buffers.
-void forward(sc_trainer* t, const Rows& R, float* logits) {
+// Activation buffers of one forward pass: X[l] (layer inputs, l >= 1), MSG[l],
+// MEAN[l], inv. Training keeps one buffer per layer (the backward's cache);
+// evaluation may alias them (ping-pong X, one MSG, one MEAN).
+struct Acts {
+    std::vector<float*> X, MSG, MEAN;
+    float* inv = nullptr;
+};
+Acts train_acts(sc_trainer* t) {
+    Acts a;
+    a.X.assign(t->L + 1, nullptr);
+    for (int l = 1; l <= t->L; ++l) a.X[l] = t->X[l].get();
+    for (int l = 0; l < t->L; ++l) {
+        a.MSG.push_back(t->MSG[l].get());
+        a.MEAN.push_back(t->MEAN[l].get());
+    }
+    a.inv = t->inv.get();
+    return a;
+}
+
+// sage_forward (nn.hpp:192-242). Writes logits; the cache lands in A.
+void forward(sc_trainer* t, const Rows& R, float* logits, const Acts& A) {
     cudaStream_t s = t->ctx->stream;
     Profiler& P = t->prof;
     const int64_t n = R.n;
     P.begin("inv_degree", double(n) * 12 + double(R.offsets ? 8 : 0) * n, s);
-    inv_degree(n, R.offsets, R.bits, t->inv.get(), s);
+    inv_degree(n, R.offsets, R.bits, A.inv, s);
     P.end(s);
     const MatA x0{R.x0, R.x0_ld, nullptr, t->d};
     for (int l = 0; l < t->L; ++l) {
         const LayerOff& lo = t->lay[l];
-        const MatA xin = l == 0 ? x0 : MatA{t->X[l].get(), lo.in, nullptr, lo.in};
+        const MatA xin = l == 0 ? x0 : MatA{A.X[l], lo.in, nullptr, lo.in};
         const float* xin_amax = l == 0 ? t->g->feat_amax.get() : t->amax_x(l);
         // msg = relu(h W^T)   (nn.hpp:220-221)
         P.begin("gemm_msg", 4.0 * n * (lo.in + lo.H), s, 2.0 * n * lo.in * lo.H);
         t->tc.nt(t, xin, xin_amax, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, nullptr,
-                 t->MSG[l].get(), lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l));
+                 A.MSG[l], lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l));
         P.end(s);
         // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
         P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
-        spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->inv.get(), t->MSG[l].get(), t->MEAN[l].get(), s, R.hv,
-                 t->heavy_ws.get());
+        spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, A.inv, A.MSG[l], A.MEAN[l], s, R.hv, t->heavy_ws.get());
         P.end(s);
         // h' = mean U_L^T + h U_R^T   (nn.hpp:233-234)
         const MatB uL{t->theta.get() + lo.U, lo.H + lo.in, false};
         const MatB uR{t->theta.get() + lo.U + lo.H, lo.H + lo.in, false};
-        const MatA mean{t->MEAN[l].get(), lo.H, nullptr, lo.H};
+        const MatA mean{A.MEAN[l], lo.H, nullptr, lo.H};
         P.begin("gemm_update", 4.0 * n * (2 * lo.H + lo.in), s, 2.0 * n * (lo.H + lo.in) * lo.H);
         // |mean| <= max|msg| (a mean of msg rows): msg's bound scales it.
-        t->tc.nt(t, mean, t->amax_msg(l), uL, &xin, xin_amax, &uR, t->X[l + 1].get(), lo.H, n, lo.H, kEpiNone, nullptr,
+        t->tc.nt(t, mean, t->amax_msg(l), uL, &xin, xin_amax, &uR, A.X[l + 1], lo.H, n, lo.H, kEpiNone, nullptr,
                  t->amax_x(l + 1));
         P.end(s);
     }
-    const MatA emb = t->L == 0 ? x0 : MatA{t->X[t->L].get(), t->E, nullptr, t->E};
+    const MatA emb = t->L == 0 ? x0 : MatA{A.X[t->L], t->E, nullptr, t->E};
     P.begin("gemm_head", 4.0 * n * (t->E + t->C), s, 2.0 * n * t->E * t->C);
     const float* emb_amax = t->L == 0 ? t->g->feat_amax.get() : t->amax_x(t->L);
     t->tc.nt(t, emb, emb_amax, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, nullptr, logits,
@@ -457,14 +501,14 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get(),
                  st.x0.get(), t->dp, &st.heavy};
     SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
-    forward(t, R, st.logits.get());
+    forward(t, R, st.logits.get(), train_acts(t));
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
     if (t->loss == 0)
         softmax_ce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
                    t->G.get(), t->row_loss.get(), s);
     else
-        bce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(), t->G.get(),
-            t->row_loss.get(), s);
+        bce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), t->g->multilabel ? t->g->targets.get() : nullptr,
+            pd.nodes.get(), st.w.get(), st.scale.get(), t->G.get(), t->row_loss.get(), s);
     sum_f64(st.n, t->row_loss.get(), t->red_partial.get(), t->part_loss.get() + i, t->normalizer, s);
     t->prof.end(s);
     exchange_bucket(t, -1, i / t->world);
@@ -511,8 +555,8 @@ void trainer_step_async(sc_trainer* t, int epoch) {
     commit_staged_features(t);
     t->prof.records.clear();
     t->prof.used = 0;
-    if (t->world > 1 && !t->comm)
-        throw std::invalid_argument("sc_trainer_init_comm must be called before stepping with world > 1");
+    if (t->world > 1 && !t->comm && !t->xfn)
+        throw std::invalid_argument("sc_trainer_init_comm (or an exchange callback) must precede stepping at world > 1");
     // Exchange round j trains partition j*world + rank on every rank; each
     // finished gradient bucket (and the partition loss) is all-gathered on the
     // comm stream while the rest of backward runs. Every slot has exactly one
@@ -520,6 +564,7 @@ void trainer_step_async(sc_trainer* t, int epoch) {
     // the reference's single-process gather for any GPU count.
     t->xfer_used = 0;
     t->fork_used = 0;
+    t->audit_floats = uint64_t(t->local.size()) * uint64_t(t->P);  // each local partition hands |theta| floats over
     const int rounds = t->pp / t->world;
     for (int j = 0; j < rounds; ++j) {
         const int i = j * t->world + t->rank;
@@ -568,36 +613,100 @@ void trainer_finish(sc_trainer* t, double* loss, double* gnorm) {
     if (gnorm) *gnorm = t->last_gnorm;
 }
 
-void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
+namespace {
+// Full-graph forward (evaluate_splits, trainer.hpp:132-140) into t->eval_logits
+// with the current parameters; returns nothing, logits stay on the device.
+void eval_forward(sc_trainer* t) {
     cudaStream_t s = t->ctx->stream;
     sc_graph* g = t->g;
-    ensure_rows(t, g->n);
-    if (t->eval_logits.size() < size_t(g->n) * t->Cp) t->eval_logits.alloc(size_t(g->n) * t->Cp);
+    const int64_t n = g->n;
+    if (t->eval_logits.size() < size_t(n) * t->Cp) t->eval_logits.alloc(std::max<int64_t>(n * t->Cp, 1));
+    int32_t maxH = 1;
+    for (auto& lo : t->lay) maxH = std::max(maxH, lo.H);
     if (!t->eval_heavy_built) {
-        build_heavy_rows(t->ctx, g->n, g->offsets.get(), t->eval_heavy);
+        build_heavy_rows(t->ctx, n, g->offsets.get(), t->eval_heavy);
         t->eval_heavy_built = true;
-        int32_t maxH = 1;
-        for (auto& lo : t->lay) maxH = std::max(maxH, lo.H);
         if (size_t(t->eval_heavy.nseg) * maxH > t->heavy_ws.size()) t->heavy_ws.alloc(size_t(t->eval_heavy.nseg) * maxH);
     }
-    const Rows R{g->n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr,
-                 g->features.get(), g->dim, &t->eval_heavy};
+    Acts A;
+    if (!t->eval_only && n <= t->rows_cap) {
+        A = train_acts(t);  // the step is complete: its cache is free to overwrite
+    } else {
+        for (auto& b : t->ev_x) b.ensure(std::max<int64_t>(n * maxH, 1));
+        t->ev_msg.ensure(std::max<int64_t>(n * maxH, 1));
+        t->ev_mean.ensure(std::max<int64_t>(n * maxH, 1));
+        t->ev_inv.ensure(std::max<int64_t>(n, 1));
+        A.X.assign(t->L + 1, nullptr);
+        for (int l = 1; l <= t->L; ++l) A.X[l] = t->ev_x[l & 1].get();
+        A.MSG.assign(t->L, t->ev_msg.get());
+        A.MEAN.assign(t->L, t->ev_mean.get());
+        A.inv = t->ev_inv.get();
+    }
+    // layer-0 rows: the features themselves, or a 16-byte-row copy so the GEMMs stay on TMA
+    const float* x0 = g->features.get();
+    int64_t x0_ld = g->dim;
+    if (t->dp != t->d) {
+        if (t->eval_x0_version != g->feat_version || t->eval_x0.size() < size_t(n) * t->dp) {
+            t->eval_x0.ensure(std::max<int64_t>(n * t->dp, 1));
+            gather_rows(n, t->d, nullptr, g->features.get(), t->eval_x0.get(), s, t->dp);
+            t->eval_x0_version = g->feat_version;
+        }
+        x0 = t->eval_x0.get();
+        x0_ld = t->dp;
+    }
+    const Rows R{n, g->offsets.get(), g->nbrs.get(), nullptr, nullptr, 2 * g->m, 2 * g->m, nullptr, x0, x0_ld,
+                 &t->eval_heavy};
     const bool was = t->prof.enabled;
     t->prof.enabled = false;
-    forward(t, R, t->eval_logits.get());
+    SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // operand |max| slots of this pass
+    forward(t, R, t->eval_logits.get(), A);
     t->prof.enabled = was;
-    DevBuf<unsigned long long> cnt(6);
+}
+
+// metric_from_logits (trainer.cpp:66-97) over each device mask.
+void eval_metrics(sc_trainer* t, const uint8_t* const* masks, int nm, double* out) {
+    cudaStream_t s = t->ctx->stream;
+    sc_graph* g = t->g;
+    DevBuf<unsigned long long> cnt(4 * nm);
     SC_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-    count_correct(g->n, t->C, t->Cp, t->eval_logits.get(), g->labels.get(), g->train.get(), cnt.get(), s);
-    count_correct(g->n, t->C, t->Cp, t->eval_logits.get(), g->labels.get(), g->val.get(), cnt.get() + 2, s);
-    count_correct(g->n, t->C, t->Cp, t->eval_logits.get(), g->labels.get(), g->test.get(), cnt.get() + 4, s);
-    unsigned long long h[6];
-    d2h(h, cnt.get(), 6, s);
+    for (int i = 0; i < nm; ++i) {
+        if (g->multilabel)
+            f1_counts(g->n, t->C, t->Cp, t->eval_logits.get(), g->targets.get(), masks[i], cnt.get() + 4 * i, s);
+        else
+            count_correct(g->n, t->C, t->Cp, t->eval_logits.get(), g->labels.get(), masks[i], cnt.get() + 4 * i, s);
+    }
+    std::vector<unsigned long long> h(4 * nm);
+    d2h(h.data(), cnt.get(), 4 * nm, s);
     SC_CUDA(cudaStreamSynchronize(s));
-    auto frac = [](unsigned long long c, unsigned long long n) { return n ? double(c) / double(n) : 0.0; };
-    *tr = frac(h[0], h[1]);
-    *va = frac(h[2], h[3]);
-    *te = frac(h[4], h[5]);
+    for (int i = 0; i < nm; ++i) {
+        const unsigned long long* c = h.data() + 4 * i;
+        if (g->multilabel) {  // micro-F1 with positives at logit > 0
+            const unsigned long long denom = 2 * c[0] + c[1] + c[2];
+            out[i] = (c[3] == 0 || denom == 0) ? 0.0 : 2.0 * double(c[0]) / double(denom);
+        } else {
+            out[i] = c[1] ? double(c[0]) / double(c[1]) : 0.0;
+        }
+    }
+}
+}  // namespace
+
+void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te) {
+    trainer_finish(t, nullptr, nullptr);  // metrics of a settled step only
+    eval_forward(t);
+    const uint8_t* masks[3] = {t->g->train.get(), t->g->val.get(), t->g->test.get()};
+    double out[3];
+    eval_metrics(t, masks, 3, out);
+    *tr = out[0];
+    *va = out[1];
+    *te = out[2];
+}
+
+double trainer_evaluate_mask(sc_trainer* t, const uint8_t* mask_dev) {
+    trainer_finish(t, nullptr, nullptr);
+    eval_forward(t);
+    double out = 0.0;
+    eval_metrics(t, &mask_dev, 1, &out);
+    return out;
 }
 
 void trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
@@ -610,9 +719,42 @@ void trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
     if (!t->comm_done) SC_CUDA(cudaEventCreateWithFlags(&t->comm_done, cudaEventDisableTiming));
 }
 
+namespace {
+// The same all-gather through the caller's host transport: wait for the
+// producer, stage this rank's bytes in pinned memory, call out, copy the
+// gathered range back. Synchronous (test / fallback transport, not the fast path).
+void exchange_host(sc_trainer* t, int b, int round, cudaStream_t s) {
+    const int first = round * t->world;
+    const int kind = b < 0 ? 1 : 0;
+    const size_t per = b < 0 ? sizeof(double) : sizeof(float) * size_t(t->b_len(b));
+    unsigned char* base = b < 0 ? reinterpret_cast<unsigned char*>(t->part_loss.get() + first)
+                                : reinterpret_cast<unsigned char*>(t->slot_ptr(b, first));
+    const size_t need = per * (size_t(t->world) + 1);
+    if (t->xhost_bytes < need) {
+        if (t->xhost) SC_CUDA(cudaFreeHost(t->xhost));
+        t->xhost = nullptr;
+        SC_CUDA(cudaMallocHost(&t->xhost, need));
+        t->xhost_bytes = need;
+    }
+    unsigned char* send = static_cast<unsigned char*>(t->xhost);
+    unsigned char* recv = send + per;
+    SC_CUDA(cudaMemcpyAsync(send, base + per * t->rank, per, cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaStreamSynchronize(s));
+    if (t->xfn(t->xuser, kind, round, b, send, recv, static_cast<int64_t>(per)) != 0)
+        throw std::runtime_error("gradient exchange callback failed (round " + std::to_string(round) + ", bucket " +
+                                 std::to_string(b) + ")");
+    SC_CUDA(cudaMemcpyAsync(base, recv, per * t->world, cudaMemcpyHostToDevice, s));
+    SC_CUDA(cudaStreamSynchronize(s));
+}
+}  // namespace
+
 void exchange_bucket(sc_trainer* t, int b, int round, cudaStream_t producer) {
-    if (!t->comm) return;  // world == 1 without a communicator: nothing to exchange
     cudaStream_t s = producer ? producer : t->ctx->stream;
+    if (t->xfn) {
+        exchange_host(t, b, round, s);
+        return;
+    }
+    if (!t->comm) return;  // world == 1 without a communicator: nothing to exchange
     if (t->xfer_used == t->xfer_events.size()) {
         cudaEvent_t e;
         SC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -103,6 +103,18 @@ struct sc_trainer {
     sc::DevBuf<float> heavy_ws;   // segment partial sums of the heavy-row aggregation
     sc::HeavyRows eval_heavy;     // heavy rows of the full graph (evaluate_splits)
     bool eval_heavy_built = false;
+    // Full-graph evaluation reuses the training activations when they hold at
+    // least n rows (rows_cap >= n, e.g. products at p = 8); otherwise it runs on
+    // its own forward-only set: two ping-pong layer outputs, one message and one
+    // mean buffer, so a partition trainer never grows every training buffer to
+    // the full graph.
+    sc::DevBuf<float> ev_x[2], ev_msg, ev_mean, ev_inv;
+    sc::DevBuf<float> eval_x0;  // the full feature matrix with 16-byte rows (d % 4 != 0)
+    uint64_t eval_x0_version = 0;
+    bool eval_only = false;     // sc_evaluate's forward-only engine (no partitions, no optimizer)
+    // CommAudit (trainer.hpp:61-76): parameter-gradient floats this rank's
+    // partitions handed to the exchange in the last epoch (p * |theta| at world 1).
+    uint64_t audit_floats = 0;
     // Backward runs the weight-gradient GEMMs that only need dh (head: G^T emb;
     // update: dh^T [mean | h]) on a high-priority side stream, concurrently with
     // the dgrad -> transposed aggregation -> dW chain on the main stream.
@@ -136,6 +148,12 @@ struct sc_trainer {
     double last_loss = 0, last_gnorm = 0;
     sc::TcGemm tc;
     sc::Profiler prof;
+    // Host transport (sc_trainer_set_exchange), used instead of NCCL when set.
+    using ExchangeFn = int32_t (*)(void*, int32_t, int32_t, int32_t, const void*, void*, int64_t);
+    ExchangeFn xfn = nullptr;
+    void* xuser = nullptr;
+    void* xhost = nullptr;       // pinned staging: send (one rank's bytes) + recv (world x)
+    size_t xhost_bytes = 0;
     ncclComm_t comm = nullptr;
     cudaStream_t comm_stream = nullptr;      // gradient exchange, overlapped with backward
     std::vector<cudaEvent_t> xfer_events;    // compute -> comm stream hand-offs (reused per step)
@@ -152,6 +170,11 @@ void run_partition(sc_trainer* t, int i, int epoch);
 void trainer_step_async(sc_trainer* t, int epoch);
 void trainer_finish(sc_trainer* t, double* loss, double* gnorm);
 void trainer_evaluate(sc_trainer* t, double* tr, double* va, double* te);
+// evaluate (trainer.cpp:101-112): the current model's full-graph metric over one
+// split mask (device); accuracy, or micro-F1 on multi-label graphs.
+double trainer_evaluate_mask(sc_trainer* t, const uint8_t* mask_dev);
+// Forward-only engine over g for a given model (sc_evaluate).
+void trainer_init_eval_only(sc_trainer* t);
 void trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
 // Stage the next step's features (host or device source): the copy runs on the
 // graph's copy stream (copy engine only), overlapping the current step; the

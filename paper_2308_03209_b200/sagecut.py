@@ -65,6 +65,11 @@ _sig("sc_build_graph", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i
 _sig("sc_build_graph_dev", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i64)])
 _sig("sc_graph_set_data", [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp])
 _sig("sc_graph_set_features", [_vp, _vp, C.c_int])
+_sig("sc_graph_set_multilabels", [_vp, _vp, _i32])
+_sig("sc_graph_set_part_ownership", [_vp, _i32, _i32])
+_sig("sc_vcut_part_held", [_vp, _i32, C.POINTER(_i32)])
+EXCHANGE_FN = C.CFUNCTYPE(_i32, _vp, _i32, _i32, _i32, _vp, _vp, _i64)
+_sig("sc_trainer_set_exchange", [_vp, EXCHANGE_FN, _vp])
 _sig("sc_graph_info", [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i32)])
 _sig("sc_graph_copy_edges", [_vp, _vp])
 _sig("sc_graph_copy_csr", [_vp, _vp, _vp, _vp, _vp])
@@ -126,6 +131,13 @@ _sig("sc_trainer_get_part_loss", [_vp, _i32, C.POINTER(_f64)])
 _sig("sc_trainer_get_part_mask", [_vp, _i32, C.POINTER(_i32)])
 _sig("sc_trainer_evaluate", [_vp, C.POINTER(_f64), C.POINTER(_f64), C.POINTER(_f64)])
 _sig("sc_trainer_profile", [_vp, _i32])
+_sig("sc_trainer_evaluate_mask", [_vp, _vp, C.POINTER(_f64)])
+_sig("sc_evaluate", [_vp, _vp, _vp, _vp, _i32, _vp, C.POINTER(_f64)])
+_sig("sc_trainer_comm_audit", [_vp, C.POINTER(_u64), C.POINTER(_u64)])
+_sig("sc_trainer_fallback_count", [_vp, C.POINTER(_i64)])
+_sig("sc_comm_volume", [_i32, _i32, _u64, _u64, _u64, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)])
+_sig("sc_expected_rf_random", [_i32, _i64, C.POINTER(_f64)])
+_sig("sc_imbalance_lower_bound", [_i32, _i64, _i64, C.POINTER(_f64)])
 _sig("sc_trainer_kernel_times", [_vp, C.POINTER(C.c_char_p), C.POINTER(_f64), C.POINTER(_f64), _i32,
                                  C.POINTER(_i32)])
 _sig("sc_trainer_kernel_flops", [_vp, C.POINTER(_f64), _i32, C.POINTER(_i32)])
@@ -254,6 +266,7 @@ class Graph:
         n, m, d, c = _i32(), _i64(), _i32(), _i32()
         _check(_lib.sc_graph_info(self.h, C.byref(n), C.byref(m), C.byref(d), C.byref(c)))
         self.num_nodes, self._m, self.dim, self.num_classes = n.value, m.value, d.value, c.value
+        self.multilabel = False
 
     def num_edges(self) -> int:
         return self._m
@@ -285,6 +298,21 @@ class Graph:
         _check(_lib.sc_graph_set_data(self.h, _ptr(f), f.shape[1], _ptr(lab), int(num_classes), _ptr(tr), _ptr(va),
                                       _ptr(te)), "set_data")
         self.dim, self.num_classes = f.shape[1], int(num_classes)
+        self.multilabel = False
+
+    def set_part_ownership(self, rank: int, world: int):
+        """Vertex cuts built after this hold only the parts this rank trains (i % world == rank)."""
+        _check(_lib.sc_graph_set_part_ownership(self.h, rank, world), "set_part_ownership")
+
+    def set_multilabels(self, targets):
+        """Graph::multilabels (graph.hpp:64): n x C of 0/1; the graph then trains with bce
+        and evaluates with micro-F1 (trainer.cpp:72-87)."""
+        y = np.ascontiguousarray(targets, np.float32)
+        if y.ndim != 2 or y.shape[0] != self.num_nodes:
+            raise ValueError("set_multilabels: targets must be num_nodes x C")
+        _check(_lib.sc_graph_set_multilabels(self.h, _ptr(y), y.shape[1]), "set_multilabels")
+        self.num_classes = y.shape[1]
+        self.multilabel = True
 
     def set_features(self, features, device_ptr: Optional[int] = None, host_ptr: Optional[int] = None):
         """Replace the n x d feature matrix (same shape) from a numpy array, a host
@@ -380,6 +408,11 @@ class VertexCutPartition:
         return s
 
     @property
+    def part_held(self, i: int) -> bool:
+        x = _i32()
+        _check(_lib.sc_vcut_part_held(self.h, i, C.byref(x)))
+        return bool(x.value)
+
     def parts(self) -> List[PartSubgraph]:
         return [self.part(i) for i in range(self.num_parts)]
 
@@ -639,7 +672,7 @@ class CoFreeTrainer:
     """The state of train_cofree_impl (trainer.hpp:202-313) on one rank."""
 
     def __init__(self, g: Graph, part: VertexCutPartition, config: TrainConfig, rank: int = 0, world: int = 1,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, _defer_comm: bool = False):
         config.validate()
         self.g, self.part, self.config = g, part, config
         self.hidden = np.ascontiguousarray(config.resolved_hidden(), np.int32)
@@ -654,11 +687,32 @@ class CoFreeTrainer:
         _check(_lib.sc_trainer_param_count(self.h, C.byref(n)))
         self.param_count = n.value
         self.rank, self.world = rank, world
-        if world > 1 and nccl_id is None:
-            raise ValueError("world > 1 needs the rank-0 NCCL unique id")
+        if world > 1 and nccl_id is None and not _defer_comm:
+            raise ValueError("world > 1 needs the rank-0 NCCL unique id (or set_exchange with _defer_comm=True)")
         if nccl_id is not None:  # (world == 1 too: a single-rank communicator runs the exchange path)
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             _check(_lib.sc_trainer_init_comm(self.h, buf), "init_comm")
+
+    def set_exchange(self, allgather):
+        """Host transport for the gradient exchange instead of NCCL: allgather(kind, round, bucket, send: bytes)
+        must return the world ranks' byte strings concatenated in rank order (kind 0: one f32 gradient
+        bucket, 1: the round's f64 partition losses). None restores NCCL."""
+        if allgather is None:
+            self._xfn = None
+            _check(_lib.sc_trainer_set_exchange(self.h, EXCHANGE_FN(), None))
+            return
+
+        def cb(_user, kind, rnd, bucket, send, recv, nbytes):
+            try:
+                out = allgather(kind, rnd, bucket, C.string_at(send, nbytes))
+                C.memmove(recv, out, len(out))
+                return 0
+            except Exception as e:  # noqa: BLE001 (reported through the status code)
+                self._xerr = e
+                return 1
+
+        self._xfn = EXCHANGE_FN(cb)  # keep the trampoline alive
+        _check(_lib.sc_trainer_set_exchange(self.h, self._xfn, None))
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -740,6 +794,27 @@ class CoFreeTrainer:
         _check(_lib.sc_trainer_evaluate(self.h, C.byref(a), C.byref(b), C.byref(c)), "evaluate")
         return a.value, b.value, c.value
 
+    def evaluate_mask(self, mask) -> float:
+        """evaluate (trainer.cpp:101-112) of the current model over one split mask."""
+        m = np.ascontiguousarray(mask, np.uint8)
+        if m.size != self.g.num_nodes:
+            raise ValueError("evaluate: mask length != node count")
+        x = _f64()
+        _check(_lib.sc_trainer_evaluate_mask(self.h, _ptr(m), C.byref(x)), "evaluate")
+        return x.value
+
+    def comm_audit(self):
+        """CommAudit of the last step (trainer.hpp:61-76): (gradient floats, embedding floats)."""
+        a, b = _u64(), _u64()
+        _check(_lib.sc_trainer_comm_audit(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def fallback_count(self) -> int:
+        """GEMMs that fell back to the fp32 SIMT kernels on the tensor-core path (0 on TMA-friendly shapes)."""
+        x = _i64()
+        _check(_lib.sc_trainer_fallback_count(self.h, C.byref(x)))
+        return x.value
+
     def profile(self, enable: bool = True):
         _check(_lib.sc_trainer_profile(self.h, int(enable)))
 
@@ -771,9 +846,60 @@ class CoFreeTrainer:
 
 
 @dataclass
+class CommAudit:  # trainer.hpp:61-67
+    gradient_floats_per_epoch: List[int] = field(default_factory=list)
+    embedding_floats: int = 0
+
+
+@dataclass
+class CommReport:  # trainer.hpp:48-53
+    mode: str
+    floats_per_iteration: int
+    gradient_floats: int
+    embedding_floats: int
+
+
+def comm_volume(mode: str, num_parts: int, param_count: int, num_layers: int, hidden_dim: int,
+                total_halo: int) -> CommReport:  # trainer.cpp:38-49
+    a, b, c = _u64(), _u64(), _u64()
+    _check(_lib.sc_comm_volume({"cofree": 0, "halo_sync_model": 1}[mode], num_parts, param_count, num_layers,
+                               hidden_dim, total_halo, C.byref(a), C.byref(b), C.byref(c)), "comm_volume")
+    return CommReport(mode, a.value, b.value, c.value)
+
+
+def expected_rf_random(num_parts: int, degree: int) -> float:  # partition.cpp:344-349
+    x = _f64()
+    _check(_lib.sc_expected_rf_random(num_parts, degree, C.byref(x)), "expected_rf_random")
+    return x.value
+
+
+def imbalance_lower_bound(num_parts: int, max_degree: int, min_degree: int) -> float:  # partition.cpp:351-362
+    x = _f64()
+    _check(_lib.sc_imbalance_lower_bound(num_parts, max_degree, min_degree, C.byref(x)), "imbalance_lower_bound")
+    return x.value
+
+
+def evaluate(model, g: Graph, mask, hidden: Sequence[int]) -> float:
+    """evaluate (trainer.cpp:101-112): full-graph metric of a flat model (for_each_matrix
+    order; hidden = the resolved per-layer dims) over one split mask, forward-only on the device."""
+    theta = np.ascontiguousarray(model, np.float32)
+    h = np.ascontiguousarray(hidden, np.int32)
+    m = np.ascontiguousarray(mask, np.uint8)
+    if m.size != g.num_nodes:
+        raise ValueError("evaluate: mask length != node count")
+    if theta.size != param_count(g.dim, list(h), g.num_classes):
+        raise ValueError("evaluate: model does not match the graph's dims")
+    x = _f64()
+    _check(_lib.sc_evaluate(g.ctx.h, g.h, _ptr(theta), _ptr(h) if h.size else None, h.size, _ptr(m), C.byref(x)),
+           "evaluate")
+    return x.value
+
+
+@dataclass
 class TrainResult:  # trainer.hpp:71-75
     model: np.ndarray
     metrics: List[EpochMetrics]
+    audit: CommAudit = field(default_factory=CommAudit)
 
 
 def train_full_graph(g: Graph, config: TrainConfig, evaluate: bool = True) -> TrainResult:
@@ -794,8 +920,10 @@ def train_cofree(g: Graph, part: VertexCutPartition, config: TrainConfig, evalua
     and (like the reference) a full-graph evaluation after every epoch."""
     t = CoFreeTrainer(g, part, config)
     metrics = []
+    audit = CommAudit()
     for epoch in range(config.epochs):
         loss, gn = t.step(epoch)
+        audit.gradient_floats_per_epoch.append(t.comm_audit()[0])
         tr, va, te = t.evaluate() if evaluate else (0.0, 0.0, 0.0)
         metrics.append(EpochMetrics(epoch, loss, tr, va, te, gn, part.num_parts * t.param_count))
-    return TrainResult(t.params(), metrics)
+    return TrainResult(t.params(), metrics, audit)

@@ -81,6 +81,15 @@ int main(int argc, char** argv) {
             std::printf("ckpt_same %d\n", sb::load_checkpoint(dir + "/model.ckpt") == res.model ? 1 : 0);
             sb::write_metrics_jsonl(res.metrics, dir + "/metrics.jsonl");
         }
+        // evaluate / CommAudit / analytic helpers (trainer.cpp:38-49, 101-112; partition.cpp:344-362)
+        std::printf("eval_test %.17g\n", sb::evaluate(res, g, te));
+        std::printf("audit");
+        for (auto f : res.audit.gradient_floats_per_epoch) std::printf(" %llu", (unsigned long long)f);
+        std::printf(" %llu\n", (unsigned long long)res.audit.embedding_floats);
+        const auto cv = sb::comm_volume(sb::CommMode::halo_sync_model, p, res.model.size(), 2, 16, 100);
+        std::printf("comm %llu %llu %llu\n", (unsigned long long)cv.floats_per_iteration,
+                    (unsigned long long)cv.gradient_floats, (unsigned long long)cv.embedding_floats);
+        std::printf("erf %.17g\nilb %.17g\n", sb::expected_rf_random(p, 13), sb::imbalance_lower_bound(p, 9, 2));
         std::printf("loss");
         for (const auto& e : res.metrics) std::printf(" %.17g", e.train_loss);
         std::printf("\nparams");

@@ -75,6 +75,14 @@ class CpuLib:
         f("graph_labels").argtypes = [_p, _i32p]
         f("graph_masks").argtypes = [_p, _u8p, _u8p, _u8p]
         f("graph_set_data").argtypes = [_p, _f32p, C.c_int, _i32p, C.c_int, _u8p, _u8p, _u8p]
+        f("graph_set_multilabels").argtypes = [_p, _f32p, C.c_int]
+        f("evaluate").argtypes = [_p, _f64p, _i32p, C.c_int, _u8p, C.POINTER(C.c_double)]
+        f("comm_volume").argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _u64p]
+        f("expected_rf_random").argtypes = [C.c_int, C.c_int64, C.POINTER(C.c_double)]
+        f("imbalance_lower_bound").argtypes = [C.c_int, C.c_int64, C.c_int64, C.POINTER(C.c_double)]
+        if prefix == "or_":
+            f("spmm").argtypes = [C.c_int, C.c_int64, C.c_int32, _p, _p, _p, _p, _p, _p, _p, C.c_int]
+            f("spmm").restype = None
         f("partition").restype = _p
         f("partition").argtypes = [_p, C.c_int, C.c_int, C.c_uint64]
         f("partition_ne").restype = _p
@@ -144,6 +152,38 @@ class CpuLib:
         d = np.zeros(n, np.float64)
         self._f("rng_draws")(seed, kind, arg, n, u.ctypes.data_as(C.c_void_p), d.ctypes.data_as(C.c_void_p))
         return u if kind in (0, 1) else d
+
+    # ---- analytic models (trainer.cpp:38-49, partition.cpp:344-362) ----
+    def comm_volume(self, mode, p, params, layers, hidden, halo):
+        out = np.zeros(3, np.uint64)
+        self._check(self._f("comm_volume")({"cofree": 0, "halo_sync_model": 1}[mode], p, params, layers, hidden,
+                                           halo, out), "comm_volume")
+        return [int(x) for x in out]
+
+    def expected_rf_random(self, p, degree):
+        x = C.c_double()
+        self._check(self._f("expected_rf_random")(p, degree, C.byref(x)), "expected_rf_random")
+        return x.value
+
+    def imbalance_lower_bound(self, p, max_d, min_d):
+        x = C.c_double()
+        self._check(self._f("imbalance_lower_bound")(p, max_d, min_d, C.byref(x)), "imbalance_lower_bound")
+        return x.value
+
+    def spmm(self, bwd, offsets, nbrs, eids, mask, src, msg=None, threads=8):
+        """The restatement's masked mean aggregation (nn.hpp:209-230) or its transpose (:277-288)."""
+        assert self.pre == "or_"
+        off = np.ascontiguousarray(offsets, np.int64)
+        nb = np.ascontiguousarray(nbrs, np.int32)
+        ei = np.ascontiguousarray(eids, np.int32)
+        src = np.ascontiguousarray(src, np.float32)
+        n, H = len(off) - 1, src.shape[1]
+        out = np.empty((n, H), np.float32)
+        mk = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        ms = None if msg is None else np.ascontiguousarray(msg, np.float32)
+        self._f("spmm")(int(bwd), n, H, off.ctypes.data, nb.ctypes.data, ei.ctypes.data, _ptr_or_null(mk),
+                        src.ctypes.data, _ptr_or_null(ms), out.ctypes.data, threads)
+        return out
 
     # ---- graphs ----
     def graph_build(self, n, uv):
@@ -225,6 +265,18 @@ class Graph:
             self.h, feats.reshape(-1), feats.shape[1], np.ascontiguousarray(labels, np.int32), classes,
             np.ascontiguousarray(train, np.uint8), np.ascontiguousarray(val, np.uint8),
             np.ascontiguousarray(test, np.uint8)), "set_data")
+
+    def set_multilabels(self, y):
+        y = np.ascontiguousarray(y, np.float32)
+        self.lib._check(self.lib._f("graph_set_multilabels")(self.h, y.reshape(-1), y.shape[1]), "set_multilabels")
+
+    def evaluate(self, theta, hidden, mask):
+        """evaluate (trainer.cpp:101-112) of a flat f64 model over one mask."""
+        x = C.c_double()
+        self.lib._check(self.lib._f("evaluate")(self.h, np.ascontiguousarray(theta, np.float64),
+                                                np.ascontiguousarray(hidden, np.int32), len(hidden),
+                                                np.ascontiguousarray(mask, np.uint8), C.byref(x)), "evaluate")
+        return x.value
 
     def partition(self, algo, p, seed):
         algo_id = {"random": 0, "dbh": 1, "ne": 2, "ec2vc": 3}[algo]

@@ -58,3 +58,11 @@ def test_cpp_facade_matches_oracle(tmp_path):
     assert len((tmp_path / "metrics.jsonl").read_text().splitlines()) == epochs
     assert '"weight_scheme": "dar"' in (tmp_path / "part.json").read_text()
     assert res["error"].startswith("invalid_argument num_parts must be >= 1")
+    # evaluate of the trained model, CommAudit, comm_volume, expected_rf / imbalance bound
+    assert abs(float(res["eval_test"]) - O.graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7).evaluate(
+        theta, [16, 16], te)) <= 0.02
+    P = len(theta)
+    assert [int(x) for x in res["audit"].split()] == [p * P] * epochs + [0]
+    assert [int(x) for x in res["comm"].split()] == O.comm_volume("halo_sync_model", p, P, 2, 16, 100)
+    assert float(res["erf"]) == O.expected_rf_random(p, 13)
+    assert float(res["ilb"]) == O.imbalance_lower_bound(p, 9, 2)

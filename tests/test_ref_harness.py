@@ -27,10 +27,13 @@ def test_harness_equals_train_cofree():
             out = np.zeros(t.nparam)
             L, G, M = np.zeros(6), np.zeros(6), np.zeros(18)
             fn = R.lib.ref_train_cofree
+            audit = np.zeros(7, np.uint64)
             fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
-                           C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 4
+                           C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 5
             st = fn(g.h, part.h, hidden.ctypes.data, 2, 0.01, 0, 0, de, 10, 0.5, 1, f32, 1, 6,
-                    out.ctypes.data, L.ctypes.data, G.ctypes.data, M.ctypes.data)
+                    out.ctypes.data, L.ctypes.data, G.ctypes.data, M.ctypes.data, audit.ctypes.data)
             assert st == 0
+            # TrainResult::audit: p * |theta| gradient floats per epoch, no embeddings (trainer.hpp:303-309)
+            assert audit[:6].tolist() == [8 * t.nparam] * 6 and audit[6] == 0
             np.testing.assert_array_equal(theta, out)
             np.testing.assert_array_equal(losses, L)
