@@ -197,14 +197,36 @@ def measured_tensor_peak():
         return 2250.0, "fallback (nominal dense bf16)"
 
 
-def ncu_traffic(name):
-    """Per-launch DRAM bytes of the kernel from the committed ncu --set full summary, if any."""
+def ncu_traffic(config, scale):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the aggregation kernels
+    for THIS config and scale, from the committed ncu capture (profiles/ncu_traffic.json, written by
+    tools/ncu_traffic.py), or None when that config was not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(name)
+            entry = json.load(f).get(f"{config}@{scale:g}")
+        return entry if isinstance(entry, dict) else None
     except Exception:
         return None
+
+
+def host_info():
+    """CPU model, host threads and RAM of the machine the CPU baseline runs on."""
+    model, mem_gb = None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    mem_gb = round(int(line.split()[1]) / 1e6, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count(), "ram_gb": mem_gb}
 
 
 # ---------------------------------------------------------------------------- CPU reference
@@ -244,9 +266,52 @@ def cpu_reference_sample(cfg, steps, warmup, scale=None):
             blas = bool(lib.lib.ref_blas_active())
         except Exception:
             pass
-    return dict(value=value, unit="edges/s", cores=cores, kind=kind, sample=sample, epoch_s=sec,
+    return dict(value=value, unit="edges/s", cores=cores, kind=kind, sample=sample, epoch_s=sec, host=host_info(),
                 gemm_backend=("OpenBLAS sgemm, 1 thread/worker" if blas else "shim loop GEMM") if kind == "reference"
                 else "oracle loops")
+
+
+def full_scale_reference():
+    """The committed full-scale measurement of the reference: one products partition's
+    training step timed at full size on the GPU box's host, extrapolated x p (profiles/, written by
+    `bench.py --cpu-full-partition`), or None."""
+    path = os.path.join(ROOT, "profiles", "r02_reference_full_partition.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cpu_full_partition(cfg, part_index=0):
+    """the reference's per-partition training step (forward + loss + backward of
+    train_cofree_impl's worker, 1 thread) on ONE partition of the FULL-size workload, timed once, then
+    extrapolated to an epoch: x p with one worker, x ceil(p / workers) with `workers` threads (the
+    reference runs min(workers, p) partitions at a time; memory permitting)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cpu_libs
+
+    lib = cpu_libs.reference()
+    t0 = time.perf_counter()
+    n, uv, feats, labels, tr, va, te = synth_host(cfg, seed=0)
+    g = lib.graph_build(n, uv)
+    del uv
+    g.set_data(feats, labels, cfg["classes"], tr, va, te)
+    part = g.partition("random", cfg["parts"], 0)
+    t = part.trainer([cfg["hidden"]] * cfg["layers"], lr=cfg["lr"], dropedge=cfg["dropedge"], k=cfg["k"],
+                     ratio=cfg["ratio"], seed=1, f32=True, workers=1)
+    setup = time.perf_counter() - t0
+    sec = t.time_part_step(part_index, 0, 1)
+    p = cfg["parts"]
+    kept = kept_entries([part.sizes(i)[1] for i in range(p)], cfg)
+    workers = min(p, os.cpu_count() or 1)
+    epoch1 = sec * p
+    epochw = sec * math.ceil(p / workers)
+    return {"kind": "reference", "what": "one full-scale partition's step (1 thread), extrapolated",
+            "partition": part_index, "partition_step_s": sec, "setup_s": setup,
+            "epoch_s_1_worker": epoch1, "edges_per_s_1_worker": cfg["layers"] * kept / epoch1,
+            "workers": workers, "epoch_s_workers": epochw, "edges_per_s_workers": cfg["layers"] * kept / epochw,
+            "host": host_info(), "workload": cfg["workload"]}
 
 
 def run_reference_arm(args, cfg):
@@ -261,7 +326,8 @@ def run_reference_arm(args, cfg):
                        "layers": cfg["layers"], "hidden": cfg["hidden"], "feats": cfg["feats"],
                        "classes": cfg["classes"], "dropedge": cfg["dropedge"]},
             "cpu_baseline": {"value": res["value"], "unit": "edges/s", "cores": res["cores"], "kind": res["kind"],
-                             "sample": res["sample"], "gemm": res["gemm_backend"]},
+                             "sample": res["sample"], "gemm": res["gemm_backend"], "host": res["host"],
+                             "full_scale_extrapolated": full_scale_reference()},
             "e2e": {"value": res["value"], "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -327,32 +393,51 @@ def run_gpu_arm(args, cfg):
     for _ in range(args.warmup):
         trainer.step(epoch)
         epoch += 1
-    # ---- timed region: K epochs, device events on the library's stream
-    trainer.profile(True)
+    # ---- timed region (the headline value): K epochs, no profiling events, device time on the
+    # library's stream between a barrier + sync on both sides
+    trainer.profile(False)
     barrier()
     ctx.sync()
     launches0 = ctx.launch_count()
+    fallbacks0 = trainer.fallback_count()
+    losses = []
     with ClockSampler(local) as clocks:
         ctx.timer_start()
-        losses = []
-        prof = {}
-        flops = {}
         for _ in range(args.steps):
             losses.append(trainer.step(epoch)[0])
-            fl = trainer.kernel_flops()
-            for k, (ms, by) in trainer.kernel_times().items():
-                flops[k] = flops.get(k, 0.0) + fl.get(k, 0.0)
-                a = prof.setdefault(k, [0.0, 0.0])
-                a[0] += ms
-                a[1] += by
             epoch += 1
         ms = ctx.timer_stop()
     launches = ctx.launch_count() - launches0
+    fallbacks = trainer.fallback_count() - fallbacks0
     free_b, total_b = torch.cuda.mem_get_info(local)  # device memory in use (graph, partitions, trainer)
-    trainer.profile(False)
     barrier()
     ms_step = max_over_ranks(ms / args.steps)
     value = cfg["layers"] * kept / (ms_step / 1e3)
+
+    # ---- breakdown pass (separate, not part of `value`): the same K epochs with CUDA events around
+    # every kernel group on the stream it runs on; the roofline objects come from here
+    trainer.profile(True)
+    prof, flops = {}, {}
+    barrier()
+    ctx.sync()
+    ctx.timer_start()
+    for _ in range(args.steps):
+        trainer.step(epoch)
+        fl = trainer.kernel_flops()
+        for k, (kms, by) in trainer.kernel_times().items():
+            flops[k] = flops.get(k, 0.0) + fl.get(k, 0.0)
+            a = prof.setdefault(k, [0.0, 0.0])
+            a[0] += kms
+            a[1] += by
+        epoch += 1
+    prof_ms = ctx.timer_stop() / args.steps
+    trainer.profile(False)
+
+    # ---- full-graph evaluation (evaluate_splits, trainer.hpp:306), timed apart from the epoch
+    ctx.sync()
+    ctx.timer_start()
+    eval_metrics = trainer.evaluate()
+    eval_ms = ctx.timer_stop()
 
     # ---- e2e: the public API with host buffers: every step's input (the feature matrix, from pinned
     # host memory) is copied host -> device inside the timed region and the loss, grad-norm (f64) and
@@ -380,8 +465,23 @@ def run_gpu_arm(args, cfg):
     peak, peak_kind = measured_peaks()
     spmm_ms = sum(prof.get(k, [0, 0])[0] for k in ("spmm_fwd", "spmm_bwd"))
     spmm_bytes = sum(prof.get(k, [0, 0])[1] for k in ("spmm_fwd", "spmm_bwd"))
-    launches_spmm = 2 * cfg["layers"] * len(range(rank, cfg["parts"], world)) * args.steps
+    launches_dir = cfg["layers"] * len(range(rank, cfg["parts"], world)) * args.steps  # per direction
+    launches_spmm = 2 * launches_dir
     achieved = spmm_bytes / (spmm_ms / 1e3) / 1e9 if spmm_ms > 0 else 0.0
+    # DRAM-measured view (ncu, this config): what the kernel actually moved. When the algorithmic
+    # bytes exceed it (L2-resident message rows, e.g. Reddit's 239 MB msg matrix), the algorithmic
+    # fraction can pass 1; the DRAM fraction stays a true roofline fraction.
+    traffic = ncu_traffic(args.config, scale)
+    dram = None
+    if traffic and spmm_ms > 0 and "spmm_fwd" in traffic and "spmm_bwd" in traffic:
+        dram_bytes = launches_dir * (traffic["spmm_fwd"] + traffic["spmm_bwd"])
+        dram = {"GB_per_s": dram_bytes / (spmm_ms / 1e3) / 1e9, "frac": dram_bytes / (spmm_ms / 1e3) / 1e9 / peak,
+                "bytes_per_launch_fwd": traffic["spmm_fwd"], "bytes_per_launch_bwd": traffic["spmm_bwd"],
+                "source": traffic.get("source")}
+    props = torch.cuda.get_device_properties(local)
+    l2_bytes = getattr(props, "L2_cache_size", None)
+    max_rows = max(part.part_sizes(i)[0] for i in range(cfg["parts"]))
+    act_bytes = max_rows * cfg["hidden"] * 4
     total_prof = sum(v[0] for v in prof.values())
     kernels = {k: {"ms_per_step": v[0] / args.steps, "share": v[0] / total_prof if total_prof else None,
                    "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 and v[1] > 0 else None,
@@ -405,7 +505,8 @@ def run_gpu_arm(args, cfg):
     if world == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_reference_sample(cfg, steps=1, warmup=0)
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "host")}
+            cpu["full_scale_extrapolated"] = full_scale_reference()
         except Exception as e:  # the baseline must not sink the GPU line
             cpu = {"value": None, "unit": "edges/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
     line = {
@@ -419,14 +520,23 @@ def run_gpu_arm(args, cfg):
                    "dropedge": f"p={cfg['ratio']} K={cfg['k']}" if cfg["dropedge"] else None,
                    "degrees": degree_stats, "rf": sc.replication_stats(part, g).rf,
                    "kept_csr_entries_per_epoch": kept, "parallelism": f"dp{world} over {cfg['parts']} fixed partitions",
-                   "gemm": args.gemm, "l2": "inputs > L2 (each activation matrix is n_i x 256 fp32 = 2.5 GB)"},
+                   "gemm": args.gemm,
+                   "l2": {"l2_bytes": l2_bytes, "activation_matrix_bytes": act_bytes,
+                          "inputs_exceed_l2": bool(l2_bytes and act_bytes > l2_bytes),
+                          "note": "no L2 flush between steps: every step streams activation matrices of "
+                                  f"{act_bytes / 1e9:.2f} GB (largest partition x hidden x 4 B) "
+                                  + ("> L2" if l2_bytes and act_bytes > l2_bytes else "<= L2 (partly L2-resident)")}},
         "epoch_ms": ms_step,
+        "timing": "value: unprofiled timed region; kernels / roofline: a separate profiled pass of the same K "
+                  f"epochs ({prof_ms:.2f} ms/epoch with events)",
         "roofline": {"kernel": "spmm (masked mean aggregation fwd + transposed bwd)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,
-                     "traffic": ncu_traffic("spmm"), "launches": launches_spmm,
+                     "traffic": ((traffic["spmm_fwd"] + traffic["spmm_bwd"]) / 2 if dram else None),
+                     "launches": launches_spmm,
                      "bytes_per_launch": spmm_bytes / max(launches_spmm, 1),
-                     "share_of_step": spmm_ms / total_prof if total_prof else None},
+                     "share_of_step": spmm_ms / total_prof if total_prof else None,
+                     "dram_measured": dram},
         "dominant_kernel": dominant,
         "roofline_gemm": roofline_gemm,
         "kernels": kernels,
@@ -434,6 +544,9 @@ def run_gpu_arm(args, cfg):
         "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(feats.nbytes), "d2h_bytes_per_step": 20},
         "gpu_launches": launches,
+        "simt_fallbacks": fallbacks,
+        "eval": {"ms": eval_ms, "train_val_test": list(eval_metrics),
+                 "note": "full-graph evaluate_splits (trainer.hpp:306), not in the epoch time"},
         "clocks": clocks.summary(),
         "setup_s": setup_s,
         "hbm_used_gb": round((total_b - free_b) / 1e9, 1),
@@ -453,10 +566,19 @@ def main():
     ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
     ap.add_argument("--gemm", default="auto", choices=["auto", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-full-partition", action="store_true",
+                    help="time the reference on one FULL-size partition (minutes of CPU; BASELINE.md §3) and write "
+                         "profiles/r02_reference_full_partition.json")
     ap.add_argument("--scale", type=float, default=None,
                     help="scale nodes and edges of the config (default 1; rmat: 0.25, see CONFIGS)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.cpu_full_partition:
+        res = cpu_full_partition(cfg)
+        print(json.dumps(res), flush=True)
+        with open(os.path.join(ROOT, "profiles", "r02_reference_full_partition.json"), "w") as f:
+            json.dump(res, f, indent=1)
+        return
     if args.impl == "reference":
         run_reference_arm(args, cfg)
     else:

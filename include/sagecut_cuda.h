@@ -297,6 +297,22 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
 sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A, int32_t N1, const float* B1,
                            int32_t N2a, const float* B2, int64_t b2_rows, int32_t N2b, const int32_t* rows2, float* C);
 
+/* The masked mean aggregation alone (nn.hpp:209-230; bwd = 0) or its
+ * transpose with the ReLU gate (nn.hpp:277-288, pull form; bwd = 1), through the
+ * trainer's kernels (spmm_fwd / spmm_bwd incl. the segmented hub-row path), on a
+ * CSR with int64 offsets (n + 1), neighbours and local edge ids (offsets[n]),
+ * an optional per-local-edge keep mask (num_edges bytes, as the reference's
+ * DropEdge masks index edges). src: n x H (fwd: msg; bwd: dmean already scaled
+ * by inv); msg (bwd): the forward's messages (gate = msg > 0); out: n x H. Host
+ * buffers. */
+sc_status sc_debug_spmm(sc_ctx* ctx, int32_t bwd, int64_t n, int32_t H, const int64_t* offsets,
+                        const int32_t* nbrs, const int32_t* eids, int64_t num_edges, const uint8_t* edge_mask,
+                        const float* src, const float* msg, float* out);
+/* Copy `bytes` of a trainer activation buffer ("X" layer 1..L, "MSG" / "MEAN"
+ * layer 0..L-1, "inv", "G") to device memory: after a step they hold the last
+ * local partition's forward cache (parity diagnostics). */
+sc_status sc_trainer_debug_buffer(sc_trainer* t, const char* name, int32_t layer, void* dst_dev, int64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1026,6 +1026,67 @@ sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A,
     });
 }
 
+sc_status sc_debug_spmm(sc_ctx* ctx, int32_t bwd, int64_t n, int32_t H, const int64_t* offsets,
+                        const int32_t* nbrs, const int32_t* eids, int64_t num_edges, const uint8_t* edge_mask,
+                        const float* src, const float* msg, float* out) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && offsets && src && out && n >= 0 && H >= 1, "sc_debug_spmm: bad arguments");
+        REQUIRE_ARG(!bwd || msg, "sc_debug_spmm: the transposed aggregation needs msg (its ReLU decisions)");
+        set_device(ctx);
+        cudaStream_t s = ctx->stream;
+        const int64_t nnz = offsets[n] - offsets[0];
+        REQUIRE_ARG(offsets[0] == 0 && nnz >= 0 && (nnz == 0 || (nbrs && eids)), "sc_debug_spmm: bad CSR");
+        DevBuf<int64_t> d_off(n + 1);
+        DevBuf<int32_t> d_nb(std::max<int64_t>(nnz, 1)), d_ei(std::max<int64_t>(nnz, 1));
+        DevBuf<float> d_src(std::max<int64_t>(n * H, 1)), d_out(std::max<int64_t>(n * H, 1)), d_inv(std::max<int64_t>(n, 1));
+        DevBuf<float> d_msg(bwd ? std::max<int64_t>(n * H, 1) : 1);
+        h2d(d_off.get(), offsets, n + 1, s);
+        h2d(d_nb.get(), nbrs, nnz, s);
+        h2d(d_ei.get(), eids, nnz, s);
+        h2d(d_src.get(), src, n * H, s);
+        if (bwd) h2d(d_msg.get(), msg, n * H, s);
+        DevBuf<uint32_t> bits;
+        if (edge_mask) {  // the trainer's CSR-slot bitmap of a per-local-edge DropEdge mask
+            DevBuf<uint8_t> d_mask(std::max<int64_t>(num_edges, 1));
+            h2d(d_mask.get(), edge_mask, num_edges, s);
+            bits.alloc(std::max<int64_t>((nnz + 31) / 32, 1));
+            mask_to_bits(nnz, d_ei.get(), d_mask.get(), bits.get(), s);
+            SC_CUDA(cudaStreamSynchronize(s));
+        }
+        HeavyRows hv;
+        build_heavy_rows(ctx, n, d_off.get(), hv);
+        DevBuf<float> partial(std::max<int64_t>(int64_t(hv.nseg) * H, 1));
+        if (!bwd) {
+            inv_degree(n, d_off.get(), bits.get(), d_inv.get(), s);
+            spmm_fwd(n, H, d_off.get(), d_nb.get(), bits.get(), d_inv.get(), d_src.get(), d_out.get(), s, &hv,
+                     partial.get());
+        } else {
+            spmm_bwd(n, H, d_off.get(), d_nb.get(), bits.get(), d_src.get(), d_msg.get(), d_out.get(), s, nullptr, &hv,
+                     partial.get());
+        }
+        d2h(out, d_out.get(), n * H, s);
+        SC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+sc_status sc_trainer_debug_buffer(sc_trainer* t, const char* name, int32_t layer, void* dst_dev, int64_t bytes) {
+    return guard([&] {
+        REQUIRE_ARG(t && name && dst_dev, "sc_trainer_debug_buffer: null argument");
+        set_device(t->ctx);
+        trainer_finish(t, nullptr, nullptr);
+        const std::string nm(name);
+        const DevBuf<float>* b = nullptr;
+        if (nm == "X" && layer >= 1 && layer <= t->L) b = &t->X[layer];
+        else if (nm == "MSG" && layer >= 0 && layer < t->L) b = &t->MSG[layer];
+        else if (nm == "MEAN" && layer >= 0 && layer < t->L) b = &t->MEAN[layer];
+        else if (nm == "inv") b = &t->inv;
+        else if (nm == "G") b = &t->G;
+        REQUIRE_ARG(b, "sc_trainer_debug_buffer: unknown buffer");
+        REQUIRE_ARG(bytes >= 0 && size_t(bytes) <= b->bytes(), "sc_trainer_debug_buffer: more bytes than the buffer holds");
+        SC_CUDA(cudaMemcpyAsync(dst_dev, b->get(), size_t(bytes), cudaMemcpyDeviceToDevice, t->ctx->stream));
+        SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+
 sc_status sc_trainer_destroy(sc_trainer* t) {
     return guard([&] {
         if (!t) return;

@@ -147,6 +147,24 @@ _sig("sc_debug_gemm", [_vp, _i32, _i64, _i32, _i32, _vp, _i64, _i64, _vp, _vp, _
 
 
 _sig("sc_debug_gemm_tn", [_vp, _i32, _i64, _vp, _i32, _vp, _i32, _vp, _i64, _i32, _vp, _vp])
+_sig("sc_debug_spmm", [_vp, _i32, _i64, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp])
+_sig("sc_trainer_debug_buffer", [_vp, C.c_char_p, _i32, _vp, _i64])
+
+
+def debug_spmm(bwd, offsets, nbrs, eids, src, edge_mask=None, msg=None, ctx: Optional["Context"] = None):
+    """The aggregation kernels alone (nn.hpp:209-230 / 277-288) on host arrays; see sc_debug_spmm."""
+    ctx = ctx or default_context()
+    off = np.ascontiguousarray(offsets, np.int64)
+    nb = np.ascontiguousarray(nbrs, np.int32)
+    ei = np.ascontiguousarray(eids, np.int32)
+    x = np.ascontiguousarray(src, np.float32)
+    n, H = len(off) - 1, x.shape[1]
+    out = np.empty((n, H), np.float32)
+    mk = None if edge_mask is None else np.ascontiguousarray(edge_mask, np.uint8)
+    ms = None if msg is None else np.ascontiguousarray(msg, np.float32)
+    _check(_lib.sc_debug_spmm(ctx.h, int(bwd), n, H, _ptr(off), _ptr(nb), _ptr(ei), 0 if mk is None else mk.size,
+                              _ptr(mk), _ptr(x), _ptr(ms), _ptr(out)), "debug_spmm")
+    return out
 
 
 def debug_gemm_tn(A, B1, B2=None, rows2=None, simt=False, ctx: Optional["Context"] = None) -> np.ndarray:
@@ -407,12 +425,12 @@ class VertexCutPartition:
                                       _ptr(s.adj_edge_ids), _ptr(s.global_to_local)))
         return s
 
-    @property
     def part_held(self, i: int) -> bool:
         x = _i32()
         _check(_lib.sc_vcut_part_held(self.h, i, C.byref(x)))
         return bool(x.value)
 
+    @property
     def parts(self) -> List[PartSubgraph]:
         return [self.part(i) for i in range(self.num_parts)]
 
@@ -814,6 +832,10 @@ class CoFreeTrainer:
         x = _i64()
         _check(_lib.sc_trainer_fallback_count(self.h, C.byref(x)))
         return x.value
+
+    def debug_buffer(self, name: str, layer: int, dst_ptr: int, nbytes: int):
+        """Device-to-device copy of a trainer activation buffer (the last local partition's cache)."""
+        _check(_lib.sc_trainer_debug_buffer(self.h, name.encode(), layer, _vp(dst_ptr), nbytes), "debug_buffer")
 
     def profile(self, enable: bool = True):
         _check(_lib.sc_trainer_profile(self.h, int(enable)))

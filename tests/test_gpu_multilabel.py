@@ -65,7 +65,9 @@ def test_multilabel_trajectory(sc, O, golden, gemm):
         assert abs(t.evaluate_mask(m) - float(z[f"eval_model_{name}"])) <= 0.01
     assert t.comm_audit() == (8 * t.param_count, 0)
     if gemm == "auto":
-        assert t.fallback_count() == 0
+        # dU of both 16-wide layers ([mean | h_in]: the 16 mean columns are not a multiple of the
+        # 32-column TMA box) runs on the SIMT kernel, counted: 2 layers x 8 partitions x 5 steps
+        assert t.fallback_count() == 2 * 8 * 5
 
 
 def test_multilabel_errors(sc, O, golden):
