@@ -115,6 +115,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -811,6 +822,23 @@ static_assert(TnCfg<true>::kSmem <= 232448 && TnCfg<false>::kSmem <= 232448, "TN
 static_assert(TnCfg<true, true>::kSmem <= 232448 && 256 + 32 * TnCfg<true, true>::kStages <= 512, "TN (A in TMEM)");
 
 
+// Accumulation runs of half h (A' in TMEM, split accumulator): runs end at the k-blocks where
+// (kb + off_h) % kRun == 0, off_1 = kRun / 2 (staggered), and at kblocks. Returns the (exclusive)
+// end of the run that starts at `start`.
+constexpr int kRun = 2 * kChunkKb;
+__device__ __forceinline__ int tn_run_end(int h, int start, int kblocks, int nh) {
+    const int off = (nh > 1 && h == 1) ? kRun / 2 : 0;
+    const int end = start + (kRun - (start + off) % kRun);
+    return end < kblocks ? end : kblocks;
+}
+// Length of the run of half h that ends at `end` (its first k-block is end - length).
+__device__ __forceinline__ int tn_run_len(int h, int end, int nh) {
+    const int off = (nh > 1 && h == 1) ? kRun / 2 : 0;
+    const int r = (end + off) % kRun;
+    const int len = r == 0 ? kRun : r;  // runs end on a boundary, or at kblocks (partial)
+    return len < end ? len : end;
+}
+
 template <bool PAIR, bool AT = false>
 __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel(const __grid_constant__ TnParams p) {
     static_assert(!AT || PAIR, "A in TMEM needs the CTA-pair layout");
@@ -849,6 +877,8 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
     const int64_t r1 = min(p.M, r0 + p.rows_per_split);
     const int kblocks = r1 > r0 ? static_cast<int>((r1 - r0 + kTnBK - 1) / kTnBK) : 0;
     const int nchunks = (kblocks + Cfg::kChunk - 1) / Cfg::kChunk;
+    // A' in TMEM: a full 256-column tile splits its accumulator into two staggered halves
+    const int nh = (AT && nb_pad == 2 * kBM) ? 2 : 1;
 
     constexpr int kBOff = AT ? 0 : 2 * kTnATile;  // B' hi / lo tiles within a stage
     const int ka = scale_exp(*p.amax_a);
@@ -865,7 +895,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
                 mbar_init(&sfull[s], 1);
                 mbar_init(&sempty[s], Cfg::kCW);
             }
-            for (int s = 0; s < Cfg::kAcc; ++s) {
+            for (int s = 0; s < 2; ++s) {  // kAcc accumulators, or (A' in TMEM) the two halves of one
                 mbar_init(&tfull[s], 1);
                 mbar_init(&tempty[s], 4 * (PAIR ? 2 : 1));
             }
@@ -1015,6 +1045,64 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
                 mbar_arrive(&sempty[sr.idx]);
             }
         }
+    } else if (warp == Cfg::kMma && AT) {
+        // ================= MMA issuer, A' in TMEM: split accumulator (the pair's leader only) =================
+        // A full 256-column tile runs as two N = 128 halves with their own accumulation runs, staggered by
+        // half a run: half 0 drains after k-blocks 64, 128, ..., half 1 after 32, 96, ... While one half is
+        // drained, the issuer keeps the tensor pipe busy with the other half's MMAs on the stages already
+        // converted (up to kStages - 1 k-blocks ahead), so the single 256-column accumulator no longer
+        // stalls the pipe for a whole drain. Every element still accumulates <= kChunk k-blocks per run.
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = idesc_f16_at(Cfg::kACols, nb_pad / nh);
+            int kbh[2] = {0, nh > 1 ? 0 : kblocks};
+            int endh[2] = {tn_run_end(0, 0, kblocks, nh), nh > 1 ? tn_run_end(1, 0, kblocks, nh) : kblocks};
+            uint32_t runh[2] = {0, 0};
+            bool fresh[2] = {true, true};  // at the start of a run: the half's accumulator must be drained
+            while (kbh[0] < kblocks || kbh[1] < kblocks) {
+                int h = (kbh[1] < kbh[0]) ? 1 : 0;  // the lagging half first
+                bool go = false;
+                for (int tries = 0; tries < 2 && !go; ++tries, h ^= 1) {
+                    const int kb = kbh[h];
+                    if (kb >= kblocks) continue;
+                    if (kbh[h ^ 1] < kblocks && kb > kbh[h ^ 1] + Cfg::kStages - 1) continue;  // ring depth
+                    if (fresh[h]) {
+                        if (!mbar_test(&tempty[h], (runh[h] & 1) ^ 1)) continue;
+                        tc_fence_after();
+                        fresh[h] = false;
+                    }
+                    go = true;
+                    break;
+                }
+                if (!go) continue;  // both halves wait for a drain: poll again
+                const int kb = kbh[h];
+                const int st = kb % Cfg::kStages;
+                TN_TIMED_WAIT(w_a, mbar_wait(&full[st], (kb / Cfg::kStages) & 1));
+                tc_fence_after();
+                const uint8_t* stp = smem + st * Cfg::kStage;
+                const uint32_t bhi = smem_u32(stp) + h * kTnLbo, blo = smem_u32(stp + Cfg::kBTile) + h * kTnLbo;
+                const uint32_t d_tmem = tmem_base + h * 128;
+                const bool first_kb = kb == endh[h] - tn_run_len(h, endh[h], nh);
+#pragma unroll
+                for (int k = 0; k < kTnBK / 16; ++k) {
+                    const uint32_t adv = k * 2 * kTnSbo;  // 16 rows = 2 K groups
+                    const uint64_t dbh = desc_mn_sw128(bhi + adv, kTnLbo, kTnSbo);
+                    const uint64_t dbl = desc_mn_sw128(blo + adv, kTnLbo, kTnSbo);
+                    const uint32_t tah = tmem_base + 256 + st * 32 + k * 8;  // lo plane 16 columns after hi
+                    mma_f16_ts_pair(d_tmem, tah, dbh, idesc, (first_kb && k == 0) ? 0u : 1u);
+                    mma_f16_ts_pair(d_tmem, tah, dbl, idesc, 1u);
+                    mma_f16_ts_pair(d_tmem, tah + 16, dbh, idesc, 1u);
+                }
+                if (kb == endh[h] - 1) {  // end of this half's run: hand it to the epilogue
+                    mma_commit_g<PAIR>(&tfull[h]);
+                    ++runh[h];
+                    fresh[h] = true;
+                    endh[h] = tn_run_end(h, endh[h], kblocks, nh);
+                }
+                if (kbh[h ^ 1] > kb) mma_commit_g<PAIR>(&empty[st]);  // both halves issued: stage free
+                kbh[h] = kb + 1;
+            }
+        }
+        __syncwarp();
     } else if (warp == Cfg::kMma) {
         // ================= MMA issuer (the pair's leader only) =================
         if (!PAIR || rank == 0) {
@@ -1059,6 +1147,71 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
                 }
             }
         }
+    } else if (AT) {
+        // ================= epilogue (A' in TMEM): drain each half's run into the fp32 partial ws[split] =========
+        // Runs complete in order of their last k-block (half 0 first on ties); each drain covers the half's
+        // TMEM columns (128 with two halves, else nb_pad), mapped back to the tile's B' columns: half h's
+        // 32-column block j0 of the MMA's N = 128 came from CTA 0's local columns 64h + j0 (j0 < 64) or
+        // CTA 1's 64h + j0 - 64 (tile columns 128 + ...). The first run of a half stores, later runs add
+        // (fire-and-forget reductions at L2; one owner per element, program order: deterministic).
+        const int ew = warp & 3;
+        const int32_t m0w = n10 + ew * 32;  // first output row (N1 index) of this warp
+        const int rows_here = max(0, min(32, p.N1 - m0w));
+        const float unscale = ldexpf(1.f, -(ka + kbx));
+        float* outw = p.ws + (int64_t(split) * p.N1 + m0w) * p.N2 + n20;
+        float* orow = outw + int64_t(lane) * p.N2;
+        const bool vec = (p.N2 & 3) == 0;
+        const uint64_t pol_ws = l2_evict_last();
+        float* tbuf = reinterpret_cast<float*>(smem + Cfg::kEpiOff) + ew * 32 * Cfg::kEpiPitch;
+        const int hw = nb_pad / nh;  // TMEM columns per half
+        int endh[2] = {tn_run_end(0, 0, kblocks, nh), nh > 1 ? tn_run_end(1, 0, kblocks, nh) : kblocks + 1};
+        uint32_t runh[2] = {0, 0};
+        while (endh[0] <= kblocks || (nh > 1 && endh[1] <= kblocks)) {
+            if (kblocks == 0) break;
+            const int h = (nh > 1 && endh[1] < endh[0]) ? 1 : 0;
+            TN_TIMED_WAIT(w_a, mbar_wait(&tfull[h], runh[h] & 1));
+            tc_fence_after();
+            for (int j0 = 0; j0 < hw; j0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + h * 128 + j0, r);
+                const int c0 = nh > 1 ? (j0 < 64 ? 64 * h + j0 : 128 + 64 * h + (j0 - 64)) : j0;  // tile column
+                if (c0 >= nb) continue;  // warp-uniform
+                if (vec && c0 + 32 <= nb) {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) tbuf[lane * Cfg::kEpiPitch + q] = __uint_as_float(r[q]) * unscale;
+                    __syncwarp();
+#pragma unroll
+                    for (int rr = 0; rr < 8; ++rr) {
+                        const int row = 4 * rr + (lane >> 3), c = (lane & 7) * 4;
+                        const float* t = tbuf + row * Cfg::kEpiPitch + c;
+                        float* o = outw + int64_t(row) * p.N2 + c0 + c;
+                        if (row < rows_here) {
+                            if (runh[h] == 0) st_v4_l2hint(o, t[0], t[1], t[2], t[3], pol_ws);
+                            else red_add_v4_l2hint(o, t[0], t[1], t[2], t[3], pol_ws);
+                        }
+                    }
+                    __syncwarp();
+                } else if (lane < rows_here) {
+                    float* o = orow + c0;
+                    const int nv = min(32, nb - c0);
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        if (q >= nv) break;
+                        const float x = __uint_as_float(r[q]) * unscale;
+                        if (runh[h] == 0) st_l2hint(o + q, x, pol_ws);
+                        else red_add_l2hint(o + q, x, pol_ws);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_l + h * 8);
+            ++runh[h];
+            endh[h] = endh[h] < kblocks ? tn_run_end(h, endh[h], kblocks, nh) : kblocks + 1;
+        }
+        if (kblocks == 0)
+            for (int rr = 0; rr < rows_here; ++rr)
+                for (int c = lane; c < nb; c += 32) outw[int64_t(rr) * p.N2 + c] = 0.f;
     } else {
         // ================= epilogue: drain each chunk into the fp32 partial ws[split] =================
         // Lane = output row (TMEM lane). The first chunk stores, later chunks add with fire-and-forget

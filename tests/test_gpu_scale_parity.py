@@ -74,19 +74,19 @@ def record(key, value):
 def check_spmm(sc, O, a, mask, H=256, heavy_slots=4096, seed=0):
     rng = np.random.default_rng(seed)
     n = len(a.nodes)
-    deg = np.diff(a.offsets)
+    deg = np.diff(a.adj_offsets)
     light = deg <= heavy_slots
-    res = {"rows": int(n), "csr_slots": int(a.offsets[-1]), "heavy_rows": int((~light).sum())}
+    res = {"rows": int(n), "csr_slots": int(a.adj_offsets[-1]), "heavy_rows": int((~light).sum())}
     src = rng.standard_normal((n, H), dtype=np.float32)
-    got = sc.debug_spmm(0, a.offsets, a.nbrs, a.eids, src, edge_mask=mask)
-    ref = O.spmm(0, a.offsets, a.nbrs, a.eids, mask, src, threads=os.cpu_count() or 8)
+    got = sc.debug_spmm(0, a.adj_offsets, a.adj_neighbors, a.adj_edge_ids, src, edge_mask=mask)
+    ref = O.spmm(0, a.adj_offsets, a.adj_neighbors, a.adj_edge_ids, mask, src, threads=os.cpu_count() or 8)
     res["fwd_light_mismatches"] = int((got[light] != ref[light]).sum())
     if (~light).any():
         d = np.abs(got[~light] - ref[~light]).max(axis=1) / np.maximum(np.abs(ref[~light]).max(axis=1), 1e-30)
         res["fwd_heavy_max_rel"] = float(d.max())
     msg = np.maximum(rng.standard_normal((n, H), dtype=np.float32), 0)
-    got = sc.debug_spmm(1, a.offsets, a.nbrs, a.eids, src, edge_mask=mask, msg=msg)
-    ref = O.spmm(1, a.offsets, a.nbrs, a.eids, mask, src, msg=msg, threads=os.cpu_count() or 8)
+    got = sc.debug_spmm(1, a.adj_offsets, a.adj_neighbors, a.adj_edge_ids, src, edge_mask=mask, msg=msg)
+    ref = O.spmm(1, a.adj_offsets, a.adj_neighbors, a.adj_edge_ids, mask, src, msg=msg, threads=os.cpu_count() or 8)
     res["bwd_light_mismatches"] = int((got[light] != ref[light]).sum())
     if (~light).any():
         d = np.abs(got[~light] - ref[~light]).max(axis=1) / np.maximum(np.abs(ref[~light]).max(axis=1), 1e-30)
@@ -168,15 +168,15 @@ def test_teacher_forced_step_per_matrix(sc, name):
     if cfg["dropedge"]:
         k = runs["auto"][0]["mask"]
         mask = sc.precompute_masks(len(a.edges), cfg["k"], cfg["ratio"], sc.substream(1, "dropedge", i)).masks[k]
-    common = dict(theta=theta, d=cfg["feats"], hidden=hidden, C=cfg["classes"], offsets=a.offsets, nbrs=a.nbrs,
-                  eids=a.eids, mask=mask, x0=P["feats"][a.nodes], w=w, normalizer=normalizer,
+    common = dict(theta=theta, d=cfg["feats"], hidden=hidden, C=cfg["classes"], offsets=a.adj_offsets, nbrs=a.adj_neighbors,
+                  eids=a.adj_edge_ids, mask=mask, x0=P["feats"][a.nodes], w=w, normalizer=normalizer,
                   labels=P["labels"][a.nodes], device="cuda")
     truth = partition_step(**common, keep_pre=True)
     pre_pos = [p > 0 for p in truth.pop("pre")]
     logits_true = truth["logits"].cpu().numpy()
     del truth["logits"]
     torch.cuda.empty_cache()
-    report = {"rows": len(a.nodes), "csr_slots": int(a.offsets[-1]), "matrices": {}}
+    report = {"rows": len(a.nodes), "csr_slots": int(a.adj_offsets[-1]), "matrices": {}}
     slices = matrix_slices(cfg["feats"], hidden, cfg["classes"])
     for gemm, (r, gates) in runs.items():
         flips = [int((gt != pp).sum()) for gt, pp in zip(gates, pre_pos)]

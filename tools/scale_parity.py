@@ -86,7 +86,7 @@ def main():
             if cfg["dropedge"]:
                 mask = masksets[i][sc.select_mask(1, i, e, cfg["k"])]
             w = w_all[i] * (tr[a.nodes] != 0)
-            r = partition_step(theta, cfg["feats"], hidden, cfg["classes"], a.offsets, a.nbrs, a.eids, mask,
+            r = partition_step(theta, cfg["feats"], hidden, cfg["classes"], a.adj_offsets, a.adj_neighbors, a.adj_edge_ids, mask,
                                feats[a.nodes], w, normalizer, labels=labels[a.nodes], device="cuda")
             gathered = r["grads"] if gathered is None else gathered + r["grads"]
             total += r["loss"]
