@@ -297,6 +297,13 @@ sc_status sc_debug_gemm(sc_ctx* ctx, int32_t mode, int64_t M, int32_t N, int32_t
 sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A, int32_t N1, const float* B1,
                            int32_t N2a, const float* B2, int64_t b2_rows, int32_t N2b, const int32_t* rows2, float* C);
 
+/* The dual weight-gradient launch alone (one layer's dU and dW, nn.hpp:271-272 +
+ * :289): C1 = A1^T [B1 | B2] (N1a x (N2a + N2b)) and C2 = A2^T B2 (N1b x N2b)
+ * over M rows in ONE tcgen05 fp16x3 split-K launch. Host buffers, row-major
+ * M x N matrices; SC_EINVAL if the shapes do not fit the dual launch
+ * (N1a and N2a multiples of 256). */
+sc_status sc_debug_gemm_tn_dual(sc_ctx* ctx, int64_t M, const float* A1, int32_t N1a, const float* A2, int32_t N1b,
+                               const float* B1, int32_t N2a, const float* B2, int32_t N2b, float* C1, float* C2);
 /* The masked mean aggregation alone (nn.hpp:209-230; bwd = 0) or its
  * transpose with the ReLU gate (nn.hpp:277-288, pull form; bwd = 1), through the
  * trainer's kernels (spmm_fwd / spmm_bwd incl. the segmented hub-row path), on a

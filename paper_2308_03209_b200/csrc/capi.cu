@@ -1026,6 +1026,36 @@ sc_status sc_debug_gemm_tn(sc_ctx* ctx, int32_t mode, int64_t M, const float* A,
     });
 }
 
+sc_status sc_debug_gemm_tn_dual(sc_ctx* ctx, int64_t M, const float* A1, int32_t N1a, const float* A2, int32_t N1b,
+                               const float* B1, int32_t N2a, const float* B2, int32_t N2b, float* C1, float* C2) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && A1 && A2 && B1 && B2 && C1 && C2 && M >= 0, "sc_debug_gemm_tn_dual: bad arguments");
+        set_device(ctx);
+        cudaStream_t s = ctx->stream;
+        auto up = [&](const float* h, int64_t rows, int32_t cols) {
+            DevBuf<float> d(std::max<int64_t>(rows * cols, 1));
+            h2d(d.get(), h, rows * cols, s);
+            return d;
+        };
+        auto dA1 = up(A1, M, N1a), dA2 = up(A2, M, N1b), dB1 = up(B1, M, N2a), dB2 = up(B2, M, N2b);
+        const MatT a1{dA1.get(), N1a, nullptr, N1a}, a2{dA2.get(), N1b, nullptr, N1b};
+        const MatT b1{dB1.get(), N2a, nullptr, N2a}, b2{dB2.get(), N2b, nullptr, N2b};
+        REQUIRE_ARG(tn_dual_supported(a1, a2, b1, b2), "sc_debug_gemm_tn_dual: shapes not supported by the dual launch");
+        DevBuf<float> am(4), dC1(int64_t(N1a) * (N2a + N2b)), dC2(int64_t(N1b) * N2b);
+        SC_CUDA(cudaMemsetAsync(am.get(), 0, 4 * sizeof(float), s));
+        absmax(M * N1a, a1.ptr, am.get(), s);
+        absmax(M * N1b, a2.ptr, am.get() + 1, s);
+        absmax(M * N2a, b1.ptr, am.get() + 2, s);
+        absmax(M * N2b, b2.ptr, am.get() + 3, s);
+        const int64_t wsf = gemm_tn_workspace_floats(N1a + N1b, N2a + N2b);
+        DevBuf<float> ws(wsf);
+        gemm_tn_f16x3_dual(a1, am.get(), a2, am.get() + 1, b1, am.get() + 2, b2, am.get() + 3, M, dC1.get(), N2a + N2b,
+                           dC2.get(), N2b, ws.get(), wsf, s);
+        d2h(C1, dC1.get(), int64_t(N1a) * (N2a + N2b), s);
+        d2h(C2, dC2.get(), int64_t(N1b) * N2b, s);
+        SC_CUDA(cudaStreamSynchronize(s));
+    });
+}
 sc_status sc_debug_spmm(sc_ctx* ctx, int32_t bwd, int64_t n, int32_t H, const int64_t* offsets,
                         const int32_t* nbrs, const int32_t* eids, int64_t num_edges, const uint8_t* edge_mask,
                         const float* src, const float* msg, float* out) {

@@ -757,6 +757,14 @@ struct alignas(64) TnParams {
     int64_t M;
     int64_t rows_per_split;
     int32_t tiles1, tiles2;
+    // Second A source (dual weight-gradient launch, A = [A1 | A2]: dU and dW of one layer share
+    // their B columns and stream every operand once): A' columns >= n1a come from tm_a2.
+    CUtensorMap tm_a2;
+    const float* amax_a2;
+    int32_t n1a;
+    // The (A' tile, B' tile) pairs computed per split (a dual launch skips A2 x B1).
+    int32_t ntiles;
+    int8_t tile_a[8], tile_b[8];
     float* ws;       // [splits][N1][N2] fp32 partials
     unsigned long long* trace;  // optional (SC_TN_TRACE=1): per-role wait / total cycles, summed over CTAs
 };
@@ -862,10 +870,12 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
     const long long t_start = p.trace ? clock64() : 0;
 #endif
     const int unit = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-    const int tiles = p.tiles1 * p.tiles2;
-    const int split = unit / tiles, tile = unit % tiles;
-    const int32_t n10 = (tile / p.tiles2) * Cfg::kACols + static_cast<int32_t>(rank) * kBM;  // this CTA's A' cols
-    const int32_t n20 = (tile % p.tiles2) * kMaxN;                                           // tile's B' cols
+    const int split = unit / p.ntiles, tile = unit % p.ntiles;
+    const int32_t n10 = p.tile_a[tile] * Cfg::kACols + static_cast<int32_t>(rank) * kBM;  // this CTA's A' cols
+    const int32_t n20 = p.tile_b[tile] * kMaxN;                                           // tile's B' cols
+    const bool a_second = n10 >= p.n1a;  // this CTA's A' columns come from A2 (dual launch)
+    const CUtensorMap* tm_a = a_second ? &p.tm_a2 : &p.tm_a;
+    const int32_t a_col0 = a_second ? n10 - p.n1a : n10;  // first A' column within its source
     const int32_t na = max(0, min(kBM, p.N1 - n10));  // valid A' columns of this CTA
     const int32_t nb = min(kMaxN, p.N2 - n20);        // valid B' columns of the tile
     // MMA N; a pair splits it into two 32-column-aligned halves (TMA boxes never straddle B1 | B2)
@@ -881,7 +891,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
     const int nh = (AT && nb_pad == 2 * kBM) ? 2 : 1;
 
     constexpr int kBOff = AT ? 0 : 2 * kTnATile;  // B' hi / lo tiles within a stage
-    const int ka = scale_exp(*p.amax_a);
+    const int ka = scale_exp(*(a_second ? p.amax_a2 : p.amax_a));
     int kbx = scale_exp(*p.b[0].amax);
     if (p.nb > 1) kbx = min(kbx, scale_exp(*p.b[1].amax));
 
@@ -926,7 +936,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
             uint8_t* sb = sa + kTnStgA;
             if (lane == 0) mbar_arrive_expect_tx(&sfull[ring.idx], bytes);
             __syncwarp();
-            if (lane < a_boxes) tma_load_2d(sa + lane * kTnBox, &p.tm_a, n10 + 32 * lane, k0, &sfull[ring.idx]);
+            if (lane < a_boxes) tma_load_2d(sa + lane * kTnBox, tm_a, a_col0 + 32 * lane, k0, &sfull[ring.idx]);
             if (lane < b_boxes) {  // B' columns are read by this CTA only: stream them through L2
                 const int32_t c = nb0 + 32 * lane;
                 if (c < p.n2a) tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[ring.idx], pol_b);
@@ -1296,6 +1306,21 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
     }
 }
 
+// Dual launch: rows [0, n1a) of the split sum -> C1 (all N2 columns), rows [n1a, N1) -> C2
+// (columns [n2a, N2) only: the A2 x B1 block is never computed).
+__global__ void tn_reduce_dual_kernel(int32_t S, int32_t N1, int32_t N2, int32_t n1a, int32_t n2a, const float* ws,
+                                      float* C1, int64_t ldc1, float* C2, int64_t ldc2) {
+    const int64_t total = int64_t(N1) * N2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / N2, c = i % N2;
+        if (r >= n1a && c < n2a) continue;
+        float acc = 0.f;
+        for (int32_t s = 0; s < S; ++s) acc += ws[int64_t(s) * total + i];
+        if (r < n1a) C1[r * ldc1 + c] = acc;
+        else C2[(r - n1a) * ldc2 + (c - n2a)] = acc;
+    }
+}
+
 __global__ void tn_reduce_kernel(int32_t S, int32_t N1, int32_t N2, const float* ws, float* C, int64_t ldc) {
     const int64_t total = int64_t(N1) * N2;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
@@ -1375,37 +1400,9 @@ int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M) {
     return static_cast<int32_t>(std::max<int64_t>(s, 1));
 }
 
-void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
-                   const float* amax_b2, int64_t M, float* C, int64_t ldc, float* ws, int64_t ws_floats,
-                   cudaStream_t s) {
-    const int32_t N1 = a.cols, N2 = b1.cols + (b2 ? b2->cols : 0);
-    if (N1 <= 0 || N2 <= 0) return;
-    if (M <= 0) {
-        for (int32_t r = 0; r < N1; ++r) SC_CUDA(cudaMemsetAsync(C + int64_t(r) * ldc, 0, sizeof(float) * N2, s));
-        return;
-    }
-    const bool pair = tn_use_pair(N1);
-    tc::TnParams p{};
-    p.a = a.ptr;
-    p.lda = a.ld;
-    p.N1 = N1;
-    p.amax_a = amax_a;
-    p.b[0] = tc::TnB{b1.ptr, b1.ld, b1.rows, b1.cols, amax_b1};
-    encode_2d(&p.tm_a, a.ptr, M, N1, a.ld, 32, tc::kTnBK);
-    encode_2d(&p.tm_b1, b1.ptr, M, b1.cols, b1.ld, 32, tc::kTnBK);
-    if (b2) encode_2d(&p.tm_b2, b2->ptr, M, b2->cols, b2->ld, 32, tc::kTnBK);
-    p.nb = b2 ? 2 : 1;
-    if (b2) p.b[1] = tc::TnB{b2->ptr, b2->ld, b2->rows, b2->cols, amax_b2};
-    p.n2a = b1.cols;
-    p.N2 = N2;
-    p.M = M;
-    const int32_t S = tn_f16x3_splits(N1, N2, M);
-    if (int64_t(S) * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn_f16x3: workspace too small");
-    p.rows_per_split = ((M + S - 1) / S + tc::kTnBK - 1) / tc::kTnBK * tc::kTnBK;
-    const int32_t acols = pair ? 2 * tc::kBM : tc::kBM;
-    p.tiles1 = (N1 + acols - 1) / acols;
-    p.tiles2 = (N2 + tc::kMaxN - 1) / tc::kMaxN;
-    p.ws = ws;
+namespace {
+// Split-K launch of the TN kernel over p's tile list, S splits; ws holds [S][N1][N2] partials.
+void tn_launch(tc::TnParams& p, bool pair, int32_t S, cudaStream_t s) {
     static const bool trace = [] {
         const char* e = std::getenv("SC_TN_TRACE");
         return e && std::atoi(e) != 0;
@@ -1416,7 +1413,7 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
         SC_CUDA(cudaMemsetAsync(trace_buf.get(), 0, 16 * sizeof(unsigned long long), s));
         p.trace = trace_buf.get();
     }
-    const int64_t units = int64_t(S) * p.tiles1 * p.tiles2;
+    const int64_t units = int64_t(S) * p.ntiles;
     auto launch = [&](auto kernel, int smem_bytes, int threads) {
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
         cudaLaunchConfig_t cfg{};
@@ -1451,17 +1448,118 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
         SC_CUDA(cudaMemcpyAsync(h, trace_buf.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
         SC_CUDA(cudaStreamSynchronize(s));
         const char* names[4] = {"conv(empty,sfull)", "epi(tfull,-)", "mma(full,tempty)", "load(sempty,-)"};
-        std::fprintf(stderr, "TN trace M=%lld N1=%d N2=%d:", static_cast<long long>(M), N1, N2);
+        std::fprintf(stderr, "TN trace M=%lld N1=%d N2=%d:", static_cast<long long>(p.M), p.N1, p.N2);
         for (int r = 0; r < 4; ++r) {
             const double c = h[4 * r + 3] ? double(h[4 * r + 3]) : 1.0;
             std::fprintf(stderr, " %s %.0f/%.0f of %.0f;", names[r], h[4 * r] / c, h[4 * r + 1] / c, h[4 * r + 2] / c);
         }
         std::fprintf(stderr, "\n");
     }
+}
+
+// Common TN parameters: A (N1 columns as one source), B1 | B2, M rows, S splits.
+int32_t tn_fill(tc::TnParams& p, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1,
+                const MatT* b2, const float* amax_b2, int32_t N1, int64_t M, bool pair) {
+    const int32_t N2 = b1.cols + (b2 ? b2->cols : 0);
+    p.a = a.ptr;
+    p.lda = a.ld;
+    p.N1 = N1;
+    p.amax_a = amax_a;
+    p.amax_a2 = amax_a;
+    p.n1a = N1;
+    p.b[0] = tc::TnB{b1.ptr, b1.ld, b1.rows, b1.cols, amax_b1};
+    encode_2d(&p.tm_a, a.ptr, M, a.cols, a.ld, 32, tc::kTnBK);
+    p.tm_a2 = p.tm_a;
+    encode_2d(&p.tm_b1, b1.ptr, M, b1.cols, b1.ld, 32, tc::kTnBK);
+    if (b2) encode_2d(&p.tm_b2, b2->ptr, M, b2->cols, b2->ld, 32, tc::kTnBK);
+    p.nb = b2 ? 2 : 1;
+    if (b2) p.b[1] = tc::TnB{b2->ptr, b2->ld, b2->rows, b2->cols, amax_b2};
+    p.n2a = b1.cols;
+    p.N2 = N2;
+    p.M = M;
+    const int32_t acols = pair ? 2 * tc::kBM : tc::kBM;
+    p.tiles1 = (N1 + acols - 1) / acols;
+    p.tiles2 = (N2 + tc::kMaxN - 1) / tc::kMaxN;
+    return N2;
+}
+}  // namespace
+
+void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
+                   const float* amax_b2, int64_t M, float* C, int64_t ldc, float* ws, int64_t ws_floats,
+                   cudaStream_t s) {
+    const int32_t N1 = a.cols, N2 = b1.cols + (b2 ? b2->cols : 0);
+    if (N1 <= 0 || N2 <= 0) return;
+    if (M <= 0) {
+        for (int32_t r = 0; r < N1; ++r) SC_CUDA(cudaMemsetAsync(C + int64_t(r) * ldc, 0, sizeof(float) * N2, s));
+        return;
+    }
+    const bool pair = tn_use_pair(N1);
+    tc::TnParams p{};
+    tn_fill(p, a, amax_a, b1, amax_b1, b2, amax_b2, N1, M, pair);
+    if (p.tiles1 * p.tiles2 > 8) throw std::logic_error("gemm_tn_f16x3: too many tiles");
+    p.ntiles = 0;
+    for (int t1 = 0; t1 < p.tiles1; ++t1)
+        for (int t2 = 0; t2 < p.tiles2; ++t2) {
+            p.tile_a[p.ntiles] = static_cast<int8_t>(t1);
+            p.tile_b[p.ntiles] = static_cast<int8_t>(t2);
+            ++p.ntiles;
+        }
+    const int32_t S = tn_f16x3_splits(N1, N2, M);
+    if (int64_t(S) * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn_f16x3: workspace too small");
+    p.rows_per_split = ((M + S - 1) / S + tc::kTnBK - 1) / tc::kTnBK * tc::kTnBK;
+    p.ws = ws;
+    tn_launch(p, pair, S, s);
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();
     count_launch(2);
 }
+
+bool tn_dual_supported(const MatT& a1, const MatT& a2, const MatT& b1, const MatT& b2) {
+    const int32_t tile = 2 * tc::kBM;
+    return tn_use_pair(a1.cols + a2.cols) && tn_supported(a1, b1, &b2) && tn_supported(a2, b2, nullptr) &&
+           a1.cols % tile == 0 && b1.cols % tc::kMaxN == 0 && (a1.cols + a2.cols + tile - 1) / tile *
+           ((b1.cols + b2.cols + tc::kMaxN - 1) / tc::kMaxN) <= 8;
+}
+
+void gemm_tn_f16x3_dual(const MatT& a1, const float* amax_a1, const MatT& a2, const float* amax_a2, const MatT& b1,
+                        const float* amax_b1, const MatT& b2, const float* amax_b2, int64_t M, float* C1,
+                        int64_t ldc1, float* C2, int64_t ldc2, float* ws, int64_t ws_floats, cudaStream_t s) {
+    if (!tn_dual_supported(a1, a2, b1, b2)) throw std::logic_error("gemm_tn_f16x3_dual: unsupported shapes");
+    const int32_t N1 = a1.cols + a2.cols;
+    if (M <= 0) {
+        for (int32_t r = 0; r < a1.cols; ++r)
+            SC_CUDA(cudaMemsetAsync(C1 + int64_t(r) * ldc1, 0, sizeof(float) * (b1.cols + b2.cols), s));
+        for (int32_t r = 0; r < a2.cols; ++r) SC_CUDA(cudaMemsetAsync(C2 + int64_t(r) * ldc2, 0, sizeof(float) * b2.cols, s));
+        return;
+    }
+    tc::TnParams p{};
+    const int32_t N2 = tn_fill(p, a1, amax_a1, b1, amax_b1, &b2, amax_b2, N1, M, true);
+    encode_2d(&p.tm_a2, a2.ptr, M, a2.cols, a2.ld, 32, tc::kTnBK);
+    p.amax_a2 = amax_a2;
+    p.n1a = a1.cols;
+    p.ntiles = 0;
+    const int32_t tile = 2 * tc::kBM;
+    for (int t1 = 0; t1 < p.tiles1; ++t1)
+        for (int t2 = 0; t2 < p.tiles2; ++t2) {
+            if (t1 * tile >= p.n1a && (t2 + 1) * tc::kMaxN <= p.n2a) continue;  // A2 x B1: not needed
+            p.tile_a[p.ntiles] = static_cast<int8_t>(t1);
+            p.tile_b[p.ntiles] = static_cast<int8_t>(t2);
+            ++p.ntiles;
+        }
+    // splits sized for the tiles actually computed
+    const int32_t slots = std::max(1, num_sms() / 2);
+    int64_t S = std::max<int64_t>(1, slots / p.ntiles);
+    S = std::max<int64_t>(1, std::min<int64_t>(S, (M + 4095) / 4096));
+    if (S * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn_f16x3_dual: workspace too small");
+    p.rows_per_split = ((M + S - 1) / S + tc::kTnBK - 1) / tc::kTnBK * tc::kTnBK;
+    p.ws = ws;
+    tn_launch(p, true, static_cast<int32_t>(S), s);
+    tc::tn_reduce_dual_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(static_cast<int32_t>(S), N1, N2, p.n1a,
+                                                                             p.n2a, ws, C1, ldc1, C2, ldc2);
+    SC_LAUNCH_CHECK();
+    count_launch(2);
+}
+
 bool tc_supported(const MatA& a1, const MatA* a2, int32_t N) {
     // rows are fetched in whole 16 B units by bulk copies: 16 B aligned rows (ld % 4 == 0)
     // operands stream through 2D TMA (no row gathers): 16 B aligned rows
@@ -1639,6 +1737,19 @@ void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b
         if (enabled) ++simt_fallbacks;
         gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
     }
+}
+
+bool TcGemm::tn_dual(sc_trainer* t, const MatT& a1, const float* amax_a1, const MatT& a2, const float* amax_a2,
+                     const MatT& b1, const float* amax_b1, const MatT& b2, const float* amax_b2, int64_t M, float* C1,
+                     int64_t ldc1, float* C2, int64_t ldc2) {
+    static const bool on = [] {
+        const char* e = std::getenv("SC_TN_DUAL");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || !enabled || !tn_dual_supported(a1, a2, b1, b2)) return false;
+    gemm_tn_f16x3_dual(a1, amax_a1, a2, amax_a2, b1, amax_b1, b2, amax_b2, M, C1, ldc1, C2, ldc2, t->ws.get(),
+                       t->ws_floats, t->ctx->stream);
+    return true;
 }
 
 void TcGemm::tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1,

@@ -42,6 +42,15 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
                    const float* amax_b2, int64_t M, float* C, int64_t ldc, float* ws, int64_t ws_floats,
                    cudaStream_t s);
 
+// Dual weight-gradient launch of one layer: C1 = A1^T [B1 | B2] and C2 = A2^T B2 in one split-K
+// TN launch over A = [A1 | A2] (the A2 x B1 block skipped), so B2 (the layer input) and the
+// converted tiles are streamed once for both products (CTA pairs; A1 columns a multiple of 256,
+// B1 columns a multiple of 256).
+bool tn_dual_supported(const MatT& a1, const MatT& a2, const MatT& b1, const MatT& b2);
+void gemm_tn_f16x3_dual(const MatT& a1, const float* amax_a1, const MatT& a2, const float* amax_a2, const MatT& b1,
+                        const float* amax_b1, const MatT& b2, const float* amax_b2, int64_t M, float* C1,
+                        int64_t ldc1, float* C2, int64_t ldc2, float* ws, int64_t ws_floats, cudaStream_t s);
+
 // Uses gemm_f16x3 when the trainer allows it and the shape is supported,
 // otherwise the fp32 SIMT kernel (nn.cu). Weight images are cached per
 // operand and rebuilt when `version` changes (after every Adam step).
@@ -63,6 +72,10 @@ struct TcGemm {
     void nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2, const float* amax2,
             const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
             float* amax_out);
+    // dU and dW of one layer in one launch (false: unsupported here, caller runs tn twice)
+    bool tn_dual(sc_trainer* t, const MatT& a1, const float* amax_a1, const MatT& a2, const float* amax_a2,
+                 const MatT& b1, const float* amax_b1, const MatT& b2, const float* amax_b2, int64_t M, float* C1,
+                 int64_t ldc1, float* C2, int64_t ldc2);
     // s / ws: stream and split-K workspace (default: the context stream, t->ws)
     void tn(sc_trainer* t, const MatT& a, const float* amax_a, const MatT& b1, const float* amax_b1, const MatT* b2,
             const float* amax_b2, int64_t M, float* C, int64_t ldc, cudaStream_t s = nullptr, float* ws = nullptr);

@@ -233,7 +233,7 @@ void trainer_init(sc_trainer* t) {
     if (max_seg) t->heavy_ws.alloc(max_seg * maxH);
     int32_t maxN1 = t->C, maxN2 = t->E;
     for (auto& lo : t->lay) {
-        maxN1 = std::max(maxN1, lo.H);
+        maxN1 = std::max(maxN1, 2 * lo.H);  // the dual dU + dW launch: A = [dh | dz]
         maxN2 = std::max(maxN2, lo.H + lo.in);
     }
     t->ws_floats = gemm_tn_workspace_floats(maxN1, maxN2);
@@ -441,26 +441,38 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr,
                  nullptr, nullptr, t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get(), nullptr);
         P.end(s);
-        // dU = dh^T [mean | h_in] (:271-272) on the side stream: tensor-bound, it
-        // shares the SMs with the HBM-bound transposed aggregation below
-        hand_off(s, w);
-        P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), w, 2.0 * n * lo.H * (lo.H + lo.in));
-        t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, t->slot_ptr(2 * l + 1, i), lo.H + lo.in,
-                 w, ws_w);
-        P.end(w);
-        exchange_bucket(t, 2 * l + 1, round, w);
-        // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
+        // One launch for dU = dh^T [mean | h_in] (:271-272) and dW = dz^T h_in (:289) after the
+        // transposed aggregation, so h_in (and the tiles' conversions) stream once for both;
+        // otherwise dU runs first (optionally on the side stream) and dW after.
         float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
+        const MatT dzt{t->dz.get(), lo.H, nullptr, lo.H};
+        const bool dual = !t->overlap && tn_dual_supported(dht, dzt, meant, xint) && t->tc.enabled;
+        if (!dual) {
+            hand_off(s, w);
+            P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), w, 2.0 * n * lo.H * (lo.H + lo.in));
+            t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, t->slot_ptr(2 * l + 1, i),
+                     lo.H + lo.in, w, ws_w);
+            P.end(w);
+            exchange_bucket(t, 2 * l + 1, round, w);
+        }
+        // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
         SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
         P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
         spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s, dz_amax, R.hv,
                  t->heavy_ws.get());
         P.end(s);
-        // dW = dz^T h_in   (:289)
-        P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s, 2.0 * n * lo.H * lo.in);
-        t->tc.tn(t, MatT{t->dz.get(), lo.H, nullptr, lo.H}, dz_amax, xint, xin_amax, nullptr, nullptr, n,
-                 t->slot_ptr(2 * l, i), lo.in);
-        P.end(s);
+        if (dual) {
+            P.begin("wgrad", 4.0 * n * (3 * lo.H + lo.in), s, 2.0 * n * lo.H * (lo.H + 2 * lo.in));
+            t->tc.tn_dual(t, dht, dh_amax, dzt, dz_amax, meant, t->amax_msg(l), xint, xin_amax, n,
+                          t->slot_ptr(2 * l + 1, i), lo.H + lo.in, t->slot_ptr(2 * l, i), lo.in);
+            P.end(s);
+            exchange_bucket(t, 2 * l + 1, round);
+        } else {
+            // dW = dz^T h_in   (:289)
+            P.begin("wgrad", 4.0 * n * (lo.H + lo.in), s, 2.0 * n * lo.H * lo.in);
+            t->tc.tn(t, dzt, dz_amax, xint, xin_amax, nullptr, nullptr, n, t->slot_ptr(2 * l, i), lo.in);
+            P.end(s);
+        }
         exchange_bucket(t, 2 * l, round);
         if (l > 0) {  // dh = dh U_R + dz W   (:275, :290); layer 0's is unused
             const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz.get(), lo.H, nullptr, lo.H};

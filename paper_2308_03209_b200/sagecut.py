@@ -147,6 +147,21 @@ _sig("sc_debug_gemm", [_vp, _i32, _i64, _i32, _i32, _vp, _i64, _i64, _vp, _vp, _
 
 
 _sig("sc_debug_gemm_tn", [_vp, _i32, _i64, _vp, _i32, _vp, _i32, _vp, _i64, _i32, _vp, _vp])
+_sig("sc_debug_gemm_tn_dual", [_vp, _i64, _vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _vp, _vp])
+
+
+def debug_gemm_tn_dual(A1, A2, B1, B2, ctx: Optional["Context"] = None):
+    """Kernel-level hook of the dual weight-gradient launch: (A1^T [B1 | B2], A2^T B2)."""
+    ctx = ctx or default_context()
+    A1, A2, B1, B2 = (np.ascontiguousarray(x, np.float32) for x in (A1, A2, B1, B2))
+    M = A1.shape[0]
+    C1 = np.zeros((A1.shape[1], B1.shape[1] + B2.shape[1]), np.float32)
+    C2 = np.zeros((A2.shape[1], B2.shape[1]), np.float32)
+    _check(_lib.sc_debug_gemm_tn_dual(ctx.h, M, _ptr(A1), A1.shape[1], _ptr(A2), A2.shape[1], _ptr(B1), B1.shape[1],
+                                      _ptr(B2), B2.shape[1], _ptr(C1), _ptr(C2)), "debug_gemm_tn_dual")
+    return C1, C2
+
+
 _sig("sc_debug_spmm", [_vp, _i32, _i64, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp])
 _sig("sc_trainer_debug_buffer", [_vp, C.c_char_p, _i32, _vp, _i64])
 

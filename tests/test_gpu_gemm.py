@@ -118,6 +118,31 @@ def test_tn_f16x3_matches_fp64(sc, case):
     assert e_tc <= 1e-5
 
 
+DUAL_CASES = [  # M, H, in: one layer's (dU, dW) = (dh^T [mean | h_in], dz^T h_in)
+    (50_000, 256, 256),
+    (30_001, 256, 100),
+    (300_000, 256, 256),
+    (777, 256, 64),
+]
+
+
+@pytest.mark.parametrize("case", DUAL_CASES, ids=[str(c) for c in DUAL_CASES])
+def test_tn_dual_matches_fp64(sc, case):
+    """The dual dU + dW launch (A = [dh | dz], the dz x mean block skipped) against fp64."""
+    M, H, d = case
+    rng = np.random.default_rng(M + d)
+    dh = rng.standard_normal((M, H)).astype(np.float32) * 1e-3
+    dz = rng.standard_normal((M, H)).astype(np.float32) * 3e-5
+    mean = np.maximum(rng.standard_normal((M, H)), 0).astype(np.float32)
+    hin = rng.standard_normal((M, d)).astype(np.float32)
+    dU, dW = sc.debug_gemm_tn_dual(dh, dz, mean, hin)
+    refU = dh.astype(np.float64).T @ np.concatenate([mean, hin], axis=1).astype(np.float64)
+    refW = dz.astype(np.float64).T @ hin.astype(np.float64)
+    eU, eW = rel(dU, refU), rel(dW, refW)
+    print(f"dual {case}: dU {eU:.2e} dW {eW:.2e}")
+    assert eU <= 1e-5 and eW <= 1e-5
+
+
 def test_tn_smem_operand_path_subprocess():
     """The CTA-pair weight-gradient kernel with the A' operand in shared memory (SC_TN_ATMEM=0,
     read once per process) passes the same fp64 checks."""
