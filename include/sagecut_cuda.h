@@ -84,6 +84,35 @@ sc_status sc_graph_copy_edges(sc_graph* g, int32_t* uv);
 sc_status sc_graph_copy_csr(sc_graph* g, int64_t* offsets, int32_t* neighbors, int32_t* edge_ids, int32_t* degrees);
 sc_status sc_graph_destroy(sc_graph* g);
 
+/* ---- dataset files (proj/include/sagecut/graph_io.hpp, proj/src/graph_io.cpp) ---- */
+/* load_graph (graph_io.cpp:41-80): "u v" text lines ('#' comments, blank lines
+ * skipped), then build_graph on the device. num_nodes < 0: 1 + the largest id
+ * (LoadOptions::num_nodes); strict: SC_ERUNTIME if a node id never appears.
+ * Parse errors: SC_ERUNTIME "<path>:<line>: <what>" as the reference. */
+sc_status sc_load_graph(sc_ctx* ctx, const char* path, int32_t num_nodes, int32_t strict, sc_graph** out,
+                        int64_t* dropped_self_loops, int64_t* merged_duplicates);
+/* The edge-list parse of load_graph alone (host only): raw (u, v) pairs in file
+ * order (cap = pairs the buffer holds; uv = NULL to size) and the node count. */
+sc_status sc_read_edge_list(const char* path, int32_t num_nodes, int32_t* uv, int64_t cap, int64_t* m, int32_t* n);
+/* load_features (graph_io.cpp:82-160): CSV or "CFM1" binary (sniffed), as fp32
+ * row-major. Call with out = NULL to get rows / cols, then with a buffer. */
+sc_status sc_load_features(const char* path, int32_t expected_nodes, float* out, int64_t cap, int64_t* rows,
+                           int64_t* cols);
+/* load_labels (graph_io.cpp:188-242): class ids (labels, n) or a multi-label 0/1
+ * matrix (targets, n x num_classes; *is_multilabel = 1). NULL outputs: query only. */
+sc_status sc_load_labels(const char* path, int32_t num_nodes, int32_t* labels, float* targets, int64_t cap,
+                         int32_t* num_classes, int32_t* is_multilabel);
+/* load_masks (graph_io.cpp:256-283): "train|val|test <id>" lines -> n-byte masks. */
+sc_status sc_load_masks(const char* path, int32_t num_nodes, uint8_t* train, uint8_t* val, uint8_t* test);
+/* save_edge_list / save_features_csv|binary / save_labels / save_masks
+ * (graph_io.cpp:75-80, 162-186, 244-254, 285-296), byte-compatible. */
+sc_status sc_save_edge_list(sc_graph* g, const char* path);
+sc_status sc_save_features(const char* path, const float* features, int64_t rows, int64_t cols, int32_t binary);
+sc_status sc_save_labels(const char* path, int32_t num_nodes, const int32_t* labels, const float* targets,
+                         int32_t num_classes);
+sc_status sc_save_masks(const char* path, int32_t num_nodes, const uint8_t* train, const uint8_t* val,
+                        const uint8_t* test);
+
 /* ---- vertex cut (proj/include/sagecut/partition.hpp, proj/src/partition.cpp) */
 /* partition_random (partition.cpp:92-100): edge e takes the e-th next_below(p)
  * draw of Rng(substream(seed,"partition.random")). */

@@ -11,6 +11,7 @@
 
 #include "../../include/sagecut_cuda.h"
 #include "internal.hpp"
+#include "graph_io.hpp"
 #include "io.hpp"
 #include "trainer.hpp"
 
@@ -261,6 +262,112 @@ sc_status sc_graph_destroy(sc_graph* g) {
         if (!g) return;
         set_device(g->ctx);
         delete g;
+    });
+}
+
+// ---- dataset files (graph_io.cpp:41-296) ----
+sc_status sc_load_graph(sc_ctx* ctx, const char* path, int32_t num_nodes, int32_t strict, sc_graph** out,
+                        int64_t* self_loops, int64_t* dups) {
+    return guard([&] {
+        REQUIRE_ARG(ctx && path && out, "sc_load_graph: null argument");
+        const std::string p(path);
+        const EdgeList el = read_edge_list(p, num_nodes);
+        set_device(ctx);
+        const int64_t m = static_cast<int64_t>(el.uv.size() / 2);
+        DevBuf<int32_t> raw(std::max<int64_t>(2 * m, 2));
+        h2d(raw.get(), el.uv.data(), 2 * m, ctx->stream);
+        auto g = build_graph_device(ctx, el.num_nodes, raw.get(), m, self_loops, dups);
+        if (strict && g->n > 0) {  // ValidationReport::isolated_nodes must be empty (graph_io.cpp:73-76)
+            std::vector<int32_t> deg(static_cast<size_t>(g->n));
+            d2h(deg.data(), g->degrees.get(), g->n, ctx->stream);
+            SC_CUDA(cudaStreamSynchronize(ctx->stream));
+            int64_t isolated = 0;
+            for (int32_t d : deg) isolated += d == 0;
+            if (isolated)
+                throw std::runtime_error(p + ": " + std::to_string(isolated) +
+                                         " node id(s) absent from the edge list (strict mode)");
+        }
+        *out = g.release();
+    });
+}
+sc_status sc_read_edge_list(const char* path, int32_t num_nodes, int32_t* uv, int64_t cap, int64_t* m,
+                            int32_t* n) {
+    return guard([&] {
+        REQUIRE_ARG(path && m && n, "sc_read_edge_list: null argument");
+        const EdgeList el = read_edge_list(path, num_nodes);
+        *m = static_cast<int64_t>(el.uv.size() / 2);
+        *n = el.num_nodes;
+        if (!uv) return;
+        REQUIRE_ARG(cap >= *m, "sc_read_edge_list: output buffer too small");
+        std::copy(el.uv.begin(), el.uv.end(), uv);
+    });
+}
+sc_status sc_load_features(const char* path, int32_t expected_nodes, float* out, int64_t cap, int64_t* rows,
+                           int64_t* cols) {
+    return guard([&] {
+        REQUIRE_ARG(path && rows && cols, "sc_load_features: null argument");
+        const HostFeatures f = read_features(path, expected_nodes);
+        *rows = f.rows;
+        *cols = f.cols;
+        if (!out) return;
+        REQUIRE_ARG(cap >= f.rows * f.cols, "sc_load_features: output buffer too small");
+        std::copy(f.values.begin(), f.values.end(), out);
+    });
+}
+sc_status sc_load_labels(const char* path, int32_t num_nodes, int32_t* labels, float* targets, int64_t cap,
+                         int32_t* num_classes, int32_t* is_multilabel) {
+    return guard([&] {
+        REQUIRE_ARG(path && num_classes && is_multilabel, "sc_load_labels: null argument");
+        const HostLabels L = read_labels(path, num_nodes);
+        *num_classes = L.num_classes;
+        *is_multilabel = L.multilabel ? 1 : 0;
+        if (L.multilabel && targets) {
+            REQUIRE_ARG(cap >= int64_t(L.targets.size()), "sc_load_labels: output buffer too small");
+            std::copy(L.targets.begin(), L.targets.end(), targets);
+        }
+        if (!L.multilabel && labels) std::copy(L.labels.begin(), L.labels.end(), labels);
+    });
+}
+sc_status sc_load_masks(const char* path, int32_t num_nodes, uint8_t* train, uint8_t* val, uint8_t* test) {
+    return guard([&] {
+        REQUIRE_ARG(path && train && val && test, "sc_load_masks: null argument");
+        std::vector<uint8_t> tr, va, te;
+        read_masks(path, num_nodes, tr, va, te);
+        std::copy(tr.begin(), tr.end(), train);
+        std::copy(va.begin(), va.end(), val);
+        std::copy(te.begin(), te.end(), test);
+    });
+}
+sc_status sc_save_edge_list(sc_graph* g, const char* path) {
+    return guard([&] {
+        REQUIRE_ARG(g && path, "sc_save_edge_list: null argument");
+        set_device(g->ctx);
+        std::vector<int32_t> u(g->m), v(g->m);
+        d2h(u.data(), g->eu.get(), g->m, g->ctx->stream);
+        d2h(v.data(), g->ev.get(), g->m, g->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(g->ctx->stream));
+        write_edge_list(path, u.data(), v.data(), g->m);
+    });
+}
+sc_status sc_save_features(const char* path, const float* features, int64_t rows, int64_t cols, int32_t binary) {
+    return guard([&] {
+        REQUIRE_ARG(path && (features || rows * cols == 0), "sc_save_features: null argument");
+        if (binary) write_features_binary(path, features, rows, cols);
+        else write_features_csv(path, features, rows, cols);
+    });
+}
+sc_status sc_save_labels(const char* path, int32_t num_nodes, const int32_t* labels, const float* targets,
+                         int32_t num_classes) {
+    return guard([&] {
+        REQUIRE_ARG(path && (labels || targets), "sc_save_labels: null argument");
+        write_labels(path, num_nodes, labels, targets, num_classes);
+    });
+}
+sc_status sc_save_masks(const char* path, int32_t num_nodes, const uint8_t* train, const uint8_t* val,
+                        const uint8_t* test) {
+    return guard([&] {
+        REQUIRE_ARG(path && train && val && test, "sc_save_masks: null argument");
+        write_masks(path, num_nodes, train, val, test);
     });
 }
 

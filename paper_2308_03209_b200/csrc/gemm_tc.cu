@@ -765,6 +765,7 @@ struct alignas(64) TnParams {
     // The (A' tile, B' tile) pairs computed per split (a dual launch skips A2 x B1).
     int32_t ntiles;
     int8_t tile_a[8], tile_b[8];
+    int32_t split_acc;  // A' in TMEM: split full tiles' accumulator into two staggered halves
     float* ws;       // [splits][N1][N2] fp32 partials
     unsigned long long* trace;  // optional (SC_TN_TRACE=1): per-role wait / total cycles, summed over CTAs
 };
@@ -888,7 +889,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
     const int kblocks = r1 > r0 ? static_cast<int>((r1 - r0 + kTnBK - 1) / kTnBK) : 0;
     const int nchunks = (kblocks + Cfg::kChunk - 1) / Cfg::kChunk;
     // A' in TMEM: a full 256-column tile splits its accumulator into two staggered halves
-    const int nh = (AT && nb_pad == 2 * kBM) ? 2 : 1;
+    const int nh = (AT && p.split_acc && nb_pad == 2 * kBM) ? 2 : 1;
 
     constexpr int kBOff = AT ? 0 : 2 * kTnATile;  // B' hi / lo tiles within a stage
     const int ka = scale_exp(*(a_second ? p.amax_a2 : p.amax_a));
@@ -1413,6 +1414,11 @@ void tn_launch(tc::TnParams& p, bool pair, int32_t S, cudaStream_t s) {
         SC_CUDA(cudaMemsetAsync(trace_buf.get(), 0, 16 * sizeof(unsigned long long), s));
         p.trace = trace_buf.get();
     }
+    static const int split_acc = [] {
+        const char* e = std::getenv("SC_TN_SPLIT");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.split_acc = split_acc;
     const int64_t units = int64_t(S) * p.ntiles;
     auto launch = [&](auto kernel, int smem_bytes, int threads) {
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));

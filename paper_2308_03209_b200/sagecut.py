@@ -66,6 +66,15 @@ _sig("sc_build_graph_dev", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTE
 _sig("sc_graph_set_data", [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp])
 _sig("sc_graph_set_features", [_vp, _vp, C.c_int])
 _sig("sc_graph_set_multilabels", [_vp, _vp, _i32])
+_sig("sc_load_graph", [_vp, C.c_char_p, _i32, _i32, _pp, C.POINTER(_i64), C.POINTER(_i64)])
+_sig("sc_read_edge_list", [C.c_char_p, _i32, _vp, _i64, C.POINTER(_i64), C.POINTER(_i32)])
+_sig("sc_load_features", [C.c_char_p, _i32, _vp, _i64, C.POINTER(_i64), C.POINTER(_i64)])
+_sig("sc_load_labels", [C.c_char_p, _i32, _vp, _vp, _i64, C.POINTER(_i32), C.POINTER(_i32)])
+_sig("sc_load_masks", [C.c_char_p, _i32, _vp, _vp, _vp])
+_sig("sc_save_edge_list", [_vp, C.c_char_p])
+_sig("sc_save_features", [C.c_char_p, _vp, _i64, _i64, _i32])
+_sig("sc_save_labels", [C.c_char_p, _i32, _vp, _vp, _i32])
+_sig("sc_save_masks", [C.c_char_p, _i32, _vp, _vp, _vp])
 _sig("sc_graph_set_part_ownership", [_vp, _i32, _i32])
 _sig("sc_vcut_part_held", [_vp, _i32, C.POINTER(_i32)])
 EXCHANGE_FN = C.CFUNCTYPE(_i32, _vp, _i32, _i32, _i32, _vp, _vp, _i64)
@@ -373,6 +382,78 @@ def build_graph(num_nodes: int, raw_edges, ctx: Optional[Context] = None):
     _check(_lib.sc_build_graph(ctx.h, int(num_nodes), _ptr(raw), len(raw), C.byref(h), C.byref(sl), C.byref(du)),
            "build_graph")
     return Graph(h, ctx), ValidationReport(sl.value, du.value)
+
+
+def load_graph(path: str, num_nodes: Optional[int] = None, strict: bool = False, ctx: Optional[Context] = None):
+    """load_graph (graph_io.cpp:41-80) -> (Graph, ValidationReport)."""
+    ctx = ctx or default_context()
+    h, sl, dp = _vp(), _i64(), _i64()
+    _check(_lib.sc_load_graph(ctx.h, os.fsencode(path), -1 if num_nodes is None else num_nodes, int(strict),
+                              C.byref(h), C.byref(sl), C.byref(dp)), "load_graph")
+    return Graph(h, ctx), ValidationReport(sl.value, dp.value)
+
+
+def read_edge_list(path: str, num_nodes: Optional[int] = None):
+    """load_graph's parse alone (host only): (raw pairs [m, 2] in file order, node count)."""
+    m, n = _i64(), _i32()
+    nn = -1 if num_nodes is None else num_nodes
+    _check(_lib.sc_read_edge_list(os.fsencode(path), nn, None, 0, C.byref(m), C.byref(n)), "load_graph")
+    uv = np.zeros((m.value, 2), np.int32)
+    _check(_lib.sc_read_edge_list(os.fsencode(path), nn, _ptr(uv), m.value, C.byref(m), C.byref(n)), "load_graph")
+    return uv, n.value
+
+
+def load_features(path: str, expected_nodes: int) -> np.ndarray:  # graph_io.cpp:82-160
+    r, c = _i64(), _i64()
+    _check(_lib.sc_load_features(os.fsencode(path), expected_nodes, None, 0, C.byref(r), C.byref(c)), "load_features")
+    out = np.zeros((r.value, c.value), np.float32)
+    _check(_lib.sc_load_features(os.fsencode(path), expected_nodes, _ptr(out), out.size, C.byref(r), C.byref(c)),
+           "load_features")
+    return out
+
+
+def load_labels(path: str, num_nodes: int):
+    """load_labels (graph_io.cpp:188-242) -> (class ids or None, 0/1 targets or None, num_classes)."""
+    nc, ml = _i32(), _i32()
+    _check(_lib.sc_load_labels(os.fsencode(path), num_nodes, None, None, 0, C.byref(nc), C.byref(ml)), "load_labels")
+    if ml.value:
+        y = np.zeros((num_nodes, nc.value), np.float32)
+        _check(_lib.sc_load_labels(os.fsencode(path), num_nodes, None, _ptr(y), y.size, C.byref(nc), C.byref(ml)),
+               "load_labels")
+        return None, y, nc.value
+    lab = np.zeros(num_nodes, np.int32)
+    _check(_lib.sc_load_labels(os.fsencode(path), num_nodes, _ptr(lab), None, 0, C.byref(nc), C.byref(ml)),
+           "load_labels")
+    return lab, None, nc.value
+
+
+def load_masks(path: str, num_nodes: int):  # graph_io.cpp:256-283
+    tr, va, te = (np.zeros(num_nodes, np.uint8) for _ in range(3))
+    _check(_lib.sc_load_masks(os.fsencode(path), num_nodes, _ptr(tr), _ptr(va), _ptr(te)), "load_masks")
+    return tr, va, te
+
+
+def save_edge_list(g: "Graph", path: str):  # graph_io.cpp:75-80
+    _check(_lib.sc_save_edge_list(g.h, os.fsencode(path)), "save_edge_list")
+
+
+def save_features(features, path: str, binary: bool = False):  # graph_io.cpp:162-186
+    f = np.ascontiguousarray(features, np.float32)
+    _check(_lib.sc_save_features(os.fsencode(path), _ptr(f), f.shape[0], f.shape[1], int(binary)), "save_features")
+
+
+def save_labels(path: str, labels=None, targets=None):  # graph_io.cpp:244-254
+    if targets is not None:
+        y = np.ascontiguousarray(targets, np.float32)
+        _check(_lib.sc_save_labels(os.fsencode(path), y.shape[0], None, _ptr(y), y.shape[1]), "save_labels")
+    else:
+        lab = np.ascontiguousarray(labels, np.int32)
+        _check(_lib.sc_save_labels(os.fsencode(path), lab.size, _ptr(lab), None, 0), "save_labels")
+
+
+def save_masks(path: str, train, val, test):  # graph_io.cpp:285-296
+    tr, va, te = (np.ascontiguousarray(x, np.uint8) for x in (train, val, test))
+    _check(_lib.sc_save_masks(os.fsencode(path), tr.size, _ptr(tr), _ptr(va), _ptr(te)), "save_masks")
 
 
 def build_graph_device(num_nodes: int, raw_dev_ptr: int, m_raw: int, ctx: Optional[Context] = None):

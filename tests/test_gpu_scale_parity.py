@@ -132,9 +132,14 @@ def fp32_step(sc, P, gemm, i):
     n = P["part"].part_sizes(i)[0]
     gates = []
     for l in range(cfg["layers"]):
+        # the library copies on its own stream: torch's queue must be idle before the caching
+        # allocator hands a (possibly recycled) block to it
+        torch.cuda.synchronize()
         m = torch.empty((n, cfg["hidden"]), dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
         t.debug_buffer("MSG", l, m.data_ptr(), m.numel() * 4)
         gates.append(m > 0)
+        torch.cuda.synchronize()
         del m
     out = dict(theta=theta, grads=t.part_grads(i).astype(np.float64), logits=t.part_logits(i),
                mask=t.part_mask(i), fallbacks=t.fallback_count())
