@@ -399,7 +399,13 @@ def run_gpu_arm(args, cfg):
     barrier()
     ctx.sync()
     launches0 = ctx.launch_count()
-    fallbacks0 = trainer.fallback_count()
+    def fallback_count():
+        try:
+            return trainer.fallback_count()
+        except AttributeError:  # an older library build under SC_LIB (A/B runs)
+            return -1
+
+    fallbacks0 = fallback_count()
     losses = []
     with ClockSampler(local) as clocks:
         ctx.timer_start()
@@ -408,7 +414,7 @@ def run_gpu_arm(args, cfg):
             epoch += 1
         ms = ctx.timer_stop()
     launches = ctx.launch_count() - launches0
-    fallbacks = trainer.fallback_count() - fallbacks0
+    fallbacks = fallback_count() - fallbacks0
     free_b, total_b = torch.cuda.mem_get_info(local)  # device memory in use (graph, partitions, trainer)
     barrier()
     ms_step = max_over_ranks(ms / args.steps)

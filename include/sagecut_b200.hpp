@@ -130,6 +130,97 @@ inline std::pair<Graph, ValidationReport> build_graph(Context& ctx, NodeId num_n
     return {Graph(ctx, h), rep};
 }
 
+// ---- dataset files (graph_io.hpp / graph_io.cpp:41-296) ----------------------------
+struct LoadOptions {  // graph_io.hpp:12-19
+    std::int32_t num_nodes = -1;  // -1: 1 + max id seen
+    bool strict = false;
+};
+// load_graph (graph_io.cpp:41-80): text edge list -> build_graph on the device.
+inline std::pair<Graph, ValidationReport> load_graph(Context& ctx, const std::string& path,
+                                                     const LoadOptions& options = {}) {
+    sc_graph* h = nullptr;
+    ValidationReport rep;
+    check(sc_load_graph(ctx.get(), path.c_str(), options.num_nodes, options.strict ? 1 : 0, &h,
+                        &rep.dropped_self_loops, &rep.merged_duplicate_edges));
+    return {Graph(ctx, h), rep};
+}
+struct FeatureMatrix {  // Eigen::MatrixXd of load_features, as fp32 row-major
+    std::int64_t rows = 0, cols = 0;
+    std::vector<float> values;
+};
+inline FeatureMatrix load_features(const std::string& path, NodeId expected_nodes) {  // graph_io.cpp:82-160
+    FeatureMatrix m;
+    check(sc_load_features(path.c_str(), expected_nodes, nullptr, 0, &m.rows, &m.cols));
+    m.values.resize(static_cast<std::size_t>(m.rows * m.cols));
+    check(sc_load_features(path.c_str(), expected_nodes, m.values.data(), static_cast<std::int64_t>(m.values.size()),
+                           &m.rows, &m.cols));
+    return m;
+}
+struct LabelData {  // Graph::labels / multilabels / num_classes after load_labels
+    std::vector<NodeId> labels;        // multi-class
+    std::vector<float> multilabels;    // n x num_classes 0/1
+    int num_classes = 0;
+    bool is_multilabel() const { return !multilabels.empty(); }
+};
+inline LabelData load_labels(const std::string& path, NodeId num_nodes) {  // graph_io.cpp:188-242
+    LabelData d;
+    std::int32_t nc = 0, ml = 0;
+    check(sc_load_labels(path.c_str(), num_nodes, nullptr, nullptr, 0, &nc, &ml));
+    d.num_classes = nc;
+    if (ml) {
+        d.multilabels.resize(static_cast<std::size_t>(num_nodes) * static_cast<std::size_t>(nc));
+        check(sc_load_labels(path.c_str(), num_nodes, nullptr, d.multilabels.data(),
+                             static_cast<std::int64_t>(d.multilabels.size()), &nc, &ml));
+    } else {
+        d.labels.resize(static_cast<std::size_t>(num_nodes));
+        check(sc_load_labels(path.c_str(), num_nodes, d.labels.data(), nullptr, 0, &nc, &ml));
+    }
+    return d;
+}
+struct SplitMasks {
+    std::vector<std::uint8_t> train, val, test;
+};
+inline SplitMasks load_masks(const std::string& path, NodeId num_nodes) {  // graph_io.cpp:256-283
+    SplitMasks m;
+    m.train.resize(static_cast<std::size_t>(num_nodes));
+    m.val.resize(m.train.size());
+    m.test.resize(m.train.size());
+    check(sc_load_masks(path.c_str(), num_nodes, m.train.data(), m.val.data(), m.test.data()));
+    return m;
+}
+// main.cpp:137 load_dataset: graph + features + labels (+ multi-label) + masks on the device
+inline std::pair<Graph, ValidationReport> load_dataset(Context& ctx, const std::string& edges,
+                                                       const std::string& features, const std::string& labels,
+                                                       const std::string& masks, const LoadOptions& options = {}) {
+    auto gr = load_graph(ctx, edges, options);
+    Graph& g = gr.first;
+    const FeatureMatrix f = load_features(features, g.num_nodes);
+    const LabelData l = load_labels(labels, g.num_nodes);
+    const SplitMasks m = load_masks(masks, g.num_nodes);
+    const std::vector<NodeId> ids = l.is_multilabel() ? std::vector<NodeId>(static_cast<std::size_t>(g.num_nodes), 0)
+                                                      : l.labels;
+    g.set_data(f.values, static_cast<int>(f.cols), ids, l.num_classes, m.train, m.val, m.test);
+    if (l.is_multilabel()) g.set_multilabels(l.multilabels, l.num_classes);
+    return gr;
+}
+inline void save_edge_list(const Graph& g, const std::string& path) {  // graph_io.cpp:75-80
+    check(sc_save_edge_list(g.get(), path.c_str()));
+}
+inline void save_features_csv(const FeatureMatrix& m, const std::string& path) {  // graph_io.cpp:162-172
+    check(sc_save_features(path.c_str(), m.values.data(), m.rows, m.cols, 0));
+}
+inline void save_features_binary(const FeatureMatrix& m, const std::string& path) {  // graph_io.cpp:174-186
+    check(sc_save_features(path.c_str(), m.values.data(), m.rows, m.cols, 1));
+}
+inline void save_labels(const LabelData& l, NodeId num_nodes, const std::string& path) {  // graph_io.cpp:244-254
+    check(sc_save_labels(path.c_str(), num_nodes, l.is_multilabel() ? nullptr : l.labels.data(),
+                         l.is_multilabel() ? l.multilabels.data() : nullptr, l.num_classes));
+}
+inline void save_masks(const SplitMasks& m, const std::string& path) {  // graph_io.cpp:285-296
+    check(sc_save_masks(path.c_str(), static_cast<std::int32_t>(m.train.size()), m.train.data(), m.val.data(),
+                        m.test.data()));
+}
+
 struct PartSubgraph {  // partition.hpp:14-31 (host copy)
     std::vector<NodeId> nodes;
     std::vector<NodeId> global_to_local;

@@ -1071,20 +1071,18 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
             bool fresh[2] = {true, true};  // at the start of a run: the half's accumulator must be drained
             while (kbh[0] < kblocks || kbh[1] < kblocks) {
                 int h = (kbh[1] < kbh[0]) ? 1 : 0;  // the lagging half first
-                bool go = false;
-                for (int tries = 0; tries < 2 && !go; ++tries, h ^= 1) {
-                    const int kb = kbh[h];
-                    if (kb >= kblocks) continue;
-                    if (kbh[h ^ 1] < kblocks && kb > kbh[h ^ 1] + Cfg::kStages - 1) continue;  // ring depth
-                    if (fresh[h]) {
-                        if (!mbar_test(&tempty[h], (runh[h] & 1) ^ 1)) continue;
-                        tc_fence_after();
-                        fresh[h] = false;
-                    }
-                    go = true;
-                    break;
+                if (nh > 1 && fresh[h] && !mbar_test(&tempty[h], (runh[h] & 1) ^ 1)) {
+                    // its accumulator is still draining: run the other half ahead if it can go now
+                    const int o = h ^ 1;
+                    if (kbh[o] < kblocks && kbh[o] <= kbh[h] + Cfg::kStages - 1 &&
+                        (!fresh[o] || mbar_test(&tempty[o], (runh[o] & 1) ^ 1)))
+                        h = o;
                 }
-                if (!go) continue;  // both halves wait for a drain: poll again
+                if (fresh[h]) {  // otherwise block (suspended in try_wait, no issue-slot spinning)
+                    TN_TIMED_WAIT(w_b, mbar_wait(&tempty[h], (runh[h] & 1) ^ 1));
+                    tc_fence_after();
+                    fresh[h] = false;
+                }
                 const int kb = kbh[h];
                 const int st = kb % Cfg::kStages;
                 TN_TIMED_WAIT(w_a, mbar_wait(&full[st], (kb / Cfg::kStages) & 1));
@@ -1719,7 +1717,11 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     }
 }
 
-void TcGemm::init(sc_trainer* t) { enabled = t->gemm_mode == 0; }
+void TcGemm::init(sc_trainer* t) {
+    enabled = t->gemm_mode == 0;
+    const char* e = std::getenv("SC_TN_DUAL");
+    dual = !(e && e[0] == '0');
+}
 
 const BImage& TcGemm::image(const MatB& b, int32_t N, int32_t K, cudaStream_t s) {
     const Key key{b.ptr, b.ld, b.nn, N, K};
@@ -1748,11 +1750,7 @@ void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b
 bool TcGemm::tn_dual(sc_trainer* t, const MatT& a1, const float* amax_a1, const MatT& a2, const float* amax_a2,
                      const MatT& b1, const float* amax_b1, const MatT& b2, const float* amax_b2, int64_t M, float* C1,
                      int64_t ldc1, float* C2, int64_t ldc2) {
-    static const bool on = [] {
-        const char* e = std::getenv("SC_TN_DUAL");
-        return !(e && e[0] == '0');
-    }();
-    if (!on || !enabled || !tn_dual_supported(a1, a2, b1, b2)) return false;
+    if (!dual || !enabled || !tn_dual_supported(a1, a2, b1, b2)) return false;
     gemm_tn_f16x3_dual(a1, amax_a1, a2, amax_a2, b1, amax_b1, b2, amax_b2, M, C1, ldc1, C2, ldc2, t->ws.get(),
                        t->ws_floats, t->ctx->stream);
     return true;

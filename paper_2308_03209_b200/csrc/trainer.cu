@@ -446,7 +446,7 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         // otherwise dU runs first (optionally on the side stream) and dW after.
         float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
         const MatT dzt{t->dz.get(), lo.H, nullptr, lo.H};
-        const bool dual = !t->overlap && tn_dual_supported(dht, dzt, meant, xint) && t->tc.enabled;
+        const bool dual = !t->overlap && t->tc.enabled && t->tc.dual && tn_dual_supported(dht, dzt, meant, xint);
         if (!dual) {
             hand_off(s, w);
             P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), w, 2.0 * n * lo.H * (lo.H + lo.in));
@@ -463,8 +463,9 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         P.end(s);
         if (dual) {
             P.begin("wgrad", 4.0 * n * (3 * lo.H + lo.in), s, 2.0 * n * lo.H * (lo.H + 2 * lo.in));
-            t->tc.tn_dual(t, dht, dh_amax, dzt, dz_amax, meant, t->amax_msg(l), xint, xin_amax, n,
-                          t->slot_ptr(2 * l + 1, i), lo.H + lo.in, t->slot_ptr(2 * l, i), lo.in);
+            if (!t->tc.tn_dual(t, dht, dh_amax, dzt, dz_amax, meant, t->amax_msg(l), xint, xin_amax, n,
+                               t->slot_ptr(2 * l + 1, i), lo.H + lo.in, t->slot_ptr(2 * l, i), lo.in))
+                throw std::logic_error("dual weight-gradient launch refused a supported shape");
             P.end(s);
             exchange_bucket(t, 2 * l + 1, round);
         } else {

@@ -66,3 +66,71 @@ def test_cpp_facade_matches_oracle(tmp_path):
     assert [int(x) for x in res["comm"].split()] == O.comm_volume("halo_sync_model", p, P, 2, 16, 100)
     assert float(res["erf"]) == O.expected_rf_random(p, 13)
     assert float(res["ilb"]) == O.imbalance_lower_bound(p, 9, 2)
+
+
+EXE_IO = os.path.join(ROOT, "tests", "cpp", "facade_io_main")
+
+
+def write_dataset(tmp_path, golden, multilabel):
+    """The karate club (the reference's proj/tests/fixtures/karate.edges, from the golden dump) in the
+    reference's file formats: a messy edge list (comments, blank and CRLF lines, reversed pairs, a
+    duplicate, a self-loop), CFM1 features, class-id or multi-label rows, and split-mask lines."""
+    import struct
+    z = golden("karate")
+    e = z["edges"].astype(int)
+    n = int(z["n"])
+    rng = np.random.default_rng(5)
+    lines = ["# Zachary's karate club", ""]
+    for k, (u, v) in enumerate(e[rng.permutation(len(e))]):
+        lines.append(f"{v} {u}" if k % 3 == 0 else f"{u} {v}" + ("\r" if k % 5 == 0 else ""))
+    lines += [f"{e[0][0]} {e[0][1]}", "7 7", "   # trailing comment"]
+    (tmp_path / "g.edges").write_text("\n".join(lines) + "\n")
+    f = rng.standard_normal((n, 8)).astype(np.float32)
+    (tmp_path / "f.bin").write_bytes(b"CFM1" + struct.pack("<QQ", n, 8) + f.astype("<f4").tobytes())
+    deg = np.bincount(e.ravel(), minlength=n)
+    if multilabel:
+        y = ((rng.random((n, 3)) < 0.4) | (np.arange(3)[None, :] == (deg % 3)[:, None])).astype(np.float32)
+        (tmp_path / "l.txt").write_text("\n".join(",".join(str(int(v)) for v in row) for row in y) + "\n")
+        lab = None
+    else:
+        lab = (deg % 4).astype(np.int32)
+        y = None
+        (tmp_path / "l.txt").write_text("\n".join(str(int(v)) for v in lab) + "\n")
+    perm = rng.permutation(n)
+    tr, va, te = (np.zeros(n, np.uint8) for _ in range(3))
+    tr[perm[:20]] = 1
+    va[perm[20:27]] = 1
+    te[perm[27:]] = 1
+    (tmp_path / "m.txt").write_text("".join(f"{t} {v}\n" for t, m in (("train", tr), ("val", va), ("test", te))
+                                            for v in np.flatnonzero(m)))
+    return e, n, f, lab, y, (tr, va, te)
+
+
+@pytest.mark.parametrize("multilabel", [False, True])
+def test_cpp_facade_load_dataset_matches_oracle(tmp_path, golden, multilabel):
+    """load_dataset (graph_io.cpp:41-296 loaders through the facade) -> train_cofree, against the oracle
+    trained on the same data (row f2)."""
+    assert os.path.exists(EXE_IO)
+    e, n, f, lab, y, (tr, va, te) = write_dataset(tmp_path, golden, multilabel)
+    loss = "bce" if multilabel else "softmax_ce"
+    out = subprocess.run([EXE_IO, str(tmp_path / "g.edges"), str(tmp_path / "f.bin"), str(tmp_path / "l.txt"),
+                          str(tmp_path / "m.txt"), "2", "3", loss], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    res = {ln.split(" ", 1)[0]: ln.split(" ", 1)[1] for ln in out.stdout.strip().split("\n")}
+    gn, gm, sl, dup, d, C, ml = map(int, res["graph"].split())
+    assert (gn, gm, sl, dup, d, ml) == (n, len(e), 1, 1, 8, int(multilabel))
+    O = oracle()
+    og = O.graph_build(n, e.astype(np.int32))
+    og.set_data(f, lab if lab is not None else np.zeros(n, np.int32), C, tr, va, te)
+    if multilabel:
+        og.set_multilabels(y)
+    t = og.partition("random", 2, 3).trainer([16, 16], lr=0.01, loss=loss, dropedge=True, seed=1, f32=True)
+    ref_loss, ref_metrics = [], []
+    for ep in range(3):
+        ref_loss.append(t.step(ep)[0])
+        ref_metrics += list(t.eval())
+    np.testing.assert_allclose(np.array(res["loss"].split(), float), ref_loss, rtol=1e-5)
+    theta = np.array(res["params"].split(), float)
+    assert np.linalg.norm(theta - t.params()) / np.linalg.norm(t.params()) <= 1e-4
+    # split metrics: one prediction flipping on a near-tie moves a 7-node split by 1/7
+    np.testing.assert_allclose(np.array(res["metrics"].split(), float), ref_metrics, atol=0.15)
