@@ -904,8 +904,13 @@ sc_status sc_trainer_get_part_logits(sc_trainer* t, int32_t part, float* out) {
         REQUIRE_ARG(part >= 0 && part < t->p, "bad part index");
         REQUIRE_ARG(part % t->world == t->rank, "partition is not trained on this rank");
         set_device(t->ctx);
+        trainer_finish(t, nullptr, nullptr);
+        if (t->shared_logits && part != t->last_part)
+            throw std::invalid_argument("logits of partition " + std::to_string(part) +
+                                        " were not kept (shared logits buffer: only the last trained partition's)");
+        const float* src = t->shared_logits ? t->logits_shared.get() : t->ps[part].logits.get();
         if (t->ps[part].n > 0)
-            SC_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * t->C, t->ps[part].logits.get(), sizeof(float) * t->Cp,
+            SC_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * t->C, src, sizeof(float) * t->Cp,
                                       sizeof(float) * t->C, t->ps[part].n, cudaMemcpyDeviceToHost, t->ctx->stream));
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
     });

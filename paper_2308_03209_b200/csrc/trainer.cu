@@ -177,6 +177,17 @@ void trainer_init(sc_trainer* t) {
     SC_CUDA(cudaMemsetAsync(t->slots.get(), 0, t->slots.bytes(), s));
 
     // per-partition inputs (trainer.hpp:218-243)
+    {
+        int64_t rows = 0;
+        for (int i = t->rank; i < t->p; i += t->world) rows += vc->parts[i].n_local;
+        size_t free_b = 0, total_b = 0;
+        SC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const double budget = 0.15 * static_cast<double>(free_b);  // each cache: at most 15 % of free memory
+        const char* e = std::getenv("SC_SHARED_X0");
+        t->shared_x0 = e ? std::atoi(e) != 0 : 4.0 * rows * t->dp > budget;
+        e = std::getenv("SC_SHARED_LOGITS");
+        t->shared_logits = e ? std::atoi(e) != 0 : 4.0 * rows * t->Cp > budget;
+    }
     int64_t n_max = 1, nnz_max = 1;
     t->local.clear();
     for (int i = t->rank; i < t->p; i += t->world) t->local.push_back(i);
@@ -198,9 +209,9 @@ void trainer_init(sc_trainer* t) {
         st.g_amax.alloc(1);
         SC_CUDA(cudaMemsetAsync(st.g_amax.get(), 0, sizeof(float), s));
         absmax(st.n, st.scale.get(), st.g_amax.get(), s);
-        st.logits.alloc(std::max<int64_t>(st.n * t->Cp, 1));
+        if (!t->shared_logits) st.logits.alloc(std::max<int64_t>(st.n * t->Cp, 1));
         build_heavy_rows(t->ctx, st.n, pd.offsets.get(), st.heavy);
-        st.x0.alloc(std::max<int64_t>(st.n * t->dp, 1));
+        if (!t->shared_x0) st.x0.alloc(std::max<int64_t>(st.n * t->dp, 1));
         if (t->use_dropedge) {
             st.words = (st.nnz + 31) / 32;
             st.bits.alloc(std::max<int64_t>(st.words * t->K, 1));
@@ -225,6 +236,8 @@ void trainer_init(sc_trainer* t) {
     }
     t->nonfinite.alloc(1);
     t->red_partial.alloc(1024);
+    if (t->shared_x0) t->x0_shared.alloc(std::max<int64_t>(n_max * t->dp, 1));
+    if (t->shared_logits) t->logits_shared.alloc(std::max<int64_t>(n_max * t->Cp, 1));
     ensure_rows(t, n_max);
     int64_t max_seg = 0;
     for (int i : t->local) max_seg = std::max<int64_t>(max_seg, t->ps[i].heavy.nseg);
@@ -505,22 +518,25 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     }
     const int64_t kept =
         bits ? 2 * static_cast<int64_t>(std::ceil((1.0 - t->ratio) * static_cast<double>(pd.m_local))) : st.nnz;
-    if (st.x0_version != t->g->feat_version) {  // the partition's feature rows, contiguous (train_cofree :225-227)
-        t->prof.begin("gather_x0", 8.0 * st.n * t->d, s);
-        gather_rows(st.n, t->d, pd.nodes.get(), t->g->features.get(), st.x0.get(), s, t->dp);
+    float* x0 = t->shared_x0 ? t->x0_shared.get() : st.x0.get();
+    if (t->shared_x0 || st.x0_version != t->g->feat_version) {  // the partition's feature rows, contiguous
+        t->prof.begin("gather_x0", 8.0 * st.n * t->d, s);                   // (train_cofree :225-227)
+        gather_rows(st.n, t->d, pd.nodes.get(), t->g->features.get(), x0, s, t->dp);
         t->prof.end(s);
         st.x0_version = t->g->feat_version;
     }
+    float* logits = t->shared_logits ? t->logits_shared.get() : st.logits.get();
+    t->last_part = i;
     const Rows R{st.n, pd.offsets.get(), pd.nbrs.get(), bits, pd.nodes.get(), st.nnz, kept, st.g_amax.get(),
-                 st.x0.get(), t->dp, &st.heavy};
+                 x0, t->dp, &st.heavy};
     SC_CUDA(cudaMemsetAsync(t->amax.get(), 0, t->amax.bytes(), s));  // per-partition operand |max| slots
-    forward(t, R, st.logits.get(), train_acts(t));
+    forward(t, R, logits, train_acts(t));
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
     if (t->loss == 0)
-        softmax_ce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
+        softmax_ce(st.n, t->C, t->Cp, logits, t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
                    t->G.get(), t->row_loss.get(), s);
     else
-        bce(st.n, t->C, t->Cp, st.logits.get(), t->g->labels.get(), t->g->multilabel ? t->g->targets.get() : nullptr,
+        bce(st.n, t->C, t->Cp, logits, t->g->labels.get(), t->g->multilabel ? t->g->targets.get() : nullptr,
             pd.nodes.get(), st.w.get(), st.scale.get(), t->G.get(), t->row_loss.get(), s);
     sum_f64(st.n, t->row_loss.get(), t->red_partial.get(), t->part_loss.get() + i, t->normalizer, s);
     t->prof.end(s);

@@ -112,6 +112,14 @@ struct sc_trainer {
     sc::DevBuf<float> eval_x0;  // the full feature matrix with 16-byte rows (d % 4 != 0)
     uint64_t eval_x0_version = 0;
     bool eval_only = false;     // sc_evaluate's forward-only engine (no partitions, no optimizer)
+    // Per-partition caches that only save time: each local partition's gathered layer-0 rows
+    // (x0) and its last logits. When they would take more than their budget of device memory
+    // (large graphs: R-MAT 20M / 1B at p = 16) all partitions share one buffer instead: x0 is
+    // then gathered again for every partition every step (~n_i d 8 bytes), and only the last
+    // trained partition's logits stay readable (sc_trainer_get_part_logits).
+    bool shared_x0 = false, shared_logits = false;
+    sc::DevBuf<float> x0_shared, logits_shared;
+    int last_part = -1;
     // CommAudit (trainer.hpp:61-76): parameter-gradient floats this rank's
     // partitions handed to the exchange in the last epoch (p * |theta| at world 1).
     uint64_t audit_floats = 0;

@@ -1,0 +1,41 @@
+"""Memory modes for large graphs (R-MAT 20M / 1B at p = 16): the per-partition x0 row cache and
+logits buffers replaced by shared buffers (SC_SHARED_X0 / SC_SHARED_LOGITS, chosen automatically
+when they would exceed their budget). Same arithmetic: parameters bitwise equal to the cached mode."""
+import os
+
+import numpy as np
+import pytest
+
+from cpu_libs import oracle
+from test_gpu_parity import gpu_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def run(sc, og, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        g = gpu_graph(sc, og, 8)
+        part = sc.partition_random(g, 6, 3)
+        t = sc.CoFreeTrainer(g, part, sc.TrainConfig(layers=2, hidden=[16, 16], use_dropedge=True, seed=1))
+        losses = [t.step(e)[0] for e in range(3)]
+        return t, losses
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_shared_buffers_same_bits():
+    from paper_2308_03209_b200 import sagecut as sc
+    og = oracle().graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    a, la = run(sc, og, {"SC_SHARED_X0": "0", "SC_SHARED_LOGITS": "0"})
+    b, lb = run(sc, og, {"SC_SHARED_X0": "1", "SC_SHARED_LOGITS": "1"})
+    assert la == lb
+    np.testing.assert_array_equal(a.params(), b.params())
+    np.testing.assert_array_equal(a.part_logits(5), b.part_logits(5))  # the last trained partition
+    with pytest.raises(ValueError, match="not kept"):
+        b.part_logits(0)
