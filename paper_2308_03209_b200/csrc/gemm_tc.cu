@@ -1064,51 +1064,60 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
         // converted (up to kStages - 1 k-blocks ahead), so the single 256-column accumulator no longer
         // stalls the pipe for a whole drain. Every element still accumulates <= kChunk k-blocks per run.
         if (rank == 0 && lane == 0) {
+            // Per-half state in scalars (no runtime-indexed arrays: those live in local memory and
+            // made this single-thread loop slower than the tensor pipe it feeds).
             const uint32_t idesc = idesc_f16_at(Cfg::kACols, nb_pad / nh);
-            int kbh[2] = {0, nh > 1 ? 0 : kblocks};
-            int endh[2] = {tn_run_end(0, 0, kblocks, nh), nh > 1 ? tn_run_end(1, 0, kblocks, nh) : kblocks};
-            uint32_t runh[2] = {0, 0};
-            bool fresh[2] = {true, true};  // at the start of a run: the half's accumulator must be drained
-            while (kbh[0] < kblocks || kbh[1] < kblocks) {
-                int h = (kbh[1] < kbh[0]) ? 1 : 0;  // the lagging half first
-                if (nh > 1 && fresh[h] && !mbar_test(&tempty[h], (runh[h] & 1) ^ 1)) {
-                    // its accumulator is still draining: run the other half ahead if it can go now
-                    const int o = h ^ 1;
-                    if (kbh[o] < kblocks && kbh[o] <= kbh[h] + Cfg::kStages - 1 &&
-                        (!fresh[o] || mbar_test(&tempty[o], (runh[o] & 1) ^ 1)))
-                        h = o;
-                }
-                if (fresh[h]) {  // otherwise block (suspended in try_wait, no issue-slot spinning)
-                    TN_TIMED_WAIT(w_b, mbar_wait(&tempty[h], (runh[h] & 1) ^ 1));
+            int kb0 = 0, kb1 = nh > 1 ? 0 : kblocks;                 // next k-block of each half
+            int beg0 = 0, beg1 = 0;                                  // first k-block of the current run
+            int end0 = tn_run_end(0, 0, kblocks, nh), end1 = nh > 1 ? tn_run_end(1, 0, kblocks, nh) : kblocks;
+            uint32_t par0 = 1, par1 = 1;                             // tempty parity the next run waits for
+            bool fresh0 = true, fresh1 = true;                       // at a run start: accumulator must be free
+            auto issue = [&](int h, int& kb, int& beg, int& end, uint32_t& par, bool& fresh, int other_kb) {
+                if (fresh) {  // block (suspended in try_wait) until the epilogue has drained this half
+                    TN_TIMED_WAIT(w_b, mbar_wait(&tempty[h], par));
                     tc_fence_after();
-                    fresh[h] = false;
+                    fresh = false;
                 }
-                const int kb = kbh[h];
                 const int st = kb % Cfg::kStages;
                 TN_TIMED_WAIT(w_a, mbar_wait(&full[st], (kb / Cfg::kStages) & 1));
                 tc_fence_after();
                 const uint8_t* stp = smem + st * Cfg::kStage;
                 const uint32_t bhi = smem_u32(stp) + h * kTnLbo, blo = smem_u32(stp + Cfg::kBTile) + h * kTnLbo;
                 const uint32_t d_tmem = tmem_base + h * 128;
-                const bool first_kb = kb == endh[h] - tn_run_len(h, endh[h], nh);
 #pragma unroll
                 for (int k = 0; k < kTnBK / 16; ++k) {
                     const uint32_t adv = k * 2 * kTnSbo;  // 16 rows = 2 K groups
                     const uint64_t dbh = desc_mn_sw128(bhi + adv, kTnLbo, kTnSbo);
                     const uint64_t dbl = desc_mn_sw128(blo + adv, kTnLbo, kTnSbo);
                     const uint32_t tah = tmem_base + 256 + st * 32 + k * 8;  // lo plane 16 columns after hi
-                    mma_f16_ts_pair(d_tmem, tah, dbh, idesc, (first_kb && k == 0) ? 0u : 1u);
+                    mma_f16_ts_pair(d_tmem, tah, dbh, idesc, (kb == beg && k == 0) ? 0u : 1u);
                     mma_f16_ts_pair(d_tmem, tah, dbl, idesc, 1u);
                     mma_f16_ts_pair(d_tmem, tah + 16, dbh, idesc, 1u);
                 }
-                if (kb == endh[h] - 1) {  // end of this half's run: hand it to the epilogue
+                if (kb == end - 1) {  // end of this half's run: hand it to the epilogue
                     mma_commit_g<PAIR>(&tfull[h]);
-                    ++runh[h];
-                    fresh[h] = true;
-                    endh[h] = tn_run_end(h, endh[h], kblocks, nh);
+                    par ^= 1u;
+                    fresh = true;
+                    beg = end;
+                    end = tn_run_end(h, end, kblocks, nh);
                 }
-                if (kbh[h ^ 1] > kb) mma_commit_g<PAIR>(&empty[st]);  // both halves issued: stage free
-                kbh[h] = kb + 1;
+                if (other_kb > kb) mma_commit_g<PAIR>(&empty[st]);  // both halves issued: stage free
+                ++kb;
+            };
+            while (kb0 < kblocks || kb1 < kblocks) {
+                bool one = kb1 >= kb0;  // the lagging half first (ties: half 0)
+                if (nh > 1) {
+                    // the lagging half's accumulator is still draining: run the other one ahead if it can
+                    // go now (within the stage ring, its own accumulator free)
+                    if (one && fresh0 && !mbar_test(&tempty[0], par0) && kb1 < kblocks &&
+                        kb1 <= kb0 + Cfg::kStages - 1 && (!fresh1 || mbar_test(&tempty[1], par1)))
+                        one = false;
+                    else if (!one && fresh1 && !mbar_test(&tempty[1], par1) && kb0 < kblocks &&
+                             kb0 <= kb1 + Cfg::kStages - 1 && (!fresh0 || mbar_test(&tempty[0], par0)))
+                        one = true;
+                }
+                if (one) issue(0, kb0, beg0, end0, par0, fresh0, kb1);
+                else issue(1, kb1, beg1, end1, par1, fresh1, kb0);
             }
         }
         __syncwarp();
