@@ -50,6 +50,12 @@ CONFIGS = {
     "rmat": dict(workload="power-law R-MAT synthetic (BASELINE configs[3])", nodes=20_000_000, pairs=1_000_000_000,
                  feats=128, classes=47, layers=3, hidden=256, parts=8, dropedge=False, k=10, ratio=0.5, lr=3e-3,
                  rmat=(0.57, 0.19, 0.19, 0.05), default_scale=0.25),
+    # configs[3] at FULL size (20M nodes / 1B samples) on one GPU: p = 16 partitions time-multiplexed
+    # (the layout 8 GPUs would run as two partitions each); activations switch to the compact set
+    # (shared msg buffer + ReLU sign bits) automatically when the per-layer set would not fit.
+    "rmat_full": dict(workload="power-law R-MAT synthetic (BASELINE configs[3]), full size, p = 16",
+                      nodes=20_000_000, pairs=1_000_000_000, feats=128, classes=47, layers=3, hidden=256, parts=16,
+                      dropedge=False, k=10, ratio=0.5, lr=3e-3, rmat=(0.57, 0.19, 0.19, 0.05), default_scale=1.0),
     # configs[0]: ER 10k / 200k, 64 feats, 2 layers (reference default hidden 32), p = 4
     "er10k": dict(workload="Erdos-Renyi 10k/200k (BASELINE configs[0])", nodes=10_000, pairs=200_000, feats=64,
                   classes=4, layers=2, hidden=32, parts=4, dropedge=False, k=10, ratio=0.5, lr=1e-2),
@@ -416,6 +422,10 @@ def run_gpu_arm(args, cfg):
     launches = ctx.launch_count() - launches0
     fallbacks = fallback_count() - fallbacks0
     free_b, total_b = torch.cuda.mem_get_info(local)  # device memory in use (graph, partitions, trainer)
+    try:
+        mem_mode = trainer.memory_mode()
+    except AttributeError:  # an older library build under SC_LIB (A/B runs)
+        mem_mode = None
     barrier()
     ms_step = max_over_ranks(ms / args.steps)
     value = cfg["layers"] * kept / (ms_step / 1e3)
@@ -556,6 +566,7 @@ def run_gpu_arm(args, cfg):
         "clocks": clocks.summary(),
         "setup_s": setup_s,
         "hbm_used_gb": round((total_b - free_b) / 1e9, 1),
+        "memory_mode": mem_mode,
         "loss_first_last": [losses[0], losses[-1]] if losses else None,
     }
     print(json.dumps(line), flush=True)
@@ -575,10 +586,13 @@ def main():
     ap.add_argument("--cpu-full-partition", action="store_true",
                     help="time the reference on one FULL-size partition (minutes of CPU; BASELINE.md §3) and write "
                          "profiles/r02_reference_full_partition.json")
+    ap.add_argument("--parts", type=int, default=None, help="override the config's partition count p")
     ap.add_argument("--scale", type=float, default=None,
                     help="scale nodes and edges of the config (default 1; rmat: 0.25, see CONFIGS)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.parts:
+        cfg["parts"] = args.parts
     if args.cpu_full_partition:
         res = cpu_full_partition(cfg)
         print(json.dumps(res), flush=True)

@@ -259,6 +259,11 @@ sc_status sc_trainer_comm_audit(sc_trainer* t, uint64_t* gradient_floats, uint64
 /* GEMMs that ran on the fp32 SIMT kernels although the tensor-core path was
  * enabled (operand layout not TMA-compatible), since the trainer was created. */
 sc_status sc_trainer_fallback_count(sc_trainer* t, int64_t* count);
+/* Memory layout the trainer chose (no reference counterpart: the reference keeps
+ * every per-layer cache in host RAM, nn.hpp:160-170). flags bit 0: compact
+ * activations (one msg buffer + ReLU sign bits); bit 1: shared x0 rows; bit 2:
+ * shared logits. arena_bytes: the per-row activation arena. */
+sc_status sc_trainer_memory_mode(sc_trainer* t, int32_t* flags, int64_t* arena_bytes);
 /* Per-kernel timing of the last step (CUDA events), for bench.py's roofline. */
 sc_status sc_trainer_profile(sc_trainer* t, int32_t enable);
 sc_status sc_trainer_kernel_times(sc_trainer* t, const char** names, double* ms, double* bytes, int32_t cap,

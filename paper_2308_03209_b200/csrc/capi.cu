@@ -985,6 +985,13 @@ sc_status sc_trainer_fallback_count(sc_trainer* t, int64_t* count) {
         *count = t->tc.simt_fallbacks;
     });
 }
+sc_status sc_trainer_memory_mode(sc_trainer* t, int32_t* flags, int64_t* arena_bytes) {
+    return guard([&] {
+        REQUIRE_ARG(t, "sc_trainer_memory_mode: null argument");
+        if (flags) *flags = (t->compact ? 1 : 0) | (t->shared_x0 ? 2 : 0) | (t->shared_logits ? 4 : 0);
+        if (arena_bytes) *arena_bytes = static_cast<int64_t>(t->arena.bytes());
+    });
+}
 sc_status sc_comm_volume(int32_t mode, int32_t num_parts, uint64_t param_count, uint64_t num_layers,
                          uint64_t hidden_dim, uint64_t total_halo, uint64_t* floats_per_iteration,
                          uint64_t* gradient_floats, uint64_t* embedding_floats) {
@@ -1216,15 +1223,34 @@ sc_status sc_trainer_debug_buffer(sc_trainer* t, const char* name, int32_t layer
         set_device(t->ctx);
         trainer_finish(t, nullptr, nullptr);
         const std::string nm(name);
-        const DevBuf<float>* b = nullptr;
-        if (nm == "X" && layer >= 1 && layer <= t->L) b = &t->X[layer];
-        else if (nm == "MSG" && layer >= 0 && layer < t->L) b = &t->MSG[layer];
-        else if (nm == "MEAN" && layer >= 0 && layer < t->L) b = &t->MEAN[layer];
-        else if (nm == "inv") b = &t->inv;
-        else if (nm == "G") b = &t->G;
+        const void* b = nullptr;
+        size_t width = 0;  // bytes per row
+        const int32_t H = layer >= 0 && layer < t->L ? t->lay[layer].H : 0;
+        if (nm == "X" && layer >= 1 && layer <= t->L) {
+            b = t->X[layer];
+            width = 4 * size_t(t->lay[layer - 1].H);
+        } else if (nm == "MSG" && layer >= 0 && layer < t->L) {
+            REQUIRE_ARG(!t->compact, "sc_trainer_debug_buffer: compact activations keep only the ReLU bits (POS)");
+            b = t->MSG[layer];
+            width = 4 * size_t(H);
+        } else if (nm == "POS" && layer >= 0 && layer < t->L) {
+            REQUIRE_ARG(t->compact, "sc_trainer_debug_buffer: POS exists with compact activations only");
+            b = t->POS[layer];
+            width = 4 * size_t((H + 31) / 32);
+        } else if (nm == "MEAN" && layer >= 0 && layer < t->L) {
+            b = t->MEAN[layer];
+            width = 4 * size_t(H);
+        } else if (nm == "inv") {
+            b = t->inv;
+            width = 4;
+        } else if (nm == "G") {
+            b = t->G;
+            width = 4 * size_t(t->Cp);
+        }
         REQUIRE_ARG(b, "sc_trainer_debug_buffer: unknown buffer");
-        REQUIRE_ARG(bytes >= 0 && size_t(bytes) <= b->bytes(), "sc_trainer_debug_buffer: more bytes than the buffer holds");
-        SC_CUDA(cudaMemcpyAsync(dst_dev, b->get(), size_t(bytes), cudaMemcpyDeviceToDevice, t->ctx->stream));
+        REQUIRE_ARG(bytes >= 0 && size_t(bytes) <= width * size_t(t->rows_cap),
+                    "sc_trainer_debug_buffer: more bytes than the buffer holds");
+        SC_CUDA(cudaMemcpyAsync(dst_dev, b, size_t(bytes), cudaMemcpyDeviceToDevice, t->ctx->stream));
         SC_CUDA(cudaStreamSynchronize(t->ctx->stream));
     });
 }

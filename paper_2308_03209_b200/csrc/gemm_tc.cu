@@ -88,6 +88,7 @@ struct alignas(64) Params {
     int epi;
     const float* row_scale;
     float* amax_out;
+    uint32_t* relu_pos;  // optional (EPI == kEpiRelu): bit c % 32 of word [row][c / 32] = C[row][c] > 0
     int64_t tiles;
     unsigned long long* trace;  // optional (SC_TN_TRACE_BUILD + SC_TN_TRACE=1), as TnParams::trace
 };
@@ -630,13 +631,17 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
                 if (lane == 0) TN_TIMED_WAIT(w_b, bulk_wait_read<0>());  // the previous store has read the box
                 __syncwarp();
+                uint32_t pos = 0;  // ReLU decisions of this row's 32 columns (compact activations)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     float x[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         float v = __uint_as_float(r[4 * j + q]) * unscale;
-                        if (EPI == kEpiRelu) v = fmaxf(v, 0.f);
+                        if (EPI == kEpiRelu) {
+                            v = fmaxf(v, 0.f);
+                            pos |= (v > 0.f ? 1u : 0u) << (4 * j + q);
+                        }
                         if (EPI == kEpiRowScale) v = sc * v;
                         if (AMAX) amx = fmaxf(amx, fabsf(v));
                         x[q] = v;
@@ -644,6 +649,8 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                     *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
                         make_float4(x[0], x[1], x[2], x[3]);
                 }
+                if (EPI == kEpiRelu && p.relu_pos && c0 < p.N && row0 + lane < p.M)
+                    p.relu_pos[(row0 + lane) * ((p.N + 31) >> 5) + (c0 >> 5)] = pos;
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0 && row0 < p.M) tma_store_2d(&p.tmap_c, box, c0, static_cast<int32_t>(row0));
@@ -1619,7 +1626,7 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
 
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-                float* amax_out, cudaStream_t s) {
+                float* amax_out, cudaStream_t s, uint32_t* relu_pos) {
     if (M <= 0 || N <= 0) return;
     if (!tc_supported(a1, a2, N) || !tc_out_supported(C, ldc))
         throw std::logic_error("gemm_f16x3: unsupported operand layout");
@@ -1649,6 +1656,7 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.epi = epi;
     p.row_scale = row_scale;
     p.amax_out = amax_out;
+    p.relu_pos = epi == kEpiRelu ? relu_pos : nullptr;
     static const bool trace = [] {
         const char* e = std::getenv("SC_TN_TRACE");
         return e && std::atoi(e) != 0;
@@ -1744,15 +1752,16 @@ const BImage& TcGemm::image(const MatB& b, int32_t N, int32_t K, cudaStream_t s)
 
 void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2,
                 const float* amax2, const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi,
-                const float* row_scale, float* amax_out) {
+                const float* row_scale, float* amax_out, uint32_t* relu_pos) {
     cudaStream_t s = t->ctx->stream;
     if (enabled && tc_supported(a1, a2, N) && tc_out_supported(C, ldc)) {
         const BImage& i1 = image(b1, N, a1.K, s);
         const BImage* i2 = a2 ? &image(*b2, N, a2->K, s) : nullptr;
-        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s);
+        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s, relu_pos);
     } else {
         if (enabled) ++simt_fallbacks;
         gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
+        if (epi == kEpiRelu && relu_pos) relu_sign_bits(M, N, C, ldc, relu_pos, s);
     }
 }
 

@@ -332,10 +332,12 @@ __device__ __forceinline__ void gather_rows_sum(int64_t a, int64_t b, int lane, 
 
 // Output row v: forward mean = inv[v] * sum (nn.hpp:229); backward dz =
 // 1[msg > 0] * sum (nn.hpp:287-288). Returns max|out| of the lane's chunks.
+// The ReLU decision comes from the msg row, or (compact activations) from its
+// sign bits: word [v][c / 32], bit c % 32, written by the msg GEMM's epilogue.
 template <int NCH, bool kBwd>
 __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int32_t H4, const float* __restrict__ inv,
-                                            const float* __restrict__ msg, float* __restrict__ out,
-                                            const float4 (&acc)[NCH]) {
+                                            const float* __restrict__ msg, const uint32_t* __restrict__ pos,
+                                            float* __restrict__ out, const float4 (&acc)[NCH]) {
     float amx = 0.f;
     const float s = kBwd ? 1.f : inv[v];
 #pragma unroll
@@ -348,6 +350,12 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
             r.y *= s;
             r.z *= s;
             r.w *= s;
+        } else if (pos) {
+            const uint32_t b = __ldg(pos + v * ((H + 31) >> 5) + (ch >> 3)) >> ((4 * ch) & 31);
+            r.x = (b & 1u) ? r.x : 0.f;
+            r.y = (b & 2u) ? r.y : 0.f;
+            r.z = (b & 4u) ? r.z : 0.f;
+            r.w = (b & 8u) ? r.w : 0.f;
         } else {
             const float4 mv = __ldg(reinterpret_cast<const float4*>(msg + v * H) + ch);
             r.x = mv.x > 0.f ? r.x : 0.f;
@@ -368,7 +376,8 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
                                                    const int32_t* __restrict__ nbrs,
                                                    const uint32_t* __restrict__ bits, const float* __restrict__ inv,
                                                    const float* __restrict__ src, const float* __restrict__ msg,
-                                                   float* __restrict__ out, float* amax_out, int64_t max_slots) {
+                                                   const uint32_t* __restrict__ pos, float* __restrict__ out,
+                                                   float* amax_out, int64_t max_slots) {
     float amx = 0.f;
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
-        amx = fmaxf(amx, finish_row<NCH, kBwd>(v, lane, H, H4, inv, msg, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd>(v, lane, H, H4, inv, msg, pos, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -421,8 +430,9 @@ __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int3
                                                                 const int32_t* __restrict__ seg_first,
                                                                 const float* __restrict__ partial,
                                                                 const float* __restrict__ inv,
-                                                                const float* __restrict__ msg, float* __restrict__ out,
-                                                                float* amax_out) {
+                                                                const float* __restrict__ msg,
+                                                                const uint32_t* __restrict__ pos,
+                                                                float* __restrict__ out, float* amax_out) {
     const int lane = threadIdx.x & 31;
     const int32_t H4 = H >> 2;
     float amx = 0.f;
@@ -441,7 +451,7 @@ __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int3
                     acc[c].z += p.z;
                     acc[c].w += p.w;
                 }
-        amx = fmaxf(amx, finish_row<NCH, kBwd>(rows[h], lane, H, H4, inv, msg, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd>(rows[h], lane, H, H4, inv, msg, pos, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -476,7 +486,8 @@ template <bool kBwd>
 __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                    const int32_t* __restrict__ nbrs, const uint32_t* __restrict__ bits,
                                    const float* __restrict__ inv, const float* __restrict__ src,
-                                   const float* __restrict__ msg, float* __restrict__ out, float* amax_out) {
+                                   const float* __restrict__ msg, const uint32_t* __restrict__ pos,
+                                   float* __restrict__ out, float* amax_out) {
     const int64_t total = n * H;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t v = i / H;
@@ -484,20 +495,21 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
         float acc = 0.f;
         for (int64_t k = off[v]; k < off[v + 1]; ++k)
             if (slot_kept(bits, k)) acc += src[int64_t(nbrs[k]) * H + c];
-        out[i] = kBwd ? (msg[i] > 0.f ? acc : 0.f) : acc * inv[v];
+        const bool on = !kBwd || (pos ? ((pos[v * ((H + 31) >> 5) + (c >> 5)] >> (c & 31)) & 1u) != 0 : msg[i] > 0.f);
+        out[i] = kBwd ? (on ? acc : 0.f) : acc * inv[v];
         if (amax_out) atomic_max_abs(amax_out, out[i]);
     }
 }
 
 template <int NCH, bool kBwd>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
-              const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv,
-              float* partial) {
+              const float* src, const float* msg, const uint32_t* pos, float* out, cudaStream_t s, float* amax_out,
+              const HeavyRows* hv, float* partial) {
     // 64 blocks of 8 warps per SM: ~13 waves at 5 resident blocks, so the grid-stride tail is short
     // (A/B, profiles/r01_spmm_grid_ab.txt: x16 -> x64 blocks per SM = 0.82 -> 0.92 of HBM peak)
     const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
     const bool heavy = hv && hv->nh > 0;
-    spmm_kernel<NCH, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out,
+    spmm_kernel<NCH, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out, amax_out,
                                                 heavy ? int64_t(kHeavySlots) : INT64_MAX);
     SC_LAUNCH_CHECK();
     count_launch();
@@ -506,27 +518,28 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
         hv->nseg, H, off, nbrs, bits, hv->seg_row.get(), hv->seg_begin.get(), src, partial);
     SC_LAUNCH_CHECK();
     spmm_heavy_finish_kernel<NCH, kBwd><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
-        hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, msg, out, amax_out);
+        hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, msg, pos, out, amax_out);
     SC_LAUNCH_CHECK();
     count_launch(2);
 }
 
 template <bool kBwd>
 void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
-                 const float* src, const float* msg, float* out, cudaStream_t s, float* amax_out,
-                 const HeavyRows* hv, float* partial) {
+                 const float* src, const float* msg, const uint32_t* pos, float* out, cudaStream_t s,
+                 float* amax_out, const HeavyRows* hv, float* partial) {
     if (n <= 0) return;
     if (H % 4 != 0) {  // scalar fallback: thread per output element (any H, any degree)
-        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, out, amax_out);
+        spmm_scalar_kernel<kBwd><<<grid_for(n * H, 256), 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out,
+                                                                      amax_out);
         SC_LAUNCH_CHECK();
         count_launch();
         return;
     }
     const int nch = (H / 4 + 31) / 32;
-    if (nch <= 1) spmm_vec<1, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
-    else if (nch == 2) spmm_vec<2, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
-    else if (nch <= 4) spmm_vec<4, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
-    else spmm_vec<8, kBwd>(n, H, off, nbrs, bits, inv, src, msg, out, s, amax_out, hv, partial);
+    if (nch <= 1) spmm_vec<1, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    else if (nch == 2) spmm_vec<2, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    else if (nch <= 4) spmm_vec<4, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    else spmm_vec<8, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
 }
 
 __global__ void mask_bits_kernel(int64_t nnz, const int32_t* __restrict__ eids, const uint8_t* __restrict__ mask,
@@ -885,12 +898,30 @@ void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* bits, float* 
 }
 void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* msg, float* mean, cudaStream_t s, const HeavyRows* hv, float* partial) {
-    spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, mean, s, nullptr, hv, partial);
+    spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, nullptr, mean, s, nullptr, hv, partial);
 }
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
               const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out, const HeavyRows* hv,
-              float* partial) {
-    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, dz, s, amax_out, hv, partial);
+              float* partial, const uint32_t* relu_pos) {
+    spmm_launch<true>(n, H, offsets, nbrs, bits, nullptr, dmean_s, msg, relu_pos, dz, s, amax_out, hv, partial);
+}
+
+__global__ void relu_sign_bits_kernel(int64_t M, int32_t N, const float* __restrict__ C, int64_t ldc,
+                                      uint32_t* __restrict__ pos) {
+    const int32_t W = (N + 31) >> 5;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M * W; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / W;
+        const int32_t w = static_cast<int32_t>(i - r * W);
+        uint32_t b = 0;
+        for (int q = 0; q < 32 && 32 * w + q < N; ++q) b |= (C[r * ldc + 32 * w + q] > 0.f ? 1u : 0u) << q;
+        pos[i] = b;
+    }
+}
+void relu_sign_bits(int64_t M, int32_t N, const float* C, int64_t ldc, uint32_t* pos, cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    relu_sign_bits_kernel<<<grid_for(M * ((N + 31) / 32), 256), 256, 0, s>>>(M, N, C, ldc, pos);
+    SC_LAUNCH_CHECK();
+    count_launch();
 }
 
 void build_heavy_rows(sc_ctx* ctx, int64_t n, const int64_t* off, HeavyRows& hv) {

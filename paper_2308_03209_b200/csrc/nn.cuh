@@ -73,10 +73,14 @@ void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* mask_bits, fl
 void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
               const float* inv, const float* msg, float* mean, cudaStream_t s, const HeavyRows* hv = nullptr,
               float* partial = nullptr);
-// dz[u] = 1[msg[u] > 0] * sum_{v in CSR(u), kept} dmean_s[v]   (nn.hpp:277-288, pull form)
+// dz[u] = 1[msg[u] > 0] * sum_{v in CSR(u), kept} dmean_s[v]   (nn.hpp:277-288, pull form).
+// relu_pos (compact activations): the ReLU decisions as sign bits, [n][ceil(H / 32)]
+// words (bit c % 32 of word c / 32), read instead of the msg rows (msg may be null).
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
               const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out = nullptr,
-              const HeavyRows* hv = nullptr, float* partial = nullptr);
+              const HeavyRows* hv = nullptr, float* partial = nullptr, const uint32_t* relu_pos = nullptr);
+// pos[r][w] bit q = C[r][32 w + q] > 0 (for GEMM paths whose epilogue does not emit the bits).
+void relu_sign_bits(int64_t M, int32_t N, const float* C, int64_t ldc, uint32_t* pos, cudaStream_t s);
 // CSR-slot bitmap of a local-edge-indexed byte mask: bit k = mask[eids[k]].
 void mask_to_bits(int64_t nnz, const int32_t* eids, const uint8_t* mask, uint32_t* bits, cudaStream_t s);
 

@@ -238,6 +238,18 @@ void trainer_init(sc_trainer* t) {
     t->red_partial.alloc(1024);
     if (t->shared_x0) t->x0_shared.alloc(std::max<int64_t>(n_max * t->dp, 1));
     if (t->shared_logits) t->logits_shared.alloc(std::max<int64_t>(n_max * t->Cp, 1));
+    {  // compact activations when the full per-layer set would not leave headroom
+        const char* e = std::getenv("SC_COMPACT_ACTS");
+        t->compact = false;
+        if (e) {
+            t->compact = std::atoi(e) != 0;
+        } else {
+            size_t free_b = 0, total_b = 0;
+            SC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            const double full = 4.0 * static_cast<double>(carve_train(t, nullptr, n_max));
+            t->compact = full > 0.85 * static_cast<double>(free_b) - 2e9;
+        }
+    }
     ensure_rows(t, n_max);
     int64_t max_seg = 0;
     for (int i : t->local) max_seg = std::max<int64_t>(max_seg, t->ps[i].heavy.nseg);
@@ -291,31 +303,54 @@ void loss_weights(sc_trainer* t, int i) {
     count_launch();
 }
 
+namespace {
+// 256-byte-aligned sub-buffers of one allocation (base null: sizing pass).
+struct Carver {
+    float* base = nullptr;
+    size_t off = 0;
+    float* take(size_t floats) {
+        float* p = base ? base + off : nullptr;
+        off += (std::max<size_t>(floats, 1) + 63) / 64 * 64;
+        return p;
+    }
+};
+int32_t max_hidden(const sc_trainer* t) {
+    int32_t h = std::max<int32_t>(t->E, 1);
+    for (auto& lo : t->lay) h = std::max(h, lo.H);
+    return h;
+}
+}  // namespace
+
+size_t carve_train(sc_trainer* t, float* base, int64_t n) {
+    Carver c{base};
+    const int32_t maxH = max_hidden(t);
+    int32_t maxW = std::max<int32_t>(std::max(t->E, t->d), maxH);
+    for (auto& lo : t->lay) maxW = std::max(maxW, std::max(lo.H, lo.in));
+    t->X.assign(t->L + 1, nullptr);
+    t->MSG.assign(t->L, nullptr);
+    t->MEAN.assign(t->L, nullptr);
+    t->POS.assign(t->L, nullptr);
+    for (int l = 0; l < t->L; ++l) t->X[l + 1] = c.take(size_t(n) * t->lay[l].H);
+    float* shared_msg = t->compact && t->L > 0 ? c.take(size_t(n) * maxH) : nullptr;
+    for (int l = 0; l < t->L; ++l) {
+        t->MSG[l] = t->compact ? shared_msg : c.take(size_t(n) * t->lay[l].H);
+        t->MEAN[l] = c.take(size_t(n) * t->lay[l].H);
+        if (t->compact) t->POS[l] = reinterpret_cast<uint32_t*>(c.take(size_t(n) * ((t->lay[l].H + 31) / 32)));
+    }
+    t->inv = c.take(n);
+    t->G = c.take(size_t(n) * t->Cp);
+    t->dh = c.take(size_t(n) * maxW);
+    t->dmean = c.take(size_t(n) * maxW);  // also the dh ping-pong partner (backward)
+    t->dz = c.take(size_t(n) * maxH);
+    return c.off;
+}
+
 void ensure_rows(sc_trainer* t, int64_t n) {
     if (n <= t->rows_cap) return;
     t->rows_cap = n;
-    int32_t maxH = std::max<int32_t>(t->E, 1), maxW = std::max<int32_t>(t->E, t->d);
-    for (auto& lo : t->lay) {
-        maxH = std::max(maxH, lo.H);
-        maxW = std::max(maxW, std::max(lo.H, lo.in));
-    }
-    t->X.clear();
-    t->MSG.clear();
-    t->MEAN.clear();
-    t->X.resize(t->L + 1);
-    t->MSG.resize(t->L);
-    t->MEAN.resize(t->L);
-    for (int l = 0; l < t->L; ++l) {
-        t->X[l + 1].alloc(n * t->lay[l].H);
-        t->MSG[l].alloc(n * t->lay[l].H);
-        t->MEAN[l].alloc(n * t->lay[l].H);
-    }
-    t->inv.alloc(n);
-    t->G.alloc(n * t->Cp);
-    t->dh.alloc(n * maxW);
-    t->dh2.alloc(n * maxW);
-    t->dmean.alloc(n * maxH);
-    t->dz.alloc(n * maxH);
+    const size_t need = carve_train(t, nullptr, n);
+    t->arena.ensure(need);
+    carve_train(t, t->arena.get(), n);
     t->row_loss.alloc(n);
     t->eval_logits.release();
 }
@@ -350,17 +385,16 @@ double spmm_bytes(const Rows& R, int H, bool bwd) {
 // evaluation may alias them (ping-pong X, one MSG, one MEAN).
 struct Acts {
     std::vector<float*> X, MSG, MEAN;
+    std::vector<uint32_t*> POS;  // ReLU sign bits of MSG[l] (compact training), else null
     float* inv = nullptr;
 };
 Acts train_acts(sc_trainer* t) {
     Acts a;
-    a.X.assign(t->L + 1, nullptr);
-    for (int l = 1; l <= t->L; ++l) a.X[l] = t->X[l].get();
-    for (int l = 0; l < t->L; ++l) {
-        a.MSG.push_back(t->MSG[l].get());
-        a.MEAN.push_back(t->MEAN[l].get());
-    }
-    a.inv = t->inv.get();
+    a.X = t->X;
+    a.MSG = t->MSG;
+    a.MEAN = t->MEAN;
+    a.POS = t->POS;
+    a.inv = t->inv;
     return a;
 }
 
@@ -380,7 +414,7 @@ void forward(sc_trainer* t, const Rows& R, float* logits, const Acts& A) {
         // msg = relu(h W^T)   (nn.hpp:220-221)
         P.begin("gemm_msg", 4.0 * n * (lo.in + lo.H), s, 2.0 * n * lo.in * lo.H);
         t->tc.nt(t, xin, xin_amax, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, nullptr,
-                 A.MSG[l], lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l));
+                 A.MSG[l], lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l), A.POS.empty() ? nullptr : A.POS[l]);
         P.end(s);
         // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
         P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
@@ -421,18 +455,20 @@ void backward(sc_trainer* t, const Rows& R, int i) {
     Profiler& P = t->prof;
     const int64_t n = R.n;
     const MatT x0t{R.x0, R.x0_ld, nullptr, t->d};
-    const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L].get(), t->E, nullptr, t->E};
+    const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L], t->E, nullptr, t->E};
     // head grad = G^T emb (side) ; dh = G head (main)   (:259-260)
     hand_off(s, w);
     P.begin("wgrad", 4.0 * n * (t->C + t->E), w, 2.0 * n * t->C * t->E);
     const float* x0_amax = t->g->feat_amax.get();
     const float* emb_amax = t->L == 0 ? x0_amax : t->amax_x(t->L);
-    t->tc.tn(t, MatT{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
+    t->tc.tn(t, MatT{t->G, t->Cp, nullptr, t->C}, R.g_amax, embt, emb_amax, nullptr, nullptr, n,
              t->slot_ptr(2 * t->L, i), t->E, w, ws_w);
     P.end(w);
     exchange_bucket(t, 2 * t->L, round, w);
-    float* dh = t->dh.get();
-    float* dh2 = t->dh2.get();
+    // dh ping-pongs with dmean's buffer: each layer's dmean (dh2 below) is dead once the
+    // transposed aggregation has read it, and the next dh is written there.
+    float* dh = t->dh;
+    float* dh2 = t->dmean;
     float* dh_amax = t->amax_slot(sc_trainer::kSlotDh0);
     float* dh2_amax = t->amax_slot(sc_trainer::kSlotDh1);
     if (t->L == 0) {
@@ -440,25 +476,25 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         return;
     }
     P.begin("gemm_dgrad", 4.0 * n * (t->C + t->E), s, 2.0 * n * t->C * t->E);
-    t->tc.nt(t, MatA{t->G.get(), t->Cp, nullptr, t->C}, R.g_amax, MatB{t->theta.get() + t->head_off, t->E, true},
+    t->tc.nt(t, MatA{t->G, t->Cp, nullptr, t->C}, R.g_amax, MatB{t->theta.get() + t->head_off, t->E, true},
              nullptr, nullptr, nullptr, dh, t->E, n, t->E, kEpiNone, nullptr, dh_amax);
     P.end(s);
     for (int l = t->L - 1; l >= 0; --l) {
         const LayerOff& lo = t->lay[l];
-        const MatT xint = l == 0 ? x0t : MatT{t->X[l].get(), lo.in, nullptr, lo.in};
+        const MatT xint = l == 0 ? x0t : MatT{t->X[l], lo.in, nullptr, lo.in};
         const MatT dht{dh, lo.H, nullptr, lo.H};
-        const MatT meant{t->MEAN[l].get(), lo.H, nullptr, lo.H};
+        const MatT meant{t->MEAN[l], lo.H, nullptr, lo.H};
         const float* xin_amax = l == 0 ? x0_amax : t->amax_x(l);
         // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
         P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s, 2.0 * n * lo.H * lo.H);
         t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr,
-                 nullptr, nullptr, t->dmean.get(), lo.H, n, lo.H, kEpiRowScale, t->inv.get(), nullptr);
+                 nullptr, nullptr, dh2, lo.H, n, lo.H, kEpiRowScale, t->inv, nullptr);
         P.end(s);
         // One launch for dU = dh^T [mean | h_in] (:271-272) and dW = dz^T h_in (:289) after the
         // transposed aggregation, so h_in (and the tiles' conversions) stream once for both;
         // otherwise dU runs first (optionally on the side stream) and dW after.
         float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
-        const MatT dzt{t->dz.get(), lo.H, nullptr, lo.H};
+        const MatT dzt{t->dz, lo.H, nullptr, lo.H};
         const bool dual = !t->overlap && t->tc.enabled && t->tc.dual && tn_dual_supported(dht, dzt, meant, xint);
         if (!dual) {
             hand_off(s, w);
@@ -471,8 +507,8 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
         SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
         P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
-        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, t->dmean.get(), t->MSG[l].get(), t->dz.get(), s, dz_amax, R.hv,
-                 t->heavy_ws.get());
+        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, dh2, t->compact ? nullptr : t->MSG[l], t->dz, s, dz_amax, R.hv,
+                 t->heavy_ws.get(), t->POS[l]);
         P.end(s);
         if (dual) {
             P.begin("wgrad", 4.0 * n * (3 * lo.H + lo.in), s, 2.0 * n * lo.H * (lo.H + 2 * lo.in));
@@ -489,7 +525,7 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         }
         exchange_bucket(t, 2 * l, round);
         if (l > 0) {  // dh = dh U_R + dz W   (:275, :290); layer 0's is unused
-            const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz.get(), lo.H, nullptr, lo.H};
+            const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz, lo.H, nullptr, lo.H};
             P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s, 2.0 * n * 2 * lo.H * lo.in);
             const MatB wB{t->theta.get() + lo.W, lo.in, true};
             SC_CUDA(cudaMemsetAsync(dh2_amax, 0, sizeof(float), s));
@@ -534,10 +570,10 @@ void run_partition(sc_trainer* t, int i, int epoch) {
     t->prof.begin("loss", double(st.n) * (8.0 * t->C + 24), s);
     if (t->loss == 0)
         softmax_ce(st.n, t->C, t->Cp, logits, t->g->labels.get(), pd.nodes.get(), st.w.get(), st.scale.get(),
-                   t->G.get(), t->row_loss.get(), s);
+                   t->G, t->row_loss.get(), s);
     else
         bce(st.n, t->C, t->Cp, logits, t->g->labels.get(), t->g->multilabel ? t->g->targets.get() : nullptr,
-            pd.nodes.get(), st.w.get(), st.scale.get(), t->G.get(), t->row_loss.get(), s);
+            pd.nodes.get(), st.w.get(), st.scale.get(), t->G, t->row_loss.get(), s);
     sum_f64(st.n, t->row_loss.get(), t->red_partial.get(), t->part_loss.get() + i, t->normalizer, s);
     t->prof.end(s);
     exchange_bucket(t, -1, i / t->world);
@@ -657,19 +693,29 @@ void eval_forward(sc_trainer* t) {
         t->eval_heavy_built = true;
         if (size_t(t->eval_heavy.nseg) * maxH > t->heavy_ws.size()) t->heavy_ws.alloc(size_t(t->eval_heavy.nseg) * maxH);
     }
+    // Forward-only set carved from the training arena (the step is complete, its cache is
+    // dead): ping-pong layer outputs, one msg, one mean, inv. The arena grows if n needs more.
     Acts A;
-    if (!t->eval_only && n <= t->rows_cap) {
-        A = train_acts(t);  // the step is complete: its cache is free to overwrite
-    } else {
-        for (auto& b : t->ev_x) b.ensure(std::max<int64_t>(n * maxH, 1));
-        t->ev_msg.ensure(std::max<int64_t>(n * maxH, 1));
-        t->ev_mean.ensure(std::max<int64_t>(n * maxH, 1));
-        t->ev_inv.ensure(std::max<int64_t>(n, 1));
-        A.X.assign(t->L + 1, nullptr);
-        for (int l = 1; l <= t->L; ++l) A.X[l] = t->ev_x[l & 1].get();
-        A.MSG.assign(t->L, t->ev_msg.get());
-        A.MEAN.assign(t->L, t->ev_mean.get());
-        A.inv = t->ev_inv.get();
+    {
+        auto carve_eval = [&](float* base) {
+            Carver c{base};
+            float* x[2] = {c.take(size_t(n) * maxH), c.take(size_t(n) * maxH)};
+            float* msg = c.take(size_t(n) * maxH);
+            float* mean = c.take(size_t(n) * maxH);
+            A.X.assign(t->L + 1, nullptr);
+            for (int l = 1; l <= t->L; ++l) A.X[l] = x[l & 1];
+            A.MSG.assign(t->L, msg);
+            A.MEAN.assign(t->L, mean);
+            A.inv = c.take(n);
+            return c.off;
+        };
+        const size_t need = carve_eval(nullptr);
+        if (t->arena.size() < need) {
+            SC_CUDA(cudaStreamSynchronize(s));  // nothing in flight reads the old arena
+            t->arena.alloc(need);
+            if (t->rows_cap > 0) carve_train(t, t->arena.get(), t->rows_cap);
+        }
+        carve_eval(t->arena.get());
     }
     // layer-0 rows: the features themselves, or a 16-byte-row copy so the GEMMs stay on TMA
     const float* x0 = g->features.get();

@@ -96,19 +96,25 @@ struct sc_trainer {
     // partitions
     std::vector<int> local;
     std::vector<sc::PartState> ps;
-    // activations (rows_cap rows)
+    // Per-row activation / gradient buffers (rows_cap rows), carved from ONE arena
+    // (carve_train): X[l] (l >= 1), MSG[l], MEAN[l], inv, G, dh, dmean, dz. The
+    // backward's dh ping-pong reuses dmean's buffer (dmean is dead once the
+    // transposed aggregation has read it). Full-graph evaluation carves its
+    // forward-only set (two ping-pong layer outputs, one msg, one mean, inv) from
+    // the same arena, growing it if needed, so the two never hold memory at once.
+    // compact (large graphs, or SC_COMPACT_ACTS=1): one msg buffer shared by every
+    // layer plus the ReLU decisions as sign bits POS[l] ([rows][ceil(H/32)] words,
+    // written by the msg GEMM's epilogue) for the backward.
     int64_t rows_cap = 0;
-    std::vector<sc::DevBuf<float>> X, MSG, MEAN;
-    sc::DevBuf<float> inv, G, dh, dh2, dmean, dz, eval_logits, ws, ws_side;
+    bool compact = false;
+    sc::DevBuf<float> arena;
+    std::vector<float*> X, MSG, MEAN;
+    std::vector<uint32_t*> POS;
+    float *inv = nullptr, *G = nullptr, *dh = nullptr, *dmean = nullptr, *dz = nullptr;
+    sc::DevBuf<float> eval_logits, ws, ws_side;
     sc::DevBuf<float> heavy_ws;   // segment partial sums of the heavy-row aggregation
     sc::HeavyRows eval_heavy;     // heavy rows of the full graph (evaluate_splits)
     bool eval_heavy_built = false;
-    // Full-graph evaluation reuses the training activations when they hold at
-    // least n rows (rows_cap >= n, e.g. products at p = 8); otherwise it runs on
-    // its own forward-only set: two ping-pong layer outputs, one message and one
-    // mean buffer, so a partition trainer never grows every training buffer to
-    // the full graph.
-    sc::DevBuf<float> ev_x[2], ev_msg, ev_mean, ev_inv;
     sc::DevBuf<float> eval_x0;  // the full feature matrix with 16-byte rows (d % 4 != 0)
     uint64_t eval_x0_version = 0;
     bool eval_only = false;     // sc_evaluate's forward-only engine (no partitions, no optimizer)
@@ -174,6 +180,8 @@ namespace sc {
 void trainer_init(sc_trainer* t);
 void loss_weights(sc_trainer* t, int i);
 void ensure_rows(sc_trainer* t, int64_t n);
+// Lay the training buffers for `rows` rows out from base (null: sizing pass); returns floats used.
+size_t carve_train(sc_trainer* t, float* base, int64_t rows);
 void run_partition(sc_trainer* t, int i, int epoch);
 void trainer_step_async(sc_trainer* t, int epoch);
 void trainer_finish(sc_trainer* t, double* loss, double* gnorm);

@@ -146,6 +146,7 @@ _sig("sc_trainer_evaluate_mask", [_vp, _vp, C.POINTER(_f64)])
 _sig("sc_evaluate", [_vp, _vp, _vp, _vp, _i32, _vp, C.POINTER(_f64)])
 _sig("sc_trainer_comm_audit", [_vp, C.POINTER(_u64), C.POINTER(_u64)])
 _sig("sc_trainer_fallback_count", [_vp, C.POINTER(_i64)])
+_sig("sc_trainer_memory_mode", [_vp, C.POINTER(C.c_int32), C.POINTER(_i64)])
 _sig("sc_comm_volume", [_i32, _i32, _u64, _u64, _u64, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)])
 _sig("sc_expected_rf_random", [_i32, _i64, C.POINTER(_f64)])
 _sig("sc_imbalance_lower_bound", [_i32, _i64, _i64, C.POINTER(_f64)])
@@ -930,6 +931,13 @@ class CoFreeTrainer:
         x = _i64()
         _check(_lib.sc_trainer_fallback_count(self.h, C.byref(x)))
         return x.value
+
+    def memory_mode(self) -> dict:
+        """Device memory layout the trainer chose for this graph (compact activations, shared caches)."""
+        f, b = C.c_int32(), _i64()
+        _check(_lib.sc_trainer_memory_mode(self.h, C.byref(f), C.byref(b)))
+        return {"compact_activations": bool(f.value & 1), "shared_x0": bool(f.value & 2),
+                "shared_logits": bool(f.value & 4), "arena_gb": round(b.value / 1e9, 2)}
 
     def debug_buffer(self, name: str, layer: int, dst_ptr: int, nbytes: int):
         """Device-to-device copy of a trainer activation buffer (the last local partition's cache)."""

@@ -39,3 +39,34 @@ def test_shared_buffers_same_bits():
     np.testing.assert_array_equal(a.part_logits(5), b.part_logits(5))  # the last trained partition
     with pytest.raises(ValueError, match="not kept"):
         b.part_logits(0)
+
+
+@pytest.mark.parametrize("hidden", [[64, 64, 64], [40, 40]])
+def test_compact_activations_same_bits(hidden):
+    """Compact activations (SC_COMPACT_ACTS=1, chosen automatically when the per-layer set would
+    not fit, e.g. R-MAT 20M / 1B at p = 16): one msg buffer shared by the layers and the ReLU
+    decisions kept as sign bits for the transposed aggregation. The decision bit is the same
+    comparison the msg row gives, so every step, gradient and eval metric is bitwise the same."""
+    from paper_2308_03209_b200 import sagecut as sc
+    og = oracle().graph_sbm(300, 4, 0.15, 0.01, 8, 0.3, 7)
+    out = []
+    for compact in ("0", "1"):
+        old = os.environ.get("SC_COMPACT_ACTS")
+        os.environ["SC_COMPACT_ACTS"] = compact
+        try:
+            g = gpu_graph(sc, og, 8)
+            part = sc.partition_random(g, 4, 3)
+            t = sc.CoFreeTrainer(g, part, sc.TrainConfig(layers=len(hidden), hidden=hidden, use_dropedge=True,
+                                                         seed=1))
+            steps = [t.step(e) for e in range(3)]
+            out.append((steps, t.params(), t.grads(), t.evaluate()))
+        finally:
+            if old is None:
+                os.environ.pop("SC_COMPACT_ACTS", None)
+            else:
+                os.environ["SC_COMPACT_ACTS"] = old
+    (sa, pa, ga, ea), (sb, pb, gb, eb) = out
+    assert sa == sb
+    np.testing.assert_array_equal(pa, pb)
+    np.testing.assert_array_equal(ga, gb)
+    assert ea == eb
