@@ -9,7 +9,8 @@
 //
 // Differences from the reference, by design:
 //   * Graph holds a device handle (features fp32 row-major, no Eigen);
-//   * precision is always f32 (the reference's Precision::f32 path);
+//   * precision is always f32 (the reference's Precision::f32 path); TrainConfig::precision
+//     defaults to f32 here and f64 is rejected with std::invalid_argument;
 //   * train_cofree's per-epoch evaluation is optional (TrainConfig::evaluate).
 // Errors: the reference's exception types and message texts are rethrown
 // (std::invalid_argument, std::runtime_error, std::logic_error).
@@ -428,6 +429,8 @@ inline int select_mask(std::uint64_t seed, std::uint64_t part, std::uint64_t epo
 
 enum class LossKind { softmax_ce, bce };  // nn.hpp:296
 
+enum class Precision { f64, f32 };  // trainer.hpp:18
+
 struct TrainConfig {  // trainer.hpp:20-33
     int layers = 2;
     std::vector<int> hidden = {32};
@@ -439,6 +442,11 @@ struct TrainConfig {  // trainer.hpp:20-33
     int dropedge_k = 10;
     double drop_ratio = 0.5;
     std::uint64_t seed = 0;
+    // The device path computes in f32 (the reference's Precision::f32 arithmetic: f32 features,
+    // model and Adam; f64 loss, weights and grad-norm). The reference defaults to f64, which
+    // this library rejects rather than silently narrowing (train_cofree throws).
+    Precision precision = Precision::f32;
+    int workers = 1;            // accepted for source compatibility: results never depend on it
     bool evaluate = true;       // per-epoch full-graph metrics (trainer.hpp:306)
     bool deterministic = true;  // ascending-partition gradient sum
 };
@@ -535,6 +543,9 @@ inline void save_edge_cut(const Graph& g, const EdgeCutPartition& ec, const std:
 // multi-GPU run create one sc_trainer per rank through the C ABI.
 inline TrainResult train_cofree(const Graph& g, const VertexCutPartition& part, const TrainConfig& c) {
     if (c.epochs < 0) throw std::invalid_argument("epochs must be >= 0");
+    if (c.precision != Precision::f32)
+        throw std::invalid_argument("sagecut_b200 trains in Precision::f32 only (set TrainConfig::precision)");
+    if (c.workers < 1) throw std::invalid_argument("workers must be >= 1");  // trainer.cpp:25
     const std::vector<int> hidden = resolved_hidden_dims(c);
     sc_train_config cfg{};
     cfg.layers = static_cast<std::int32_t>(hidden.size());

@@ -67,7 +67,7 @@ struct TcGemm {
     // GEMMs that ran on the fp32 SIMT kernels although the tensor-core path was
     // enabled (operand layout not TMA-compatible): counted, never silent.
     int64_t simt_fallbacks = 0;
-    bool dual = true;  // one launch for a layer's dU and dW where shapes allow (SC_TN_DUAL=0: two)
+    bool dual = false;  // one launch for a layer's dU and dW where shapes allow (SC_TN_DUAL=1; default: two)
     void init(sc_trainer* t);
     void invalidate() { ++version; }
     const BImage& image(const MatB& b, int32_t N, int32_t K, cudaStream_t s);

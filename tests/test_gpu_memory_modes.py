@@ -70,3 +70,28 @@ def test_compact_activations_same_bits(hidden):
     np.testing.assert_array_equal(pa, pb)
     np.testing.assert_array_equal(ga, gb)
     assert ea == eb
+
+
+def test_tn_dual_launch_matches_two_launches():
+    """SC_TN_DUAL=1 (opt-in): a layer's dU and dW in one split-K launch over A = [dh | dz]. Same
+    products, different split-K partition of the rows, so gradients agree to fp32 rounding."""
+    from paper_2308_03209_b200 import sagecut as sc
+    og = oracle().graph_sbm(300, 4, 0.15, 0.01, 8, 0.3, 7)
+    out = []
+    for dual in ("0", "1"):
+        old = os.environ.get("SC_TN_DUAL")
+        os.environ["SC_TN_DUAL"] = dual
+        try:
+            # TcGemm reads SC_TN_DUAL when the trainer is created
+            g = gpu_graph(sc, og, 8)
+            part = sc.partition_random(g, 2, 3)
+            t = sc.CoFreeTrainer(g, part, sc.TrainConfig(layers=2, hidden=[256, 256], use_dropedge=True, seed=1))
+            t.step(0)
+            out.append(t.grads())
+        finally:
+            if old is None:
+                os.environ.pop("SC_TN_DUAL", None)
+            else:
+                os.environ["SC_TN_DUAL"] = old
+    a, b = out
+    assert np.linalg.norm(a - b) <= 2e-6 * np.linalg.norm(a)

@@ -44,8 +44,12 @@ def main():
             continue
         d = per.setdefault(r[ii], {"name": r[ki]})
         d[r[mi]] = float(r[vi].replace(",", ""))
-    fwd = [d for d in per.values() if "false" in d["name"]]
-    bwd = [d for d in per.values() if "true" in d["name"]]
+    def backward(name):  # spmm_kernel<NCH, kBwd>: ncu prints the bool as 0/1 (or false/true)
+        last = name.split("(")[0].rstrip().rstrip(">").split(",")[-1].strip()
+        return last in ("1", "true")
+
+    fwd = [d for d in per.values() if not backward(d["name"])]
+    bwd = [d for d in per.values() if backward(d["name"])]
 
     def avg(ds):
         return sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in ds) / len(ds) if ds else None
