@@ -689,6 +689,254 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
     }
 }
 
+// ---- NT, single source, K <= 256: A' in TMEM, weight image resident in shared memory -----------
+// The general NT kernel above is shared-memory-bandwidth bound: per 32-k stage a CTA writes the
+// fp32 staging (TMA) and reads it (converters), writes the fp16 hi / lo A tiles and the stage's
+// weight-image rows (TMA), and the tensor core reads A and B three times — ~146 B/clk at full MMA
+// rate against the SM's 128 B/clk. Here, for one source with K <= 256 (msg, dmean, head and head
+// dgrad GEMMs):
+//   * the whole weight image (this CTA's B' rows, every k-block, hi + lo: <= 128 KB) is loaded
+//     into shared memory once per launch and stays there;
+//   * the converters write A' (the tile's 128 rows x K, hi / lo) into TMEM with tcgen05.st
+//     (lane = row, two fp16 per column), and the MMAs read A from TMEM;
+// leaving the staging write + read and the B' operand reads: ~73 B/clk at full MMA rate.
+// TMEM: A' for the whole K (kblocks x 32 columns, <= 256) + two accumulators of Np columns.
+// N > 128 runs as two passes of Np = n_pad / 2 over the same A' (accumulator h), so the second
+// pass's MMAs overlap the first pass's epilogue; N <= 128: one pass, accumulators alternate by tile.
+// A' stage kb is released for the next tile after the tile's last pass has read it.
+struct NtTmCfg {
+    static constexpr int kCW = 8;                       // converter warps
+    static constexpr int kMma = kCW + kNtEpiWarps, kLoad = kMma + 1, kThr = (kLoad + 1) * 32;
+    static constexpr int kStg = 4;                      // fp32 staging slots
+    static constexpr int kMaxKb = 8;                    // K <= 256
+    static constexpr int kBOff = 0;                     // resident B' (<= kMaxKb x n_pad x 64 B per CTA)
+    static constexpr int kBBytes = kMaxKb * kMaxN * 64 / 2;
+    static constexpr int kStgOff = kBOff + kBBytes;
+    static constexpr int kEpiOff = kStgOff + kStg * kNtStgBytes;
+    static constexpr int kBarOff = kEpiOff + kNtEpiBytes;
+    static constexpr int kSmem = kBarOff + 256 + 1024;
+    static constexpr int kRows = 2 * kBM;
+};
+static_assert(NtTmCfg::kSmem <= 232448, "NT (A in TMEM) shared memory");
+
+template <int EPI, bool AMAX>
+__global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __grid_constant__ Params p) {
+    using Cfg = NtTmCfg;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* bres = smem + Cfg::kBOff;
+    uint8_t* stg_base = smem + Cfg::kStgOff;
+    uint8_t* epi_base = smem + Cfg::kEpiOff;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
+    uint64_t* full = bars;                       // [kMaxKb] converters -> MMA (leader's)
+    uint64_t* empty = full + Cfg::kMaxKb;        // [kMaxKb] MMA -> converters
+    uint64_t* sfull = empty + Cfg::kMaxKb;       // [kStg] loader (tx) -> converters
+    uint64_t* sempty = sfull + Cfg::kStg;        // [kStg] converters -> loader
+    uint64_t* tfull = sempty + Cfg::kStg;        // [2] MMA -> epilogue
+    uint64_t* tempty = tfull + 2;                // [2] epilogue -> MMA (leader's)
+    uint64_t* bready = tempty + 2;               // resident B' landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int64_t tile0 = blockIdx.x >> 1, tstep = gridDim.x >> 1;
+    const Src& S = p.src[0];
+    const int kbl = S.kblocks;                                  // <= kMaxKb
+    const int np = p.n_pad > kBM ? 2 : 1;                       // passes
+    const int Np = p.n_pad / np;                                // MMA N (multiple of 32)
+    const uint32_t bt = static_cast<uint32_t>(Np / 2) * 64u;    // one resident (pass, kb, plane) tile
+    const int kt = scale_exp(*S.amax_a) + *S.bexp;
+    const float sa = ldexpf(1.f, kt - *S.bexp);
+
+    if (warp == Cfg::kMma) {
+        if (lane == 0) {
+            for (int s = 0; s < Cfg::kMaxKb; ++s) {
+                mbar_init(&full[s], Cfg::kCW * 2);
+                mbar_init(&empty[s], 1);
+            }
+            for (int s = 0; s < Cfg::kStg; ++s) {
+                mbar_init(&sfull[s], 1);
+                mbar_init(&sempty[s], Cfg::kCW);
+            }
+            for (int s = 0; s < 2; ++s) {
+                mbar_init(&tfull[s], 1);
+                mbar_init(&tempty[s], kNtEpiWarps * 2);
+            }
+            mbar_init(bready, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        tmem_alloc_g<true>(tmem_slot);
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t full_l = mapa(smem_u32(full), 0);
+    const uint32_t tempty_l = mapa(smem_u32(tempty), 0);
+
+    if (warp == Cfg::kLoad) {
+        if (lane == 0) {
+            // resident B': for pass h, k-block kb, plane q, this CTA's Np / 2 rows of the image
+            // (image rows [kb][q][n_pad]; pass h covers columns h Np .. h Np + Np - 1, split by rank).
+            // Both CTAs' bytes are counted on the leader's barrier (its MMAs read both halves).
+            if (rank == 0) mbar_arrive_expect_tx(bready, 2u * static_cast<uint32_t>(np * kbl * 2) * bt);
+            const uint32_t bready_l = mapa(smem_u32(bready), 0);
+            for (int h = 0; h < np; ++h)
+                for (int kb = 0; kb < kbl; ++kb)
+                    for (int q = 0; q < 2; ++q)
+                        tma_load_2d_pair(bres + ((h * kbl + kb) * 2 + q) * bt, &S.tmap_b, 0,
+                                         (kb * 2 + q) * p.n_pad + h * Np + static_cast<int32_t>(rank) * (Np / 2),
+                                         bready_l);
+        }
+        __syncwarp();
+        Ring ring;
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
+            for (int kb = 0; kb < kbl; ++kb, ring.next(Cfg::kStg)) {
+                mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&sfull[ring.idx], kNtStgBytes);
+                    tma_load_2d(stg_base + ring.idx * kNtStgBytes, &S.tmap, kb * kNtBK,
+                                static_cast<int32_t>(tile * Cfg::kRows + rank * kBM), &sfull[ring.idx]);
+                }
+                __syncwarp();
+            }
+    } else if (warp < Cfg::kCW) {
+        // converters: warp w owns TMEM lane quarter q = w & 3 (rows 32q + lane) and k half kh = w >> 2
+        // of each 32-k stage: 16 fp32 of its row (4 x LDS.128 from the SW128 staging) -> 8 hi + 8 lo
+        // columns of A' stage kb (hi at column 32 kb + 8 kh, lo 16 columns further).
+        const int q = warp & 3, kh = warp >> 2;
+        const int r = 32 * q + lane;
+        Ring sr;
+        uint32_t t = 0;
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t)
+            for (int kb = 0; kb < kbl; ++kb, sr.next(Cfg::kStg)) {
+                mbar_wait(&empty[kb], (t & 1) ^ 1);  // the previous tile's last pass has read stage kb
+                mbar_wait(&sfull[sr.idx], sr.phase);
+                const uint8_t* rowp = stg_base + sr.idx * kNtStgBytes + r * (kNtBK * 4);
+                float4 x[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    x[c] = *reinterpret_cast<const float4*>(rowp + (((4 * kh + c) ^ (r & 7)) << 4));
+                uint32_t hi[8], lo[8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    split2(x[c].x, x[c].y, sa, hi[2 * c], lo[2 * c]);
+                    split2(x[c].z, x[c].w, sa, hi[2 * c + 1], lo[2 * c + 1]);
+                }
+                tc_fence_after();  // orders the stores after the MMAs that read this stage last
+                const uint32_t tcol = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + kb * 32 + 8 * kh;
+                tmem_st8(tcol, hi);
+                tmem_st8(tcol + 16, lo);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_cluster(full_l + kb * 8);
+                    mbar_arrive(&sempty[sr.idx]);
+                }
+            }
+    } else if (warp == Cfg::kMma) {
+        if (rank == 0) {
+            mbar_wait(bready, 0);
+            const uint32_t idesc = idesc_f16(Cfg::kRows, Np);
+            uint32_t t = 0;
+            for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t)
+                for (int h = 0; h < np; ++h) {
+                    const uint32_t u = t * np + h, acc = u & 1;
+                    mbar_wait_cluster(&tempty[acc], ((u >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + 256 + acc * Np;
+                    for (int kb = 0; kb < kbl; ++kb) {
+                        if (h == 0) {
+                            mbar_wait_cluster(&full[kb], t & 1);
+                            tc_fence_after();
+                        }
+                        if (lane == 0) {
+                            const uint8_t* bt0 = bres + ((h * kbl + kb) * 2) * bt;
+                            const uint64_t bhi = desc_sw64(smem_u32(bt0)), blo = desc_sw64(smem_u32(bt0 + bt));
+#pragma unroll
+                            for (int k = 0; k < kNtBK / 16; ++k) {
+                                const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;
+                                const uint32_t tah = tmem_base + kb * 32 + k * 8;  // lo plane 16 columns after hi
+                                mma_f16_ts_pair(d_tmem, tah, bhi + adv, idesc, (kb | k) ? 1u : 0u);
+                                mma_f16_ts_pair(d_tmem, tah, blo + adv, idesc, 1u);
+                                mma_f16_ts_pair(d_tmem, tah + 16, bhi + adv, idesc, 1u);
+                            }
+                            if (h == np - 1) mma_commit_g<true>(&empty[kb]);
+                            if (kb == kbl - 1) mma_commit_g<true>(&tfull[acc]);
+                        }
+                        __syncwarp();
+                    }
+                }
+        }
+    } else {
+        // epilogue (8 warps): as the general kernel, per pass: TMEM columns 256 + acc Np + c0 are output
+        // columns h Np + c0.
+        const int ew = warp & 3;
+        const int half = (warp - Cfg::kCW) >> 2;
+        const float unscale = ldexpf(1.f, -kt);
+        uint8_t* box = epi_base + (warp - Cfg::kCW) * kNtEpiBuf;
+        float amx = 0.f;
+        uint32_t t = 0;
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t) {
+            const int64_t row0 = tile * Cfg::kRows + rank * kBM + ew * 32;
+            float sc = 1.f;
+            if (EPI == kEpiRowScale && row0 + lane < p.M) sc = p.row_scale[row0 + lane];
+            for (int h = 0; h < np; ++h) {
+                const uint32_t u = t * np + h, acc = u & 1;
+                mbar_wait(&tfull[acc], (u >> 1) & 1);
+                tc_fence_after();
+                for (int c0 = half * 32; c0 < Np; c0 += 64) {
+                    uint32_t rr[32];
+                    tmem_ld32(tmem_base + 256 + acc * Np + (static_cast<uint32_t>(ew * 32) << 16) + c0, rr);
+                    if (lane == 0) bulk_wait_read<0>();
+                    __syncwarp();
+                    const int col = h * Np + c0;
+                    uint32_t pos = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float x[4];
+#pragma unroll
+                        for (int qq = 0; qq < 4; ++qq) {
+                            float v = __uint_as_float(rr[4 * j + qq]) * unscale;
+                            if (EPI == kEpiRelu) {
+                                v = fmaxf(v, 0.f);
+                                pos |= (v > 0.f ? 1u : 0u) << (4 * j + qq);
+                            }
+                            if (EPI == kEpiRowScale) v = sc * v;
+                            if (AMAX) amx = fmaxf(amx, fabsf(v));
+                            x[qq] = v;
+                        }
+                        *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                            make_float4(x[0], x[1], x[2], x[3]);
+                    }
+                    if (EPI == kEpiRelu && p.relu_pos && col < p.N && row0 + lane < p.M)
+                        p.relu_pos[(row0 + lane) * ((p.N + 31) >> 5) + (col >> 5)] = pos;
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0 && row0 < p.M) tma_store_2d(&p.tmap_c, box, col, static_cast<int32_t>(row0));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
+            }
+        }
+        if (lane == 0) bulk_wait_read<0>();
+        if (AMAX) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out), __float_as_uint(amx));
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == Cfg::kMma) {
+        tc_fence_after();
+        tmem_dealloc_g<true>(tmem_base);
+    }
+}
+
 // ---- B image prep (two grid-wide passes): |B| max -> exponent kB, then fp32 B
 // (NT [N x K] or NN [K x N]) * 2^kB split into per-k-block [hi tile | lo tile],
 // each n_pad rows x 32 k fp16 in the SW64 K-major layout.
@@ -1384,6 +1632,14 @@ void encode_img(CUtensorMap* map, const uint8_t* img, int64_t rows, uint32_t box
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (image) failed (" + std::to_string(int(r)) + ")");
 }
+// Single-source NT GEMMs with K <= 256 use the A'-in-TMEM kernel unless SC_NT_TM=0.
+bool nt_tm_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SC_NT_TM");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 // NT GEMMs run on CTA pairs (cta_group::2) unless SC_NT_PAIR=0.
 bool nt_pair_enabled() {
     static const bool on = [] {
@@ -1668,16 +1924,23 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
         p.trace = trace_buf.get();
     }
     const bool pair = nt_pair_enabled();
-    if (pair)
+    // single source, K <= 256: the A'-in-TMEM kernel with the weight image resident in shared memory
+    const bool tm = pair && nt_tm_enabled() && p.nsrc == 1 && b1.kblocks <= tc::NtTmCfg::kMaxKb &&
+                    (b1.n_pad <= tc::kBM || b1.n_pad % 64 == 0);
+    if (tm) {
+        const int np = b1.n_pad > tc::kBM ? 2 : 1;
+        encode_img(&p.src[0].tmap_b, b1.img.get(), int64_t(b1.kblocks) * 2 * b1.n_pad, b1.n_pad / np / 2);
+    } else if (pair) {
         for (int i = 0; i < p.nsrc; ++i)
             encode_img(&p.src[i].tmap_b, bs[i]->img.get(), int64_t(bs[i]->kblocks) * 2 * bs[i]->n_pad, bs[i]->n_pad / 2);
+    }
     const int64_t rows_per_tile = pair ? 2 * tc::kBM : tc::kBM;
     p.tiles = (M + rows_per_tile - 1) / rows_per_tile;
     auto launch = [&](auto kernel, int smem_bytes) {
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
         cudaLaunchConfig_t cfg{};
         cudaLaunchAttribute attr[1];
-        cfg.blockDim = dim3(pair ? tc::NtCfg<true>::kThr : tc::NtCfg<false>::kThr);
+        cfg.blockDim = dim3(tm ? tc::NtTmCfg::kThr : pair ? tc::NtCfg<true>::kThr : tc::NtCfg<false>::kThr);
         cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes);
         cfg.stream = s;
         if (pair) {
@@ -1697,7 +1960,8 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     auto dispatch = [&](auto epi_tag, auto amax_tag) {
         constexpr int E = decltype(epi_tag)::value;
         constexpr bool A = decltype(amax_tag)::value;
-        if (pair) launch(tc::gemm_f16x3_kernel<E, A, true>, tc::NtCfg<true>::kSmem);
+        if (tm) launch(tc::gemm_nt_tm_kernel<E, A>, tc::NtTmCfg::kSmem);
+        else if (pair) launch(tc::gemm_f16x3_kernel<E, A, true>, tc::NtCfg<true>::kSmem);
         else launch(tc::gemm_f16x3_kernel<E, A, false>, tc::NtCfg<false>::kSmem);
     };
     using T = std::true_type;

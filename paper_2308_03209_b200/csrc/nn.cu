@@ -334,7 +334,7 @@ __device__ __forceinline__ void gather_rows_sum(int64_t a, int64_t b, int lane, 
 // 1[msg > 0] * sum (nn.hpp:287-288). Returns max|out| of the lane's chunks.
 // The ReLU decision comes from the msg row, or (compact activations) from its
 // sign bits: word [v][c / 32], bit c % 32, written by the msg GEMM's epilogue.
-template <int NCH, bool kBwd>
+template <int NCH, bool kBwd, bool kPos>
 __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int32_t H4, const float* __restrict__ inv,
                                             const float* __restrict__ msg, const uint32_t* __restrict__ pos,
                                             float* __restrict__ out, const float4 (&acc)[NCH]) {
@@ -350,7 +350,7 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
             r.y *= s;
             r.z *= s;
             r.w *= s;
-        } else if (pos) {
+        } else if (kPos) {
             const uint32_t b = __ldg(pos + v * ((H + 31) >> 5) + (ch >> 3)) >> ((4 * ch) & 31);
             r.x = (b & 1u) ? r.x : 0.f;
             r.y = (b & 2u) ? r.y : 0.f;
@@ -371,7 +371,7 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
 
 // Warp per row over rows with at most `max_slots` CSR slots (heavier rows go
 // through the segmented path below).
-template <int NCH, bool kBwd>
+template <int NCH, bool kBwd, bool kPos = false>
 __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                    const int32_t* __restrict__ nbrs,
                                                    const uint32_t* __restrict__ bits, const float* __restrict__ inv,
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
-        amx = fmaxf(amx, finish_row<NCH, kBwd>(v, lane, H, H4, inv, msg, pos, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd, kPos>(v, lane, H, H4, inv, msg, pos, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256) spmm_segments_kernel(int32_t nseg, int32_
     }
 }
 
-template <int NCH, bool kBwd>
+template <int NCH, bool kBwd, bool kPos>
 __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int32_t H,
                                                                 const int32_t* __restrict__ rows,
                                                                 const int32_t* __restrict__ seg_first,
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int3
                     acc[c].z += p.z;
                     acc[c].w += p.w;
                 }
-        amx = fmaxf(amx, finish_row<NCH, kBwd>(rows[h], lane, H, H4, inv, msg, pos, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd, kPos>(rows[h], lane, H, H4, inv, msg, pos, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -501,7 +501,7 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
     }
 }
 
-template <int NCH, bool kBwd>
+template <int NCH, bool kBwd, bool kPos>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* src, const float* msg, const uint32_t* pos, float* out, cudaStream_t s, float* amax_out,
               const HeavyRows* hv, float* partial) {
@@ -509,7 +509,7 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
     // (A/B, profiles/r01_spmm_grid_ab.txt: x16 -> x64 blocks per SM = 0.82 -> 0.92 of HBM peak)
     const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
     const bool heavy = hv && hv->nh > 0;
-    spmm_kernel<NCH, kBwd><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out, amax_out,
+    spmm_kernel<NCH, kBwd, kPos><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out, amax_out,
                                                 heavy ? int64_t(kHeavySlots) : INT64_MAX);
     SC_LAUNCH_CHECK();
     count_launch();
@@ -517,10 +517,19 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
     spmm_segments_kernel<NCH><<<grid_for(int64_t(hv->nseg) * 32, 256, int64_t(num_sms()) * 16), 256, 0, s>>>(
         hv->nseg, H, off, nbrs, bits, hv->seg_row.get(), hv->seg_begin.get(), src, partial);
     SC_LAUNCH_CHECK();
-    spmm_heavy_finish_kernel<NCH, kBwd><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
+    spmm_heavy_finish_kernel<NCH, kBwd, kPos><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
         hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, msg, pos, out, amax_out);
     SC_LAUNCH_CHECK();
     count_launch(2);
+}
+
+// the ReLU-bits variant is a separate instantiation: the msg path keeps its own code
+template <int NCH, bool kBwd>
+void spmm_vec_pos(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits,
+                  const float* inv, const float* src, const float* msg, const uint32_t* pos, float* out,
+                  cudaStream_t s, float* amax_out, const HeavyRows* hv, float* partial) {
+    if (kBwd && pos) spmm_vec<NCH, kBwd, true>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    else spmm_vec<NCH, kBwd, false>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
 }
 
 template <bool kBwd>
@@ -536,10 +545,10 @@ void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, 
         return;
     }
     const int nch = (H / 4 + 31) / 32;
-    if (nch <= 1) spmm_vec<1, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
-    else if (nch == 2) spmm_vec<2, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
-    else if (nch <= 4) spmm_vec<4, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
-    else spmm_vec<8, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    if (nch <= 1) spmm_vec_pos<1, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    else if (nch == 2) spmm_vec_pos<2, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    else if (nch <= 4) spmm_vec_pos<4, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+    else spmm_vec_pos<8, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
 }
 
 __global__ void mask_bits_kernel(int64_t nnz, const int32_t* __restrict__ eids, const uint8_t* __restrict__ mask,
