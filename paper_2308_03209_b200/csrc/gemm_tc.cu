@@ -710,7 +710,7 @@ struct NtTmCfg {
     static constexpr int kStg = 4;                      // fp32 staging slots
     static constexpr int kMaxKb = 8;                    // K <= 256
     static constexpr int kBOff = 0;                     // resident B' (<= kMaxKb x n_pad x 64 B per CTA)
-    static constexpr int kBBytes = kMaxKb * kMaxN * 64 / 2;
+    static constexpr int kBBytes = kMaxKb * 2 * (kMaxN / 2) * 64;  // k-blocks x {hi, lo} x this CTA's rows x 64 B
     static constexpr int kStgOff = kBOff + kBBytes;
     static constexpr int kEpiOff = kStgOff + kStg * kNtStgBytes;
     static constexpr int kBarOff = kEpiOff + kNtEpiBytes;
@@ -1020,6 +1020,7 @@ struct alignas(64) TnParams {
     // The (A' tile, B' tile) pairs computed per split (a dual launch skips A2 x B1).
     int32_t ntiles;
     int8_t tile_a[8], tile_b[8];
+    int32_t stagger;    // A' in TMEM, one accumulator: stagger the pairs' drain points (tn_run_end)
     int32_t split_acc;  // A' in TMEM: split full tiles' accumulator into two staggered halves
     float* ws;       // [splits][N1][N2] fp32 partials
     unsigned long long* trace;  // optional (SC_TN_TRACE=1): per-role wait / total cycles, summed over CTAs
@@ -1090,17 +1091,12 @@ static_assert(TnCfg<true, true>::kSmem <= 232448 && 256 + 32 * TnCfg<true, true>
 // (kb + off_h) % kRun == 0, off_1 = kRun / 2 (staggered), and at kblocks. Returns the (exclusive)
 // end of the run that starts at `start`.
 constexpr int kRun = 2 * kChunkKb;
-__device__ __forceinline__ int tn_run_end(int h, int start, int kblocks, int nh) {
-    const int off = (nh > 1 && h == 1) ? kRun / 2 : 0;
+// `stag` (one accumulator) shifts a CTA pair's run boundaries so that the pairs' drains, during
+// which their tensor pipe and HBM stream pause, do not all fall on the same k-blocks.
+__device__ __forceinline__ int tn_run_end(int h, int start, int kblocks, int nh, int stag) {
+    const int off = nh > 1 ? (h == 1 ? kRun / 2 : 0) : stag;
     const int end = start + (kRun - (start + off) % kRun);
     return end < kblocks ? end : kblocks;
-}
-// Length of the run of half h that ends at `end` (its first k-block is end - length).
-__device__ __forceinline__ int tn_run_len(int h, int end, int nh) {
-    const int off = (nh > 1 && h == 1) ? kRun / 2 : 0;
-    const int r = (end + off) % kRun;
-    const int len = r == 0 ? kRun : r;  // runs end on a boundary, or at kblocks (partial)
-    return len < end ? len : end;
 }
 
 template <bool PAIR, bool AT = false>
@@ -1145,6 +1141,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
     const int nchunks = (kblocks + Cfg::kChunk - 1) / Cfg::kChunk;
     // A' in TMEM: a full 256-column tile splits its accumulator into two staggered halves
     const int nh = (AT && p.split_acc && nb_pad == 2 * kBM) ? 2 : 1;
+    const int stag = p.stagger ? (unit & 3) * (kRun / 4) : 0;
 
     constexpr int kBOff = AT ? 0 : 2 * kTnATile;  // B' hi / lo tiles within a stage
     const int ka = scale_exp(*(a_second ? p.amax_a2 : p.amax_a));
@@ -1324,7 +1321,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
             const uint32_t idesc = idesc_f16_at(Cfg::kACols, nb_pad / nh);
             int kb0 = 0, kb1 = nh > 1 ? 0 : kblocks;                 // next k-block of each half
             int beg0 = 0, beg1 = 0;                                  // first k-block of the current run
-            int end0 = tn_run_end(0, 0, kblocks, nh), end1 = nh > 1 ? tn_run_end(1, 0, kblocks, nh) : kblocks;
+            int end0 = tn_run_end(0, 0, kblocks, nh, stag), end1 = nh > 1 ? tn_run_end(1, 0, kblocks, nh, stag) : kblocks;
             uint32_t par0 = 1, par1 = 1;                             // tempty parity the next run waits for
             bool fresh0 = true, fresh1 = true;                       // at a run start: accumulator must be free
             auto issue = [&](int h, int& kb, int& beg, int& end, uint32_t& par, bool& fresh, int other_kb) {
@@ -1354,7 +1351,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
                     par ^= 1u;
                     fresh = true;
                     beg = end;
-                    end = tn_run_end(h, end, kblocks, nh);
+                    end = tn_run_end(h, end, kblocks, nh, stag);
                 }
                 if (other_kb > kb) mma_commit_g<PAIR>(&empty[st]);  // both halves issued: stage free
                 ++kb;
@@ -1437,7 +1434,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
         const uint64_t pol_ws = l2_evict_last();
         float* tbuf = reinterpret_cast<float*>(smem + Cfg::kEpiOff) + ew * 32 * Cfg::kEpiPitch;
         const int hw = nb_pad / nh;  // TMEM columns per half
-        int endh[2] = {tn_run_end(0, 0, kblocks, nh), nh > 1 ? tn_run_end(1, 0, kblocks, nh) : kblocks + 1};
+        int endh[2] = {tn_run_end(0, 0, kblocks, nh, stag), nh > 1 ? tn_run_end(1, 0, kblocks, nh, stag) : kblocks + 1};
         uint32_t runh[2] = {0, 0};
         while (endh[0] <= kblocks || (nh > 1 && endh[1] <= kblocks)) {
             if (kblocks == 0) break;
@@ -1480,7 +1477,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_l + h * 8);
             ++runh[h];
-            endh[h] = endh[h] < kblocks ? tn_run_end(h, endh[h], kblocks, nh) : kblocks + 1;
+            endh[h] = endh[h] < kblocks ? tn_run_end(h, endh[h], kblocks, nh, stag) : kblocks + 1;
         }
         if (kblocks == 0)
             for (int rr = 0; rr < rows_here; ++rr)
@@ -1632,13 +1629,15 @@ void encode_img(CUtensorMap* map, const uint8_t* img, int64_t rows, uint32_t box
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (image) failed (" + std::to_string(int(r)) + ")");
 }
-// Single-source NT GEMMs with K <= 256 use the A'-in-TMEM kernel unless SC_NT_TM=0.
-bool nt_tm_enabled() {
-    static const bool on = [] {
+// Single-source NT GEMMs with K <= 256 and the A'-in-TMEM kernel. SC_NT_TM: 0 off, 1 (default)
+// for N <= 128 (one pass: the head GEMM), 2 also two-pass N = 256 (msg, dmean, head dgrad:
+// measured slower, profiles/r02_nt_tm_ab.txt).
+int nt_tm_mode() {
+    static const int mode = [] {
         const char* e = std::getenv("SC_NT_TM");
-        return !(e && e[0] == '0');
+        return e ? std::atoi(e) : 1;
     }();
-    return on;
+    return mode;
 }
 // NT GEMMs run on CTA pairs (cta_group::2) unless SC_NT_PAIR=0.
 bool nt_pair_enabled() {
@@ -1689,6 +1688,11 @@ void tn_launch(tc::TnParams& p, bool pair, int32_t S, cudaStream_t s) {
         return e ? std::atoi(e) : 0;
     }();
     p.split_acc = split_acc;
+    static const int stagger = [] {
+        const char* e = std::getenv("SC_TN_STAGGER");
+        return e ? std::atoi(e) : 1;
+    }();
+    p.stagger = stagger;
     const int64_t units = int64_t(S) * p.ntiles;
     auto launch = [&](auto kernel, int smem_bytes, int threads) {
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
@@ -1925,8 +1929,9 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     }
     const bool pair = nt_pair_enabled();
     // single source, K <= 256: the A'-in-TMEM kernel with the weight image resident in shared memory
-    const bool tm = pair && nt_tm_enabled() && p.nsrc == 1 && b1.kblocks <= tc::NtTmCfg::kMaxKb &&
-                    (b1.n_pad <= tc::kBM || b1.n_pad % 64 == 0);
+    const int tm_mode = nt_tm_mode();
+    const bool tm = pair && tm_mode > 0 && p.nsrc == 1 && b1.kblocks <= tc::NtTmCfg::kMaxKb &&
+                    (b1.n_pad <= tc::kBM || (tm_mode > 1 && b1.n_pad % 64 == 0));
     if (tm) {
         const int np = b1.n_pad > tc::kBM ? 2 : 1;
         encode_img(&p.src[0].tmap_b, b1.img.get(), int64_t(b1.kblocks) * 2 * b1.n_pad, b1.n_pad / np / 2);

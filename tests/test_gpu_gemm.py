@@ -156,15 +156,17 @@ def test_tn_smem_operand_path_subprocess():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
-def test_nt_smem_operand_path_subprocess():
-    """Single-source K <= 256 NT GEMMs run on the A'-in-TMEM kernel with the weight image resident
-    in shared memory; with SC_NT_TM=0 (read once per process) they run on the general CTA-pair
-    kernel (A' and streamed weight tiles in shared memory), which must pass the same fp64 checks."""
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_nt_tm_modes_subprocess(mode):
+    """Single-source K <= 256 NT GEMMs with N <= 128 run on the A'-in-TMEM kernel (weight image
+    resident in shared memory) by default. SC_NT_TM (read once per process) = 0 sends every NT GEMM
+    to the general CTA-pair kernel (A' and streamed weight tiles in shared memory); = 2 also runs
+    N = 256 on the A'-in-TMEM kernel as two N = 128 passes. Both must pass the same fp64 checks."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SC_NT_TM="0")
+    env = dict(os.environ, SC_NT_TM=mode)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_gemm.py"), "-q", "-k",
                         "test_f16x3_matches_fp64 or test_f16x3_scaling"], capture_output=True, text=True, env=env,
                        timeout=600, cwd=root)
