@@ -68,6 +68,8 @@ sc_status sc_build_graph_dev(sc_ctx* ctx, int32_t num_nodes, const int32_t* raw_
                              sc_graph** out, int64_t* dropped_self_loops, int64_t* merged_duplicates);
 /* Attach features (fp32 n x d), class ids, and the train/val/test masks
  * (Graph::features, labels, num_classes, train/val/test_mask). Host buffers. */
+/* Graph::features / labels / masks (graph.hpp:58-66). features may be NULL: a zero n x dim
+ * matrix is allocated (fill it with sc_graph_set_feature_rows). */
 sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, const int32_t* labels,
                             int32_t num_classes, const uint8_t* train, const uint8_t* val, const uint8_t* test);
 /* Multi-label targets (Graph::multilabels, graph.hpp:64; load_labels' multi-label
@@ -79,6 +81,11 @@ sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, con
 sc_status sc_graph_set_multilabels(sc_graph* g, const float* targets, int32_t num_classes);
 /* Replace only the features (e.g. a new batch of the same graph). Host or device source. */
 sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_device);
+/* Write feature rows [row0, row0 + rows) (host or device source), e.g. a matrix too large to
+ * stage whole; sc_graph_set_data with features == NULL allocates a zero matrix to fill this way
+ * (load_features' row-by-row fill, graph_io.cpp:82-160). The operand scale max|features| is
+ * raised by the new rows (exact when every row is written once over zeros). */
+sc_status sc_graph_set_feature_rows(sc_graph* g, int64_t row0, int64_t rows, const float* src, int is_device);
 sc_status sc_graph_info(sc_graph* g, int32_t* num_nodes, int64_t* num_edges, int32_t* dim, int32_t* num_classes);
 sc_status sc_graph_copy_edges(sc_graph* g, int32_t* uv);
 sc_status sc_graph_copy_csr(sc_graph* g, int64_t* offsets, int32_t* neighbors, int32_t* edge_ids, int32_t* degrees);
@@ -207,6 +214,11 @@ sc_status sc_trainer_create(sc_ctx* ctx, sc_graph* g, sc_vcut* vc, const sc_trai
  * (optional at world == 1: a single-rank communicator runs the same exchange). */
 sc_status sc_nccl_unique_id(uint8_t out[128]);
 sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]);
+/* Time ONE rank's share of a world > 1 job on a single GPU (no peers): the trainer runs this
+ * rank's partitions and exchange rounds exactly as it would in the job, but the all-gathers are
+ * skipped, so the other ranks' gradient slots stay zero and the gathered gradient / Adam step
+ * cover this rank's partitions only (timing and memory only, not a training result). */
+sc_status sc_trainer_emulate_rank(sc_trainer* t);
 /* Host transport for the gradient exchange, instead of NCCL (multi-process
  * runs without a GPU per rank, e.g. several ranks time-sharing one device in
  * tests, or any collective library the caller already runs). Called once per

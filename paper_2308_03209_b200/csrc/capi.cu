@@ -137,7 +137,7 @@ sc_status sc_build_graph(sc_ctx* ctx, int32_t n, const int32_t* raw_uv, int64_t 
 sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, const int32_t* labels, int32_t classes,
                             const uint8_t* train, const uint8_t* val, const uint8_t* test) {
     return guard([&] {
-        REQUIRE_ARG(g && features && labels && train && val && test, "sc_graph_set_data: null argument");
+        REQUIRE_ARG(g && labels && train && val && test, "sc_graph_set_data: null argument");
         REQUIRE_ARG(dim >= 1, "sc_graph_set_data: feature dim must be positive");
         REQUIRE_ARG(classes >= 1, "sc_graph_set_data: num_classes must be positive");
         set_device(g->ctx);
@@ -156,7 +156,8 @@ sc_status sc_graph_set_data(sc_graph* g, const float* features, int32_t dim, con
         g->train.alloc(std::max<int64_t>(n, 1));
         g->val.alloc(std::max<int64_t>(n, 1));
         g->test.alloc(std::max<int64_t>(n, 1));
-        h2d(g->features.get(), features, n * dim, s);
+        if (features) h2d(g->features.get(), features, n * dim, s);
+        else SC_CUDA(cudaMemsetAsync(g->features.get(), 0, g->features.bytes(), s));
         h2d(g->labels.get(), labels, n, s);
         h2d(g->train.get(), train, n, s);
         h2d(g->val.get(), val, n, s);
@@ -200,6 +201,23 @@ sc_status sc_graph_set_features(sc_graph* g, const float* features, int is_devic
         ++g->feat_version;
         SC_CUDA(cudaMemsetAsync(g->feat_amax.get(), 0, sizeof(float), g->ctx->stream));
         absmax(int64_t(g->n) * g->dim, g->features.get(), g->feat_amax.get(), g->ctx->stream);
+    });
+}
+sc_status sc_graph_set_feature_rows(sc_graph* g, int64_t row0, int64_t rows, const float* src, int is_device) {
+    return guard([&] {
+        REQUIRE_ARG(g && g->dim > 0, "sc_graph_set_feature_rows: graph has no feature buffer");
+        REQUIRE_ARG(row0 >= 0 && rows >= 0 && row0 + rows <= g->n, "sc_graph_set_feature_rows: rows out of range");
+        REQUIRE_ARG(src || rows == 0, "sc_graph_set_feature_rows: null source");
+        REQUIRE_ARG(!g->staged, "sc_graph_set_feature_rows: features are staged for the next step");
+        if (rows == 0) return;
+        set_device(g->ctx);
+        float* dst = g->features.get() + row0 * g->dim;
+        const int64_t k = rows * g->dim;
+        SC_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * size_t(k),
+                                is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->ctx->stream));
+        ++g->feat_version;
+        absmax(k, dst, g->feat_amax.get(), g->ctx->stream);
+        SC_CUDA(cudaStreamSynchronize(g->ctx->stream));  // the caller may reuse src
     });
 }
 sc_status sc_graph_set_part_ownership(sc_graph* g, int32_t rank, int32_t world) {
@@ -492,7 +510,12 @@ sc_status sc_vcut_part_copy(sc_vcut* vc, int32_t part, int32_t* nodes, int32_t* 
         if (offsets) d2h(offsets, pd.offsets.get(), pd.n_local + 1, s);
         if (nbrs) d2h(nbrs, pd.nbrs.get(), 2 * pd.m_local, s);
         if (eids) d2h(eids, pd.eids.get(), 2 * pd.m_local, s);
-        if (g2l) d2h(g2l, vc->g2l.get() + pd.g2l_slot * vc->g->n, vc->g->n, s);
+        if (g2l) {
+            DevBuf<int32_t> tmp(std::max<int64_t>(vc->g->n, 1));
+            part_g2l_device(vc, part, tmp.get());
+            d2h(g2l, tmp.get(), vc->g->n, s);
+            SC_CUDA(cudaStreamSynchronize(s));
+        }
         std::vector<int32_t> u, v;
         if (edges_uv) {
             u.resize(pd.m_local);
@@ -827,6 +850,12 @@ sc_status sc_trainer_init_comm(sc_trainer* t, const uint8_t id[128]) {
     return guard([&] {
         REQUIRE_ARG(t && id, "sc_trainer_init_comm: null argument");
         trainer_init_comm(t, id);  // world == 1: a single-rank communicator (exercises the exchange path)
+    });
+}
+sc_status sc_trainer_emulate_rank(sc_trainer* t) {
+    return guard([&] {
+        REQUIRE_ARG(t, "sc_trainer_emulate_rank: null trainer");
+        t->emulate = true;
     });
 }
 sc_status sc_trainer_set_exchange(sc_trainer* t, sc_exchange_fn fn, void* user) {

@@ -304,43 +304,38 @@ __global__ void check_assign_kernel(int64_t m, int32_t p, const int32_t* a, int*
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m; e += int64_t(gridDim.x) * blockDim.x)
         if (a[e] < 0 || a[e] >= p) *bad = 1;
 }
-__global__ void member_edges_kernel(int64_t m, int64_t n, const int32_t* __restrict__ a, const int32_t* __restrict__ u,
-                                    const int32_t* __restrict__ v, uint8_t* member, int32_t* part_count) {
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m; e += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t base = static_cast<int64_t>(a[e]) * n;
-        member[base + u[e]] = 1;
-        member[base + v[e]] = 1;
+__global__ void count_parts_kernel(int64_t m, const int32_t* __restrict__ a, int32_t* part_count) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m; e += int64_t(gridDim.x) * blockDim.x)
         atomicAdd(&part_count[a[e]], 1);
-    }
 }
-__global__ void isolated_flag_kernel(int64_t n, const int32_t* deg, int32_t* flag) {
-    for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x)
-        flag[x] = deg[x] == 0 ? 1 : 0;
-}
-// Isolated nodes go round-robin in ascending id, starting at part 0 (:45-50).
-__global__ void isolated_member_kernel(int64_t n, int32_t p, const int32_t* deg, const int32_t* rank,
-                                       uint8_t* member) {
-    for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x)
-        if (deg[x] == 0) member[static_cast<int64_t>(rank[x] % p) * n + x] = 1;
-}
-__global__ void g2l_kernel(int64_t n, const uint8_t* __restrict__ member, const int32_t* __restrict__ scan,
-                           int32_t* g2l, int32_t* nodes) {
-    for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x) {
-        if (member[x]) {
-            g2l[x] = scan[x];
-            nodes[scan[x]] = static_cast<int32_t>(x);
+// Endpoints of part i's edges (perm[0 .. mi) = its global edge ids), then the isolated nodes it
+// receives round-robin in ascending id, starting at part 0 (:45-50): iso[i], iso[i + p], ...
+__global__ void part_endpoints_kernel(int64_t mi, const int32_t* __restrict__ perm, const int32_t* __restrict__ u,
+                                      const int32_t* __restrict__ v, const int32_t* __restrict__ iso, int64_t niso_i,
+                                      int32_t i, int32_t p, int32_t* out) {
+    const int64_t total = 2 * mi + niso_i;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        if (k < 2 * mi) {
+            const int32_t e = perm[k >> 1];
+            out[k] = (k & 1) ? v[e] : u[e];
         } else {
-            g2l[x] = -1;
+            out[k] = iso[i + (k - 2 * mi) * p];
         }
     }
 }
-__global__ void rf_kernel(int64_t n, int32_t p, const uint8_t* member, int32_t* rf) {
-    for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x) {
-        int32_t c = 0;
-        for (int32_t i = 0; i < p; ++i) c += member[static_cast<int64_t>(i) * n + x];
-        rf[x] = c;
-    }
+// per_node_rf (:316-321): one increment per part that contains the node (nodes are unique per part)
+__global__ void rf_inc_kernel(int64_t nl, const int32_t* __restrict__ nodes, int32_t* rf) {
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nl; j += int64_t(gridDim.x) * blockDim.x)
+        rf[nodes[j]] += 1;
 }
+__global__ void scatter_g2l_kernel(int64_t nl, const int32_t* __restrict__ nodes, int32_t* g2l, bool clear) {
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nl; j += int64_t(gridDim.x) * blockDim.x)
+        g2l[nodes[j]] = clear ? -1 : static_cast<int32_t>(j);
+}
+struct IsDeg0 {
+    const int32_t* deg;
+    __host__ __device__ bool operator()(int32_t x) const { return deg[x] == 0; }
+};
 __global__ void local_edges_kernel(int64_t mi, const int32_t* __restrict__ perm, const int32_t* __restrict__ u,
                                    const int32_t* __restrict__ v, const int32_t* __restrict__ g2l, int32_t* lu,
                                    int32_t* lv, int32_t* gids) {
@@ -351,9 +346,6 @@ __global__ void local_edges_kernel(int64_t mi, const int32_t* __restrict__ perm,
         gids[k] = e;
     }
 }
-struct U8ToI32 {
-    __host__ __device__ int32_t operator()(uint8_t x) const { return x; }
-};
 }  // namespace
 
 std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<int32_t>&& assign) {
@@ -377,74 +369,39 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
     SC_CUDA(cudaStreamSynchronize(s));
     if (hbad) throw std::invalid_argument("edge assignment references an invalid part");
 
-    DevBuf<uint8_t> member(static_cast<size_t>(p) * std::max<int64_t>(n, 1));
-    DevBuf<int32_t> part_count(p), tmp(std::max<int64_t>(n, 1)), scan(std::max<int64_t>(n, 1));
-    SC_CUDA(cudaMemsetAsync(member.get(), 0, member.bytes(), s));
+    // Sparse construction: no p x n arrays. Edge ids are stably sorted by part (ascending global
+    // order within a part, :62-70); each part's node set is the sorted unique set of its edges'
+    // endpoints plus its round-robin isolated nodes (= the reference's ascending membership scan,
+    // :37-58); local ids come from a scratch n-array scattered and cleared per held part.
+    DevBuf<int32_t> part_count(p);
     SC_CUDA(cudaMemsetAsync(part_count.get(), 0, p * 4, s));
     if (m > 0) {
-        member_edges_kernel<<<grid_for(m, kBlock), kBlock, 0, s>>>(m, n, vc->assign.get(), g->eu.get(), g->ev.get(),
-                                                                   member.get(), part_count.get());
+        count_parts_kernel<<<grid_for(m, kBlock), kBlock, 0, s>>>(m, vc->assign.get(), part_count.get());
         SC_LAUNCH_CHECK();
         count_launch();
     }
+    // isolated nodes, ascending
+    DevBuf<int32_t> iso(std::max<int64_t>(n, 1));
+    DevBuf<int64_t> niso_dev(1);
+    int64_t niso = 0;
     if (n > 0) {
-        isolated_flag_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, g->degrees.get(), tmp.get());
+        cub::CountingInputIterator<int32_t> ids(0);
         size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, tmp.get(), scan.get(), n, s);
-        cub::DeviceScan::ExclusiveSum(ctx->temp(tb), tb, tmp.get(), scan.get(), n, s);
-        isolated_member_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, p, g->degrees.get(), scan.get(),
-                                                                      member.get());
-        SC_LAUNCH_CHECK();
-        count_launch(4);
+        cub::DeviceSelect::If(nullptr, tb, ids, iso.get(), niso_dev.get(), n, IsDeg0{g->degrees.get()}, s);
+        cub::DeviceSelect::If(ctx->temp(tb), tb, ids, iso.get(), niso_dev.get(), n, IsDeg0{g->degrees.get()}, s);
+        d2h(&niso, niso_dev.get(), 1, s);
+        count_launch(2);
     }
-    // per-part local numbering (ascending global id); arrays only for the parts this rank holds
     vc->own_rank = g->own_rank;
     vc->own_world = g->own_world;
     vc->parts.resize(p);
-    int64_t nheld = 0;
-    for (int32_t i = 0; i < p; ++i) {
-        vc->parts[i].held = g->owns(i);
-        vc->parts[i].g2l_slot = vc->parts[i].held ? nheld++ : -1;
-    }
-    vc->g2l.alloc(static_cast<size_t>(std::max<int64_t>(nheld, 1)) * std::max<int64_t>(n, 1));
     vc->per_node_rf.alloc(std::max<int64_t>(n, 1));
-    std::vector<int32_t> n_local(p, 0);
-    DevBuf<int32_t> total(1);
-    for (int32_t i = 0; i < p; ++i) {
-        const uint8_t* mem_i = member.get() + static_cast<int64_t>(i) * n;
-        cub::TransformInputIterator<int32_t, U8ToI32, const uint8_t*> it(mem_i, U8ToI32{});
-        if (n > 0) {
-            size_t tb = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tb, it, scan.get(), n, s);
-            cub::DeviceScan::ExclusiveSum(ctx->temp(tb), tb, it, scan.get(), n, s);
-            tb = 0;
-            cub::DeviceReduce::Sum(nullptr, tb, it, total.get(), n, s);
-            cub::DeviceReduce::Sum(ctx->temp(tb), tb, it, total.get(), n, s);
-            d2h(&n_local[i], total.get(), 1, s);
-            SC_CUDA(cudaStreamSynchronize(s));
-            count_launch(4);
-        }
-        PartDev& pd = vc->parts[i];
-        pd.n_local = n_local[i];
-        if (!pd.held) continue;
-        pd.nodes.alloc(std::max<int64_t>(pd.n_local, 1));
-        if (n > 0) {
-            g2l_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, mem_i, scan.get(), vc->g2l.get() + pd.g2l_slot * n,
-                                                              pd.nodes.get());
-            SC_LAUNCH_CHECK();
-            count_launch();
-        }
-    }
-    if (n > 0) {
-        rf_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, p, member.get(), vc->per_node_rf.get());
-        SC_LAUNCH_CHECK();
-        count_launch();
-    }
-    // local edges: stable sort of edge ids by part keeps ascending global order (:62-70)
+    SC_CUDA(cudaMemsetAsync(vc->per_node_rf.get(), 0, vc->per_node_rf.bytes(), s));
     std::vector<int32_t> counts(p, 0);
     d2h(counts.data(), part_count.get(), p, s);
-    DevBuf<int32_t> idx(std::max<int64_t>(m, 1)), keys_out(std::max<int64_t>(m, 1)), perm(std::max<int64_t>(m, 1));
+    DevBuf<int32_t> perm(std::max<int64_t>(m, 1));
     if (m > 0) {
+        DevBuf<int32_t> idx(m), keys_out(m);
         iota_kernel<<<grid_for(m, kBlock), kBlock, 0, s>>>(idx.get(), m);
         SC_LAUNCH_CHECK();
         size_t tb = 0;
@@ -453,26 +410,75 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
                                         s);
         cub::DeviceRadixSort::SortPairs(ctx->temp(tb), tb, vc->assign.get(), keys_out.get(), idx.get(), perm.get(), m,
                                         0, eb, s);
-        count_launch(5);
+        count_launch(3);
+        SC_CUDA(cudaStreamSynchronize(s));  // idx / keys_out are freed on scope exit
     }
     SC_CUDA(cudaStreamSynchronize(s));
+    int64_t max_ends = 1;
+    for (int32_t i = 0; i < p; ++i) {
+        const int64_t niso_i = niso > i ? (niso - i + p - 1) / p : 0;
+        max_ends = std::max<int64_t>(max_ends, 2 * int64_t(counts[i]) + niso_i);
+    }
+    DevBuf<int32_t> ends(max_ends), ends_sorted(max_ends), uniq(max_ends);
+    DevBuf<int64_t> nuniq(1);
+    bool any_held = false;
+    for (int32_t i = 0; i < p; ++i) any_held |= g->owns(i);
+    DevBuf<int32_t> g2l_scr;  // -1 everywhere between held parts
+    if (any_held && n > 0) {
+        g2l_scr.alloc(n);
+        fill(g2l_scr.get(), n, int32_t(-1), s);
+    }
+    const int nb = bits_for(static_cast<uint64_t>(std::max<int64_t>(n, 1)));
     int64_t start = 0;
     for (int32_t i = 0; i < p; ++i) {
         PartDev& pd = vc->parts[i];
+        pd.held = g->owns(i);
         pd.m_local = counts[i];
         const int64_t mi = pd.m_local;
+        const int64_t niso_i = niso > i ? (niso - i + p - 1) / p : 0;
+        const int64_t ne = 2 * mi + niso_i;
+        int64_t nl = 0;
+        if (ne > 0) {
+            part_endpoints_kernel<<<grid_for(ne, kBlock), kBlock, 0, s>>>(mi, perm.get() + start, g->eu.get(),
+                                                                           g->ev.get(), iso.get(), niso_i, i, p,
+                                                                           ends.get());
+            SC_LAUNCH_CHECK();
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tb, ends.get(), ends_sorted.get(), ne, 0, nb, s);
+            cub::DeviceRadixSort::SortKeys(ctx->temp(tb), tb, ends.get(), ends_sorted.get(), ne, 0, nb, s);
+            tb = 0;
+            cub::DeviceSelect::Unique(nullptr, tb, ends_sorted.get(), uniq.get(), nuniq.get(), ne, s);
+            cub::DeviceSelect::Unique(ctx->temp(tb), tb, ends_sorted.get(), uniq.get(), nuniq.get(), ne, s);
+            d2h(&nl, nuniq.get(), 1, s);
+            SC_CUDA(cudaStreamSynchronize(s));
+            if (nl > 0) rf_inc_kernel<<<grid_for(nl, kBlock), kBlock, 0, s>>>(nl, uniq.get(), vc->per_node_rf.get());
+            SC_LAUNCH_CHECK();
+            count_launch(6);
+        }
+        pd.n_local = nl;
         if (!pd.held) {
             start += mi;
             continue;
+        }
+        pd.nodes.alloc(std::max<int64_t>(nl, 1));
+        if (nl > 0) {
+            SC_CUDA(cudaMemcpyAsync(pd.nodes.get(), uniq.get(), nl * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            scatter_g2l_kernel<<<grid_for(nl, kBlock), kBlock, 0, s>>>(nl, pd.nodes.get(), g2l_scr.get(), false);
+            SC_LAUNCH_CHECK();
+            count_launch();
         }
         pd.lu.alloc(std::max<int64_t>(mi, 1));
         pd.lv.alloc(std::max<int64_t>(mi, 1));
         pd.edge_gids.alloc(std::max<int64_t>(mi, 1));
         if (mi > 0) {
             local_edges_kernel<<<grid_for(mi, kBlock), kBlock, 0, s>>>(mi, perm.get() + start, g->eu.get(), g->ev.get(),
-                                                                       vc->g2l.get() + pd.g2l_slot * n, pd.lu.get(),
-                                                                       pd.lv.get(),
+                                                                       g2l_scr.get(), pd.lu.get(), pd.lv.get(),
                                                                        pd.edge_gids.get());
+            SC_LAUNCH_CHECK();
+            count_launch();
+        }
+        if (nl > 0) {
+            scatter_g2l_kernel<<<grid_for(nl, kBlock), kBlock, 0, s>>>(nl, pd.nodes.get(), g2l_scr.get(), true);
             SC_LAUNCH_CHECK();
             count_launch();
         }
@@ -486,6 +492,20 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
     }
     SC_CUDA(cudaStreamSynchronize(s));
     return vc;
+}
+
+// global_to_local of a held part (partition.hpp:20): -1 everywhere, then j at nodes[j]
+void part_g2l_device(const sc_vcut* vc, int32_t part, int32_t* out_dev) {
+    const PartDev& pd = vc->held(part);
+    cudaStream_t s = vc->g->ctx->stream;
+    const int64_t n = vc->g->n;
+    if (n == 0) return;
+    fill(out_dev, n, int32_t(-1), s);
+    if (pd.n_local > 0) {
+        scatter_g2l_kernel<<<grid_for(pd.n_local, kBlock), kBlock, 0, s>>>(pd.n_local, pd.nodes.get(), out_dev, false);
+        SC_LAUNCH_CHECK();
+        count_launch(2);
+    }
 }
 
 // ---- reweight.cpp:23-71 --------------------------------------------------------------

@@ -123,7 +123,6 @@ struct sc_graph {
 struct PartDev {
     int64_t n_local = 0, m_local = 0;
     bool held = true;                       // arrays materialised on this rank (sc_graph_set_part_ownership)
-    int64_t g2l_slot = -1;                  // row of sc_vcut::g2l (held parts only)
     sc::DevBuf<int32_t> nodes;              // global ids ascending
     sc::DevBuf<int32_t> lu, lv;             // local endpoints, local-edge order
     sc::DevBuf<int32_t> edge_gids;          // global edge id per local edge
@@ -136,7 +135,6 @@ struct sc_vcut {
     sc_graph* g = nullptr;
     int32_t p = 0;
     sc::DevBuf<int32_t> assign;        // m
-    sc::DevBuf<int32_t> g2l;           // held parts x n, -1 where absent (PartDev::g2l_slot)
     int32_t own_rank = 0, own_world = 1;  // the graph's ownership when this cut was built
     const PartDev& held(int32_t i) const {
         if (!parts[i].held)
@@ -158,6 +156,7 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
 void assign_random(sc_graph* g, int32_t p, uint64_t seed, int32_t* assign);
 void assign_dbh(sc_graph* g, int32_t p, uint64_t seed, int32_t* assign);
 void compute_weights_device(sc_vcut* vc, int scheme, int32_t part, double* out_dev);
+void part_g2l_device(const sc_vcut* vc, int32_t part, int32_t* out_dev);  // global_to_local (n, -1 absent)
 // partition_seq.cu (partition.cpp:116-308)
 std::vector<int32_t> ne_assign_host(sc_graph* g, int32_t p, double slack, std::vector<std::string>& warnings);
 std::vector<int32_t> edge_cut_greedy_host(sc_graph* g, int32_t p, uint64_t seed);

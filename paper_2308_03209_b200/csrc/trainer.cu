@@ -620,7 +620,7 @@ void trainer_step_async(sc_trainer* t, int epoch) {
     commit_staged_features(t);
     t->prof.records.clear();
     t->prof.used = 0;
-    if (t->world > 1 && !t->comm && !t->xfn)
+    if (t->world > 1 && !t->comm && !t->xfn && !t->emulate)
         throw std::invalid_argument("sc_trainer_init_comm (or an exchange callback) must precede stepping at world > 1");
     // Exchange round j trains partition j*world + rank on every rank; each
     // finished gradient bucket (and the partition loss) is all-gathered on the
@@ -825,6 +825,7 @@ void exchange_host(sc_trainer* t, int b, int round, cudaStream_t s) {
 
 void exchange_bucket(sc_trainer* t, int b, int round, cudaStream_t producer) {
     cudaStream_t s = producer ? producer : t->ctx->stream;
+    if (t->emulate) return;  // no peers: the other ranks' slots stay zero
     if (t->xfn) {
         exchange_host(t, b, round, s);
         return;

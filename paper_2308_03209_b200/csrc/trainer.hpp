@@ -165,6 +165,7 @@ struct sc_trainer {
     // Host transport (sc_trainer_set_exchange), used instead of NCCL when set.
     using ExchangeFn = int32_t (*)(void*, int32_t, int32_t, int32_t, const void*, void*, int64_t);
     ExchangeFn xfn = nullptr;
+    bool emulate = false;  // sc_trainer_emulate_rank: one rank of a world > 1 job, exchange skipped
     void* xuser = nullptr;
     void* xhost = nullptr;       // pinned staging: send (one rank's bytes) + recv (world x)
     size_t xhost_bytes = 0;

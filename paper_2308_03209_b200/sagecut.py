@@ -67,6 +67,7 @@ _sig("sc_build_graph", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i
 _sig("sc_build_graph_dev", [_vp, _i32, _vp, _i64, _pp, C.POINTER(_i64), C.POINTER(_i64)])
 _sig("sc_graph_set_data", [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp])
 _sig("sc_graph_set_features", [_vp, _vp, C.c_int])
+_sig("sc_graph_set_feature_rows", [_vp, _i64, _i64, _vp, C.c_int])
 _sig("sc_graph_set_multilabels", [_vp, _vp, _i32])
 _sig("sc_load_graph", [_vp, C.c_char_p, _i32, _i32, _pp, C.POINTER(_i64), C.POINTER(_i64)])
 _sig("sc_read_edge_list", [C.c_char_p, _i32, _vp, _i64, C.POINTER(_i64), C.POINTER(_i32)])
@@ -129,6 +130,7 @@ class _TrainConfigC(C.Structure):
 _sig("sc_trainer_create", [_vp, _vp, _vp, C.POINTER(_TrainConfigC), _i32, _i32, _pp])
 _sig("sc_nccl_unique_id", [_vp])
 _sig("sc_trainer_init_comm", [_vp, _vp])
+_sig("sc_trainer_emulate_rank", [_vp])
 _sig("sc_trainer_step", [_vp, _i32, C.POINTER(_f64), C.POINTER(_f64)])
 _sig("sc_trainer_step_async", [_vp, _i32])
 _sig("sc_trainer_stage_features", [_vp, _vp, _i32])
@@ -334,16 +336,35 @@ class Graph:
         _check(_lib.sc_graph_copy_csr(self.h, None, None, None, _ptr(dg)))
         return dg
 
-    def set_data(self, features, labels, num_classes, train_mask, val_mask, test_mask):
-        f = np.ascontiguousarray(features, np.float32)
-        if f.ndim != 2 or f.shape[0] != self.num_nodes:
-            raise ValueError("set_data: features must be num_nodes x d")
+    def set_data(self, features, labels, num_classes, train_mask, val_mask, test_mask, dim: Optional[int] = None):
+        """features: n x d array, or None with `dim` given (a zero matrix to fill with set_feature_rows)."""
+        if features is None:
+            if not dim or dim < 1:
+                raise ValueError("set_data: features=None needs dim")
+            f, d = None, int(dim)
+        else:
+            f = np.ascontiguousarray(features, np.float32)
+            if f.ndim != 2 or f.shape[0] != self.num_nodes:
+                raise ValueError("set_data: features must be num_nodes x d")
+            d = f.shape[1]
         lab = np.ascontiguousarray(labels, np.int32)
         tr, va, te = (np.ascontiguousarray(x, np.uint8) for x in (train_mask, val_mask, test_mask))
-        _check(_lib.sc_graph_set_data(self.h, _ptr(f), f.shape[1], _ptr(lab), int(num_classes), _ptr(tr), _ptr(va),
+        _check(_lib.sc_graph_set_data(self.h, _ptr(f), d, _ptr(lab), int(num_classes), _ptr(tr), _ptr(va),
                                       _ptr(te)), "set_data")
-        self.dim, self.num_classes = f.shape[1], int(num_classes)
+        self.dim, self.num_classes = d, int(num_classes)
         self.multilabel = False
+
+    def set_feature_rows(self, row0: int, rows=None, device_ptr: Optional[int] = None, num_rows: int = 0):
+        """Write feature rows [row0, row0 + k): from a host array `rows` (k x d), or k = num_rows rows
+        at a device pointer."""
+        if device_ptr is not None:
+            _check(_lib.sc_graph_set_feature_rows(self.h, int(row0), int(num_rows), _vp(device_ptr), 1),
+                   "set_feature_rows")
+        else:
+            f = np.ascontiguousarray(rows, np.float32)
+            if f.ndim != 2 or f.shape[1] != self.dim:
+                raise ValueError("set_feature_rows: rows must be k x d")
+            _check(_lib.sc_graph_set_feature_rows(self.h, int(row0), f.shape[0], _ptr(f), 0), "set_feature_rows")
 
     def set_part_ownership(self, rank: int, world: int):
         """Vertex cuts built after this hold only the parts this rank trains (i % world == rank)."""
@@ -830,6 +851,11 @@ class CoFreeTrainer:
 
         self._xfn = EXCHANGE_FN(cb)  # keep the trampoline alive
         _check(_lib.sc_trainer_set_exchange(self.h, self._xfn, None))
+
+    def emulate_rank(self):
+        """Time this rank's share of the world-size job on one GPU: exchanges skipped, the other
+        ranks' gradient slots stay zero (timing / memory only)."""
+        _check(_lib.sc_trainer_emulate_rank(self.h), "emulate_rank")
 
     @staticmethod
     def nccl_unique_id() -> bytes:
