@@ -91,6 +91,7 @@ struct alignas(64) Params {
     uint32_t* relu_pos;  // optional (EPI == kEpiRelu): bit c % 32 of word [row][c / 32] = C[row][c] > 0
     int64_t tiles;
     unsigned long long* trace;  // optional (SC_TN_TRACE_BUILD + SC_TN_TRACE=1), as TnParams::trace
+    int32_t prefetch;           // L2-prefetch the CTA's next tile's A rows at the start of each tile
 };
 
 // ---- PTX helpers -------------------------------------------------------------
@@ -220,6 +221,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                  "r"(x), "r"(y), "r"(smem_u32(src))
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// L2 prefetch of a 2D TMA box (no shared memory, no barrier): raises the HBM bytes in flight beyond
+// what the shared-memory staging ring can hold, so the later tensor load hits L2.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y)
+                 : "memory");
 }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -503,7 +512,14 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
         // ================= loader: one 2D TMA per stage, HBM -> fp32 staging =================
         // box 32 k (128 B) x 128 rows, SWIZZLE_128B; out-of-range rows / k are zero-filled
         Ring ring;
-        for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep) {
+            if (p.prefetch && tile + tstep < p.tiles) {  // the next tile's rows: one box per (source, k-block)
+                const int32_t y = static_cast<int32_t>((tile + tstep) * Cfg::kRows + rank * kBM);
+                int j = 0;
+                for (int src = 0; src < p.nsrc; ++src)
+                    for (int kb = 0; kb < p.src[src].kblocks; ++kb, ++j)
+                        if ((j & 31) == lane) tma_prefetch_2d(&p.src[src].tmap, kb * kNtBK, y);
+            }
             for (int src = 0; src < p.nsrc; ++src)
                 for (int kb = 0; kb < p.src[src].kblocks; ++kb, ring.next(Cfg::kStg)) {
                     TN_TIMED_WAIT(w_a, mbar_wait(&sempty[ring.idx], ring.phase ^ 1));
@@ -514,6 +530,7 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                     }
                     __syncwarp();
                 }
+        }
     } else if (warp < Cfg::kCW) {
         // ================= converters: staging fp32 -> scaled fp16 hi/lo (SW64) =================
         // Row-fastest mapping: 8 consecutive threads read the same chunk of 8 different rows, which
@@ -793,6 +810,8 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
         Ring ring;
         for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
             for (int kb = 0; kb < kbl; ++kb, ring.next(Cfg::kStg)) {
+                if (p.prefetch && kb == 0 && tile + tstep < p.tiles && lane < kbl)
+                    tma_prefetch_2d(&S.tmap, lane * kNtBK, static_cast<int32_t>((tile + tstep) * Cfg::kRows + rank * kBM));
                 mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&sfull[ring.idx], kNtStgBytes);
@@ -1021,6 +1040,7 @@ struct alignas(64) TnParams {
     int32_t ntiles;
     int8_t tile_a[8], tile_b[8];
     int32_t stagger;    // A' in TMEM, one accumulator: stagger the pairs' drain points (tn_run_end)
+    int32_t pf_dist;    // L2-prefetch the operand boxes of k-block kb + pf_dist when loading kb (0: off)
     int32_t split_acc;  // A' in TMEM: split full tiles' accumulator into two staggered halves
     float* ws;       // [splits][N1][N2] fp32 partials
     unsigned long long* trace;  // optional (SC_TN_TRACE=1): per-role wait / total cycles, summed over CTAs
@@ -1194,6 +1214,15 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
                 const int32_t c = nb0 + 32 * lane;
                 if (c < p.n2a) tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b1, c, k0, &sfull[ring.idx], pol_b);
                 else tma_load_2d_hint(sb + lane * kTnBox, &p.tm_b2, c - p.n2a, k0, &sfull[ring.idx], pol_b);
+            }
+            if (p.pf_dist > 0 && kb + p.pf_dist < kblocks) {  // the same boxes pf_dist k-blocks ahead -> L2
+                const int32_t kp = k0 + p.pf_dist * kTnBK;
+                if (lane < a_boxes) tma_prefetch_2d(tm_a, a_col0 + 32 * lane, kp);
+                if (lane < b_boxes) {
+                    const int32_t c = nb0 + 32 * lane;
+                    if (c < p.n2a) tma_prefetch_2d(&p.tm_b1, c, kp);
+                    else tma_prefetch_2d(&p.tm_b2, c - p.n2a, kp);
+                }
             }
         }
     } else if (warp < Cfg::kCW) {
@@ -1693,6 +1722,11 @@ void tn_launch(tc::TnParams& p, bool pair, int32_t S, cudaStream_t s) {
         return e ? std::atoi(e) : 1;
     }();
     p.stagger = stagger;
+    static const int pf_dist = [] {
+        const char* e = std::getenv("SC_TN_PF");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.pf_dist = pf_dist;
     const int64_t units = int64_t(S) * p.ntiles;
     auto launch = [&](auto kernel, int smem_bytes, int threads) {
         SC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
@@ -1927,6 +1961,11 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
         SC_CUDA(cudaMemsetAsync(trace_buf.get(), 0, 16 * sizeof(unsigned long long), s));
         p.trace = trace_buf.get();
     }
+    static const int nt_pf = [] {
+        const char* e = std::getenv("SC_NT_PF");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.prefetch = nt_pf;
     const bool pair = nt_pair_enabled();
     // single source, K <= 256: the A'-in-TMEM kernel with the weight image resident in shared memory
     const int tm_mode = nt_tm_mode();

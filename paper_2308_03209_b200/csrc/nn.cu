@@ -1002,6 +1002,54 @@ void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, fl
     SC_LAUNCH_CHECK();
     count_launch();
 }
+// ---- small weight-space products (the composed top layer, trainer.cu) --------------------------
+// C[M x N] = op(A) op(B): a(i, k) = ta ? A[k lda + i] : A[i lda + k], b(k, j) = tb ? B[j ldb + k] :
+// B[k ldb + j]. fp64 accumulation, k ascending per lane, fixed-shape lane reduction: deterministic.
+// (!ta, tb): k is contiguous in both operands -> a warp per output, lanes stride k; otherwise a
+// thread per output with j across the warp (coalesced B rows, broadcast A).
+namespace {
+__global__ void small_gemm_warp_kernel(int M, int N, int K, const float* __restrict__ A, int64_t lda,
+                                       const float* __restrict__ B, int64_t ldb, float* C, int64_t ldc) {
+    const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= int64_t(M) * N) return;
+    const int i = static_cast<int>(w / N), j = static_cast<int>(w % N);
+    double acc = 0.0;
+    for (int k = lane; k < K; k += 32) acc += double(A[i * lda + k]) * double(B[j * ldb + k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) C[i * ldc + j] = static_cast<float>(acc);
+}
+__global__ void small_gemm_thread_kernel(int M, int N, int K, const float* __restrict__ A, int64_t lda, bool ta,
+                                         const float* __restrict__ B, int64_t ldb, bool tb, float* C, int64_t ldc) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (t >= int64_t(M) * N) return;
+    const int i = static_cast<int>(t / N), j = static_cast<int>(t % N);
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) {
+        const float a = ta ? A[int64_t(k) * lda + i] : A[i * lda + k];
+        const float b = tb ? B[j * ldb + k] : B[int64_t(k) * ldb + j];
+        acc += double(a) * double(b);
+    }
+    C[i * ldc + j] = static_cast<float>(acc);
+}
+}  // namespace
+
+void small_gemm(int M, int N, int K, const float* A, int64_t lda, bool ta, const float* B, int64_t ldb, bool tb,
+                float* C, int64_t ldc, cudaStream_t s) {
+    const int64_t outs = int64_t(M) * N;
+    if (outs <= 0) return;
+    if (!ta && tb) {
+        small_gemm_warp_kernel<<<static_cast<unsigned>((outs * 32 + 255) / 256), 256, 0, s>>>(M, N, K, A, lda, B, ldb,
+                                                                                              C, ldc);
+    } else {
+        small_gemm_thread_kernel<<<static_cast<unsigned>((outs + 255) / 256), 256, 0, s>>>(M, N, K, A, lda, ta, B, ldb,
+                                                                                          tb, C, ldc);
+    }
+    SC_LAUNCH_CHECK();
+    count_launch();
+}
+
 void absmax(int64_t n, const float* x, float* out, cudaStream_t s) {
     if (n <= 0) return;
     absmax_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, x, out);

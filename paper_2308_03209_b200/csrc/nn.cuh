@@ -51,6 +51,9 @@ void gather_rows(int64_t n, int32_t d, const int32_t* rows, const float* src, fl
 
 // *out = max(*out, max |x[0..n)|) (non-negative floats compare like their bit patterns).
 void absmax(int64_t n, const float* x, float* out, cudaStream_t s);
+// C[M x N] = op(A) op(B) in fp32 with fp64 accumulation (small weight-space products).
+void small_gemm(int M, int N, int K, const float* A, int64_t lda, bool ta, const float* B, int64_t ldb, bool tb,
+                float* C, int64_t ldc, cudaStream_t s);
 
 // Weight gradient: C[N1 x N2] = A^T [N1 x M] * Bcat [M x N2], where Bcat's
 // columns [0, n2a) come from b1 and [n2a, N2) from b2 (b2 may gather rows).

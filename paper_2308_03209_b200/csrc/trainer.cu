@@ -129,6 +129,24 @@ void init_model(sc_trainer* t) {
     init_params_device(t->ctx, t->d, t->hidden.data(), t->L, t->C, t->seed, t->theta.get());
     t->amax.alloc(sc_trainer::kSlotBase + 2 * std::max(t->L, 1));
     t->tc.init(t);
+    const char* e = std::getenv("SC_FUSE_TOP");
+    t->fuse_top = t->L >= 1 && t->tc.enabled && !(e && e[0] == '0');
+    if (t->fuse_top) {
+        const LayerOff& lo = t->lay[t->L - 1];
+        t->Z.alloc(int64_t(t->C) * (lo.H + lo.in));
+        t->Xp.alloc(int64_t(t->C) * (lo.H + lo.in));
+        t->z_version = 0;
+    }
+}
+
+// Z = head U_{L-1} (C x (H + in)) for the current weights (composed top layer)
+void ensure_z(sc_trainer* t, cudaStream_t s) {
+    if (t->z_version == t->tc.version) return;
+    const LayerOff& lo = t->lay[t->L - 1];
+    const int zl = lo.H + lo.in;
+    small_gemm(t->C, zl, lo.H, t->theta.get() + t->head_off, t->E, false, t->theta.get() + lo.U, zl, false,
+               t->Z.get(), zl, s);
+    t->z_version = t->tc.version;
 }
 }  // namespace
 
@@ -330,7 +348,9 @@ size_t carve_train(sc_trainer* t, float* base, int64_t n) {
     t->MSG.assign(t->L, nullptr);
     t->MEAN.assign(t->L, nullptr);
     t->POS.assign(t->L, nullptr);
-    for (int l = 0; l < t->L; ++l) t->X[l + 1] = c.take(size_t(n) * t->lay[l].H);
+    // X[L] (the embedding) is never formed when the top layer is composed with the head
+    for (int l = 0; l < t->L; ++l)
+        if (!(t->fuse_top && l == t->L - 1)) t->X[l + 1] = c.take(size_t(n) * t->lay[l].H);
     float* shared_msg = t->compact && t->L > 0 ? c.take(size_t(n) * maxH) : nullptr;
     for (int l = 0; l < t->L; ++l) {
         t->MSG[l] = t->compact ? shared_msg : c.take(size_t(n) * t->lay[l].H);
@@ -420,6 +440,18 @@ void forward(sc_trainer* t, const Rows& R, float* logits, const Acts& A) {
         P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
         spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, A.inv, A.MSG[l], A.MEAN[l], s, R.hv, t->heavy_ws.get());
         P.end(s);
+        if (t->fuse_top && l == t->L - 1) {
+            // logits = h_L head^T = mean Z_L^T + h Z_R^T   (nn.hpp:233-234, 240 composed)
+            ensure_z(t, s);
+            const int zl = lo.H + lo.in;
+            const MatA mean{A.MEAN[l], lo.H, nullptr, lo.H};
+            const MatB zL{t->Z.get(), zl, false}, zR{t->Z.get() + lo.H, zl, false};
+            P.begin("gemm_head", 4.0 * n * (lo.H + lo.in + t->C), s, 2.0 * n * zl * t->C);
+            t->tc.nt(t, mean, t->amax_msg(l), zL, &xin, xin_amax, &zR, logits, t->Cp, n, t->C, kEpiNone, nullptr,
+                     nullptr);
+            P.end(s);
+            return;
+        }
         // h' = mean U_L^T + h U_R^T   (nn.hpp:233-234)
         const MatB uL{t->theta.get() + lo.U, lo.H + lo.in, false};
         const MatB uR{t->theta.get() + lo.U + lo.H, lo.H + lo.in, false};
@@ -436,6 +468,50 @@ void forward(sc_trainer* t, const Rows& R, float* logits, const Acts& A) {
     t->tc.nt(t, emb, emb_amax, MatB{t->theta.get() + t->head_off, t->E, false}, nullptr, nullptr, nullptr, logits,
              t->Cp, n, t->C, kEpiNone, nullptr, nullptr);
     P.end(s);
+}
+
+// Layers l = top .. 0 of sage_backward (nn.hpp:262-291) given dh of layer `top` in `dh` (amax in
+// dh_amax); layer top's dmean / dU come from the caller when `top_done` (composed top layer).
+void backward_layers(sc_trainer* t, const Rows& R, int i, int top, float* dh, float* dh_amax, float* dh2,
+                     float* dh2_amax, bool top_done);
+
+// The composed top layer's backward (see sc_trainer::fuse_top), then layers L-2 .. 0 as usual.
+void backward_fused(sc_trainer* t, const Rows& R, int i) {
+    const int round = i / t->world;
+    cudaStream_t s = t->ctx->stream;
+    Profiler& P = t->prof;
+    const int64_t n = R.n;
+    const int T = t->L - 1;
+    const LayerOff& lo = t->lay[T];
+    const int zl = lo.H + lo.in;
+    const MatT x0t{R.x0, R.x0_ld, nullptr, t->d};
+    const MatT xint = T == 0 ? x0t : MatT{t->X[T], lo.in, nullptr, lo.in};
+    const float* xin_amax = T == 0 ? t->g->feat_amax.get() : t->amax_x(T);
+    const MatT meant{t->MEAN[T], lo.H, nullptr, lo.H};
+    const MatT gt{t->G, t->Cp, nullptr, t->C};
+    const MatA ga{t->G, t->Cp, nullptr, t->C};
+    // Xp = G^T [mean | h_in]; dHead = Xp U^T (nn.hpp:259 with emb = mean U_L^T + h U_R^T);
+    // dU = head^T Xp (:271-272 with dh = G head)
+    ensure_z(t, s);
+    P.begin("wgrad", 4.0 * n * (t->C + zl), s, 2.0 * n * t->C * zl);
+    t->tc.tn(t, gt, R.g_amax, meant, t->amax_msg(T), &xint, xin_amax, n, t->Xp.get(), zl);
+    P.end(s);
+    P.begin("wgrad_small", 4.0 * t->C * zl * 2 + 4.0 * lo.H * zl, s, 2.0 * t->C * zl * lo.H * 2);
+    small_gemm(t->C, t->E, zl, t->Xp.get(), zl, false, t->theta.get() + lo.U, zl, true, t->slot_ptr(2 * t->L, i),
+               t->E, s);
+    small_gemm(lo.H, zl, t->C, t->theta.get() + t->head_off, t->E, true, t->Xp.get(), zl, false,
+               t->slot_ptr(2 * T + 1, i), zl, s);
+    P.end(s);
+    exchange_bucket(t, 2 * t->L, round);
+    exchange_bucket(t, 2 * T + 1, round);
+    // dmean_s = inv * (dh U_L) = inv * (G Z_L)   (:274)
+    float* dh2 = t->dmean;
+    float* dh2_amax = t->amax_slot(sc_trainer::kSlotDh1);
+    P.begin("gemm_dgrad", 4.0 * n * (t->C + lo.H + 1), s, 2.0 * n * t->C * lo.H);
+    t->tc.nt(t, ga, R.g_amax, MatB{t->Z.get(), zl, true}, nullptr, nullptr, nullptr, dh2, lo.H, n, lo.H,
+             kEpiRowScale, t->inv, nullptr);
+    P.end(s);
+    backward_layers(t, R, i, T, t->dh, t->amax_slot(sc_trainer::kSlotDh0), dh2, dh2_amax, true);
 }
 
 // sage_backward (nn.hpp:246-293) into partition i's gradient slot; each
@@ -455,6 +531,10 @@ void backward(sc_trainer* t, const Rows& R, int i) {
     Profiler& P = t->prof;
     const int64_t n = R.n;
     const MatT x0t{R.x0, R.x0_ld, nullptr, t->d};
+    if (t->fuse_top) {
+        backward_fused(t, R, i);
+        return;
+    }
     const MatT embt = t->L == 0 ? x0t : MatT{t->X[t->L], t->E, nullptr, t->E};
     // head grad = G^T emb (side) ; dh = G head (main)   (:259-260)
     hand_off(s, w);
@@ -479,24 +559,47 @@ void backward(sc_trainer* t, const Rows& R, int i) {
     t->tc.nt(t, MatA{t->G, t->Cp, nullptr, t->C}, R.g_amax, MatB{t->theta.get() + t->head_off, t->E, true},
              nullptr, nullptr, nullptr, dh, t->E, n, t->E, kEpiNone, nullptr, dh_amax);
     P.end(s);
-    for (int l = t->L - 1; l >= 0; --l) {
+    backward_layers(t, R, i, t->L - 1, dh, dh_amax, dh2, dh2_amax, false);
+}
+
+void backward_layers(sc_trainer* t, const Rows& R, int i, int top, float* dh, float* dh_amax, float* dh2,
+                     float* dh2_amax, bool top_done) {
+    const int round = i / t->world;
+    cudaStream_t s = t->ctx->stream;
+    cudaStream_t w = t->overlap ? t->side : s;
+    float* ws_w = t->overlap ? t->ws_side.get() : t->ws.get();
+    auto hand_off = [&](cudaStream_t from, cudaStream_t to) {
+        if (from == to) return;
+        cudaEvent_t ev = t->fork_event();
+        SC_CUDA(cudaEventRecord(ev, from));
+        SC_CUDA(cudaStreamWaitEvent(to, ev, 0));
+    };
+    Profiler& P = t->prof;
+    const int64_t n = R.n;
+    const MatT x0t{R.x0, R.x0_ld, nullptr, t->d};
+    const float* x0_amax = t->g->feat_amax.get();
+    for (int l = top; l >= 0; --l) {
         const LayerOff& lo = t->lay[l];
+        const bool composed = top_done && l == top;  // dmean and dU already done (backward_fused)
         const MatT xint = l == 0 ? x0t : MatT{t->X[l], lo.in, nullptr, lo.in};
         const MatT dht{dh, lo.H, nullptr, lo.H};
         const MatT meant{t->MEAN[l], lo.H, nullptr, lo.H};
         const float* xin_amax = l == 0 ? x0_amax : t->amax_x(l);
-        // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
-        P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s, 2.0 * n * lo.H * lo.H);
-        t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true}, nullptr,
-                 nullptr, nullptr, dh2, lo.H, n, lo.H, kEpiRowScale, t->inv, nullptr);
-        P.end(s);
+        if (!composed) {
+            // dmean_s = inv * (dh U_L)   (:274, pre-scaled for the pull aggregation)
+            P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + 1), s, 2.0 * n * lo.H * lo.H);
+            t->tc.nt(t, MatA{dh, lo.H, nullptr, lo.H}, dh_amax, MatB{t->theta.get() + lo.U, lo.H + lo.in, true},
+                     nullptr, nullptr, nullptr, dh2, lo.H, n, lo.H, kEpiRowScale, t->inv, nullptr);
+            P.end(s);
+        }
         // One launch for dU = dh^T [mean | h_in] (:271-272) and dW = dz^T h_in (:289) after the
         // transposed aggregation, so h_in (and the tiles' conversions) stream once for both;
         // otherwise dU runs first (optionally on the side stream) and dW after.
         float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
         const MatT dzt{t->dz, lo.H, nullptr, lo.H};
-        const bool dual = !t->overlap && t->tc.enabled && t->tc.dual && tn_dual_supported(dht, dzt, meant, xint);
-        if (!dual) {
+        const bool dual = !composed && !t->overlap && t->tc.enabled && t->tc.dual &&
+                          tn_dual_supported(dht, dzt, meant, xint);
+        if (!dual && !composed) {
             hand_off(s, w);
             P.begin("wgrad", 4.0 * n * (2 * lo.H + lo.in), w, 2.0 * n * lo.H * (lo.H + lo.in));
             t->tc.tn(t, dht, dh_amax, meant, t->amax_msg(l), &xint, xin_amax, n, t->slot_ptr(2 * l + 1, i),
@@ -525,12 +628,20 @@ void backward(sc_trainer* t, const Rows& R, int i) {
         }
         exchange_bucket(t, 2 * l, round);
         if (l > 0) {  // dh = dh U_R + dz W   (:275, :290); layer 0's is unused
-            const MatA dhA{dh, lo.H, nullptr, lo.H}, dzA{t->dz, lo.H, nullptr, lo.H};
-            P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s, 2.0 * n * 2 * lo.H * lo.in);
+            const MatA dzA{t->dz, lo.H, nullptr, lo.H};
             const MatB wB{t->theta.get() + lo.W, lo.in, true};
             SC_CUDA(cudaMemsetAsync(dh2_amax, 0, sizeof(float), s));
-            t->tc.nt(t, dhA, dh_amax, MatB{t->theta.get() + lo.U + lo.H, lo.H + lo.in, true}, &dzA, dz_amax, &wB, dh2,
-                     lo.in, n, lo.in, kEpiNone, nullptr, dh2_amax);
+            if (composed) {  // dh U_R = G head U_R = G Z_R
+                const int zl = lo.H + lo.in;
+                P.begin("gemm_dgrad", 4.0 * n * (t->C + lo.H + lo.in), s, 2.0 * n * (t->C + lo.H) * lo.in);
+                t->tc.nt(t, MatA{t->G, t->Cp, nullptr, t->C}, R.g_amax, MatB{t->Z.get() + lo.H, zl, true}, &dzA,
+                         dz_amax, &wB, dh2, lo.in, n, lo.in, kEpiNone, nullptr, dh2_amax);
+            } else {
+                const MatA dhA{dh, lo.H, nullptr, lo.H};
+                P.begin("gemm_dgrad", 4.0 * n * (2 * lo.H + lo.in), s, 2.0 * n * 2 * lo.H * lo.in);
+                t->tc.nt(t, dhA, dh_amax, MatB{t->theta.get() + lo.U + lo.H, lo.H + lo.in, true}, &dzA, dz_amax, &wB,
+                         dh2, lo.in, n, lo.in, kEpiNone, nullptr, dh2_amax);
+            }
             P.end(s);
             std::swap(dh, dh2);
             std::swap(dh_amax, dh2_amax);

@@ -162,6 +162,14 @@ struct sc_trainer {
     double last_loss = 0, last_gnorm = 0;
     sc::TcGemm tc;
     sc::Profiler prof;
+    // Composed top layer (tensor-core path, L >= 1, SC_FUSE_TOP != 0): the last layer's update
+    // h_L = mean U_L^T + h U_R^T and the head logits = h_L head^T are both linear, so
+    // logits = mean Z_L^T + h Z_R^T with Z = head U_{L-1} (C x (H + in), once per weight version),
+    // and h_L is never formed. Backward: Xp = G^T [mean | h] (one TN GEMM with C output rows) gives
+    // dHead = Xp U^T and dU_{L-1} = head^T Xp; dmean = inv (G Z_L); dh_{L-1} = G Z_R + dz W.
+    bool fuse_top = false;
+    sc::DevBuf<float> Z, Xp;
+    uint64_t z_version = 0;
     // Host transport (sc_trainer_set_exchange), used instead of NCCL when set.
     using ExchangeFn = int32_t (*)(void*, int32_t, int32_t, int32_t, const void*, void*, int64_t);
     ExchangeFn xfn = nullptr;

@@ -53,3 +53,61 @@ def test_world_invariance(case, world, tmp_path):
         assert z["local"].tolist() == list(range(r, p, world))
         assert int(z["audit"][0]) == len(z["local"]) * P and int(z["audit"][1]) == 0
     assert int(ref["audit"][0]) == p * P
+
+
+def test_emulated_rank_matches_its_share():
+    """sc_trainer_emulate_rank (the bench's configs[4] run: rank 0 of an 8-GPU job on one GPU): the
+    rank holds and trains exactly its partitions (i % world == rank), each partition's gradient and
+    loss are bitwise those of the full world-1 run, and with the exchange skipped the gathered
+    gradient is the ordered sum of this rank's partitions only (the others' slots stay zero)."""
+    from cpu_libs import oracle
+    from paper_2308_03209_b200 import sagecut as sc
+    from test_gpu_parity import gpu_graph
+    og = oracle().graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    cfg = sc.TrainConfig(layers=2, hidden=[16, 16], use_dropedge=True, seed=1)
+    g1 = gpu_graph(sc, og, 8)
+    t1 = sc.CoFreeTrainer(g1, sc.partition_random(g1, 8, 3), cfg)
+    t1.step(0)
+    world, rank = 4, 0
+    g2 = gpu_graph(sc, og, 8)
+    g2.set_part_ownership(rank, world)
+    part2 = sc.partition_random(g2, 8, 3)
+    assert [part2.part_held(i) for i in range(8)] == [i % world == rank for i in range(8)]
+    t2 = sc.CoFreeTrainer(g2, part2, cfg, rank=rank, world=world, _defer_comm=True)
+    t2.emulate_rank()
+    t2.step(0)
+    mine = list(range(rank, 8, world))
+    expect = np.zeros(t1.param_count, np.float32)
+    for i in mine:
+        np.testing.assert_array_equal(t2.part_grads(i), t1.part_grads(i))
+        assert t2.part_loss(i) == t1.part_loss(i)
+        expect = expect + t1.part_grads(i)  # float32, ascending partition order
+    np.testing.assert_array_equal(t2.grads(), expect)
+
+
+def test_feature_rows_fill_same_bits():
+    """set_data(features=None, dim) + set_feature_rows in chunks (host and device sources; the bench's
+    device-side synthesis for configs[4]) trains bitwise like set_data with the whole matrix."""
+    import torch
+    from cpu_libs import oracle
+    from paper_2308_03209_b200 import sagecut as sc
+    from test_gpu_parity import gpu_graph
+    og = oracle().graph_sbm(200, 4, 0.15, 0.01, 8, 0.3, 7)
+    cfg = sc.TrainConfig(layers=2, hidden=[16, 16], use_dropedge=True, seed=1)
+    ga = gpu_graph(sc, og, 8)
+    ta = sc.CoFreeTrainer(ga, sc.partition_random(ga, 4, 3), cfg)
+    la = [ta.step(e)[0] for e in range(3)]
+    feats = og.features(8).astype(np.float32)
+    gb, _ = sc.build_graph(og.n, og.edges())
+    tr, va, te = og.masks()
+    gb.set_data(None, og.labels(), int(og.labels().max()) + 1, tr, va, te, dim=8)
+    gb.set_feature_rows(0, feats[:70])                      # host rows
+    dev = torch.from_numpy(feats[70:]).cuda()
+    torch.cuda.synchronize()
+    gb.set_feature_rows(70, device_ptr=dev.data_ptr(), num_rows=dev.shape[0])  # device rows
+    tb = sc.CoFreeTrainer(gb, sc.partition_random(gb, 4, 3), cfg)
+    lb = [tb.step(e)[0] for e in range(3)]
+    assert la == lb
+    np.testing.assert_array_equal(ta.params(), tb.params())
+    with pytest.raises(Exception, match="out of range"):
+        gb.set_feature_rows(og.n - 1, feats[:2])
