@@ -724,14 +724,13 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
 struct NtTmCfg {
     static constexpr int kCW = 8;                       // converter warps
     static constexpr int kMma = kCW + kNtEpiWarps, kLoad = kMma + 1, kThr = (kLoad + 1) * 32;
-    static constexpr int kStg = 4;                      // fp32 staging slots
-    static constexpr int kMaxKb = 8;                    // K <= 256
-    static constexpr int kBOff = 0;                     // resident B' (<= kMaxKb x n_pad x 64 B per CTA)
+    static constexpr int kMaxStg = 12;                  // fp32 staging slots (as many as fit after B')
+    static constexpr int kMaxKb = 8;                    // A' stages in TMEM (256 columns)
+    static constexpr int kBOff = 0;                     // resident B' (<= kBBytes per CTA), then the staging ring
     static constexpr int kBBytes = kMaxKb * 2 * (kMaxN / 2) * 64;  // k-blocks x {hi, lo} x this CTA's rows x 64 B
-    static constexpr int kStgOff = kBOff + kBBytes;
-    static constexpr int kEpiOff = kStgOff + kStg * kNtStgBytes;
-    static constexpr int kBarOff = kEpiOff + kNtEpiBytes;
-    static constexpr int kSmem = kBarOff + 256 + 1024;
+    static constexpr int kSmem = kBBytes + 4 * kNtStgBytes + kNtEpiBytes + 512 + 1024;
+    static constexpr int kBarOff = kSmem - 1024 - 512;  // barriers + TMEM slot (after the 1 KB alignment slack)
+    static constexpr int kEpiOff = kBarOff - kNtEpiBytes;
     static constexpr int kRows = 2 * kBM;
 };
 static_assert(NtTmCfg::kSmem <= 232448, "NT (A in TMEM) shared memory");
@@ -742,14 +741,13 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* bres = smem + Cfg::kBOff;
-    uint8_t* stg_base = smem + Cfg::kStgOff;
     uint8_t* epi_base = smem + Cfg::kEpiOff;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
     uint64_t* full = bars;                       // [kMaxKb] converters -> MMA (leader's)
     uint64_t* empty = full + Cfg::kMaxKb;        // [kMaxKb] MMA -> converters
-    uint64_t* sfull = empty + Cfg::kMaxKb;       // [kStg] loader (tx) -> converters
-    uint64_t* sempty = sfull + Cfg::kStg;        // [kStg] converters -> loader
-    uint64_t* tfull = sempty + Cfg::kStg;        // [2] MMA -> epilogue
+    uint64_t* sfull = empty + Cfg::kMaxKb;       // [kMaxStg] loader (tx) -> converters
+    uint64_t* sempty = sfull + Cfg::kMaxStg;     // [kMaxStg] converters -> loader
+    uint64_t* tfull = sempty + Cfg::kMaxStg;     // [2] MMA -> epilogue
     uint64_t* tempty = tfull + 2;                // [2] epilogue -> MMA (leader's)
     uint64_t* bready = tempty + 2;               // resident B' landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
@@ -757,13 +755,26 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const int64_t tile0 = blockIdx.x >> 1, tstep = gridDim.x >> 1;
-    const Src& S = p.src[0];
-    const int kbl = S.kblocks;                                  // <= kMaxKb
+    const int kb0 = p.src[0].kblocks;                           // k-blocks of source 0 (source 1 follows)
+    const int kbl = kb0 + (p.nsrc > 1 ? p.src[1].kblocks : 0);  // per tile, both sources
     const int np = p.n_pad > kBM ? 2 : 1;                       // passes
     const int Np = p.n_pad / np;                                // MMA N (multiple of 32)
+    // A' stage ring: one pass -> kMaxKb stages, each released after its MMAs; two passes -> the
+    // tile's whole K stays resident (kbl stages) until the second pass has read it.
+    const int R = np > 1 ? kbl : Cfg::kMaxKb;
     const uint32_t bt = static_cast<uint32_t>(Np / 2) * 64u;    // one resident (pass, kb, plane) tile
-    const int kt = scale_exp(*S.amax_a) + *S.bexp;
-    const float sa = ldexpf(1.f, kt - *S.bexp);
+    // the staging ring takes the shared memory the resident B' leaves (a small weight image -> more
+    // fp32 rows in flight: the narrow-N GEMMs stream A and are bound by the HBM bytes in flight)
+    const uint32_t stg_off = (static_cast<uint32_t>(np * kbl * 2) * bt + 1023u) & ~1023u;
+    const int nstg = min(Cfg::kMaxStg, static_cast<int>((Cfg::kEpiOff - stg_off) / kNtStgBytes));
+    uint8_t* stg_base = smem + stg_off;
+    int kt = 1 << 20;
+    int bexp[2] = {0, 0};
+    for (int q = 0; q < p.nsrc; ++q) {
+        bexp[q] = *p.src[q].bexp;
+        kt = min(kt, scale_exp(*p.src[q].amax_a) + bexp[q]);
+    }
+    const float sa0 = ldexpf(1.f, kt - bexp[0]), sa1 = ldexpf(1.f, kt - bexp[1]);
 
     if (warp == Cfg::kMma) {
         if (lane == 0) {
@@ -771,7 +782,7 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
                 mbar_init(&full[s], Cfg::kCW * 2);
                 mbar_init(&empty[s], 1);
             }
-            for (int s = 0; s < Cfg::kStg; ++s) {
+            for (int s = 0; s < Cfg::kMaxStg; ++s) {
                 mbar_init(&sfull[s], 1);
                 mbar_init(&sempty[s], Cfg::kCW);
             }
@@ -794,28 +805,29 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
 
     if (warp == Cfg::kLoad) {
         if (lane == 0) {
-            // resident B': for pass h, k-block kb, plane q, this CTA's Np / 2 rows of the image
-            // (image rows [kb][q][n_pad]; pass h covers columns h Np .. h Np + Np - 1, split by rank).
-            // Both CTAs' bytes are counted on the leader's barrier (its MMAs read both halves).
+            // resident B': for pass h, k-block kb (both sources), plane q, this CTA's Np / 2 rows of the
+            // source's image (rows [kb][q][n_pad]; pass h covers columns h Np .. h Np + Np - 1, split by
+            // rank). Both CTAs' bytes are counted on the leader's barrier (its MMAs read both halves).
             if (rank == 0) mbar_arrive_expect_tx(bready, 2u * static_cast<uint32_t>(np * kbl * 2) * bt);
             const uint32_t bready_l = mapa(smem_u32(bready), 0);
             for (int h = 0; h < np; ++h)
                 for (int kb = 0; kb < kbl; ++kb)
-                    for (int q = 0; q < 2; ++q)
-                        tma_load_2d_pair(bres + ((h * kbl + kb) * 2 + q) * bt, &S.tmap_b, 0,
-                                         (kb * 2 + q) * p.n_pad + h * Np + static_cast<int32_t>(rank) * (Np / 2),
+                    for (int q = 0; q < 2; ++q) {
+                        const int src = kb < kb0 ? 0 : 1, kl = kb < kb0 ? kb : kb - kb0;
+                        tma_load_2d_pair(bres + ((h * kbl + kb) * 2 + q) * bt, &p.src[src].tmap_b, 0,
+                                         (kl * 2 + q) * p.n_pad + h * Np + static_cast<int32_t>(rank) * (Np / 2),
                                          bready_l);
+                    }
         }
         __syncwarp();
         Ring ring;
         for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
-            for (int kb = 0; kb < kbl; ++kb, ring.next(Cfg::kStg)) {
-                if (p.prefetch && kb == 0 && tile + tstep < p.tiles && lane < kbl)
-                    tma_prefetch_2d(&S.tmap, lane * kNtBK, static_cast<int32_t>((tile + tstep) * Cfg::kRows + rank * kBM));
+            for (int kb = 0; kb < kbl; ++kb, ring.next(nstg)) {
+                const int src = kb < kb0 ? 0 : 1, kl = kb < kb0 ? kb : kb - kb0;
                 mbar_wait(&sempty[ring.idx], ring.phase ^ 1);
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&sfull[ring.idx], kNtStgBytes);
-                    tma_load_2d(stg_base + ring.idx * kNtStgBytes, &S.tmap, kb * kNtBK,
+                    tma_load_2d(stg_base + ring.idx * kNtStgBytes, &p.src[src].tmap, kl * kNtBK,
                                 static_cast<int32_t>(tile * Cfg::kRows + rank * kBM), &sfull[ring.idx]);
                 }
                 __syncwarp();
@@ -823,14 +835,16 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
     } else if (warp < Cfg::kCW) {
         // converters: warp w owns TMEM lane quarter q = w & 3 (rows 32q + lane) and k half kh = w >> 2
         // of each 32-k stage: 16 fp32 of its row (4 x LDS.128 from the SW128 staging) -> 8 hi + 8 lo
-        // columns of A' stage kb (hi at column 32 kb + 8 kh, lo 16 columns further).
+        // columns of A' stage st (hi at column 32 st + 8 kh, lo 16 columns further).
         const int q = warp & 3, kh = warp >> 2;
         const int r = 32 * q + lane;
         Ring sr;
-        uint32_t t = 0;
-        for (int64_t tile = tile0; tile < p.tiles; tile += tstep, ++t)
-            for (int kb = 0; kb < kbl; ++kb, sr.next(Cfg::kStg)) {
-                mbar_wait(&empty[kb], (t & 1) ^ 1);  // the previous tile's last pass has read stage kb
+        uint32_t g = 0;  // k-blocks converted so far (A' ring position)
+        for (int64_t tile = tile0; tile < p.tiles; tile += tstep)
+            for (int kb = 0; kb < kbl; ++kb, sr.next(nstg), ++g) {
+                const uint32_t st = g % R;
+                const float sa = kb < kb0 ? sa0 : sa1;
+                mbar_wait(&empty[st], ((g / R) & 1) ^ 1);  // the MMAs that read this stage last are done
                 mbar_wait(&sfull[sr.idx], sr.phase);
                 const uint8_t* rowp = stg_base + sr.idx * kNtStgBytes + r * (kNtBK * 4);
                 float4 x[4];
@@ -844,14 +858,14 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
                     split2(x[c].z, x[c].w, sa, hi[2 * c + 1], lo[2 * c + 1]);
                 }
                 tc_fence_after();  // orders the stores after the MMAs that read this stage last
-                const uint32_t tcol = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + kb * 32 + 8 * kh;
+                const uint32_t tcol = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + st * 32 + 8 * kh;
                 tmem_st8(tcol, hi);
                 tmem_st8(tcol + 16, lo);
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive_cluster(full_l + kb * 8);
+                    mbar_arrive_cluster(full_l + st * 8);
                     mbar_arrive(&sempty[sr.idx]);
                 }
             }
@@ -867,8 +881,9 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + 256 + acc * Np;
                     for (int kb = 0; kb < kbl; ++kb) {
+                        const uint32_t g = t * kbl + kb, st = g % R;
                         if (h == 0) {
-                            mbar_wait_cluster(&full[kb], t & 1);
+                            mbar_wait_cluster(&full[st], (g / R) & 1);
                             tc_fence_after();
                         }
                         if (lane == 0) {
@@ -877,12 +892,12 @@ __global__ void __launch_bounds__(NtTmCfg::kThr, 1) gemm_nt_tm_kernel(const __gr
 #pragma unroll
                             for (int k = 0; k < kNtBK / 16; ++k) {
                                 const uint64_t adv = static_cast<uint64_t>(k * 32) >> 4;
-                                const uint32_t tah = tmem_base + kb * 32 + k * 8;  // lo plane 16 columns after hi
+                                const uint32_t tah = tmem_base + st * 32 + k * 8;  // lo plane 16 columns after hi
                                 mma_f16_ts_pair(d_tmem, tah, bhi + adv, idesc, (kb | k) ? 1u : 0u);
                                 mma_f16_ts_pair(d_tmem, tah, blo + adv, idesc, 1u);
                                 mma_f16_ts_pair(d_tmem, tah + 16, bhi + adv, idesc, 1u);
                             }
-                            if (h == np - 1) mma_commit_g<true>(&empty[kb]);
+                            if (h == np - 1) mma_commit_g<true>(&empty[st]);
                             if (kb == kbl - 1) mma_commit_g<true>(&tfull[acc]);
                         }
                         __syncwarp();
@@ -1658,9 +1673,10 @@ void encode_img(CUtensorMap* map, const uint8_t* img, int64_t rows, uint32_t box
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (image) failed (" + std::to_string(int(r)) + ")");
 }
-// Single-source NT GEMMs with K <= 256 and the A'-in-TMEM kernel. SC_NT_TM: 0 off, 1 (default)
-// for N <= 128 (one pass: the head GEMM), 2 also two-pass N = 256 (msg, dmean, head dgrad:
-// measured slower, profiles/r02_nt_tm_ab.txt).
+// Which NT GEMMs run on the A'-in-TMEM kernel, SC_NT_TM bit mask: 1 (default) one source, N <= 128
+// (one pass: the head GEMM); 2 one source, N = 256 as two passes, K <= 256 (msg, dmean: measured
+// slower, profiles/r02_nt_tm_ab.txt); 4 two sources, N <= 128 (the composed head: measured 0.6 ms
+// per epoch slower than the general kernel, profiles/r02_nt_tm_ab.txt).
 int nt_tm_mode() {
     static const int mode = [] {
         const char* e = std::getenv("SC_NT_TM");
@@ -1968,12 +1984,19 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.prefetch = nt_pf;
     const bool pair = nt_pair_enabled();
     // single source, K <= 256: the A'-in-TMEM kernel with the weight image resident in shared memory
+    // one pass (N <= 128): A' streams through an 8-stage TMEM ring, both sources, the weight images
+    // resident in shared memory if they fit; two passes (N = 256, SC_NT_TM=2): one source, K <= 256.
     const int tm_mode = nt_tm_mode();
-    const bool tm = pair && tm_mode > 0 && p.nsrc == 1 && b1.kblocks <= tc::NtTmCfg::kMaxKb &&
-                    (b1.n_pad <= tc::kBM || (tm_mode > 1 && b1.n_pad % 64 == 0));
+    const int kb_all = b1.kblocks + (p.nsrc > 1 ? bs[1]->kblocks : 0);
+    const bool tm1 = (tm_mode & (p.nsrc == 1 ? 1 : 4)) && b1.n_pad <= tc::kBM &&
+                     int64_t(kb_all) * b1.n_pad * 64 <= tc::NtTmCfg::kBBytes;
+    const bool tm2 = (tm_mode & 2) && p.nsrc == 1 && b1.kblocks <= tc::NtTmCfg::kMaxKb && b1.n_pad % 64 == 0;
+    const bool tm = pair && (tm1 || tm2);
     if (tm) {
         const int np = b1.n_pad > tc::kBM ? 2 : 1;
-        encode_img(&p.src[0].tmap_b, b1.img.get(), int64_t(b1.kblocks) * 2 * b1.n_pad, b1.n_pad / np / 2);
+        for (int i = 0; i < p.nsrc; ++i)
+            encode_img(&p.src[i].tmap_b, bs[i]->img.get(), int64_t(bs[i]->kblocks) * 2 * bs[i]->n_pad,
+                       bs[i]->n_pad / np / 2);
     } else if (pair) {
         for (int i = 0; i < p.nsrc; ++i)
             encode_img(&p.src[i].tmap_b, bs[i]->img.get(), int64_t(bs[i]->kblocks) * 2 * bs[i]->n_pad, bs[i]->n_pad / 2);

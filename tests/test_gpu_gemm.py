@@ -29,6 +29,10 @@ CASES = [  # M, N, K1, b1_nn, K2, b2_nn, gather, epi
     (513, 48, 64, False, 16, False, False, 1),
     (257, 12, 20, False, 0, False, False, 0),
     (300_000, 256, 256, False, 0, False, False, 1),
+    (5000, 47, 256, False, 256, False, False, 0),   # the composed head: [mean | h] Z^T (A' ring, dual source)
+    (3001, 64, 256, True, 256, True, False, 2),
+    (2000, 100, 100, False, 256, False, True, 0),
+    (1000, 128, 320, False, 256, False, False, 0),  # weight images too large to stay resident: general kernel
 ]
 
 
@@ -59,7 +63,7 @@ def test_f16x3_matches_fp64(sc, case):
     e_tc, e_simt = rel(C_tc, ref), rel(C_simt, ref)
     print(f"{case}: tcgen05 fp16x3 rel err {e_tc:.2e}, simt fp32 {e_simt:.2e}")
     assert e_simt <= 1e-6
-    assert e_tc <= 2e-6
+    assert e_tc <= 2e-6 * max(1.0, (K1 + K2) / 512)  # the tensor core's truncating accumulation grows with K
 
 
 @pytest.mark.parametrize("sa,sb,sa2", [(1e-7, 1.0, 1.0), (3e4, 1e-3, 1e-5), (1.0, 1e-6, 1e3)])
@@ -156,12 +160,13 @@ def test_tn_smem_operand_path_subprocess():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("mode", ["0", "2"])
+@pytest.mark.parametrize("mode", ["0", "7"])
 def test_nt_tm_modes_subprocess(mode):
     """Single-source K <= 256 NT GEMMs with N <= 128 run on the A'-in-TMEM kernel (weight image
     resident in shared memory) by default. SC_NT_TM (read once per process) = 0 sends every NT GEMM
-    to the general CTA-pair kernel (A' and streamed weight tiles in shared memory); = 2 also runs
-    N = 256 on the A'-in-TMEM kernel as two N = 128 passes. Both must pass the same fp64 checks."""
+    to the general CTA-pair kernel (A' and streamed weight tiles in shared memory); = 7 also runs
+    N = 256 (two N = 128 passes) and two-source GEMMs on the A'-in-TMEM kernel. Both must pass the
+    same fp64 checks."""
     import os
     import subprocess
     import sys
