@@ -89,6 +89,8 @@ struct alignas(64) Params {
     const float* row_scale;
     float* amax_out;
     uint32_t* relu_pos;  // optional (EPI == kEpiRelu): bit c % 32 of word [row][c / 32] = C[row][c] > 0
+    const float* mask_msg;     // EPI == kEpiMask: C = 1[msg > 0] acc, msg row stride N ...
+    const uint32_t* mask_pos;  // ... or its sign bits ([row][ceil(N / 32)] words)
     int64_t tiles;
     unsigned long long* trace;  // optional (SC_TN_TRACE_BUILD + SC_TN_TRACE=1), as TnParams::trace
     int32_t prefetch;           // L2-prefetch the CTA's next tile's A rows at the start of each tile
@@ -195,6 +197,25 @@ __device__ __forceinline__ void split2(float x0, float x1, float s, uint32_t& hi
     const __half2 l = __float22half2_rn(d);
     hi = *reinterpret_cast<const uint32_t*>(&h);
     lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// kEpiMask: bit q = 1[msg[row][c0 + q] > 0] for the 32 columns from c0 (all-ones past M / N).
+__device__ __forceinline__ uint32_t mask_bits32(const Params& p, int64_t row, int32_t c0) {
+    if (row >= p.M || c0 >= p.N) return ~0u;
+    if (p.mask_pos) return p.mask_pos[row * ((p.N + 31) >> 5) + (c0 >> 5)];
+    const float* m = p.mask_msg + row * p.N + c0;
+    uint32_t b = 0;
+    if (c0 + 32 <= p.N && (p.N & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(m) + j);
+            b |= (v.x > 0.f ? 1u : 0u) << (4 * j) | (v.y > 0.f ? 1u : 0u) << (4 * j + 1) |
+                 (v.z > 0.f ? 1u : 0u) << (4 * j + 2) | (v.w > 0.f ? 1u : 0u) << (4 * j + 3);
+        }
+    } else {
+        for (int q = 0; q < 32 && c0 + q < p.N; ++q) b |= (m[q] > 0.f ? 1u : 0u) << q;
+    }
+    return b;
 }
 
 // K-major SWIZZLE_64B descriptor: 8-row core groups of 512 B (SBO), swizzle mode 4.
@@ -648,6 +669,8 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                 tmem_ld32(tmem_base + acc * 256 + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
                 if (lane == 0) TN_TIMED_WAIT(w_b, bulk_wait_read<0>());  // the previous store has read the box
                 __syncwarp();
+                uint32_t keep = ~0u;  // kEpiMask: the ReLU decisions of this row's 32 columns
+                if (EPI == kEpiMask) keep = mask_bits32(p, row0 + lane, c0);
                 uint32_t pos = 0;  // ReLU decisions of this row's 32 columns (compact activations)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -660,6 +683,7 @@ __global__ void __launch_bounds__(NtCfg<PAIR>::kThr, 1) gemm_f16x3_kernel(const 
                             pos |= (v > 0.f ? 1u : 0u) << (4 * j + q);
                         }
                         if (EPI == kEpiRowScale) v = sc * v;
+                        if (EPI == kEpiMask) v = ((keep >> (4 * j + q)) & 1u) ? v : 0.f;
                         if (AMAX) amx = fmaxf(amx, fabsf(v));
                         x[q] = v;
                     }
@@ -1936,7 +1960,8 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
 
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-                float* amax_out, cudaStream_t s, uint32_t* relu_pos) {
+                float* amax_out, cudaStream_t s, uint32_t* relu_pos, const float* mask_msg,
+                const uint32_t* mask_pos) {
     if (M <= 0 || N <= 0) return;
     if (!tc_supported(a1, a2, N) || !tc_out_supported(C, ldc))
         throw std::logic_error("gemm_f16x3: unsupported operand layout");
@@ -1967,6 +1992,9 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     p.row_scale = row_scale;
     p.amax_out = amax_out;
     p.relu_pos = epi == kEpiRelu ? relu_pos : nullptr;
+    p.mask_msg = mask_msg;
+    p.mask_pos = mask_pos;
+    if (epi == kEpiMask && !mask_msg && !mask_pos) throw std::logic_error("gemm_f16x3: mask epilogue without a mask");
     static const bool trace = [] {
         const char* e = std::getenv("SC_TN_TRACE");
         return e && std::atoi(e) != 0;
@@ -1991,7 +2019,7 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
     const bool tm1 = (tm_mode & (p.nsrc == 1 ? 1 : 4)) && b1.n_pad <= tc::kBM &&
                      int64_t(kb_all) * b1.n_pad * 64 <= tc::NtTmCfg::kBBytes;
     const bool tm2 = (tm_mode & 2) && p.nsrc == 1 && b1.kblocks <= tc::NtTmCfg::kMaxKb && b1.n_pad % 64 == 0;
-    const bool tm = pair && (tm1 || tm2);
+    const bool tm = pair && (tm1 || tm2) && epi != kEpiMask;  // (the A'-in-TMEM epilogue has no mask)
     if (tm) {
         const int np = b1.n_pad > tc::kBM ? 2 : 1;
         for (int i = 0; i < p.nsrc; ++i)
@@ -2047,6 +2075,10 @@ void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA
             amax ? dispatch(std::integral_constant<int, kEpiRowScale>{}, T{})
                  : dispatch(std::integral_constant<int, kEpiRowScale>{}, F{});
             break;
+        case kEpiMask:
+            amax ? dispatch(std::integral_constant<int, kEpiMask>{}, T{})
+                 : dispatch(std::integral_constant<int, kEpiMask>{}, F{});
+            break;
         default: throw std::logic_error("gemm_f16x3: bad epilogue");
     }
     SC_LAUNCH_CHECK();
@@ -2084,15 +2116,17 @@ const BImage& TcGemm::image(const MatB& b, int32_t N, int32_t K, cudaStream_t s)
 
 void TcGemm::nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2,
                 const float* amax2, const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi,
-                const float* row_scale, float* amax_out, uint32_t* relu_pos) {
+                const float* row_scale, float* amax_out, uint32_t* relu_pos, const float* mask_msg,
+                const uint32_t* mask_pos) {
     cudaStream_t s = t->ctx->stream;
     if (enabled && tc_supported(a1, a2, N) && tc_out_supported(C, ldc)) {
         const BImage& i1 = image(b1, N, a1.K, s);
         const BImage* i2 = a2 ? &image(*b2, N, a2->K, s) : nullptr;
-        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s, relu_pos);
+        gemm_f16x3(a1, amax1, i1, a2, amax2, i2, C, ldc, M, N, epi, row_scale, amax_out, s, relu_pos, mask_msg,
+                   mask_pos);
     } else {
         if (enabled) ++simt_fallbacks;
-        gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out);
+        gemm_nt(a1, b1, a2, b2, C, ldc, M, N, epi, row_scale, s, amax_out, mask_msg, mask_pos);
         if (epi == kEpiRelu && relu_pos) relu_sign_bits(M, N, C, ldc, relu_pos, s);
     }
 }

@@ -33,7 +33,8 @@ void prep_bimage(BImage& im, const MatB& b, int32_t N, int32_t K, cudaStream_t s
 // epi == kEpiRelu): the ReLU decisions as bits, [M][ceil(N / 32)] words.
 void gemm_f16x3(const MatA& a1, const float* amax1, const BImage& b1, const MatA* a2, const float* amax2,
                 const BImage* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-                float* amax_out, cudaStream_t s, uint32_t* relu_pos = nullptr);
+                float* amax_out, cudaStream_t s, uint32_t* relu_pos = nullptr, const float* mask_msg = nullptr,
+                const uint32_t* mask_pos = nullptr);
 
 // Weight gradient C[N1 x N2] = A^T [B1 | B2] (K = M rows) on the tensor cores,
 // fp16x3, split-K with a fixed-order reduction (deterministic). ws needs
@@ -73,7 +74,8 @@ struct TcGemm {
     const BImage& image(const MatB& b, int32_t N, int32_t K, cudaStream_t s);
     void nt(sc_trainer* t, const MatA& a1, const float* amax1, const MatB& b1, const MatA* a2, const float* amax2,
             const MatB* b2, float* C, int64_t ldc, int64_t M, int32_t N, int epi, const float* row_scale,
-            float* amax_out, uint32_t* relu_pos = nullptr);
+            float* amax_out, uint32_t* relu_pos = nullptr, const float* mask_msg = nullptr,
+            const uint32_t* mask_pos = nullptr);
     // dU and dW of one layer in one launch (false: unsupported here, caller runs tn twice)
     bool tn_dual(sc_trainer* t, const MatT& a1, const float* amax_a1, const MatT& a2, const float* amax_a2,
                  const MatT& b1, const float* amax_b1, const MatT& b2, const float* amax_b2, int64_t M, float* C1,

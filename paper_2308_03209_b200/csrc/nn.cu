@@ -34,6 +34,8 @@ struct GemmArgs {
     int epi;
     const float* row_scale;
     float* amax_out;
+    const float* mask_msg;     // kEpiMask (row stride N)
+    const uint32_t* mask_pos;  // kEpiMask, sign bits
 };
 
 // |v| max-reduction into a float slot: non-negative floats order like their bits.
@@ -121,6 +123,11 @@ __global__ void __launch_bounds__(NT) gemm_nt_kernel(GemmArgs args) {
             float v = acc[i][j];
             if (args.epi == kEpiRelu) v = fmaxf(v, 0.f);
             else if (args.epi == kEpiRowScale) v = sc * v;
+            else if (args.epi == kEpiMask) {
+                const bool keep = args.mask_pos ? ((args.mask_pos[r * ((args.N + 31) >> 5) + (c >> 5)] >> (c & 31)) & 1u)
+                                                : args.mask_msg[r * args.N + c] > 0.f;
+                v = keep ? v : 0.f;
+            }
             args.C[r * args.ldc + c] = v;
             mx = fmaxf(mx, fabsf(v));
         }
@@ -334,18 +341,22 @@ __device__ __forceinline__ void gather_rows_sum(int64_t a, int64_t b, int lane, 
 // 1[msg > 0] * sum (nn.hpp:287-288). Returns max|out| of the lane's chunks.
 // The ReLU decision comes from the msg row, or (compact activations) from its
 // sign bits: word [v][c / 32], bit c % 32, written by the msg GEMM's epilogue.
-template <int NCH, bool kBwd, bool kPos>
+// kX (variants of the composed top layer, trainer.cu): 0 as above; 1 forward, added to the row
+// already in out (logits = h Z_R^T + inv * sum P[nbr]); 2 the plain sum (no inv, no mask: the pull
+// form of the transposed aggregation of rows pre-scaled by inv).
+template <int NCH, bool kBwd, bool kPos, int kX = 0>
 __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int32_t H4, const float* __restrict__ inv,
                                             const float* __restrict__ msg, const uint32_t* __restrict__ pos,
                                             float* __restrict__ out, const float4 (&acc)[NCH]) {
     float amx = 0.f;
-    const float s = kBwd ? 1.f : inv[v];
+    const float s = (kBwd || kX == 2) ? 1.f : inv[v];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         const int32_t ch = lane + 32 * c;
         if (ch >= H4) continue;
         float4 r = acc[c];
-        if (!kBwd) {
+        if (kX == 2) {
+        } else if (!kBwd) {
             r.x *= s;
             r.y *= s;
             r.z *= s;
@@ -363,6 +374,13 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
             r.z = mv.z > 0.f ? r.z : 0.f;
             r.w = mv.w > 0.f ? r.w : 0.f;
         }
+        if (kX == 1) {
+            const float4 o = reinterpret_cast<const float4*>(out + v * H)[ch];
+            r.x = o.x + r.x;
+            r.y = o.y + r.y;
+            r.z = o.z + r.z;
+            r.w = o.w + r.w;
+        }
         reinterpret_cast<float4*>(out + v * H)[ch] = r;
         amx = fmaxf(amx, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
     }
@@ -371,7 +389,7 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
 
 // Warp per row over rows with at most `max_slots` CSR slots (heavier rows go
 // through the segmented path below).
-template <int NCH, bool kBwd, bool kPos = false>
+template <int NCH, bool kBwd, bool kPos = false, int kX = 0>
 __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                    const int32_t* __restrict__ nbrs,
                                                    const uint32_t* __restrict__ bits, const float* __restrict__ inv,
@@ -389,7 +407,7 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
-        amx = fmaxf(amx, finish_row<NCH, kBwd, kPos>(v, lane, H, H4, inv, msg, pos, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd, kPos, kX>(v, lane, H, H4, inv, msg, pos, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -424,7 +442,7 @@ __global__ void __launch_bounds__(256) spmm_segments_kernel(int32_t nseg, int32_
     }
 }
 
-template <int NCH, bool kBwd, bool kPos>
+template <int NCH, bool kBwd, bool kPos, int kX = 0>
 __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int32_t H,
                                                                 const int32_t* __restrict__ rows,
                                                                 const int32_t* __restrict__ seg_first,
@@ -451,7 +469,7 @@ __global__ void __launch_bounds__(256) spmm_heavy_finish_kernel(int32_t nh, int3
                     acc[c].z += p.z;
                     acc[c].w += p.w;
                 }
-        amx = fmaxf(amx, finish_row<NCH, kBwd, kPos>(rows[h], lane, H, H4, inv, msg, pos, out, acc));
+        amx = fmaxf(amx, finish_row<NCH, kBwd, kPos, kX>(rows[h], lane, H, H4, inv, msg, pos, out, acc));
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -501,7 +519,7 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
     }
 }
 
-template <int NCH, bool kBwd, bool kPos>
+template <int NCH, bool kBwd, bool kPos, int kX = 0>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* src, const float* msg, const uint32_t* pos, float* out, cudaStream_t s, float* amax_out,
               const HeavyRows* hv, float* partial) {
@@ -509,7 +527,7 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
     // (A/B, profiles/r01_spmm_grid_ab.txt: x16 -> x64 blocks per SM = 0.82 -> 0.92 of HBM peak)
     const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
     const bool heavy = hv && hv->nh > 0;
-    spmm_kernel<NCH, kBwd, kPos><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out, amax_out,
+    spmm_kernel<NCH, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out, amax_out,
                                                 heavy ? int64_t(kHeavySlots) : INT64_MAX);
     SC_LAUNCH_CHECK();
     count_launch();
@@ -517,7 +535,7 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
     spmm_segments_kernel<NCH><<<grid_for(int64_t(hv->nseg) * 32, 256, int64_t(num_sms()) * 16), 256, 0, s>>>(
         hv->nseg, H, off, nbrs, bits, hv->seg_row.get(), hv->seg_begin.get(), src, partial);
     SC_LAUNCH_CHECK();
-    spmm_heavy_finish_kernel<NCH, kBwd, kPos><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
+    spmm_heavy_finish_kernel<NCH, kBwd, kPos, kX><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
         hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, msg, pos, out, amax_out);
     SC_LAUNCH_CHECK();
     count_launch(2);
@@ -549,6 +567,31 @@ void spmm_launch(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, 
     else if (nch == 2) spmm_vec_pos<2, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
     else if (nch <= 4) spmm_vec_pos<4, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
     else spmm_vec_pos<8, kBwd>(n, H, off, nbrs, bits, inv, src, msg, pos, out, s, amax_out, hv, partial);
+}
+
+// The composed top layer's aggregations (kX = 1, 2; H a multiple of 4, the padded class count).
+template <int kX>
+void spmm_variant(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits,
+                  const float* inv, const float* src, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv,
+                  float* partial) {
+    if (n <= 0) return;
+    if (H % 4 != 0) throw std::logic_error("spmm variant: row width must be a multiple of 4");
+    const int nch = (H / 4 + 31) / 32;
+    constexpr bool kB = kX == 2;
+    if (nch <= 1) spmm_vec<1, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
+    else if (nch == 2) spmm_vec<2, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
+    else if (nch <= 4) spmm_vec<4, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
+    else spmm_vec<8, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
+}
+
+__global__ void scale_rows_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ scale,
+                                  const float* __restrict__ src, float* __restrict__ dst) {
+    const int64_t total = n * ld;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / ld;
+        const int32_t c = static_cast<int32_t>(i - r * ld);
+        dst[i] = c < C ? scale[r] * src[i] : 0.f;
+    }
 }
 
 __global__ void mask_bits_kernel(int64_t nnz, const int32_t* __restrict__ eids, const uint8_t* __restrict__ mask,
@@ -845,10 +888,13 @@ __global__ void f1_counts_kernel(int64_t n, int32_t C, int32_t ld, const float* 
 }  // namespace
 
 void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
-             int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out) {
+             int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out, const float* mask_msg,
+             const uint32_t* mask_pos) {
     if (M <= 0 || N <= 0) return;
     GemmArgs args{};
     args.amax_out = amax_out;
+    args.mask_msg = mask_msg;
+    args.mask_pos = mask_pos;
     args.a[0] = a1;
     args.b[0] = b1;
     args.nsrc = 1;
@@ -908,6 +954,20 @@ void inv_degree(int64_t n, const int64_t* offsets, const uint32_t* bits, float* 
 void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* msg, float* mean, cudaStream_t s, const HeavyRows* hv, float* partial) {
     spmm_launch<false>(n, H, offsets, nbrs, bits, inv, msg, nullptr, nullptr, mean, s, nullptr, hv, partial);
+}
+void spmm_fwd_add(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
+                  const float* inv, const float* src, float* out, cudaStream_t s, const HeavyRows* hv, float* partial) {
+    spmm_variant<1>(n, H, offsets, nbrs, bits, inv, src, out, s, nullptr, hv, partial);
+}
+void spmm_sum(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
+              const float* src, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv, float* partial) {
+    spmm_variant<2>(n, H, offsets, nbrs, bits, nullptr, src, out, s, amax_out, hv, partial);
+}
+void scale_rows(int64_t n, int32_t C, int32_t ld, const float* scale, const float* src, float* dst, cudaStream_t s) {
+    if (n <= 0) return;
+    scale_rows_kernel<<<grid_for(n * ld, 256), 256, 0, s>>>(n, C, ld, scale, src, dst);
+    SC_LAUNCH_CHECK();
+    count_launch();
 }
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
               const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out, const HeavyRows* hv,

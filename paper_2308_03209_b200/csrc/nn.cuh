@@ -37,12 +37,15 @@ struct MatB {
     bool nn = false;
 };
 
-enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2 };
+// kEpiMask: C = 1[msg > 0] * acc, the ReLU decision of the N-wide msg row (mask_msg, row stride N) or
+// its sign bits (mask_pos, [M][ceil(N / 32)] words) — the transposed aggregation's dz (nn.hpp:287-288).
+enum Epilogue : int { kEpiNone = 0, kEpiRelu = 1, kEpiRowScale = 2, kEpiMask = 3 };
 
 // C[M x N] = A1 * op(B1) (+ A2 * op(B2)), fp32 in/out, fp32 accumulate, then epilogue.
 // amax_out (optional): atomically max-reduced with |C| (the next GEMM's operand scale).
 void gemm_nt(const MatA& a1, const MatB& b1, const MatA* a2, const MatB* b2, float* C, int64_t ldc, int64_t M,
-             int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out = nullptr);
+             int32_t N, int epi, const float* row_scale, cudaStream_t s, float* amax_out = nullptr,
+             const float* mask_msg = nullptr, const uint32_t* mask_pos = nullptr);
 
 // dst[r][:] = src[rows[r]][:] (n x d); dst_ld > d pads each destination row with zeros
 // (and then rows may be null: identity).
@@ -79,6 +82,14 @@ void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs,
 // dz[u] = 1[msg[u] > 0] * sum_{v in CSR(u), kept} dmean_s[v]   (nn.hpp:277-288, pull form).
 // relu_pos (compact activations): the ReLU decisions as sign bits, [n][ceil(H / 32)]
 // words (bit c % 32 of word c / 32), read instead of the msg rows (msg may be null).
+// out += inv * sum_kept src[nbr] (the composed top layer's forward aggregation of projected rows)
+void spmm_fwd_add(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
+                  const float* inv, const float* src, float* out, cudaStream_t s, const HeavyRows* hv, float* partial);
+// out = sum_kept src[nbr] (pull form of the transposed aggregation of rows pre-scaled by inv)
+void spmm_sum(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
+              const float* src, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv, float* partial);
+// dst[r][c] = scale[r] src[r][c] for c < C, 0 for C <= c < ld
+void scale_rows(int64_t n, int32_t C, int32_t ld, const float* scale, const float* src, float* dst, cudaStream_t s);
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
               const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out = nullptr,
               const HeavyRows* hv = nullptr, float* partial = nullptr, const uint32_t* relu_pos = nullptr);

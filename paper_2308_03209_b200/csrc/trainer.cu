@@ -133,9 +133,12 @@ void init_model(sc_trainer* t) {
     t->fuse_top = t->L >= 1 && t->tc.enabled && !(e && e[0] == '0');
     if (t->fuse_top) {
         const LayerOff& lo = t->lay[t->L - 1];
-        t->Z.alloc(int64_t(t->C) * (lo.H + lo.in));
+        t->Z.alloc(int64_t(t->Cp) * (lo.H + lo.in));
+        SC_CUDA(cudaMemsetAsync(t->Z.get(), 0, t->Z.bytes(), t->ctx->stream));
         t->Xp.alloc(int64_t(t->C) * (lo.H + lo.in));
         t->z_version = 0;
+        e = std::getenv("SC_PTA");
+        t->pta = 2 * t->Cp <= lo.H && !(e && e[0] == '0');
     }
 }
 
@@ -355,7 +358,9 @@ size_t carve_train(sc_trainer* t, float* base, int64_t n) {
     for (int l = 0; l < t->L; ++l) {
         t->MSG[l] = t->compact ? shared_msg : c.take(size_t(n) * t->lay[l].H);
         t->MEAN[l] = c.take(size_t(n) * t->lay[l].H);
-        if (t->compact) t->POS[l] = reinterpret_cast<uint32_t*>(c.take(size_t(n) * ((t->lay[l].H + 31) / 32)));
+        // sign bits: compact activations (every layer), or the projected top layer's dz mask
+        if (t->compact || (t->pta && l == t->L - 1))
+            t->POS[l] = reinterpret_cast<uint32_t*>(c.take(size_t(n) * ((t->lay[l].H + 31) / 32)));
     }
     t->inv = c.take(n);
     t->G = c.take(size_t(n) * t->Cp);
@@ -436,6 +441,23 @@ void forward(sc_trainer* t, const Rows& R, float* logits, const Acts& A) {
         t->tc.nt(t, xin, xin_amax, MatB{t->theta.get() + lo.W, lo.in, false}, nullptr, nullptr, nullptr,
                  A.MSG[l], lo.H, n, lo.H, kEpiRelu, nullptr, t->amax_msg(l), A.POS.empty() ? nullptr : A.POS[l]);
         P.end(s);
+        if (t->pta && l == t->L - 1) {
+            // logits = h Z_R^T + inv * sum_kept (msg Z_L^T)[nbr]: the projection P = msg Z_L^T (Cp wide,
+            // into MEAN[l]'s buffer) is aggregated instead of msg (nn.hpp:222-234, 240 re-associated)
+            ensure_z(t, s);
+            const int zl = lo.H + lo.in;
+            float* proj = A.MEAN[l];
+            P.begin("gemm_head", 4.0 * n * (lo.H + lo.in + 2 * t->Cp), s, 2.0 * n * zl * t->C);
+            t->tc.nt(t, MatA{A.MSG[l], lo.H, nullptr, lo.H}, t->amax_msg(l), MatB{t->Z.get(), zl, false}, nullptr,
+                     nullptr, nullptr, proj, t->Cp, n, t->Cp, kEpiNone, nullptr, nullptr);
+            t->tc.nt(t, xin, xin_amax, MatB{t->Z.get() + lo.H, zl, false}, nullptr, nullptr, nullptr, logits, t->Cp, n,
+                     t->Cp, kEpiNone, nullptr, nullptr);
+            P.end(s);
+            P.begin("spmm_fwd", spmm_bytes(R, t->Cp, false) + 4.0 * n * t->Cp, s);
+            spmm_fwd_add(n, t->Cp, R.offsets, R.nbrs, R.bits, A.inv, proj, logits, s, R.hv, t->heavy_ws.get());
+            P.end(s);
+            return;
+        }
         // mean = inv * sum_kept msg[nbr]   (nn.hpp:222-230)
         P.begin("spmm_fwd", spmm_bytes(R, lo.H, false), s);
         spmm_fwd(n, lo.H, R.offsets, R.nbrs, R.bits, A.inv, A.MSG[l], A.MEAN[l], s, R.hv, t->heavy_ws.get());
@@ -472,8 +494,10 @@ void forward(sc_trainer* t, const Rows& R, float* logits, const Acts& A) {
 
 // Layers l = top .. 0 of sage_backward (nn.hpp:262-291) given dh of layer `top` in `dh` (amax in
 // dh_amax); layer top's dmean / dU come from the caller when `top_done` (composed top layer).
+// top_done: 0 none; 1 the composed top layer's dmean is in dh2 and its dU done (backward_fused);
+// 2 also its dz (projected top-layer aggregation).
 void backward_layers(sc_trainer* t, const Rows& R, int i, int top, float* dh, float* dh_amax, float* dh2,
-                     float* dh2_amax, bool top_done);
+                     float* dh2_amax, int top_done);
 
 // The composed top layer's backward (see sc_trainer::fuse_top), then layers L-2 .. 0 as usual.
 void backward_fused(sc_trainer* t, const Rows& R, int i) {
@@ -493,9 +517,30 @@ void backward_fused(sc_trainer* t, const Rows& R, int i) {
     // Xp = G^T [mean | h_in]; dHead = Xp U^T (nn.hpp:259 with emb = mean U_L^T + h U_R^T);
     // dU = head^T Xp (:271-272 with dh = G head)
     ensure_z(t, s);
-    P.begin("wgrad", 4.0 * n * (t->C + zl), s, 2.0 * n * t->C * zl);
-    t->tc.tn(t, gt, R.g_amax, meant, t->amax_msg(T), &xint, xin_amax, n, t->Xp.get(), zl);
-    P.end(s);
+    float* dh2 = t->dmean;
+    float* dh2_amax = t->amax_slot(sc_trainer::kSlotDh1);
+    float* ghat_amax = t->amax_slot(sc_trainer::kSlotDh0);
+    if (t->pta) {
+        // G^T mean = G^T D^-1 A msg = Ghat^T msg with Ghat = A^T (inv * G): one Cp-wide pull aggregation
+        // (A symmetric; the same kept-slot sums as :277-286) instead of the H-wide mean / dmean.
+        float* gs = dh2;
+        float* ghat = t->dh;
+        P.begin("spmm_bwd", spmm_bytes(R, t->Cp, false) + 8.0 * n * t->Cp, s);
+        scale_rows(n, t->C, t->Cp, t->inv, t->G, gs, s);
+        SC_CUDA(cudaMemsetAsync(ghat_amax, 0, sizeof(float), s));
+        spmm_sum(n, t->Cp, R.offsets, R.nbrs, R.bits, gs, ghat, s, ghat_amax, R.hv, t->heavy_ws.get());
+        P.end(s);
+        const MatT msgt{t->MSG[T], lo.H, nullptr, lo.H};
+        P.begin("wgrad", 4.0 * n * (2 * t->C + zl), s, 2.0 * n * t->C * zl);
+        t->tc.tn(t, MatT{ghat, t->Cp, nullptr, t->C}, ghat_amax, msgt, t->amax_msg(T), nullptr, nullptr, n,
+                 t->Xp.get(), zl);
+        t->tc.tn(t, gt, R.g_amax, xint, xin_amax, nullptr, nullptr, n, t->Xp.get() + lo.H, zl);
+        P.end(s);
+    } else {
+        P.begin("wgrad", 4.0 * n * (t->C + zl), s, 2.0 * n * t->C * zl);
+        t->tc.tn(t, gt, R.g_amax, meant, t->amax_msg(T), &xint, xin_amax, n, t->Xp.get(), zl);
+        P.end(s);
+    }
     P.begin("wgrad_small", 4.0 * t->C * zl * 2 + 4.0 * lo.H * zl, s, 2.0 * t->C * zl * lo.H * 2);
     small_gemm(t->C, t->E, zl, t->Xp.get(), zl, false, t->theta.get() + lo.U, zl, true, t->slot_ptr(2 * t->L, i),
                t->E, s);
@@ -504,14 +549,23 @@ void backward_fused(sc_trainer* t, const Rows& R, int i) {
     P.end(s);
     exchange_bucket(t, 2 * t->L, round);
     exchange_bucket(t, 2 * T + 1, round);
+    if (t->pta) {
+        // dz = 1[msg > 0] * A^T (inv * G Z_L) = 1[msg > 0] * (Ghat Z_L)   (:274-288 re-associated)
+        float* dz_amax = t->amax_slot(sc_trainer::kSlotDz);
+        SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
+        P.begin("gemm_dgrad", 4.0 * n * (t->Cp + 2 * lo.H), s, 2.0 * n * t->C * lo.H);
+        t->tc.nt(t, MatA{t->dh, t->Cp, nullptr, t->C}, ghat_amax, MatB{t->Z.get(), zl, true}, nullptr, nullptr,
+                 nullptr, t->dz, lo.H, n, lo.H, kEpiMask, nullptr, dz_amax, nullptr, nullptr, t->POS[T]);
+        P.end(s);
+        backward_layers(t, R, i, T, t->dh, ghat_amax, dh2, dh2_amax, 2);
+        return;
+    }
     // dmean_s = inv * (dh U_L) = inv * (G Z_L)   (:274)
-    float* dh2 = t->dmean;
-    float* dh2_amax = t->amax_slot(sc_trainer::kSlotDh1);
     P.begin("gemm_dgrad", 4.0 * n * (t->C + lo.H + 1), s, 2.0 * n * t->C * lo.H);
     t->tc.nt(t, ga, R.g_amax, MatB{t->Z.get(), zl, true}, nullptr, nullptr, nullptr, dh2, lo.H, n, lo.H,
              kEpiRowScale, t->inv, nullptr);
     P.end(s);
-    backward_layers(t, R, i, T, t->dh, t->amax_slot(sc_trainer::kSlotDh0), dh2, dh2_amax, true);
+    backward_layers(t, R, i, T, t->dh, t->amax_slot(sc_trainer::kSlotDh0), dh2, dh2_amax, 1);
 }
 
 // sage_backward (nn.hpp:246-293) into partition i's gradient slot; each
@@ -559,11 +613,11 @@ void backward(sc_trainer* t, const Rows& R, int i) {
     t->tc.nt(t, MatA{t->G, t->Cp, nullptr, t->C}, R.g_amax, MatB{t->theta.get() + t->head_off, t->E, true},
              nullptr, nullptr, nullptr, dh, t->E, n, t->E, kEpiNone, nullptr, dh_amax);
     P.end(s);
-    backward_layers(t, R, i, t->L - 1, dh, dh_amax, dh2, dh2_amax, false);
+    backward_layers(t, R, i, t->L - 1, dh, dh_amax, dh2, dh2_amax, 0);
 }
 
 void backward_layers(sc_trainer* t, const Rows& R, int i, int top, float* dh, float* dh_amax, float* dh2,
-                     float* dh2_amax, bool top_done) {
+                     float* dh2_amax, int top_done) {
     const int round = i / t->world;
     cudaStream_t s = t->ctx->stream;
     cudaStream_t w = t->overlap ? t->side : s;
@@ -580,7 +634,8 @@ void backward_layers(sc_trainer* t, const Rows& R, int i, int top, float* dh, fl
     const float* x0_amax = t->g->feat_amax.get();
     for (int l = top; l >= 0; --l) {
         const LayerOff& lo = t->lay[l];
-        const bool composed = top_done && l == top;  // dmean and dU already done (backward_fused)
+        const bool composed = top_done > 0 && l == top;  // dmean and dU already done (backward_fused)
+        const bool dz_ready = top_done == 2 && l == top;
         const MatT xint = l == 0 ? x0t : MatT{t->X[l], lo.in, nullptr, lo.in};
         const MatT dht{dh, lo.H, nullptr, lo.H};
         const MatT meant{t->MEAN[l], lo.H, nullptr, lo.H};
@@ -608,11 +663,13 @@ void backward_layers(sc_trainer* t, const Rows& R, int i, int top, float* dh, fl
             exchange_bucket(t, 2 * l + 1, round, w);
         }
         // dz = 1[msg > 0] * sum_kept dmean_s[nbr]   (:277-288)
-        SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
-        P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
-        spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, dh2, t->compact ? nullptr : t->MSG[l], t->dz, s, dz_amax, R.hv,
-                 t->heavy_ws.get(), t->POS[l]);
-        P.end(s);
+        if (!dz_ready) {
+            SC_CUDA(cudaMemsetAsync(dz_amax, 0, sizeof(float), s));
+            P.begin("spmm_bwd", spmm_bytes(R, lo.H, true), s);
+            spmm_bwd(n, lo.H, R.offsets, R.nbrs, R.bits, dh2, t->compact ? nullptr : t->MSG[l], t->dz, s, dz_amax,
+                     R.hv, t->heavy_ws.get(), t->POS[l]);
+            P.end(s);
+        }
         if (dual) {
             P.begin("wgrad", 4.0 * n * (3 * lo.H + lo.in), s, 2.0 * n * lo.H * (lo.H + 2 * lo.in));
             if (!t->tc.tn_dual(t, dht, dh_amax, dzt, dz_amax, meant, t->amax_msg(l), xint, xin_amax, n,

@@ -168,7 +168,12 @@ struct sc_trainer {
     // and h_L is never formed. Backward: Xp = G^T [mean | h] (one TN GEMM with C output rows) gives
     // dHead = Xp U^T and dU_{L-1} = head^T Xp; dmean = inv (G Z_L); dh_{L-1} = G Z_R + dz W.
     bool fuse_top = false;
-    sc::DevBuf<float> Z, Xp;
+    // ... and (pta, when the padded class count is at most half the top layer's width) the top
+    // layer's aggregation runs on projected rows: logits = h Z_R^T + A_norm (msg Z_L^T), whose rows are
+    // Cp wide instead of H (nn.hpp:222-234 re-associated; A_norm the masked mean). Backward: Ghat =
+    // A^T (inv * G) (Cp-wide pull), Xp = [Ghat^T msg | G^T h], dz = 1[msg > 0] (Ghat Z_L).
+    bool pta = false;
+    sc::DevBuf<float> Z, Xp;  // Z: Cp rows (rows C .. Cp-1 zero), so Cp-wide products have zero padding
     uint64_t z_version = 0;
     // Host transport (sc_trainer_set_exchange), used instead of NCCL when set.
     using ExchangeFn = int32_t (*)(void*, int32_t, int32_t, int32_t, const void*, void*, int64_t);

@@ -21,26 +21,32 @@ def rel(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(np.asarray(b, np.float64)), 1e-30))
 
 
-def trainer(sc, og, hidden, fuse, dropedge=True):
-    old = os.environ.get("SC_FUSE_TOP")
-    os.environ["SC_FUSE_TOP"] = "1" if fuse else "0"
+def trainer(sc, og, hidden, fuse, pta="1", dropedge=True, compact="0"):
+    env = {"SC_FUSE_TOP": "1" if fuse else "0", "SC_PTA": pta, "SC_COMPACT_ACTS": compact}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         g = gpu_graph(sc, og, 24)
         part = sc.partition_random(g, 4, 3)
         return sc.CoFreeTrainer(g, part, sc.TrainConfig(layers=len(hidden), hidden=hidden, use_dropedge=dropedge,
                                                         seed=1, learning_rate=1e-2))
     finally:
-        if old is None:
-            os.environ.pop("SC_FUSE_TOP", None)
-        else:
-            os.environ["SC_FUSE_TOP"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
-@pytest.mark.parametrize("hidden", [[32], [64, 64], [48, 48, 48]])
-def test_composed_top_layer_matches_unfused(hidden):
+# pta = "1": with 2 Cp <= H (here C = 6 -> Cp = 8) the top layer also aggregates projected rows
+# (logits = h Z_R^T + A_norm (msg Z_L^T); backward Ghat = A^T (inv G), Xp = [Ghat^T msg | G^T h],
+# dz = 1[msg > 0] (Ghat Z_L)); compact = "1": the ReLU decisions come from sign bits
+@pytest.mark.parametrize("hidden,pta,compact", [([32], "1", "0"), ([64, 64], "1", "0"), ([48, 48, 48], "1", "0"),
+                                                ([64, 64], "0", "0"), ([64, 64], "1", "1")])
+def test_composed_top_layer_matches_unfused(hidden, pta, compact):
     from paper_2308_03209_b200 import sagecut as sc
     og = oracle().graph_sbm(400, 6, 0.1, 0.01, 24, 0.3, 7)
-    a = trainer(sc, og, hidden, True)
+    a = trainer(sc, og, hidden, True, pta, compact=compact)
     b = trainer(sc, og, hidden, False)
     la, lb = a.step(0), b.step(0)
     assert abs(la[0] - lb[0]) <= 1e-6 * abs(lb[0])
