@@ -415,6 +415,79 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
     }
 }
 
+// Narrow rows (H <= 4 * LPR floats, e.g. the projected top layer's Cp = 48): a warp serves 32 / LPR
+// rows at once, LPR lanes each (lane = one float4 chunk), so as many more neighbour rows are in
+// flight per warp. Per row the kept slots are summed in CSR order exactly as in spmm_kernel (the same
+// bits).
+template <int LPR, bool kBwd, bool kPos, int kX>
+__global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
+                                                          const int32_t* __restrict__ nbrs,
+                                                          const uint32_t* __restrict__ bits,
+                                                          const float* __restrict__ inv, const float* __restrict__ src,
+                                                          const float* __restrict__ msg,
+                                                          const uint32_t* __restrict__ pos, float* __restrict__ out,
+                                                          float* amax_out, int64_t max_slots) {
+    constexpr int G = 32 / LPR;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / LPR, gl = lane % LPR;
+    const unsigned gmask = (LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u)) << (grp * LPR);
+    const int32_t H4 = H >> 2;
+    float amx = 0.f;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t v0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * G; v0 < n; v0 += warps * G) {
+        const int64_t v = v0 + grp;
+        int64_t a = 0, b = 0;
+        bool skip = v >= n;
+        if (!skip) {
+            a = off[v];
+            b = off[v + 1];
+            skip = b - a > max_slots;  // hub row: the segmented path writes it
+            if (skip) b = a;
+        }
+        float4 acc[1] = {make_float4(0.f, 0.f, 0.f, 0.f)};
+        for (int64_t base = a; base < b; base += LPR) {  // uniform within the group
+            const int64_t k = base + gl;
+            const bool valid = k < b;
+            const int32_t nb = valid ? __ldg(nbrs + k) : 0;
+            const bool kept = valid && slot_kept(bits, k);
+            unsigned ballot = (__ballot_sync(gmask, kept) & gmask) >> (grp * LPR);
+            while (ballot) {
+                int32_t u[4];
+                int cnt = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (ballot) {
+                        const int sl = __ffs(ballot) - 1;
+                        ballot &= ballot - 1;
+                        u[q] = __shfl_sync(gmask, nb, grp * LPR + sl);
+                        ++cnt;
+                    } else {
+                        u[q] = -1;
+                    }
+                }
+                float4 vals[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    vals[q] = (q < cnt && gl < H4) ? __ldg(reinterpret_cast<const float4*>(src + int64_t(u[q]) * H) + gl)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q < cnt) {
+                        acc[0].x += vals[q].x;
+                        acc[0].y += vals[q].y;
+                        acc[0].z += vals[q].z;
+                        acc[0].w += vals[q].w;
+                    }
+            }
+        }
+        if (!skip) amx = fmaxf(amx, finish_row<1, kBwd, kPos, kX>(v, gl, H, H4, inv, msg, pos, out, acc));
+    }
+    if (amax_out) {
+        amx = warp_max_f(amx);
+        if (lane == 0) atomic_max_abs(amax_out, amx);
+    }
+}
+
 // Skewed degrees (hubs): a row with more than kHeavySlots slots is cut into
 // kSegSlots-slot segments, one warp each, whose partial sums are then added in
 // segment order by one warp per row (deterministic; the association differs
@@ -519,16 +592,39 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
     }
 }
 
+// rows of H <= 64 floats run several per warp (spmm_narrow_kernel) unless SC_SPMM_NARROW=0
+bool narrow_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SC_SPMM_NARROW");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int NCH, bool kBwd, bool kPos, int kX = 0>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* src, const float* msg, const uint32_t* pos, float* out, cudaStream_t s, float* amax_out,
               const HeavyRows* hv, float* partial) {
     // 64 blocks of 8 warps per SM: ~13 waves at 5 resident blocks, so the grid-stride tail is short
     // (A/B, profiles/r01_spmm_grid_ab.txt: x16 -> x64 blocks per SM = 0.82 -> 0.92 of HBM peak)
-    const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
     const bool heavy = hv && hv->nh > 0;
-    spmm_kernel<NCH, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out, amax_out,
-                                                heavy ? int64_t(kHeavySlots) : INT64_MAX);
+    const int64_t max_slots = heavy ? int64_t(kHeavySlots) : INT64_MAX;
+    const int32_t H4 = H / 4;
+    if (NCH == 1 && H4 <= 16 && narrow_enabled()) {  // several rows per warp
+        const int lpr = H4 <= 8 ? 8 : 16;
+        const int64_t rows_per_warp = 32 / lpr;
+        const unsigned grid = grid_for((n + rows_per_warp - 1) / rows_per_warp * 32, 256, int64_t(num_sms()) * 64);
+        if (lpr == 8)
+            spmm_narrow_kernel<8, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out,
+                                                                       amax_out, max_slots);
+        else
+            spmm_narrow_kernel<16, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos,
+                                                                        out, amax_out, max_slots);
+    } else {
+        const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
+        spmm_kernel<NCH, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out,
+                                                             amax_out, max_slots);
+    }
     SC_LAUNCH_CHECK();
     count_launch();
     if (!heavy) return;
