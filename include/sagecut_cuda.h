@@ -357,7 +357,9 @@ sc_status sc_debug_gemm_tn_dual(sc_ctx* ctx, int64_t M, const float* A1, int32_t
  * an optional per-local-edge keep mask (num_edges bytes, as the reference's
  * DropEdge masks index edges). src: n x H (fwd: msg; bwd: dmean already scaled
  * by inv); msg (bwd): the forward's messages (gate = msg > 0); out: n x H. Host
- * buffers. */
+ * buffers. bwd = 2 / 3: the projected top layer's aggregations (trainer.hpp pta):
+ * 2 = sum_kept inv[nbr] src[nbr] (no gate), 3 = msg + inv * sum_kept src[nbr]
+ * (msg = the addend), inv the masked inverse degrees. */
 sc_status sc_debug_spmm(sc_ctx* ctx, int32_t bwd, int64_t n, int32_t H, const int64_t* offsets,
                         const int32_t* nbrs, const int32_t* eids, int64_t num_edges, const uint8_t* edge_mask,
                         const float* src, const float* msg, float* out);

@@ -1209,7 +1209,8 @@ sc_status sc_debug_spmm(sc_ctx* ctx, int32_t bwd, int64_t n, int32_t H, const in
                         const float* src, const float* msg, float* out) {
     return guard([&] {
         REQUIRE_ARG(ctx && offsets && src && out && n >= 0 && H >= 1, "sc_debug_spmm: bad arguments");
-        REQUIRE_ARG(!bwd || msg, "sc_debug_spmm: the transposed aggregation needs msg (its ReLU decisions)");
+        REQUIRE_ARG(bwd >= 0 && bwd <= 3, "sc_debug_spmm: mode must be 0 .. 3");
+        REQUIRE_ARG((bwd != 1 && bwd != 3) || msg, "sc_debug_spmm: modes 1 and 3 need msg (ReLU decisions / addend)");
         set_device(ctx);
         cudaStream_t s = ctx->stream;
         const int64_t nnz = offsets[n] - offsets[0];
@@ -1217,12 +1218,13 @@ sc_status sc_debug_spmm(sc_ctx* ctx, int32_t bwd, int64_t n, int32_t H, const in
         DevBuf<int64_t> d_off(n + 1);
         DevBuf<int32_t> d_nb(std::max<int64_t>(nnz, 1)), d_ei(std::max<int64_t>(nnz, 1));
         DevBuf<float> d_src(std::max<int64_t>(n * H, 1)), d_out(std::max<int64_t>(n * H, 1)), d_inv(std::max<int64_t>(n, 1));
-        DevBuf<float> d_msg(bwd ? std::max<int64_t>(n * H, 1) : 1);
+        const bool has_msg = bwd == 1 || bwd == 3;
+        DevBuf<float> d_msg(has_msg ? std::max<int64_t>(n * H, 1) : 1);
         h2d(d_off.get(), offsets, n + 1, s);
         h2d(d_nb.get(), nbrs, nnz, s);
         h2d(d_ei.get(), eids, nnz, s);
         h2d(d_src.get(), src, n * H, s);
-        if (bwd) h2d(d_msg.get(), msg, n * H, s);
+        if (has_msg) h2d(d_msg.get(), msg, n * H, s);
         DevBuf<uint32_t> bits;
         if (edge_mask) {  // the trainer's CSR-slot bitmap of a per-local-edge DropEdge mask
             DevBuf<uint8_t> d_mask(std::max<int64_t>(num_edges, 1));
@@ -1234,10 +1236,17 @@ sc_status sc_debug_spmm(sc_ctx* ctx, int32_t bwd, int64_t n, int32_t H, const in
         HeavyRows hv;
         build_heavy_rows(ctx, n, d_off.get(), hv);
         DevBuf<float> partial(std::max<int64_t>(int64_t(hv.nseg) * H, 1));
-        if (!bwd) {
-            inv_degree(n, d_off.get(), bits.get(), d_inv.get(), s);
+        if (bwd != 1) inv_degree(n, d_off.get(), bits.get(), d_inv.get(), s);
+        if (bwd == 0) {
             spmm_fwd(n, H, d_off.get(), d_nb.get(), bits.get(), d_inv.get(), d_src.get(), d_out.get(), s, &hv,
                      partial.get());
+        } else if (bwd == 2) {  // the projected top layer's backward: sum_kept inv[nbr] src[nbr]
+            spmm_sum_scaled(n, H, d_off.get(), d_nb.get(), bits.get(), d_inv.get(), d_src.get(), d_out.get(), s,
+                            nullptr, &hv, partial.get());
+        } else if (bwd == 3) {  // its forward: msg (the addend) + inv * sum_kept src[nbr]
+            SC_CUDA(cudaMemcpyAsync(d_out.get(), d_msg.get(), sizeof(float) * n * H, cudaMemcpyDeviceToDevice, s));
+            spmm_fwd_add(n, H, d_off.get(), d_nb.get(), bits.get(), d_inv.get(), d_src.get(), d_out.get(), s, &hv,
+                         partial.get());
         } else {
             spmm_bwd(n, H, d_off.get(), d_nb.get(), bits.get(), d_src.get(), d_msg.get(), d_out.get(), s, nullptr, &hv,
                      partial.get());

@@ -288,10 +288,12 @@ __global__ void inv_degree_kernel(int64_t n, const int64_t* __restrict__ off, co
 
 // Sum of the kept source rows over CSR slots [a, b) in slot order (the
 // reference's order); lanes own float4 column chunks, up to 4 row loads in flight.
-template <int NCH>
+// kScale: every gathered row is scaled by inv[nbr] first (spmm_sum_scaled's hub segments)
+template <int NCH, bool kScale = false>
 __device__ __forceinline__ void gather_rows_sum(int64_t a, int64_t b, int lane, int32_t H, int32_t H4,
                                                 const int32_t* __restrict__ nbrs, const uint32_t* __restrict__ bits,
-                                                const float* __restrict__ src, float4 (&acc)[NCH]) {
+                                                const float* __restrict__ src, float4 (&acc)[NCH],
+                                                const float* __restrict__ inv = nullptr) {
     for (int64_t base = a; base < b; base += 32) {
         const int64_t k = base + lane;
         const bool valid = k < b;
@@ -325,14 +327,23 @@ __device__ __forceinline__ void gather_rows_sum(int64_t a, int64_t b, int lane, 
                 }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (q < cnt)
+                if (q < cnt) {
+                    const float sq = kScale ? __ldg(inv + u[q]) : 1.f;
 #pragma unroll
                     for (int c = 0; c < NCH; ++c) {
-                        acc[c].x += vals[q][c].x;
-                        acc[c].y += vals[q][c].y;
-                        acc[c].z += vals[q][c].z;
-                        acc[c].w += vals[q][c].w;
+                        float4 x = vals[q][c];
+                        if (kScale) {  // separately rounded products, as in spmm_narrow_kernel
+                            x.x = __fmul_rn(sq, x.x);
+                            x.y = __fmul_rn(sq, x.y);
+                            x.z = __fmul_rn(sq, x.z);
+                            x.w = __fmul_rn(sq, x.w);
+                        }
+                        acc[c].x += x.x;
+                        acc[c].y += x.y;
+                        acc[c].z += x.z;
+                        acc[c].w += x.w;
                     }
+                }
         }
     }
 }
@@ -349,13 +360,13 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
                                             const float* __restrict__ msg, const uint32_t* __restrict__ pos,
                                             float* __restrict__ out, const float4 (&acc)[NCH]) {
     float amx = 0.f;
-    const float s = (kBwd || kX == 2) ? 1.f : inv[v];
+    const float s = (kBwd || kX >= 2) ? 1.f : inv[v];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         const int32_t ch = lane + 32 * c;
         if (ch >= H4) continue;
         float4 r = acc[c];
-        if (kX == 2) {
+        if (kX >= 2) {
         } else if (!kBwd) {
             r.x *= s;
             r.y *= s;
@@ -374,12 +385,12 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
             r.z = mv.z > 0.f ? r.z : 0.f;
             r.w = mv.w > 0.f ? r.w : 0.f;
         }
-        if (kX == 1) {
+        if (kX == 1) {  // (inv * sum) rounded, then added: no FMA contraction
             const float4 o = reinterpret_cast<const float4*>(out + v * H)[ch];
-            r.x = o.x + r.x;
-            r.y = o.y + r.y;
-            r.z = o.z + r.z;
-            r.w = o.w + r.w;
+            r.x = __fadd_rn(o.x, r.x);
+            r.y = __fadd_rn(o.y, r.y);
+            r.z = __fadd_rn(o.z, r.z);
+            r.w = __fadd_rn(o.w, r.w);
         }
         reinterpret_cast<float4*>(out + v * H)[ch] = r;
         amx = fmaxf(amx, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
@@ -415,11 +426,12 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
     }
 }
 
-// Narrow rows (H <= 4 * LPR floats, e.g. the projected top layer's Cp = 48): a warp serves 32 / LPR
-// rows at once, LPR lanes each (lane = one float4 chunk), so as many more neighbour rows are in
-// flight per warp. Per row the kept slots are summed in CSR order exactly as in spmm_kernel (the same
-// bits).
-template <int LPR, bool kBwd, bool kPos, int kX>
+// Narrow rows (H <= 4 * LPR * CPL floats, e.g. the projected top layer's Cp = 48): a warp serves
+// 32 / LPR rows at once, LPR lanes each, CPL float4 chunks per lane, so many more neighbour rows are
+// in flight per warp. Per row the kept slots are summed in CSR order exactly as in spmm_kernel (the
+// same bits). kX == 3: every gathered row is first scaled by inv[nbr] (the pull form of the
+// transposed aggregation of inv-scaled rows, nn.hpp:284: inv_d * dmean.row(v)).
+template <int LPR, int CPL, bool kBwd, bool kPos, int kX>
 __global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                           const int32_t* __restrict__ nbrs,
                                                           const uint32_t* __restrict__ bits,
@@ -444,7 +456,9 @@ __global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, 
             skip = b - a > max_slots;  // hub row: the segmented path writes it
             if (skip) b = a;
         }
-        float4 acc[1] = {make_float4(0.f, 0.f, 0.f, 0.f)};
+        float4 acc[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int64_t base = a; base < b; base += LPR) {  // uniform within the group
             const int64_t k = base + gl;
             const bool valid = k < b;
@@ -465,22 +479,47 @@ __global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, 
                         u[q] = -1;
                     }
                 }
-                float4 vals[4];
+                float4 vals[4][CPL];
+                float sc[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    vals[q] = (q < cnt && gl < H4) ? __ldg(reinterpret_cast<const float4*>(src + int64_t(u[q]) * H) + gl)
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int q = 0; q < 4; ++q) {
+                    sc[q] = (kX == 3 && q < cnt) ? __ldg(inv + u[q]) : 1.f;
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (q < cnt) {
-                        acc[0].x += vals[q].x;
-                        acc[0].y += vals[q].y;
-                        acc[0].z += vals[q].z;
-                        acc[0].w += vals[q].w;
+                    for (int c = 0; c < CPL; ++c) {
+                        const int32_t ch = gl + LPR * c;
+                        vals[q][c] = (q < cnt && ch < H4)
+                                         ? __ldg(reinterpret_cast<const float4*>(src + int64_t(u[q]) * H) + ch)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q < cnt)
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) {
+                            float4 x = vals[q][c];
+                            if (kX == 3) {  // separately rounded products (no FMA contraction): the
+                                x.x = __fmul_rn(sc[q], x.x);  // reference's inv_d * dmean.row(v), then +=
+                                x.y = __fmul_rn(sc[q], x.y);
+                                x.z = __fmul_rn(sc[q], x.z);
+                                x.w = __fmul_rn(sc[q], x.w);
+                            }
+                            acc[c].x += x.x;
+                            acc[c].y += x.y;
+                            acc[c].z += x.z;
+                            acc[c].w += x.w;
+                        }
             }
         }
-        if (!skip) amx = fmaxf(amx, finish_row<1, kBwd, kPos, kX>(v, gl, H, H4, inv, msg, pos, out, acc));
+        if (!skip) {
+            // finish_row's chunk index is lane + 32 c; here chunk c of this lane is gl + LPR c
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                float4 one[1] = {acc[c]};
+                const int32_t ch = gl + LPR * c;
+                if (ch < H4) amx = fmaxf(amx, finish_row<1, kBwd, kPos, kX>(v, ch, H, H4, inv, msg, pos, out, one));
+            }
+        }
     }
     if (amax_out) {
         amx = warp_max_f(amx);
@@ -492,13 +531,14 @@ __global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, 
 // kSegSlots-slot segments, one warp each, whose partial sums are then added in
 // segment order by one warp per row (deterministic; the association differs
 // from the reference's single running sum only for these rows).
-template <int NCH>
+template <int NCH, bool kScale = false>
 __global__ void __launch_bounds__(256) spmm_segments_kernel(int32_t nseg, int32_t H, const int64_t* __restrict__ off,
                                                             const int32_t* __restrict__ nbrs,
                                                             const uint32_t* __restrict__ bits,
                                                             const int32_t* __restrict__ seg_row,
                                                             const int64_t* __restrict__ seg_begin,
-                                                            const float* __restrict__ src, float* __restrict__ partial) {
+                                                            const float* __restrict__ src, float* __restrict__ partial,
+                                                            const float* __restrict__ inv = nullptr) {
     const int lane = threadIdx.x & 31;
     const int32_t H4 = H >> 2;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -508,7 +548,7 @@ __global__ void __launch_bounds__(256) spmm_segments_kernel(int32_t nseg, int32_
         float4 acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
+        gather_rows_sum<NCH, kScale>(a, b, lane, H, H4, nbrs, bits, src, acc, inv);
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
             if (lane + 32 * c < H4) reinterpret_cast<float4*>(partial + sg * H)[lane + 32 * c] = acc[c];
@@ -610,16 +650,21 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
     const bool heavy = hv && hv->nh > 0;
     const int64_t max_slots = heavy ? int64_t(kHeavySlots) : INT64_MAX;
     const int32_t H4 = H / 4;
-    if (NCH == 1 && H4 <= 16 && narrow_enabled()) {  // several rows per warp
-        const int lpr = H4 <= 8 ? 8 : 16;
-        const int64_t rows_per_warp = 32 / lpr;
-        const unsigned grid = grid_for((n + rows_per_warp - 1) / rows_per_warp * 32, 256, int64_t(num_sms()) * 64);
-        if (lpr == 8)
-            spmm_narrow_kernel<8, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out,
-                                                                       amax_out, max_slots);
-        else
-            spmm_narrow_kernel<16, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos,
-                                                                        out, amax_out, max_slots);
+    if (kX == 3 && !(NCH == 1 && H4 <= 32))
+        throw std::logic_error("spmm: inv-scaled sums need rows of at most 128 floats");
+    if (NCH == 1 && H4 <= 32 && (narrow_enabled() || kX == 3)) {  // several rows per warp
+        auto go = [&](auto lpr_tag, auto cpl_tag) {
+            constexpr int LPR = decltype(lpr_tag)::value, CPL = decltype(cpl_tag)::value;
+            const unsigned grid = grid_for((n + 32 / LPR - 1) / (32 / LPR) * 32, 256, int64_t(num_sms()) * 64);
+            spmm_narrow_kernel<LPR, CPL, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg,
+                                                                              pos, out, amax_out, max_slots);
+        };
+        using I4 = std::integral_constant<int, 4>;
+        using I8 = std::integral_constant<int, 8>;
+        if (H4 <= 8) go(I4{}, std::integral_constant<int, 2>{});
+        else if (H4 <= 12) go(I4{}, std::integral_constant<int, 3>{});
+        else if (H4 <= 16) go(I4{}, I4{});
+        else go(I8{}, I4{});
     } else {
         const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
         spmm_kernel<NCH, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out,
@@ -628,8 +673,8 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
     SC_LAUNCH_CHECK();
     count_launch();
     if (!heavy) return;
-    spmm_segments_kernel<NCH><<<grid_for(int64_t(hv->nseg) * 32, 256, int64_t(num_sms()) * 16), 256, 0, s>>>(
-        hv->nseg, H, off, nbrs, bits, hv->seg_row.get(), hv->seg_begin.get(), src, partial);
+    spmm_segments_kernel<NCH, kX == 3><<<grid_for(int64_t(hv->nseg) * 32, 256, int64_t(num_sms()) * 16), 256, 0, s>>>(
+        hv->nseg, H, off, nbrs, bits, hv->seg_row.get(), hv->seg_begin.get(), src, partial, inv);
     SC_LAUNCH_CHECK();
     spmm_heavy_finish_kernel<NCH, kBwd, kPos, kX><<<grid_for(int64_t(hv->nh) * 32, 256), 256, 0, s>>>(
         hv->nh, H, hv->rows.get(), hv->seg_first.get(), partial, inv, msg, pos, out, amax_out);
@@ -673,21 +718,11 @@ void spmm_variant(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs,
     if (n <= 0) return;
     if (H % 4 != 0) throw std::logic_error("spmm variant: row width must be a multiple of 4");
     const int nch = (H / 4 + 31) / 32;
-    constexpr bool kB = kX == 2;
+    constexpr bool kB = kX >= 2;
     if (nch <= 1) spmm_vec<1, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
     else if (nch == 2) spmm_vec<2, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
     else if (nch <= 4) spmm_vec<4, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
     else spmm_vec<8, kB, false, kX>(n, H, off, nbrs, bits, inv, src, nullptr, nullptr, out, s, amax_out, hv, partial);
-}
-
-__global__ void scale_rows_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ scale,
-                                  const float* __restrict__ src, float* __restrict__ dst) {
-    const int64_t total = n * ld;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t r = i / ld;
-        const int32_t c = static_cast<int32_t>(i - r * ld);
-        dst[i] = c < C ? scale[r] * src[i] : 0.f;
-    }
 }
 
 __global__ void mask_bits_kernel(int64_t nnz, const int32_t* __restrict__ eids, const uint8_t* __restrict__ mask,
@@ -736,6 +771,7 @@ __global__ void softmax_ce_kernel(int64_t n, int32_t C, int32_t ld, const float*
         const float* z = logits + r * ld;
         float* g = G + r * ld;
         const double wr = w[r];
+        for (int32_t c = C + lane; c < ld; c += 32) g[c] = 0.f;  // padding columns (row stride ld)
         if (wr == 0.0) {  // nn.hpp:330 rows with zero weight contribute nothing
             for (int32_t c = lane; c < C; c += 32) g[c] = 0.f;
             if (lane == 0) row_loss[r] = 0.0;
@@ -825,6 +861,7 @@ __global__ void bce_kernel(int64_t n, int32_t C, int32_t ld, const float* __rest
         const float* z = logits + r * ld;
         float* g = G + r * ld;
         const double wr = w[r];
+        for (int32_t c = C + lane; c < ld; c += 32) g[c] = 0.f;  // padding columns (row stride ld)
         if (wr == 0.0) {
             for (int32_t c = lane; c < C; c += 32) g[c] = 0.f;
             if (lane == 0) row_loss[r] = 0.0;
@@ -1055,15 +1092,10 @@ void spmm_fwd_add(int64_t n, int32_t H, const int64_t* offsets, const int32_t* n
                   const float* inv, const float* src, float* out, cudaStream_t s, const HeavyRows* hv, float* partial) {
     spmm_variant<1>(n, H, offsets, nbrs, bits, inv, src, out, s, nullptr, hv, partial);
 }
-void spmm_sum(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
-              const float* src, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv, float* partial) {
-    spmm_variant<2>(n, H, offsets, nbrs, bits, nullptr, src, out, s, amax_out, hv, partial);
-}
-void scale_rows(int64_t n, int32_t C, int32_t ld, const float* scale, const float* src, float* dst, cudaStream_t s) {
-    if (n <= 0) return;
-    scale_rows_kernel<<<grid_for(n * ld, 256), 256, 0, s>>>(n, C, ld, scale, src, dst);
-    SC_LAUNCH_CHECK();
-    count_launch();
+void spmm_sum_scaled(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
+                     const float* inv, const float* src, float* out, cudaStream_t s, float* amax_out,
+                     const HeavyRows* hv, float* partial) {
+    spmm_variant<3>(n, H, offsets, nbrs, bits, inv, src, out, s, amax_out, hv, partial);
 }
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* bits,
               const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out, const HeavyRows* hv,

@@ -85,11 +85,11 @@ void spmm_fwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs,
 // out += inv * sum_kept src[nbr] (the composed top layer's forward aggregation of projected rows)
 void spmm_fwd_add(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
                   const float* inv, const float* src, float* out, cudaStream_t s, const HeavyRows* hv, float* partial);
-// out = sum_kept src[nbr] (pull form of the transposed aggregation of rows pre-scaled by inv)
-void spmm_sum(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
-              const float* src, float* out, cudaStream_t s, float* amax_out, const HeavyRows* hv, float* partial);
-// dst[r][c] = scale[r] src[r][c] for c < C, 0 for C <= c < ld
-void scale_rows(int64_t n, int32_t C, int32_t ld, const float* scale, const float* src, float* dst, cudaStream_t s);
+// out = sum_kept inv[nbr] src[nbr] (pull form of the transposed aggregation, nn.hpp:277-286, without the
+// ReLU mask; rows of at most 128 floats)
+void spmm_sum_scaled(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
+                     const float* inv, const float* src, float* out, cudaStream_t s, float* amax_out,
+                     const HeavyRows* hv, float* partial);
 void spmm_bwd(int64_t n, int32_t H, const int64_t* offsets, const int32_t* nbrs, const uint32_t* mask_bits,
               const float* dmean_s, const float* msg, float* dz, cudaStream_t s, float* amax_out = nullptr,
               const HeavyRows* hv = nullptr, float* partial = nullptr, const uint32_t* relu_pos = nullptr);

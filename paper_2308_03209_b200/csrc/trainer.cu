@@ -523,12 +523,11 @@ void backward_fused(sc_trainer* t, const Rows& R, int i) {
     if (t->pta) {
         // G^T mean = G^T D^-1 A msg = Ghat^T msg with Ghat = A^T (inv * G): one Cp-wide pull aggregation
         // (A symmetric; the same kept-slot sums as :277-286) instead of the H-wide mean / dmean.
-        float* gs = dh2;
         float* ghat = t->dh;
-        P.begin("spmm_bwd", spmm_bytes(R, t->Cp, false) + 8.0 * n * t->Cp, s);
-        scale_rows(n, t->C, t->Cp, t->inv, t->G, gs, s);
+        P.begin("spmm_bwd", spmm_bytes(R, t->Cp, false), s);
         SC_CUDA(cudaMemsetAsync(ghat_amax, 0, sizeof(float), s));
-        spmm_sum(n, t->Cp, R.offsets, R.nbrs, R.bits, gs, ghat, s, ghat_amax, R.hv, t->heavy_ws.get());
+        spmm_sum_scaled(n, t->Cp, R.offsets, R.nbrs, R.bits, t->inv, t->G, ghat, s, ghat_amax, R.hv,
+                        t->heavy_ws.get());
         P.end(s);
         const MatT msgt{t->MSG[T], lo.H, nullptr, lo.H};
         P.begin("wgrad", 4.0 * n * (2 * t->C + zl), s, 2.0 * n * t->C * zl);

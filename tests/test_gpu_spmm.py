@@ -46,3 +46,31 @@ def test_spmm_widths_bitwise(part0, H):
         assert int((got[light] != ref[light]).sum()) == 0, (H, bwd)
         d = np.abs(got[~light] - ref[~light]).max() / np.abs(ref[~light]).max()
         assert d <= 1e-5, (H, bwd, d)
+
+
+@pytest.mark.parametrize("H", [8, 12, 48, 64, 128])
+def test_projected_top_layer_sums_bitwise(part0, H):
+    """The projected top layer's two aggregations (sc_debug_spmm modes 2 / 3): the backward's
+    sum_kept inv[nbr] src[nbr] and the forward's addend + inv * sum_kept src[nbr], bitwise against the
+    oracle's restatement on inv-scaled rows (inv = 1 / masked degree in fp32, as inv_degree)."""
+    sc, a, mask = part0
+    O = oracle()
+    rng = np.random.default_rng(100 + H)
+    n = len(a.nodes)
+    off = a.adj_offsets
+    light = np.diff(off) <= 4096
+    cs = np.concatenate([[0], np.cumsum(mask[a.adj_edge_ids].astype(np.int64))])
+    deg = cs[off[1:]] - cs[off[:-1]]  # kept CSR slots per row (masked_degrees, nn.hpp:174-188)
+    inv = np.where(deg > 0, np.float32(1) / np.maximum(deg, 1).astype(np.float32), np.float32(0)).astype(np.float32)
+    src = rng.standard_normal((n, H), dtype=np.float32)
+    add = rng.standard_normal((n, H), dtype=np.float32)
+    ones = np.ones((n, H), np.float32)
+    got = sc.debug_spmm(2, off, a.adj_neighbors, a.adj_edge_ids, src, edge_mask=mask)
+    ref = O.spmm(1, off, a.adj_neighbors, a.adj_edge_ids, mask, (src * inv[:, None]).astype(np.float32), msg=ones,
+                 threads=os.cpu_count() or 8)
+    assert int((got[light] != ref[light]).sum()) == 0, H
+    assert np.abs(got[~light] - ref[~light]).max() / np.abs(ref[~light]).max() <= 1e-5
+    got = sc.debug_spmm(3, off, a.adj_neighbors, a.adj_edge_ids, src, edge_mask=mask, msg=add)
+    ref = add + O.spmm(0, off, a.adj_neighbors, a.adj_edge_ids, mask, src, threads=os.cpu_count() or 8)
+    assert int((got[light] != ref[light]).sum()) == 0, H
+    assert np.abs(got[~light] - ref[~light]).max() / np.abs(ref[~light]).max() <= 1e-5

@@ -4,7 +4,8 @@ captured launch, so this is never a timing run):
     python tools/ncu_traffic.py --config products [--scale 1]   (appends to profiles/ncu_traffic.json)
 
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none on
-the first forward and backward spmm_kernel launches of `bench.py --steps 1 --warmup 0`; with
+the first forward and backward aggregation launches (spmm_kernel, and spmm_narrow_kernel for the
+projected top layer's 48-wide rows) of `bench.py --steps 1 --warmup 0`; with
 --cache-control none the L2 keeps whatever the previous kernels left, as in the real step, so for an
 L2-resident message matrix (Reddit) the DRAM bytes come out below the algorithmic bytes. Written as
 {"<config>@<scale>": {"spmm_fwd": bytes/launch, "spmm_bwd": bytes/launch, "source": ...}}; bench.py
@@ -31,7 +32,7 @@ def main():
     import bench
     scale = args.scale if args.scale is not None else bench.CONFIGS[args.config].get("default_scale", 1.0)
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--cache-control", "none", "--clock-control", "none", "-k", "regex:spmm_kernel", "-c", str(args.count),
+           "--cache-control", "none", "--clock-control", "none", "-k", "regex:spmm_(kernel|narrow_kernel)", "-c", str(args.count),
            "--csv", sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "0",
            "--no-cpu-baseline", "--config", args.config, "--scale", str(scale)]
     out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT).stdout
@@ -44,9 +45,10 @@ def main():
             continue
         d = per.setdefault(r[ii], {"name": r[ki]})
         d[r[mi]] = float(r[vi].replace(",", ""))
-    def backward(name):  # spmm_kernel<NCH, kBwd>: ncu prints the bool as 0/1 (or false/true)
-        last = name.split("(")[0].rstrip().rstrip(">").split(",")[-1].strip()
-        return last in ("1", "true")
+    def backward(name):  # spmm_kernel<NCH, kBwd, ...> / spmm_narrow_kernel<LPR, CPL, kBwd, ...>: ncu prints 0/1 or false/true
+        args_ = name.split("(")[0]
+        args_ = args_[args_.index("<") + 1:args_.rindex(">")].split(",")
+        return args_[2 if "narrow" in name else 1].strip() in ("1", "true")  # narrow: <LPR, CPL, kBwd, ...>
 
     fwd = [d for d in per.values() if not backward(d["name"])]
     bwd = [d for d in per.values() if backward(d["name"])]
@@ -60,7 +62,7 @@ def main():
     data[f"{args.config}@{scale:g}"] = {
         "spmm_fwd": avg(fwd), "spmm_bwd": avg(bwd), "launches": {"fwd": len(fwd), "bwd": len(bwd)},
         "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --cache-control none, "
-                  f"first {args.count} spmm_kernel launches of bench.py --config {args.config} --scale {scale:g}"}
+                  f"first {args.count} aggregation launches (spmm_kernel, spmm_narrow_kernel) of bench.py --config {args.config} --scale {scale:g}"}
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)
     print(json.dumps(data[f"{args.config}@{scale:g}"]))
 
