@@ -251,6 +251,25 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t 
                  "r"(x), "r"(y)
                  : "memory");
 }
+// 3D TMA store / reduce-add of one smem box (the weight-gradient partials [split][N1][N2]; the N1 and
+// N2 extents clip a box's rows / columns beyond the matrix). One bulk group each.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y, int32_t z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y,
+                                                  int32_t z) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// all of this thread's bulk groups complete (writes performed), not just their source reads
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
@@ -1082,6 +1101,8 @@ struct alignas(64) TnParams {
     int32_t pf_dist;    // L2-prefetch the operand boxes of k-block kb + pf_dist when loading kb (0: off)
     int32_t split_acc;  // A' in TMEM: split full tiles' accumulator into two staggered halves
     float* ws;       // [splits][N1][N2] fp32 partials
+    CUtensorMap tm_ws;  // 3D map over ws (box 32 x 32 x 1, SW128): the drains' TMA stores / reduce-adds
+    int32_t ws_tma;     // use tm_ws (N2 % 4 == 0, one accumulator, SC_TN_TMA_DRAIN != 0)
     unsigned long long* trace;  // optional (SC_TN_TRACE=1): per-role wait / total cycles, summed over CTAs
 };
 
@@ -1501,6 +1522,50 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
         const bool vec = (p.N2 & 3) == 0;
         const uint64_t pol_ws = l2_evict_last();
         float* tbuf = reinterpret_cast<float*>(smem + Cfg::kEpiOff) + ew * 32 * Cfg::kEpiPitch;
+        if (p.ws_tma && nh == 1) {
+            // TMA drain: each 32-column block of the run goes TMEM -> registers -> (unscaled) SW128 smem box
+            // -> one bulk store (first run) or bulk reduce-add (later runs) into ws[split]; the tensor map
+            // clips rows >= N1 / columns >= N2. The previous run's bulk groups are complete before the
+            // next run's are issued, so every element's additions keep the run order (deterministic, the
+            // same adds as the reduction path). The accumulator goes back to the MMAs once the TMEM loads
+            // and box hand-offs are done, not after the L2 reductions.
+            uint8_t* box = smem + Cfg::kEpiOff + ew * 4096;
+            int endr = tn_run_end(0, 0, kblocks, 1, stag);
+            uint32_t run = 0;
+            while (kblocks > 0 && endr <= kblocks) {
+                TN_TIMED_WAIT(w_a, mbar_wait(&tfull[0], run & 1));
+                tc_fence_after();
+                if (lane == 0) bulk_wait_all();
+                __syncwarp();
+                for (int j0 = 0; j0 < nb_pad; j0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + j0, r);
+                    if (j0 >= nb || rows_here == 0) continue;  // warp-uniform
+                    if (lane == 0) bulk_wait_read<0>();         // the previous box has been read
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                            make_float4(__uint_as_float(r[4 * j]) * unscale, __uint_as_float(r[4 * j + 1]) * unscale,
+                                        __uint_as_float(r[4 * j + 2]) * unscale, __uint_as_float(r[4 * j + 3]) * unscale);
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (run == 0) tma_store_3d(&p.tm_ws, box, n20 + j0, m0w, split);
+                        else tma_reduce_add_3d(&p.tm_ws, box, n20 + j0, m0w, split);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_l);
+                ++run;
+                endr = endr < kblocks ? tn_run_end(0, endr, kblocks, 1, stag) : kblocks + 1;
+            }
+            if (lane == 0) bulk_wait_all();
+            if (kblocks == 0)
+                for (int rr = 0; rr < rows_here; ++rr)
+                    for (int c = lane; c < nb; c += 32) outw[int64_t(rr) * p.N2 + c] = 0.f;
+        } else {
         const int hw = nb_pad / nh;  // TMEM columns per half
         int endh[2] = {tn_run_end(0, 0, kblocks, nh, stag), nh > 1 ? tn_run_end(1, 0, kblocks, nh, stag) : kblocks + 1};
         uint32_t runh[2] = {0, 0};
@@ -1550,6 +1615,7 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
         if (kblocks == 0)
             for (int rr = 0; rr < rows_here; ++rr)
                 for (int c = lane; c < nb; c += 32) outw[int64_t(rr) * p.N2 + c] = 0.f;
+        }
     } else {
         // ================= epilogue: drain each chunk into the fp32 partial ws[split] =================
         // Lane = output row (TMEM lane). The first chunk stores, later chunks add with fire-and-forget
@@ -1740,6 +1806,26 @@ int32_t tn_f16x3_splits(int32_t N1, int32_t N2, int64_t M) {
 }
 
 namespace {
+// TMA drains of the A'-in-TMEM TN kernel into ws [S][N1][N2] (SC_TN_TMA_DRAIN=0: L2 reductions)
+void encode_ws(tc::TnParams& p, int32_t S, int32_t N1, int32_t N2) {
+    static const bool on = [] {
+        const char* e = std::getenv("SC_TN_TMA_DRAIN");
+        return !(e && e[0] == '0');
+    }();
+    p.ws_tma = 0;
+    if (!on || N2 % 4 != 0 || (reinterpret_cast<uintptr_t>(p.ws) & 15) != 0) return;
+    const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(N2), static_cast<cuuint64_t>(N1), static_cast<cuuint64_t>(S)};
+    const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(N2) * sizeof(float),
+                                   static_cast<cuuint64_t>(N1) * N2 * sizeof(float)};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&p.tm_ws, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, p.ws, gdim, gstride, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (ws) failed (" + std::to_string(int(r)) + ")");
+    p.ws_tma = 1;
+}
+
 // Split-K launch of the TN kernel over p's tile list, S splits; ws holds [S][N1][N2] partials.
 void tn_launch(tc::TnParams& p, bool pair, int32_t S, cudaStream_t s) {
     static const bool trace = [] {
@@ -1862,6 +1948,7 @@ void gemm_tn_f16x3(const MatT& a, const float* amax_a, const MatT& b1, const flo
     if (int64_t(S) * N1 * N2 > ws_floats) throw std::logic_error("gemm_tn_f16x3: workspace too small");
     p.rows_per_split = ((M + S - 1) / S + tc::kTnBK - 1) / tc::kTnBK * tc::kTnBK;
     p.ws = ws;
+    encode_ws(p, S, N1, N2);
     tn_launch(p, pair, S, s);
     tc::tn_reduce_kernel<<<grid_for(int64_t(N1) * N2, 256), 256, 0, s>>>(S, N1, N2, ws, C, ldc);
     SC_LAUNCH_CHECK();

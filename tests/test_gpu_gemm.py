@@ -176,3 +176,39 @@ def test_nt_tm_modes_subprocess(mode):
                         "test_f16x3_matches_fp64 or test_f16x3_scaling"], capture_output=True, text=True, env=env,
                        timeout=600, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+_DRAIN_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2308_03209_b200 import sagecut as sc
+out = []
+for (M, N1, N2a, N2b) in [(300_000, 256, 256, 0), (40_000, 256, 256, 100), (6000, 384, 256, 0), (4100, 200, 256, 100)]:
+    rng = np.random.default_rng(M + N1)
+    A = rng.standard_normal((M, N1)).astype(np.float32) * 1e-3
+    B1 = rng.standard_normal((M, N2a)).astype(np.float32)
+    B2 = rng.standard_normal((M, N2b)).astype(np.float32) if N2b else None
+    out.append(sc.debug_gemm_tn(A, B1, B2))
+np.savez(sys.argv[2], *out)
+"""
+
+
+def test_tn_tma_drain_same_bits(tmp_path):
+    """The weight-gradient kernel's drains through TMA bulk store / reduce-add (default) and through
+    per-thread L2 reductions (SC_TN_TMA_DRAIN=0) add the same per-run partials in the same order:
+    bitwise equal results (CTA-pair shapes, split-K over up to 300k rows)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "drain.py"
+    script.write_text(_DRAIN_SCRIPT)
+    outs = []
+    for mode in ("1", "0"):
+        o = tmp_path / f"drain{mode}.npz"
+        r = subprocess.run([sys.executable, str(script), root, str(o)], capture_output=True, text=True,
+                           env=dict(os.environ, SC_TN_TMA_DRAIN=mode), timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        outs.append(np.load(o))
+    for k in outs[0].files:
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
