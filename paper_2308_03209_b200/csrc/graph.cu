@@ -304,9 +304,23 @@ __global__ void check_assign_kernel(int64_t m, int32_t p, const int32_t* a, int*
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m; e += int64_t(gridDim.x) * blockDim.x)
         if (a[e] < 0 || a[e] >= p) *bad = 1;
 }
-__global__ void count_parts_kernel(int64_t m, const int32_t* __restrict__ a, int32_t* part_count) {
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m; e += int64_t(gridDim.x) * blockDim.x)
-        atomicAdd(&part_count[a[e]], 1);
+// per-part edge counts: a shared-memory histogram per block (p <= kHistParts), then one global add per
+// (block, part) — instead of m global atomics on p counters
+constexpr int kHistParts = 4096;
+__global__ void count_parts_kernel(int64_t m, int32_t p, const int32_t* __restrict__ a, int32_t* part_count) {
+    __shared__ int32_t h[kHistParts];
+    const bool shared = p <= kHistParts;
+    if (shared)
+        for (int i = threadIdx.x; i < p; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m; e += int64_t(gridDim.x) * blockDim.x) {
+        if (shared) atomicAdd(&h[a[e]], 1);
+        else atomicAdd(&part_count[a[e]], 1);
+    }
+    __syncthreads();
+    if (shared)
+        for (int i = threadIdx.x; i < p; i += blockDim.x)
+            if (h[i]) atomicAdd(&part_count[i], h[i]);
 }
 // Endpoints of part i's edges (perm[0 .. mi) = its global edge ids), then the isolated nodes it
 // receives round-robin in ascending id, starting at part 0 (:45-50): iso[i], iso[i + p], ...
@@ -376,7 +390,8 @@ std::unique_ptr<sc_vcut> build_vertex_cut_device(sc_graph* g, int32_t p, DevBuf<
     DevBuf<int32_t> part_count(p);
     SC_CUDA(cudaMemsetAsync(part_count.get(), 0, p * 4, s));
     if (m > 0) {
-        count_parts_kernel<<<grid_for(m, kBlock), kBlock, 0, s>>>(m, vc->assign.get(), part_count.get());
+        count_parts_kernel<<<grid_for(m, kBlock, int64_t(num_sms()) * 8), kBlock, 0, s>>>(m, p, vc->assign.get(),
+                                                                                         part_count.get());
         SC_LAUNCH_CHECK();
         count_launch();
     }
