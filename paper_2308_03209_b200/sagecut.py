@@ -181,7 +181,9 @@ _sig("sc_trainer_debug_buffer", [_vp, C.c_char_p, _i32, _vp, _i64])
 
 
 def debug_spmm(bwd, offsets, nbrs, eids, src, edge_mask=None, msg=None, ctx: Optional["Context"] = None):
-    """The aggregation kernels alone (nn.hpp:209-230 / 277-288) on host arrays; see sc_debug_spmm."""
+    """The aggregation kernels alone (nn.hpp:209-230 / 277-288) on host arrays; see sc_debug_spmm.
+    bwd: 0 mean (inv * sum), 1 transposed with the ReLU gate of msg, 2 sum of inv[nbr]-scaled rows,
+    3 msg + inv * sum (the projected top layer's two aggregations)."""
     ctx = ctx or default_context()
     off = np.ascontiguousarray(offsets, np.int64)
     nb = np.ascontiguousarray(nbrs, np.int32)
