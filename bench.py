@@ -560,8 +560,10 @@ def run_gpu_arm(args, cfg):
             dist.destroy_process_group()
         return
     peak, peak_kind = measured_peaks()
-    spmm_ms = sum(prof.get(k, [0, 0])[0] for k in ("spmm_fwd", "spmm_bwd"))
-    spmm_bytes = sum(prof.get(k, [0, 0])[1] for k in ("spmm_fwd", "spmm_bwd"))
+    # aggregation groups: H-wide layers, and (projected top layer) the Cp-wide top-layer aggregations
+    spmm_groups = ("spmm_fwd", "spmm_bwd", "spmm_fwd_top", "spmm_bwd_top")
+    spmm_ms = sum(prof.get(k, [0, 0])[0] for k in spmm_groups)
+    spmm_bytes = sum(prof.get(k, [0, 0])[1] for k in spmm_groups)
     launches_dir = cfg["layers"] * len(mine) * args.steps  # per direction
     launches_spmm = 2 * launches_dir
     achieved = spmm_bytes / (spmm_ms / 1e3) / 1e9 if spmm_ms > 0 else 0.0
@@ -633,6 +635,10 @@ def run_gpu_arm(args, cfg):
                      "launches": launches_spmm,
                      "bytes_per_launch": spmm_bytes / max(launches_spmm, 1),
                      "share_of_step": spmm_ms / total_prof if total_prof else None,
+                     "by_group": {k: {"ms_per_step": prof[k][0] / args.steps,
+                                      "GB_per_s": prof[k][1] / (prof[k][0] / 1e3) / 1e9,
+                                      "frac": prof[k][1] / (prof[k][0] / 1e3) / 1e9 / peak if peak else None}
+                                  for k in spmm_groups if k in prof and prof[k][0] > 0},
                      "dram_measured": dram},
         "dominant_kernel": dominant,
         "roofline_gemm": roofline_gemm,

@@ -453,7 +453,7 @@ void forward(sc_trainer* t, const Rows& R, float* logits, const Acts& A) {
             t->tc.nt(t, xin, xin_amax, MatB{t->Z.get() + lo.H, zl, false}, nullptr, nullptr, nullptr, logits, t->Cp, n,
                      t->Cp, kEpiNone, nullptr, nullptr);
             P.end(s);
-            P.begin("spmm_fwd", spmm_bytes(R, t->Cp, false) + 4.0 * n * t->Cp, s);
+            P.begin("spmm_fwd_top", spmm_bytes(R, t->Cp, false) + 4.0 * n * t->Cp, s);
             spmm_fwd_add(n, t->Cp, R.offsets, R.nbrs, R.bits, A.inv, proj, logits, s, R.hv, t->heavy_ws.get());
             P.end(s);
             return;
@@ -524,7 +524,7 @@ void backward_fused(sc_trainer* t, const Rows& R, int i) {
         // G^T mean = G^T D^-1 A msg = Ghat^T msg with Ghat = A^T (inv * G): one Cp-wide pull aggregation
         // (A symmetric; the same kept-slot sums as :277-286) instead of the H-wide mean / dmean.
         float* ghat = t->dh;
-        P.begin("spmm_bwd", spmm_bytes(R, t->Cp, false), s);
+        P.begin("spmm_bwd_top", spmm_bytes(R, t->Cp, false), s);
         SC_CUDA(cudaMemsetAsync(ghat_amax, 0, sizeof(float), s));
         spmm_sum_scaled(n, t->Cp, R.offsets, R.nbrs, R.bits, t->inv, t->G, ghat, s, ghat_amax, R.hv,
                         t->heavy_ws.get());
