@@ -400,24 +400,26 @@ __device__ __forceinline__ float finish_row(int64_t v, int lane, int32_t H, int3
 
 // Warp per row over rows with at most `max_slots` CSR slots (heavier rows go
 // through the segmented path below).
-template <int NCH, bool kBwd, bool kPos = false, int kX = 0>
+template <int NCH, bool kBwd, bool kPos = false, int kX = 0, bool kList = false>
 __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                    const int32_t* __restrict__ nbrs,
                                                    const uint32_t* __restrict__ bits, const float* __restrict__ inv,
                                                    const float* __restrict__ src, const float* __restrict__ msg,
                                                    const uint32_t* __restrict__ pos, float* __restrict__ out,
-                                                   float* amax_out, int64_t max_slots) {
+                                                   float* amax_out, int64_t max_slots, int64_t min_slots = -1,
+                                                   const int32_t* __restrict__ rowlist = nullptr) {
     float amx = 0.f;
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int32_t H4 = H >> 2;
-    for (int64_t v = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += warps) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+        const int64_t v = kList ? rowlist[i] : i;  // (kList: n = the list's length)
         const int64_t a = off[v], b = off[v + 1];
-        if (b - a > max_slots) continue;
+        if (b - a > max_slots || (!kList && b - a <= min_slots)) continue;  // hub rows / the narrow kernel's rows
         float4 acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        gather_rows_sum<NCH>(a, b, lane, H, H4, nbrs, bits, src, acc);
+        gather_rows_sum<NCH, kX == 3>(a, b, lane, H, H4, nbrs, bits, src, acc, inv);
         amx = fmaxf(amx, finish_row<NCH, kBwd, kPos, kX>(v, lane, H, H4, inv, msg, pos, out, acc));
     }
     if (amax_out) {
@@ -612,6 +614,13 @@ struct IsHeavy {
     const int64_t* off;
     __device__ bool operator()(int64_t v) const { return off[v + 1] - off[v] > kHeavySlots; }
 };
+struct IsMid {
+    const int64_t* off;
+    __device__ bool operator()(int64_t v) const {
+        const int64_t d = off[v + 1] - off[v];
+        return d > kNarrowSlots && d <= kHeavySlots;
+    }
+};
 
 template <bool kBwd>
 __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
@@ -632,7 +641,8 @@ __global__ void spmm_scalar_kernel(int64_t n, int32_t H, const int64_t* __restri
     }
 }
 
-// rows of H <= 64 floats run several per warp (spmm_narrow_kernel) unless SC_SPMM_NARROW=0
+// rows of H <= 128 floats and <= kNarrowSlots CSR slots run several per warp (spmm_narrow_kernel)
+// unless SC_SPMM_NARROW=0
 bool narrow_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("SC_SPMM_NARROW");
@@ -650,14 +660,15 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
     const bool heavy = hv && hv->nh > 0;
     const int64_t max_slots = heavy ? int64_t(kHeavySlots) : INT64_MAX;
     const int32_t H4 = H / 4;
-    if (kX == 3 && !(NCH == 1 && H4 <= 32))
-        throw std::logic_error("spmm: inv-scaled sums need rows of at most 128 floats");
-    if (NCH == 1 && H4 <= 32 && (narrow_enabled() || kX == 3)) {  // several rows per warp
+    if (NCH == 1 && H4 <= 32 && narrow_enabled()) {
+        // several rows per warp for rows of at most kNarrowSlots CSR slots (a warp's rows finish together,
+        // so long rows — skewed degrees — would hold the other lanes); a warp-per-row pass takes the rest
+        const int64_t nmax = std::min<int64_t>(max_slots, kNarrowSlots);
         auto go = [&](auto lpr_tag, auto cpl_tag) {
             constexpr int LPR = decltype(lpr_tag)::value, CPL = decltype(cpl_tag)::value;
             const unsigned grid = grid_for((n + 32 / LPR - 1) / (32 / LPR) * 32, 256, int64_t(num_sms()) * 64);
             spmm_narrow_kernel<LPR, CPL, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg,
-                                                                              pos, out, amax_out, max_slots);
+                                                                              pos, out, amax_out, nmax);
         };
         using I4 = std::integral_constant<int, 4>;
         using I8 = std::integral_constant<int, 8>;
@@ -665,6 +676,21 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
         else if (H4 <= 12) go(I4{}, std::integral_constant<int, 3>{});
         else if (H4 <= 16) go(I4{}, I4{});
         else go(I8{}, I4{});
+        SC_LAUNCH_CHECK();
+        if (hv && hv->built) {  // the mid rows, from their list
+            if (hv->nmid > 0) {
+                const unsigned grid = grid_for(int64_t(hv->nmid) * 32, 256, int64_t(num_sms()) * 64);
+                spmm_kernel<NCH, kBwd, kPos, kX, true><<<grid, 256, 0, s>>>(hv->nmid, H, off, nbrs, bits, inv, src,
+                                                                           msg, pos, out, amax_out, max_slots, nmax,
+                                                                           hv->mid.get());
+                count_launch();
+            }
+        } else if (max_slots > nmax) {  // no row table: a pass over every row picks them out
+            const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
+            spmm_kernel<NCH, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out,
+                                                                 amax_out, max_slots, nmax);
+            count_launch();
+        }
     } else {
         const unsigned grid = grid_for(n * 32, 256, int64_t(num_sms()) * 64);
         spmm_kernel<NCH, kBwd, kPos, kX><<<grid, 256, 0, s>>>(n, H, off, nbrs, bits, inv, src, msg, pos, out,
@@ -1123,12 +1149,31 @@ void relu_sign_bits(int64_t M, int32_t N, const float* C, int64_t ldc, uint32_t*
 
 void build_heavy_rows(sc_ctx* ctx, int64_t n, const int64_t* off, HeavyRows& hv) {
     cudaStream_t s = ctx->stream;
-    hv.nh = hv.nseg = 0;
+    hv.nh = hv.nseg = hv.nmid = 0;
+    hv.built = true;
     if (n <= 0) return;
     DevBuf<int32_t> cnt(1);
     hv.rows.alloc(1);
-    IsHeavy pred{off};
     cub::CountingInputIterator<int64_t> it(0);
+    {  // mid rows (warp-per-row pass next to the narrow kernel)
+        cub::TransformInputIterator<bool, IsMid, cub::CountingInputIterator<int64_t>> mflags(it, IsMid{off});
+        DevBuf<int32_t> midx(n);
+        cub::CountingInputIterator<int32_t> ids(0);
+        size_t tmp = 0;
+        SC_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, ids, mflags, midx.get(), cnt.get(), n, s));
+        SC_CUDA(cub::DeviceSelect::Flagged(ctx->temp(tmp), tmp, ids, mflags, midx.get(), cnt.get(), n, s));
+        int32_t nm = 0;
+        d2h(&nm, cnt.get(), 1, s);
+        SC_CUDA(cudaStreamSynchronize(s));
+        count_launch(1);
+        if (nm > 0) {
+            hv.mid.alloc(nm);
+            SC_CUDA(cudaMemcpyAsync(hv.mid.get(), midx.get(), sizeof(int32_t) * nm, cudaMemcpyDeviceToDevice, s));
+            SC_CUDA(cudaStreamSynchronize(s));
+        }
+        hv.nmid = nm;
+    }
+    IsHeavy pred{off};
     // pass 1: count heavy rows
     cub::TransformInputIterator<bool, IsHeavy, cub::CountingInputIterator<int64_t>> flags(it, pred);
     DevBuf<int32_t> idx(n);

@@ -13,7 +13,13 @@ namespace sc {
 // split into kSegSlots-slot segments so no single warp walks a hub row.
 constexpr int64_t kHeavySlots = 4096;
 constexpr int64_t kSegSlots = 1024;
+// Narrow rows (<= 128 floats) of at most kNarrowSlots CSR slots are aggregated several per warp; the
+// longer ones (the "mid" rows, up to kHeavySlots) a warp each, from a list.
+constexpr int64_t kNarrowSlots = 64;
 struct HeavyRows {
+    DevBuf<int32_t> mid;        // nmid rows with kNarrowSlots < slots <= kHeavySlots, ascending
+    int32_t nmid = 0;
+    bool built = false;
     DevBuf<int32_t> rows;       // nh heavy rows, ascending
     DevBuf<int32_t> seg_first;  // nh + 1: segments of row h are [seg_first[h], seg_first[h+1])
     DevBuf<int32_t> seg_row;    // nseg

@@ -1,8 +1,9 @@
 """The aggregation kernels at every row width the trainer uses (nn.hpp:222-230 / 277-288), bitwise
 against the oracle's restatement (float sums in CSR order, then * inv) on a vertex-cut partition with
-a DropEdge mask: H = 8 .. 64 run several rows per warp (spmm_narrow_kernel, e.g. the projected top
-layer's Cp = 48), H = 100 .. 256 a warp per row (spmm_kernel). A hub row above kHeavySlots (4096 CSR
-slots) takes the segmented path (ordered segment partials: tolerance); every other row is bitwise."""
+a DropEdge mask: rows of H <= 128 floats and <= 64 CSR slots run several per warp
+(spmm_narrow_kernel, e.g. the projected top layer's Cp = 48), longer rows and wider H a warp per row
+(spmm_kernel; 40 rows of ~150 slots here). A hub row above kHeavySlots (4096 CSR slots) takes the
+segmented path (ordered segment partials: tolerance); every other row is bitwise."""
 import os
 
 import numpy as np
@@ -20,7 +21,10 @@ def part0():
     n, m = 60_000, 500_000
     uv = rng.integers(0, n, size=(m, 2), dtype=np.int32)
     hub = np.stack([np.zeros(12000, np.int32), rng.integers(1, n, size=12000, dtype=np.int32)], axis=1)
-    g, _ = sc.build_graph(n, np.concatenate([uv, hub]))
+    # rows above the narrow kernel's 64 CSR slots but below the hub threshold: the warp-per-row pass
+    mid = np.stack([np.repeat(np.arange(1, 41, dtype=np.int32), 300), rng.integers(41, n, size=40 * 300, dtype=np.int32)],
+                   axis=1)
+    g, _ = sc.build_graph(n, np.concatenate([uv, hub, mid]))
     part = sc.partition_random(g, 2, 0)
     a = part.part(0)
     masks = sc.precompute_masks(len(a.edges), 3, 0.5, 11)
