@@ -467,11 +467,12 @@ __global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, 
             const int32_t nb = valid ? __ldg(nbrs + k) : 0;
             const bool kept = valid && slot_kept(bits, k);
             unsigned ballot = (__ballot_sync(gmask, kept) & gmask) >> (grp * LPR);
+            constexpr int QN = CPL > 4 ? 2 : 4;  // neighbour rows in flight per batch (register budget)
             while (ballot) {
-                int32_t u[4];
+                int32_t u[QN];
                 int cnt = 0;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < QN; ++q) {
                     if (ballot) {
                         const int sl = __ffs(ballot) - 1;
                         ballot &= ballot - 1;
@@ -481,10 +482,10 @@ __global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, 
                         u[q] = -1;
                     }
                 }
-                float4 vals[4][CPL];
-                float sc[4];
+                float4 vals[QN][CPL];
+                float sc[QN];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < QN; ++q) {
                     sc[q] = (kX == 3 && q < cnt) ? __ldg(inv + u[q]) : 1.f;
 #pragma unroll
                     for (int c = 0; c < CPL; ++c) {
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, 
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < QN; ++q)
                     if (q < cnt)
 #pragma unroll
                         for (int c = 0; c < CPL; ++c) {
@@ -651,6 +652,16 @@ bool narrow_enabled() {
     return on;
 }
 
+// rows per warp for 68 .. 128-float rows: 8 (4 lanes x 8 chunks, two neighbour rows per batch; default:
+// papers-shaped partitions 0.60 -> 0.75 of HBM, profiles/r02_spmm_narrow_ab.txt) or 4 (SC_SPMM_NARROW128=4)
+int narrow_wide_rows() {
+    static const int r = [] {
+        const char* e = std::getenv("SC_SPMM_NARROW128");
+        return e ? std::atoi(e) : 8;
+    }();
+    return r;
+}
+
 template <int NCH, bool kBwd, bool kPos, int kX = 0>
 void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, const uint32_t* bits, const float* inv,
               const float* src, const float* msg, const uint32_t* pos, float* out, cudaStream_t s, float* amax_out,
@@ -675,6 +686,7 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
         if (H4 <= 8) go(I4{}, std::integral_constant<int, 2>{});
         else if (H4 <= 12) go(I4{}, std::integral_constant<int, 3>{});
         else if (H4 <= 16) go(I4{}, I4{});
+        else if (narrow_wide_rows() == 8) go(I4{}, I8{});  // 128 floats: 8 rows per warp
         else go(I8{}, I4{});
         SC_LAUNCH_CHECK();
         if (hv && hv->built) {  // the mid rows, from their list
