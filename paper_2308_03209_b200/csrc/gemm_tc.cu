@@ -1143,8 +1143,14 @@ __device__ __forceinline__ uint32_t mn_off(uint32_t mn, uint32_t k) {
 // accumulator is single-buffered: the MMAs wait for each 1024-row drain.
 template <bool PAIR, bool AT = false>
 struct TnCfg {
-    static constexpr int kStages = AT ? 6 : (PAIR ? 3 : 2);
-    static constexpr int kStg = PAIR ? 3 : 2;
+// A'-in-TMEM stages (TMEM ring + B' smem tiles) / fp32 staging slots: 5 / 4 (6 / 3 and 4 / 4 measured
+// 1-1.5 ms per epoch slower, profiles/r02_tn_stages_ab.txt)
+#ifndef SC_TN_AT_STAGES
+#define SC_TN_AT_STAGES 5
+#define SC_TN_AT_STG 4
+#endif
+    static constexpr int kStages = AT ? SC_TN_AT_STAGES : (PAIR ? 3 : 2);
+    static constexpr int kStg = AT ? SC_TN_AT_STG : (PAIR ? 3 : 2);
     static constexpr int kAcc = AT ? 1 : 2;                  // TMEM accumulators
     // warp roles: converters 0 .. kCW-1, epilogue kCW .. kCW+3, MMA issuer, TMA loader
     static constexpr int kCW = kConvWarps;  // (16 with A' in TMEM measured 2 % slower: converters are not the limit)
