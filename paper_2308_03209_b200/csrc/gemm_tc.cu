@@ -1769,14 +1769,15 @@ void encode_img(CUtensorMap* map, const uint8_t* img, int64_t rows, uint32_t box
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (image) failed (" + std::to_string(int(r)) + ")");
 }
-// Which NT GEMMs run on the A'-in-TMEM kernel, SC_NT_TM bit mask: 1 (default) one source, N <= 128
-// (one pass: the head GEMM); 2 one source, N = 256 as two passes, K <= 256 (msg, dmean: measured
-// slower, profiles/r02_nt_tm_ab.txt); 4 two sources, N <= 128 (the composed head: measured 0.6 ms
-// per epoch slower than the general kernel, profiles/r02_nt_tm_ab.txt).
+// Which NT GEMMs run on the A'-in-TMEM kernel, SC_NT_TM bit mask (default 0: none): 1 one source,
+// N <= 128 (one pass; the unfused head was 0.6 ms faster on it, but the projected top layer's 48-wide
+// P / Q GEMMs are 0.85 ms per epoch faster on the general kernel, profiles/r02_toggles_ab.txt); 2 one
+// source, N = 256 as two passes, K <= 256 (msg, dmean: slower, profiles/r02_nt_tm_ab.txt); 4 two
+// sources, N <= 128 (the composed head: 0.6 ms slower).
 int nt_tm_mode() {
     static const int mode = [] {
         const char* e = std::getenv("SC_NT_TM");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 0;
     }();
     return mode;
 }

@@ -160,13 +160,12 @@ def test_tn_smem_operand_path_subprocess():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("mode", ["0", "7"])
+@pytest.mark.parametrize("mode", ["1", "7"])
 def test_nt_tm_modes_subprocess(mode):
-    """Single-source K <= 256 NT GEMMs with N <= 128 run on the A'-in-TMEM kernel (weight image
-    resident in shared memory) by default. SC_NT_TM (read once per process) = 0 sends every NT GEMM
-    to the general CTA-pair kernel (A' and streamed weight tiles in shared memory); = 7 also runs
-    N = 256 (two N = 128 passes) and two-source GEMMs on the A'-in-TMEM kernel. Both must pass the
-    same fp64 checks."""
+    """The A'-in-TMEM NT kernel (weight image resident in shared memory; off by default, where every NT
+    GEMM runs on the general CTA-pair kernel): SC_NT_TM (read once per process) = 1 runs single-source
+    GEMMs with N <= 128 on it, = 7 also N = 256 (two N = 128 passes) and two-source GEMMs. Both must
+    pass the same fp64 checks."""
     import os
     import subprocess
     import sys
