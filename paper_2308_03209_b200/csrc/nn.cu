@@ -433,8 +433,13 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
 // in flight per warp. Per row the kept slots are summed in CSR order exactly as in spmm_kernel (the
 // same bits). kX == 3: every gathered row is first scaled by inv[nbr] (the pull form of the
 // transposed aggregation of inv-scaled rows, nn.hpp:284: inv_d * dmean.row(v)).
+#ifndef SC_NARROW_MINB
+#define SC_NARROW_MINB 4
+#endif
+// (minimum resident blocks: the kernel is bound by the dependent offset -> index -> row chain, so
+// resident warps matter more than registers; CPL = 8 keeps its wider accumulators at 2)
 template <int LPR, int CPL, bool kBwd, bool kPos, int kX>
-__global__ void __launch_bounds__(256) spmm_narrow_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
+__global__ void __launch_bounds__(256, CPL <= 4 ? SC_NARROW_MINB : 2) spmm_narrow_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                           const int32_t* __restrict__ nbrs,
                                                           const uint32_t* __restrict__ bits,
                                                           const float* __restrict__ inv, const float* __restrict__ src,
