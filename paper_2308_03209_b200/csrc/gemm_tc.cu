@@ -253,19 +253,22 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t 
 }
 // 3D TMA store / reduce-add of one smem box (the weight-gradient partials [split][N1][N2]; the N1 and
 // N2 extents clip a box's rows / columns beyond the matrix). One bulk group each.
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y, int32_t z) {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+// (pol: an L2 eviction policy — the split partials stay L2-resident until tn_reduce_kernel sums them)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y, int32_t z,
+                                             uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::"l"(
                      reinterpret_cast<uint64_t>(map)),
-                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src)), "l"(pol)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int32_t x, int32_t y,
-                                                  int32_t z) {
-    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
-                 : "memory");
+                                                  int32_t z, uint64_t pol) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], "
+        "%5;" ::"l"(reinterpret_cast<uint64_t>(map)),
+        "r"(x), "r"(y), "r"(z), "r"(smem_u32(src)), "l"(pol)
+        : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 // all of this thread's bulk groups complete (writes performed), not just their source reads
@@ -1557,8 +1560,8 @@ __global__ void __launch_bounds__(TnCfg<PAIR, AT>::kThr, 1) gemm_tn_f16x3_kernel
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) {
-                        if (run == 0) tma_store_3d(&p.tm_ws, box, n20 + j0, m0w, split);
-                        else tma_reduce_add_3d(&p.tm_ws, box, n20 + j0, m0w, split);
+                        if (run == 0) tma_store_3d(&p.tm_ws, box, n20 + j0, m0w, split, pol_ws);
+                        else tma_reduce_add_3d(&p.tm_ws, box, n20 + j0, m0w, split, pol_ws);
                     }
                 }
                 tc_fence_before();
