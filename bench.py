@@ -432,7 +432,9 @@ def run_gpu_arm(args, cfg):
         g.set_data(feats, labels, cfg["classes"], tr, va, te)
     if emu:
         g.set_part_ownership(0, emu)  # rank 0 holds (and trains) partitions i % emu == 0 only
-    part = sc.partition_random(g, cfg["parts"], 0)
+    partitioner = getattr(args, "partitioner", "random")
+    part = {"random": sc.partition_random, "dbh": sc.partition_dbh,
+            "ne": sc.partition_ne}[partitioner](g, cfg["parts"], 0)
     sizes_all = [part.part_sizes(i)[1] for i in range(cfg["parts"])]
     mine = range(rank, cfg["parts"], world) if not emu else range(0, cfg["parts"], emu)
     sizes_m = [sizes_all[i] for i in mine] if emu else sizes_all
@@ -615,7 +617,9 @@ def run_gpu_arm(args, cfg):
         "config": {"workload": cfg["workload"] + (f" [scale {scale}]" if scale != 1.0 else ""),
                    "nodes": g.num_nodes, "edges": g.num_edges(),
                    "feats": cfg["feats"], "classes": cfg["classes"], "layers": cfg["layers"],
-                   "hidden": cfg["hidden"], "partitions": cfg["parts"], "partitioner": "random vertex cut",
+                   "hidden": cfg["hidden"], "partitions": cfg["parts"],
+                   "partitioner": {"random": "random vertex cut", "dbh": "DBH vertex cut",
+                                   "ne": "neighbour-expansion vertex cut"}[partitioner],
                    "dropedge": f"p={cfg['ratio']} K={cfg['k']}" if cfg["dropedge"] else None,
                    "degrees": degree_stats, "rf": sc.replication_stats(part, g).rf,
                    "kept_csr_entries_per_epoch": kept, "parallelism": f"dp{world} over {cfg['parts']} fixed partitions",
@@ -684,6 +688,8 @@ def main():
                     help="time the reference on one FULL-size partition (minutes of CPU; BASELINE.md §3) and write "
                          "profiles/r02_reference_full_partition.json")
     ap.add_argument("--parts", type=int, default=None, help="override the config's partition count p")
+    ap.add_argument("--partitioner", default="random", choices=["random", "dbh", "ne"],
+                    help="vertex-cut partitioner (partition.cpp:92-201); the headline uses random")
     ap.add_argument("--scale", type=float, default=None,
                     help="scale nodes and edges of the config (default 1; rmat: 0.25, see CONFIGS)")
     args = ap.parse_args()
