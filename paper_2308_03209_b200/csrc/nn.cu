@@ -891,6 +891,56 @@ __global__ void __launch_bounds__(128) softmax_ce_rows_kernel(int64_t n, int32_t
     }
 }
 
+// Warp per row for 64 < C <= 32 NV (e.g. 172 classes): the row lives in registers (lane l holds
+// columns l, l + 32, ...), so logits are read once; the same per-lane column order and butterfly
+// reductions as softmax_ce_kernel (identical bits).
+template <int NV>
+__global__ void softmax_ce_warp_regs_kernel(int64_t n, int32_t C, int32_t ld, const float* __restrict__ logits,
+                                            const int32_t* __restrict__ labels, const int32_t* __restrict__ rows,
+                                            const double* __restrict__ w, const float* __restrict__ scale, float* G,
+                                            double* row_loss) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+        const float* z = logits + r * ld;
+        float* g = G + r * ld;
+        const double wr = w[r];
+        for (int32_t c = C + lane; c < ld; c += 32) g[c] = 0.f;  // padding columns (row stride ld)
+        if (wr == 0.0) {  // nn.hpp:330
+            for (int32_t c = lane; c < C; c += 32) g[c] = 0.f;
+            if (lane == 0) row_loss[r] = 0.0;
+            continue;
+        }
+        float zr[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) zr[j] = (lane + 32 * j < C) ? z[lane + 32 * j] : -INFINITY;
+        const int32_t y = labels[rows ? rows[r] : r];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            if (lane + 32 * j < C) mx = fmaxf(mx, zr[j]);
+        mx = warp_max(mx);
+        float se = 0.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            if (lane + 32 * j < C) se += expf(zr[j] - mx);
+        se = warp_sum(se);
+        const float lse = mx + logf(se);
+        const float sc = scale[r];
+        float zy = 0.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int32_t c = lane + 32 * j;
+            if (c < C) {
+                if (c == y) zy = zr[j];
+                g[c] = sc * (expf(zr[j] - lse) - (c == y ? 1.f : 0.f));
+            }
+        }
+        zy = __shfl_sync(0xffffffffu, zy, y & 31);
+        if (lane == 0) row_loss[r] = wr * static_cast<double>(lse - zy);
+    }
+}
+
 // targets (optional): the graph's n x C 0/1 multi-label matrix (graph.hpp:64);
 // without it the target row is the one-hot of the class id (label_targets,
 // graph.cpp:91-98).
@@ -1326,6 +1376,12 @@ void softmax_ce(int64_t n, int32_t C, int32_t ld, const float* logits, const int
         softmax_ce_rows_kernel<12><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
     else if (vec && ld <= 64)
         softmax_ce_rows_kernel<16><<<grid, 128, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G, row_loss);
+    else if (C <= 128)
+        softmax_ce_warp_regs_kernel<4><<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale,
+                                                                            G, row_loss);
+    else if (C <= 256)
+        softmax_ce_warp_regs_kernel<8><<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale,
+                                                                            G, row_loss);
     else
         softmax_ce_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, C, ld, logits, labels, rows, w, scale, G,
                                                                   row_loss);
