@@ -584,9 +584,21 @@ def run_gpu_arm(args, cfg):
     max_rows = max(part.part_sizes(i)[0] for i in range(cfg["parts"]))
     act_bytes = max_rows * cfg["hidden"] * 4
     total_prof = sum(v[0] for v in prof.values())
+    tpeak_all, _ = measured_tensor_peak()
+
+    def bound_frac(k, v):
+        """lower-bound time of the group (its algorithmic bytes at the HBM peak, its executed fp16x3 MMA
+        flops at the measured dense tensor peak — whichever is larger) over its measured time"""
+        if v[0] <= 0 or not peak:
+            return None
+        t_hbm = v[1] / (peak * 1e9)
+        t_tc = 3 * flops.get(k, 0.0) / (tpeak_all * 1e12) if tpeak_all else 0.0
+        return max(t_hbm, t_tc) / (v[0] / 1e3)
+
     kernels = {k: {"ms_per_step": v[0] / args.steps, "share": v[0] / total_prof if total_prof else None,
                    "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 and v[1] > 0 else None,
-                   "TFLOP_per_s_fp16x3": (3 * flops[k] / (v[0] / 1e3) / 1e12) if flops.get(k) and v[0] > 0 else None}
+                   "TFLOP_per_s_fp16x3": (3 * flops[k] / (v[0] / 1e3) / 1e12) if flops.get(k) and v[0] > 0 else None,
+                   "frac_of_bound": bound_frac(k, v)}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     dominant = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
     # tensor roofline of the dominant GEMM group: fp16x3 issues three fp16 MMAs per fp32-equivalent
