@@ -438,14 +438,15 @@ __global__ void __launch_bounds__(256) spmm_kernel(int64_t n, int32_t H, const i
 #endif
 // (minimum resident blocks: the kernel is bound by the dependent offset -> index -> row chain, so
 // resident warps matter more than registers; CPL = 8 keeps its wider accumulators at 2)
-template <int LPR, int CPL, bool kBwd, bool kPos, int kX>
+template <int LPR, int CPL, bool kBwd, bool kPos, int kX, bool kList = false>
 __global__ void __launch_bounds__(256, CPL <= 4 ? SC_NARROW_MINB : 2) spmm_narrow_kernel(int64_t n, int32_t H, const int64_t* __restrict__ off,
                                                           const int32_t* __restrict__ nbrs,
                                                           const uint32_t* __restrict__ bits,
                                                           const float* __restrict__ inv, const float* __restrict__ src,
                                                           const float* __restrict__ msg,
                                                           const uint32_t* __restrict__ pos, float* __restrict__ out,
-                                                          float* amax_out, int64_t max_slots) {
+                                                          float* amax_out, int64_t max_slots,
+                                                          const int32_t* __restrict__ rowlist = nullptr) {
     constexpr int G = 32 / LPR;
     const int lane = threadIdx.x & 31;
     const int grp = lane / LPR, gl = lane % LPR;
@@ -454,9 +455,10 @@ __global__ void __launch_bounds__(256, CPL <= 4 ? SC_NARROW_MINB : 2) spmm_narro
     float amx = 0.f;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t v0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * G; v0 < n; v0 += warps * G) {
-        const int64_t v = v0 + grp;
+        const int64_t vi = v0 + grp;  // (kList: an index into the row list, n its length)
+        bool skip = vi >= n;
+        const int64_t v = kList ? (skip ? 0 : rowlist[vi]) : vi;
         int64_t a = 0, b = 0;
-        bool skip = v >= n;
         if (!skip) {
             a = off[v];
             b = off[v + 1];
@@ -695,7 +697,12 @@ void spmm_vec(int64_t n, int32_t H, const int64_t* off, const int32_t* nbrs, con
         else go(I8{}, I4{});
         SC_LAUNCH_CHECK();
         if (hv && hv->built) {  // the mid rows, from their list
-            if (hv->nmid > 0) {
+            if (hv->nmid > 0 && H4 <= 16) {  // two 16-lane rows per warp (rows of similar length)
+                const unsigned grid = grid_for((int64_t(hv->nmid) + 1) / 2 * 32, 256, int64_t(num_sms()) * 64);
+                spmm_narrow_kernel<16, 1, kBwd, kPos, kX, true><<<grid, 256, 0, s>>>(
+                    hv->nmid, H, off, nbrs, bits, inv, src, msg, pos, out, amax_out, max_slots, hv->mid.get());
+                count_launch();
+            } else if (hv->nmid > 0) {
                 const unsigned grid = grid_for(int64_t(hv->nmid) * 32, 256, int64_t(num_sms()) * 64);
                 spmm_kernel<NCH, kBwd, kPos, kX, true><<<grid, 256, 0, s>>>(hv->nmid, H, off, nbrs, bits, inv, src,
                                                                            msg, pos, out, amax_out, max_slots, nmax,
